@@ -1,0 +1,242 @@
+"""CPU oracle for ECMG_jcg (arXiv:1506.02983) -- TEST INFRASTRUCTURE.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs may
+import this package. The product path (paper_1506_02983_b200/) never imports it and shares no
+code with it. The arithmetic lives in ecmg_oracle.cpp (plain C++, fp64, -ffp-contract=off);
+this module only builds it (g++) and marshals numpy arrays through ctypes.
+
+Parity status of each function is recorded in DESIGN.md ("Oracle pins"); every function here is
+pinned by a `-m "not gpu"` test in tests/test_oracle_*.py.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SRC = os.path.join(HERE, "ecmg_oracle.cpp")
+LIB = os.path.join(HERE, "liboracle.so")
+
+# problem ids / face kinds (interface numbers; the CUDA registry declares the same ids itself)
+C1, C2, C3, C4, C5 = 1, 2, 3, 4, 5
+P1, P2, P3 = 11, 12, 13
+PATCH_TRILINEAR, PATCH_LAYERED, PATCH_ROBIN, CONST_F = 21, 22, 23, 24
+DIRICHLET, ROBIN = 0, 1
+
+NSTAT = 17
+STAT_FIELDS = ["iterations", "rel_recur", "rel_true", "normb", "err_l2", "err_linf",
+               "err_tilde_l2", "err_tilde_linf", "err_w_l2", "err_w_linf", "r_h",
+               "t_setup", "t_exp", "t_solve", "t_rich", "status", "free_unknowns"]
+
+_lock = threading.Lock()
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with g++ -O2 -ffp-contract=off."""
+    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
+        tmp = LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["g++", "-std=c++17", "-O2", "-ffp-contract=off", "-shared", "-fPIC",
+                               "-o", tmp, SRC])
+        os.replace(tmp, LIB)
+    return LIB
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            L = C.CDLL(LIB)
+            dp, ip, vp = C.POINTER(C.c_double), C.POINTER(C.c_int), C.c_void_p
+            L.orc_build_level.restype = vp
+            L.orc_build_level.argtypes = [dp, dp, ip, C.c_int, dp, C.c_int, ip]
+            L.orc_free_level.argtypes = [vp]
+            L.orc_num_nodes.restype = C.c_long
+            L.orc_num_nodes.argtypes = [vp]
+            L.orc_get_matrix.argtypes = [vp, dp]
+            L.orc_get_load.argtypes = [vp, dp]
+            L.orc_get_rhs.restype = C.c_double
+            L.orc_get_rhs.argtypes = [vp, dp]
+            L.orc_get_dirichlet.argtypes = [vp, C.POINTER(C.c_ubyte), dp]
+            L.orc_apply.argtypes = [vp, dp, dp]
+            L.orc_jcg.restype = C.c_int
+            L.orc_jcg.argtypes = [vp, dp, C.c_double, C.c_int, C.c_int, ip, dp, dp, dp]
+            L.orc_dsolve.restype = C.c_int
+            L.orc_dsolve.argtypes = [vp, dp]
+            L.orc_exact.argtypes = [vp, dp]
+            L.orc_exp_finite.restype = C.c_int
+            L.orc_exp_finite.argtypes = [vp, dp, dp, dp, C.c_int]
+            L.orc_exp_true.restype = C.c_int
+            L.orc_exp_true.argtypes = [vp, dp, dp, dp]
+            L.orc_norms.argtypes = [vp, dp, dp, dp]
+            L.orc_element_stiffness.argtypes = [dp, C.c_double, dp]
+            L.orc_face_integrals.argtypes = [C.c_double, C.c_double, dp, dp, dp, dp]
+            L.orc_serendipity_weights.argtypes = [C.c_double, C.c_double, C.c_double, dp]
+            L.orc_ecmg.restype = C.c_int
+            L.orc_ecmg.argtypes = [dp, dp, ip, C.c_int, C.c_int, dp, C.c_int, ip, C.c_double, C.c_int,
+                                   C.c_int, C.c_int, dp, dp, dp, dp]
+            _lib = L
+    return _lib
+
+
+def _d(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _i(a):
+    return a.ctypes.data_as(C.POINTER(C.c_int))
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def default_faces(problem_id: int):
+    f = [DIRICHLET] * 6
+    if problem_id in (C3, PATCH_ROBIN):
+        f[5] = ROBIN
+    elif problem_id == P1:
+        f[1] = f[3] = f[5] = ROBIN
+    elif problem_id == P2:
+        f[1] = f[3] = ROBIN
+    return f
+
+
+class Level:
+    """One assembled grid level (explicit 27-band matrix, lifted RHS, node classes)."""
+
+    def __init__(self, n_cells, problem_id, params=None, lo=(0, 0, 0), hi=(1, 1, 1), faces=None):
+        L = lib()
+        self.n = tuple(int(v) for v in n_cells)
+        self.shape = (self.n[2] + 1, self.n[1] + 1, self.n[0] + 1)
+        self.N = self.shape[0] * self.shape[1] * self.shape[2]
+        self.problem_id = problem_id
+        self.params = _f64(params if params is not None else np.zeros(1))
+        self.faces = np.array(faces if faces is not None else default_faces(problem_id), dtype=np.int32)
+        self.lo, self.hi = _f64(lo), _f64(hi)
+        n = np.array(self.n, dtype=np.int32)
+        self._h = L.orc_build_level(_d(self.lo), _d(self.hi), _i(n), problem_id, _d(self.params),
+                                    int(self.params.size if params is not None else 0), _i(self.faces))
+        if not self._h:
+            raise ValueError("oracle: invalid level / problem")
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib().orc_free_level(h)
+            self._h = None
+
+    def matrix(self):
+        A = np.empty(self.N * 27)
+        lib().orc_get_matrix(self._h, _d(A))
+        return A.reshape(self.N, 27)
+
+    def load(self):
+        F = np.empty(self.N)
+        lib().orc_get_load(self._h, _d(F))
+        return F
+
+    def rhs(self):
+        b = np.empty(self.N)
+        nb = lib().orc_get_rhs(self._h, _d(b))
+        return b, nb
+
+    def dirichlet(self):
+        m = np.empty(self.N, dtype=np.uint8)
+        g = np.empty(self.N)
+        lib().orc_get_dirichlet(self._h, m.ctypes.data_as(C.POINTER(C.c_ubyte)), _d(g))
+        return m.astype(bool), g
+
+    def apply(self, p):
+        p = _f64(p)
+        q = np.empty(self.N)
+        lib().orc_apply(self._h, _d(p), _d(q))
+        return q
+
+    def jcg(self, x0, eps, max_iter, precond=True):
+        x = _f64(x0).copy()
+        it, rr, rt, nb = C.c_int(), C.c_double(), C.c_double(), C.c_double()
+        st = lib().orc_jcg(self._h, _d(x), float(eps), int(max_iter), 1 if precond else 0,
+                           C.byref(it), C.byref(rr), C.byref(rt), C.byref(nb))
+        return x, dict(status=st, iterations=it.value, rel_recur=rr.value, rel_true=rt.value, normb=nb.value)
+
+    def dsolve(self):
+        x = np.zeros(self.N)
+        st = lib().orc_dsolve(self._h, _d(x))
+        if st != 0:
+            raise RuntimeError(f"oracle dsolve failed: {st}")
+        return x
+
+    def exact(self):
+        u = np.empty(self.N)
+        lib().orc_exact(self._h, _d(u))
+        return u
+
+    def exp_finite(self, u2h, u4h, variant=0):
+        """variant 0: 20-node Serendipity; 1: Remark 2's 27-node Lagrange."""
+        w = np.empty(self.N)
+        st = lib().orc_exp_finite(self._h, _d(_f64(u2h)), _d(_f64(u4h)), _d(w), int(variant))
+        if st != 0:
+            raise ValueError(f"oracle exp_finite: {st}")
+        return w
+
+    def exp_true(self, uh, u2h):
+        ut = np.empty(self.N)
+        st = lib().orc_exp_true(self._h, _d(_f64(uh)), _d(_f64(u2h)), _d(ut))
+        if st != 0:
+            raise ValueError(f"oracle exp_true: {st}")
+        return ut
+
+    def norms(self, e):
+        l2, li = C.c_double(), C.c_double()
+        lib().orc_norms(self._h, _d(_f64(e)), C.byref(l2), C.byref(li))
+        return l2.value, li.value
+
+
+def element_stiffness(h, beta=1.0):
+    K = np.empty(64)
+    lib().orc_element_stiffness(_d(_f64(h)), float(beta), _d(K))
+    return K.reshape(8, 8)
+
+
+def face_integrals(h1, h2, alpha_q, g_q):
+    M = np.empty(16)
+    G = np.empty(4)
+    lib().orc_face_integrals(float(h1), float(h2), _d(_f64(alpha_q)), _d(_f64(g_q)), _d(M), _d(G))
+    return M.reshape(4, 4), G
+
+
+SEED_LABELS = [1, 3, 5, 11, 15, 21, 23, 25, 51, 55, 71, 75, 101, 103, 105, 111, 115, 121, 123, 125]
+
+
+def serendipity_weights(xi, eta, zeta):
+    w = np.empty(20)
+    lib().orc_serendipity_weights(float(xi), float(eta), float(zeta), _d(w))
+    return w
+
+
+def ecmg(n0, levels, problem_id, eps, params=None, lo=(0, 0, 0), hi=(1, 1, 1), faces=None,
+         max_iter=100000, precond=True, want_w=False, exp_variant=0):
+    """Alg. 4. Returns (status, stats[levels, NSTAT], u_fine, ut_fine[, w_fine])."""
+    n0 = np.array([n0] * 3 if np.isscalar(n0) else list(n0), dtype=np.int32)
+    nf = n0 * (1 << (levels - 1))
+    N = int(np.prod(nf + 1))
+    stats = np.empty(levels * NSTAT)
+    u = np.empty(N)
+    ut = np.empty(N)
+    w = np.empty(N) if want_w else None
+    prm = _f64(params if params is not None else np.zeros(1))
+    fc = np.array(faces if faces is not None else default_faces(problem_id), dtype=np.int32)
+    st = lib().orc_ecmg(_d(_f64(lo)), _d(_f64(hi)), _i(n0), int(levels), int(problem_id), _d(prm),
+                        int(prm.size if params is not None else 0), _i(fc), float(eps), int(max_iter),
+                        1 if precond else 0, int(exp_variant), _d(stats), _d(u), _d(ut),
+                        _d(w) if w is not None else None)
+    stats = stats.reshape(levels, NSTAT)
+    if want_w:
+        return st, stats, u, ut, w
+    return st, stats, u, ut
