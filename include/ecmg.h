@@ -1,0 +1,170 @@
+/*
+ * ecmg.h -- C ABI of libecmg, the B200-native hot path of ECMG_jcg (Pan, He, Hu,
+ * "A new extrapolation cascadic multigrid method for 3D elliptic boundary value problems",
+ * arXiv:1506.02983). "P:n" cites /root/reference/PAPER.md line n; section / equation labels
+ * are the LaTeX \label names of the paper.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - Every function returns ECMG_OK (0) or a negative ecmg_status; none throws or aborts.
+ *  - A grid is bound to one CUDA device and one CUDA stream (given at creation). All device work
+ *    of a call is enqueued on that stream; a call returns after its results are complete
+ *    (calls synchronise the stream before returning, so host-visible outputs are valid).
+ *  - Nodal vectors passed by the caller are contiguous fp64 arrays over all (nx+1)(ny+1)(nz+1)
+ *    nodes of the level, x fastest: index ix + (nx+1)(iy + (ny+1) iz).
+ *    Device pointers are required except where a parameter says "device or host".
+ *    The caller owns them; the library reads / writes them only during the call.
+ *  - The grid owns all internal workspace (pitched free-box vectors, element coefficients,
+ *    reduction buffers); nothing the caller passes is retained after a call returns.
+ *  - There is no CPU fallback: without a usable CUDA device ecmg_create_grid fails with
+ *    ECMG_ECUDA.
+ *  - A grid is not thread safe; distinct grids may be used from distinct threads.
+ */
+#ifndef ECMG_H
+#define ECMG_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  ECMG_OK = 0,
+  ECMG_EINVAL = -1,      /* bad argument (sizes, pointers, problem parameters, beta <= 0, alpha < 0) */
+  ECMG_ENOMEM = -2,      /* device allocation failed */
+  ECMG_ENOTCONV = -3,    /* relative-residual tolerance not met within max_iter (stats still filled) */
+  ECMG_EBREAKDOWN = -4,  /* p.Ap <= 0 inside JCG: the operator is not SPD */
+  ECMG_EDIAG = -5,       /* non-positive diagonal entry: Jacobi preconditioner undefined */
+  ECMG_EMISMATCH = -6,   /* level index / grid embedding mismatch */
+  ECMG_ECUDA = -7,       /* CUDA runtime error or no device */
+  ECMG_ENCCL = -8        /* NCCL error (multi-GPU z-slabs) */
+} ecmg_status;
+
+/* Boundary kinds of Eq. (bvp). Robin with alpha = 0 is Neumann. */
+typedef enum { ECMG_DIRICHLET = 0, ECMG_ROBIN = 1 } ecmg_face_kind;
+
+/* Built-in problems (device-side registry; beta, f, g_D, alpha, g_R as functions of x).
+ * C1..C5 are BASELINE.json configs[0..4]; P1..P3 are the paper's Problems 1-3;
+ * PATCH_* are Galerkin-exact patch tests; CONST_F is f = 1 with homogeneous Dirichlet. */
+typedef enum {
+  ECMG_PROB_C1 = 1,   /* beta=1, u=sin(pi x)sin(pi y)sin(pi z), Dirichlet all faces */
+  ECMG_PROB_C2 = 2,   /* beta=1, u=exp(x+y+z), Dirichlet all faces */
+  ECMG_PROB_C3 = 3,   /* beta=1+sin(2pi x)cos(2pi y)sin(2pi z)/2, u=cos(pi x)cos(pi y)e^z, Robin z=1 (alpha=1) */
+  ECMG_PROB_C4 = 4,   /* beta=1, u=(x^2+y^2+z^2)^(3/4), Dirichlet all faces */
+  ECMG_PROB_C5 = 5,   /* layered geology: params[48] (layout in synth/__init__.py), f Gaussian, g_D=0 */
+  ECMG_PROB_P1 = 11,  /* paper Problem 1: Neumann on x=1,y=1,z=1 */
+  ECMG_PROB_P2 = 12,  /* paper Problem 2: Neumann on x=1,y=1 */
+  ECMG_PROB_P3 = 13,  /* paper Problem 3: singular, Dirichlet all faces */
+  ECMG_PROB_PATCH_TRILINEAR = 21,
+  ECMG_PROB_PATCH_LAYERED = 22, /* params[15]: the C5 layer set */
+  ECMG_PROB_PATCH_ROBIN = 23,
+  ECMG_PROB_CONST_F = 24
+} ecmg_problem_id;
+
+typedef struct { double lo[3], hi[3]; } ecmg_box;  /* domain Omega = [lo, hi]; hi > lo */
+
+/* Multi-GPU z-slab decomposition (NULL or nranks == 1: single GPU). nccl_id is the 128-byte
+ * ncclUniqueId that rank 0 created and the caller broadcast (e.g. with torch.distributed). */
+typedef struct { int rank, nranks; unsigned char nccl_id[128]; } ecmg_dist;
+
+typedef struct ecmg_grid ecmg_grid;  /* opaque; owns all internal workspace */
+
+/* Build the embedded grid hierarchy of Alg. 4: level k has coarsest_cells[d] * 2^k
+ * cells along axis d, k = 0 .. num_levels-1; the finest mesh size is H / 2^(num_levels-1)
+ * (P:287-288 with L = num_levels - 2). Levels 0 and 1 are the DSOLVE levels.
+ *   dom            domain box, extents > 0
+ *   coarsest_cells >= 1 per axis (>= 2 recommended)
+ *   num_levels     >= 3 (two DSOLVE levels + at least one ECMG level)
+ *   dist           NULL for a single GPU
+ *   cuda_stream    cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream); NULL = default stream
+ *   out            receives the grid; *out is NULL on failure
+ * Errors: ECMG_EINVAL, ECMG_ECUDA (no device), ECMG_ENOMEM (workspace for the finest level). */
+int ecmg_create_grid(const ecmg_box* dom, const int coarsest_cells[3], int num_levels,
+                     const ecmg_dist* dist, void* cuda_stream, ecmg_grid** out);
+
+typedef struct {
+  ecmg_face_kind face[6];   /* x-, x+, y-, y+, z-, z+; must equal the problem's own boundary kinds */
+  int problem_id;           /* ecmg_problem_id */
+  const double* params;     /* host array, problem parameters (C5: 48 doubles, PATCH_LAYERED: 15) */
+  int n_params;
+} ecmg_problem;
+
+/* Bind the problem of Eq. (bvp) to the grid. Level operators are matrix-free; the
+ * per-level setup (element beta at centroids, 2x2x2-Gauss load, 2x2-Gauss Robin terms, Dirichlet
+ * lifting, ||f_h||) runs inside ecmg_solve_level / ecmg_run (it is part of the timed hot path).
+ * Errors: ECMG_EINVAL (unknown id, wrong n_params, face kinds differ from the problem's,
+ * beta <= 0 or alpha < 0 in the parameters). */
+int ecmg_set_coeffs(ecmg_grid* grid, const ecmg_problem* problem);
+
+typedef enum {
+  ECMG_OPT_EXP_VARIANT = 1,  /* 0 (default): 20-node Serendipity EXP_finite;
+                                1: Remark 2's 27-node tri-quadratic Lagrange */
+  ECMG_OPT_PRECOND = 2,      /* 1 (default): Jacobi, ECMG_jcg; 0: plain CG, ECMG_cg */
+  ECMG_OPT_ZCHUNK = 3        /* planes per CTA in the z-marching JCG kernels (tuning; 0 = auto) */
+} ecmg_option;
+int ecmg_set_option(ecmg_grid* grid, int option, int value);
+
+typedef struct {
+  int iterations;        /* JCG iterations performed (number of A.p products); DSOLVE levels: iterations of
+                            the 1e-14 JCG surrogate (reading A12) */
+  double rel_res_recur;  /* ||r_k||_2 / ||f_h||_2 from the CG recurrence at exit */
+  double rel_res_true;   /* "RRe": ||f_h - A_h u_h||_2 / ||f_h||_2 recomputed at exit */
+  double norm_b;         /* ||f_h||_2 over free rows (lifted RHS) */
+  int converged;
+  int status;            /* ecmg_status of this level */
+  double ms_setup, ms_exp, ms_solve, ms_rich;  /* device time (CUDA events) of the level's phases */
+} ecmg_stats;
+
+/* JCG solve of level `level` (Alg. 4 l.7-9): textbook PCG with M = diag(A_h),
+ * iterate while ||r||_2 > eps ||f_h||_2 (recurrence residual, tested before every iteration
+ * including the first; ||f_h|| = 0 -> absolute residual). eps <= 0 runs exactly max_iter
+ * iterations (fixed-iteration benchmark / parity mode). max_iter <= 0 -> 10000.
+ *   u      device, level-sized: in = initial guess (free nodes; Dirichlet entries ignored),
+ *          out = iterate; Dirichlet entries are set to g_D.
+ *   stats  may be NULL.
+ * Errors: ECMG_ENOTCONV (stats filled, u holds the last iterate), ECMG_EBREAKDOWN, ECMG_EDIAG,
+ * ECMG_EINVAL (no problem bound, level out of range). */
+int ecmg_solve_level(ecmg_grid* grid, int level, double eps, int max_iter, double* u, ecmg_stats* stats);
+
+/* EXP_finite (Alg. 4 l.6): W_h on level `level` (>= 2) from u_2h (level-1) and
+ * u_4h (level-2): corners by Eq. (jiedian) (5U^1-U^0)/4, edge midpoints by Eq. (zhongdian),
+ * all other nodes by 20-node Serendipity interpolation of Eq. (inter) (or Remark 2's Lagrange
+ * variant, ECMG_OPT_EXP_VARIANT); Dirichlet nodes get g_D. All three device arrays.
+ * Requires cells divisible by 4 per axis on `level`. Errors: ECMG_EMISMATCH, ECMG_EINVAL. */
+int ecmg_prolongate_extrapolate(ecmg_grid* grid, int level, const double* u2h, const double* u4h, double* w);
+
+/* EXP_true (Alg. 4 l.10): u~_h = (4U^1 - U^0)/3 at 2h nodes (Eq. t1) and the
+ * Chen-Lin formula (Eq. chenlin) at 2h edge centres, averaged over the face / space diagonals at
+ * face and cell centres; Dirichlet nodes get g_D. uh: level `level`, u2h: level-1, ut: level. */
+int ecmg_richardson(ecmg_grid* grid, int level, const double* uh, const double* u2h, double* ut);
+
+/* Alg. 4 end to end: DSOLVE on levels 0 and 1, then for k = 2..num_levels-1:
+ * setup(k), W_k = EXP_finite(u_{k-1}, u_{k-2}), JCG(eps) from W_k, u~_k = EXP_true(u_k, u_{k-1}).
+ *   per_level  host array [num_levels] or NULL
+ *   u_fine     finest-level u_h (device or host pointer; a host pointer is filled by a D2H copy
+ *              inside the call)
+ *   ut_fine    finest-level u~_h (device or host) or NULL
+ * Returns the first failing level's status (ECMG_ENOTCONV etc.) or ECMG_OK. */
+int ecmg_run(ecmg_grid* grid, double eps, ecmg_stats* per_level, double* u_fine, double* ut_fine);
+
+/* Diagnostics used by the parity tests (same kernels as the solve):
+ * ecmg_apply_operator: q = A_ff p on free nodes, q = 0 on Dirichlet nodes (p's Dirichlet entries
+ *   are ignored). ecmg_level_rhs: lifted right-hand side b_f = F_f + G_f - A_fD g_D on free nodes,
+ *   0 on Dirichlet nodes, and ||b_f||_2. Both arrays device, level-sized. */
+int ecmg_apply_operator(ecmg_grid* grid, int level, const double* p, double* q);
+int ecmg_level_rhs(ecmg_grid* grid, int level, double* b, double* norm_b);
+
+/* Level geometry: cells per axis, number of nodes of the caller-visible vector, and the z-plane
+ * range [z_lo, z_hi] of the nodes this rank owns (whole level for one GPU). */
+int ecmg_level_shape(const ecmg_grid* grid, int level, int n_cells3[3], long long* nodes, int* z_lo, int* z_hi);
+
+/* Device time of the last solve's JCG iteration kernels (K1 + K2), for roofline reporting:
+ * total milliseconds and number of iterations timed (CUDA events around the iteration loop). */
+int ecmg_last_jcg_timing(const ecmg_grid* grid, double* ms, int* iterations, long long* free_unknowns);
+
+int ecmg_destroy_grid(ecmg_grid* grid);
+const char* ecmg_strerror(int status);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ECMG_H */

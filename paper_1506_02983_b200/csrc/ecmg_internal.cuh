@@ -1,0 +1,116 @@
+// ecmg_internal.cuh -- internal types of libecmg (B200 / sm_100a). Not part of the ABI.
+//
+// Data layout in HBM:
+//  * Caller-visible nodal vectors: contiguous (nx+1)(ny+1)(nz+1) fp64, x fastest.
+//  * JCG work vectors x, r, p, b live on the FREE BOX only. Dirichlet is imposed per face, so the
+//    free nodes of a level are the box [flo, flo+nf) per axis (flo = 1 if the face is Dirichlet,
+//    nf = n+1 minus the Dirichlet faces). Row pitch P = nf_x rounded up to 32 doubles (256 B
+//    rows), plane stride S = P * nf_y. Nodes outside the box are never stored: loads outside it
+//    return 0, which is exactly "p = 0 on Dirichlet nodes" of the eliminated system (§8c A5).
+//  * Element coefficients beta_e (element-beta path) on the global element grid with a zero
+//    ring of width 2: element (ex,ey,ez), -2 <= e <= n+1, at beta[(ez+2)*BS + (ey+2)*BP + ex+2].
+//    beta_e = 0 outside the domain, which truncates the stencil at Robin / Neumann faces.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ecmg {
+
+constexpr int kMaxParams = 48;
+
+enum Face { XM = 0, XP = 1, YM = 2, YP = 3, ZM = 4, ZP = 5 };
+enum { FACE_DIRICHLET = 0, FACE_ROBIN = 1 };
+
+// Problem registry entry passed by value to kernels (device-side evaluation of Eq. (bvp) data).
+struct Problem {
+  int id;
+  int face[6];
+  double alpha[6];        // Robin alpha per face (0 = Neumann)
+  double params[kMaxParams];
+  int n_params;
+};
+
+struct LevelGeom {
+  int n[3];          // cells per axis
+  double lo[3], h[3];
+  int flo[3];        // free box origin (global node index)
+  int nf[3];         // free box extent (nodes)
+  long long P, S;    // free-box vector row pitch / plane stride (doubles)
+  long long BP, BS;  // element-beta row pitch / plane stride (doubles), zero ring of 2
+  int elem_path;     // 1: element-beta stencil (variable beta or Robin faces); 0: constant stencil
+};
+
+// Constant-coefficient 27-point stencil (beta constant, all faces Dirichlet):
+// (A p)_i = sum_{oz} [c0[|oz|] p + cx[|oz|] (p_{x-1}+p_{x+1}) + cy[|oz|] (p_{y-1}+p_{y+1})
+//                    + cd[|oz|] (4 in-plane diagonals)] over the planes z+oz, oz in {-1,0,1}.
+// Derived from A = beta (K_x (x) M_y (x) M_z + M_x (x) K_y (x) M_z + M_x (x) M_y (x) K_z) with the
+// 1D stiffness K_d = [-1,2,-1]/h_d and mass M_d = h_d [1/6,2/3,1/6] (exact Q1 integrals).
+struct ConstStencil {
+  double c0[2], cx[2], cy[2], cd[2];
+  double dinv;   // 1 / diag (Jacobi), or 1 for plain CG
+};
+
+// Element stencil: K_ref[a][b] = kappa[pattern(a,b)], pattern = bit d set if a, b differ along d.
+// kappa[pat] = V sum_d (1/h_d^2) k(pat_d) prod_{e != d} m(pat_e), k(same)=1, k(diff)=-1,
+// m(same)=1/3, m(diff)=1/6. Robin face mass on face F: alpha h1 h2 m2[pat2], m2 = {1/9,1/18,1/18,1/36}.
+struct ElemStencil {
+  double kappa[8];
+  double robin[6];     // alpha_F * h1 * h2 for Robin faces with alpha != 0, else 0
+  int precond;         // 1 = Jacobi, 0 = plain CG (dinv = 1)
+};
+
+// Device-resident CG scalars (no host round trip inside the iteration).
+struct JcgScalars {
+  double rho;        // r.z
+  double rr;         // r.r
+  double alpha, beta, sigma;
+  double bb;         // ||b||^2 (set by the RHS kernel)
+  double rr_true;    // ||b - A x||^2 (set by the true-residual pass)
+  double thresh;     // eps * ||b|| (or eps if ||b|| = 0); <= 0: fixed-iteration mode
+  int iter, max_iter, done, status;
+  unsigned int counter;   // last-block-done counter (reset by the last block)
+  int pad_;
+};
+
+enum KMode { MODE_K1 = 1, MODE_K2 = 2, MODE_INIT = 3, MODE_TRUE = 4, MODE_APPLY = 5 };
+
+struct KArgs {
+  const double* h0;   // halo-read vector (K1: r, K2: p, INIT/TRUE: x, APPLY: p)
+  const double* h1;   // K1: p_old
+  const double* i0;   // interior-read vector (K2: x, INIT/TRUE: b)
+  const double* i1;   // K2: r
+  double* o0;         // K1: p_new, K2: x, INIT: r, APPLY: q
+  double* o1;         // K2: r
+  const double* beta; // element path: beta_e with zero ring
+  double* partials;   // per-block partial dot products (2 per block)
+  JcgScalars* sc;
+  int zc;             // planes per CTA
+  double eps;         // INIT only
+  int max_iter;       // INIT only
+};
+
+// status codes (mirror of ecmg_status)
+enum { ST_OK = 0, ST_EINVAL = -1, ST_ENOMEM = -2, ST_ENOTCONV = -3, ST_EBREAKDOWN = -4, ST_EDIAG = -5,
+       ST_EMISMATCH = -6, ST_ECUDA = -7, ST_ENCCL = -8 };
+
+// ---- launchers (kernels_*.cu) -------------------------------------------------------------
+cudaError_t launch_jcg_const(int mode, const LevelGeom& g, const ConstStencil& cs, const KArgs& a,
+                             cudaStream_t st);
+cudaError_t launch_jcg_elem(int mode, const LevelGeom& g, const ElemStencil& es, const Problem& pb,
+                            const KArgs& a, cudaStream_t st);
+int jcg_num_blocks(const LevelGeom& g, int elem_path, int zc);
+
+cudaError_t launch_beta(const LevelGeom& g, const Problem& pb, double* beta, cudaStream_t st);
+cudaError_t launch_rhs(const LevelGeom& g, const Problem& pb, const ElemStencil& es, double beta_const,
+                       const double* beta, double* b, double* partials, JcgScalars* sc, cudaStream_t st);
+cudaError_t launch_gather(const LevelGeom& g, const double* u, double* x, cudaStream_t st);
+cudaError_t launch_scatter(const LevelGeom& g, const double* x, double* u, cudaStream_t st);
+cudaError_t launch_dirichlet_fill(const LevelGeom& g, const Problem& pb, double* u, double value_if_none,
+                                  int zero_instead, cudaStream_t st);
+cudaError_t launch_exp_finite(const LevelGeom& gf, const Problem& pb, const double* u2h, const double* u4h,
+                              double* w, int variant, cudaStream_t st);
+cudaError_t launch_exp_true(const LevelGeom& gf, const Problem& pb, const double* uh, const double* u2h,
+                            double* ut, cudaStream_t st);
+cudaError_t launch_zero_vec(const LevelGeom& g, double* v, cudaStream_t st);
+
+}  // namespace ecmg
