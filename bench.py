@@ -1,0 +1,300 @@
+"""Benchmark of the ECMG_jcg hot path on B200 (driver contract: one JSON line from rank 0).
+
+Workload (BASELINE.json metric "fine-grid JCG unknown-iters/s (fp64) + ECMG time-to-solution at
+512^3"): configs[3] = C4, the singular solution u = r^{3/2} on the unit cube, beta = 1, Dirichlet
+everywhere, Q1 FE on 4^3 -> 512^3 (8 levels, 133,432,831 free unknowns on the finest grid),
+fp64, eps = 1e-9, final Richardson extrapolation.
+
+  step         one ecmg_run: all §8(a) rows (per-level setup, DSOLVE, EXP_finite, JCG, EXP_true)
+  ms_per_step  ECMG time-to-solution (device time, CUDA events, max over ranks)
+  value        whole-job JCG throughput of the step: sum over levels of free unknowns x JCG
+               iterations, divided by the time-to-solution ("unknown-iters/s")
+  jcg_fixed    the fine-grid JCG unknown-iters/s of SURVEY.md §8d D.1(i): 100 iterations of the
+               512^3 system from a seeded guess, stopping test off, CUDA events
+  roofline     the fused JCG iteration (K1 + K2) against the measured HBM copy peak
+  e2e          the same ecmg_run through the C ABI with HOST output buffers (D2H inside the step)
+  cpu_baseline the CPU oracle (oracle/, as it stands) on a bounded sample, rank 0, N = 1
+
+--impl reference times the oracle (the reference arm of this tier) on the host cores.
+Inputs larger than L2 (5+ GB working set vs 126 MB L2): no explicit L2 flush between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fine-grid JCG unknown-iters/s (fp64) + ECMG time-to-solution at 512^3"
+UNIT = "unknown-iters/s"
+BYTES_PER_UNKNOWN_ITER = 64   # x 1R+1W, r 2R+1W, p 2R+1W (constant-beta path)
+
+CONFIGS = {
+    # name: (problem id, coarsest, levels, eps, description)
+    "c4": (4, 4, 8, 1e-9, "C4 (BASELINE configs[3]): u=r^{3/2}, beta=1, Dirichlet, Q1, 4^3->512^3, eps=1e-9"),
+    "c2": (2, 4, 6, 1e-10, "C2 (BASELINE configs[1]): u=exp(x+y+z), beta=1, Dirichlet, Q1, 4^3->128^3, eps=1e-10"),
+    "c1": (1, 4, 4, 1e-8, "C1 (BASELINE configs[0]): u=sin sin sin, beta=1, Dirichlet, Q1, 4^3->32^3, eps=1e-8"),
+}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index, self.samples, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([s.strip() for s in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and s[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_oracle_sample(cfg_name, max_seconds_hint=30.0):
+    """The oracle as it stands, single thread, on a bounded sample of the workload: the same
+    problem and eps with the cascade truncated so the run takes ~10-30 s on one host core."""
+    import oracle
+    pid, n0, levels, eps, _ = CONFIGS[cfg_name]
+    sample_levels = min(levels, 6)   # 4^3 -> 128^3
+    t0 = time.perf_counter()
+    st, stats, _, _ = oracle.ecmg(n0, sample_levels, pid, eps)
+    dt = time.perf_counter() - t0
+    units = float(sum(max(0, r[0]) * r[16] for r in stats))
+    return {"value": units / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{cfg_name.upper()} truncated to {n0 * 2 ** (sample_levels - 1)}^3 ({sample_levels} levels), "
+                      f"eps={eps}; units = sum_k free_k*iters_k = {units:.4g}; wall {dt:.2f} s",
+            "status": int(st), "wall_s": dt}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    cfg = CONFIGS[args.config]
+    samples = []
+    for _ in range(args.warmup):
+        cpu_oracle_sample(args.config)
+    for _ in range(args.steps):
+        samples.append(cpu_oracle_sample(args.config))
+    v = statistics.mean(s["value"] for s in samples)
+    ms = statistics.mean(s["wall_s"] for s in samples) * 1e3
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (analytic problem, no dataset)",
+            "config": {"workload": cfg[4], "sample": samples[-1]["sample"]},
+            "cpu_baseline": {k: samples[-1][k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ecmg", choices=["ecmg", "reference"])
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--fixed-iters", type=int, default=100)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1506_02983_b200 import Grid, ecmg
+
+    pid, n0, levels, eps, desc = CONFIGS[args.config]
+    stream = torch.cuda.current_stream()
+    grid = Grid(n0, levels, pid)
+    shape, nodes = grid.shape(levels - 1)
+    u = torch.empty(nodes, dtype=torch.float64, device="cuda")
+    ut = torch.empty(nodes, dtype=torch.float64, device="cuda")
+
+    def barrier():
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if ws == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(max(3, args.warmup)):
+        grid.run(eps, u, ut)
+
+    # ---- timed region: K ECMG runs ------------------------------------------------------------
+    barrier()
+    l0 = ecmg.kernel_launches()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    units_total, fine_units, fine_ms = 0.0, 0.0, 0.0
+    per_level = None
+    with ClockSampler(local) as clk:
+        evs[0].record(stream)
+        for _ in range(args.steps):
+            st, stats = grid.run(eps, u, ut)
+            assert st == 0, ecmg.strerror(st)
+            per_level = stats
+            ms_j, it_j, nf_j = grid.last_jcg_timing()
+            fine_units += nf_j * it_j
+            fine_ms += ms_j
+            for k, s in enumerate(stats):
+                shp, _ = grid.shape(k)
+                nfree = (shp[0] - 1) * (shp[1] - 1) * (shp[2] - 1)
+                units_total += nfree * s["iterations"]
+        evs[1].record(stream)
+        barrier()
+    launches = ecmg.kernel_launches() - l0
+    t_ms = max_over_ranks(evs[0].elapsed_time(evs[1]))
+    ms_per_step = t_ms / args.steps
+    value = units_total * ws / (t_ms / 1e3)
+
+    # ---- fixed-iteration fine-grid JCG benchmark and roofline --------------
+    import numpy as np
+    import synth
+    fine = levels - 1
+    x0 = torch.from_numpy(synth.random_nodal(14, shape, (1, 1, 1), tuple(v - 1 for v in shape))).cuda()
+    xb = x0.clone()
+    grid.solve_level(fine, 0.0, 5, xb)   # warm-up (also sets up the level)
+    jt = []
+    for _ in range(3):
+        xb.copy_(x0)
+        grid.solve_level(fine, 0.0, args.fixed_iters, xb)
+        ms_j, it_j, nf_j = grid.last_jcg_timing()
+        jt.append((ms_j, it_j, nf_j))
+    ms_j, it_j, nf_j = sorted(jt)[len(jt) // 2]
+    jcg_ups = nf_j * it_j / (ms_j / 1e3)
+    peak, peak_src = load_peaks()
+    achieved = BYTES_PER_UNKNOWN_ITER * nf_j * it_j / (ms_j / 1e3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "jcg_traffic.json")) as f:
+            traffic = json.load(f).get("bytes_per_iteration_k1_k2")
+    except Exception:
+        pass
+
+    # ---- e2e: the same call with host output buffers -------------------------------------------
+    uh = torch.empty(nodes, dtype=torch.float64).pin_memory()
+    uth = torch.empty(nodes, dtype=torch.float64).pin_memory()
+    grid.run(eps, uh, uth)
+    barrier()
+    t0 = time.perf_counter()
+    e_units = 0.0
+    e_steps = max(1, min(args.steps, 3))
+    for _ in range(e_steps):
+        st, stats = grid.run(eps, uh, uth)
+        for k, s in enumerate(stats):
+            shp, _ = grid.shape(k)
+            e_units += (shp[0] - 1) * (shp[1] - 1) * (shp[2] - 1) * s["iterations"]
+    barrier()
+    e_s = max_over_ranks(time.perf_counter() - t0)
+    e2e = {"value": e_units * ws / e_s, "unit": UNIT, "h2d_bytes_per_step": 0,
+           "d2h_bytes_per_step": 2 * nodes * 8, "ms_per_step": e_s / e_steps * 1e3,
+           "note": "C ABI ecmg_run with pinned host u_h and u~_h (D2H inside the call); C4 inputs are analytic (no H2D)"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            c = cpu_oracle_sample(args.config)
+            cpu = {k: c[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as ex:   # the oracle is a reported baseline, never a fallback
+            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": f"failed: {ex}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (analytic C4 problem; no dataset)",
+            "config": {"workload": desc, "levels": levels, "finest_cells": list(shape), "eps": eps,
+                       "free_unknowns_finest": int(nf_j), "parallelism": "replicas" if ws > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (no flush)",
+                       "iterations_per_level": [s["iterations"] for s in per_level]},
+            "ecmg_tts_ms": ms_per_step,
+            "fine_grid_jcg_in_run": {"value": fine_units / (fine_ms / 1e3), "unit": UNIT,
+                                     "iterations": int(per_level[-1]["iterations"])},
+            "jcg_fixed": {"value": jcg_ups, "unit": UNIT, "iterations": it_j, "ms": ms_j,
+                          "ms_per_iteration": ms_j / it_j},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "kernel": "jcg K1+K2 (one CG iteration)",
+                         "bytes_per_unit": BYTES_PER_UNKNOWN_ITER, "peak_source": peak_src},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "per_level_ms": [{"setup": s["ms_setup"], "exp": s["ms_exp"], "solve": s["ms_solve"], "rich": s["ms_rich"]}
+                             for s in per_level],
+        }
+        print(json.dumps(line), flush=True)
+    grid.close()
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -161,6 +161,10 @@ int ecmg_level_shape(const ecmg_grid* grid, int level, int n_cells3[3], long lon
  * total milliseconds and number of iterations timed (CUDA events around the iteration loop). */
 int ecmg_last_jcg_timing(const ecmg_grid* grid, double* ms, int* iterations, long long* free_unknowns);
 
+/* Number of CUDA kernels libecmg has launched in this process (all grids; monotone counter).
+ * bench.py reports the difference across its timed region as "gpu_launches". */
+long long ecmg_kernel_launches(void);
+
 int ecmg_destroy_grid(ecmg_grid* grid);
 const char* ecmg_strerror(int status);
 

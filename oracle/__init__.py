@@ -65,7 +65,7 @@ def lib():
             L.orc_get_dirichlet.argtypes = [vp, C.POINTER(C.c_ubyte), dp]
             L.orc_apply.argtypes = [vp, dp, dp]
             L.orc_jcg.restype = C.c_int
-            L.orc_jcg.argtypes = [vp, dp, C.c_double, C.c_int, C.c_int, ip, dp, dp, dp]
+            L.orc_jcg.argtypes = [vp, dp, C.c_double, C.c_int, C.c_int, C.c_int, ip, dp, dp, dp]
             L.orc_dsolve.restype = C.c_int
             L.orc_dsolve.argtypes = [vp, dp]
             L.orc_exact.argtypes = [vp, dp]
@@ -158,10 +158,12 @@ class Level:
         lib().orc_apply(self._h, _d(p), _d(q))
         return q
 
-    def jcg(self, x0, eps, max_iter, precond=True):
+    def jcg(self, x0, eps, max_iter, precond=True, dot_reverse=False):
+        """Textbook JCG / CG. dot_reverse sums the dot products in reverse node order: only for
+        measuring the oracle's own rounding-order spread."""
         x = _f64(x0).copy()
         it, rr, rt, nb = C.c_int(), C.c_double(), C.c_double(), C.c_double()
-        st = lib().orc_jcg(self._h, _d(x), float(eps), int(max_iter), 1 if precond else 0,
+        st = lib().orc_jcg(self._h, _d(x), float(eps), int(max_iter), 1 if precond else 0, 1 if dot_reverse else 0,
                            C.byref(it), C.byref(rr), C.byref(rt), C.byref(nb))
         return x, dict(status=st, iterations=it.value, rel_recur=rr.value, rel_true=rt.value, normb=nb.value)
 

@@ -418,6 +418,15 @@ double dot_free(const Level& L, const double* a, const double* b) {
   return s;
 }
 
+// the same sum in reverse node order: used only to measure the oracle's own rounding-order spread
+// of CG iterates (reading §8c A22), never for a reported result
+double dot_free_reversed(const Level& L, const double* a, const double* b) {
+  double s = 0.0;
+  for (long i = L.N - 1; i >= 0; --i)
+    if (!L.dir[i]) s += a[i] * b[i];
+  return s;
+}
+
 struct SolveStats {
   int iterations = 0;
   double rel_recur = 0.0, rel_true = 0.0, normb = 0.0;
@@ -427,8 +436,11 @@ struct SolveStats {
 // Textbook JCG (precond = 1) or CG (precond = 0), SURVEY.md §8c O7. x is a full nodal vector:
 // on entry its free part is the initial guess, on exit the iterate; Dirichlet entries := g_D.
 // eps <= 0 means "run exactly max_iter iterations" (fixed-iteration parity and benchmark mode).
-SolveStats jcg(const Level& L, double* x, double eps, int max_iter, int precond) {
+SolveStats jcg(const Level& L, double* x, double eps, int max_iter, int precond, int dot_reverse = 0) {
   SolveStats st;
+  auto dot_free = [&](const Level& LL, const double* a, const double* b) {
+    return dot_reverse ? dot_free_reversed(LL, a, b) : ::dot_free(LL, a, b);
+  };
   const long N = L.N;
   std::vector<double> r(N, 0.0), z(N, 0.0), p(N, 0.0), w(N, 0.0), dinv(N, 0.0);
   for (long i = 0; i < N; ++i) {
@@ -748,9 +760,9 @@ void orc_get_dirichlet(const orc_level* h, unsigned char* mask, double* gD) {
 }
 void orc_apply(const orc_level* h, const double* p, double* q) { apply_ff(h->L, p, q); }
 
-int orc_jcg(const orc_level* h, double* x, double eps, int max_iter, int precond, int* iters,
+int orc_jcg(const orc_level* h, double* x, double eps, int max_iter, int precond, int dot_reverse, int* iters,
             double* rel_recur, double* rel_true, double* normb) {
-  SolveStats st = jcg(h->L, x, eps, max_iter, precond);
+  SolveStats st = jcg(h->L, x, eps, max_iter, precond, dot_reverse);
   *iters = st.iterations; *rel_recur = st.rel_recur; *rel_true = st.rel_true; *normb = st.normb;
   return st.status;
 }

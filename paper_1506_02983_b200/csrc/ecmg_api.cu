@@ -18,6 +18,10 @@
 
 using namespace ecmg;
 
+#include <atomic>
+static std::atomic<long long> g_launches{0};
+namespace ecmg { void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); } }
+
 struct ecmg_grid {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -276,6 +280,8 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
 
 extern "C" {
 
+long long ecmg_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
+
 const char* ecmg_strerror(int s) {
   switch (s) {
     case ECMG_OK: return "ok";
@@ -464,7 +470,6 @@ int ecmg_apply_operator(ecmg_grid* G, int level, const double* p, double* q) {
   ECMG_CUDA(cudaMemsetAsync(q, 0, sizeof(double) * level_nodes(g), G->stream));
   ECMG_CUDA(launch_scatter(g, G->r, q, G->stream));
   ECMG_CUDA(cudaStreamSynchronize(G->stream));
-  G->setup_level = G->elem_path ? G->setup_level : G->setup_level;
   return ECMG_OK;
 }
 

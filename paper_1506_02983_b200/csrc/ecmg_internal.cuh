@@ -94,6 +94,8 @@ enum { ST_OK = 0, ST_EINVAL = -1, ST_ENOMEM = -2, ST_ENOTCONV = -3, ST_EBREAKDOW
        ST_EMISMATCH = -6, ST_ECUDA = -7, ST_ENCCL = -8 };
 
 // ---- launchers (kernels_*.cu) -------------------------------------------------------------
+// Every launcher bumps this process-wide counter once per kernel launch (ecmg_kernel_launches).
+void count_launch(int n = 1);
 cudaError_t launch_jcg_const(int mode, const LevelGeom& g, const ConstStencil& cs, const KArgs& a,
                              cudaStream_t st);
 cudaError_t launch_jcg_elem(int mode, const LevelGeom& g, const ElemStencil& es, const Problem& pb,

@@ -183,6 +183,7 @@ __global__ void k_exp_true(const LevelGeom gf, const Problem pb, const double* _
 cudaError_t launch_exp_finite(const LevelGeom& gf, const Problem& pb, const double* u2h, const double* u4h, double* w,
                               int variant, cudaStream_t st) {
   dim3 grid((gf.n[0] + 1 + EFX - 1) / EFX, (gf.n[1] + 1 + 3) / 4, (gf.n[2] + 1 + 3) / 4);
+  count_launch();
   k_exp_finite<<<grid, ENTH, 0, st>>>(gf, pb, u2h, u4h, w, variant);
   return cudaGetLastError();
 }
@@ -190,6 +191,7 @@ cudaError_t launch_exp_finite(const LevelGeom& gf, const Problem& pb, const doub
 cudaError_t launch_exp_true(const LevelGeom& gf, const Problem& pb, const double* uh, const double* u2h, double* ut,
                             cudaStream_t st) {
   dim3 grid((gf.n[0] + 1 + 127) / 128, gf.n[1] + 1, gf.n[2] + 1);
+  count_launch();
   k_exp_true<<<grid, 128, 0, st>>>(gf, pb, uh, u2h, ut);
   return cudaGetLastError();
 }

@@ -541,11 +541,11 @@ cudaError_t launch_jcg_const(int mode, const LevelGeom& g, const ConstStencil& c
   dim3 block(TX, WARPS);
   dim3 grid((g.nf[0] + TX - 1) / TX, (g.nf[1] + CTY - 1) / CTY, (g.nf[2] + a.zc - 1) / a.zc);
   switch (mode) {
-    case MODE_K1: k_jcg_const<MODE_K1><<<grid, block, 0, st>>>(g, cs, a); break;
-    case MODE_K2: k_jcg_const<MODE_K2><<<grid, block, 0, st>>>(g, cs, a); break;
-    case MODE_INIT: k_jcg_const<MODE_INIT><<<grid, block, 0, st>>>(g, cs, a); break;
-    case MODE_TRUE: k_jcg_const<MODE_TRUE><<<grid, block, 0, st>>>(g, cs, a); break;
-    case MODE_APPLY: k_jcg_const<MODE_APPLY><<<grid, block, 0, st>>>(g, cs, a); break;
+    case MODE_K1: count_launch(); k_jcg_const<MODE_K1><<<grid, block, 0, st>>>(g, cs, a); break;
+    case MODE_K2: count_launch(); k_jcg_const<MODE_K2><<<grid, block, 0, st>>>(g, cs, a); break;
+    case MODE_INIT: count_launch(); k_jcg_const<MODE_INIT><<<grid, block, 0, st>>>(g, cs, a); break;
+    case MODE_TRUE: count_launch(); k_jcg_const<MODE_TRUE><<<grid, block, 0, st>>>(g, cs, a); break;
+    case MODE_APPLY: count_launch(); k_jcg_const<MODE_APPLY><<<grid, block, 0, st>>>(g, cs, a); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -560,6 +560,7 @@ static cudaError_t launch_elem_mode(dim3 grid, dim3 block, const LevelGeom& g, c
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
+  count_launch();
   k_jcg_elem<MODE><<<grid, block, ELEM_SMEM, st>>>(g, es, pb, a);
   return cudaGetLastError();
 }

@@ -239,6 +239,7 @@ __global__ void k_zero_free(const LevelGeom g, double* __restrict__ v) {
 cudaError_t launch_beta(const LevelGeom& g, const Problem& pb, double* beta, cudaStream_t st) {
   const long long total = (long long)(g.n[0] + 4) * (g.n[1] + 4) * (g.n[2] + 4);
   const int nb = (int)std::min<long long>((total + 255) / 256, 148LL * 32);
+  count_launch();
   k_beta<<<nb, 256, 0, st>>>(g, pb, beta);
   return cudaGetLastError();
 }
@@ -246,18 +247,21 @@ cudaError_t launch_beta(const LevelGeom& g, const Problem& pb, double* beta, cud
 cudaError_t launch_rhs(const LevelGeom& g, const Problem& pb, const ElemStencil& es, double beta_const, const double* beta,
                        double* b, double* partials, JcgScalars* sc, cudaStream_t st) {
   dim3 grid((g.nf[0] + RX - 1) / RX, (g.nf[1] + RY - 1) / RY, (g.nf[2] + RZ - 1) / RZ);
+  count_launch();
   k_rhs<<<grid, RNTH, 0, st>>>(g, pb, es, beta_const, beta, b, partials, sc);
   return cudaGetLastError();
 }
 
 cudaError_t launch_gather(const LevelGeom& g, const double* u, double* x, cudaStream_t st) {
   dim3 grid((g.nf[0] + 127) / 128, g.nf[1], g.nf[2]);
+  count_launch();
   k_gather<<<grid, 128, 0, st>>>(g, u, x);
   return cudaGetLastError();
 }
 
 cudaError_t launch_scatter(const LevelGeom& g, const double* x, double* u, cudaStream_t st) {
   dim3 grid((g.nf[0] + 127) / 128, g.nf[1], g.nf[2]);
+  count_launch();
   k_scatter<<<grid, 128, 0, st>>>(g, x, u);
   return cudaGetLastError();
 }
@@ -269,6 +273,7 @@ cudaError_t launch_dirichlet_fill(const LevelGeom& g, const Problem& pb, double*
     const int d = F >> 1;
     const int d1 = (d == 0) ? 1 : 0, d2 = (d == 2) ? 1 : 2;
     dim3 grid((g.n[d1] + 1 + 127) / 128, g.n[d2] + 1);
+    count_launch();
     k_dirichlet_face<<<grid, 128, 0, st>>>(g, pb, u, F, zero_instead);
   }
   return cudaGetLastError();
@@ -276,6 +281,7 @@ cudaError_t launch_dirichlet_fill(const LevelGeom& g, const Problem& pb, double*
 
 cudaError_t launch_zero_vec(const LevelGeom& g, double* v, cudaStream_t st) {
   dim3 grid((g.nf[0] + 127) / 128, g.nf[1], g.nf[2]);
+  count_launch();
   k_zero_free<<<grid, 128, 0, st>>>(g, v);
   return cudaGetLastError();
 }

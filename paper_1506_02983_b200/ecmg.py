@@ -24,8 +24,8 @@ OPT_EXP_VARIANT, OPT_PRECOND, OPT_ZCHUNK = 1, 2, 3
 
 EXPORTS = ["ecmg_create_grid", "ecmg_set_coeffs", "ecmg_set_option", "ecmg_solve_level",
            "ecmg_prolongate_extrapolate", "ecmg_richardson", "ecmg_run", "ecmg_apply_operator",
-           "ecmg_level_rhs", "ecmg_level_shape", "ecmg_last_jcg_timing", "ecmg_destroy_grid",
-           "ecmg_strerror"]
+           "ecmg_level_rhs", "ecmg_level_shape", "ecmg_last_jcg_timing", "ecmg_kernel_launches",
+           "ecmg_destroy_grid", "ecmg_strerror"]
 
 
 class ecmg_box(C.Structure):
@@ -79,12 +79,14 @@ def lib():
         L.ecmg_level_rhs.argtypes = [vp, C.c_int, vp, dp]
         L.ecmg_level_shape.argtypes = [vp, C.c_int, ip, C.POINTER(C.c_longlong), ip, ip]
         L.ecmg_last_jcg_timing.argtypes = [vp, dp, ip, C.POINTER(C.c_longlong)]
+        L.ecmg_kernel_launches.argtypes = []
         L.ecmg_destroy_grid.argtypes = [vp]
         L.ecmg_strerror.argtypes = [C.c_int]
         L.ecmg_strerror.restype = C.c_char_p
         for name in EXPORTS:
-            if name != "ecmg_strerror":
+            if name not in ("ecmg_strerror", "ecmg_kernel_launches"):
                 getattr(L, name).restype = C.c_int
+        L.ecmg_kernel_launches.restype = C.c_longlong
         _lib = L
     return _lib
 
@@ -174,6 +176,10 @@ def last_jcg_timing(grid):
     ms, it, nf = C.c_double(), C.c_int(), C.c_longlong()
     s = lib().ecmg_last_jcg_timing(grid, C.byref(ms), C.byref(it), C.byref(nf))
     return s, ms.value, it.value, nf.value
+
+
+def kernel_launches():
+    return int(lib().ecmg_kernel_launches())
 
 
 def destroy_grid(grid):
