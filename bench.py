@@ -228,6 +228,12 @@ def main():
         jt.append((ms_j, it_j, nf_j))
     ms_j, it_j, nf_j = sorted(jt)[len(jt) // 2]
     jcg_ups = nf_j * it_j / (ms_j / 1e3)
+    # ablation: the register-prefetch (non-TMA) kernels on the same system
+    grid.set_option(ecmg.OPT_KERNEL, 0)
+    xb.copy_(x0)
+    grid.solve_level(fine, 0.0, args.fixed_iters, xb)
+    ms_p, it_p, _ = grid.last_jcg_timing()
+    grid.set_option(ecmg.OPT_KERNEL, 1)
     peak, peak_src = load_peaks()
     achieved = BYTES_PER_UNKNOWN_ITER * nf_j * it_j / (ms_j / 1e3) / 1e9
     traffic = None
@@ -278,7 +284,10 @@ def main():
             "fine_grid_jcg_in_run": {"value": fine_units / (fine_ms / 1e3), "unit": UNIT,
                                      "iterations": int(per_level[-1]["iterations"])},
             "jcg_fixed": {"value": jcg_ups, "unit": UNIT, "iterations": it_j, "ms": ms_j,
-                          "ms_per_iteration": ms_j / it_j},
+                          "ms_per_iteration": ms_j / it_j, "kernel": "TMA-fed (default)"},
+            "jcg_fixed_ablation_prefetch": {"value": nf_j * it_p / (ms_p / 1e3), "unit": UNIT,
+                                            "ms_per_iteration": ms_p / max(1, it_p),
+                                            "kernel": "register-prefetch loads (ECMG_OPT_KERNEL=0)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "kernel": "jcg K1+K2 (one CG iteration)",
                          "bytes_per_unit": BYTES_PER_UNKNOWN_ITER, "peak_source": peak_src},

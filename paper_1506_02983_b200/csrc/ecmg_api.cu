@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -44,10 +45,14 @@ struct ecmg_grid {
   JcgScalars* sc_host = nullptr;   // pinned, 2 slots
   std::vector<double*> u;          // per-level full nodal vectors (ecmg_run)
   double* ut_tmp = nullptr;
+  double* scratch1d = nullptr;     // 1D Gauss load tables (separable right-hand sides)
+  double* seeds = nullptr;         // EXP_finite: extrapolated values on the 2h grid of the finest level
   long long vec_doubles = 0, beta_doubles = 0, partial_doubles = 0;
   int setup_level = -1;
   cudaEvent_t ev[16];
   bool ev_init = false;
+  int kernel_variant = 1;   // ECMG_OPT_KERNEL
+  struct Maps { int level = -1; CUtensorMap xh, xi, rh, ri, ph[2], bi; bool ok = false; } maps;
   double last_jcg_ms = 0.0;
   int last_jcg_iters = 0;
   long long last_free = 0;
@@ -57,10 +62,17 @@ namespace {
 
 inline int cuda_status(cudaError_t e) { return e == cudaSuccess ? ECMG_OK : (e == cudaErrorMemoryAllocation ? ECMG_ENOMEM : ECMG_ECUDA); }
 
-#define ECMG_CUDA(call)                          \
-  do {                                           \
-    cudaError_t e_ = (call);                     \
-    if (e_ != cudaSuccess) return cuda_status(e_); \
+// ECMG_DEBUG=1 in the environment prints the failing call and the CUDA error string
+inline int report_cuda(cudaError_t e, const char* what, int line) {
+  static const bool dbg = std::getenv("ECMG_DEBUG") != nullptr;
+  if (dbg) std::fprintf(stderr, "libecmg: %s failed at ecmg_api.cu:%d: %s\n", what, line, cudaGetErrorString(e));
+  return cuda_status(e);
+}
+
+#define ECMG_CUDA(call)                                              \
+  do {                                                               \
+    cudaError_t e_ = (call);                                         \
+    if (e_ != cudaSuccess) return report_cuda(e_, #call, __LINE__);  \
   } while (0)
 
 bool problem_faces(int id, int face[6], double alpha[6], int* nparams_required) {
@@ -156,12 +168,56 @@ int auto_zc(const ecmg_grid* G, const LevelGeom& g) {
   return (int)((g.nf[2] + nchunks - 1) / nchunks);
 }
 
+// TMA descriptors of the free-box work vectors for one level (cached; rebuilt when the level changes)
+bool ensure_maps(ecmg_grid* G, const LevelGeom& g, int level) {
+  auto& M = G->maps;
+  if (M.level == level) return M.ok;
+  const int hx = tma_halo_box_x(), hy = tma_halo_box_y(), ix = tma_int_box_x(), iy = tma_int_box_y();
+  M.ok = make_vec_tensor_map(&M.xh, G->x, g, hx, hy) == 0 && make_vec_tensor_map(&M.xi, G->x, g, ix, iy) == 0 &&
+         make_vec_tensor_map(&M.rh, G->r, g, hx, hy) == 0 && make_vec_tensor_map(&M.ri, G->r, g, ix, iy) == 0 &&
+         make_vec_tensor_map(&M.ph[0], G->p[0], g, hx, hy) == 0 && make_vec_tensor_map(&M.ph[1], G->p[1], g, hx, hy) == 0 &&
+         make_vec_tensor_map(&M.bi, G->b, g, ix, iy) == 0;
+  M.level = level;
+  return M.ok;
+}
+
+const CUtensorMap* halo_map(ecmg_grid* G, const double* p) {
+  auto& M = G->maps;
+  if (p == G->x) return &M.xh;
+  if (p == G->r) return &M.rh;
+  if (p == G->p[0]) return &M.ph[0];
+  if (p == G->p[1]) return &M.ph[1];
+  return nullptr;
+}
+const CUtensorMap* int_map(ecmg_grid* G, const double* p) {
+  auto& M = G->maps;
+  if (p == G->x) return &M.xi;
+  if (p == G->r) return &M.ri;
+  if (p == G->b) return &M.bi;
+  return nullptr;
+}
+
+int level_of(const ecmg_grid* G, const LevelGeom& g) {
+  for (int k = 0; k < G->L; ++k) if (&G->geom[k] == &g) return k;
+  return -1;
+}
+
 cudaError_t launch_mode(ecmg_grid* G, int mode, const LevelGeom& g, const KArgs& a) {
   if (G->elem_path) {
     const ElemStencil es = make_elem_stencil(g, G->prob, G->precond);
     return launch_jcg_elem(mode, g, es, G->prob, a, G->stream);
   }
   const ConstStencil cs = make_const_stencil(g, 1.0, G->precond);
+  if (G->kernel_variant == 1 && ensure_maps(G, g, level_of(G, g))) {
+    const CUtensorMap* h0 = halo_map(G, a.h0);
+    const CUtensorMap* h1 = a.h1 ? halo_map(G, a.h1) : h0;
+    const CUtensorMap* i0 = a.i0 ? int_map(G, a.i0) : h0;
+    const CUtensorMap* i1 = a.i1 ? int_map(G, a.i1) : h0;
+    if (h0 && h1 && i0 && i1) {
+      CUtensorMap m[4] = {*h0, *h1, *i0, *i1};
+      return launch_jcg_const_tma(mode, g, cs, a, m, G->stream);
+    }
+  }
   return launch_jcg_const(mode, g, cs, a, G->stream);
 }
 
@@ -169,7 +225,7 @@ int setup_level(ecmg_grid* G, int k) {
   const LevelGeom& g = G->geom[k];
   const ElemStencil es = make_elem_stencil(g, G->prob, G->precond);
   if (G->elem_path) ECMG_CUDA(launch_beta(g, G->prob, G->beta, G->stream));
-  ECMG_CUDA(launch_rhs(g, G->prob, es, 1.0, G->elem_path ? G->beta : nullptr, G->b, G->partials, G->sc, G->stream));
+  ECMG_CUDA(launch_rhs(g, G->prob, es, 1.0, G->elem_path ? G->beta : nullptr, G->b, G->scratch1d, G->stream));
   G->setup_level = k;
   return ECMG_OK;
 }
@@ -323,7 +379,7 @@ int ecmg_create_grid(const ecmg_box* dom, const int coarsest_cells[3], int num_l
   G->beta_doubles = (long long)(gmax.n[0] + 4) * (gmax.n[1] + 4) * (gmax.n[2] + 4);
   const long long rhs_blocks = (long long)((gmax.nf[0] + 7) / 8) * ((gmax.nf[1] + 7) / 8) * ((gmax.nf[2] + 3) / 4);
   const long long jcg_blocks = (long long)((gmax.nf[0] + 31) / 32) * ((gmax.nf[1] + 7) / 8) * gmax.nf[2];
-  G->partial_doubles = 2 * std::max(rhs_blocks, jcg_blocks) + 64;
+  G->partial_doubles = 3 * std::max(rhs_blocks, jcg_blocks) + 64;
   int st = ECMG_OK;
   auto alloc = [&](double** p, long long n) {
     if (st != ECMG_OK) return;
@@ -336,6 +392,8 @@ int ecmg_create_grid(const ecmg_box* dom, const int coarsest_cells[3], int num_l
   alloc(&G->p[1], G->vec_doubles);
   alloc(&G->b, G->vec_doubles);
   alloc(&G->partials, G->partial_doubles);
+  alloc(&G->scratch1d, 3LL * (std::max(gmax.n[0], std::max(gmax.n[1], gmax.n[2])) + 1));
+  alloc(&G->seeds, (long long)(gmax.n[0] / 2 + 1) * (gmax.n[1] / 2 + 1) * (gmax.n[2] / 2 + 1));
   if (st == ECMG_OK && cudaMalloc(&G->sc, sizeof(JcgScalars)) != cudaSuccess) st = ECMG_ENOMEM;
   if (st == ECMG_OK && cudaMemsetAsync(G->sc, 0, sizeof(JcgScalars), G->stream) != cudaSuccess) st = ECMG_ECUDA;
   if (st == ECMG_OK && cudaHostAlloc(&G->sc_host, 2 * sizeof(JcgScalars), cudaHostAllocDefault) != cudaSuccess) st = ECMG_ENOMEM;
@@ -356,6 +414,8 @@ int ecmg_destroy_grid(ecmg_grid* G) {
   cudaFree(G->beta); cudaFree(G->partials); cudaFree(G->sc);
   for (double* p : G->u) cudaFree(p);
   cudaFree(G->ut_tmp);
+  cudaFree(G->scratch1d);
+  cudaFree(G->seeds);
   if (G->sc_host) cudaFreeHost(G->sc_host);
   if (G->ev_init) for (int i = 0; i < 16; ++i) cudaEventDestroy(G->ev[i]);
   cudaGetLastError();
@@ -394,6 +454,7 @@ int ecmg_set_coeffs(ecmg_grid* G, const ecmg_problem* pr) {
   for (int k = 0; k < G->L; ++k) G->geom.push_back(make_geom(G, k, pb.face, elem_path));
   G->has_problem = true;
   G->setup_level = -1;
+  G->maps.level = -1;
   return ECMG_OK;
 }
 
@@ -403,6 +464,7 @@ int ecmg_set_option(ecmg_grid* G, int option, int value) {
     case ECMG_OPT_EXP_VARIANT: if (value != 0 && value != 1) return ECMG_EINVAL; G->exp_variant = value; break;
     case ECMG_OPT_PRECOND: if (value != 0 && value != 1) return ECMG_EINVAL; G->precond = value; G->setup_level = -1; break;
     case ECMG_OPT_ZCHUNK: if (value < 0) return ECMG_EINVAL; G->zchunk = value; break;
+    case ECMG_OPT_KERNEL: if (value != 0 && value != 1) return ECMG_EINVAL; G->kernel_variant = value; break;
     default: return ECMG_EINVAL;
   }
   return ECMG_OK;
@@ -444,7 +506,7 @@ int ecmg_prolongate_extrapolate(ecmg_grid* G, int level, const double* u2h, cons
   if (!G || !u2h || !u4h || !w || !G->has_problem || level < 2 || level >= G->L) return ECMG_EINVAL;
   const LevelGeom& g = G->geom[level];
   for (int d = 0; d < 3; ++d) if (g.n[d] % 4) return ECMG_EMISMATCH;
-  ECMG_CUDA(launch_exp_finite(g, G->prob, u2h, u4h, w, G->exp_variant, G->stream));
+  ECMG_CUDA(launch_exp_finite(g, G->prob, u2h, u4h, w, G->exp_variant, G->seeds, 0, G->stream));
   ECMG_CUDA(cudaStreamSynchronize(G->stream));
   return ECMG_OK;
 }
@@ -479,6 +541,14 @@ int ecmg_level_rhs(ecmg_grid* G, int level, double* bout, double* norm_b) {
   if (G->setup_level != level) { int s = setup_level(G, level); if (s) return s; }
   ECMG_CUDA(cudaMemsetAsync(bout, 0, sizeof(double) * level_nodes(g), G->stream));
   ECMG_CUDA(launch_scatter(g, G->b, bout, G->stream));
+  // ||b||^2 is accumulated by the JCG init pass; run it at x = 0
+  ECMG_CUDA(launch_zero_vec(g, G->x, G->stream));
+  {
+    KArgs a{};
+    a.partials = G->partials; a.sc = G->sc; a.zc = auto_zc(G, g); a.beta = G->beta;
+    a.h0 = G->x; a.i0 = G->b; a.o0 = G->r; a.eps = 0.0; a.max_iter = 0;
+    ECMG_CUDA(launch_mode(G, MODE_INIT, g, a));
+  }
   ECMG_CUDA(cudaMemcpyAsync(&G->sc_host[0], G->sc, sizeof(JcgScalars), cudaMemcpyDeviceToHost, G->stream));
   ECMG_CUDA(cudaStreamSynchronize(G->stream));
   if (norm_b) *norm_b = std::sqrt(G->sc_host[0].bb);
@@ -529,8 +599,8 @@ int ecmg_run(ecmg_grid* G, double eps, ecmg_stats* per_level, double* u_fine, do
       if (s == ECMG_ENOTCONV) s = ECMG_OK;   // tiny systems may stall just above 1e-14; accepted
     } else {
       // W_h = EXP_finite(u_2h, u_4h) (Alg. 4 l.6), then JCG from W_h (l.7-9)
-      ECMG_CUDA(launch_exp_finite(g, G->prob, G->u[k - 1], G->u[k - 2], G->u[k], G->exp_variant, G->stream));
-      ECMG_CUDA(launch_gather(g, G->u[k], G->x, G->stream));
+      // written straight into the free-box work vector (Dirichlet values are filled after the solve)
+      ECMG_CUDA(launch_exp_finite(g, G->prob, G->u[k - 1], G->u[k - 2], G->x, G->exp_variant, G->seeds, 1, G->stream));
       ECMG_CUDA(cudaEventRecord(e2, G->stream));
       s = run_jcg(G, k, eps, 10000, &st);
     }

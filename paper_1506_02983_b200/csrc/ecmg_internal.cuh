@@ -101,16 +101,26 @@ cudaError_t launch_jcg_const(int mode, const LevelGeom& g, const ConstStencil& c
 cudaError_t launch_jcg_elem(int mode, const LevelGeom& g, const ElemStencil& es, const Problem& pb,
                             const KArgs& a, cudaStream_t st);
 int jcg_num_blocks(const LevelGeom& g, int elem_path, int zc);
+}  // namespace ecmg
+#include <cuda.h>
+namespace ecmg {
+cudaError_t launch_jcg_const_tma(int mode, const LevelGeom& g, const ConstStencil& cs, const KArgs& a,
+                                 const CUtensorMap* maps, cudaStream_t st);
+int make_vec_tensor_map(CUtensorMap* map, const double* base, const LevelGeom& g, int bx, int by);
+int tma_halo_box_x();
+int tma_halo_box_y();
+int tma_int_box_x();
+int tma_int_box_y();
 
 cudaError_t launch_beta(const LevelGeom& g, const Problem& pb, double* beta, cudaStream_t st);
 cudaError_t launch_rhs(const LevelGeom& g, const Problem& pb, const ElemStencil& es, double beta_const,
-                       const double* beta, double* b, double* partials, JcgScalars* sc, cudaStream_t st);
+                       const double* beta, double* b, double* scratch, cudaStream_t st);
 cudaError_t launch_gather(const LevelGeom& g, const double* u, double* x, cudaStream_t st);
 cudaError_t launch_scatter(const LevelGeom& g, const double* x, double* u, cudaStream_t st);
 cudaError_t launch_dirichlet_fill(const LevelGeom& g, const Problem& pb, double* u, double value_if_none,
                                   int zero_instead, cudaStream_t st);
 cudaError_t launch_exp_finite(const LevelGeom& gf, const Problem& pb, const double* u2h, const double* u4h,
-                              double* w, int variant, cudaStream_t st);
+                              double* w, int variant, double* seeds, int freebox, cudaStream_t st);
 cudaError_t launch_exp_true(const LevelGeom& gf, const Problem& pb, const double* uh, const double* u2h,
                             double* ut, cudaStream_t st);
 cudaError_t launch_zero_vec(const LevelGeom& g, double* v, cudaStream_t st);

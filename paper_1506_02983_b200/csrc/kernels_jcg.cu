@@ -16,93 +16,10 @@
 // partial sums kept in registers, so every value is loaded from shared memory a few times only.
 #include "ecmg_internal.cuh"
 #include "problems.cuh"
+#include "jcg_common.cuh"
 
 namespace ecmg {
 namespace {
-
-constexpr int TX = 32;
-constexpr int WARPS = 8;
-constexpr int NTH = TX * WARPS;
-
-// ---- deterministic reductions and the device-side CG scalar updates -----------------------
-
-__device__ __forceinline__ void block_sum2(double& a, double& b, double* red) {
-  const int tid = threadIdx.x + TX * threadIdx.y;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    a += __shfl_down_sync(0xffffffffu, a, o);
-    b += __shfl_down_sync(0xffffffffu, b, o);
-  }
-  if ((tid & 31) == 0) { red[2 * (tid >> 5)] = a; red[2 * (tid >> 5) + 1] = b; }
-  __syncthreads();
-  if (tid == 0) {
-    double sa = 0.0, sb = 0.0;
-    for (int w = 0; w < NTH / 32; ++w) { sa += red[2 * w]; sb += red[2 * w + 1]; }
-    a = sa; b = sb;
-  }
-}
-
-__device__ void finalize(int mode, const KArgs& a, double s0, double s1) {
-  JcgScalars* sc = a.sc;
-  switch (mode) {
-    case MODE_INIT: {
-      sc->rho = s0; sc->rr = s1; sc->alpha = 0.0; sc->beta = 0.0; sc->sigma = 0.0;
-      sc->iter = 0; sc->status = ST_OK; sc->max_iter = a.max_iter;
-      const double nb = sqrt(sc->bb);
-      const double nbe = nb > 0.0 ? nb : 1.0;             // ||f|| = 0: absolute residual (§8c A11)
-      sc->thresh = a.eps > 0.0 ? a.eps * nbe : -1.0;      // eps <= 0: fixed iteration count
-      int done = (a.max_iter <= 0) || (sc->thresh > 0.0 && !(sqrt(s1) > sc->thresh));
-      if (!isfinite(s1)) { sc->status = ST_EBREAKDOWN; done = 1; }
-      sc->done = done;
-      break;
-    }
-    case MODE_K1: {
-      sc->sigma = s0;
-      if (!(s0 > 0.0)) { sc->status = ST_EBREAKDOWN; sc->done = 1; }   // p.Ap <= 0
-      else sc->alpha = sc->rho / s0;
-      break;
-    }
-    case MODE_K2: {
-      const double rho_new = s0;
-      sc->beta = rho_new / sc->rho;
-      sc->rho = rho_new;
-      sc->rr = s1;
-      sc->iter += 1;
-      int done = (sc->iter >= sc->max_iter) || (sc->thresh > 0.0 && !(sqrt(s1) > sc->thresh));
-      if (!isfinite(s1)) { sc->status = ST_EBREAKDOWN; done = 1; }
-      sc->done = done;
-      break;
-    }
-    case MODE_TRUE: sc->rr_true = s1; break;
-    default: break;
-  }
-}
-
-__device__ void reduce_finalize(int mode, const KArgs& a, double v0, double v1) {
-  __shared__ double red[2 * (NTH / 32)];
-  __shared__ int is_last;
-  block_sum2(v0, v1, red);
-  const int tid = threadIdx.x + TX * threadIdx.y;
-  const unsigned nb = gridDim.x * gridDim.y * gridDim.z;
-  const unsigned bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-  if (tid == 0) {
-    a.partials[2 * bid] = v0;
-    a.partials[2 * bid + 1] = v1;
-    __threadfence();
-    const unsigned prev = atomicAdd(&a.sc->counter, 1u);
-    is_last = (prev == nb - 1);
-  }
-  __syncthreads();
-  if (!is_last) return;
-  __threadfence();
-  double s0 = 0.0, s1 = 0.0;
-  for (unsigned b = tid; b < nb; b += NTH) { s0 += __ldcg(a.partials + 2 * b); s1 += __ldcg(a.partials + 2 * b + 1); }
-  block_sum2(s0, s1, red);
-  if (tid == 0) {
-    finalize(mode, a, s0, s1);
-    a.sc->counter = 0;
-  }
-}
 
 // ============================================================================================
 // Constant-coefficient path (beta constant, all faces Dirichlet): C1, C2, C4 and the patch test.
@@ -186,7 +103,7 @@ __global__ void __launch_bounds__(NTH, 2) k_jcg_const(const LevelGeom g, const C
   double part[CRY], q1p[CRY], pp[CRY];
 #pragma unroll
   for (int j = 0; j < CRY; ++j) { part[j] = q1p[j] = pp[j] = 0.0; }
-  double acc0 = 0.0, acc1 = 0.0;
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
 
   load_halo(z0 - 1);
   const int nsteps = z1 - z0 + 2;
@@ -235,6 +152,7 @@ __global__ void __launch_bounds__(NTH, 2) k_jcg_const(const LevelGeom g, const C
           a.o0[off] = xn;
           a.o1[off] = rn;
         } else if (MODE == MODE_INIT) {
+          acc2 += ii0[j] * ii0[j];
           const double rn = ii0[j] - ap;
           const double zz = dinv * rn;
           acc0 += rn * zz;
@@ -252,7 +170,7 @@ __global__ void __launch_bounds__(NTH, 2) k_jcg_const(const LevelGeom g, const C
       pp[j] = cc;
     }
   }
-  if (MODE != MODE_APPLY) reduce_finalize(MODE, a, acc0, acc1);
+  if (MODE != MODE_APPLY) reduce_finalize(MODE, a, acc0, acc1, acc2);
 }
 
 // ============================================================================================
@@ -390,7 +308,7 @@ __global__ void __launch_bounds__(NTH, 2) k_jcg_elem(const LevelGeom g, const El
     return es.kappa[0] * sb + rob;
   };
 
-  double acc0 = 0.0, acc1 = 0.0;
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
   load_halo(z0 - 1);
   load_beta(z0 - 2);
   // prologue: element plane z0-2 into its ring slot
@@ -513,6 +431,7 @@ __global__ void __launch_bounds__(NTH, 2) k_jcg_elem(const LevelGeom g, const El
         a.o0[off] = xn;
         a.o1[off] = rn;
       } else if (MODE == MODE_INIT) {
+        acc2 += ii0 * ii0;
         const double rn = ii0 - ap;
         const double zz = dinv * rn;
         acc0 += rn * zz;
@@ -526,7 +445,7 @@ __global__ void __launch_bounds__(NTH, 2) k_jcg_elem(const LevelGeom g, const El
       }
     }
   }
-  if (MODE != MODE_APPLY) reduce_finalize(MODE, a, acc0, acc1);
+  if (MODE != MODE_APPLY) reduce_finalize(MODE, a, acc0, acc1, acc2);
 }
 
 }  // namespace

@@ -1,0 +1,282 @@
+// kernels_jcg_tma.cu -- TMA-fed z-marching JCG kernels for the constant-coefficient stencil
+// (beta constant, all faces Dirichlet: C1, C2, C4). Same arithmetic and the
+// same device-side CG scalar recurrences as kernels_jcg.cu (Alg. 4 l.7-9).
+//
+// Data movement (B200-native): every z-plane of every input vector reaches shared memory through
+// ONE cp.async.bulk.tensor.3d per CTA (box 34 x 34 for halo-read vectors, 32 x 32 for interior
+// vectors), issued by one thread into an NS-deep ring of stages and completed on an mbarrier
+// (expect_tx). Out-of-bounds boxes are zero-filled by the TMA unit, which is exactly "p = 0 on
+// Dirichlet nodes" of the eliminated system, so the kernel has no boundary predication on loads.
+// Stage k holds halo plane zl and interior plane zl-1 (the plane whose A.p completes in that step).
+// The refill of a stage is issued one step after it was consumed, right after the per-plane
+// __syncthreads, so no separate "empty" barrier is needed.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include "ecmg_internal.cuh"
+#include "jcg_common.cuh"
+
+namespace ecmg {
+namespace {
+
+constexpr int RY = 4;             // rows per warp
+constexpr int TY = WARPS * RY;    // 32
+// The innermost TMA box start must be 16-byte aligned (x = -1 traps with an illegal instruction
+// on sm_100a, measured: tools/tma_probe3.cu), so the halo box starts at x = X0 - 2 and is 36 wide;
+// columns 0 and 35 are loaded but unused.
+constexpr int HX = TX + 4;        // 36 (x = X0-2 .. X0+33)
+constexpr int XO = 2;             // smem column of x = X0
+constexpr int HY = TY + 2;        // 34
+constexpr int HBYTES = HX * HY * 8;            // 9792
+constexpr int HSTRIDE = (HBYTES + 127) / 128 * 128;   // 9856
+constexpr int IBYTES = TX * TY * 8;            // 8192
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// loads of step t (halo plane z0-1+t, interior plane z0-2+t) into stage st
+template <bool kH1, int kNI, int SBYTES>
+__device__ __forceinline__ void issue_stage(unsigned char* smem, uint64_t* full, int st, int t, int z0, int X0, int Y0,
+                                            uint32_t tx_bytes, bool first, const CUtensorMap* pH0, const CUtensorMap* pH1,
+                                            const CUtensorMap* pI0, const CUtensorMap* pI1) {
+  unsigned char* base = smem + st * SBYTES;
+  mbar_expect_tx(&full[st], tx_bytes);
+  const int zh = z0 - 1 + t;
+  tma_load_3d(base, pH0, X0 - XO, Y0 - 1, zh, &full[st]);
+  if (kH1 && !first) tma_load_3d(base + HSTRIDE, pH1, X0 - XO, Y0 - 1, zh, &full[st]);
+  if (kNI >= 1) tma_load_3d(base + HSTRIDE * (kH1 ? 2 : 1), pI0, X0, Y0, zh - 1, &full[st]);
+  if (kNI >= 2) tma_load_3d(base + HSTRIDE * (kH1 ? 2 : 1) + IBYTES, pI1, X0, Y0, zh - 1, &full[st]);
+}
+
+template <int MODE, int NS>
+__global__ void __launch_bounds__(NTH, 2)
+    k_jcg_const_tma(const LevelGeom g, const ConstStencil cs, const KArgs a, const __grid_constant__ CUtensorMap mH0,
+                    const __grid_constant__ CUtensorMap mH1, const __grid_constant__ CUtensorMap mI0,
+                    const __grid_constant__ CUtensorMap mI1) {
+  constexpr bool kH1 = (MODE == MODE_K1);
+  constexpr int kNI = (MODE == MODE_K2) ? 2 : ((MODE == MODE_INIT || MODE == MODE_TRUE) ? 1 : 0);
+  constexpr int SBYTES = HSTRIDE * (kH1 ? 2 : 1) + IBYTES * kNI;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full[NS];
+  // TMA destinations must be 128-byte aligned in the shared window: align the stage base explicitly
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  JcgScalars* sc = a.sc;
+  if (MODE == MODE_K1 || MODE == MODE_K2) {
+    if (*(volatile int*)&sc->done) return;
+  }
+  const int lane = threadIdx.x, w = threadIdx.y, tid = lane + TX * w;
+  const int nfx = g.nf[0], nfy = g.nf[1];
+  const long long P = g.P, S = g.S;
+  const int X0 = blockIdx.x * TX, Y0 = blockIdx.y * TY;
+  const int z0 = blockIdx.z * a.zc;
+  const int z1 = min(z0 + a.zc, g.nf[2]);
+  const int x = X0 + lane, yb = Y0 + RY * w;
+  const int nsteps = z1 - z0 + 2;
+
+  double bcg = 0.0, alpha = 0.0;
+  bool first = false;
+  if (MODE == MODE_K1) { bcg = sc->beta; first = (sc->iter == 0); }
+  if (MODE == MODE_K2) alpha = sc->alpha;
+  const double dinv = cs.dinv;
+  const uint32_t tx_bytes = HBYTES + ((kH1 && !first) ? HBYTES : 0) + IBYTES * kNI;
+
+  auto stage_ptr = [&](int st) { return smem + st * SBYTES; };
+  // descriptor addresses taken directly from the __grid_constant__ parameters (param space)
+  const CUtensorMap* pH0 = &mH0;
+  const CUtensorMap* pH1 = &mH1;
+  const CUtensorMap* pI0 = &mI0;
+  const CUtensorMap* pI1 = &mI1;
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) mbar_init(&full[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int t = 0; t < NS - 1 && t < nsteps; ++t)
+      issue_stage<kH1, kNI, SBYTES>(smem, full, t % NS, t, z0, X0, Y0, tx_bytes, first, pH0, pH1, pI0, pI1);
+  }
+
+  // halo ring slot of this thread (transform in place, K1 only): rows y = Y0-1, Y0+32 (x = X0-1 ..
+  // X0+32, smem columns 1..34) and columns x = X0-1, X0+32 (smem columns 1, 34) of rows Y0..Y0+31
+  constexpr int RW = TX + 2;   // 34
+  int rhx = -1, rhy = -1;
+  if (tid < 2 * RW) { rhx = 1 + tid % RW; rhy = (tid < RW) ? 0 : HY - 1; }
+  else if (tid < 2 * RW + 2 * TY) { const int t = tid - 2 * RW; rhx = (t < TY) ? 1 : RW; rhy = 1 + (t % TY); }
+
+  bool own_ok[RY];
+  long long own_off[RY];
+#pragma unroll
+  for (int j = 0; j < RY; ++j) {
+    own_ok[j] = (x < nfx) && (yb + j < nfy);
+    own_off[j] = own_ok[j] ? (long long)(yb + j) * P + x : 0;
+  }
+  double part[RY], q1p[RY], pp[RY];
+#pragma unroll
+  for (int j = 0; j < RY; ++j) { part[j] = q1p[j] = pp[j] = 0.0; }
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+
+  for (int s = 0; s < nsteps; ++s) {
+    const int zl = z0 - 1 + s;
+    const int st = s % NS;
+    if (s > 0) __syncthreads();   // every thread is done with step s-1: its stage may be refilled
+    if (tid == 0 && s + NS - 1 < nsteps) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes before async-proxy writes
+      const int t = s + NS - 1;                                      // into stage (s-1) % NS
+      issue_stage<kH1, kNI, SBYTES>(smem, full, t % NS, t, z0, X0, Y0, tx_bytes, first, pH0, pH1, pI0, pI1);
+    }
+    mbar_wait(&full[st], (uint32_t)((s / NS) & 1));
+    double* H = reinterpret_cast<double*>(stage_ptr(st));
+    if (MODE == MODE_K1) {
+      const double* H1 = reinterpret_cast<const double*>(stage_ptr(st) + HSTRIDE);
+#pragma unroll
+      for (int j = 0; j < RY; ++j) {
+        const int o = (1 + RY * w + j) * HX + XO + lane;
+        H[o] = first ? dinv * H[o] : dinv * H[o] + bcg * H1[o];
+      }
+      if (rhx >= 0) {
+        const int o = rhy * HX + rhx;
+        H[o] = first ? dinv * H[o] : dinv * H[o] + bcg * H1[o];
+      }
+      __syncthreads();
+    }
+    double col[RY + 2][3];
+#pragma unroll
+    for (int r = 0; r < RY + 2; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) col[r][c] = H[(RY * w + r) * HX + XO - 1 + lane + c];
+    const double* I0 = reinterpret_cast<const double*>(stage_ptr(st) + HSTRIDE * (kH1 ? 2 : 1));
+    const double* I1 = I0 + TX * TY;
+    const int z = zl - 1;
+#pragma unroll
+    for (int j = 0; j < RY; ++j) {
+      const double cc = col[j + 1][1];
+      const double ax = col[j + 1][0] + col[j + 1][2];
+      const double ay = col[j][1] + col[j + 2][1];
+      const double dd = (col[j][0] + col[j][2]) + (col[j + 2][0] + col[j + 2][2]);
+      const double q0 = cs.c0[0] * cc + cs.cx[0] * ax + cs.cy[0] * ay + cs.cd[0] * dd;
+      const double q1 = cs.c0[1] * cc + cs.cx[1] * ax + cs.cy[1] * ay + cs.cd[1] * dd;
+      if (s >= 2 && own_ok[j]) {
+        const double ap = part[j] + q1;
+        const long long off = (long long)z * S + own_off[j];
+        const int io = (RY * w + j) * TX + lane;
+        if (MODE == MODE_K1) {
+          acc0 += pp[j] * ap;
+          a.o0[off] = pp[j];
+        } else if (MODE == MODE_K2) {
+          const double xn = I0[io] + alpha * pp[j];
+          const double rn = I1[io] - alpha * ap;
+          const double zz = dinv * rn;
+          acc0 += rn * zz;
+          acc1 += rn * rn;
+          a.o0[off] = xn;
+          a.o1[off] = rn;
+        } else if (MODE == MODE_INIT) {
+          acc2 += I0[io] * I0[io];
+          const double rn = I0[io] - ap;
+          const double zz = dinv * rn;
+          acc0 += rn * zz;
+          acc1 += rn * rn;
+          a.o0[off] = rn;
+        } else if (MODE == MODE_TRUE) {
+          const double rn = I0[io] - ap;
+          acc1 += rn * rn;
+        } else {
+          a.o0[off] = ap;
+        }
+      }
+      part[j] = q1p[j] + q0;
+      q1p[j] = q1;
+      pp[j] = cc;
+    }
+  }
+  if (MODE != MODE_APPLY) reduce_finalize(MODE, a, acc0, acc1, acc2);
+}
+
+template <int MODE, int NS>
+cudaError_t launch_tma_mode(dim3 grid, dim3 block, const LevelGeom& g, const ConstStencil& cs, const KArgs& a,
+                            const CUtensorMap* maps, cudaStream_t st) {
+  constexpr bool kH1 = (MODE == MODE_K1);
+  constexpr int kNI = (MODE == MODE_K2) ? 2 : ((MODE == MODE_INIT || MODE == MODE_TRUE) ? 1 : 0);
+  constexpr int SBYTES = HSTRIDE * (kH1 ? 2 : 1) + IBYTES * kNI;
+  constexpr int SMEM = SBYTES * NS + 128;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_jcg_const_tma<MODE, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  count_launch();
+  k_jcg_const_tma<MODE, NS><<<grid, block, SMEM, st>>>(g, cs, a, maps[0], maps[1], maps[2], maps[3]);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// maps[0..3] = H0, H1, I0, I1 tensor maps (unused entries may be any valid map)
+cudaError_t launch_jcg_const_tma(int mode, const LevelGeom& g, const ConstStencil& cs, const KArgs& a,
+                                 const CUtensorMap* maps, cudaStream_t st) {
+  dim3 block(TX, WARPS);
+  dim3 grid((g.nf[0] + TX - 1) / TX, (g.nf[1] + TY - 1) / TY, (g.nf[2] + a.zc - 1) / a.zc);
+  switch (mode) {
+    case MODE_K1: return launch_tma_mode<MODE_K1, 4>(grid, block, g, cs, a, maps, st);
+    case MODE_K2: return launch_tma_mode<MODE_K2, 3>(grid, block, g, cs, a, maps, st);
+    case MODE_INIT: return launch_tma_mode<MODE_INIT, 4>(grid, block, g, cs, a, maps, st);
+    case MODE_TRUE: return launch_tma_mode<MODE_TRUE, 4>(grid, block, g, cs, a, maps, st);
+    case MODE_APPLY: return launch_tma_mode<MODE_APPLY, 4>(grid, block, g, cs, a, maps, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// Tensor map of a free-box work vector: dims (nf_x, nf_y, nf_z), strides (P, S) doubles,
+// box (bx, by, 1), zero fill out of bounds.
+int make_vec_tensor_map(CUtensorMap* map, const double* base, const LevelGeom& g, int bx, int by) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn) {
+      cudaGetLastError();
+      return -1;
+    }
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  cuuint64_t dims[3] = {(cuuint64_t)g.nf[0], (cuuint64_t)g.nf[1], (cuuint64_t)g.nf[2]};
+  cuuint64_t strides[2] = {(cuuint64_t)g.P * 8, (cuuint64_t)g.S * 8};
+  cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -1;
+}
+
+int tma_halo_box_x() { return HX; }
+int tma_halo_box_y() { return HY; }
+int tma_int_box_x() { return TX; }
+int tma_int_box_y() { return TY; }
+
+}  // namespace ecmg

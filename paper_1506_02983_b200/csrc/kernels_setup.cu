@@ -2,6 +2,7 @@
 // load vector by 2x2x2 Gauss quadrature (reading §8c A2), Robin face load by 2x2 Gauss (§8c A4),
 // symmetric Dirichlet elimination (lifting, §8c A5), ||f_h||_2, and the gather / scatter between
 // caller-visible nodal vectors and the free-box work vectors.
+#include <algorithm>
 #include "ecmg_internal.cuh"
 #include "problems.cuh"
 
@@ -25,172 +26,208 @@ __global__ void k_beta(const LevelGeom g, const Problem pb, double* __restrict__
 }
 
 // ---- right-hand side ---------------------------------------------------------------------------
-// CTA = 8 x 8 x 4 free nodes. Phase 1: the element load vectors F_e[a] = sum_q f(x_q) N_a(xi_q) V/8
-// of the 9 x 9 x 5 elements touching the tile go to shared memory (each f evaluation done once
-// per tile). Phase 2: each node gathers its 8 element entries, adds the Robin face load
-// G = sum_q g_R(x_q) N_c h1 h2 / 4 and subtracts A_fD g_D (element-wise couplings beta_e kappa
-// plus Robin face mass to Dirichlet neighbours), giving b_f = F_f + G_f - A_fD g_D.
-constexpr int RX = 8, RY = 8, RZ = 4, RNTH = RX * RY * RZ;
-constexpr int REX = RX + 1, REY = RY + 1, REZ = RZ + 1, RNE = REX * REY * REZ;
+// b_f = F_f + G_f - A_fD g_D (§8c A2/A4/A5) in up to three passes:
+//  (1) volume load F by 2x2x2 Gauss. Separable f = A g_x(x) g_y(y) g_z(z) (C1, C2, C5, P1, P2, the
+//      patch tests): F_i = A L_x(i_x) L_y(i_y) L_z(i_z), with the 1D Gauss loads
+//      L_d(i) = sum_{e in {i-1,i}} (h_d/2) sum_{q=+-} g_d(x_q) N(xi_q) (the 3D rule factorises exactly).
+//      Otherwise (C3, C4, P3): z-marching CTAs evaluate f once per Gauss point of each element plane
+//      (shared memory), form the element load vectors, and every node gathers its 8 entries.
+//  (2) boundary shell of the free box: Robin face load G (2x2 Gauss) and the lifting -A_fD g_D.
+// ||b||^2 is accumulated by the JCG init pass, which reads b anyway.
+constexpr int VX = 32, VY = 8, VNTH = VX * VY;
+constexpr int VEX = VX + 1, VEY = VY + 1, VNE = VEX * VEY;     // 33 x 9 elements per plane
+constexpr int VSMEM = (VNE * 8 + 2 * VNE * 8) * (int)sizeof(double);
 
-__device__ __forceinline__ double beta_at(const LevelGeom& g, const double* beta, double beta_const, int gex, int gey,
-                                          int gez) {
-  if (gex < 0 || gex >= g.n[0] || gey < 0 || gey >= g.n[1] || gez < 0 || gez >= g.n[2]) return 0.0;
-  if (!beta) return beta_const;
-  return beta[(long long)(gez + 2) * g.BS + (long long)(gey + 2) * g.BP + (gex + 2)];
+// separable factor g_d and amplitude: returns false if f is not a product of 1D functions
+__host__ __device__ inline bool prob_separable(int id) {
+  switch (id) {
+    case 1: case 2: case 5: case 11: case 12: case 21: case 22: case 23: case 24: return true;
+    default: return false;
+  }
+}
+__device__ inline double sep_amp(const Problem& P) {
+  const double pi = kPi();
+  switch (P.id) {
+    case 1: return 3.0 * pi * pi;
+    case 2: return -3.0;
+    case 5: return P.params[47];
+    case 11: return 0.75 * pi * pi;
+    case 12: return -(1.0 - 2.5 * pi * pi);
+    case 24: return 1.0;
+    default: return 0.0;   // patch tests: f = 0
+  }
+}
+__device__ inline double sep_g(const Problem& P, int d, double t) {
+  const double pi = kPi();
+  switch (P.id) {
+    case 1: return sin(pi * t);
+    case 2: return exp(t);
+    case 5: { const double c = P.params[43 + d], s = P.params[46]; return exp(-(t - c) * (t - c) / (2.0 * s * s)); }
+    case 11: return sin(0.5 * pi * t);
+    case 12: return d == 0 ? sin(1.5 * pi * t) : (d == 1 ? sin(0.5 * pi * t) : exp(t));
+    default: return 1.0;
+  }
 }
 
-__global__ void __launch_bounds__(RNTH) k_rhs(const LevelGeom g, const Problem pb, const ElemStencil es, double beta_const,
-                                              const double* __restrict__ beta, double* __restrict__ b, double* partials,
-                                              JcgScalars* sc) {
-  __shared__ double Fe[RNE][8];
-  __shared__ double red[2 * (RNTH / 32)];
-  __shared__ int is_last;
-  const int tid = threadIdx.x;
-  const int X0 = blockIdx.x * RX, Y0 = blockIdx.y * RY, Z0 = blockIdx.z * RZ;
+// L_d(i), i = 0..n_d, for d = 0, 1, 2 stored at L[d * (nmax + 1) + i]
+__global__ void k_load1d(const LevelGeom g, const Problem pb, double* __restrict__ L, int stride) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x, d = blockIdx.y;
+  if (i > g.n[d]) return;
+  double v = 0.0;
+  for (int e = i - 1; e <= i; ++e) {
+    if (e < 0 || e >= g.n[d]) continue;
+    const double side = (e == i - 1) ? 1.0 : -1.0;   // node is local 1 (xi = +1) of e = i-1, local 0 of e = i
+    for (int q = 0; q < 2; ++q) {
+      const double xi = q ? kGauss : -kGauss;
+      v += sep_g(pb, d, g.lo[d] + (e + (1.0 + xi) / 2.0) * g.h[d]) * ((1.0 + side * xi) / 2.0) * (g.h[d] / 2.0);
+    }
+  }
+  L[(long long)d * stride + i] = v;
+}
+
+__global__ void k_rhs_sep(const LevelGeom g, const Problem pb, const double* __restrict__ L, int stride,
+                          double* __restrict__ b) {
+  const int fx = blockIdx.x * blockDim.x + threadIdx.x, fy = blockIdx.y, fz = blockIdx.z;
+  if (fx >= g.nf[0]) return;
+  const double A = sep_amp(pb);
+  const double v = A * __ldg(L + g.flo[0] + fx) * __ldg(L + stride + g.flo[1] + fy) * __ldg(L + 2 * stride + g.flo[2] + fz);
+  b[(long long)fz * g.S + (long long)fy * g.P + fx] = v;
+}
+
+__global__ void __launch_bounds__(VNTH) k_rhs_vol(const LevelGeom g, const Problem pb, double* __restrict__ b, int zc) {
+  extern __shared__ double vs[];
+  double* fq = vs;              // [VNE][8] f at the Gauss points of one element plane
+  double* Fe = vs + VNE * 8;    // [2][VNE][8] element load vectors, ring of two element planes
+  const int lane = threadIdx.x, w = threadIdx.y, tid = lane + VX * w;
+  const int X0 = blockIdx.x * VX, Y0 = blockIdx.y * VY;
+  const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, g.nf[2]);
   const double detJ = g.h[0] * g.h[1] * g.h[2] / 8.0;
-
-  // phase 1: element loads
-  for (int e = tid; e < RNE; e += RNTH) {
-    const int lx = e % REX, ly = (e / REX) % REY, lz = e / (REX * REY);
-    const int gex = g.flo[0] + X0 - 1 + lx, gey = g.flo[1] + Y0 - 1 + ly, gez = g.flo[2] + Z0 - 1 + lz;
-    double F[8];
+  const double wA = (1.0 + kGauss) / 2.0, wB = (1.0 - kGauss) / 2.0;   // N at the near / far Gauss point
+  for (int fez = z0 - 1; fez < z1; ++fez) {
+    // (a) f at the 8 Gauss points of every element of the plane (33 x 9 x 8 evaluations)
+    const int gez = g.flo[2] + fez;
+    for (int t = tid; t < VNE * 8; t += VNTH) {
+      const int e = t >> 3, q = t & 7;
+      const int gex = g.flo[0] + X0 - 1 + e % VEX, gey = g.flo[1] + Y0 - 1 + e / VEX;
+      double v = 0.0;
+      if (gex >= 0 && gex < g.n[0] && gey >= 0 && gey < g.n[1] && gez >= 0 && gez < g.n[2]) {
+        const double xi = (q & 1) ? kGauss : -kGauss, eta = (q & 2) ? kGauss : -kGauss, ze = (q & 4) ? kGauss : -kGauss;
+        v = prob_f(pb, g.lo[0] + (gex + (1.0 + xi) / 2.0) * g.h[0], g.lo[1] + (gey + (1.0 + eta) / 2.0) * g.h[1],
+                   g.lo[2] + (gez + (1.0 + ze) / 2.0) * g.h[2]);
+      }
+      fq[t] = v;
+    }
+    __syncthreads();
+    // (b) element load vectors F_e[a] = detJ sum_q f_q N_a(q): a 2x2x2 tensor transform
+    double* Fp = Fe + (fez & 1) * VNE * 8;
+    for (int e = tid; e < VNE; e += VNTH) {
+      double t1[8], t2[8];
+      const double* f = fq + e * 8;
 #pragma unroll
-    for (int a = 0; a < 8; ++a) F[a] = 0.0;
-    if (gex >= 0 && gex < g.n[0] && gey >= 0 && gey < g.n[1] && gez >= 0 && gez < g.n[2]) {
+      for (int i = 0; i < 8; ++i) {   // along x: node bit 0 vs Gauss bit 0
+        const int qb = i & ~1;
+        t1[i] = (i & 1) ? (wB * f[qb] + wA * f[qb | 1]) : (wA * f[qb] + wB * f[qb | 1]);
+      }
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const double xi[3] = {(q & 1) ? kGauss : -kGauss, (q & 2) ? kGauss : -kGauss, (q & 4) ? kGauss : -kGauss};
-        const double fq = prob_f(pb, g.lo[0] + (gex + (1.0 + xi[0]) / 2.0) * g.h[0],
-                                 g.lo[1] + (gey + (1.0 + xi[1]) / 2.0) * g.h[1],
-                                 g.lo[2] + (gez + (1.0 + xi[2]) / 2.0) * g.h[2]);
+      for (int i = 0; i < 8; ++i) {   // along y
+        const int qb = i & ~2;
+        t2[i] = (i & 2) ? (wB * t1[qb] + wA * t1[qb | 2]) : (wA * t1[qb] + wB * t1[qb | 2]);
+      }
 #pragma unroll
-        for (int a = 0; a < 8; ++a) {
-          const double N = ((1.0 + ((a & 1) ? xi[0] : -xi[0])) / 2.0) * ((1.0 + ((a & 2) ? xi[1] : -xi[1])) / 2.0) *
-                           ((1.0 + ((a & 4) ? xi[2] : -xi[2])) / 2.0);
-          F[a] += fq * N * detJ;
-        }
+      for (int i = 0; i < 8; ++i) {   // along z
+        const int qb = i & ~4;
+        Fp[e * 8 + i] = detJ * ((i & 4) ? (wB * t2[qb] + wA * t2[qb | 4]) : (wA * t2[qb] + wB * t2[qb | 4]));
       }
     }
+    __syncthreads();
+    // (c) node plane fz = fez gathers from element planes fez-1 and fez
+    const int fz = fez, fx = X0 + lane, fy = Y0 + w;
+    if (fz >= z0 && fx < g.nf[0] && fy < g.nf[1]) {
+      double v = 0.0;
 #pragma unroll
-    for (int a = 0; a < 8; ++a) Fe[e][a] = F[a];
-  }
-  __syncthreads();
-
-  // phase 2: nodes
-  const int lx = tid % RX, ly = (tid / RX) % RY, lz = tid / (RX * RY);
-  const int fx = X0 + lx, fy = Y0 + ly, fz = Z0 + lz;
-  double bsq = 0.0;
-  if (fx < g.nf[0] && fy < g.nf[1] && fz < g.nf[2]) {
-    const int gx = g.flo[0] + fx, gy = g.flo[1] + fy, gz = g.flo[2] + fz;
-    const int gi[3] = {gx, gy, gz};
-    double v = 0.0;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const int ex = e & 1, ey = (e >> 1) & 1, ez = (e >> 2) & 1;   // element = node - 1 + e_d
-      const int a = (1 - ex) | ((1 - ey) << 1) | ((1 - ez) << 2);    // node's local index in it
-      v += Fe[(lx + ex) + REX * ((ly + ey) + REY * (lz + ez))][a];
-    }
-    // Robin faces: load G and face-mass coupling
-    for (int F = 0; F < 6; ++F) {
-      if (pb.face[F] != FACE_ROBIN) continue;
-      const int d = F >> 1, side = F & 1;
-      if (gi[d] != (side ? g.n[d] : 0)) continue;
-      const int d1 = (d == 0) ? 1 : 0, d2 = (d == 2) ? 1 : 2;
-      const double hh = g.h[d1] * g.h[d2] / 4.0;
-      for (int e2 = -1; e2 <= 0; ++e2)
-        for (int e1 = -1; e1 <= 0; ++e1) {
-          const int f1 = gi[d1] + e1, f2 = gi[d2] + e2;   // face element lower corner
-          if (f1 < 0 || f1 >= g.n[d1] || f2 < 0 || f2 >= g.n[d2]) continue;
-          const int c1 = -e1, c2 = -e2;                  // node's local face index
-          for (int q = 0; q < 4; ++q) {
-            const double xi1 = (q & 1) ? kGauss : -kGauss, xi2 = (q & 2) ? kGauss : -kGauss;
-            double xq[3];
-            xq[d] = g.lo[d] + gi[d] * g.h[d];
-            xq[d1] = g.lo[d1] + (f1 + (1.0 + xi1) / 2.0) * g.h[d1];
-            xq[d2] = g.lo[d2] + (f2 + (1.0 + xi2) / 2.0) * g.h[d2];
-            const double N = ((1.0 + (c1 ? xi1 : -xi1)) / 2.0) * ((1.0 + (c2 ? xi2 : -xi2)) / 2.0);
-            v += prob_gR(pb, F, xq[0], xq[1], xq[2]) * N * hh;
-          }
-        }
-    }
-    // lifting: subtract couplings to Dirichlet neighbours (nodes outside the free box)
-    const bool near = (fx == 0 && g.flo[0] == 1) || (fx == g.nf[0] - 1 && g.flo[0] + g.nf[0] == g.n[0]) ||
-                      (fy == 0 && g.flo[1] == 1) || (fy == g.nf[1] - 1 && g.flo[1] + g.nf[1] == g.n[1]) ||
-                      (fz == 0 && g.flo[2] == 1) || (fz == g.nf[2] - 1 && g.flo[2] + g.nf[2] == g.n[2]);
-    if (near) {
-      double sub = 0.0;
       for (int e = 0; e < 8; ++e) {
-        const int ex = e & 1, ey = (e >> 1) & 1, ez = (e >> 2) & 1;
-        const double be = beta_at(g, beta, beta_const, gx - 1 + ex, gy - 1 + ey, gz - 1 + ez);
-        if (be == 0.0) continue;
-        for (int bn = 0; bn < 8; ++bn) {
-          const int bx = bn & 1, by = (bn >> 1) & 1, bz = (bn >> 2) & 1;
-          const int jx = gx - 1 + ex + bx, jy = gy - 1 + ey + by, jz = gz - 1 + ez + bz;
-          const bool jfree = jx >= g.flo[0] && jx < g.flo[0] + g.nf[0] && jy >= g.flo[1] && jy < g.flo[1] + g.nf[1] &&
-                             jz >= g.flo[2] && jz < g.flo[2] + g.nf[2];
-          if (jfree) continue;
-          const int pat = ((ex + bx) != 1 ? 1 : 0) | ((ey + by) != 1 ? 2 : 0) | ((ez + bz) != 1 ? 4 : 0);
-          const double gD = prob_gD(pb, g.lo[0] + jx * g.h[0], g.lo[1] + jy * g.h[1], g.lo[2] + jz * g.h[2]);
-          sub += be * es.kappa[pat] * gD;
-        }
-        // Robin face mass coupling with Dirichlet nodes on the same face
-        for (int F = 0; F < 6; ++F) {
-          if (es.robin[F] == 0.0) continue;
-          const int d = F >> 1, side = F & 1;
-          if (gi[d] != (side ? g.n[d] : 0)) continue;
-          const int e3[3] = {ex, ey, ez};
-          for (int bn = 0; bn < 8; ++bn) {
-            const int b3[3] = {bn & 1, (bn >> 1) & 1, (bn >> 2) & 1};
-            if (b3[d] != 1 - e3[d]) continue;
-            const int jx = gx - 1 + ex + b3[0], jy = gy - 1 + ey + b3[1], jz = gz - 1 + ez + b3[2];
-            const bool jfree = jx >= g.flo[0] && jx < g.flo[0] + g.nf[0] && jy >= g.flo[1] && jy < g.flo[1] + g.nf[1] &&
-                               jz >= g.flo[2] && jz < g.flo[2] + g.nf[2];
-            if (jfree) continue;
-            int nd = 0;
-            for (int t = 0; t < 3; ++t) if (t != d && b3[t] != 1 - e3[t]) ++nd;
-            const double m2 = nd == 0 ? (1.0 / 9.0) : (nd == 1 ? (1.0 / 18.0) : (1.0 / 36.0));
-            const double gD = prob_gD(pb, g.lo[0] + jx * g.h[0], g.lo[1] + jy * g.h[1], g.lo[2] + jz * g.h[2]);
-            sub += es.robin[F] * m2 * gD;
-          }
+        const int ex = e & 1, ey = (e >> 1) & 1, ez = (e >> 2) & 1;   // element = node - 1 + e_d
+        const int a = (1 - ex) | ((1 - ey) << 1) | ((1 - ez) << 2);
+        v += Fe[((fz - 1 + ez) & 1) * VNE * 8 + ((lane + ex) + VEX * (w + ey)) * 8 + a];
+      }
+      b[(long long)fz * g.S + (long long)fy * g.P + fx] = v;
+    }
+  }
+}
+
+// Boundary shell of the free box: Robin load G and lifting -A_fD g_D, added to b.
+// blockIdx.z = face of the free box (axis d = face/2, side = face&1); a node is handled by the
+// lowest-numbered free-box face it lies on.
+__global__ void k_rhs_shell(const LevelGeom g, const Problem pb, const ElemStencil es, double beta_const,
+                            const double* __restrict__ beta, double* __restrict__ b) {
+  const int face = blockIdx.z, d = face >> 1, side = face & 1;
+  const int d1 = (d == 0) ? 1 : 0, d2 = (d == 2) ? 1 : 2;
+  const int i1 = blockIdx.x * blockDim.x + threadIdx.x, i2 = blockIdx.y;
+  if (i1 >= g.nf[d1] || i2 >= g.nf[d2]) return;
+  int f[3];
+  f[d] = side ? g.nf[d] - 1 : 0;
+  f[d1] = i1;
+  f[d2] = i2;
+  for (int fc = 0; fc < face; ++fc) {   // owned by a lower face?
+    const int dd = fc >> 1;
+    if (f[dd] == ((fc & 1) ? g.nf[dd] - 1 : 0)) return;
+  }
+  const int gi[3] = {g.flo[0] + f[0], g.flo[1] + f[1], g.flo[2] + f[2]};
+  const int gx = gi[0], gy = gi[1], gz = gi[2];
+  double v = 0.0;
+  // Robin face load G = sum_q g_R(x_q) N_c h1 h2 / 4 on every Robin face through the node
+  for (int F = 0; F < 6; ++F) {
+    if (pb.face[F] != FACE_ROBIN) continue;
+    const int dF = F >> 1;
+    if (gi[dF] != ((F & 1) ? g.n[dF] : 0)) continue;
+    const int e1d = (dF == 0) ? 1 : 0, e2d = (dF == 2) ? 1 : 2;
+    const double hh = g.h[e1d] * g.h[e2d] / 4.0;
+    for (int e2 = -1; e2 <= 0; ++e2)
+      for (int e1 = -1; e1 <= 0; ++e1) {
+        const int f1 = gi[e1d] + e1, f2 = gi[e2d] + e2;
+        if (f1 < 0 || f1 >= g.n[e1d] || f2 < 0 || f2 >= g.n[e2d]) continue;
+        for (int q = 0; q < 4; ++q) {
+          const double xi1 = (q & 1) ? kGauss : -kGauss, xi2 = (q & 2) ? kGauss : -kGauss;
+          double xq[3];
+          xq[dF] = g.lo[dF] + gi[dF] * g.h[dF];
+          xq[e1d] = g.lo[e1d] + (f1 + (1.0 + xi1) / 2.0) * g.h[e1d];
+          xq[e2d] = g.lo[e2d] + (f2 + (1.0 + xi2) / 2.0) * g.h[e2d];
+          const double N = ((1.0 + (e1 ? xi1 : -xi1)) / 2.0) * ((1.0 + (e2 ? xi2 : -xi2)) / 2.0);
+          v += prob_gR(pb, F, xq[0], xq[1], xq[2]) * N * hh;
         }
       }
-      v -= sub;
+  }
+  // lifting: couplings to Dirichlet neighbours (domain nodes outside the free box)
+  double sub = 0.0;
+  for (int e = 0; e < 8; ++e) {
+    const int ex = e & 1, ey = (e >> 1) & 1, ez = (e >> 2) & 1;
+    const int ge[3] = {gx - 1 + ex, gy - 1 + ey, gz - 1 + ez};
+    if (ge[0] < 0 || ge[0] >= g.n[0] || ge[1] < 0 || ge[1] >= g.n[1] || ge[2] < 0 || ge[2] >= g.n[2]) continue;
+    const double be = beta ? beta[(long long)(ge[2] + 2) * g.BS + (long long)(ge[1] + 2) * g.BP + (ge[0] + 2)] : beta_const;
+    for (int bn = 0; bn < 8; ++bn) {
+      const int bx = bn & 1, by = (bn >> 1) & 1, bz = (bn >> 2) & 1;
+      const int jx = ge[0] + bx, jy = ge[1] + by, jz = ge[2] + bz;
+      const bool jfree = jx >= g.flo[0] && jx < g.flo[0] + g.nf[0] && jy >= g.flo[1] && jy < g.flo[1] + g.nf[1] &&
+                         jz >= g.flo[2] && jz < g.flo[2] + g.nf[2];
+      if (jfree) continue;
+      const double gD = prob_gD(pb, g.lo[0] + jx * g.h[0], g.lo[1] + jy * g.h[1], g.lo[2] + jz * g.h[2]);
+      const int pat = ((ex + bx) != 1 ? 1 : 0) | ((ey + by) != 1 ? 2 : 0) | ((ez + bz) != 1 ? 4 : 0);
+      sub += be * es.kappa[pat] * gD;
+      // Robin face mass between this node and the Dirichlet node j on a common Robin face
+      for (int F = 0; F < 6; ++F) {
+        if (es.robin[F] == 0.0) continue;
+        const int dF = F >> 1;
+        const int plane = (F & 1) ? g.n[dF] : 0;
+        if (gi[dF] != plane) continue;
+        const int jj[3] = {jx, jy, jz};
+        if (jj[dF] != plane) continue;
+        int nd = 0;
+        for (int t = 0; t < 3; ++t) if (t != dF && jj[t] != gi[t]) ++nd;
+        sub += es.robin[F] * (nd == 0 ? (1.0 / 9.0) : (nd == 1 ? (1.0 / 18.0) : (1.0 / 36.0))) * gD;
+      }
     }
-    b[(long long)fz * g.S + (long long)fy * g.P + fx] = v;
-    bsq = v * v;
   }
-
-  // ||b||^2: deterministic block reduction + last-CTA sum in CTA order
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) bsq += __shfl_down_sync(0xffffffffu, bsq, o);
-  if ((tid & 31) == 0) red[tid >> 5] = bsq;
-  __syncthreads();
-  const unsigned nb = gridDim.x * gridDim.y * gridDim.z;
-  const unsigned bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-  if (tid == 0) {
-    double s = 0.0;
-    for (int w = 0; w < RNTH / 32; ++w) s += red[w];
-    partials[bid] = s;
-    __threadfence();
-    is_last = (atomicAdd(&sc->counter, 1u) == nb - 1);
-  }
-  __syncthreads();
-  if (!is_last) return;
-  __threadfence();
-  double s = 0.0;
-  for (unsigned k = tid; k < nb; k += RNTH) s += __ldcg(partials + k);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-  __syncthreads();
-  if ((tid & 31) == 0) red[tid >> 5] = s;
-  __syncthreads();
-  if (tid == 0) {
-    double t = 0.0;
-    for (int w = 0; w < RNTH / 32; ++w) t += red[w];
-    sc->bb = t;
-    sc->counter = 0;
-  }
+  if (v != 0.0 || sub != 0.0) b[(long long)f[2] * g.S + (long long)f[1] * g.P + f[0]] += v - sub;
 }
 
 // ---- gather / scatter between full nodal vectors and the free box ------------------------------
@@ -245,10 +282,32 @@ cudaError_t launch_beta(const LevelGeom& g, const Problem& pb, double* beta, cud
 }
 
 cudaError_t launch_rhs(const LevelGeom& g, const Problem& pb, const ElemStencil& es, double beta_const, const double* beta,
-                       double* b, double* partials, JcgScalars* sc, cudaStream_t st) {
-  dim3 grid((g.nf[0] + RX - 1) / RX, (g.nf[1] + RY - 1) / RY, (g.nf[2] + RZ - 1) / RZ);
+                       double* b, double* scratch, cudaStream_t st) {
+  if (prob_separable(pb.id)) {
+    const int nmax = std::max(g.n[0], std::max(g.n[1], g.n[2]));
+    const int stride = nmax + 1;
+    dim3 g1((stride + 127) / 128, 3);
+    count_launch();
+    k_load1d<<<g1, 128, 0, st>>>(g, pb, scratch, stride);
+    dim3 g2((g.nf[0] + 127) / 128, g.nf[1], g.nf[2]);
+    count_launch();
+    k_rhs_sep<<<g2, 128, 0, st>>>(g, pb, scratch, stride, b);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(k_rhs_vol, cudaFuncAttributeMaxDynamicSharedMemorySize, VSMEM);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    const int zc = 32;
+    dim3 grid((g.nf[0] + VX - 1) / VX, (g.nf[1] + VY - 1) / VY, (g.nf[2] + zc - 1) / zc);
+    count_launch();
+    k_rhs_vol<<<grid, dim3(VX, VY), VSMEM, st>>>(g, pb, b, zc);
+  }
+  const int m = std::max(g.nf[0], std::max(g.nf[1], g.nf[2]));
+  dim3 gs((m + 127) / 128, m, 6);
   count_launch();
-  k_rhs<<<grid, RNTH, 0, st>>>(g, pb, es, beta_const, beta, b, partials, sc);
+  k_rhs_shell<<<gs, 128, 0, st>>>(g, pb, es, beta_const, beta, b);
   return cudaGetLastError();
 }
 

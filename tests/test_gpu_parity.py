@@ -219,3 +219,27 @@ def test_edge_cases():
     bad = synth.c5_geometry(0)
     bad[7] = -1.0
     assert ecmg.set_coeffs(g.h, PROB["C5"], [0] * 6, bad) == ecmg.EINVAL   # beta <= 0
+
+
+@pytest.mark.parametrize("pid,level", [(o.C2, 4), (o.C4, 4), (o.C1, 2)])
+def test_tma_and_prefetch_kernels_bitwise(pid, level):
+    # the TMA-fed and the register-prefetch constant-stencil kernels do the same arithmetic in
+    # the same order (same tiles, same reduction tree): iterates must agree bitwise
+    n = (4 << level,) * 3
+    L = o.Level(n, pid)
+    fr = free_box(L)
+    x0 = np.where(fr, synth.random_nodal(14, n), 0.0)
+    outs = []
+    for kv in (1, 0):
+        g = Grid(4, level + 1, pid)
+        g.set_option(ecmg.OPT_KERNEL, kv)
+        u = dev(x0)
+        st, s = g.solve_level(level, 0.0, 20, u)
+        assert st == 0
+        outs.append(host(u))
+        q = g.new_vec(level)
+        g.apply_operator(level, dev(x0), q)
+        outs.append(host(q))
+    assert np.array_equal(outs[0], outs[2]) and np.array_equal(outs[1], outs[3])
+    xo, _ = L.jcg(x0, 0.0, 20)
+    assert rel(outs[0][fr], xo[fr]) <= 1e-12
