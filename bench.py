@@ -234,6 +234,16 @@ def main():
     grid.solve_level(fine, 0.0, args.fixed_iters, xb)
     ms_p, it_p, _ = grid.last_jcg_timing()
     grid.set_option(ecmg.OPT_KERNEL, 1)
+    # ablation: host-driven JCG loop (batched readbacks) instead of the CUDA-graph WHILE loop
+    grid.set_option(ecmg.OPT_GRAPH, 0)
+    grid.run(eps, u, ut)
+    ev_h = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev_h[0].record(stream)
+    grid.run(eps, u, ut)
+    ev_h[1].record(stream)
+    torch.cuda.synchronize()
+    tts_hostloop = ev_h[0].elapsed_time(ev_h[1])
+    grid.set_option(ecmg.OPT_GRAPH, 1)
     peak, peak_src = load_peaks()
     achieved = BYTES_PER_UNKNOWN_ITER * nf_j * it_j / (ms_j / 1e3) / 1e9
     traffic = None
@@ -281,6 +291,7 @@ def main():
                        "l2": "inputs larger than L2 (no flush)",
                        "iterations_per_level": [s["iterations"] for s in per_level]},
             "ecmg_tts_ms": ms_per_step,
+            "ecmg_tts_ms_ablation_hostloop": tts_hostloop,
             "fine_grid_jcg_in_run": {"value": fine_units / (fine_ms / 1e3), "unit": UNIT,
                                      "iterations": int(per_level[-1]["iterations"])},
             "jcg_fixed": {"value": jcg_ups, "unit": UNIT, "iterations": it_j, "ms": ms_j,

@@ -100,8 +100,10 @@ typedef enum {
                                 1: Remark 2's 27-node tri-quadratic Lagrange */
   ECMG_OPT_PRECOND = 2,      /* 1 (default): Jacobi, ECMG_jcg; 0: plain CG, ECMG_cg */
   ECMG_OPT_ZCHUNK = 3,       /* planes per CTA in the z-marching JCG kernels (tuning; 0 = auto) */
-  ECMG_OPT_KERNEL = 4        /* constant-coefficient JCG kernels: 1 (default) TMA-fed smem ring,
+  ECMG_OPT_KERNEL = 4,       /* constant-coefficient JCG kernels: 1 (default) TMA-fed smem ring,
                                 0 register-prefetch loads (ablation) */
+  ECMG_OPT_GRAPH = 5         /* tolerance-stopped JCG loop: 1 (default) one CUDA graph per level with a
+                                device-set conditional WHILE node; 0 host loop with batched readbacks */
 } ecmg_option;
 int ecmg_set_option(ecmg_grid* grid, int option, int value);
 

@@ -52,6 +52,10 @@ struct ecmg_grid {
   cudaEvent_t ev[16];
   bool ev_init = false;
   int kernel_variant = 1;   // ECMG_OPT_KERNEL
+  int use_graph = 1;        // ECMG_OPT_GRAPH: device-driven JCG loop (CUDA graph, conditional WHILE node)
+  cudaStream_t cap_stream = nullptr;          // private stream used only for graph capture
+  struct ParamHost { double eps; int max_iter; int pad; }* param_host = nullptr;   // pinned
+  std::vector<cudaGraphExec_t> graphs;        // per level, lazily built
   struct Maps { int level = -1; CUtensorMap xh, xi, rh, ri, ph[2], bi; bool ok = false; } maps;
   double last_jcg_ms = 0.0;
   int last_jcg_iters = 0;
@@ -59,6 +63,12 @@ struct ecmg_grid {
 };
 
 namespace {
+
+void clear_graphs(ecmg_grid* G) {
+  for (auto& e : G->graphs)
+    if (e) cudaGraphExecDestroy(e);
+  G->graphs.assign(G->L, nullptr);
+}
 
 inline int cuda_status(cudaError_t e) { return e == cudaSuccess ? ECMG_OK : (e == cudaErrorMemoryAllocation ? ECMG_ENOMEM : ECMG_ECUDA); }
 
@@ -232,6 +242,106 @@ int setup_level(ecmg_grid* G, int k) {
 
 long long free_count(const LevelGeom& g) { return (long long)g.nf[0] * g.nf[1] * g.nf[2]; }
 
+int fill_stats(ecmg_grid* G, const LevelGeom& g, double eps, ecmg_stats* st) {
+  const JcgScalars s = G->sc_host[0];
+  G->last_jcg_iters = s.iter;
+  G->last_free = free_count(g);
+  const double nb = std::sqrt(s.bb);
+  const double nbe = nb > 0.0 ? nb : 1.0;
+  int status = s.status;
+  const bool conv = (eps <= 0.0) || !(std::sqrt(s.rr) > eps * nbe);
+  if (status == ECMG_OK && !conv) status = ECMG_ENOTCONV;
+  if (st) {
+    st->iterations = s.iter;
+    st->rel_res_recur = std::sqrt(s.rr) / nbe;
+    st->rel_res_true = std::sqrt(s.rr_true) / nbe;
+    st->norm_b = nb;
+    st->converged = conv && status == ECMG_OK;
+    st->status = status;
+  }
+  return status;
+}
+
+// Device-driven JCG (Alg. 4 l.7-9): one CUDA graph per level = init -> WHILE(cond){K1,K2,K1,K2} -> true
+// residual. The init pass and every K2 (and K1 on breakdown) set cond = !done from their last CTA,
+// so the loop stops after exactly the iteration that meets ||r|| <= eps ||f|| (the second K1/K2 of a
+// body run after convergence sees done and returns). No host round trip per iteration.
+cudaError_t build_level_graph(ecmg_grid* G, int k, cudaGraphExec_t* out) {
+  const LevelGeom& g = G->geom[k];
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaGraphCreate(&graph, 0);
+  if (e != cudaSuccess) return e;
+  cudaGraphConditionalHandle h;
+  e = cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault);
+  KArgs a{};
+  a.partials = G->partials; a.sc = G->sc; a.zc = auto_zc(G, g); a.beta = G->beta;
+  a.cond = h; a.use_cond = 1;
+  const long long launches_before = ecmg_kernel_launches();
+  cudaStream_t user = G->stream;
+  G->stream = G->cap_stream;   // launchers enqueue on G->stream: point it at the capture stream
+  cudaGraphNode_t init_node = nullptr, cond_node = nullptr;
+  auto done = [&](cudaError_t err) { G->stream = user; return err; };
+  if (e != cudaSuccess) return done(e);
+  // init pass
+  e = cudaStreamBeginCaptureToGraph(G->cap_stream, graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) return done(e);
+  { KArgs ai = a; ai.h0 = G->x; ai.i0 = G->b; ai.o0 = G->r; e = launch_mode(G, MODE_INIT, g, ai); }
+  cudaError_t e2 = cudaStreamEndCapture(G->cap_stream, &graph);
+  if (e != cudaSuccess || e2 != cudaSuccess) return done(e != cudaSuccess ? e : e2);
+  size_t nn = 1;
+  e = cudaGraphGetNodes(graph, &init_node, &nn);
+  if (e != cudaSuccess || nn != 1) return done(e != cudaSuccess ? e : cudaErrorUnknown);
+  // WHILE node and its body (two JCG iterations: p ping-pong)
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  e = cudaGraphAddNode(&cond_node, graph, &init_node, 1, &cp);
+  if (e != cudaSuccess) return done(e);
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  e = cudaStreamBeginCaptureToGraph(G->cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) return done(e);
+  for (int half = 0; half < 2 && e == cudaSuccess; ++half) {
+    KArgs a1 = a;
+    a1.h0 = G->r; a1.h1 = G->p[half]; a1.o0 = G->p[1 - half];
+    e = launch_mode(G, MODE_K1, g, a1);
+    if (e != cudaSuccess) break;
+    KArgs a2 = a;
+    a2.h0 = G->p[1 - half]; a2.i0 = G->x; a2.i1 = G->r; a2.o0 = G->x; a2.o1 = G->r;
+    e = launch_mode(G, MODE_K2, g, a2);
+  }
+  e2 = cudaStreamEndCapture(G->cap_stream, &body);
+  if (e != cudaSuccess || e2 != cudaSuccess) return done(e != cudaSuccess ? e : e2);
+  // true residual after the loop
+  e = cudaStreamBeginCaptureToGraph(G->cap_stream, graph, &cond_node, nullptr, 1, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) return done(e);
+  { KArgs at = a; at.use_cond = 0; at.h0 = G->x; at.i0 = G->b; e = launch_mode(G, MODE_TRUE, g, at); }
+  e2 = cudaStreamEndCapture(G->cap_stream, &graph);
+  if (e != cudaSuccess || e2 != cudaSuccess) return done(e != cudaSuccess ? e : e2);
+  e = cudaGraphInstantiate(out, graph, 0);
+  cudaGraphDestroy(graph);
+  count_launch((int)(launches_before - ecmg_kernel_launches()));   // captured, not launched
+  return done(e);
+}
+
+int run_jcg_graph(ecmg_grid* G, int k, double eps, ecmg_stats* st) {
+  const LevelGeom& g = G->geom[k];
+  if ((int)G->graphs.size() != G->L) G->graphs.assign(G->L, nullptr);
+  if (!G->graphs[k]) ECMG_CUDA(build_level_graph(G, k, &G->graphs[k]));
+  ECMG_CUDA(cudaEventRecord(G->ev[0], G->stream));
+  ECMG_CUDA(cudaGraphLaunch(G->graphs[k], G->stream));
+  ECMG_CUDA(cudaEventRecord(G->ev[1], G->stream));
+  ECMG_CUDA(cudaMemcpyAsync(&G->sc_host[0], G->sc, sizeof(JcgScalars), cudaMemcpyDeviceToHost, G->stream));
+  ECMG_CUDA(cudaStreamSynchronize(G->stream));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, G->ev[0], G->ev[1]);
+  G->last_jcg_ms = ms;
+  const int it = G->sc_host[0].iter;
+  count_launch(2 + 4 * ((it + 1) / 2));   // init + true residual + executed loop bodies
+  return fill_stats(G, g, eps, st);
+}
+
 // JCG on the level whose RHS is in G->b, starting from G->x. Fills stats (except timings).
 int run_jcg(ecmg_grid* G, int k, double eps, int max_iter, ecmg_stats* st) {
   const LevelGeom& g = G->geom[k];
@@ -242,8 +352,11 @@ int run_jcg(ecmg_grid* G, int k, double eps, int max_iter, ecmg_stats* st) {
   a.sc = G->sc;
   a.zc = auto_zc(G, g);
   a.beta = G->beta;
-  a.eps = eps;
-  a.max_iter = max_iter;
+  // eps and max_iter reach the init pass through the device scalars
+  G->param_host->eps = eps;
+  G->param_host->max_iter = max_iter;
+  ECMG_CUDA(cudaMemcpyAsync(&G->sc->eps_in, G->param_host, sizeof(double) + sizeof(int), cudaMemcpyHostToDevice, G->stream));
+  if (eps > 0.0 && G->use_graph) return run_jcg_graph(G, k, eps, st);
   // r = b - A x, rho = r.z, rr = r.r, stop test
   {
     KArgs ai = a;
@@ -296,26 +409,10 @@ int run_jcg(ecmg_grid* G, int k, double eps, int max_iter, ecmg_stats* st) {
   }
   ECMG_CUDA(cudaMemcpyAsync(&G->sc_host[0], G->sc, sizeof(JcgScalars), cudaMemcpyDeviceToHost, G->stream));
   ECMG_CUDA(cudaStreamSynchronize(G->stream));
-  const JcgScalars s = G->sc_host[0];
   float ms = 0.f;
   cudaEventElapsedTime(&ms, G->ev[0], G->ev[1]);
   G->last_jcg_ms = ms;
-  G->last_jcg_iters = s.iter;
-  G->last_free = free_count(g);
-  const double nb = std::sqrt(s.bb);
-  const double nbe = nb > 0.0 ? nb : 1.0;
-  int status = s.status;
-  const bool conv = (eps <= 0.0) || !(std::sqrt(s.rr) > eps * nbe);
-  if (status == ECMG_OK && !conv) status = ECMG_ENOTCONV;
-  if (st) {
-    st->iterations = s.iter;
-    st->rel_res_recur = std::sqrt(s.rr) / nbe;
-    st->rel_res_true = std::sqrt(s.rr_true) / nbe;
-    st->norm_b = nb;
-    st->converged = conv && status == ECMG_OK;
-    st->status = status;
-  }
-  return status;
+  return fill_stats(G, g, eps, st);
 }
 
 bool is_device_ptr(const void* p) {
@@ -397,6 +494,12 @@ int ecmg_create_grid(const ecmg_box* dom, const int coarsest_cells[3], int num_l
   if (st == ECMG_OK && cudaMalloc(&G->sc, sizeof(JcgScalars)) != cudaSuccess) st = ECMG_ENOMEM;
   if (st == ECMG_OK && cudaMemsetAsync(G->sc, 0, sizeof(JcgScalars), G->stream) != cudaSuccess) st = ECMG_ECUDA;
   if (st == ECMG_OK && cudaHostAlloc(&G->sc_host, 2 * sizeof(JcgScalars), cudaHostAllocDefault) != cudaSuccess) st = ECMG_ENOMEM;
+  if (st == ECMG_OK && cudaHostAlloc(&G->param_host, sizeof(*G->param_host), cudaHostAllocDefault) != cudaSuccess) st = ECMG_ENOMEM;
+  if (st == ECMG_OK && cudaStreamCreateWithFlags(&G->cap_stream, cudaStreamNonBlocking) != cudaSuccess) st = ECMG_ECUDA;
+  G->graphs.assign(num_levels, nullptr);
+  if (st == ECMG_OK && (init_tma_kernel_attributes() != cudaSuccess || init_elem_kernel_attributes() != cudaSuccess ||
+                        init_setup_kernel_attributes() != cudaSuccess))
+    st = ECMG_ECUDA;
   if (st == ECMG_OK) {
     for (int i = 0; i < 16; ++i) cudaEventCreate(&G->ev[i]);
     G->ev_init = true;
@@ -417,6 +520,9 @@ int ecmg_destroy_grid(ecmg_grid* G) {
   cudaFree(G->scratch1d);
   cudaFree(G->seeds);
   if (G->sc_host) cudaFreeHost(G->sc_host);
+  if (G->param_host) cudaFreeHost(G->param_host);
+  clear_graphs(G);
+  if (G->cap_stream) cudaStreamDestroy(G->cap_stream);
   if (G->ev_init) for (int i = 0; i < 16; ++i) cudaEventDestroy(G->ev[i]);
   cudaGetLastError();
   delete G;
@@ -455,6 +561,7 @@ int ecmg_set_coeffs(ecmg_grid* G, const ecmg_problem* pr) {
   G->has_problem = true;
   G->setup_level = -1;
   G->maps.level = -1;
+  clear_graphs(G);
   return ECMG_OK;
 }
 
@@ -462,9 +569,10 @@ int ecmg_set_option(ecmg_grid* G, int option, int value) {
   if (!G) return ECMG_EINVAL;
   switch (option) {
     case ECMG_OPT_EXP_VARIANT: if (value != 0 && value != 1) return ECMG_EINVAL; G->exp_variant = value; break;
-    case ECMG_OPT_PRECOND: if (value != 0 && value != 1) return ECMG_EINVAL; G->precond = value; G->setup_level = -1; break;
-    case ECMG_OPT_ZCHUNK: if (value < 0) return ECMG_EINVAL; G->zchunk = value; break;
-    case ECMG_OPT_KERNEL: if (value != 0 && value != 1) return ECMG_EINVAL; G->kernel_variant = value; break;
+    case ECMG_OPT_PRECOND: if (value != 0 && value != 1) return ECMG_EINVAL; G->precond = value; G->setup_level = -1; clear_graphs(G); break;
+    case ECMG_OPT_ZCHUNK: if (value < 0) return ECMG_EINVAL; G->zchunk = value; clear_graphs(G); break;
+    case ECMG_OPT_KERNEL: if (value != 0 && value != 1) return ECMG_EINVAL; G->kernel_variant = value; clear_graphs(G); break;
+    case ECMG_OPT_GRAPH: if (value != 0 && value != 1) return ECMG_EINVAL; G->use_graph = value; break;
     default: return ECMG_EINVAL;
   }
   return ECMG_OK;

@@ -67,6 +67,8 @@ struct JcgScalars {
   double bb;         // ||b||^2 (set by the RHS kernel)
   double rr_true;    // ||b - A x||^2 (set by the true-residual pass)
   double thresh;     // eps * ||b|| (or eps if ||b|| = 0); <= 0: fixed-iteration mode
+  double eps_in;     // requested eps (written by the host before the init pass)
+  int max_iter_in;   // requested max_iter (idem)
   int iter, max_iter, done, status;
   unsigned int counter;   // last-block-done counter (reset by the last block)
   int pad_;
@@ -85,8 +87,10 @@ struct KArgs {
   double* partials;   // per-block partial dot products (2 per block)
   JcgScalars* sc;
   int zc;             // planes per CTA
-  double eps;         // INIT only
-  int max_iter;       // INIT only
+  double eps;         // unused (eps / max_iter are read from JcgScalars::eps_in / max_iter_in)
+  int max_iter;
+  cudaGraphConditionalHandle cond;   // CUDA-graph WHILE condition (device-driven JCG loop)
+  int use_cond;                      // 1: the init / K2 passes set `cond` = !done
 };
 
 // status codes (mirror of ecmg_status)
@@ -107,6 +111,9 @@ namespace ecmg {
 cudaError_t launch_jcg_const_tma(int mode, const LevelGeom& g, const ConstStencil& cs, const KArgs& a,
                                  const CUtensorMap* maps, cudaStream_t st);
 int make_vec_tensor_map(CUtensorMap* map, const double* base, const LevelGeom& g, int bx, int by);
+cudaError_t init_tma_kernel_attributes();
+cudaError_t init_elem_kernel_attributes();
+cudaError_t init_setup_kernel_attributes();
 int tma_halo_box_x();
 int tma_halo_box_y();
 int tma_int_box_x();

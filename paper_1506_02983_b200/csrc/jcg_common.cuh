@@ -12,6 +12,20 @@ constexpr int NTH = TX * WARPS;
 
 // ---- deterministic reductions and the device-side CG scalar updates -----------------------
 
+// ---- the per-node arithmetic of the constant-stencil kernels, with explicit rounding ------------
+// (shared by the TMA-fed and the register-prefetch kernels so both produce bitwise-equal iterates)
+// p_new = D^-1 r + beta_cg p_old (textbook PCG search direction, O7)
+__device__ __forceinline__ double pcg_direction(double dinv, double r, double bcg, double pold, bool first) {
+  return first ? dinv * r : __fma_rn(bcg, pold, dinv * r);
+}
+// per-plane partial sums of the constant 27-point stencil: q0 (plane is the centre plane) and
+// q1 (plane is a neighbour plane) from the centre value and the in-plane sums
+__device__ __forceinline__ void stencil_q(const ConstStencil& cs, double cc, double ax, double ay, double dd, double& q0,
+                                          double& q1) {
+  q0 = __fma_rn(cs.cd[0], dd, __fma_rn(cs.cy[0], ay, __fma_rn(cs.cx[0], ax, cs.c0[0] * cc)));
+  q1 = __fma_rn(cs.cd[1], dd, __fma_rn(cs.cy[1], ay, __fma_rn(cs.cx[1], ax, cs.c0[1] * cc)));
+}
+
 __device__ __forceinline__ void block_sum3(double& a, double& b, double& c, double* red) {
   const int tid = threadIdx.x + TX * threadIdx.y;
 #pragma unroll
@@ -35,18 +49,25 @@ __device__ void finalize(int mode, const KArgs& a, double s0, double s1, double 
     case MODE_INIT: {
       sc->bb = s2;   // ||b||^2 of the lifted right-hand side (read by this pass anyway)
       sc->rho = s0; sc->rr = s1; sc->alpha = 0.0; sc->beta = 0.0; sc->sigma = 0.0;
-      sc->iter = 0; sc->status = ST_OK; sc->max_iter = a.max_iter;
+      const double eps = sc->eps_in;
+      const int max_iter = sc->max_iter_in;
+      sc->iter = 0; sc->status = ST_OK; sc->max_iter = max_iter;
       const double nb = sqrt(sc->bb);
       const double nbe = nb > 0.0 ? nb : 1.0;             // ||f|| = 0: absolute residual (§8c A11)
-      sc->thresh = a.eps > 0.0 ? a.eps * nbe : -1.0;      // eps <= 0: fixed iteration count
-      int done = (a.max_iter <= 0) || (sc->thresh > 0.0 && !(sqrt(s1) > sc->thresh));
+      sc->thresh = eps > 0.0 ? eps * nbe : -1.0;          // eps <= 0: fixed iteration count
+      int done = (max_iter <= 0) || (sc->thresh > 0.0 && !(sqrt(s1) > sc->thresh));
       if (!isfinite(s1)) { sc->status = ST_EBREAKDOWN; done = 1; }
       sc->done = done;
+      if (a.use_cond) cudaGraphSetConditional(a.cond, done ? 0u : 1u);
       break;
     }
     case MODE_K1: {
       sc->sigma = s0;
-      if (!(s0 > 0.0)) { sc->status = ST_EBREAKDOWN; sc->done = 1; }   // p.Ap <= 0
+      if (!(s0 > 0.0)) {   // p.Ap <= 0
+        sc->status = ST_EBREAKDOWN;
+        sc->done = 1;
+        if (a.use_cond) cudaGraphSetConditional(a.cond, 0u);
+      }
       else sc->alpha = sc->rho / s0;
       break;
     }
@@ -59,6 +80,7 @@ __device__ void finalize(int mode, const KArgs& a, double s0, double s1, double 
       int done = (sc->iter >= sc->max_iter) || (sc->thresh > 0.0 && !(sqrt(s1) > sc->thresh));
       if (!isfinite(s1)) { sc->status = ST_EBREAKDOWN; done = 1; }
       sc->done = done;
+      if (a.use_cond) cudaGraphSetConditional(a.cond, done ? 0u : 1u);
       break;
     }
     case MODE_TRUE: sc->rr_true = s1; break;

@@ -151,24 +151,42 @@ __global__ void k_exp_interp(const LevelGeom gf, const Problem pb, const double*
 }
 
 // EXP_true, one thread per 2h cell (cx, cy, cz); owned fine nodes 2c + {0,1} per axis (+2 in the
-// last cell along an axis)
-__global__ void k_exp_true(const LevelGeom gf, const Problem pb, const double* __restrict__ uh, const double* __restrict__ u2h,
-                           double* __restrict__ ut) {
+// last cell along an axis). Cells whose owned nodes are all free take the fast path (no Dirichlet
+// tests, pointer increments only).
+__global__ void __launch_bounds__(128, 6) k_exp_true(const LevelGeom gf, const Problem pb, const double* __restrict__ uh,
+                                                  const double* __restrict__ u2h, double* __restrict__ ut) {
   const int n2x = gf.n[0] / 2, n2y = gf.n[1] / 2, n2z = gf.n[2] / 2;
   const int cx = blockIdx.x * blockDim.x + threadIdx.x, cy = blockIdx.y, cz = blockIdx.z;
   if (cx >= n2x) return;
-  const long long nx = gf.n[0] + 1, ny = gf.n[1] + 1;
-  const long long nx2 = n2x + 1, ny2 = n2y + 1;
+  const long long nx = gf.n[0] + 1, ny = gf.n[1] + 1, pl = nx * ny;
+  const long long nx2 = n2x + 1, pl2 = nx2 * (n2y + 1);
+  const long long c0 = 2LL * cx + nx * 2LL * cy + pl * 2LL * cz;     // fine index of the cell's first node
+  const long long k0 = (long long)cx + nx2 * cy + pl2 * cz;          // 2h index of the cell's first corner
   double d[2][2][2];
 #pragma unroll
   for (int c = 0; c < 2; ++c)
 #pragma unroll
     for (int b = 0; b < 2; ++b)
 #pragma unroll
-      for (int a = 0; a < 2; ++a) {
-        const long long X = cx + a, Y = cy + b, Z = cz + c;
-        d[c][b][a] = __ldg(uh + 2 * X + nx * (2 * Y + ny * 2 * Z)) - __ldg(u2h + X + nx2 * (Y + ny2 * Z));
+      for (int a = 0; a < 2; ++a)
+        d[c][b][a] = __ldg(uh + c0 + 2 * (a + nx * b + pl * c)) - __ldg(u2h + k0 + a + nx2 * b + pl2 * c);
+  const bool last = (cx == n2x - 1) || (cy == n2y - 1) || (cz == n2z - 1);
+  const bool inner = !last && 2 * cx >= gf.flo[0] && 2 * cy >= gf.flo[1] && 2 * cz >= gf.flo[2] &&
+                     2 * cx + 1 < gf.flo[0] + gf.nf[0] && 2 * cy + 1 < gf.flo[1] + gf.nf[1] && 2 * cz + 1 < gf.flo[2] + gf.nf[2];
+  if (inner) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const double wz1 = 0.5 * c, wz0 = 1.0 - wz1, wy1 = 0.5 * b, wy0 = 1.0 - wy1;
+        const double r0 = wz0 * (wy0 * d[0][0][0] + wy1 * d[0][1][0]) + wz1 * (wy0 * d[1][0][0] + wy1 * d[1][1][0]);
+        const double r1 = wz0 * (wy0 * d[0][0][1] + wy1 * d[0][1][1]) + wz1 * (wy0 * d[1][0][1] + wy1 * d[1][1][1]);
+        const long long i = c0 + nx * b + pl * c;
+        ut[i] = __ldg(uh + i) + r0 / 3.0;
+        ut[i + 1] = __ldg(uh + i + 1) + (0.5 * r0 + 0.5 * r1) / 3.0;
       }
+    return;
+  }
   const int ea = (cx == n2x - 1) ? 3 : 2, eb = (cy == n2y - 1) ? 3 : 2, ec = (cz == n2z - 1) ? 3 : 2;
   for (int c = 0; c < ec; ++c) {
     const double wz[2] = {1.0 - 0.5 * c, 0.5 * c};
@@ -210,9 +228,9 @@ cudaError_t launch_exp_finite(const LevelGeom& gf, const Problem& pb, const doub
 
 cudaError_t launch_exp_true(const LevelGeom& gf, const Problem& pb, const double* uh, const double* u2h, double* ut,
                             cudaStream_t st) {
-  dim3 grid((gf.n[0] / 2 + 63) / 64, gf.n[1] / 2, gf.n[2] / 2);
+  dim3 grid((gf.n[0] / 2 + 127) / 128, gf.n[1] / 2, gf.n[2] / 2);
   count_launch();
-  k_exp_true<<<grid, 64, 0, st>>>(gf, pb, uh, u2h, ut);
+  k_exp_true<<<grid, 128, 0, st>>>(gf, pb, uh, u2h, ut);
   return cudaGetLastError();
 }
 

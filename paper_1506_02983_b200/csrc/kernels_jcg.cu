@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(NTH, 2) k_jcg_const(const LevelGeom g, const C
     }
   };
   auto transform = [&](double v0, double v1) -> double {
-    if (MODE == MODE_K1) return first ? dinv * v0 : dinv * v0 + bcg * v1;
+    if (MODE == MODE_K1) return pcg_direction(dinv, v0, bcg, v1, first);
     return v0;
   };
 
@@ -135,32 +135,32 @@ __global__ void __launch_bounds__(NTH, 2) k_jcg_const(const LevelGeom g, const C
       const double ax = col[j + 1][0] + col[j + 1][2];
       const double ay = col[j][1] + col[j + 2][1];
       const double dd = (col[j][0] + col[j][2]) + (col[j + 2][0] + col[j + 2][2]);
-      const double q0 = cs.c0[0] * cc + cs.cx[0] * ax + cs.cy[0] * ay + cs.cd[0] * dd;
-      const double q1 = cs.c0[1] * cc + cs.cx[1] * ax + cs.cy[1] * ay + cs.cd[1] * dd;
+      double q0, q1;
+      stencil_q(cs, cc, ax, ay, dd, q0, q1);
       if (s >= 2 && own_ok[j]) {
         const double ap = part[j] + q1;   // (A p) at plane z
         const long long off = (long long)z * S + own_off[j];
         if (MODE == MODE_K1) {
-          acc0 += pp[j] * ap;
+          acc0 = __fma_rn(pp[j], ap, acc0);
           a.o0[off] = pp[j];
         } else if (MODE == MODE_K2) {
-          const double xn = ii0[j] + alpha * pp[j];
-          const double rn = ii1[j] - alpha * ap;
+          const double xn = __fma_rn(alpha, pp[j], ii0[j]);
+          const double rn = __fma_rn(-alpha, ap, ii1[j]);
           const double zz = dinv * rn;
-          acc0 += rn * zz;
-          acc1 += rn * rn;
+          acc0 = __fma_rn(rn, zz, acc0);
+          acc1 = __fma_rn(rn, rn, acc1);
           a.o0[off] = xn;
           a.o1[off] = rn;
         } else if (MODE == MODE_INIT) {
-          acc2 += ii0[j] * ii0[j];
+          acc2 = __fma_rn(ii0[j], ii0[j], acc2);
           const double rn = ii0[j] - ap;
           const double zz = dinv * rn;
-          acc0 += rn * zz;
-          acc1 += rn * rn;
+          acc0 = __fma_rn(rn, zz, acc0);
+          acc1 = __fma_rn(rn, rn, acc1);
           a.o0[off] = rn;
         } else if (MODE == MODE_TRUE) {
           const double rn = ii0[j] - ap;
-          acc1 += rn * rn;
+          acc1 = __fma_rn(rn, rn, acc1);
         } else {
           a.o0[off] = ap;
         }
@@ -426,20 +426,20 @@ __global__ void __launch_bounds__(NTH, 2) k_jcg_elem(const LevelGeom g, const El
         const double xn = ii0 + alpha * pc;
         const double rn = ii1 - alpha * ap;
         const double zz = dinv * rn;
-        acc0 += rn * zz;
-        acc1 += rn * rn;
+        acc0 = __fma_rn(rn, zz, acc0);
+        acc1 = __fma_rn(rn, rn, acc1);
         a.o0[off] = xn;
         a.o1[off] = rn;
       } else if (MODE == MODE_INIT) {
         acc2 += ii0 * ii0;
         const double rn = ii0 - ap;
         const double zz = dinv * rn;
-        acc0 += rn * zz;
-        acc1 += rn * rn;
+        acc0 = __fma_rn(rn, zz, acc0);
+        acc1 = __fma_rn(rn, rn, acc1);
         a.o0[off] = rn;
       } else if (MODE == MODE_TRUE) {
         const double rn = ii0 - ap;
-        acc1 += rn * rn;
+        acc1 = __fma_rn(rn, rn, acc1);
       } else {
         a.o0[off] = ap;
       }
@@ -470,15 +470,18 @@ cudaError_t launch_jcg_const(int mode, const LevelGeom& g, const ConstStencil& c
   return cudaGetLastError();
 }
 
+cudaError_t init_elem_kernel_attributes() {
+  cudaError_t e = cudaFuncSetAttribute(k_jcg_elem<MODE_K1>, cudaFuncAttributeMaxDynamicSharedMemorySize, ELEM_SMEM);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_jcg_elem<MODE_K2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ELEM_SMEM);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_jcg_elem<MODE_INIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, ELEM_SMEM);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_jcg_elem<MODE_TRUE>, cudaFuncAttributeMaxDynamicSharedMemorySize, ELEM_SMEM);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_jcg_elem<MODE_APPLY>, cudaFuncAttributeMaxDynamicSharedMemorySize, ELEM_SMEM);
+  return e;
+}
+
 template <int MODE>
 static cudaError_t launch_elem_mode(dim3 grid, dim3 block, const LevelGeom& g, const ElemStencil& es,
                                     const Problem& pb, const KArgs& a, cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_jcg_elem<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, ELEM_SMEM);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
   count_launch();
   k_jcg_elem<MODE><<<grid, block, ELEM_SMEM, st>>>(g, es, pb, a);
   return cudaGetLastError();

@@ -154,11 +154,11 @@ __global__ void __launch_bounds__(NTH, 2)
 #pragma unroll
       for (int j = 0; j < RY; ++j) {
         const int o = (1 + RY * w + j) * HX + XO + lane;
-        H[o] = first ? dinv * H[o] : dinv * H[o] + bcg * H1[o];
+        H[o] = pcg_direction(dinv, H[o], bcg, H1[o], first);
       }
       if (rhx >= 0) {
         const int o = rhy * HX + rhx;
-        H[o] = first ? dinv * H[o] : dinv * H[o] + bcg * H1[o];
+        H[o] = pcg_direction(dinv, H[o], bcg, H1[o], first);
       }
       __syncthreads();
     }
@@ -176,33 +176,33 @@ __global__ void __launch_bounds__(NTH, 2)
       const double ax = col[j + 1][0] + col[j + 1][2];
       const double ay = col[j][1] + col[j + 2][1];
       const double dd = (col[j][0] + col[j][2]) + (col[j + 2][0] + col[j + 2][2]);
-      const double q0 = cs.c0[0] * cc + cs.cx[0] * ax + cs.cy[0] * ay + cs.cd[0] * dd;
-      const double q1 = cs.c0[1] * cc + cs.cx[1] * ax + cs.cy[1] * ay + cs.cd[1] * dd;
+      double q0, q1;
+      stencil_q(cs, cc, ax, ay, dd, q0, q1);
       if (s >= 2 && own_ok[j]) {
         const double ap = part[j] + q1;
         const long long off = (long long)z * S + own_off[j];
         const int io = (RY * w + j) * TX + lane;
         if (MODE == MODE_K1) {
-          acc0 += pp[j] * ap;
+          acc0 = __fma_rn(pp[j], ap, acc0);
           a.o0[off] = pp[j];
         } else if (MODE == MODE_K2) {
-          const double xn = I0[io] + alpha * pp[j];
-          const double rn = I1[io] - alpha * ap;
+          const double xn = __fma_rn(alpha, pp[j], I0[io]);
+          const double rn = __fma_rn(-alpha, ap, I1[io]);
           const double zz = dinv * rn;
-          acc0 += rn * zz;
-          acc1 += rn * rn;
+          acc0 = __fma_rn(rn, zz, acc0);
+          acc1 = __fma_rn(rn, rn, acc1);
           a.o0[off] = xn;
           a.o1[off] = rn;
         } else if (MODE == MODE_INIT) {
-          acc2 += I0[io] * I0[io];
+          acc2 = __fma_rn(I0[io], I0[io], acc2);
           const double rn = I0[io] - ap;
           const double zz = dinv * rn;
-          acc0 += rn * zz;
-          acc1 += rn * rn;
+          acc0 = __fma_rn(rn, zz, acc0);
+          acc1 = __fma_rn(rn, rn, acc1);
           a.o0[off] = rn;
         } else if (MODE == MODE_TRUE) {
           const double rn = I0[io] - ap;
-          acc1 += rn * rn;
+          acc1 = __fma_rn(rn, rn, acc1);
         } else {
           a.o0[off] = ap;
         }
@@ -222,18 +222,30 @@ cudaError_t launch_tma_mode(dim3 grid, dim3 block, const LevelGeom& g, const Con
   constexpr int kNI = (MODE == MODE_K2) ? 2 : ((MODE == MODE_INIT || MODE == MODE_TRUE) ? 1 : 0);
   constexpr int SBYTES = HSTRIDE * (kH1 ? 2 : 1) + IBYTES * kNI;
   constexpr int SMEM = SBYTES * NS + 128;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_jcg_const_tma<MODE, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
   count_launch();
   k_jcg_const_tma<MODE, NS><<<grid, block, SMEM, st>>>(g, cs, a, maps[0], maps[1], maps[2], maps[3]);
   return cudaGetLastError();
 }
 
+template <int MODE, int NS>
+cudaError_t set_tma_attr() {
+  constexpr bool kH1 = (MODE == MODE_K1);
+  constexpr int kNI = (MODE == MODE_K2) ? 2 : ((MODE == MODE_INIT || MODE == MODE_TRUE) ? 1 : 0);
+  constexpr int SMEM = (HSTRIDE * (kH1 ? 2 : 1) + IBYTES * kNI) * NS + 128;
+  return cudaFuncSetAttribute(k_jcg_const_tma<MODE, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+}
+
 }  // namespace
+
+// set every dynamic-smem attribute up front (never inside a stream capture)
+cudaError_t init_tma_kernel_attributes() {
+  cudaError_t e = set_tma_attr<MODE_K1, 4>();
+  if (e == cudaSuccess) e = set_tma_attr<MODE_K2, 3>();
+  if (e == cudaSuccess) e = set_tma_attr<MODE_INIT, 4>();
+  if (e == cudaSuccess) e = set_tma_attr<MODE_TRUE, 4>();
+  if (e == cudaSuccess) e = set_tma_attr<MODE_APPLY, 4>();
+  return e;
+}
 
 // maps[0..3] = H0, H1, I0, I1 tensor maps (unused entries may be any valid map)
 cudaError_t launch_jcg_const_tma(int mode, const LevelGeom& g, const ConstStencil& cs, const KArgs& a,

@@ -94,7 +94,18 @@ __global__ void k_rhs_sep(const LevelGeom g, const Problem pb, const double* __r
   b[(long long)fz * g.S + (long long)fy * g.P + fx] = v;
 }
 
-__global__ void __launch_bounds__(VNTH) k_rhs_vol(const LevelGeom g, const Problem pb, double* __restrict__ b, int zc) {
+// f specialised per problem at compile time (PID = 0: generic registry switch)
+template <int PID>
+__device__ __forceinline__ double f_at(const Problem& pb, double x, double y, double z) {
+  if (PID == 4) {   // C4: -(15/4) r^{-1/2}
+    const double r2 = x * x + y * y + z * z;
+    return r2 == 0.0 ? 0.0 : -3.75 * rsqrt(sqrt(r2));
+  }
+  return prob_f(pb, x, y, z);
+}
+
+template <int PID>
+__global__ void __launch_bounds__(VNTH, 3) k_rhs_vol(const LevelGeom g, const Problem pb, double* __restrict__ b, int zc) {
   extern __shared__ double vs[];
   double* fq = vs;              // [VNE][8] f at the Gauss points of one element plane
   double* Fe = vs + VNE * 8;    // [2][VNE][8] element load vectors, ring of two element planes
@@ -112,8 +123,8 @@ __global__ void __launch_bounds__(VNTH) k_rhs_vol(const LevelGeom g, const Probl
       double v = 0.0;
       if (gex >= 0 && gex < g.n[0] && gey >= 0 && gey < g.n[1] && gez >= 0 && gez < g.n[2]) {
         const double xi = (q & 1) ? kGauss : -kGauss, eta = (q & 2) ? kGauss : -kGauss, ze = (q & 4) ? kGauss : -kGauss;
-        v = prob_f(pb, g.lo[0] + (gex + (1.0 + xi) / 2.0) * g.h[0], g.lo[1] + (gey + (1.0 + eta) / 2.0) * g.h[1],
-                   g.lo[2] + (gez + (1.0 + ze) / 2.0) * g.h[2]);
+        v = f_at<PID>(pb, g.lo[0] + (gex + (1.0 + xi) / 2.0) * g.h[0], g.lo[1] + (gey + (1.0 + eta) / 2.0) * g.h[1],
+                      g.lo[2] + (gez + (1.0 + ze) / 2.0) * g.h[2]);
       }
       fq[t] = v;
     }
@@ -281,6 +292,12 @@ cudaError_t launch_beta(const LevelGeom& g, const Problem& pb, double* beta, cud
   return cudaGetLastError();
 }
 
+cudaError_t init_setup_kernel_attributes() {
+  cudaError_t e = cudaFuncSetAttribute(k_rhs_vol<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, VSMEM);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_rhs_vol<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, VSMEM);
+  return e;
+}
+
 cudaError_t launch_rhs(const LevelGeom& g, const Problem& pb, const ElemStencil& es, double beta_const, const double* beta,
                        double* b, double* scratch, cudaStream_t st) {
   if (prob_separable(pb.id)) {
@@ -293,16 +310,11 @@ cudaError_t launch_rhs(const LevelGeom& g, const Problem& pb, const ElemStencil&
     count_launch();
     k_rhs_sep<<<g2, 128, 0, st>>>(g, pb, scratch, stride, b);
   } else {
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(k_rhs_vol, cudaFuncAttributeMaxDynamicSharedMemorySize, VSMEM);
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
     const int zc = 32;
     dim3 grid((g.nf[0] + VX - 1) / VX, (g.nf[1] + VY - 1) / VY, (g.nf[2] + zc - 1) / zc);
     count_launch();
-    k_rhs_vol<<<grid, dim3(VX, VY), VSMEM, st>>>(g, pb, b, zc);
+    if (pb.id == 4) k_rhs_vol<4><<<grid, dim3(VX, VY), VSMEM, st>>>(g, pb, b, zc);
+    else k_rhs_vol<0><<<grid, dim3(VX, VY), VSMEM, st>>>(g, pb, b, zc);
   }
   const int m = std::max(g.nf[0], std::max(g.nf[1], g.nf[2]));
   dim3 gs((m + 127) / 128, m, 6);

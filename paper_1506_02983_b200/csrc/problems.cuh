@@ -55,20 +55,21 @@ __host__ __device__ inline double prob_f(const Problem& P, double x, double y, d
     case 1: return 3.0 * pi * pi * prob_exact(P, x, y, z);
     case 2: return -3.0 * exp(x + y + z);
     case 3: {
-      // f = -beta Lap u - grad beta . grad u, Lap u = (1 - 2 pi^2) u
-      double sx = sin(pi * x), cx = cos(pi * x), sy = sin(pi * y), cy = cos(pi * y), ez = exp(z);
-      double u = cx * cy * ez;
-      double s2x = sin(2 * pi * x), c2x = cos(2 * pi * x), s2y = sin(2 * pi * y), c2y = cos(2 * pi * y);
-      double s2z = sin(2 * pi * z), c2z = cos(2 * pi * z);
-      double b = 1.0 + 0.5 * s2x * c2y * s2z;
-      double bx = pi * c2x * c2y * s2z, by = -pi * s2x * s2y * s2z, bz = pi * s2x * c2y * c2z;
-      double ux = -pi * sx * cy * ez, uy = -pi * cx * sy * ez;
+      // f = -beta Lap u - grad beta . grad u, Lap u = (1 - 2 pi^2) u   (sincospi: sin(pi t), cos(pi t))
+      double sx, cx, sy, cy, s2x, c2x, s2y, c2y, s2z, c2z;
+      sincospi(x, &sx, &cx); sincospi(y, &sy, &cy);
+      sincospi(2.0 * x, &s2x, &c2x); sincospi(2.0 * y, &s2y, &c2y); sincospi(2.0 * z, &s2z, &c2z);
+      const double ez = exp(z);
+      const double u = cx * cy * ez;
+      const double b = 1.0 + 0.5 * s2x * c2y * s2z;
+      const double bx = pi * c2x * c2y * s2z, by = -pi * s2x * s2y * s2z, bz = pi * s2x * c2y * c2z;
+      const double ux = -pi * sx * cy * ez, uy = -pi * cx * sy * ez;
       return -b * (1.0 - 2.0 * pi * pi) * u - (bx * ux + by * uy + bz * u);
     }
     case 4: {  // -Lap r^{3/2} = -(15/4) r^{-1/2}; f(0) := 0 (never evaluated at a node)
       double r2 = x * x + y * y + z * z;
       if (r2 == 0.0) return 0.0;
-      return -3.75 / sqrt(sqrt(r2));
+      return -3.75 * rsqrt(sqrt(r2));   // r^{-1/2}
     }
     case 5: {
       const double* x0 = &P.params[43];

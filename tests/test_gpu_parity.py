@@ -243,3 +243,20 @@ def test_tma_and_prefetch_kernels_bitwise(pid, level):
     assert np.array_equal(outs[0], outs[2]) and np.array_equal(outs[1], outs[3])
     xo, _ = L.jcg(x0, 0.0, 20)
     assert rel(outs[0][fr], xo[fr]) <= 1e-12
+
+
+@pytest.mark.parametrize("pid,eps", [(o.C2, 1e-10), (o.C3, 1e-10), (o.C4, 1e-9)])
+def test_graph_loop_equals_host_loop(pid, eps):
+    # the device-driven JCG loop (CUDA graph with a conditional WHILE node) and the host loop
+    # launch the same kernels in the same order: same iteration count, bitwise equal iterates
+    res = []
+    for use_graph in (1, 0):
+        g = Grid(4, 5, pid, params_for(pid))
+        g.set_option(ecmg.OPT_GRAPH, use_graph)
+        u = g.new_vec(4)
+        ut = g.new_vec(4)
+        st, stats = g.run(eps, u, ut)
+        assert st == 0
+        res.append(([s["iterations"] for s in stats], host(u), host(ut)))
+    assert res[0][0] == res[1][0]
+    assert np.array_equal(res[0][1], res[1][1]) and np.array_equal(res[0][2], res[1][2])
