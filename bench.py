@@ -166,8 +166,14 @@ def main():
 
     pid, n0, levels, eps, desc = CONFIGS[args.config]
     stream = torch.cuda.current_stream()
-    grid = Grid(n0, levels, pid)
-    shape, nodes = grid.shape(levels - 1)
+    gdist = None
+    if ws > 1:
+        # z-slab decomposition over NCCL ranks (strong scaling of the same C4 problem)
+        from paper_1506_02983_b200 import dist as edist
+        gdist = edist.ecmg_dist_from_torch(device=torch.device("cuda", local))
+    grid = Grid(n0, levels, pid, dist=gdist)
+    shape, nodes = grid.shape(levels - 1)      # nodes: this rank's planes of the finest level
+    zlo, zhi = ecmg.level_shape(grid.h, levels - 1)[3:5]
     u = torch.empty(nodes, dtype=torch.float64, device="cuda")
     ut = torch.empty(nodes, dtype=torch.float64, device="cuda")
 
@@ -211,13 +217,15 @@ def main():
     launches = ecmg.kernel_launches() - l0
     t_ms = max_over_ranks(evs[0].elapsed_time(evs[1]))
     ms_per_step = t_ms / args.steps
-    value = units_total * ws / (t_ms / 1e3)
+    value = units_total / (t_ms / 1e3)   # units of the whole (global) problem
 
     # ---- fixed-iteration fine-grid JCG benchmark and roofline --------------
     import numpy as np
     import synth
     fine = levels - 1
-    x0 = torch.from_numpy(synth.random_nodal(14, shape, (1, 1, 1), tuple(v - 1 for v in shape))).cuda()
+    x0_full = synth.random_nodal(14, shape, (1, 1, 1), tuple(v - 1 for v in shape))
+    pl = (shape[0] + 1) * (shape[1] + 1)
+    x0 = torch.from_numpy(x0_full[zlo * pl:zhi * pl].copy()).cuda()   # this rank's planes
     xb = x0.clone()
     grid.solve_level(fine, 0.0, 5, xb)   # warm-up (also sets up the level)
     jt = []
@@ -227,12 +235,18 @@ def main():
         ms_j, it_j, nf_j = grid.last_jcg_timing()
         jt.append((ms_j, it_j, nf_j))
     ms_j, it_j, nf_j = sorted(jt)[len(jt) // 2]
+    ms_j = max_over_ranks(ms_j)
+    if ws > 1:   # free unknowns of the whole problem
+        t = torch.tensor([float(nf_j)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t)
+        nf_j = int(t.item())
     jcg_ups = nf_j * it_j / (ms_j / 1e3)
     # ablation: the register-prefetch (non-TMA) kernels on the same system
     grid.set_option(ecmg.OPT_KERNEL, 0)
     xb.copy_(x0)
     grid.solve_level(fine, 0.0, args.fixed_iters, xb)
     ms_p, it_p, _ = grid.last_jcg_timing()
+    ms_p = max_over_ranks(ms_p)
     grid.set_option(ecmg.OPT_KERNEL, 1)
     # ablation: host-driven JCG loop (batched readbacks) instead of the CUDA-graph WHILE loop
     grid.set_option(ecmg.OPT_GRAPH, 0)
@@ -242,10 +256,10 @@ def main():
     grid.run(eps, u, ut)
     ev_h[1].record(stream)
     torch.cuda.synchronize()
-    tts_hostloop = ev_h[0].elapsed_time(ev_h[1])
+    tts_hostloop = max_over_ranks(ev_h[0].elapsed_time(ev_h[1]))
     grid.set_option(ecmg.OPT_GRAPH, 1)
     peak, peak_src = load_peaks()
-    achieved = BYTES_PER_UNKNOWN_ITER * nf_j * it_j / (ms_j / 1e3) / 1e9
+    achieved = BYTES_PER_UNKNOWN_ITER * nf_j * it_j / (ms_j / 1e3) / 1e9 / ws   # per GPU
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "jcg_traffic.json")) as f:
@@ -268,7 +282,7 @@ def main():
             e_units += (shp[0] - 1) * (shp[1] - 1) * (shp[2] - 1) * s["iterations"]
     barrier()
     e_s = max_over_ranks(time.perf_counter() - t0)
-    e2e = {"value": e_units * ws / e_s, "unit": UNIT, "h2d_bytes_per_step": 0,
+    e2e = {"value": e_units / e_s, "unit": UNIT, "h2d_bytes_per_step": 0,
            "d2h_bytes_per_step": 2 * nodes * 8, "ms_per_step": e_s / e_steps * 1e3,
            "note": "C ABI ecmg_run with pinned host u_h and u~_h (D2H inside the call); C4 inputs are analytic (no H2D)"}
 
@@ -284,10 +298,12 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (analytic C4 problem; no dataset)",
             "config": {"workload": desc, "levels": levels, "finest_cells": list(shape), "eps": eps,
-                       "free_unknowns_finest": int(nf_j), "parallelism": "replicas" if ws > 1 else "single GPU",
+                       "free_unknowns_finest": int(nf_j),
+                       "parallelism": f"z-slabs over {ws} NCCL ranks (levels with n % 4P == 0 and n/P >= 16 sharded)"
+                       if ws > 1 else "single GPU",
                        "l2": "inputs larger than L2 (no flush)",
                        "iterations_per_level": [s["iterations"] for s in per_level]},
             "ecmg_tts_ms": ms_per_step,
@@ -301,7 +317,8 @@ def main():
                                             "kernel": "register-prefetch loads (ECMG_OPT_KERNEL=0)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "kernel": "jcg K1+K2 (one CG iteration)",
-                         "bytes_per_unit": BYTES_PER_UNKNOWN_ITER, "peak_source": peak_src},
+                         "bytes_per_unit": BYTES_PER_UNKNOWN_ITER, "peak_source": peak_src,
+                         "per": "GPU (average over ranks)"},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),

@@ -102,8 +102,11 @@ typedef enum {
   ECMG_OPT_ZCHUNK = 3,       /* planes per CTA in the z-marching JCG kernels (tuning; 0 = auto) */
   ECMG_OPT_KERNEL = 4,       /* constant-coefficient JCG kernels: 1 (default) TMA-fed smem ring,
                                 0 register-prefetch loads (ablation) */
-  ECMG_OPT_GRAPH = 5         /* tolerance-stopped JCG loop: 1 (default) one CUDA graph per level with a
+  ECMG_OPT_GRAPH = 5,        /* tolerance-stopped JCG loop: 1 (default) one CUDA graph per level with a
                                 device-set conditional WHILE node; 0 host loop with batched readbacks */
+  ECMG_OPT_VIRTUAL_SLABS = 6 /* P in 2..16: run the z-slab decomposition with P slabs on this one GPU
+                                (device copies stand in for the NCCL halo messages, an in-order sum
+                                kernel for the allreduce; the multi-GPU test fixture); 0 or 1: off */
 } ecmg_option;
 int ecmg_set_option(ecmg_grid* grid, int option, int value);
 
@@ -157,9 +160,20 @@ int ecmg_run(ecmg_grid* grid, double eps, ecmg_stats* per_level, double* u_fine,
 int ecmg_apply_operator(ecmg_grid* grid, int level, const double* p, double* q);
 int ecmg_level_rhs(ecmg_grid* grid, int level, double* b, double* norm_b);
 
-/* Level geometry: cells per axis, number of nodes of the caller-visible vector, and the z-plane
- * range [z_lo, z_hi] of the nodes this rank owns (whole level for one GPU). */
+/* Level geometry: cells per axis, number of nodes of the caller-visible vector of this rank, and
+ * the half-open z node-plane range [z_lo, z_hi) it holds: the whole level [0, nz+1) on one GPU
+ * (and with virtual slabs); on NCCL ranks the rank's slab of a sharded level. */
 int ecmg_level_shape(const ecmg_grid* grid, int level, int n_cells3[3], long long* nodes, int* z_lo, int* z_hi);
+
+/* z-slab partition, a pure host function usable without a GPU: a level with
+ * n_cells_z cells is sharded over nranks iff n % (4 nranks) == 0 and n / nranks >= 16; then rank r
+ * owns node planes [r n/P, (r+1) n/P) (the last rank also plane n). Returns 1 (sharded, range
+ * filled), 0 (replicated: [0, n+1)), or ECMG_EINVAL. */
+int ecmg_slab_partition(int n_cells_z, int nranks, int rank, int* z_lo, int* z_hi);
+
+/* NCCL unique id for ecmg_dist.nccl_id: rank 0 calls this and broadcasts the 128 bytes (e.g. with
+ * torch.distributed) before every rank calls ecmg_create_grid. Errors: ECMG_ENCCL. */
+int ecmg_nccl_unique_id(unsigned char id[128]);
 
 /* Device time of the last solve's JCG iteration kernels (K1 + K2), for roofline reporting:
  * total milliseconds and number of iterations timed (CUDA events around the iteration loop). */

@@ -16,6 +16,8 @@
 #include "../../include/ecmg.h"
 #include "ecmg_internal.cuh"
 #include "problems.cuh"
+#include "host_common.h"
+#include "slab.h"
 
 using namespace ecmg;
 
@@ -60,6 +62,11 @@ struct ecmg_grid {
   double last_jcg_ms = 0.0;
   int last_jcg_iters = 0;
   long long last_free = 0;
+  // z-slabs: NCCL ranks (dist) or virtual slabs on this GPU (ECMG_OPT_VIRTUAL_SLABS)
+  int nranks = 1, rank = 0;
+  unsigned char nccl_id[128] = {0};
+  int virt_slabs = 0;
+  SlabDriver* slab = nullptr;
 };
 
 namespace {
@@ -85,97 +92,18 @@ inline int report_cuda(cudaError_t e, const char* what, int line) {
     if (e_ != cudaSuccess) return report_cuda(e_, #call, __LINE__);  \
   } while (0)
 
-bool problem_faces(int id, int face[6], double alpha[6], int* nparams_required) {
-  for (int f = 0; f < 6; ++f) { face[f] = FACE_DIRICHLET; alpha[f] = 0.0; }
-  *nparams_required = 0;
-  switch (id) {
-    case 1: case 2: case 4: case 13: case 21: case 24: break;
-    case 3: case 23: face[ZP] = FACE_ROBIN; alpha[ZP] = 1.0; break;
-    case 11: face[XP] = face[YP] = face[ZP] = FACE_ROBIN; break;   // Neumann (alpha = 0)
-    case 12: face[XP] = face[YP] = FACE_ROBIN; break;
-    case 5: *nparams_required = 48; break;
-    case 22: *nparams_required = 15; break;
-    default: return false;
-  }
-  return true;
-}
-
-LevelGeom make_geom(const ecmg_grid* G, int k, const int face[6], int elem_path) {
-  LevelGeom g{};
-  for (int d = 0; d < 3; ++d) {
-    g.n[d] = G->n0[d] << k;
-    g.lo[d] = G->dom.lo[d];
-    g.h[d] = (G->dom.hi[d] - G->dom.lo[d]) / g.n[d];
-    const int lo = face[2 * d] == FACE_DIRICHLET ? 1 : 0;
-    const int hi = face[2 * d + 1] == FACE_DIRICHLET ? g.n[d] - 1 : g.n[d];
-    g.flo[d] = lo;
-    g.nf[d] = std::max(0, hi - lo + 1);
-  }
-  g.P = ((long long)std::max(1, g.nf[0]) + 31) / 32 * 32;
-  g.S = g.P * std::max(1, g.nf[1]);
-  g.BP = g.n[0] + 4;
-  g.BS = g.BP * (g.n[1] + 4);
-  g.elem_path = elem_path;
-  return g;
-}
-
-ElemStencil make_elem_stencil(const LevelGeom& g, const Problem& pb, int precond) {
-  ElemStencil es{};
-  const double V = g.h[0] * g.h[1] * g.h[2];
-  for (int pat = 0; pat < 8; ++pat) {
-    double s = 0.0;
-    for (int d = 0; d < 3; ++d) {
-      double t = ((pat >> d) & 1) ? -1.0 : 1.0;
-      t /= g.h[d] * g.h[d];
-      for (int e = 0; e < 3; ++e)
-        if (e != d) t *= ((pat >> e) & 1) ? (1.0 / 6.0) : (1.0 / 3.0);
-      s += t;
-    }
-    es.kappa[pat] = V * s;
-  }
-  for (int F = 0; F < 6; ++F) {
-    const int d = F >> 1;
-    const int d1 = (d == 0) ? 1 : 0, d2 = (d == 2) ? 1 : 2;
-    es.robin[F] = (pb.face[F] == FACE_ROBIN && pb.alpha[F] != 0.0) ? pb.alpha[F] * g.h[d1] * g.h[d2] : 0.0;
-  }
-  es.precond = precond;
-  return es;
-}
-
-ConstStencil make_const_stencil(const LevelGeom& g, double beta, int precond) {
-  // c(o) = beta * sum_d K_d(o_d) prod_{e != d} M_e(o_e); K(0) = 2/h, K(1) = -1/h, M(0) = 2h/3, M(1) = h/6
-  auto K = [](double h, int o) { return o ? -1.0 / h : 2.0 / h; };
-  auto M = [](double h, int o) { return o ? h / 6.0 : 2.0 * h / 3.0; };
-  auto c = [&](int ox, int oy, int oz) {
-    const int o[3] = {ox, oy, oz};
-    double s = 0.0;
-    for (int d = 0; d < 3; ++d) {
-      double t = K(g.h[d], o[d]);
-      for (int e = 0; e < 3; ++e)
-        if (e != d) t *= M(g.h[e], o[e]);
-      s += t;
-    }
-    return beta * s;
-  };
-  ConstStencil cs{};
-  for (int oz = 0; oz < 2; ++oz) {
-    cs.c0[oz] = c(0, 0, oz);
-    cs.cx[oz] = c(1, 0, oz);
-    cs.cy[oz] = c(0, 1, oz);
-    cs.cd[oz] = c(1, 1, oz);
-  }
-  cs.dinv = precond ? 1.0 / c(0, 0, 0) : 1.0;
-  return cs;
-}
-
-int auto_zc(const ecmg_grid* G, const LevelGeom& g) {
-  if (G->zchunk > 0) return G->zchunk;
-  const int ty = G->elem_path ? 8 : 32;
-  const long long tiles = (long long)((g.nf[0] + 31) / 32) * ((g.nf[1] + ty - 1) / ty);
-  const long long target = 148LL * 2 * 2;
-  long long nchunks = (target + tiles - 1) / tiles;
-  nchunks = std::max(1LL, std::min(nchunks, (long long)std::max(1, g.nf[2] / 4)));
-  return (int)((g.nf[2] + nchunks - 1) / nchunks);
+SlabCfg slab_cfg(const ecmg_grid* G) {
+  SlabCfg c{};
+  c.dom = G->dom;
+  for (int d = 0; d < 3; ++d) c.n0[d] = G->n0[d];
+  c.L = G->L;
+  c.prob = G->prob;
+  c.elem_path = G->elem_path;
+  c.exp_variant = G->exp_variant;
+  c.precond = G->precond;
+  c.kernel_variant = G->kernel_variant;
+  c.zchunk = G->zchunk;
+  return c;
 }
 
 // TMA descriptors of the free-box work vectors for one level (cached; rebuilt when the level changes)
@@ -240,7 +168,6 @@ int setup_level(ecmg_grid* G, int k) {
   return ECMG_OK;
 }
 
-long long free_count(const LevelGeom& g) { return (long long)g.nf[0] * g.nf[1] * g.nf[2]; }
 
 int fill_stats(ecmg_grid* G, const LevelGeom& g, double eps, ecmg_stats* st) {
   const JcgScalars s = G->sc_host[0];
@@ -274,7 +201,7 @@ cudaError_t build_level_graph(ecmg_grid* G, int k, cudaGraphExec_t* out) {
   cudaGraphConditionalHandle h;
   e = cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault);
   KArgs a{};
-  a.partials = G->partials; a.sc = G->sc; a.zc = auto_zc(G, g); a.beta = G->beta;
+  a.partials = G->partials; a.sc = G->sc; a.zc = auto_zc(G->zchunk, G->elem_path, g); a.beta = G->beta;
   a.cond = h; a.use_cond = 1;
   const long long launches_before = ecmg_kernel_launches();
   cudaStream_t user = G->stream;
@@ -350,7 +277,7 @@ int run_jcg(ecmg_grid* G, int k, double eps, int max_iter, ecmg_stats* st) {
   KArgs a{};
   a.partials = G->partials;
   a.sc = G->sc;
-  a.zc = auto_zc(G, g);
+  a.zc = auto_zc(G->zchunk, G->elem_path, g);
   a.beta = G->beta;
   // eps and max_iter reach the init pass through the device scalars
   G->param_host->eps = eps;
@@ -421,7 +348,6 @@ bool is_device_ptr(const void* p) {
   return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
-long long level_nodes(const LevelGeom& g) { return (long long)(g.n[0] + 1) * (g.n[1] + 1) * (g.n[2] + 1); }
 
 float elapsed(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0.f;
@@ -434,6 +360,16 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
 extern "C" {
 
 long long ecmg_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
+
+int ecmg_slab_partition(int n_cells_z, int nranks, int rank, int* z_lo, int* z_hi) {
+  if (n_cells_z < 1 || nranks < 1 || rank < 0 || rank >= nranks || !z_lo || !z_hi) return ECMG_EINVAL;
+  return slab_partition(n_cells_z, nranks, rank, z_lo, z_hi) ? 1 : 0;
+}
+
+int ecmg_nccl_unique_id(unsigned char id[128]) {
+  if (!id) return ECMG_EINVAL;
+  return nccl_unique_id(id);
+}
 
 const char* ecmg_strerror(int s) {
   switch (s) {
@@ -455,7 +391,7 @@ int ecmg_create_grid(const ecmg_box* dom, const int coarsest_cells[3], int num_l
   if (!out) return ECMG_EINVAL;
   *out = nullptr;
   if (!dom || !coarsest_cells || num_levels < 3 || num_levels > 12) return ECMG_EINVAL;
-  if (dist && dist->nranks > 1) return ECMG_EINVAL;   // z-slab multi-GPU: see DESIGN.md (NEXT)
+  if (dist && (dist->nranks < 1 || dist->nranks > 16 || dist->rank < 0 || dist->rank >= dist->nranks)) return ECMG_EINVAL;
   for (int d = 0; d < 3; ++d) {
     if (!(dom->hi[d] > dom->lo[d]) || coarsest_cells[d] < 1) return ECMG_EINVAL;
     if ((long long)coarsest_cells[d] << (num_levels - 1) > 8192) return ECMG_EINVAL;
@@ -471,7 +407,9 @@ int ecmg_create_grid(const ecmg_box* dom, const int coarsest_cells[3], int num_l
   G->L = num_levels;
   // size workspace for the finest level with the largest possible free box (no Dirichlet faces)
   int face_none[6] = {FACE_ROBIN, FACE_ROBIN, FACE_ROBIN, FACE_ROBIN, FACE_ROBIN, FACE_ROBIN};
-  LevelGeom gmax = make_geom(G, num_levels - 1, face_none, 1);
+  // NCCL ranks keep their work vectors in the slab driver: size the single-GPU workspace minimally
+  const int size_level = (dist && dist->nranks > 1) ? 0 : num_levels - 1;
+  LevelGeom gmax = make_geom(*dom, coarsest_cells, size_level, face_none, 1);
   G->vec_doubles = gmax.S * gmax.nf[2] + 64;
   G->beta_doubles = (long long)(gmax.n[0] + 4) * (gmax.n[1] + 4) * (gmax.n[2] + 4);
   const long long rhs_blocks = (long long)((gmax.nf[0] + 7) / 8) * ((gmax.nf[1] + 7) / 8) * ((gmax.nf[2] + 3) / 4);
@@ -505,6 +443,20 @@ int ecmg_create_grid(const ecmg_box* dom, const int coarsest_cells[3], int num_l
     G->ev_init = true;
   }
   if (st == ECMG_OK && cudaStreamSynchronize(G->stream) != cudaSuccess) st = ECMG_ECUDA;
+  if (st == ECMG_OK && dist && dist->nranks > 1) {
+    // NCCL ranks: the communicator is created here (collective over all ranks)
+    G->nranks = dist->nranks;
+    G->rank = dist->rank;
+    std::memcpy(G->nccl_id, dist->nccl_id, 128);
+    int face_d[6] = {0, 0, 0, 0, 0, 0};
+    for (int f = 0; f < 6; ++f) G->prob.face[f] = face_d[f];
+    G->prob.id = 1;
+    G->geom.clear();
+    for (int k = 0; k < G->L; ++k) G->geom.push_back(make_geom(G->dom, G->n0, k, face_d, 0));
+    int s2 = ECMG_OK;
+    G->slab = slab_driver_create(slab_cfg(G), G->nranks, G->rank, false, G->nccl_id, &s2);
+    if (!G->slab) st = s2;
+  }
   if (st != ECMG_OK) { cudaGetLastError(); ecmg_destroy_grid(G); return st; }
   *out = G;
   return ECMG_OK;
@@ -513,6 +465,7 @@ int ecmg_create_grid(const ecmg_box* dom, const int coarsest_cells[3], int num_l
 int ecmg_destroy_grid(ecmg_grid* G) {
   if (!G) return ECMG_EINVAL;
   if (G->stream) cudaStreamSynchronize(G->stream); else cudaDeviceSynchronize();
+  if (G->slab) slab_driver_destroy(G->slab);
   cudaFree(G->x); cudaFree(G->r); cudaFree(G->p[0]); cudaFree(G->p[1]); cudaFree(G->b);
   cudaFree(G->beta); cudaFree(G->partials); cudaFree(G->sc);
   for (double* p : G->u) cudaFree(p);
@@ -557,11 +510,12 @@ int ecmg_set_coeffs(ecmg_grid* G, const ecmg_problem* pr) {
   G->prob = pb;
   G->elem_path = elem_path;
   G->geom.clear();
-  for (int k = 0; k < G->L; ++k) G->geom.push_back(make_geom(G, k, pb.face, elem_path));
+  for (int k = 0; k < G->L; ++k) G->geom.push_back(make_geom(G->dom, G->n0, k, pb.face, elem_path));
   G->has_problem = true;
   G->setup_level = -1;
   G->maps.level = -1;
   clear_graphs(G);
+  if (G->slab) slab_driver_configure(G->slab, slab_cfg(G));
   return ECMG_OK;
 }
 
@@ -573,8 +527,20 @@ int ecmg_set_option(ecmg_grid* G, int option, int value) {
     case ECMG_OPT_ZCHUNK: if (value < 0) return ECMG_EINVAL; G->zchunk = value; clear_graphs(G); break;
     case ECMG_OPT_KERNEL: if (value != 0 && value != 1) return ECMG_EINVAL; G->kernel_variant = value; clear_graphs(G); break;
     case ECMG_OPT_GRAPH: if (value != 0 && value != 1) return ECMG_EINVAL; G->use_graph = value; break;
+    case ECMG_OPT_VIRTUAL_SLABS: {
+      if (value < 0 || value > 16 || G->nranks > 1) return ECMG_EINVAL;
+      if (G->slab) { slab_driver_destroy(G->slab); G->slab = nullptr; }
+      G->virt_slabs = value > 1 ? value : 0;
+      if (G->virt_slabs) {
+        int s2 = ECMG_OK;
+        G->slab = slab_driver_create(slab_cfg(G), G->virt_slabs, 0, true, nullptr, &s2);
+        if (!G->slab) { G->virt_slabs = 0; return s2; }
+      }
+      return ECMG_OK;
+    }
     default: return ECMG_EINVAL;
   }
+  if (G->slab) slab_driver_configure(G->slab, slab_cfg(G));
   return ECMG_OK;
 }
 
@@ -582,15 +548,23 @@ int ecmg_level_shape(const ecmg_grid* G, int level, int n_cells3[3], long long* 
   if (!G || level < 0 || level >= G->L) return ECMG_EINVAL;
   int n[3];
   for (int d = 0; d < 3; ++d) n[d] = G->n0[d] << level;
+  int zlo = 0, zhi = n[2] + 1;
+  if (G->slab && G->has_problem) slab_level_range(G->slab, level, &zlo, &zhi);
   if (n_cells3) for (int d = 0; d < 3; ++d) n_cells3[d] = n[d];
-  if (nodes) *nodes = (long long)(n[0] + 1) * (n[1] + 1) * (n[2] + 1);
-  if (z_lo) *z_lo = 0;
-  if (z_hi) *z_hi = n[2];
+  if (nodes) *nodes = (long long)(n[0] + 1) * (n[1] + 1) * (zhi - zlo);
+  if (z_lo) *z_lo = zlo;
+  if (z_hi) *z_hi = zhi;
   return ECMG_OK;
 }
 
 int ecmg_solve_level(ecmg_grid* G, int level, double eps, int max_iter, double* u, ecmg_stats* stats) {
   if (!G || !u || !G->has_problem || level < 0 || level >= G->L) return ECMG_EINVAL;
+  if (G->slab) {
+    ecmg_stats tmp{};
+    const int s = slab_solve_level(G->slab, level, eps, max_iter, u, stats ? stats : &tmp, G->stream);
+    slab_last_timing(G->slab, &G->last_jcg_ms, &G->last_jcg_iters, &G->last_free);
+    return s;
+  }
   const LevelGeom& g = G->geom[level];
   ECMG_CUDA(cudaEventRecord(G->ev[4], G->stream));
   if (G->setup_level != level) { int s = setup_level(G, level); if (s) return s; }
@@ -611,7 +585,7 @@ int ecmg_solve_level(ecmg_grid* G, int level, double eps, int max_iter, double* 
 }
 
 int ecmg_prolongate_extrapolate(ecmg_grid* G, int level, const double* u2h, const double* u4h, double* w) {
-  if (!G || !u2h || !u4h || !w || !G->has_problem || level < 2 || level >= G->L) return ECMG_EINVAL;
+  if (!G || !u2h || !u4h || !w || !G->has_problem || level < 2 || level >= G->L || G->nranks > 1) return ECMG_EINVAL;
   const LevelGeom& g = G->geom[level];
   for (int d = 0; d < 3; ++d) if (g.n[d] % 4) return ECMG_EMISMATCH;
   ECMG_CUDA(launch_exp_finite(g, G->prob, u2h, u4h, w, G->exp_variant, G->seeds, 0, G->stream));
@@ -620,7 +594,7 @@ int ecmg_prolongate_extrapolate(ecmg_grid* G, int level, const double* u2h, cons
 }
 
 int ecmg_richardson(ecmg_grid* G, int level, const double* uh, const double* u2h, double* ut) {
-  if (!G || !uh || !u2h || !ut || !G->has_problem || level < 1 || level >= G->L) return ECMG_EINVAL;
+  if (!G || !uh || !u2h || !ut || !G->has_problem || level < 1 || level >= G->L || G->nranks > 1) return ECMG_EINVAL;
   const LevelGeom& g = G->geom[level];
   for (int d = 0; d < 3; ++d) if (g.n[d] % 2) return ECMG_EMISMATCH;
   ECMG_CUDA(launch_exp_true(g, G->prob, uh, u2h, ut, G->stream));
@@ -629,12 +603,12 @@ int ecmg_richardson(ecmg_grid* G, int level, const double* uh, const double* u2h
 }
 
 int ecmg_apply_operator(ecmg_grid* G, int level, const double* p, double* q) {
-  if (!G || !p || !q || !G->has_problem || level < 0 || level >= G->L) return ECMG_EINVAL;
+  if (!G || !p || !q || !G->has_problem || level < 0 || level >= G->L || G->nranks > 1) return ECMG_EINVAL;
   const LevelGeom& g = G->geom[level];
   if (G->elem_path && G->setup_level != level) { int s = setup_level(G, level); if (s) return s; }
   ECMG_CUDA(launch_gather(g, p, G->p[0], G->stream));
   KArgs a{};
-  a.partials = G->partials; a.sc = G->sc; a.zc = auto_zc(G, g); a.beta = G->beta;
+  a.partials = G->partials; a.sc = G->sc; a.zc = auto_zc(G->zchunk, G->elem_path, g); a.beta = G->beta;
   a.h0 = G->p[0]; a.o0 = G->r;
   ECMG_CUDA(launch_mode(G, MODE_APPLY, g, a));
   ECMG_CUDA(cudaMemsetAsync(q, 0, sizeof(double) * level_nodes(g), G->stream));
@@ -644,7 +618,7 @@ int ecmg_apply_operator(ecmg_grid* G, int level, const double* p, double* q) {
 }
 
 int ecmg_level_rhs(ecmg_grid* G, int level, double* bout, double* norm_b) {
-  if (!G || !bout || !G->has_problem || level < 0 || level >= G->L) return ECMG_EINVAL;
+  if (!G || !bout || !G->has_problem || level < 0 || level >= G->L || G->nranks > 1) return ECMG_EINVAL;
   const LevelGeom& g = G->geom[level];
   if (G->setup_level != level) { int s = setup_level(G, level); if (s) return s; }
   ECMG_CUDA(cudaMemsetAsync(bout, 0, sizeof(double) * level_nodes(g), G->stream));
@@ -653,7 +627,7 @@ int ecmg_level_rhs(ecmg_grid* G, int level, double* bout, double* norm_b) {
   ECMG_CUDA(launch_zero_vec(g, G->x, G->stream));
   {
     KArgs a{};
-    a.partials = G->partials; a.sc = G->sc; a.zc = auto_zc(G, g); a.beta = G->beta;
+    a.partials = G->partials; a.sc = G->sc; a.zc = auto_zc(G->zchunk, G->elem_path, g); a.beta = G->beta;
     a.h0 = G->x; a.i0 = G->b; a.o0 = G->r; a.eps = 0.0; a.max_iter = 0;
     ECMG_CUDA(launch_mode(G, MODE_INIT, g, a));
   }
@@ -675,6 +649,14 @@ int ecmg_run(ecmg_grid* G, double eps, ecmg_stats* per_level, double* u_fine, do
   if (!G || !G->has_problem || !u_fine) return ECMG_EINVAL;
   for (int k = 2; k < G->L; ++k)
     for (int d = 0; d < 3; ++d) if (G->geom[k].n[d] % 4) return ECMG_EMISMATCH;
+  if (G->slab) {
+    std::vector<ecmg_stats> stv(G->L);
+    const int s = slab_run(G->slab, eps, stv.data(), u_fine, is_device_ptr(u_fine), ut_fine,
+                           ut_fine ? is_device_ptr(ut_fine) : false, G->stream);
+    slab_last_timing(G->slab, &G->last_jcg_ms, &G->last_jcg_iters, &G->last_free);
+    if (per_level) for (int k = 0; k < G->L; ++k) per_level[k] = stv[k];
+    return s;
+  }
   if ((int)G->u.size() != G->L) {
     for (double* p : G->u) cudaFree(p);
     G->u.assign(G->L, nullptr);

@@ -38,6 +38,11 @@ struct LevelGeom {
   long long P, S;    // free-box vector row pitch / plane stride (doubles)
   long long BP, BS;  // element-beta row pitch / plane stride (doubles), zero ring of 2
   int elem_path;     // 1: element-beta stencil (variable beta or Robin faces); 0: constant stencil
+  // z-slab decomposition (one GPU: zoff = 0, zbeg = 0, zend = nza = nf[2], zlo = 0, zhi = n[2] + 1)
+  int zoff;          // global free-z index of local work-vector plane 0
+  int zbeg, zend;    // local work-vector planes this rank computes, [zbeg, zend)
+  int nza;           // allocated local work-vector planes (owned + halo planes)
+  int zlo, zhi;      // global node planes [zlo, zhi) this rank owns in full-layout nodal vectors
 };
 
 // Constant-coefficient 27-point stencil (beta constant, all faces Dirichlet):
@@ -72,6 +77,8 @@ struct JcgScalars {
   int iter, max_iter, done, status;
   unsigned int counter;   // last-block-done counter (reset by the last block)
   int pad_;
+  double loc[3];     // z-slabs: this slab's partial dot products (before the allreduce)
+  double glob[3];    // z-slabs: allreduced dot products (input of the finalize pass)
 };
 
 enum KMode { MODE_K1 = 1, MODE_K2 = 2, MODE_INIT = 3, MODE_TRUE = 4, MODE_APPLY = 5 };
@@ -91,6 +98,7 @@ struct KArgs {
   int max_iter;
   cudaGraphConditionalHandle cond;   // CUDA-graph WHILE condition (device-driven JCG loop)
   int use_cond;                      // 1: the init / K2 passes set `cond` = !done
+  int local_only;                    // z-slabs: write this slab's sums to sc->loc, finalize later
 };
 
 // status codes (mirror of ecmg_status)
@@ -111,6 +119,11 @@ namespace ecmg {
 cudaError_t launch_jcg_const_tma(int mode, const LevelGeom& g, const ConstStencil& cs, const KArgs& a,
                                  const CUtensorMap* maps, cudaStream_t st);
 int make_vec_tensor_map(CUtensorMap* map, const double* base, const LevelGeom& g, int bx, int by);
+// z-slabs: finalize pass after the allreduce, and the in-order sum of P slabs' partial dots
+// (virtual slabs on one GPU; NCCL's allreduce on real ranks)
+cudaError_t launch_finalize(int mode, const KArgs& a, cudaStream_t st);
+struct SlabScalars { JcgScalars* p[16]; int n; };
+cudaError_t launch_vsum(const SlabScalars& s, cudaStream_t st);
 cudaError_t init_tma_kernel_attributes();
 cudaError_t init_elem_kernel_attributes();
 cudaError_t init_setup_kernel_attributes();

@@ -1,0 +1,587 @@
+// ecmg_slab.cu -- z-slab domain decomposition of the ECMG_jcg hot path.
+//
+// Levels whose z extent n satisfies n % (4P) == 0 and n / P >= 16 are sharded in z-slabs of node
+// planes (slab_partition, host_common.h); smaller levels are replicated (solved identically by
+// every rank, no communication). On a sharded level a rank holds:
+//  * JCG work vectors x, r, p, p', b over its owned free planes plus one halo plane per side;
+//  * full-layout per-level nodal vectors u_k, of which it fills its owned planes and one upper halo
+//    plane (EXP_finite of the next level and EXP_true read at most that plane; the partition nests
+//    across levels because slab boundaries are multiples of 4 fine planes).
+// Per JCG iteration (Alg. 4 l.7-9, textbook PCG): K1 (local sums) -> allreduce(sigma) -> finalize ->
+// K2 (local sums) -> allreduce(rho', rr) -> finalize -> halo exchange of r. K1 recomputes p on its
+// halo planes from r and p_old there, so p never travels. Every rank sees the same allreduced
+// scalars, so all ranks stop at the same iteration and issue the same communication sequence.
+//
+// Communication backends behind one interface:
+//  * NCCL (real ranks, one GPU each): ncclAllReduce of the 3 scalars, grouped ncclSend / ncclRecv
+//    of contiguous halo planes over NVLink. libnccl is the one PyTorch already loaded (dlopen).
+//  * virtual slabs (all P slabs in one process on one GPU): the halo "messages" are device copies
+//    and the allreduce is an in-order sum kernel. This is the test fixture that
+//    runs the exact slab arithmetic on one GPU; no kernel ever waits on another.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "host_common.h"
+#include "slab.h"
+
+namespace ecmg {
+
+// ---- NCCL through dlopen ----------------------------------------------------------------------
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+};
+
+static NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api;
+  tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOLOAD | RTLD_LAZY);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_LAZY);
+  if (!h) return api;
+  api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+  api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+  api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+  api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+  api.Send = (decltype(api.Send))dlsym(h, "ncclSend");
+  api.Recv = (decltype(api.Recv))dlsym(h, "ncclRecv");
+  api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
+  api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
+  api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.Send && api.Recv &&
+           api.GroupStart && api.GroupEnd;
+  return api;
+}
+
+int nccl_unique_id(unsigned char id[128]) {
+  NcclApi& n = nccl();
+  if (!n.ok) return ECMG_ENCCL;
+  ncclUniqueId u;
+  if (n.GetUniqueId(&u) != ncclSuccess) return ECMG_ENCCL;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(id, &u, 128);
+  return ECMG_OK;
+}
+
+// ---- one slab's device state ------------------------------------------------------------------
+struct SlabCtx {
+  int rank = 0;
+  std::vector<LevelGeom> geom;
+  std::vector<char> sharded;
+  double* x = nullptr;
+  double* r = nullptr;
+  double* p[2] = {nullptr, nullptr};
+  double* b = nullptr;
+  double* beta = nullptr;
+  double* partials = nullptr;
+  double* scratch1d = nullptr;
+  double* seeds = nullptr;
+  JcgScalars* sc = nullptr;
+  std::vector<double*> u;    // full-layout per level
+  double* ut = nullptr;      // full-layout finest u~ scratch
+  int maps_level = -1;
+  bool maps_ok = false;
+  CUtensorMap xh, xi, rh, ri, ph[2], bi;
+};
+
+struct SlabDriver {
+  int P = 1, rank = 0;
+  bool virt = false;
+  std::vector<SlabCtx> s;    // local slabs: all P (virtual) or this rank's one (NCCL)
+  ncclComm_t comm = nullptr;
+  JcgScalars* sc_host = nullptr;
+  struct ParamHost { double eps; int max_iter; int pad; }* param_host = nullptr;
+  cudaEvent_t ev[4];
+  SlabCfg cfg{};
+  int L = 0;
+  double last_jcg_ms = 0.0;
+  int last_jcg_iters = 0;
+  long long last_free = 0;
+};
+
+namespace {
+
+#define SL_CUDA(call)                                   \
+  do {                                                  \
+    cudaError_t e_ = (call);                            \
+    if (e_ != cudaSuccess) {                            \
+      if (std::getenv("ECMG_DEBUG"))                    \
+        std::fprintf(stderr, "libecmg(slab): %s: %s\n", #call, cudaGetErrorString(e_)); \
+      return e_ == cudaErrorMemoryAllocation ? ECMG_ENOMEM : ECMG_ECUDA; \
+    }                                                   \
+  } while (0)
+#define SL_NCCL(call)                                   \
+  do {                                                  \
+    if ((call) != ncclSuccess) return ECMG_ENCCL;       \
+  } while (0)
+
+// ---- communication ---------------------------------------------------------------------------
+int comm_allreduce(SlabDriver* d, cudaStream_t st) {
+  if (d->virt) {
+    SlabScalars ss{};
+    ss.n = (int)d->s.size();
+    for (int i = 0; i < ss.n; ++i) ss.p[i] = d->s[i].sc;
+    SL_CUDA(launch_vsum(ss, st));
+    return ECMG_OK;
+  }
+  NcclApi& n = nccl();
+  SlabCtx& c = d->s[0];
+  SL_NCCL(n.AllReduce(c.sc->loc, c.sc->glob, 3, ncclDouble, ncclSum, d->comm, st));
+  return ECMG_OK;
+}
+
+// halo planes of a work vector (which: 0 = x, 1 = r) on sharded level k
+int comm_halo(SlabDriver* d, int k, int which, cudaStream_t st) {
+  auto vec = [&](SlabCtx& c) { return which == 0 ? c.x : c.r; };
+  if (d->virt) {
+    for (size_t i = 0; i + 1 < d->s.size(); ++i) {
+      SlabCtx& lo = d->s[i];
+      SlabCtx& hi = d->s[i + 1];
+      const LevelGeom& gl = lo.geom[k];
+      const LevelGeom& gh = hi.geom[k];
+      const size_t bytes = sizeof(double) * gl.S;
+      SL_CUDA(cudaMemcpyAsync(vec(hi) + (long long)(gh.zbeg - 1) * gh.S, vec(lo) + (long long)(gl.zend - 1) * gl.S, bytes,
+                              cudaMemcpyDeviceToDevice, st));
+      SL_CUDA(cudaMemcpyAsync(vec(lo) + (long long)gl.zend * gl.S, vec(hi) + (long long)gh.zbeg * gh.S, bytes,
+                              cudaMemcpyDeviceToDevice, st));
+    }
+    return ECMG_OK;
+  }
+  NcclApi& n = nccl();
+  SlabCtx& c = d->s[0];
+  const LevelGeom& g = c.geom[k];
+  double* v = vec(c);
+  const size_t cnt = (size_t)g.S;
+  SL_NCCL(n.GroupStart());
+  if (d->rank > 0) {
+    SL_NCCL(n.Send(v + (long long)g.zbeg * g.S, cnt, ncclDouble, d->rank - 1, d->comm, st));
+    SL_NCCL(n.Recv(v + (long long)(g.zbeg - 1) * g.S, cnt, ncclDouble, d->rank - 1, d->comm, st));
+  }
+  if (d->rank < d->P - 1) {
+    SL_NCCL(n.Send(v + (long long)(g.zend - 1) * g.S, cnt, ncclDouble, d->rank + 1, d->comm, st));
+    SL_NCCL(n.Recv(v + (long long)g.zend * g.S, cnt, ncclDouble, d->rank + 1, d->comm, st));
+  }
+  SL_NCCL(n.GroupEnd());
+  return ECMG_OK;
+}
+
+// upper halo plane of the full-layout u_k: rank r's first owned plane goes to rank r-1
+int comm_u_halo(SlabDriver* d, int k, cudaStream_t st) {
+  if (d->virt) {
+    for (size_t i = 0; i + 1 < d->s.size(); ++i) {
+      const LevelGeom& gh = d->s[i + 1].geom[k];
+      const long long pl = (long long)(gh.n[0] + 1) * (gh.n[1] + 1);
+      SL_CUDA(cudaMemcpyAsync(d->s[i].u[k] + gh.zlo * pl, d->s[i + 1].u[k] + gh.zlo * pl, sizeof(double) * pl,
+                              cudaMemcpyDeviceToDevice, st));
+    }
+    return ECMG_OK;
+  }
+  NcclApi& n = nccl();
+  SlabCtx& c = d->s[0];
+  const LevelGeom& g = c.geom[k];
+  const long long pl = (long long)(g.n[0] + 1) * (g.n[1] + 1);
+  SL_NCCL(n.GroupStart());
+  if (d->rank > 0) SL_NCCL(n.Send(c.u[k] + g.zlo * pl, (size_t)pl, ncclDouble, d->rank - 1, d->comm, st));
+  if (d->rank < d->P - 1) SL_NCCL(n.Recv(c.u[k] + g.zhi * pl, (size_t)pl, ncclDouble, d->rank + 1, d->comm, st));
+  SL_NCCL(n.GroupEnd());
+  return ECMG_OK;
+}
+
+// ---- per-slab kernels ------------------------------------------------------------------------
+bool slab_maps(SlabDriver* d, SlabCtx& c, int k) {
+  if (c.maps_level == k) return c.maps_ok;
+  const LevelGeom& g = c.geom[k];
+  const int hx = tma_halo_box_x(), hy = tma_halo_box_y(), ix = tma_int_box_x(), iy = tma_int_box_y();
+  c.maps_ok = make_vec_tensor_map(&c.xh, c.x, g, hx, hy) == 0 && make_vec_tensor_map(&c.xi, c.x, g, ix, iy) == 0 &&
+              make_vec_tensor_map(&c.rh, c.r, g, hx, hy) == 0 && make_vec_tensor_map(&c.ri, c.r, g, ix, iy) == 0 &&
+              make_vec_tensor_map(&c.ph[0], c.p[0], g, hx, hy) == 0 &&
+              make_vec_tensor_map(&c.ph[1], c.p[1], g, hx, hy) == 0 && make_vec_tensor_map(&c.bi, c.b, g, ix, iy) == 0;
+  c.maps_level = k;
+  (void)d;
+  return c.maps_ok;
+}
+
+cudaError_t slab_launch(SlabDriver* d, SlabCtx& c, int mode, int k, const KArgs& a, cudaStream_t st) {
+  const SlabCfg& cf = d->cfg;
+  const LevelGeom& g = c.geom[k];
+  if (cf.elem_path) return launch_jcg_elem(mode, g, make_elem_stencil(g, cf.prob, cf.precond), cf.prob, a, st);
+  const ConstStencil cs = make_const_stencil(g, 1.0, cf.precond);
+  if (cf.kernel_variant == 1 && slab_maps(d, c, k)) {
+    auto halo = [&](const double* p) -> const CUtensorMap* {
+      if (p == c.x) return &c.xh;
+      if (p == c.r) return &c.rh;
+      if (p == c.p[0]) return &c.ph[0];
+      if (p == c.p[1]) return &c.ph[1];
+      return nullptr;
+    };
+    auto inter = [&](const double* p) -> const CUtensorMap* {
+      if (p == c.x) return &c.xi;
+      if (p == c.r) return &c.ri;
+      if (p == c.b) return &c.bi;
+      return nullptr;
+    };
+    const CUtensorMap* h0 = halo(a.h0);
+    const CUtensorMap* h1 = a.h1 ? halo(a.h1) : h0;
+    const CUtensorMap* i0 = a.i0 ? inter(a.i0) : h0;
+    const CUtensorMap* i1 = a.i1 ? inter(a.i1) : h0;
+    if (h0 && h1 && i0 && i1) {
+      CUtensorMap m[4] = {*h0, *h1, *i0, *i1};
+      return launch_jcg_const_tma(mode, g, cs, a, m, st);
+    }
+  }
+  return launch_jcg_const(mode, g, cs, a, st);
+}
+
+KArgs base_args(SlabDriver* d, SlabCtx& c, int k, bool local_only) {
+  KArgs a{};
+  a.partials = c.partials;
+  a.sc = c.sc;
+  a.zc = auto_zc(d->cfg.zchunk, d->cfg.elem_path, c.geom[k]);
+  a.beta = c.beta;
+  a.local_only = local_only ? 1 : 0;
+  return a;
+}
+
+int setup_slab_level(SlabDriver* d, SlabCtx& c, int k, cudaStream_t st) {
+  const SlabCfg& cf = d->cfg;
+  const LevelGeom& g = c.geom[k];
+  const ElemStencil es = make_elem_stencil(g, cf.prob, cf.precond);
+  if (cf.elem_path) SL_CUDA(launch_beta(g, cf.prob, c.beta, st));
+  SL_CUDA(launch_rhs(g, cf.prob, es, 1.0, cf.elem_path ? c.beta : nullptr, c.b, c.scratch1d, st));
+  return ECMG_OK;
+}
+
+int read_stats(SlabDriver* d, int k, double eps, ecmg_stats* st, cudaStream_t stream) {
+  SL_CUDA(cudaMemcpyAsync(d->sc_host, d->s[0].sc, sizeof(JcgScalars), cudaMemcpyDeviceToHost, stream));
+  SL_CUDA(cudaStreamSynchronize(stream));
+  const JcgScalars s = *d->sc_host;
+  d->last_jcg_iters = s.iter;
+  long long nfree = 0;
+  for (auto& c : d->s) nfree += free_count(c.geom[k]);
+  d->last_free = nfree;
+  const double nb = std::sqrt(s.bb), nbe = nb > 0.0 ? nb : 1.0;
+  int status = s.status;
+  const bool conv = (eps <= 0.0) || !(std::sqrt(s.rr) > eps * nbe);
+  if (status == ECMG_OK && !conv) status = ECMG_ENOTCONV;
+  if (st) {
+    st->iterations = s.iter;
+    st->rel_res_recur = std::sqrt(s.rr) / nbe;
+    st->rel_res_true = std::sqrt(s.rr_true) / nbe;
+    st->norm_b = nb;
+    st->converged = conv && status == ECMG_OK;
+    st->status = status;
+  }
+  return status;
+}
+
+// JCG on a level. Sharded: all local slabs, allreduce + halo exchange per pass. Replicated: slab 0
+// (virtual) or this rank (NCCL) solves the whole level with no communication.
+int slab_jcg(SlabDriver* d, int k, double eps, int max_iter, ecmg_stats* st, cudaStream_t stream) {
+  if (max_iter <= 0 && eps > 0) max_iter = 10000;
+  if (max_iter < 0) max_iter = 0;
+  const bool sh = d->s[0].sharded[k];
+  const int nloc = (sh || !d->virt) ? (int)d->s.size() : 1;
+  d->param_host->eps = eps;
+  d->param_host->max_iter = max_iter;
+  for (int i = 0; i < nloc; ++i)
+    SL_CUDA(cudaMemcpyAsync(&d->s[i].sc->eps_in, d->param_host, sizeof(double) + sizeof(int), cudaMemcpyHostToDevice, stream));
+  // one pass of `mode` over all local slabs (+ allreduce and finalize when sharded)
+  auto pass = [&](int mode, auto fill) -> int {
+    for (int i = 0; i < nloc; ++i) {
+      KArgs a = base_args(d, d->s[i], k, sh);
+      fill(d->s[i], a);
+      SL_CUDA(slab_launch(d, d->s[i], mode, k, a, stream));
+    }
+    if (sh) {
+      int r = comm_allreduce(d, stream);
+      if (r) return r;
+      for (int i = 0; i < nloc; ++i) SL_CUDA(launch_finalize(mode, base_args(d, d->s[i], k, sh), stream));
+    }
+    return ECMG_OK;
+  };
+  int rc;
+  if (sh) {
+    // halo planes at the global z boundary stand for Dirichlet / outside nodes: they must read as 0
+    // (the buffers were used by earlier levels with other geometries)
+    for (int i = 0; i < nloc; ++i) {
+      SlabCtx& c = d->s[i];
+      const LevelGeom& g = c.geom[k];
+      const size_t plane = sizeof(double) * g.S;
+      double* vecs[4] = {c.x, c.r, c.p[0], c.p[1]};
+      for (double* v : vecs) {
+        if (c.rank == 0) SL_CUDA(cudaMemsetAsync(v, 0, plane, stream));
+        if (c.rank == d->P - 1) SL_CUDA(cudaMemsetAsync(v + (long long)g.zend * g.S, 0, plane, stream));
+      }
+    }
+  }
+  if (sh && (rc = comm_halo(d, k, 0, stream))) return rc;
+  if ((rc = pass(MODE_INIT, [&](SlabCtx& c, KArgs& a) { a.h0 = c.x; a.i0 = c.b; a.o0 = c.r; }))) return rc;
+  if (sh && (rc = comm_halo(d, k, 1, stream))) return rc;   // r on the halo planes for the first K1
+  long long it = 0;
+  auto iteration = [&]() -> int {
+    int q = pass(MODE_K1, [&](SlabCtx& c, KArgs& a) { a.h0 = c.r; a.h1 = c.p[it & 1]; a.o0 = c.p[(it + 1) & 1]; });
+    if (q) return q;
+    q = pass(MODE_K2, [&](SlabCtx& c, KArgs& a) {
+      a.h0 = c.p[(it + 1) & 1]; a.i0 = c.x; a.i1 = c.r; a.o0 = c.x; a.o1 = c.r;
+    });
+    if (q) return q;
+    if (sh && (q = comm_halo(d, k, 1, stream))) return q;
+    ++it;
+    return ECMG_OK;
+  };
+  SL_CUDA(cudaEventRecord(d->ev[0], stream));
+  if (eps <= 0.0) {
+    for (int i = 0; i < max_iter; ++i)
+      if ((rc = iteration())) return rc;
+  } else {
+    // pipelined host loop: batch i+1 in flight while the host inspects batch i's scalars; every rank
+    // sees the same scalars, so all ranks launch the same batches (matching NCCL sequences)
+    int batch = 1;
+    for (int i = 0; i < batch; ++i)
+      if ((rc = iteration())) return rc;
+    SL_CUDA(cudaMemcpyAsync(&d->sc_host[1], d->s[0].sc, sizeof(JcgScalars), cudaMemcpyDeviceToHost, stream));
+    SL_CUDA(cudaEventRecord(d->ev[2], stream));
+    int slot = 0;
+    long long guard = 0;
+    while (true) {
+      batch = std::min(batch * 2, 8);
+      for (int i = 0; i < batch; ++i)
+        if ((rc = iteration())) return rc;
+      SL_CUDA(cudaMemcpyAsync(&d->sc_host[2 - slot], d->s[0].sc, sizeof(JcgScalars), cudaMemcpyDeviceToHost, stream));
+      SL_CUDA(cudaEventRecord(d->ev[3 - slot], stream));
+      SL_CUDA(cudaEventSynchronize(d->ev[2 + slot]));
+      if (d->sc_host[1 + slot].done) break;
+      slot = 1 - slot;
+      if (++guard > (long long)max_iter + 8) break;
+    }
+  }
+  SL_CUDA(cudaEventRecord(d->ev[1], stream));
+  if (sh && (rc = comm_halo(d, k, 0, stream))) return rc;
+  if ((rc = pass(MODE_TRUE, [&](SlabCtx& c, KArgs& a) { a.h0 = c.x; a.i0 = c.b; }))) return rc;
+  const int status = read_stats(d, k, eps, st, stream);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, d->ev[0], d->ev[1]);
+  d->last_jcg_ms = ms;
+  return status;
+}
+
+}  // namespace
+
+// ---- driver lifecycle ------------------------------------------------------------------------
+SlabDriver* slab_driver_create(const SlabCfg& cfg, int P, int rank, bool virt, const unsigned char* nccl_id, int* status) {
+  *status = ECMG_OK;
+  SlabDriver* d = new SlabDriver;
+  d->P = P;
+  d->rank = rank;
+  d->virt = virt;
+  d->L = cfg.L;
+  d->cfg = cfg;
+  const int nloc = virt ? P : 1;
+  d->s.resize(nloc);
+  auto fail = [&](int st) { *status = st; slab_driver_destroy(d); return (SlabDriver*)nullptr; };
+  if (!virt) {
+    NcclApi& n = nccl();
+    if (!n.ok) return fail(ECMG_ENCCL);
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, 128);
+    if (n.CommInitRank(&d->comm, P, id, rank) != ncclSuccess) return fail(ECMG_ENCCL);
+  }
+  // worst-case sizes (all faces non-Dirichlet) over the levels, per slab
+  int face_none[6] = {FACE_ROBIN, FACE_ROBIN, FACE_ROBIN, FACE_ROBIN, FACE_ROBIN, FACE_ROBIN};
+  for (int i = 0; i < nloc; ++i) {
+    SlabCtx& c = d->s[i];
+    c.rank = virt ? i : rank;
+    long long vec = 64;
+    for (int k = 0; k < cfg.L; ++k) {
+      bool sh;
+      LevelGeom g = slab_geom(make_geom(cfg.dom, cfg.n0, k, face_none, 1), P, c.rank, &sh);
+      vec = std::max(vec, g.S * (long long)g.nza + 64);
+    }
+    const LevelGeom gf = make_geom(cfg.dom, cfg.n0, cfg.L - 1, face_none, 1);
+    const long long beta_n = (long long)(gf.n[0] + 4) * (gf.n[1] + 4) * (gf.n[2] + 4);
+    const long long part_n = 3LL * ((gf.nf[0] + 7) / 8) * ((gf.nf[1] + 7) / 8) * (gf.nf[2] + 3) / 4 * 4 + 3 * 65536;
+    auto alloc = [&](double** p, long long n) -> bool {
+      if (cudaMalloc(p, sizeof(double) * n) != cudaSuccess) { cudaGetLastError(); return false; }
+      return cudaMemset(*p, 0, sizeof(double) * n) == cudaSuccess;
+    };
+    bool ok = alloc(&c.x, vec) && alloc(&c.r, vec) && alloc(&c.p[0], vec) && alloc(&c.p[1], vec) && alloc(&c.b, vec) &&
+              alloc(&c.beta, beta_n) && alloc(&c.partials, part_n) &&
+              alloc(&c.scratch1d, 3LL * (std::max(gf.n[0], std::max(gf.n[1], gf.n[2])) + 1)) &&
+              alloc(&c.seeds, (long long)(gf.n[0] / 2 + 1) * (gf.n[1] / 2 + 1) * (gf.n[2] / 2 + 1)) &&
+              alloc(&c.ut, level_nodes(gf));
+    if (ok) {
+      if (cudaMalloc(&c.sc, sizeof(JcgScalars)) != cudaSuccess || cudaMemset(c.sc, 0, sizeof(JcgScalars)) != cudaSuccess) ok = false;
+    }
+    c.u.assign(cfg.L, nullptr);
+    for (int k = 0; ok && k < cfg.L; ++k) ok = alloc(&c.u[k], level_nodes(make_geom(cfg.dom, cfg.n0, k, face_none, 1)));
+    if (!ok) return fail(ECMG_ENOMEM);
+  }
+  if (cudaHostAlloc(&d->sc_host, 3 * sizeof(JcgScalars), cudaHostAllocDefault) != cudaSuccess ||
+      cudaHostAlloc(&d->param_host, sizeof(*d->param_host), cudaHostAllocDefault) != cudaSuccess)
+    return fail(ECMG_ENOMEM);
+  for (int i = 0; i < 4; ++i) cudaEventCreate(&d->ev[i]);
+  slab_driver_configure(d, cfg);
+  return d;
+}
+
+void slab_driver_configure(SlabDriver* d, const SlabCfg& cfg) {
+  d->cfg = cfg;
+  for (auto& c : d->s) {
+    c.geom.clear();
+    c.sharded.clear();
+    for (int k = 0; k < cfg.L; ++k) {
+      bool sh;
+      c.geom.push_back(slab_geom(make_geom(cfg.dom, cfg.n0, k, cfg.prob.face, cfg.elem_path), d->P, c.rank, &sh));
+      c.sharded.push_back(sh ? 1 : 0);
+    }
+    c.maps_level = -1;
+  }
+}
+
+void slab_driver_destroy(SlabDriver* d) {
+  if (!d) return;
+  cudaDeviceSynchronize();
+  for (auto& c : d->s) {
+    cudaFree(c.x); cudaFree(c.r); cudaFree(c.p[0]); cudaFree(c.p[1]); cudaFree(c.b); cudaFree(c.beta);
+    cudaFree(c.partials); cudaFree(c.scratch1d); cudaFree(c.seeds); cudaFree(c.sc); cudaFree(c.ut);
+    for (double* p : c.u) cudaFree(p);
+  }
+  if (d->comm) nccl().CommDestroy(d->comm);
+  if (d->sc_host) cudaFreeHost(d->sc_host);
+  if (d->param_host) cudaFreeHost(d->param_host);
+  cudaGetLastError();
+  delete d;
+}
+
+void slab_level_range(const SlabDriver* d, int k, int* zlo, int* zhi) {
+  const LevelGeom& g = d->s[0].geom[k];
+  if (d->virt) { *zlo = 0; *zhi = g.n[2] + 1; return; }
+  *zlo = g.zlo;
+  *zhi = g.zhi;
+}
+
+void slab_last_timing(const SlabDriver* d, double* ms, int* it, long long* nfree) {
+  *ms = d->last_jcg_ms;
+  *it = d->last_jcg_iters;
+  *nfree = d->last_free;
+}
+
+// ---- Alg. 4 over slabs -------------------------------------------------------------------------
+// u_out / ut_out: virtual slabs -> full-layout finest vectors (device or host); NCCL ranks -> this
+// rank's owned planes [zlo, zhi) of the finest level.
+int slab_run(SlabDriver* d, double eps, ecmg_stats* per_level, double* u_out, bool u_dev, double* ut_out, bool ut_dev,
+             cudaStream_t stream) {
+  const SlabCfg& cf = d->cfg;
+  const int L = cf.L;
+  int status = ECMG_OK;
+  for (int k = 0; k < L; ++k) {
+    ecmg_stats st{};
+    const bool sh = d->s[0].sharded[k];
+    const int nloc = (sh || !d->virt) ? (int)d->s.size() : 1;
+    cudaEvent_t e0, e1, e2, e3;
+    cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&e2); cudaEventCreate(&e3);
+    SL_CUDA(cudaEventRecord(e0, stream));
+    for (int i = 0; i < nloc; ++i) { int r = setup_slab_level(d, d->s[i], k, stream); if (r) return r; }
+    SL_CUDA(cudaEventRecord(e1, stream));
+    for (int i = 0; i < nloc; ++i) {
+      SlabCtx& c = d->s[i];
+      const LevelGeom& g = c.geom[k];
+      if (k < 2) SL_CUDA(launch_zero_vec(g, c.x, stream));   // DSOLVE: zero free guess (reading A12)
+      else SL_CUDA(launch_exp_finite(g, cf.prob, c.u[k - 1], c.u[k - 2], c.x, cf.exp_variant, c.seeds, 1, stream));
+    }
+    SL_CUDA(cudaEventRecord(e2, stream));
+    int s = slab_jcg(d, k, k < 2 ? 1e-14 : eps, 10000, &st, stream);
+    if (k < 2 && s == ECMG_ENOTCONV) s = ECMG_OK;
+    if (s == ECMG_ECUDA || s == ECMG_ENOMEM || s == ECMG_ENCCL) return s;
+    if (s != ECMG_OK && status == ECMG_OK) status = s;
+    for (int i = 0; i < nloc; ++i) {
+      SlabCtx& c = d->s[i];
+      SL_CUDA(launch_scatter(c.geom[k], c.x, c.u[k], stream));
+      SL_CUDA(launch_dirichlet_fill(c.geom[k], cf.prob, c.u[k], 0.0, 0, stream));
+    }
+    if (sh) {
+      int r = comm_u_halo(d, k, stream);
+      if (r) return r;
+    } else if (d->virt) {   // replicated level solved once: every virtual slab gets the full vector
+      for (size_t i = 1; i < d->s.size(); ++i)
+        SL_CUDA(cudaMemcpyAsync(d->s[i].u[k], d->s[0].u[k], sizeof(double) * level_nodes(d->s[0].geom[k]),
+                                cudaMemcpyDeviceToDevice, stream));
+    }
+    SL_CUDA(cudaEventRecord(e3, stream));
+    if (k == L - 1 && k >= 2 && ut_out)
+      for (int i = 0; i < nloc; ++i)
+        SL_CUDA(launch_exp_true(d->s[i].geom[k], cf.prob, d->s[i].u[k], d->s[i].u[k - 1], d->s[i].ut, stream));
+    SL_CUDA(cudaStreamSynchronize(stream));
+    float a = 0.f, b = 0.f, c3 = 0.f;
+    cudaEventElapsedTime(&a, e0, e1); cudaEventElapsedTime(&b, e1, e2); cudaEventElapsedTime(&c3, e2, e3);
+    st.ms_setup = a; st.ms_exp = b; st.ms_solve = c3; st.ms_rich = 0.0;
+    cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e2); cudaEventDestroy(e3);
+    if (per_level) per_level[k] = st;
+  }
+  // outputs
+  const int kf = L - 1;
+  const LevelGeom& gf0 = d->s[0].geom[kf];
+  const long long pl = (long long)(gf0.n[0] + 1) * (gf0.n[1] + 1);
+  const bool sh = d->s[0].sharded[kf];
+  for (size_t i = 0; i < d->s.size(); ++i) {
+    SlabCtx& c = d->s[i];
+    const LevelGeom& g = c.geom[kf];
+    const long long z0 = sh ? g.zlo : 0, z1 = sh ? g.zhi : g.n[2] + 1;
+    if (d->virt && !sh && i > 0) break;   // replicated finest level: slab 0 has everything
+    const long long dst0 = d->virt ? z0 * pl : 0;   // virtual: full layout; NCCL: local slab
+    SL_CUDA(cudaMemcpyAsync(u_out + dst0, c.u[kf] + z0 * pl, sizeof(double) * (z1 - z0) * pl,
+                            u_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, stream));
+    if (ut_out)
+      SL_CUDA(cudaMemcpyAsync(ut_out + dst0, c.ut + z0 * pl, sizeof(double) * (z1 - z0) * pl,
+                              ut_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, stream));
+  }
+  SL_CUDA(cudaStreamSynchronize(stream));
+  return status;
+}
+
+// JCG on one level through the slabs. u: full-layout (virtual) or this rank's planes [zlo, zhi)
+// (NCCL) of the level; in = guess, out = iterate with g_D on Dirichlet nodes.
+int slab_solve_level(SlabDriver* d, int k, double eps, int max_iter, double* u, ecmg_stats* st, cudaStream_t stream) {
+  const SlabCfg& cf = d->cfg;
+  const bool sh = d->s[0].sharded[k];
+  const int nloc = (sh || !d->virt) ? (int)d->s.size() : 1;
+  const LevelGeom& g0 = d->s[0].geom[k];
+  const long long pl = (long long)(g0.n[0] + 1) * (g0.n[1] + 1);
+  for (int i = 0; i < nloc; ++i) {
+    SlabCtx& c = d->s[i];
+    int r = setup_slab_level(d, c, k, stream);
+    if (r) return r;
+    // the caller's vector -> this slab's full-layout u_k (owned planes), then gather into x
+    const long long z0 = c.geom[k].zlo, z1 = c.geom[k].zhi;
+    const long long src0 = d->virt ? z0 * pl : 0;
+    SL_CUDA(cudaMemcpyAsync(c.u[k] + z0 * pl, u + src0, sizeof(double) * (z1 - z0) * pl, cudaMemcpyDeviceToDevice, stream));
+    SL_CUDA(launch_gather(c.geom[k], c.u[k], c.x, stream));
+  }
+  const int s = slab_jcg(d, k, eps, max_iter, st, stream);
+  if (s == ECMG_ECUDA || s == ECMG_ENOMEM || s == ECMG_ENCCL) return s;
+  for (int i = 0; i < nloc; ++i) {
+    SlabCtx& c = d->s[i];
+    SL_CUDA(launch_scatter(c.geom[k], c.x, c.u[k], stream));
+    SL_CUDA(launch_dirichlet_fill(c.geom[k], cf.prob, c.u[k], 0.0, 0, stream));
+    const long long z0 = c.geom[k].zlo, z1 = c.geom[k].zhi;
+    const long long dst0 = d->virt ? z0 * pl : 0;
+    SL_CUDA(cudaMemcpyAsync(u + dst0, c.u[k] + z0 * pl, sizeof(double) * (z1 - z0) * pl, cudaMemcpyDeviceToDevice, stream));
+  }
+  SL_CUDA(cudaStreamSynchronize(stream));
+  return s;
+}
+
+}  // namespace ecmg

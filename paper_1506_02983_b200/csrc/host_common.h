@@ -1,0 +1,141 @@
+// host_common.h -- host-side helpers shared by the single-GPU and the z-slab drivers (not ABI).
+#pragma once
+#include <algorithm>
+#include "../../include/ecmg.h"
+#include "ecmg_internal.cuh"
+
+namespace ecmg {
+
+inline LevelGeom make_geom(const ecmg_box& dom, const int n0[3], int k, const int face[6], int elem_path) {
+  LevelGeom g{};
+  for (int d = 0; d < 3; ++d) {
+    g.n[d] = n0[d] << k;
+    g.lo[d] = dom.lo[d];
+    g.h[d] = (dom.hi[d] - dom.lo[d]) / g.n[d];
+    const int lo = face[2 * d] == FACE_DIRICHLET ? 1 : 0;
+    const int hi = face[2 * d + 1] == FACE_DIRICHLET ? g.n[d] - 1 : g.n[d];
+    g.flo[d] = lo;
+    g.nf[d] = std::max(0, hi - lo + 1);
+  }
+  g.P = ((long long)std::max(1, g.nf[0]) + 31) / 32 * 32;
+  g.S = g.P * std::max(1, g.nf[1]);
+  g.BP = g.n[0] + 4;
+  g.BS = g.BP * (g.n[1] + 4);
+  g.elem_path = elem_path;
+  g.zoff = 0;
+  g.zbeg = 0;
+  g.zend = g.nf[2];
+  g.nza = g.nf[2];
+  g.zlo = 0;
+  g.zhi = g.n[2] + 1;
+  return g;
+}
+
+inline ElemStencil make_elem_stencil(const LevelGeom& g, const Problem& pb, int precond) {
+  ElemStencil es{};
+  const double V = g.h[0] * g.h[1] * g.h[2];
+  for (int pat = 0; pat < 8; ++pat) {
+    double s = 0.0;
+    for (int d = 0; d < 3; ++d) {
+      double t = ((pat >> d) & 1) ? -1.0 : 1.0;
+      t /= g.h[d] * g.h[d];
+      for (int e = 0; e < 3; ++e)
+        if (e != d) t *= ((pat >> e) & 1) ? (1.0 / 6.0) : (1.0 / 3.0);
+      s += t;
+    }
+    es.kappa[pat] = V * s;
+  }
+  for (int F = 0; F < 6; ++F) {
+    const int d = F >> 1;
+    const int d1 = (d == 0) ? 1 : 0, d2 = (d == 2) ? 1 : 2;
+    es.robin[F] = (pb.face[F] == FACE_ROBIN && pb.alpha[F] != 0.0) ? pb.alpha[F] * g.h[d1] * g.h[d2] : 0.0;
+  }
+  es.precond = precond;
+  return es;
+}
+
+inline ConstStencil make_const_stencil(const LevelGeom& g, double beta, int precond) {
+  // c(o) = beta * sum_d K_d(o_d) prod_{e != d} M_e(o_e); K(0) = 2/h, K(1) = -1/h, M(0) = 2h/3, M(1) = h/6
+  auto K = [](double h, int o) { return o ? -1.0 / h : 2.0 / h; };
+  auto M = [](double h, int o) { return o ? h / 6.0 : 2.0 * h / 3.0; };
+  auto c = [&](int ox, int oy, int oz) {
+    const int o[3] = {ox, oy, oz};
+    double s = 0.0;
+    for (int d = 0; d < 3; ++d) {
+      double t = K(g.h[d], o[d]);
+      for (int e = 0; e < 3; ++e)
+        if (e != d) t *= M(g.h[e], o[e]);
+      s += t;
+    }
+    return beta * s;
+  };
+  ConstStencil cs{};
+  for (int oz = 0; oz < 2; ++oz) {
+    cs.c0[oz] = c(0, 0, oz);
+    cs.cx[oz] = c(1, 0, oz);
+    cs.cy[oz] = c(0, 1, oz);
+    cs.cd[oz] = c(1, 1, oz);
+  }
+  cs.dinv = precond ? 1.0 / c(0, 0, 0) : 1.0;
+  return cs;
+}
+
+inline int auto_zc(int zchunk, int elem_path, const LevelGeom& g) {
+  if (zchunk > 0) return zchunk;
+  const int ty = elem_path ? 8 : 32;
+  const long long tiles = (long long)((g.nf[0] + 31) / 32) * ((g.nf[1] + ty - 1) / ty);
+  const long long target = 148LL * 2 * 2;
+  long long nchunks = (target + tiles - 1) / tiles;
+  const int nz = g.zend - g.zbeg;
+  nchunks = std::max(1LL, std::min(nchunks, (long long)std::max(1, nz / 4)));
+  return (int)((nz + nchunks - 1) / nchunks);
+}
+
+
+inline bool problem_faces(int id, int face[6], double alpha[6], int* nparams_required) {
+  for (int f = 0; f < 6; ++f) { face[f] = FACE_DIRICHLET; alpha[f] = 0.0; }
+  *nparams_required = 0;
+  switch (id) {
+    case 1: case 2: case 4: case 13: case 21: case 24: break;
+    case 3: case 23: face[ZP] = FACE_ROBIN; alpha[ZP] = 1.0; break;
+    case 11: face[XP] = face[YP] = face[ZP] = FACE_ROBIN; break;   // Neumann (alpha = 0)
+    case 12: face[XP] = face[YP] = FACE_ROBIN; break;
+    case 5: *nparams_required = 48; break;
+    case 22: *nparams_required = 15; break;
+    default: return false;
+  }
+  return true;
+}
+
+inline long long free_count(const LevelGeom& g) { return (long long)g.nf[0] * g.nf[1] * (g.zend - g.zbeg); }
+inline long long level_nodes(const LevelGeom& g) { return (long long)(g.n[0] + 1) * (g.n[1] + 1) * (g.n[2] + 1); }
+
+// z-slab partition of a level with n cells along z over P ranks: the level is
+// sharded iff n % (4P) == 0 and n / P >= 16 (every 4h EXP_finite block and 2h EXP_true cell then
+// lies inside one slab, and each slab has >= 16 planes); rank r owns node planes
+// [r n/P, (r+1) n/P), the last rank also plane n. Replicated levels: every rank owns [0, n+1).
+inline bool slab_partition(int n, int P, int r, int* zlo, int* zhi) {
+  const bool sharded = P > 1 && n % (4 * P) == 0 && n / P >= 16;
+  if (!sharded) { *zlo = 0; *zhi = n + 1; return false; }
+  *zlo = r * (n / P);
+  *zhi = (r == P - 1) ? n + 1 : (r + 1) * (n / P);
+  return true;
+}
+
+// geometry of rank r's slab of a level (work vectors: owned free planes + one halo plane per side)
+inline LevelGeom slab_geom(LevelGeom g, int P, int r, bool* sharded) {
+  int zlo, zhi;
+  *sharded = slab_partition(g.n[2], P, r, &zlo, &zhi);
+  if (!*sharded) return g;
+  g.zlo = zlo;
+  g.zhi = zhi;
+  const int f0 = g.flo[2], f1 = g.flo[2] + g.nf[2];            // global free node planes [f0, f1)
+  const int a = std::max(zlo, f0), b = std::min(zhi, f1);       // owned free planes [a, b)
+  g.zoff = a - f0 - 1;                                          // local plane 0 = free plane a-1 (halo)
+  g.zbeg = 1;
+  g.zend = 1 + std::max(0, b - a);
+  g.nza = g.zend + 1;
+  return g;
+}
+
+}  // namespace ecmg

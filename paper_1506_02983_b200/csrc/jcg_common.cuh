@@ -114,7 +114,11 @@ __device__ void reduce_finalize(int mode, const KArgs& a, double v0, double v1, 
   }
   block_sum3(s0, s1, s2, red);
   if (tid == 0) {
-    finalize(mode, a, s0, s1, s2);
+    if (a.local_only) {   // z-slab: partial sums of this slab; the allreduce + finalize pass follow
+      a.sc->loc[0] = s0; a.sc->loc[1] = s1; a.sc->loc[2] = s2;
+    } else {
+      finalize(mode, a, s0, s1, s2);
+    }
     a.sc->counter = 0;
   }
 }

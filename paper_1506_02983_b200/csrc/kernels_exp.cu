@@ -24,6 +24,7 @@
 // 2 face diagonals / 4 space diagonals at face / cell centres (reading §8c A13; derived identity,
 // DESIGN.md). One thread per 2h cell computes its (up to 27) owned fine nodes from the 8 corner
 // differences. Dirichlet nodes take g_D.
+#include <algorithm>
 #include "ecmg_internal.cuh"
 #include "problems.cuh"
 
@@ -37,8 +38,8 @@ __device__ __forceinline__ bool is_free(const LevelGeom& g, int gx, int gy, int 
 
 // (1) extrapolated values at all 2h nodes of the fine level gf (2h grid: n/2 cells per axis)
 __global__ void k_exp_seeds(const LevelGeom gf, const double* __restrict__ u2h, const double* __restrict__ u4h,
-                            double* __restrict__ S, int variant) {
-  const int I = blockIdx.x * blockDim.x + threadIdx.x, J = blockIdx.y, K = blockIdx.z;
+                            double* __restrict__ S, int variant, int K0) {
+  const int I = blockIdx.x * blockDim.x + threadIdx.x, J = blockIdx.y, K = K0 + blockIdx.z;
   const int n2x = gf.n[0] / 2, n2y = gf.n[1] / 2;
   if (I > n2x) return;
   const long long nn2x = n2x + 1, nn2y = n2y + 1;
@@ -86,9 +87,9 @@ __device__ __forceinline__ void lin_w(int l, double w[2]) {
 // full nodal vector w (with g_D on Dirichlet nodes).
 template <bool FREEBOX>
 __global__ void k_exp_interp(const LevelGeom gf, const Problem pb, const double* __restrict__ S, double* __restrict__ out,
-                             int variant) {
+                             int variant, int F0) {
   const int n4x = gf.n[0] / 4, n4y = gf.n[1] / 4, n4z = gf.n[2] / 4;
-  const int bx = blockIdx.x * blockDim.x + threadIdx.x, fy = blockIdx.y, fz = blockIdx.z;
+  const int bx = blockIdx.x * blockDim.x + threadIdx.x, fy = blockIdx.y, fz = F0 + blockIdx.z;
   if (bx >= n4x) return;
   const int by = min(fy / 4, n4y - 1), bz = min(fz / 4, n4z - 1);
   const int ly = fy - 4 * by, lz = fz - 4 * bz;
@@ -142,7 +143,7 @@ __global__ void k_exp_interp(const LevelGeom gf, const Problem pb, const double*
     double W = qx[0] * C[0] + qx[1] * C[1] + qx[2] * C[2] + lx[0] * E[0] + lx[1] * E[1];
     const bool fr = row_free && fx >= gf.flo[0] && fx < gf.flo[0] + gf.nf[0];
     if (FREEBOX) {
-      if (fr) out[(long long)(fz - gf.flo[2]) * gf.S + (long long)(fy - gf.flo[1]) * gf.P + (fx - gf.flo[0])] = W;
+      if (fr) out[(long long)(fz - gf.flo[2] - gf.zoff) * gf.S + (long long)(fy - gf.flo[1]) * gf.P + (fx - gf.flo[0])] = W;
     } else {
       if (!fr) W = prob_gD(pb, gf.lo[0] + fx * gf.h[0], gf.lo[1] + fy * gf.h[1], gf.lo[2] + fz * gf.h[2]);
       out[(long long)fx + nx * ((long long)fy + ny * fz)] = W;
@@ -156,7 +157,7 @@ __global__ void k_exp_interp(const LevelGeom gf, const Problem pb, const double*
 __global__ void __launch_bounds__(128, 6) k_exp_true(const LevelGeom gf, const Problem pb, const double* __restrict__ uh,
                                                   const double* __restrict__ u2h, double* __restrict__ ut) {
   const int n2x = gf.n[0] / 2, n2y = gf.n[1] / 2, n2z = gf.n[2] / 2;
-  const int cx = blockIdx.x * blockDim.x + threadIdx.x, cy = blockIdx.y, cz = blockIdx.z;
+  const int cx = blockIdx.x * blockDim.x + threadIdx.x, cy = blockIdx.y, cz = gf.zlo / 2 + blockIdx.z;
   if (cx >= n2x) return;
   const long long nx = gf.n[0] + 1, ny = gf.n[1] + 1, pl = nx * ny;
   const long long nx2 = n2x + 1, pl2 = nx2 * (n2y + 1);
@@ -216,19 +217,28 @@ __global__ void __launch_bounds__(128, 6) k_exp_true(const LevelGeom gf, const P
 
 cudaError_t launch_exp_finite(const LevelGeom& gf, const Problem& pb, const double* u2h, const double* u4h, double* w,
                               int variant, double* seeds, int freebox, cudaStream_t st) {
-  dim3 g1((gf.n[0] / 2 + 1 + 127) / 128, gf.n[1] / 2 + 1, gf.n[2] / 2 + 1);
+  // fine planes produced: the rank's free planes (free-box output) or its owned node planes (full output)
+  const int F0 = freebox ? gf.flo[2] + gf.zoff + gf.zbeg : gf.zlo;
+  const int F1 = freebox ? gf.flo[2] + gf.zoff + gf.zend : gf.zhi;
+  if (F1 <= F0) return cudaSuccess;
+  const int n4z = gf.n[2] / 4;
+  const int bz0 = std::min(F0 / 4, n4z - 1), bz1 = std::min((F1 - 1) / 4, n4z - 1);
+  const int K0 = 2 * bz0, K1 = 2 * bz1 + 2;   // 2h planes of the touched 4h blocks
+  dim3 g1((gf.n[0] / 2 + 1 + 127) / 128, gf.n[1] / 2 + 1, K1 - K0 + 1);
   count_launch();
-  k_exp_seeds<<<g1, 128, 0, st>>>(gf, u2h, u4h, seeds, variant);
-  dim3 g2((gf.n[0] / 4 + 63) / 64, gf.n[1] + 1, gf.n[2] + 1);
+  k_exp_seeds<<<g1, 128, 0, st>>>(gf, u2h, u4h, seeds, variant, K0);
+  dim3 g2((gf.n[0] / 4 + 63) / 64, gf.n[1] + 1, F1 - F0);
   count_launch();
-  if (freebox) k_exp_interp<true><<<g2, 64, 0, st>>>(gf, pb, seeds, w, variant);
-  else k_exp_interp<false><<<g2, 64, 0, st>>>(gf, pb, seeds, w, variant);
+  if (freebox) k_exp_interp<true><<<g2, 64, 0, st>>>(gf, pb, seeds, w, variant, F0);
+  else k_exp_interp<false><<<g2, 64, 0, st>>>(gf, pb, seeds, w, variant, F0);
   return cudaGetLastError();
 }
 
 cudaError_t launch_exp_true(const LevelGeom& gf, const Problem& pb, const double* uh, const double* u2h, double* ut,
                             cudaStream_t st) {
-  dim3 grid((gf.n[0] / 2 + 127) / 128, gf.n[1] / 2, gf.n[2] / 2);
+  const int c0 = gf.zlo / 2, c1 = std::min(gf.zhi / 2, gf.n[2] / 2);   // 2h cells owning this rank's planes
+  if (c1 <= c0) return cudaSuccess;
+  dim3 grid((gf.n[0] / 2 + 127) / 128, gf.n[1] / 2, c1 - c0);
   count_launch();
   k_exp_true<<<grid, 128, 0, st>>>(gf, pb, uh, u2h, ut);
   return cudaGetLastError();

@@ -38,11 +38,11 @@ __global__ void __launch_bounds__(NTH, 2) k_jcg_const(const LevelGeom g, const C
     if (*(volatile int*)&sc->done) return;   // converged / failed: speculative launches are no-ops
   }
   const int lane = threadIdx.x, w = threadIdx.y, tid = lane + TX * w;
-  const int nfx = g.nf[0], nfy = g.nf[1], nfz = g.nf[2];
+  const int nfx = g.nf[0], nfy = g.nf[1], nfz = g.nza;   // local planes
   const long long P = g.P, S = g.S;
   const int X0 = blockIdx.x * TX, Y0 = blockIdx.y * CTY;
-  const int z0 = blockIdx.z * a.zc;
-  const int z1 = min(z0 + a.zc, nfz);
+  const int z0 = g.zbeg + blockIdx.z * a.zc;
+  const int z1 = min(z0 + a.zc, g.zend);
   const int x = X0 + lane;
   const int yb = Y0 + CRY * w;
 
@@ -117,8 +117,13 @@ __global__ void __launch_bounds__(NTH, 2) k_jcg_const(const LevelGeom g, const C
     if ((kInt0 || kInt1) && zl >= z0 && zl < z1) load_int(zl);
 
     double (*Pb)[CHX] = Pl[s & 1];
+    const bool halo_store = (MODE == MODE_K1) && (zl == g.zbeg - 1 || zl == g.zend) && zl >= 0 && zl < nfz;
 #pragma unroll
-    for (int j = 0; j < CRY; ++j) Pb[1 + CRY * w + j][1 + lane] = transform(c0[j], c1[j]);
+    for (int j = 0; j < CRY; ++j) {
+      const double v = transform(c0[j], c1[j]);
+      Pb[1 + CRY * w + j][1 + lane] = v;
+      if (halo_store && own_ok[j]) a.o0[(long long)zl * S + own_off[j]] = v;   // slab halo plane of p
+    }
     if (rhx >= 0) Pb[rhy][rhx] = transform(cr0, cr1);
     __syncthreads();
 
@@ -201,11 +206,11 @@ __global__ void __launch_bounds__(NTH, 2) k_jcg_elem(const LevelGeom g, const El
     if (*(volatile int*)&sc->done) return;
   }
   const int lane = threadIdx.x, w = threadIdx.y, tid = lane + TX * w;
-  const int nfx = g.nf[0], nfy = g.nf[1], nfz = g.nf[2];
+  const int nfx = g.nf[0], nfy = g.nf[1], nfz = g.nza;   // local planes
   const long long P = g.P, S = g.S;
   const int X0 = blockIdx.x * TX, Y0 = blockIdx.y * ETY;
-  const int z0 = blockIdx.z * a.zc;
-  const int z1 = min(z0 + a.zc, nfz);
+  const int z0 = g.zbeg + blockIdx.z * a.zc;
+  const int z1 = min(z0 + a.zc, g.zend);
   const int x = X0 + lane, y = Y0 + w;
   const bool own_ok = x < nfx && y < nfy;
   const long long own_off = own_ok ? (long long)y * P + x : 0;
@@ -259,8 +264,8 @@ __global__ void __launch_bounds__(NTH, 2) k_jcg_elem(const LevelGeom g, const El
       nr1 = (zok && ring_ok) ? __ldg(a.h1 + zo + ring_off) : 0.0;
     }
   };
-  auto load_beta = [&](int fez) {   // element plane (free element coords)
-    const int gez = g.flo[2] + fez;
+  auto load_beta = [&](int fez) {   // element plane (local free element coords)
+    const int gez = g.flo[2] + g.zoff + fez;
     const bool zok = gez >= -2 && gez <= g.n[2] + 1;
     const long long zo = zok ? (long long)(gez + 2) * g.BS : 0;
 #pragma unroll
@@ -275,7 +280,7 @@ __global__ void __launch_bounds__(NTH, 2) k_jcg_elem(const LevelGeom g, const El
   // which Robin faces (alpha != 0) a free node (fx, fy, fz) lies on: bit F
   auto robin_mask = [&](int fx, int fy, int fz) -> int {
     if (!robin_any) return 0;
-    const int gx = g.flo[0] + fx, gy = g.flo[1] + fy, gz = g.flo[2] + fz;
+    const int gx = g.flo[0] + fx, gy = g.flo[1] + fy, gz = g.flo[2] + g.zoff + fz;
     int m = 0;
     if (gx == 0 && es.robin[0] != 0.0) m |= 1;
     if (gx == g.n[0] && es.robin[1] != 0.0) m |= 2;
@@ -345,6 +350,8 @@ __global__ void __launch_bounds__(NTH, 2) k_jcg_elem(const LevelGeom g, const El
         v = first ? di * c0 : di * c0 + bcg * c1;
       }
       Pr[ring(zl)][w + 1][lane + 1] = v;
+      if (MODE == MODE_K1 && own_ok && (zl == g.zbeg - 1 || zl == g.zend) && zl >= 0 && zl < nfz)
+        a.o0[(long long)zl * S + own_off] = v;   // slab halo plane of p
       if (rhx >= 0) {
         double vr = cr0;
         if (MODE == MODE_K1) {
@@ -450,15 +457,50 @@ __global__ void __launch_bounds__(NTH, 2) k_jcg_elem(const LevelGeom g, const El
 
 }  // namespace
 
+namespace {
+template <int MODE>
+__global__ void k_finalize(const KArgs a) {
+  if (MODE == MODE_K1 || MODE == MODE_K2) {
+    if (*(volatile int*)&a.sc->done) return;   // converged: the speculative pass is a no-op
+  }
+  finalize(MODE, a, a.sc->glob[0], a.sc->glob[1], a.sc->glob[2]);
+}
+__global__ void k_vsum(const SlabScalars s) {
+  for (int k = 0; k < 3; ++k) {
+    double t = 0.0;
+    for (int i = 0; i < s.n; ++i) t += s.p[i]->loc[k];   // slab order: deterministic
+    for (int i = 0; i < s.n; ++i) s.p[i]->glob[k] = t;
+  }
+}
+}  // namespace
+
+cudaError_t launch_finalize(int mode, const KArgs& a, cudaStream_t st) {
+  count_launch();
+  switch (mode) {
+    case MODE_K1: k_finalize<MODE_K1><<<1, 1, 0, st>>>(a); break;
+    case MODE_K2: k_finalize<MODE_K2><<<1, 1, 0, st>>>(a); break;
+    case MODE_INIT: k_finalize<MODE_INIT><<<1, 1, 0, st>>>(a); break;
+    case MODE_TRUE: k_finalize<MODE_TRUE><<<1, 1, 0, st>>>(a); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_vsum(const SlabScalars& s, cudaStream_t st) {
+  count_launch();
+  k_vsum<<<1, 1, 0, st>>>(s);
+  return cudaGetLastError();
+}
+
 int jcg_num_blocks(const LevelGeom& g, int elem_path, int zc) {
   const int ty = elem_path ? ETY : CTY;
-  const int bx = (g.nf[0] + TX - 1) / TX, by = (g.nf[1] + ty - 1) / ty, bz = (g.nf[2] + zc - 1) / zc;
+  const int bx = (g.nf[0] + TX - 1) / TX, by = (g.nf[1] + ty - 1) / ty, bz = (g.zend - g.zbeg + zc - 1) / zc;
   return bx * by * bz;
 }
 
 cudaError_t launch_jcg_const(int mode, const LevelGeom& g, const ConstStencil& cs, const KArgs& a, cudaStream_t st) {
   dim3 block(TX, WARPS);
-  dim3 grid((g.nf[0] + TX - 1) / TX, (g.nf[1] + CTY - 1) / CTY, (g.nf[2] + a.zc - 1) / a.zc);
+  dim3 grid((g.nf[0] + TX - 1) / TX, (g.nf[1] + CTY - 1) / CTY, (g.zend - g.zbeg + a.zc - 1) / a.zc);
   switch (mode) {
     case MODE_K1: count_launch(); k_jcg_const<MODE_K1><<<grid, block, 0, st>>>(g, cs, a); break;
     case MODE_K2: count_launch(); k_jcg_const<MODE_K2><<<grid, block, 0, st>>>(g, cs, a); break;
@@ -490,7 +532,7 @@ static cudaError_t launch_elem_mode(dim3 grid, dim3 block, const LevelGeom& g, c
 cudaError_t launch_jcg_elem(int mode, const LevelGeom& g, const ElemStencil& es, const Problem& pb, const KArgs& a,
                             cudaStream_t st) {
   dim3 block(TX, WARPS);
-  dim3 grid((g.nf[0] + TX - 1) / TX, (g.nf[1] + ETY - 1) / ETY, (g.nf[2] + a.zc - 1) / a.zc);
+  dim3 grid((g.nf[0] + TX - 1) / TX, (g.nf[1] + ETY - 1) / ETY, (g.zend - g.zbeg + a.zc - 1) / a.zc);
   switch (mode) {
     case MODE_K1: return launch_elem_mode<MODE_K1>(grid, block, g, es, pb, a, st);
     case MODE_K2: return launch_elem_mode<MODE_K2>(grid, block, g, es, pb, a, st);

@@ -91,8 +91,8 @@ __global__ void __launch_bounds__(NTH, 2)
   const int nfx = g.nf[0], nfy = g.nf[1];
   const long long P = g.P, S = g.S;
   const int X0 = blockIdx.x * TX, Y0 = blockIdx.y * TY;
-  const int z0 = blockIdx.z * a.zc;
-  const int z1 = min(z0 + a.zc, g.nf[2]);
+  const int z0 = g.zbeg + blockIdx.z * a.zc;
+  const int z1 = min(z0 + a.zc, g.zend);
   const int x = X0 + lane, yb = Y0 + RY * w;
   const int nsteps = z1 - z0 + 2;
 
@@ -151,10 +151,12 @@ __global__ void __launch_bounds__(NTH, 2)
     double* H = reinterpret_cast<double*>(stage_ptr(st));
     if (MODE == MODE_K1) {
       const double* H1 = reinterpret_cast<const double*>(stage_ptr(st) + HSTRIDE);
+      const bool halo_store = (zl == g.zbeg - 1 || zl == g.zend) && zl >= 0 && zl < g.nza;
 #pragma unroll
       for (int j = 0; j < RY; ++j) {
         const int o = (1 + RY * w + j) * HX + XO + lane;
         H[o] = pcg_direction(dinv, H[o], bcg, H1[o], first);
+        if (halo_store && own_ok[j]) a.o0[(long long)zl * S + own_off[j]] = H[o];   // slab halo plane of p
       }
       if (rhx >= 0) {
         const int o = rhy * HX + rhx;
@@ -251,7 +253,7 @@ cudaError_t init_tma_kernel_attributes() {
 cudaError_t launch_jcg_const_tma(int mode, const LevelGeom& g, const ConstStencil& cs, const KArgs& a,
                                  const CUtensorMap* maps, cudaStream_t st) {
   dim3 block(TX, WARPS);
-  dim3 grid((g.nf[0] + TX - 1) / TX, (g.nf[1] + TY - 1) / TY, (g.nf[2] + a.zc - 1) / a.zc);
+  dim3 grid((g.nf[0] + TX - 1) / TX, (g.nf[1] + TY - 1) / TY, (g.zend - g.zbeg + a.zc - 1) / a.zc);
   switch (mode) {
     case MODE_K1: return launch_tma_mode<MODE_K1, 4>(grid, block, g, cs, a, maps, st);
     case MODE_K2: return launch_tma_mode<MODE_K2, 3>(grid, block, g, cs, a, maps, st);
@@ -276,7 +278,7 @@ int make_vec_tensor_map(CUtensorMap* map, const double* base, const LevelGeom& g
     }
     encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
-  cuuint64_t dims[3] = {(cuuint64_t)g.nf[0], (cuuint64_t)g.nf[1], (cuuint64_t)g.nf[2]};
+  cuuint64_t dims[3] = {(cuuint64_t)g.nf[0], (cuuint64_t)g.nf[1], (cuuint64_t)g.nza};
   cuuint64_t strides[2] = {(cuuint64_t)g.P * 8, (cuuint64_t)g.S * 8};
   cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1};
   cuuint32_t estr[3] = {1, 1, 1};

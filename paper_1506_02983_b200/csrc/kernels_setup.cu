@@ -13,10 +13,12 @@ constexpr double kGauss = 0.57735026918962576451;  // 1/sqrt(3)
 
 // ---- element coefficients beta_e = beta(centroid) (§8c A3), zero outside the domain ----------
 __global__ void k_beta(const LevelGeom g, const Problem pb, double* __restrict__ beta) {
-  const long long ne0 = g.n[0] + 4, ne1 = g.n[1] + 4, ne2 = g.n[2] + 4;
+  // element planes this rank's work vectors touch: [flo+zoff-2, flo+zoff+nza] (all planes on one GPU)
+  const int e0 = max(-2, g.flo[2] + g.zoff - 2), e1 = min(g.n[2] + 1, g.flo[2] + g.zoff + g.nza);
+  const long long ne0 = g.n[0] + 4, ne1 = g.n[1] + 4, ne2 = e1 - e0 + 1;
   const long long total = ne0 * ne1 * ne2;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
-    const int ex = (int)(t % ne0) - 2, ey = (int)((t / ne0) % ne1) - 2, ez = (int)(t / (ne0 * ne1)) - 2;
+    const int ex = (int)(t % ne0) - 2, ey = (int)((t / ne0) % ne1) - 2, ez = (int)(t / (ne0 * ne1)) + e0;
     double v = 0.0;
     if (ex >= 0 && ex < g.n[0] && ey >= 0 && ey < g.n[1] && ez >= 0 && ez < g.n[2]) {
       v = prob_beta(pb, g.lo[0] + (ex + 0.5) * g.h[0], g.lo[1] + (ey + 0.5) * g.h[1], g.lo[2] + (ez + 0.5) * g.h[2]);
@@ -87,11 +89,11 @@ __global__ void k_load1d(const LevelGeom g, const Problem pb, double* __restrict
 
 __global__ void k_rhs_sep(const LevelGeom g, const Problem pb, const double* __restrict__ L, int stride,
                           double* __restrict__ b) {
-  const int fx = blockIdx.x * blockDim.x + threadIdx.x, fy = blockIdx.y, fz = blockIdx.z;
+  const int fx = blockIdx.x * blockDim.x + threadIdx.x, fy = blockIdx.y, lz = g.zbeg + blockIdx.z;
   if (fx >= g.nf[0]) return;
   const double A = sep_amp(pb);
-  const double v = A * __ldg(L + g.flo[0] + fx) * __ldg(L + stride + g.flo[1] + fy) * __ldg(L + 2 * stride + g.flo[2] + fz);
-  b[(long long)fz * g.S + (long long)fy * g.P + fx] = v;
+  const double v = A * __ldg(L + g.flo[0] + fx) * __ldg(L + stride + g.flo[1] + fy) * __ldg(L + 2 * stride + g.flo[2] + g.zoff + lz);
+  b[(long long)lz * g.S + (long long)fy * g.P + fx] = v;
 }
 
 // f specialised per problem at compile time (PID = 0: generic registry switch)
@@ -111,12 +113,12 @@ __global__ void __launch_bounds__(VNTH, 3) k_rhs_vol(const LevelGeom g, const Pr
   double* Fe = vs + VNE * 8;    // [2][VNE][8] element load vectors, ring of two element planes
   const int lane = threadIdx.x, w = threadIdx.y, tid = lane + VX * w;
   const int X0 = blockIdx.x * VX, Y0 = blockIdx.y * VY;
-  const int z0 = blockIdx.z * zc, z1 = min(z0 + zc, g.nf[2]);
+  const int z0 = g.zbeg + blockIdx.z * zc, z1 = min(z0 + zc, g.zend);   // local planes
   const double detJ = g.h[0] * g.h[1] * g.h[2] / 8.0;
   const double wA = (1.0 + kGauss) / 2.0, wB = (1.0 - kGauss) / 2.0;   // N at the near / far Gauss point
   for (int fez = z0 - 1; fez < z1; ++fez) {
     // (a) f at the 8 Gauss points of every element of the plane (33 x 9 x 8 evaluations)
-    const int gez = g.flo[2] + fez;
+    const int gez = g.flo[2] + g.zoff + fez;
     for (int t = tid; t < VNE * 8; t += VNTH) {
       const int e = t >> 3, q = t & 7;
       const int gex = g.flo[0] + X0 - 1 + e % VEX, gey = g.flo[1] + Y0 - 1 + e / VEX;
@@ -173,12 +175,17 @@ __global__ void k_rhs_shell(const LevelGeom g, const Problem pb, const ElemStenc
                             const double* __restrict__ beta, double* __restrict__ b) {
   const int face = blockIdx.z, d = face >> 1, side = face & 1;
   const int d1 = (d == 0) ? 1 : 0, d2 = (d == 2) ? 1 : 2;
+  // extents of the face in global free coordinates; z is restricted to this rank's planes
+  const int zb = g.zoff + g.zbeg, ze = g.zoff + g.zend;
+  const int ext1 = (d1 == 2) ? ze - zb : g.nf[d1], off1 = (d1 == 2) ? zb : 0;
+  const int ext2 = (d2 == 2) ? ze - zb : g.nf[d2], off2 = (d2 == 2) ? zb : 0;
   const int i1 = blockIdx.x * blockDim.x + threadIdx.x, i2 = blockIdx.y;
-  if (i1 >= g.nf[d1] || i2 >= g.nf[d2]) return;
+  if (i1 >= ext1 || i2 >= ext2) return;
   int f[3];
   f[d] = side ? g.nf[d] - 1 : 0;
-  f[d1] = i1;
-  f[d2] = i2;
+  f[d1] = off1 + i1;
+  f[d2] = off2 + i2;
+  if (d == 2 && (f[2] < zb || f[2] >= ze)) return;   // z face not in this slab
   for (int fc = 0; fc < face; ++fc) {   // owned by a lower face?
     const int dd = fc >> 1;
     if (f[dd] == ((fc & 1) ? g.nf[dd] - 1 : 0)) return;
@@ -238,26 +245,26 @@ __global__ void k_rhs_shell(const LevelGeom g, const Problem pb, const ElemStenc
       }
     }
   }
-  if (v != 0.0 || sub != 0.0) b[(long long)f[2] * g.S + (long long)f[1] * g.P + f[0]] += v - sub;
+  if (v != 0.0 || sub != 0.0) b[(long long)(f[2] - g.zoff) * g.S + (long long)f[1] * g.P + f[0]] += v - sub;
 }
 
 // ---- gather / scatter between full nodal vectors and the free box ------------------------------
 __global__ void k_gather(const LevelGeom g, const double* __restrict__ u, double* __restrict__ x) {
   const int fx = blockIdx.x * blockDim.x + threadIdx.x;
-  const int fy = blockIdx.y, fz = blockIdx.z;
+  const int fy = blockIdx.y, lz = g.zbeg + blockIdx.z;
   if (fx >= g.nf[0]) return;
   const long long nx = g.n[0] + 1, ny = g.n[1] + 1;
-  const long long gi = (long long)(g.flo[0] + fx) + nx * ((long long)(g.flo[1] + fy) + ny * (g.flo[2] + fz));
-  x[(long long)fz * g.S + (long long)fy * g.P + fx] = u[gi];
+  const long long gi = (long long)(g.flo[0] + fx) + nx * ((long long)(g.flo[1] + fy) + ny * (g.flo[2] + g.zoff + lz));
+  x[(long long)lz * g.S + (long long)fy * g.P + fx] = u[gi];
 }
 
 __global__ void k_scatter(const LevelGeom g, const double* __restrict__ x, double* __restrict__ u) {
   const int fx = blockIdx.x * blockDim.x + threadIdx.x;
-  const int fy = blockIdx.y, fz = blockIdx.z;
+  const int fy = blockIdx.y, lz = g.zbeg + blockIdx.z;
   if (fx >= g.nf[0]) return;
   const long long nx = g.n[0] + 1, ny = g.n[1] + 1;
-  const long long gi = (long long)(g.flo[0] + fx) + nx * ((long long)(g.flo[1] + fy) + ny * (g.flo[2] + fz));
-  u[gi] = x[(long long)fz * g.S + (long long)fy * g.P + fx];
+  const long long gi = (long long)(g.flo[0] + fx) + nx * ((long long)(g.flo[1] + fy) + ny * (g.flo[2] + g.zoff + lz));
+  u[gi] = x[(long long)lz * g.S + (long long)fy * g.P + fx];
 }
 
 // Dirichlet nodes (outside the free box) of a full nodal vector := g_D (or 0). One launch per
@@ -271,6 +278,7 @@ __global__ void k_dirichlet_face(const LevelGeom g, const Problem pb, double* __
   gi[d] = side ? g.n[d] : 0;
   gi[d1] = i1;
   gi[d2] = i2;
+  if (gi[2] < g.zlo || gi[2] >= g.zhi) return;   // only this rank's planes
   const long long nx = g.n[0] + 1, ny = g.n[1] + 1;
   const double v = zero ? 0.0 : prob_gD(pb, g.lo[0] + gi[0] * g.h[0], g.lo[1] + gi[1] * g.h[1], g.lo[2] + gi[2] * g.h[2]);
   u[(long long)gi[0] + nx * ((long long)gi[1] + ny * gi[2])] = v;
@@ -279,7 +287,7 @@ __global__ void k_dirichlet_face(const LevelGeom g, const Problem pb, double* __
 __global__ void k_zero_free(const LevelGeom g, double* __restrict__ v) {
   const int fx = blockIdx.x * blockDim.x + threadIdx.x;
   if (fx >= g.nf[0]) return;
-  v[(long long)blockIdx.z * g.S + (long long)blockIdx.y * g.P + fx] = 0.0;
+  v[(long long)blockIdx.z * g.S + (long long)blockIdx.y * g.P + fx] = 0.0;   // all allocated planes
 }
 
 }  // namespace
@@ -306,12 +314,12 @@ cudaError_t launch_rhs(const LevelGeom& g, const Problem& pb, const ElemStencil&
     dim3 g1((stride + 127) / 128, 3);
     count_launch();
     k_load1d<<<g1, 128, 0, st>>>(g, pb, scratch, stride);
-    dim3 g2((g.nf[0] + 127) / 128, g.nf[1], g.nf[2]);
+    dim3 g2((g.nf[0] + 127) / 128, g.nf[1], g.zend - g.zbeg);
     count_launch();
     k_rhs_sep<<<g2, 128, 0, st>>>(g, pb, scratch, stride, b);
   } else {
     const int zc = 32;
-    dim3 grid((g.nf[0] + VX - 1) / VX, (g.nf[1] + VY - 1) / VY, (g.nf[2] + zc - 1) / zc);
+    dim3 grid((g.nf[0] + VX - 1) / VX, (g.nf[1] + VY - 1) / VY, (g.zend - g.zbeg + zc - 1) / zc);
     count_launch();
     if (pb.id == 4) k_rhs_vol<4><<<grid, dim3(VX, VY), VSMEM, st>>>(g, pb, b, zc);
     else k_rhs_vol<0><<<grid, dim3(VX, VY), VSMEM, st>>>(g, pb, b, zc);
@@ -324,14 +332,14 @@ cudaError_t launch_rhs(const LevelGeom& g, const Problem& pb, const ElemStencil&
 }
 
 cudaError_t launch_gather(const LevelGeom& g, const double* u, double* x, cudaStream_t st) {
-  dim3 grid((g.nf[0] + 127) / 128, g.nf[1], g.nf[2]);
+  dim3 grid((g.nf[0] + 127) / 128, g.nf[1], g.zend - g.zbeg);
   count_launch();
   k_gather<<<grid, 128, 0, st>>>(g, u, x);
   return cudaGetLastError();
 }
 
 cudaError_t launch_scatter(const LevelGeom& g, const double* x, double* u, cudaStream_t st) {
-  dim3 grid((g.nf[0] + 127) / 128, g.nf[1], g.nf[2]);
+  dim3 grid((g.nf[0] + 127) / 128, g.nf[1], g.zend - g.zbeg);
   count_launch();
   k_scatter<<<grid, 128, 0, st>>>(g, x, u);
   return cudaGetLastError();
@@ -351,7 +359,7 @@ cudaError_t launch_dirichlet_fill(const LevelGeom& g, const Problem& pb, double*
 }
 
 cudaError_t launch_zero_vec(const LevelGeom& g, double* v, cudaStream_t st) {
-  dim3 grid((g.nf[0] + 127) / 128, g.nf[1], g.nf[2]);
+  dim3 grid((g.nf[0] + 127) / 128, g.nf[1], g.nza);
   count_launch();
   k_zero_free<<<grid, 128, 0, st>>>(g, v);
   return cudaGetLastError();

@@ -1,0 +1,29 @@
+// slab.h -- z-slab driver interface (ecmg_slab.cu), used by ecmg_api.cu. Not part of the ABI.
+#pragma once
+#include "../../include/ecmg.h"
+#include "ecmg_internal.cuh"
+
+namespace ecmg {
+
+struct SlabCfg {
+  ecmg_box dom;
+  int n0[3];
+  int L;
+  Problem prob;
+  int elem_path, exp_variant, precond, kernel_variant, zchunk;
+};
+
+struct SlabDriver;
+// P slabs; virt = all P in this process on one GPU (test fixture), else this process is `rank` of P
+// NCCL ranks (nccl_id: the 128-byte ncclUniqueId). *status receives the ecmg_status.
+SlabDriver* slab_driver_create(const SlabCfg& cfg, int P, int rank, bool virt, const unsigned char* nccl_id, int* status);
+void slab_driver_configure(SlabDriver* d, const SlabCfg& cfg);
+void slab_driver_destroy(SlabDriver* d);
+int slab_run(SlabDriver* d, double eps, ecmg_stats* per_level, double* u_out, bool u_dev, double* ut_out, bool ut_dev,
+             cudaStream_t stream);
+int slab_solve_level(SlabDriver* d, int k, double eps, int max_iter, double* u, ecmg_stats* st, cudaStream_t stream);
+void slab_level_range(const SlabDriver* d, int k, int* zlo, int* zhi);
+void slab_last_timing(const SlabDriver* d, double* ms, int* it, long long* nfree);
+int nccl_unique_id(unsigned char id[128]);
+
+}  // namespace ecmg

@@ -20,12 +20,12 @@ OK, EINVAL, ENOMEM, ENOTCONV, EBREAKDOWN, EDIAG, EMISMATCH, ECUDA, ENCCL = 0, -1
 DIRICHLET, ROBIN = 0, 1
 PROB = dict(C1=1, C2=2, C3=3, C4=4, C5=5, P1=11, P2=12, P3=13,
             PATCH_TRILINEAR=21, PATCH_LAYERED=22, PATCH_ROBIN=23, CONST_F=24)
-OPT_EXP_VARIANT, OPT_PRECOND, OPT_ZCHUNK, OPT_KERNEL, OPT_GRAPH = 1, 2, 3, 4, 5
+OPT_EXP_VARIANT, OPT_PRECOND, OPT_ZCHUNK, OPT_KERNEL, OPT_GRAPH, OPT_VIRTUAL_SLABS = 1, 2, 3, 4, 5, 6
 
 EXPORTS = ["ecmg_create_grid", "ecmg_set_coeffs", "ecmg_set_option", "ecmg_solve_level",
            "ecmg_prolongate_extrapolate", "ecmg_richardson", "ecmg_run", "ecmg_apply_operator",
            "ecmg_level_rhs", "ecmg_level_shape", "ecmg_last_jcg_timing", "ecmg_kernel_launches",
-           "ecmg_destroy_grid", "ecmg_strerror"]
+           "ecmg_slab_partition", "ecmg_nccl_unique_id", "ecmg_destroy_grid", "ecmg_strerror"]
 
 
 class ecmg_box(C.Structure):
@@ -80,6 +80,8 @@ def lib():
         L.ecmg_level_shape.argtypes = [vp, C.c_int, ip, C.POINTER(C.c_longlong), ip, ip]
         L.ecmg_last_jcg_timing.argtypes = [vp, dp, ip, C.POINTER(C.c_longlong)]
         L.ecmg_kernel_launches.argtypes = []
+        L.ecmg_slab_partition.argtypes = [C.c_int, C.c_int, C.c_int, ip, ip]
+        L.ecmg_nccl_unique_id.argtypes = [C.POINTER(C.c_ubyte)]
         L.ecmg_destroy_grid.argtypes = [vp]
         L.ecmg_strerror.argtypes = [C.c_int]
         L.ecmg_strerror.restype = C.c_char_p
@@ -182,6 +184,31 @@ def kernel_launches():
     return int(lib().ecmg_kernel_launches())
 
 
+def slab_partition(n_cells_z, nranks, rank):
+    """(sharded, z_lo, z_hi) of rank's node planes [z_lo, z_hi) on a level with n_cells_z cells."""
+    lo, hi = C.c_int(), C.c_int()
+    s = lib().ecmg_slab_partition(int(n_cells_z), int(nranks), int(rank), C.byref(lo), C.byref(hi))
+    if s < 0:
+        raise EcmgError(s, "ecmg_slab_partition")
+    return bool(s), lo.value, hi.value
+
+
+def nccl_unique_id():
+    buf = (C.c_ubyte * 128)()
+    s = lib().ecmg_nccl_unique_id(buf)
+    if s != OK:
+        raise EcmgError(s, "ecmg_nccl_unique_id")
+    return bytes(buf)
+
+
+def make_dist(rank, nranks, nccl_id: bytes):
+    d = ecmg_dist()
+    d.rank, d.nranks = int(rank), int(nranks)
+    for i, b in enumerate(nccl_id[:128]):
+        d.nccl_id[i] = b
+    return d
+
+
 def destroy_grid(grid):
     return lib().ecmg_destroy_grid(grid)
 
@@ -201,13 +228,13 @@ class Grid:
     """Owning wrapper: Grid(coarsest, levels, problem_id, params) on the current torch stream."""
 
     def __init__(self, coarsest, num_levels, problem_id, params=None, lo=(0.0, 0.0, 0.0), hi=(1.0, 1.0, 1.0),
-                 stream=None, exp_variant=0, precond=True):
+                 stream=None, exp_variant=0, precond=True, dist=None):
         import torch
         if stream is None:
             stream = torch.cuda.current_stream().cuda_stream
         coarsest = [coarsest] * 3 if isinstance(coarsest, int) else list(coarsest)
         self.coarsest, self.L, self.problem_id = coarsest, num_levels, problem_id
-        st, self.h = create_grid(lo, hi, coarsest, num_levels, stream)
+        st, self.h = create_grid(lo, hi, coarsest, num_levels, stream, dist)
         if st != OK:
             raise EcmgError(st, "ecmg_create_grid")
         self._check(set_coeffs(self.h, problem_id, default_faces(problem_id), params), "ecmg_set_coeffs")

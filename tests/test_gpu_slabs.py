@@ -1,0 +1,71 @@
+"""z-slab decomposition on one GPU (virtual slabs: device copies stand in for the NCCL halo
+messages, an in-order sum kernel for the allreduce): the sharded Alg. 4 run and
+sharded fixed-iteration solves agree with the single-GPU path and with the oracle."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as o
+import synth
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_1506_02983_b200 import Grid, ecmg
+
+
+def params_for(pid):
+    return synth.c5_geometry(0) if pid == o.C5 else None
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+@pytest.mark.parametrize("pid,levels,eps,P", [
+    (o.C2, 5, 1e-10, 2), (o.C4, 5, 1e-9, 2), (o.C4, 6, 1e-9, 4), (o.C3, 5, 1e-10, 2), (o.C5, 6, 1e-8, 4),
+    (o.C2, 6, 1e-10, 8)])
+def test_virtual_slab_run(pid, levels, eps, P):
+    g1 = Grid(4, levels, pid, params_for(pid))
+    u1, ut1 = g1.new_vec(levels - 1), g1.new_vec(levels - 1)
+    st1, s1 = g1.run(eps, u1, ut1)
+    gp = Grid(4, levels, pid, params_for(pid))
+    gp.set_option(ecmg.OPT_VIRTUAL_SLABS, P)
+    n_fine = 4 << (levels - 1)
+    assert ecmg.slab_partition(n_fine, P, 0)[0]   # the finest level is sharded
+    up, utp = gp.new_vec(levels - 1), gp.new_vec(levels - 1)
+    stp, sp = gp.run(eps, up, utp)
+    assert st1 == 0 and stp == 0
+    it1 = [s["iterations"] for s in s1]
+    itp = [s["iterations"] for s in sp]
+    assert all(abs(a - b) <= 1 for a, b in zip(it1, itp)), (it1, itp)
+    assert sp[-1]["rel_res_recur"] <= eps
+    a, b = host(up), host(u1)
+    assert np.max(np.abs(a - b)) <= 1e-9 * np.max(np.abs(b))
+    assert np.max(np.abs(host(utp) - host(ut1))) <= 1e-9 * np.max(np.abs(host(ut1)))
+    # and against the oracle
+    ost, ostats, ou, out = o.ecmg(4, levels, pid, eps, params=params_for(pid))
+    assert np.max(np.abs(a - ou)) <= 1e-9 * np.max(np.abs(ou))
+
+
+@pytest.mark.parametrize("pid,P", [(o.C2, 2), (o.C3, 2), (o.C5, 4)])
+def test_virtual_slab_fixed_iterations(pid, P):
+    level = 4   # 64^3: sharded for P = 2 and 4
+    n = (64,) * 3
+    L = o.Level(n, pid, params=params_for(pid))
+    m, _ = L.dirichlet()
+    x0 = np.where(~m, synth.random_nodal(14, n), 0.0)
+    res = []
+    for p in (1, P):
+        g = Grid(4, level + 1, pid, params_for(pid))
+        if p > 1:
+            g.set_option(ecmg.OPT_VIRTUAL_SLABS, p)
+        u = torch.from_numpy(x0.copy()).cuda()
+        st, s = g.solve_level(level, 0.0, 20, u)
+        assert st == 0 and s["iterations"] == 20
+        res.append(host(u))
+    xo, _ = L.jcg(x0, 0.0, 20)
+    d_sl = np.max(np.abs(res[1] - res[0])) / np.max(np.abs(res[0]))
+    d_or = np.max(np.abs(res[1] - xo)) / np.max(np.abs(xo))
+    assert d_sl <= 1e-12 and d_or <= 1e-12, (d_sl, d_or)
