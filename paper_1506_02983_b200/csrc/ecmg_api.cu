@@ -443,7 +443,10 @@ int ecmg_create_grid(const ecmg_box* dom, const int coarsest_cells[3], int num_l
     G->ev_init = true;
   }
   if (st == ECMG_OK && cudaStreamSynchronize(G->stream) != cudaSuccess) st = ECMG_ECUDA;
-  if (st == ECMG_OK && dist && dist->nranks > 1) {
+  // test only: ECMG_TEST_NCCL_SINGLE=1 with nranks == 1 runs the NCCL slab path on one rank
+  const bool nccl_single = dist && dist->nranks == 1 && std::getenv("ECMG_TEST_NCCL_SINGLE") != nullptr;
+  if (nccl_single) slab_force_single() = true;
+  if (st == ECMG_OK && dist && (dist->nranks > 1 || nccl_single)) {
     // NCCL ranks: the communicator is created here (collective over all ranks)
     G->nranks = dist->nranks;
     G->rank = dist->rank;

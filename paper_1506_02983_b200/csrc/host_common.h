@@ -114,8 +114,13 @@ inline long long level_nodes(const LevelGeom& g) { return (long long)(g.n[0] + 1
 // sharded iff n % (4P) == 0 and n / P >= 16 (every 4h EXP_finite block and 2h EXP_true cell then
 // lies inside one slab, and each slab has >= 16 planes); rank r owns node planes
 // [r n/P, (r+1) n/P), the last rank also plane n. Replicated levels: every rank owns [0, n+1).
+inline bool& slab_force_single() {   // test only: shard even with P = 1 (single-rank NCCL self-test)
+  static bool f = false;
+  return f;
+}
+
 inline bool slab_partition(int n, int P, int r, int* zlo, int* zhi) {
-  const bool sharded = P > 1 && n % (4 * P) == 0 && n / P >= 16;
+  const bool sharded = (P > 1 || slab_force_single()) && n % (4 * P) == 0 && n / P >= 16;
   if (!sharded) { *zlo = 0; *zhi = n + 1; return false; }
   *zlo = r * (n / P);
   *zhi = (r == P - 1) ? n + 1 : (r + 1) * (n / P);

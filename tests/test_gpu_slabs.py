@@ -69,3 +69,32 @@ def test_virtual_slab_fixed_iterations(pid, P):
     d_sl = np.max(np.abs(res[1] - res[0])) / np.max(np.abs(res[0]))
     d_or = np.max(np.abs(res[1] - xo)) / np.max(np.abs(xo))
     assert d_sl <= 1e-12 and d_or <= 1e-12, (d_sl, d_or)
+
+
+def test_nccl_single_rank_selftest():
+    # one NCCL rank with every sharded-eligible level forced onto the slab path: exercises dlopen of
+    # libnccl, ncclGetUniqueId, ncclCommInitRank and the allreduce -> finalize passes on one GPU
+    # (no inter-rank waiting). Run in a subprocess: the force flag is process-wide.
+    import subprocess, sys, os, json
+    code = r'''
+import os, sys, json
+sys.path.insert(0, os.getcwd())
+import torch, numpy as np
+from paper_1506_02983_b200 import Grid, ecmg, PROB
+nid = ecmg.nccl_unique_id()
+g1 = Grid(4, 5, PROB["C2"]); u1 = g1.new_vec(4); st1, s1 = g1.run(1e-10, u1)
+d = ecmg.make_dist(0, 1, nid)
+gn = Grid(4, 5, PROB["C2"], dist=d); un = gn.new_vec(4); stn, sn = gn.run(1e-10, un)
+torch.cuda.synchronize()
+a, b = un.cpu().numpy(), u1.cpu().numpy()
+print(json.dumps(dict(st=[st1, stn], it1=[s["iterations"] for s in s1], itn=[s["iterations"] for s in sn],
+                      d=float(np.max(np.abs(a - b)) / np.max(np.abs(b))))))
+'''
+    env = dict(os.environ, ECMG_TEST_NCCL_SINGLE="1")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert out.returncode == 0, out.stderr[-2000:]
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    assert r["st"] == [0, 0]
+    assert r["it1"] == r["itn"]
+    assert r["d"] <= 1e-13
