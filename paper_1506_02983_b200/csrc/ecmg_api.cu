@@ -25,6 +25,8 @@ using namespace ecmg;
 static std::atomic<long long> g_launches{0};
 namespace ecmg { void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); } }
 
+struct ParamHost { double eps; int max_iter; int pad; };
+
 struct ecmg_grid {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -55,8 +57,9 @@ struct ecmg_grid {
   bool ev_init = false;
   int kernel_variant = 1;   // ECMG_OPT_KERNEL
   int use_graph = 1;        // ECMG_OPT_GRAPH: device-driven JCG loop (CUDA graph, conditional WHILE node)
+  long long persistent_max = 5000;   // ECMG_OPT_PERSISTENT: one cooperative launch per solve up to this size
   cudaStream_t cap_stream = nullptr;          // private stream used only for graph capture
-  struct ParamHost { double eps; int max_iter; int pad; }* param_host = nullptr;   // pinned
+  ParamHost* param_host = nullptr;   // pinned
   std::vector<cudaGraphExec_t> graphs;        // per level, lazily built
   struct Maps { int level = -1; CUtensorMap xh, xi, rh, ri, ph[2], bi; bool ok = false; } maps;
   double last_jcg_ms = 0.0;
@@ -67,6 +70,10 @@ struct ecmg_grid {
   unsigned char nccl_id[128] = {0};
   int virt_slabs = 0;
   SlabDriver* slab = nullptr;
+  // asynchronous ecmg_run: per-level parameters / scalars (pinned) and events
+  ParamHost* lvl_param = nullptr;
+  JcgScalars* lvl_sc = nullptr;
+  std::vector<cudaEvent_t> lvl_ev;
 };
 
 namespace {
@@ -169,6 +176,23 @@ int setup_level(ecmg_grid* G, int k) {
 }
 
 
+int stats_from(const JcgScalars& s, double eps, ecmg_stats* st) {
+  const double nb = std::sqrt(s.bb);
+  const double nbe = nb > 0.0 ? nb : 1.0;
+  int status = s.status;
+  const bool conv = (eps <= 0.0) || !(std::sqrt(s.rr) > eps * nbe);
+  if (status == ECMG_OK && !conv) status = ECMG_ENOTCONV;
+  if (st) {
+    st->iterations = s.iter;
+    st->rel_res_recur = std::sqrt(s.rr) / nbe;
+    st->rel_res_true = std::sqrt(s.rr_true) / nbe;
+    st->norm_b = nb;
+    st->converged = conv && status == ECMG_OK;
+    st->status = status;
+  }
+  return status;
+}
+
 int fill_stats(ecmg_grid* G, const LevelGeom& g, double eps, ecmg_stats* st) {
   const JcgScalars s = G->sc_host[0];
   G->last_jcg_iters = s.iter;
@@ -269,6 +293,43 @@ int run_jcg_graph(ecmg_grid* G, int k, double eps, ecmg_stats* st) {
   return fill_stats(G, g, eps, st);
 }
 
+// small constant-stencil levels: the whole solve in one cooperative launch (latency bound)
+int run_jcg_persistent(ecmg_grid* G, int k, double eps, ecmg_stats* st) {
+  const LevelGeom& g = G->geom[k];
+  const ConstStencil cs = make_const_stencil(g, 1.0, G->precond);
+  ECMG_CUDA(cudaEventRecord(G->ev[0], G->stream));
+  ECMG_CUDA(launch_jcg_persistent(g, cs, G->x, G->r, G->p[0], G->p[1], G->b, G->partials, G->sc, G->stream));
+  ECMG_CUDA(cudaEventRecord(G->ev[1], G->stream));
+  ECMG_CUDA(cudaMemcpyAsync(&G->sc_host[0], G->sc, sizeof(JcgScalars), cudaMemcpyDeviceToHost, G->stream));
+  ECMG_CUDA(cudaStreamSynchronize(G->stream));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, G->ev[0], G->ev[1]);
+  G->last_jcg_ms = ms;
+  return fill_stats(G, g, eps, st);
+}
+
+// Enqueue a device-driven JCG solve (graph or persistent path) without any host synchronisation;
+// the final scalars land in *slot (pinned) when the stream reaches them. Returns ECMG_EINVAL if
+// the level needs the host loop (ablation path).
+int enqueue_jcg(ecmg_grid* G, int k, double eps, int max_iter, ParamHost* param, JcgScalars* slot) {
+  const LevelGeom& g = G->geom[k];
+  const bool persistent = !G->elem_path && G->persistent_max > 0 && free_count(g) <= G->persistent_max;
+  if (!(eps > 0.0) || (!persistent && !G->use_graph)) return ECMG_EINVAL;
+  param->eps = eps;
+  param->max_iter = max_iter;
+  ECMG_CUDA(cudaMemcpyAsync(&G->sc->eps_in, param, sizeof(double) + sizeof(int), cudaMemcpyHostToDevice, G->stream));
+  if (persistent) {
+    ECMG_CUDA(launch_jcg_persistent(g, make_const_stencil(g, 1.0, G->precond), G->x, G->r, G->p[0], G->p[1], G->b,
+                                    G->partials, G->sc, G->stream));
+  } else {
+    if ((int)G->graphs.size() != G->L) G->graphs.assign(G->L, nullptr);
+    if (!G->graphs[k]) ECMG_CUDA(build_level_graph(G, k, &G->graphs[k]));
+    ECMG_CUDA(cudaGraphLaunch(G->graphs[k], G->stream));
+  }
+  ECMG_CUDA(cudaMemcpyAsync(slot, G->sc, sizeof(JcgScalars), cudaMemcpyDeviceToHost, G->stream));
+  return ECMG_OK;
+}
+
 // JCG on the level whose RHS is in G->b, starting from G->x. Fills stats (except timings).
 int run_jcg(ecmg_grid* G, int k, double eps, int max_iter, ecmg_stats* st) {
   const LevelGeom& g = G->geom[k];
@@ -283,6 +344,8 @@ int run_jcg(ecmg_grid* G, int k, double eps, int max_iter, ecmg_stats* st) {
   G->param_host->eps = eps;
   G->param_host->max_iter = max_iter;
   ECMG_CUDA(cudaMemcpyAsync(&G->sc->eps_in, G->param_host, sizeof(double) + sizeof(int), cudaMemcpyHostToDevice, G->stream));
+  if (!G->elem_path && G->persistent_max > 0 && free_count(g) <= G->persistent_max)
+    return run_jcg_persistent(G, k, eps, st);
   if (eps > 0.0 && G->use_graph) return run_jcg_graph(G, k, eps, st);
   // r = b - A x, rho = r.z, rr = r.r, stop test
   {
@@ -435,6 +498,12 @@ int ecmg_create_grid(const ecmg_box* dom, const int coarsest_cells[3], int num_l
   if (st == ECMG_OK && cudaHostAlloc(&G->param_host, sizeof(*G->param_host), cudaHostAllocDefault) != cudaSuccess) st = ECMG_ENOMEM;
   if (st == ECMG_OK && cudaStreamCreateWithFlags(&G->cap_stream, cudaStreamNonBlocking) != cudaSuccess) st = ECMG_ECUDA;
   G->graphs.assign(num_levels, nullptr);
+  if (st == ECMG_OK && cudaHostAlloc(&G->lvl_param, sizeof(ParamHost) * num_levels, cudaHostAllocDefault) != cudaSuccess) st = ECMG_ENOMEM;
+  if (st == ECMG_OK && cudaHostAlloc(&G->lvl_sc, sizeof(JcgScalars) * num_levels, cudaHostAllocDefault) != cudaSuccess) st = ECMG_ENOMEM;
+  if (st == ECMG_OK) {
+    G->lvl_ev.assign(5 * num_levels, nullptr);
+    for (auto& e : G->lvl_ev) cudaEventCreate(&e);
+  }
   if (st == ECMG_OK && (init_tma_kernel_attributes() != cudaSuccess || init_elem_kernel_attributes() != cudaSuccess ||
                         init_setup_kernel_attributes() != cudaSuccess))
     st = ECMG_ECUDA;
@@ -477,6 +546,9 @@ int ecmg_destroy_grid(ecmg_grid* G) {
   cudaFree(G->seeds);
   if (G->sc_host) cudaFreeHost(G->sc_host);
   if (G->param_host) cudaFreeHost(G->param_host);
+  if (G->lvl_param) cudaFreeHost(G->lvl_param);
+  if (G->lvl_sc) cudaFreeHost(G->lvl_sc);
+  for (auto& e : G->lvl_ev) if (e) cudaEventDestroy(e);
   clear_graphs(G);
   if (G->cap_stream) cudaStreamDestroy(G->cap_stream);
   if (G->ev_init) for (int i = 0; i < 16; ++i) cudaEventDestroy(G->ev[i]);
@@ -530,6 +602,7 @@ int ecmg_set_option(ecmg_grid* G, int option, int value) {
     case ECMG_OPT_ZCHUNK: if (value < 0) return ECMG_EINVAL; G->zchunk = value; clear_graphs(G); break;
     case ECMG_OPT_KERNEL: if (value != 0 && value != 1) return ECMG_EINVAL; G->kernel_variant = value; clear_graphs(G); break;
     case ECMG_OPT_GRAPH: if (value != 0 && value != 1) return ECMG_EINVAL; G->use_graph = value; break;
+    case ECMG_OPT_PERSISTENT: if (value < 0) return ECMG_EINVAL; G->persistent_max = value; break;
     case ECMG_OPT_VIRTUAL_SLABS: {
       if (value < 0 || value > 16 || G->nranks > 1) return ECMG_EINVAL;
       if (G->slab) { slab_driver_destroy(G->slab); G->slab = nullptr; }
@@ -674,50 +747,66 @@ int ecmg_run(ecmg_grid* G, double eps, ecmg_stats* per_level, double* u_fine, do
   }
   int status = ECMG_OK;
   std::vector<ecmg_stats> stv(G->L);
-  std::vector<float> t_setup(G->L), t_exp(G->L), t_solve(G->L), t_rich(G->L);
+  std::vector<char> async(G->L, 0);
+  for (auto& st : stv) std::memset(&st, 0, sizeof(st));
+  // the whole cascade is enqueued without host synchronisation when every solve is device driven
   for (int k = 0; k < G->L; ++k) {
     const LevelGeom& g = G->geom[k];
     ecmg_stats& st = stv[k];
-    std::memset(&st, 0, sizeof(st));
-    cudaEvent_t e0 = G->ev[8], e1 = G->ev[9], e2 = G->ev[10], e3 = G->ev[11], e4 = G->ev[12];
-    ECMG_CUDA(cudaEventRecord(e0, G->stream));
+    cudaEvent_t* e = &G->lvl_ev[5 * k];
+    ECMG_CUDA(cudaEventRecord(e[0], G->stream));
     { int s = setup_level(G, k); if (s) return s; }
-    ECMG_CUDA(cudaEventRecord(e1, G->stream));
-    int s;
+    ECMG_CUDA(cudaEventRecord(e[1], G->stream));
     if (k < 2) {
       // DSOLVE (Alg. 4 l.1-2): JCG from a zero free guess to 1e-14 (reading §8c A12)
       ECMG_CUDA(launch_zero_vec(g, G->x, G->stream));
-      ECMG_CUDA(cudaEventRecord(e2, G->stream));
-      s = run_jcg(G, k, 1e-14, 10000, &st);
-      if (s == ECMG_ENOTCONV) s = ECMG_OK;   // tiny systems may stall just above 1e-14; accepted
     } else {
-      // W_h = EXP_finite(u_2h, u_4h) (Alg. 4 l.6), then JCG from W_h (l.7-9)
-      // written straight into the free-box work vector (Dirichlet values are filled after the solve)
+      // W_h = EXP_finite(u_2h, u_4h) (Alg. 4 l.6), written straight into the free-box work vector
       ECMG_CUDA(launch_exp_finite(g, G->prob, G->u[k - 1], G->u[k - 2], G->x, G->exp_variant, G->seeds, 1, G->stream));
-      ECMG_CUDA(cudaEventRecord(e2, G->stream));
-      s = run_jcg(G, k, eps, 10000, &st);
+    }
+    ECMG_CUDA(cudaEventRecord(e[2], G->stream));
+    const double eps_k = k < 2 ? 1e-14 : eps;   // JCG from W_h (l.7-9)
+    int s = enqueue_jcg(G, k, eps_k, 10000, &G->lvl_param[k], &G->lvl_sc[k]);
+    if (s == ECMG_OK) {
+      async[k] = 1;
+    } else if (s == ECMG_EINVAL) {
+      s = run_jcg(G, k, eps_k, 10000, &st);   // host loop (ablation path)
+      if (k < 2 && s == ECMG_ENOTCONV) s = ECMG_OK;
+      if (s != ECMG_OK && status == ECMG_OK) status = s;
     }
     if (s == ECMG_ECUDA || s == ECMG_ENOMEM) return s;
-    if (s != ECMG_OK && status == ECMG_OK) status = s;
     ECMG_CUDA(launch_scatter(g, G->x, G->u[k], G->stream));
     ECMG_CUDA(launch_dirichlet_fill(g, G->prob, G->u[k], 0.0, 0, G->stream));
-    ECMG_CUDA(cudaEventRecord(e3, G->stream));
+    ECMG_CUDA(cudaEventRecord(e[3], G->stream));
     if (k >= 2 && k == G->L - 1 && ut_fine) {
       // u~_h = EXP_true(u_h, u_2h) (Alg. 4 l.10) on the finest level
       ECMG_CUDA(launch_exp_true(g, G->prob, G->u[k], G->u[k - 1], ut_dev ? ut_fine : G->ut_tmp, G->stream));
     }
-    ECMG_CUDA(cudaEventRecord(e4, G->stream));
-    ECMG_CUDA(cudaEventSynchronize(e4));
-    st.ms_setup = elapsed(e0, e1);
-    st.ms_exp = elapsed(e1, e2);
-    st.ms_solve = elapsed(e2, e3);
-    st.ms_rich = elapsed(e3, e4);
+    ECMG_CUDA(cudaEventRecord(e[4], G->stream));
   }
   ECMG_CUDA(cudaMemcpyAsync(u_fine, G->u[G->L - 1], sizeof(double) * Nf,
                             u_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, G->stream));
   if (ut_fine && !ut_dev)
     ECMG_CUDA(cudaMemcpyAsync(ut_fine, G->ut_tmp, sizeof(double) * Nf, cudaMemcpyDeviceToHost, G->stream));
   ECMG_CUDA(cudaStreamSynchronize(G->stream));
+  for (int k = 0; k < G->L; ++k) {
+    ecmg_stats& st = stv[k];
+    if (async[k]) {
+      int s = stats_from(G->lvl_sc[k], k < 2 ? 1e-14 : eps, &st);
+      if (k < 2 && s == ECMG_ENOTCONV) s = ECMG_OK;
+      if (s != ECMG_OK && status == ECMG_OK) status = s;
+    }
+    cudaEvent_t* e = &G->lvl_ev[5 * k];
+    st.ms_setup = elapsed(e[0], e[1]);
+    st.ms_exp = elapsed(e[1], e[2]);
+    st.ms_solve = elapsed(e[2], e[3]);
+    st.ms_rich = elapsed(e[3], e[4]);
+  }
+  if (async[G->L - 1]) {
+    G->last_jcg_iters = G->lvl_sc[G->L - 1].iter;
+    G->last_free = free_count(G->geom[G->L - 1]);
+    G->last_jcg_ms = elapsed(G->lvl_ev[5 * (G->L - 1) + 2], G->lvl_ev[5 * (G->L - 1) + 3]);
+  }
   if (per_level) for (int k = 0; k < G->L; ++k) per_level[k] = stv[k];
   return status;
 }

@@ -99,9 +99,20 @@ __global__ void k_rhs_sep(const LevelGeom g, const Problem pb, const double* __r
 // f specialised per problem at compile time (PID = 0: generic registry switch)
 template <int PID>
 __device__ __forceinline__ double f_at(const Problem& pb, double x, double y, double z) {
-  if (PID == 4) {   // C4: -(15/4) r^{-1/2}
+  if (PID == 4) {   // C4: -(15/4) r^{-1/2} = -(15/4) (r^2)^{-1/4}
     const double r2 = x * x + y * y + z * z;
-    return r2 == 0.0 ? 0.0 : -3.75 * rsqrt(sqrt(r2));
+    if (r2 == 0.0) return 0.0;
+    if (r2 < 1e-30) return -3.75 * rsqrt(sqrt(r2));   // below the fp32 seed's range
+    // y = (r^2)^{-1/4}: fp32 seed (rel. error ~1e-7) + two fp64 Newton steps for y^-4 = r^2,
+    // y <- y (5 - r^2 y^4) / 4 (quadratic: 1e-7 -> 1e-14 -> rounding level); avoids the fp64
+    // MUFU sqrt / rsqrt sequences that bound this kernel
+    const float r2f = (float)r2;
+    double yv = (double)rsqrtf(sqrtf(r2f));
+    double y2 = yv * yv;
+    yv = yv * __fma_rn(-r2, y2 * y2, 5.0) * 0.25;
+    y2 = yv * yv;
+    yv = yv * __fma_rn(-r2, y2 * y2, 5.0) * 0.25;
+    return -3.75 * yv;
   }
   return prob_f(pb, x, y, z);
 }
@@ -109,8 +120,9 @@ __device__ __forceinline__ double f_at(const Problem& pb, double x, double y, do
 template <int PID>
 __global__ void __launch_bounds__(VNTH, 3) k_rhs_vol(const LevelGeom g, const Problem pb, double* __restrict__ b, int zc) {
   extern __shared__ double vs[];
-  double* fq = vs;              // [VNE][8] f at the Gauss points of one element plane
-  double* Fe = vs + VNE * 8;    // [2][VNE][8] element load vectors, ring of two element planes
+  // structure-of-arrays layouts (consecutive threads -> consecutive doubles: no bank conflicts)
+  double* fq = vs;              // fq[q * VNE + e]: f at Gauss point q of element e of the plane
+  double* Fe = vs + VNE * 8;    // Fe[slot][a * VNE + e]: element load vectors, ring of two planes
   const int lane = threadIdx.x, w = threadIdx.y, tid = lane + VX * w;
   const int X0 = blockIdx.x * VX, Y0 = blockIdx.y * VY;
   const int z0 = g.zbeg + blockIdx.z * zc, z1 = min(z0 + zc, g.zend);   // local planes
@@ -120,7 +132,7 @@ __global__ void __launch_bounds__(VNTH, 3) k_rhs_vol(const LevelGeom g, const Pr
     // (a) f at the 8 Gauss points of every element of the plane (33 x 9 x 8 evaluations)
     const int gez = g.flo[2] + g.zoff + fez;
     for (int t = tid; t < VNE * 8; t += VNTH) {
-      const int e = t >> 3, q = t & 7;
+      const int q = t / VNE, e = t - q * VNE;
       const int gex = g.flo[0] + X0 - 1 + e % VEX, gey = g.flo[1] + Y0 - 1 + e / VEX;
       double v = 0.0;
       if (gex >= 0 && gex < g.n[0] && gey >= 0 && gey < g.n[1] && gez >= 0 && gez < g.n[2]) {
@@ -134,8 +146,9 @@ __global__ void __launch_bounds__(VNTH, 3) k_rhs_vol(const LevelGeom g, const Pr
     // (b) element load vectors F_e[a] = detJ sum_q f_q N_a(q): a 2x2x2 tensor transform
     double* Fp = Fe + (fez & 1) * VNE * 8;
     for (int e = tid; e < VNE; e += VNTH) {
-      double t1[8], t2[8];
-      const double* f = fq + e * 8;
+      double f[8], t1[8], t2[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) f[q] = fq[q * VNE + e];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {   // along x: node bit 0 vs Gauss bit 0
         const int qb = i & ~1;
@@ -149,7 +162,7 @@ __global__ void __launch_bounds__(VNTH, 3) k_rhs_vol(const LevelGeom g, const Pr
 #pragma unroll
       for (int i = 0; i < 8; ++i) {   // along z
         const int qb = i & ~4;
-        Fp[e * 8 + i] = detJ * ((i & 4) ? (wB * t2[qb] + wA * t2[qb | 4]) : (wA * t2[qb] + wB * t2[qb | 4]));
+        Fp[i * VNE + e] = detJ * ((i & 4) ? (wB * t2[qb] + wA * t2[qb | 4]) : (wA * t2[qb] + wB * t2[qb | 4]));
       }
     }
     __syncthreads();
@@ -161,7 +174,7 @@ __global__ void __launch_bounds__(VNTH, 3) k_rhs_vol(const LevelGeom g, const Pr
       for (int e = 0; e < 8; ++e) {
         const int ex = e & 1, ey = (e >> 1) & 1, ez = (e >> 2) & 1;   // element = node - 1 + e_d
         const int a = (1 - ex) | ((1 - ey) << 1) | ((1 - ez) << 2);
-        v += Fe[((fz - 1 + ez) & 1) * VNE * 8 + ((lane + ex) + VEX * (w + ey)) * 8 + a];
+        v += Fe[((fz - 1 + ez) & 1) * VNE * 8 + a * VNE + (lane + ex) + VEX * (w + ey)];
       }
       b[(long long)fz * g.S + (long long)fy * g.P + fx] = v;
     }

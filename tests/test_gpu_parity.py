@@ -260,3 +260,19 @@ def test_graph_loop_equals_host_loop(pid, eps):
         res.append(([s["iterations"] for s in stats], host(u), host(ut)))
     assert res[0][0] == res[1][0]
     assert np.array_equal(res[0][1], res[1][1]) and np.array_equal(res[0][2], res[1][2])
+
+
+@pytest.mark.parametrize("pid,eps", [(o.C1, 1e-8), (o.C2, 1e-10), (o.C4, 1e-9)])
+def test_persistent_small_levels_vs_graph(pid, eps):
+    # small constant-stencil levels run in one cooperative launch (ECMG_OPT_PERSISTENT); the
+    # z-marching graph path is the reference: same counts (+-1), iterates within rounding
+    res = []
+    for pmax in (300000, 0):
+        g = Grid(4, 5, pid)
+        g.set_option(ecmg.OPT_PERSISTENT, pmax)
+        u = g.new_vec(4)
+        st, stats = g.run(eps, u)
+        assert st == 0
+        res.append(([s["iterations"] for s in stats], host(u)))
+    assert all(abs(a - b) <= 1 for a, b in zip(res[0][0], res[1][0]))
+    assert np.max(np.abs(res[0][1] - res[1][1])) <= 1e-9 * np.max(np.abs(res[1][1]))
