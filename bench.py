@@ -38,11 +38,14 @@ UNIT = "unknown-iters/s"
 BYTES_PER_UNKNOWN_ITER = 64   # x 1R+1W, r 2R+1W, p 2R+1W (constant-beta path)
 
 CONFIGS = {
-    # name: (problem id, coarsest, levels, eps, description)
+    # name: (problem id, coarsest, levels, eps, description); C3 / C5 run the element-beta path (80 B/unknown)
     "c4": (4, 4, 8, 1e-9, "C4 (BASELINE configs[3]): u=r^{3/2}, beta=1, Dirichlet, Q1, 4^3->512^3, eps=1e-9"),
     "c2": (2, 4, 6, 1e-10, "C2 (BASELINE configs[1]): u=exp(x+y+z), beta=1, Dirichlet, Q1, 4^3->128^3, eps=1e-10"),
     "c1": (1, 4, 4, 1e-8, "C1 (BASELINE configs[0]): u=sin sin sin, beta=1, Dirichlet, Q1, 4^3->32^3, eps=1e-8"),
+    "c3": (3, 4, 7, 1e-10, "C3 (BASELINE configs[2]): variable beta, Robin z=1, Q1, 4^3->256^3, eps=1e-10"),
+    "c5": (5, 4, 9, 1e-8, "C5 (BASELINE configs[4]): layered geology (seed 0), Dirichlet, Q1, 4^3->1024^3, eps=1e-8"),
 }
+BYTES_PER_UNKNOWN_ITER_ELEM = 80   # element-beta path: + beta_e read in K1 and K2
 
 
 def load_peaks():
@@ -111,7 +114,8 @@ def cpu_oracle_sample(cfg_name, max_seconds_hint=30.0):
     pid, n0, levels, eps, _ = CONFIGS[cfg_name]
     sample_levels = min(levels, 6)   # 4^3 -> 128^3
     t0 = time.perf_counter()
-    st, stats, _, _ = oracle.ecmg(n0, sample_levels, pid, eps)
+    import synth
+    st, stats, _, _ = oracle.ecmg(n0, sample_levels, pid, eps, params=synth.c5_geometry(0) if pid == 5 else None)
     dt = time.perf_counter() - t0
     units = float(sum(max(0, r[0]) * r[16] for r in stats))
     return {"value": units / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
@@ -171,7 +175,9 @@ def main():
         # z-slab decomposition over NCCL ranks (strong scaling of the same C4 problem)
         from paper_1506_02983_b200 import dist as edist
         gdist = edist.ecmg_dist_from_torch(device=torch.device("cuda", local))
-    grid = Grid(n0, levels, pid, dist=gdist)
+    import synth as _synth
+    params = _synth.c5_geometry(0) if pid == 5 else None
+    grid = Grid(n0, levels, pid, params, dist=gdist)
     shape, nodes = grid.shape(levels - 1)      # nodes: this rank's planes of the finest level
     zlo, zhi = ecmg.level_shape(grid.h, levels - 1)[3:5]
     u = torch.empty(nodes, dtype=torch.float64, device="cuda")
@@ -259,7 +265,8 @@ def main():
     tts_hostloop = max_over_ranks(ev_h[0].elapsed_time(ev_h[1]))
     grid.set_option(ecmg.OPT_GRAPH, 1)
     peak, peak_src = load_peaks()
-    achieved = BYTES_PER_UNKNOWN_ITER * nf_j * it_j / (ms_j / 1e3) / 1e9 / ws   # per GPU
+    bpu = BYTES_PER_UNKNOWN_ITER_ELEM if pid in (3, 5) else BYTES_PER_UNKNOWN_ITER
+    achieved = bpu * nf_j * it_j / (ms_j / 1e3) / 1e9 / ws   # per GPU
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "jcg_traffic.json")) as f:
@@ -317,7 +324,7 @@ def main():
                                             "kernel": "register-prefetch loads (ECMG_OPT_KERNEL=0)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "kernel": "jcg K1+K2 (one CG iteration)",
-                         "bytes_per_unit": BYTES_PER_UNKNOWN_ITER, "peak_source": peak_src,
+                         "bytes_per_unit": bpu, "peak_source": peak_src,
                          "per": "GPU (average over ranks)"},
             "cpu_baseline": cpu,
             "e2e": e2e,

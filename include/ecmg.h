@@ -155,6 +155,13 @@ int ecmg_richardson(ecmg_grid* grid, int level, const double* uh, const double* 
  * Returns the first failing level's status (ECMG_ENOTCONV etc.) or ECMG_OK. */
 int ecmg_run(ecmg_grid* grid, double eps, ecmg_stats* per_level, double* u_fine, double* ut_fine);
 
+/* Alg. 3, the original ECMG the paper starts from: the same cascade, but each ECMG
+ * level j = 1..L (L = num_levels - 2) runs exactly m_j = ceil(m_L * ratio^(L-j)) iterations
+ * (Eq. ee; the paper's suggested setting is m_L = 4, ratio = 4) instead of the
+ * relative-residual test. The paper's Alg. 3 uses plain CG: set ECMG_OPT_PRECOND = 0 for that.
+ * Single GPU only (ECMG_EINVAL with slabs). Outputs as ecmg_run. */
+int ecmg_run_fixed(ecmg_grid* grid, int m_L, double ratio, ecmg_stats* per_level, double* u_fine, double* ut_fine);
+
 /* Diagnostics used by the parity tests (same kernels as the solve):
  * ecmg_apply_operator: q = A_ff p on free nodes, q = 0 on Dirichlet nodes (p's Dirichlet entries
  *   are ignored). ecmg_level_rhs: lifted right-hand side b_f = F_f + G_f - A_fD g_D on free nodes,

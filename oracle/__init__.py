@@ -80,6 +80,9 @@ def lib():
             L.orc_ecmg.restype = C.c_int
             L.orc_ecmg.argtypes = [dp, dp, ip, C.c_int, C.c_int, dp, C.c_int, ip, C.c_double, C.c_int,
                                    C.c_int, C.c_int, dp, dp, dp, dp]
+            L.orc_ecmg_fixed.restype = C.c_int
+            L.orc_ecmg_fixed.argtypes = [dp, dp, ip, C.c_int, C.c_int, dp, C.c_int, ip, C.c_int, C.c_double,
+                                         C.c_int, C.c_int, dp, dp, dp, dp]
             _lib = L
     return _lib
 
@@ -242,3 +245,22 @@ def ecmg(n0, levels, problem_id, eps, params=None, lo=(0, 0, 0), hi=(1, 1, 1), f
     if want_w:
         return st, stats, u, ut, w
     return st, stats, u, ut
+
+
+def ecmg_fixed(n0, levels, problem_id, m_L, ratio, params=None, lo=(0, 0, 0), hi=(1, 1, 1), faces=None,
+               precond=False, exp_variant=0, want_w=False):
+    """Alg. 3: fixed m_j = ceil(m_L ratio^(L-j)) CG iterations on the j-th ECMG level."""
+    n0 = np.array([n0] * 3 if np.isscalar(n0) else list(n0), dtype=np.int32)
+    nf = n0 * (1 << (levels - 1))
+    N = int(np.prod(nf + 1))
+    stats = np.empty(levels * NSTAT)
+    u, ut = np.empty(N), np.empty(N)
+    w = np.empty(N) if want_w else None
+    prm = _f64(params if params is not None else np.zeros(1))
+    fc = np.array(faces if faces is not None else default_faces(problem_id), dtype=np.int32)
+    st = lib().orc_ecmg_fixed(_d(_f64(lo)), _d(_f64(hi)), _i(n0), int(levels), int(problem_id), _d(prm),
+                              int(prm.size if params is not None else 0), _i(fc), int(m_L), float(ratio),
+                              1 if precond else 0, int(exp_variant), _d(stats), _d(u), _d(ut),
+                              _d(w) if w is not None else None)
+    stats = stats.reshape(levels, NSTAT)
+    return (st, stats, u, ut, w) if want_w else (st, stats, u, ut)

@@ -818,9 +818,11 @@ void orc_serendipity_weights(double xi, double eta, double zeta, double* w20) {
 // Lagrange. precond 1 = ECMG_jcg, 0 = ECMG_cg. Levels 0..num_levels-1, level k has coarsest*2^k cells per axis.
 // u_fine / ut_fine (may be NULL) receive u_h and u~_h of the finest level; w_fine (may be NULL)
 // receives W_h of the finest level. Errors are NaN when the problem has no exact solution.
-int orc_ecmg(const double* lo, const double* hi, const int* coarsest, int num_levels, int problem_id,
-             const double* params, int nparams, const int* face, double eps, int max_iter, int precond,
-             int exp_variant, double* stats, double* u_fine, double* ut_fine, double* w_fine) {
+// Shared body of Alg. 4 and Alg. 3: level k >= 2 solves with (eps_k[k], maxit_k[k]); eps_k <= 0
+// means exactly maxit_k[k] CG / JCG iterations (Alg. 3's fixed counts).
+static int ecmg_impl(const double* lo, const double* hi, const int* coarsest, int num_levels, int problem_id,
+                     const double* params, int nparams, const int* face, const double* eps_k, const int* maxit_k,
+                     int precond, int exp_variant, double* stats, double* u_fine, double* ut_fine, double* w_fine) {
   Problem P;
   if (!make_problem(problem_id, params, nparams, face, &P)) return ORC_EINVAL;
   if (num_levels < 3) return ORC_EINVAL;
@@ -862,7 +864,7 @@ int orc_ecmg(const double* lo, const double* hi, const int* coarsest, int num_le
       row[12] = t2 - t1;
       u = w;
       // while ||A u - f|| > eps ||f||: u <= JCG(A, u, f)  (Alg. 4 l.7-9)
-      SolveStats st = jcg(*L, u.data(), eps, max_iter, precond);
+      SolveStats st = jcg(*L, u.data(), eps_k[k], maxit_k[k], precond);
       double t3 = now_s();
       row[13] = t3 - t2;
       row[0] = st.iterations; row[1] = st.rel_recur; row[2] = st.rel_true; row[15] = st.status;
@@ -901,6 +903,34 @@ int orc_ecmg(const double* lo, const double* hi, const int* coarsest, int num_le
     delete L;
   }
   return status;
+}
+
+int orc_ecmg(const double* lo, const double* hi, const int* coarsest, int num_levels, int problem_id,
+             const double* params, int nparams, const int* face, double eps, int max_iter, int precond,
+             int exp_variant, double* stats, double* u_fine, double* ut_fine, double* w_fine) {
+  if (num_levels < 3 || num_levels > 16) return ORC_EINVAL;
+  std::vector<double> e(num_levels, eps);
+  std::vector<int> m(num_levels, max_iter);
+  return ecmg_impl(lo, hi, coarsest, num_levels, problem_id, params, nparams, face, e.data(), m.data(), precond,
+                   exp_variant, stats, u_fine, ut_fine, w_fine);
+}
+
+// Alg. 3: the original ECMG with a fixed number of iterations per level, Eq. (ee)
+// (P:290-295): m_j = ceil(m_L * ratio^(L-j)) on the j-th ECMG level (j = 1..L, L = num_levels - 2;
+// reading R4 in DESIGN.md), plain CG by default (precond = 0). Levels 0, 1: DSOLVE.
+int orc_ecmg_fixed(const double* lo, const double* hi, const int* coarsest, int num_levels, int problem_id,
+                   const double* params, int nparams, const int* face, int m_L, double ratio, int precond,
+                   int exp_variant, double* stats, double* u_fine, double* ut_fine, double* w_fine) {
+  if (num_levels < 3 || num_levels > 16 || m_L < 0 || !(ratio > 0.0)) return ORC_EINVAL;
+  const int Lc = num_levels - 2;
+  std::vector<double> e(num_levels, 0.0);
+  std::vector<int> m(num_levels, 0);
+  for (int k = 2; k < num_levels; ++k) {
+    const int j = k - 1;   // j-th ECMG level, j = 1..Lc
+    m[k] = (int)std::ceil(m_L * std::pow(ratio, (double)(Lc - j)) - 1e-12);
+  }
+  return ecmg_impl(lo, hi, coarsest, num_levels, problem_id, params, nparams, face, e.data(), m.data(), precond,
+                   exp_variant, stats, u_fine, ut_fine, w_fine);
 }
 
 }  // extern "C"

@@ -721,18 +721,16 @@ int ecmg_last_jcg_timing(const ecmg_grid* G, double* ms, int* iterations, long l
   return ECMG_OK;
 }
 
-int ecmg_run(ecmg_grid* G, double eps, ecmg_stats* per_level, double* u_fine, double* ut_fine) {
+}  // extern "C"
+
+// Alg. 4 / Alg. 3 cascade with per-level (eps, max_iter) for the ECMG levels k >= 2 (eps <= 0:
+// exactly max_iter iterations). Levels 0, 1: DSOLVE.
+static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const std::vector<int>& maxit_lv,
+                       ecmg_stats* per_level, double* u_fine, double* ut_fine) {
+  const double eps = eps_lv.back();
   if (!G || !G->has_problem || !u_fine) return ECMG_EINVAL;
   for (int k = 2; k < G->L; ++k)
     for (int d = 0; d < 3; ++d) if (G->geom[k].n[d] % 4) return ECMG_EMISMATCH;
-  if (G->slab) {
-    std::vector<ecmg_stats> stv(G->L);
-    const int s = slab_run(G->slab, eps, stv.data(), u_fine, is_device_ptr(u_fine), ut_fine,
-                           ut_fine ? is_device_ptr(ut_fine) : false, G->stream);
-    slab_last_timing(G->slab, &G->last_jcg_ms, &G->last_jcg_iters, &G->last_free);
-    if (per_level) for (int k = 0; k < G->L; ++k) per_level[k] = stv[k];
-    return s;
-  }
   if ((int)G->u.size() != G->L) {
     for (double* p : G->u) cudaFree(p);
     G->u.assign(G->L, nullptr);
@@ -765,12 +763,13 @@ int ecmg_run(ecmg_grid* G, double eps, ecmg_stats* per_level, double* u_fine, do
       ECMG_CUDA(launch_exp_finite(g, G->prob, G->u[k - 1], G->u[k - 2], G->x, G->exp_variant, G->seeds, 1, G->stream));
     }
     ECMG_CUDA(cudaEventRecord(e[2], G->stream));
-    const double eps_k = k < 2 ? 1e-14 : eps;   // JCG from W_h (l.7-9)
-    int s = enqueue_jcg(G, k, eps_k, 10000, &G->lvl_param[k], &G->lvl_sc[k]);
+    const double eps_k = k < 2 ? 1e-14 : eps_lv[k];   // JCG from W_h (l.7-9)
+    const int maxit_k = k < 2 ? 10000 : maxit_lv[k];
+    int s = enqueue_jcg(G, k, eps_k, maxit_k, &G->lvl_param[k], &G->lvl_sc[k]);
     if (s == ECMG_OK) {
       async[k] = 1;
     } else if (s == ECMG_EINVAL) {
-      s = run_jcg(G, k, eps_k, 10000, &st);   // host loop (ablation path)
+      s = run_jcg(G, k, eps_k, maxit_k, &st);   // host loop (ablation path / fixed counts)
       if (k < 2 && s == ECMG_ENOTCONV) s = ECMG_OK;
       if (s != ECMG_OK && status == ECMG_OK) status = s;
     }
@@ -792,7 +791,7 @@ int ecmg_run(ecmg_grid* G, double eps, ecmg_stats* per_level, double* u_fine, do
   for (int k = 0; k < G->L; ++k) {
     ecmg_stats& st = stv[k];
     if (async[k]) {
-      int s = stats_from(G->lvl_sc[k], k < 2 ? 1e-14 : eps, &st);
+      int s = stats_from(G->lvl_sc[k], k < 2 ? 1e-14 : eps_lv[k], &st);
       if (k < 2 && s == ECMG_ENOTCONV) s = ECMG_OK;
       if (s != ECMG_OK && status == ECMG_OK) status = s;
     }
@@ -808,7 +807,35 @@ int ecmg_run(ecmg_grid* G, double eps, ecmg_stats* per_level, double* u_fine, do
     G->last_jcg_ms = elapsed(G->lvl_ev[5 * (G->L - 1) + 2], G->lvl_ev[5 * (G->L - 1) + 3]);
   }
   if (per_level) for (int k = 0; k < G->L; ++k) per_level[k] = stv[k];
+  (void)eps;
   return status;
+}
+
+extern "C" {
+
+int ecmg_run(ecmg_grid* G, double eps, ecmg_stats* per_level, double* u_fine, double* ut_fine) {
+  if (!G || !G->has_problem || !u_fine || !(eps > 0.0)) return ECMG_EINVAL;
+  if (G->slab) {
+    for (int k = 2; k < G->L; ++k)
+      for (int d = 0; d < 3; ++d) if (G->geom[k].n[d] % 4) return ECMG_EMISMATCH;
+    std::vector<ecmg_stats> stv(G->L);
+    const int s = slab_run(G->slab, eps, stv.data(), u_fine, is_device_ptr(u_fine), ut_fine,
+                           ut_fine ? is_device_ptr(ut_fine) : false, G->stream);
+    slab_last_timing(G->slab, &G->last_jcg_ms, &G->last_jcg_iters, &G->last_free);
+    if (per_level) for (int k = 0; k < G->L; ++k) per_level[k] = stv[k];
+    return s;
+  }
+  return run_cascade(G, std::vector<double>(G->L, eps), std::vector<int>(G->L, 10000), per_level, u_fine, ut_fine);
+}
+
+int ecmg_run_fixed(ecmg_grid* G, int m_L, double ratio, ecmg_stats* per_level, double* u_fine, double* ut_fine) {
+  if (!G || !G->has_problem || !u_fine || m_L < 0 || !(ratio > 0.0) || G->slab) return ECMG_EINVAL;
+  const int Lc = G->L - 2;
+  std::vector<double> e(G->L, 0.0);
+  std::vector<int> m(G->L, 0);
+  for (int k = 2; k < G->L; ++k)   // Eq. (ee): m_j = ceil(m_L ratio^(L-j)), j = k - 1
+    m[k] = (int)std::ceil(m_L * std::pow(ratio, (double)(Lc - (k - 1))) - 1e-12);
+  return run_cascade(G, e, m, per_level, u_fine, ut_fine);
 }
 
 }  // extern "C"

@@ -86,13 +86,15 @@ __device__ __forceinline__ void lin_w(int l, double w[2]) {
 // (2) interpolation. FREEBOX: write the free nodes into the pitched free-box vector x, else the
 // full nodal vector w (with g_D on Dirichlet nodes).
 template <bool FREEBOX>
-__global__ void k_exp_interp(const LevelGeom gf, const Problem pb, const double* __restrict__ S, double* __restrict__ out,
-                             int variant, int F0) {
+__global__ void __launch_bounds__(64) k_exp_interp(const LevelGeom gf, const Problem pb, const double* __restrict__ S,
+                                                   double* __restrict__ out, int variant, int F0) {
+  // one thread per (4h block bx, 4h block row by, fine plane fz): the 27 seeds are loaded once and
+  // reused for the 4 (5 in the last block row) fine rows of the block and 4 (5) nodes per row
   const int n4x = gf.n[0] / 4, n4y = gf.n[1] / 4, n4z = gf.n[2] / 4;
-  const int bx = blockIdx.x * blockDim.x + threadIdx.x, fy = blockIdx.y, fz = F0 + blockIdx.z;
+  const int bx = blockIdx.x * blockDim.x + threadIdx.x, by = blockIdx.y, fz = F0 + blockIdx.z;
   if (bx >= n4x) return;
-  const int by = min(fy / 4, n4y - 1), bz = min(fz / 4, n4z - 1);
-  const int ly = fy - 4 * by, lz = fz - 4 * bz;
+  const int bz = min(fz / 4, n4z - 1);
+  const int lz = fz - 4 * bz;
   const long long nn2x = gf.n[0] / 2 + 1, nn2y = gf.n[1] / 2 + 1;
   double s[3][3][3];   // [k][j][i] seeds of block (bx, by, bz)
 #pragma unroll
@@ -102,51 +104,57 @@ __global__ void k_exp_interp(const LevelGeom gf, const Problem pb, const double*
 #pragma unroll
       for (int i = 0; i < 3; ++i)
         s[k][j][i] = __ldg(S + (2 * bx + i) + nn2x * ((2 * by + j) + nn2y * (long long)(2 * bz + k)));
-  double qy[3], qz[3], ly2[2], lz2[2];
-  quad_w(ly, qy); quad_w(lz, qz); lin_w(ly, ly2); lin_w(lz, lz2);
-  // per-row coefficients: W(xi) = sum_i qx_i(xi) C[i] + sum_a lx_a(xi) E[a]
-  double C[3], E[2];
-  if (variant == 1) {
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      double t = 0.0;
-#pragma unroll
-      for (int k = 0; k < 3; ++k) t += qz[k] * (qy[0] * s[k][0][i] + qy[1] * s[k][1][i] + qy[2] * s[k][2][i]);
-      C[i] = t;
-    }
-    E[0] = E[1] = 0.0;
-  } else {
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {   // P_x: x-edges at (y, z) in {0,2}^2 blended bilinearly
-      C[i] = ly2[0] * (lz2[0] * s[0][0][i] + lz2[1] * s[2][0][i]) + ly2[1] * (lz2[0] * s[0][2][i] + lz2[1] * s[2][2][i]);
-    }
-#pragma unroll
-    for (int a = 0; a < 2; ++a) {
-      const int A = 2 * a;
-      const double Py = lz2[0] * (qy[0] * s[0][0][A] + qy[1] * s[0][1][A] + qy[2] * s[0][2][A]) +
-                        lz2[1] * (qy[0] * s[2][0][A] + qy[1] * s[2][1][A] + qy[2] * s[2][2][A]);
-      const double Pz = ly2[0] * (qz[0] * s[0][0][A] + qz[1] * s[1][0][A] + qz[2] * s[2][0][A]) +
-                        ly2[1] * (qz[0] * s[0][2][A] + qz[1] * s[1][2][A] + qz[2] * s[2][2][A]);
-      const double T = ly2[0] * (lz2[0] * s[0][0][A] + lz2[1] * s[2][0][A]) + ly2[1] * (lz2[0] * s[0][2][A] + lz2[1] * s[2][2][A]);
-      E[a] = Py + Pz - 2.0 * T;
-    }
-  }
+  double qz[3], lz2[2];
+  quad_w(lz, qz); lin_w(lz, lz2);
   const int nl = (bx == n4x - 1) ? 5 : 4;
+  const int nrow = (by == n4y - 1) ? 5 : 4;
   const long long nx = gf.n[0] + 1, ny = gf.n[1] + 1;
-  const bool row_free = fy >= gf.flo[1] && fy < gf.flo[1] + gf.nf[1] && fz >= gf.flo[2] && fz < gf.flo[2] + gf.nf[2];
+  const bool plane_free = fz >= gf.flo[2] && fz < gf.flo[2] + gf.nf[2];
+  for (int ly = 0; ly < nrow; ++ly) {
+    const int fy = 4 * by + ly;
+    double qy[3], ly2[2];
+    quad_w(ly, qy); lin_w(ly, ly2);
+    // per-row coefficients: W(xi) = sum_i qx_i(xi) C[i] + sum_a lx_a(xi) E[a]
+    double C[3], E[2];
+    if (variant == 1) {
 #pragma unroll
-  for (int l = 0; l < 5; ++l) {
-    if (l >= nl) break;
-    const int fx = 4 * bx + l;
-    double qx[3], lx[2];
-    quad_w(l, qx); lin_w(l, lx);
-    double W = qx[0] * C[0] + qx[1] * C[1] + qx[2] * C[2] + lx[0] * E[0] + lx[1] * E[1];
-    const bool fr = row_free && fx >= gf.flo[0] && fx < gf.flo[0] + gf.nf[0];
-    if (FREEBOX) {
-      if (fr) out[(long long)(fz - gf.flo[2] - gf.zoff) * gf.S + (long long)(fy - gf.flo[1]) * gf.P + (fx - gf.flo[0])] = W;
+      for (int i = 0; i < 3; ++i) {
+        double t = 0.0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) t += qz[k] * (qy[0] * s[k][0][i] + qy[1] * s[k][1][i] + qy[2] * s[k][2][i]);
+        C[i] = t;
+      }
+      E[0] = E[1] = 0.0;
     } else {
-      if (!fr) W = prob_gD(pb, gf.lo[0] + fx * gf.h[0], gf.lo[1] + fy * gf.h[1], gf.lo[2] + fz * gf.h[2]);
-      out[(long long)fx + nx * ((long long)fy + ny * fz)] = W;
+#pragma unroll
+      for (int i = 0; i < 3; ++i)   // P_x: x-edges at (y, z) in {0,2}^2 blended bilinearly
+        C[i] = ly2[0] * (lz2[0] * s[0][0][i] + lz2[1] * s[2][0][i]) + ly2[1] * (lz2[0] * s[0][2][i] + lz2[1] * s[2][2][i]);
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        const int A = 2 * a;
+        const double Py = lz2[0] * (qy[0] * s[0][0][A] + qy[1] * s[0][1][A] + qy[2] * s[0][2][A]) +
+                          lz2[1] * (qy[0] * s[2][0][A] + qy[1] * s[2][1][A] + qy[2] * s[2][2][A]);
+        const double Pz = ly2[0] * (qz[0] * s[0][0][A] + qz[1] * s[1][0][A] + qz[2] * s[2][0][A]) +
+                          ly2[1] * (qz[0] * s[0][2][A] + qz[1] * s[1][2][A] + qz[2] * s[2][2][A]);
+        const double T = ly2[0] * (lz2[0] * s[0][0][A] + lz2[1] * s[2][0][A]) + ly2[1] * (lz2[0] * s[0][2][A] + lz2[1] * s[2][2][A]);
+        E[a] = Py + Pz - 2.0 * T;
+      }
+    }
+    const bool row_free = plane_free && fy >= gf.flo[1] && fy < gf.flo[1] + gf.nf[1];
+#pragma unroll
+    for (int l = 0; l < 5; ++l) {
+      if (l >= nl) break;
+      const int fx = 4 * bx + l;
+      double qx[3], lx[2];
+      quad_w(l, qx); lin_w(l, lx);
+      double W = qx[0] * C[0] + qx[1] * C[1] + qx[2] * C[2] + lx[0] * E[0] + lx[1] * E[1];
+      const bool fr = row_free && fx >= gf.flo[0] && fx < gf.flo[0] + gf.nf[0];
+      if (FREEBOX) {
+        if (fr) out[(long long)(fz - gf.flo[2] - gf.zoff) * gf.S + (long long)(fy - gf.flo[1]) * gf.P + (fx - gf.flo[0])] = W;
+      } else {
+        if (!fr) W = prob_gD(pb, gf.lo[0] + fx * gf.h[0], gf.lo[1] + fy * gf.h[1], gf.lo[2] + fz * gf.h[2]);
+        out[(long long)fx + nx * ((long long)fy + ny * fz)] = W;
+      }
     }
   }
 }
@@ -227,7 +235,7 @@ cudaError_t launch_exp_finite(const LevelGeom& gf, const Problem& pb, const doub
   dim3 g1((gf.n[0] / 2 + 1 + 127) / 128, gf.n[1] / 2 + 1, K1 - K0 + 1);
   count_launch();
   k_exp_seeds<<<g1, 128, 0, st>>>(gf, u2h, u4h, seeds, variant, K0);
-  dim3 g2((gf.n[0] / 4 + 63) / 64, gf.n[1] + 1, F1 - F0);
+  dim3 g2((gf.n[0] / 4 + 63) / 64, gf.n[1] / 4, F1 - F0);
   count_launch();
   if (freebox) k_exp_interp<true><<<g2, 64, 0, st>>>(gf, pb, seeds, w, variant, F0);
   else k_exp_interp<false><<<g2, 64, 0, st>>>(gf, pb, seeds, w, variant, F0);

@@ -36,8 +36,9 @@ __global__ void k_beta(const LevelGeom g, const Problem pb, double* __restrict__
 //      (shared memory), form the element load vectors, and every node gathers its 8 entries.
 //  (2) boundary shell of the free box: Robin face load G (2x2 Gauss) and the lifting -A_fD g_D.
 // ||b||^2 is accumulated by the JCG init pass, which reads b anyway.
-constexpr int VX = 32, VY = 8, VNTH = VX * VY;
-constexpr int VEX = VX + 1, VEY = VY + 1, VNE = VEX * VEY;     // 33 x 9 elements per plane
+// node tile 31 x 7 -> element tile 32 x 8 = 256 = one element (and 8 Gauss points) per thread
+constexpr int VX = 31, VY = 7, VNTH = 256;
+constexpr int VEX = VX + 1, VEY = VY + 1, VNE = VEX * VEY;     // 32 x 8 elements per plane
 constexpr int VSMEM = (VNE * 8 + 2 * VNE * 8) * (int)sizeof(double);
 
 // separable factor g_d and amplitude: returns false if f is not a product of 1D functions
@@ -123,7 +124,7 @@ __global__ void __launch_bounds__(VNTH, 3) k_rhs_vol(const LevelGeom g, const Pr
   // structure-of-arrays layouts (consecutive threads -> consecutive doubles: no bank conflicts)
   double* fq = vs;              // fq[q * VNE + e]: f at Gauss point q of element e of the plane
   double* Fe = vs + VNE * 8;    // Fe[slot][a * VNE + e]: element load vectors, ring of two planes
-  const int lane = threadIdx.x, w = threadIdx.y, tid = lane + VX * w;
+  const int lane = threadIdx.x, w = threadIdx.y, tid = lane + 32 * w;
   const int X0 = blockIdx.x * VX, Y0 = blockIdx.y * VY;
   const int z0 = g.zbeg + blockIdx.z * zc, z1 = min(z0 + zc, g.zend);   // local planes
   const double detJ = g.h[0] * g.h[1] * g.h[2] / 8.0;
@@ -168,7 +169,7 @@ __global__ void __launch_bounds__(VNTH, 3) k_rhs_vol(const LevelGeom g, const Pr
     __syncthreads();
     // (c) node plane fz = fez gathers from element planes fez-1 and fez
     const int fz = fez, fx = X0 + lane, fy = Y0 + w;
-    if (fz >= z0 && fx < g.nf[0] && fy < g.nf[1]) {
+    if (fz >= z0 && lane < VX && w < VY && fx < g.nf[0] && fy < g.nf[1]) {
       double v = 0.0;
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
@@ -334,8 +335,8 @@ cudaError_t launch_rhs(const LevelGeom& g, const Problem& pb, const ElemStencil&
     const int zc = 32;
     dim3 grid((g.nf[0] + VX - 1) / VX, (g.nf[1] + VY - 1) / VY, (g.zend - g.zbeg + zc - 1) / zc);
     count_launch();
-    if (pb.id == 4) k_rhs_vol<4><<<grid, dim3(VX, VY), VSMEM, st>>>(g, pb, b, zc);
-    else k_rhs_vol<0><<<grid, dim3(VX, VY), VSMEM, st>>>(g, pb, b, zc);
+    if (pb.id == 4) k_rhs_vol<4><<<grid, dim3(32, 8), VSMEM, st>>>(g, pb, b, zc);
+    else k_rhs_vol<0><<<grid, dim3(32, 8), VSMEM, st>>>(g, pb, b, zc);
   }
   const int m = std::max(g.nf[0], std::max(g.nf[1], g.nf[2]));
   dim3 gs((m + 127) / 128, m, 6);

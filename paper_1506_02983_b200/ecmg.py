@@ -23,7 +23,7 @@ PROB = dict(C1=1, C2=2, C3=3, C4=4, C5=5, P1=11, P2=12, P3=13,
 OPT_EXP_VARIANT, OPT_PRECOND, OPT_ZCHUNK, OPT_KERNEL, OPT_GRAPH, OPT_VIRTUAL_SLABS, OPT_PERSISTENT = 1, 2, 3, 4, 5, 6, 7
 
 EXPORTS = ["ecmg_create_grid", "ecmg_set_coeffs", "ecmg_set_option", "ecmg_solve_level",
-           "ecmg_prolongate_extrapolate", "ecmg_richardson", "ecmg_run", "ecmg_apply_operator",
+           "ecmg_prolongate_extrapolate", "ecmg_richardson", "ecmg_run", "ecmg_run_fixed", "ecmg_apply_operator",
            "ecmg_level_rhs", "ecmg_level_shape", "ecmg_last_jcg_timing", "ecmg_kernel_launches",
            "ecmg_slab_partition", "ecmg_nccl_unique_id", "ecmg_destroy_grid", "ecmg_strerror"]
 
@@ -75,6 +75,7 @@ def lib():
         L.ecmg_prolongate_extrapolate.argtypes = [vp, C.c_int, vp, vp, vp]
         L.ecmg_richardson.argtypes = [vp, C.c_int, vp, vp, vp]
         L.ecmg_run.argtypes = [vp, C.c_double, C.POINTER(ecmg_stats), vp, vp]
+        L.ecmg_run_fixed.argtypes = [vp, C.c_int, C.c_double, C.POINTER(ecmg_stats), vp, vp]
         L.ecmg_apply_operator.argtypes = [vp, C.c_int, vp, vp]
         L.ecmg_level_rhs.argtypes = [vp, C.c_int, vp, dp]
         L.ecmg_level_shape.argtypes = [vp, C.c_int, ip, C.POINTER(C.c_longlong), ip, ip]
@@ -153,6 +154,12 @@ def richardson(grid, level, uh, u2h, ut):
 def run(grid, eps, num_levels, u_fine, ut_fine=None):
     stats = (ecmg_stats * num_levels)()
     s = lib().ecmg_run(grid, float(eps), stats, _ptr(u_fine), _ptr(ut_fine))
+    return s, [stats[k] for k in range(num_levels)]
+
+
+def run_fixed(grid, m_L, ratio, num_levels, u_fine, ut_fine=None):
+    stats = (ecmg_stats * num_levels)()
+    s = lib().ecmg_run_fixed(grid, int(m_L), float(ratio), stats, _ptr(u_fine), _ptr(ut_fine))
     return s, [stats[k] for k in range(num_levels)]
 
 
@@ -270,6 +277,11 @@ class Grid:
     def run(self, eps, u_fine, ut_fine=None):
         st, stats = run(self.h, eps, self.L, u_fine, ut_fine)
         self._check(st, "ecmg_run", allow=(OK, ENOTCONV))
+        return st, [s.as_dict() for s in stats]
+
+    def run_fixed(self, m_L, ratio, u_fine, ut_fine=None):
+        st, stats = run_fixed(self.h, m_L, ratio, self.L, u_fine, ut_fine)
+        self._check(st, "ecmg_run_fixed")
         return st, [s.as_dict() for s in stats]
 
     def apply_operator(self, level, p, q):

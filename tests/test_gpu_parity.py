@@ -276,3 +276,16 @@ def test_persistent_small_levels_vs_graph(pid, eps):
         res.append(([s["iterations"] for s in stats], host(u)))
     assert all(abs(a - b) <= 1 for a, b in zip(res[0][0], res[1][0]))
     assert np.max(np.abs(res[0][1] - res[1][1])) <= 1e-9 * np.max(np.abs(res[1][1]))
+
+
+@pytest.mark.parametrize("pid,precond", [(o.C2, False), (o.C4, True), (o.C3, False)])
+def test_alg3_fixed_schedule(pid, precond):
+    # Alg. 3 with Eq. (ee) counts m_j = ceil(m_L ratio^(L-j)), here m_L = 3, ratio 2
+    g = Grid(4, 5, pid, params_for(pid), precond=precond)
+    u, ut = g.new_vec(4), g.new_vec(4)
+    st, stats = g.run_fixed(3, 2.0, u, ut)
+    ost, ostats, ou, out = o.ecmg_fixed(4, 5, pid, 3, 2.0, params=params_for(pid), precond=precond)
+    assert st == 0 and ost == 0
+    assert [s["iterations"] for s in stats[2:]] == [int(v) for v in ostats[2:, 0]] == [12, 6, 3]
+    assert np.max(np.abs(host(u) - ou)) <= 1e-11 * np.max(np.abs(ou))
+    assert np.max(np.abs(host(ut) - out)) <= 1e-11 * np.max(np.abs(out))

@@ -99,3 +99,17 @@ def test_rel_true_reported():
     assert abs(np.linalg.norm(r) / nb - st["rel_true"]) <= 1e-13
     assert st["rel_recur"] <= 1e-9
     assert np.all(x[m] == L.dirichlet()[1][m])  # Dirichlet entries = g_D
+
+
+def test_alg3_fixed_schedule():
+    # Alg. 3 / Eq. (ee): m_j = ceil(m_L ratio^(L-j)); the paper's suggested m_j = 4 * 4^(L-j)
+    st, S, u, ut = o.ecmg_fixed(4, 5, o.C2, 4, 4.0)
+    assert st == 0
+    assert [int(v) for v in S[2:, 0]] == [64, 16, 4]
+    # zero iterations: u_h is W_h = EXP_finite(u_2h, u_4h) exactly
+    st, S, u0, ut0, w0 = o.ecmg_fixed(4, 4, o.C2, 0, 2.0, want_w=True)
+    assert np.array_equal(u0, w0) and int(S[-1, 0]) == 0
+    # enough iterations: Alg. 3 reaches the same FE solution as Alg. 4 at a tight tolerance
+    st, S, ua, _ = o.ecmg_fixed(4, 4, o.C2, 200, 1.0, precond=True)
+    st2, S2, ub, _ = o.ecmg(4, 4, o.C2, 1e-13)
+    assert np.max(np.abs(ua - ub)) <= 1e-11 * np.max(np.abs(ub))
