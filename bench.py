@@ -38,14 +38,16 @@ UNIT = "unknown-iters/s"
 BYTES_PER_UNKNOWN_ITER = 64   # x 1R+1W, r 2R+1W, p 2R+1W (constant-beta path)
 
 CONFIGS = {
-    # name: (problem id, coarsest, levels, eps, description); C3 / C5 run the element-beta path (80 B/unknown)
+    # name: (problem id, coarsest, levels, eps, description); C3 / C5 run the element-beta path (88 B/unknown)
     "c4": (4, 4, 8, 1e-9, "C4 (BASELINE configs[3]): u=r^{3/2}, beta=1, Dirichlet, Q1, 4^3->512^3, eps=1e-9"),
     "c2": (2, 4, 6, 1e-10, "C2 (BASELINE configs[1]): u=exp(x+y+z), beta=1, Dirichlet, Q1, 4^3->128^3, eps=1e-10"),
     "c1": (1, 4, 4, 1e-8, "C1 (BASELINE configs[0]): u=sin sin sin, beta=1, Dirichlet, Q1, 4^3->32^3, eps=1e-8"),
     "c3": (3, 4, 7, 1e-10, "C3 (BASELINE configs[2]): variable beta, Robin z=1, Q1, 4^3->256^3, eps=1e-10"),
     "c5": (5, 4, 9, 1e-8, "C5 (BASELINE configs[4]): layered geology (seed 0), Dirichlet, Q1, 4^3->1024^3, eps=1e-8"),
 }
-BYTES_PER_UNKNOWN_ITER_ELEM = 80   # element-beta path: + beta_e read in K1 and K2
+# element-beta path (kernels_jcg_elem.cu): K1 reads z, p_old, beta_e and writes p; K2 reads p, beta_e,
+# x, r and writes x, r, z = D^-1 r (z replaces the halo diagonal): 11 x 8 B
+BYTES_PER_UNKNOWN_ITER_ELEM = 88
 
 
 def load_peaks():

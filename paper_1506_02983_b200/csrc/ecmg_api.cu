@@ -43,6 +43,7 @@ struct ecmg_grid {
   double* r = nullptr;
   double* p[2] = {nullptr, nullptr};
   double* b = nullptr;
+  double* zv = nullptr;            // element path: z = D^-1 r (K2 / INIT write it, K1 reads it)
   double* beta = nullptr;
   double* partials = nullptr;
   JcgScalars* sc = nullptr;
@@ -236,7 +237,7 @@ cudaError_t build_level_graph(ecmg_grid* G, int k, cudaGraphExec_t* out) {
   // init pass
   e = cudaStreamBeginCaptureToGraph(G->cap_stream, graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
   if (e != cudaSuccess) return done(e);
-  { KArgs ai = a; ai.h0 = G->x; ai.i0 = G->b; ai.o0 = G->r; e = launch_mode(G, MODE_INIT, g, ai); }
+  { KArgs ai = a; ai.h0 = G->x; ai.i0 = G->b; ai.o0 = G->r; ai.o1 = G->zv; e = launch_mode(G, MODE_INIT, g, ai); }
   cudaError_t e2 = cudaStreamEndCapture(G->cap_stream, &graph);
   if (e != cudaSuccess || e2 != cudaSuccess) return done(e != cudaSuccess ? e : e2);
   size_t nn = 1;
@@ -255,11 +256,11 @@ cudaError_t build_level_graph(ecmg_grid* G, int k, cudaGraphExec_t* out) {
   if (e != cudaSuccess) return done(e);
   for (int half = 0; half < 2 && e == cudaSuccess; ++half) {
     KArgs a1 = a;
-    a1.h0 = G->r; a1.h1 = G->p[half]; a1.o0 = G->p[1 - half];
+    a1.h0 = G->elem_path ? G->zv : G->r; a1.h1 = G->p[half]; a1.o0 = G->p[1 - half];
     e = launch_mode(G, MODE_K1, g, a1);
     if (e != cudaSuccess) break;
     KArgs a2 = a;
-    a2.h0 = G->p[1 - half]; a2.i0 = G->x; a2.i1 = G->r; a2.o0 = G->x; a2.o1 = G->r;
+    a2.h0 = G->p[1 - half]; a2.i0 = G->x; a2.i1 = G->r; a2.o0 = G->x; a2.o1 = G->r; a2.o2 = G->zv;
     e = launch_mode(G, MODE_K2, g, a2);
   }
   e2 = cudaStreamEndCapture(G->cap_stream, &body);
@@ -350,17 +351,17 @@ int run_jcg(ecmg_grid* G, int k, double eps, int max_iter, ecmg_stats* st) {
   // r = b - A x, rho = r.z, rr = r.r, stop test
   {
     KArgs ai = a;
-    ai.h0 = G->x; ai.i0 = G->b; ai.o0 = G->r;
+    ai.h0 = G->x; ai.i0 = G->b; ai.o0 = G->r; ai.o1 = G->zv;
     ECMG_CUDA(launch_mode(G, MODE_INIT, g, ai));
   }
   long long it = 0;
   auto launch_iter = [&]() -> cudaError_t {
     KArgs a1 = a;
-    a1.h0 = G->r; a1.h1 = G->p[it & 1]; a1.o0 = G->p[(it + 1) & 1];
+    a1.h0 = G->elem_path ? G->zv : G->r; a1.h1 = G->p[it & 1]; a1.o0 = G->p[(it + 1) & 1];
     cudaError_t e = launch_mode(G, MODE_K1, g, a1);
     if (e != cudaSuccess) return e;
     KArgs a2 = a;
-    a2.h0 = G->p[(it + 1) & 1]; a2.i0 = G->x; a2.i1 = G->r; a2.o0 = G->x; a2.o1 = G->r;
+    a2.h0 = G->p[(it + 1) & 1]; a2.i0 = G->x; a2.i1 = G->r; a2.o0 = G->x; a2.o1 = G->r; a2.o2 = G->zv;
     e = launch_mode(G, MODE_K2, g, a2);
     ++it;
     return e;
@@ -474,7 +475,7 @@ int ecmg_create_grid(const ecmg_box* dom, const int coarsest_cells[3], int num_l
   const int size_level = (dist && dist->nranks > 1) ? 0 : num_levels - 1;
   LevelGeom gmax = make_geom(*dom, coarsest_cells, size_level, face_none, 1);
   G->vec_doubles = gmax.S * gmax.nf[2] + 64;
-  G->beta_doubles = (long long)(gmax.n[0] + 4) * (gmax.n[1] + 4) * (gmax.n[2] + 4);
+  G->beta_doubles = beta_doubles(gmax);
   const long long rhs_blocks = (long long)((gmax.nf[0] + 7) / 8) * ((gmax.nf[1] + 7) / 8) * ((gmax.nf[2] + 3) / 4);
   const long long jcg_blocks = (long long)((gmax.nf[0] + 31) / 32) * ((gmax.nf[1] + 7) / 8) * gmax.nf[2];
   G->partial_doubles = 3 * std::max(rhs_blocks, jcg_blocks) + 64;
@@ -539,7 +540,7 @@ int ecmg_destroy_grid(ecmg_grid* G) {
   if (G->stream) cudaStreamSynchronize(G->stream); else cudaDeviceSynchronize();
   if (G->slab) slab_driver_destroy(G->slab);
   cudaFree(G->x); cudaFree(G->r); cudaFree(G->p[0]); cudaFree(G->p[1]); cudaFree(G->b);
-  cudaFree(G->beta); cudaFree(G->partials); cudaFree(G->sc);
+  cudaFree(G->beta); cudaFree(G->zv); cudaFree(G->partials); cudaFree(G->sc);
   for (double* p : G->u) cudaFree(p);
   cudaFree(G->ut_tmp);
   cudaFree(G->scratch1d);
@@ -581,6 +582,10 @@ int ecmg_set_coeffs(ecmg_grid* G, const ecmg_problem* pr) {
   const int elem_path = !(prob_beta_is_one(pb.id) && all_dir);
   if (elem_path && !G->beta) {
     if (cudaMalloc(&G->beta, sizeof(double) * G->beta_doubles) != cudaSuccess) { cudaGetLastError(); return ECMG_ENOMEM; }
+  }
+  if (elem_path && !G->zv) {
+    if (cudaMalloc(&G->zv, sizeof(double) * G->vec_doubles) != cudaSuccess) { cudaGetLastError(); return ECMG_ENOMEM; }
+    if (cudaMemsetAsync(G->zv, 0, sizeof(double) * G->vec_doubles, G->stream) != cudaSuccess) return ECMG_ECUDA;
   }
   G->prob = pb;
   G->elem_path = elem_path;
@@ -704,7 +709,7 @@ int ecmg_level_rhs(ecmg_grid* G, int level, double* bout, double* norm_b) {
   {
     KArgs a{};
     a.partials = G->partials; a.sc = G->sc; a.zc = auto_zc(G->zchunk, G->elem_path, g); a.beta = G->beta;
-    a.h0 = G->x; a.i0 = G->b; a.o0 = G->r; a.eps = 0.0; a.max_iter = 0;
+    a.h0 = G->x; a.i0 = G->b; a.o0 = G->r; a.o1 = G->zv; a.eps = 0.0; a.max_iter = 0;
     ECMG_CUDA(launch_mode(G, MODE_INIT, g, a));
   }
   ECMG_CUDA(cudaMemcpyAsync(&G->sc_host[0], G->sc, sizeof(JcgScalars), cudaMemcpyDeviceToHost, G->stream));

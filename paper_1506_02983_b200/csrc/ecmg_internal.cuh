@@ -84,12 +84,13 @@ struct JcgScalars {
 enum KMode { MODE_K1 = 1, MODE_K2 = 2, MODE_INIT = 3, MODE_TRUE = 4, MODE_APPLY = 5 };
 
 struct KArgs {
-  const double* h0;   // halo-read vector (K1: r, K2: p, INIT/TRUE: x, APPLY: p)
+  const double* h0;   // halo-read vector (K1: r (element path: z), K2: p, INIT/TRUE: x, APPLY: p)
   const double* h1;   // K1: p_old
   const double* i0;   // interior-read vector (K2: x, INIT/TRUE: b)
   const double* i1;   // K2: r
   double* o0;         // K1: p_new, K2: x, INIT: r, APPLY: q
-  double* o1;         // K2: r
+  double* o1;         // K2: r; element path INIT: z = D^-1 r
+  double* o2;         // element path K2: z = D^-1 r
   const double* beta; // element path: beta_e with zero ring
   double* partials;   // per-block partial dot products (2 per block)
   JcgScalars* sc;
@@ -128,6 +129,7 @@ cudaError_t launch_jcg_persistent(const LevelGeom& g, const ConstStencil& cs, do
                                   const double* b, double* partials, JcgScalars* sc, cudaStream_t st);
 cudaError_t init_tma_kernel_attributes();
 cudaError_t init_elem_kernel_attributes();
+int elem_tile_rows();
 cudaError_t init_setup_kernel_attributes();
 int tma_halo_box_x();
 int tma_halo_box_y();

@@ -83,6 +83,7 @@ struct SlabCtx {
   std::vector<char> sharded;
   double* x = nullptr;
   double* r = nullptr;
+  double* z = nullptr;   // element path: z = D^-1 r (K1 reads it on its halo planes)
   double* p[2] = {nullptr, nullptr};
   double* b = nullptr;
   double* beta = nullptr;
@@ -143,9 +144,9 @@ int comm_allreduce(SlabDriver* d, cudaStream_t st) {
   return ECMG_OK;
 }
 
-// halo planes of a work vector (which: 0 = x, 1 = r) on sharded level k
+// halo planes of a work vector (which: 0 = x, 1 = r, 2 = z) on sharded level k
 int comm_halo(SlabDriver* d, int k, int which, cudaStream_t st) {
-  auto vec = [&](SlabCtx& c) { return which == 0 ? c.x : c.r; };
+  auto vec = [&](SlabCtx& c) { return which == 0 ? c.x : (which == 1 ? c.r : c.z); };
   if (d->virt) {
     for (size_t i = 0; i + 1 < d->s.size(); ++i) {
       SlabCtx& lo = d->s[i];
@@ -320,7 +321,7 @@ int slab_jcg(SlabDriver* d, int k, double eps, int max_iter, ecmg_stats* st, cud
       SlabCtx& c = d->s[i];
       const LevelGeom& g = c.geom[k];
       const size_t plane = sizeof(double) * g.S;
-      double* vecs[4] = {c.x, c.r, c.p[0], c.p[1]};
+      double* vecs[5] = {c.x, c.r, c.z, c.p[0], c.p[1]};
       for (double* v : vecs) {
         if (c.rank == 0) SL_CUDA(cudaMemsetAsync(v, 0, plane, stream));
         if (c.rank == d->P - 1) SL_CUDA(cudaMemsetAsync(v + (long long)g.zend * g.S, 0, plane, stream));
@@ -328,17 +329,20 @@ int slab_jcg(SlabDriver* d, int k, double eps, int max_iter, ecmg_stats* st, cud
     }
   }
   if (sh && (rc = comm_halo(d, k, 0, stream))) return rc;
-  if ((rc = pass(MODE_INIT, [&](SlabCtx& c, KArgs& a) { a.h0 = c.x; a.i0 = c.b; a.o0 = c.r; }))) return rc;
-  if (sh && (rc = comm_halo(d, k, 1, stream))) return rc;   // r on the halo planes for the first K1
+  // K1 reads r (constant stencil) or z = D^-1 r (element path) on its halo planes
+  const bool elem = d->cfg.elem_path != 0;
+  const int k1_vec = elem ? 2 : 1;
+  if ((rc = pass(MODE_INIT, [&](SlabCtx& c, KArgs& a) { a.h0 = c.x; a.i0 = c.b; a.o0 = c.r; a.o1 = c.z; }))) return rc;
+  if (sh && (rc = comm_halo(d, k, k1_vec, stream))) return rc;   // halo planes for the first K1
   long long it = 0;
   auto iteration = [&]() -> int {
-    int q = pass(MODE_K1, [&](SlabCtx& c, KArgs& a) { a.h0 = c.r; a.h1 = c.p[it & 1]; a.o0 = c.p[(it + 1) & 1]; });
+    int q = pass(MODE_K1, [&](SlabCtx& c, KArgs& a) { a.h0 = elem ? c.z : c.r; a.h1 = c.p[it & 1]; a.o0 = c.p[(it + 1) & 1]; });
     if (q) return q;
     q = pass(MODE_K2, [&](SlabCtx& c, KArgs& a) {
-      a.h0 = c.p[(it + 1) & 1]; a.i0 = c.x; a.i1 = c.r; a.o0 = c.x; a.o1 = c.r;
+      a.h0 = c.p[(it + 1) & 1]; a.i0 = c.x; a.i1 = c.r; a.o0 = c.x; a.o1 = c.r; a.o2 = c.z;
     });
     if (q) return q;
-    if (sh && (q = comm_halo(d, k, 1, stream))) return q;
+    if (sh && (q = comm_halo(d, k, k1_vec, stream))) return q;
     ++it;
     return ECMG_OK;
   };
@@ -411,13 +415,13 @@ SlabDriver* slab_driver_create(const SlabCfg& cfg, int P, int rank, bool virt, c
       vec = std::max(vec, g.S * (long long)g.nza + 64);
     }
     const LevelGeom gf = make_geom(cfg.dom, cfg.n0, cfg.L - 1, face_none, 1);
-    const long long beta_n = (long long)(gf.n[0] + 4) * (gf.n[1] + 4) * (gf.n[2] + 4);
+    const long long beta_n = beta_doubles(gf);
     const long long part_n = 3LL * ((gf.nf[0] + 7) / 8) * ((gf.nf[1] + 7) / 8) * (gf.nf[2] + 3) / 4 * 4 + 3 * 65536;
     auto alloc = [&](double** p, long long n) -> bool {
       if (cudaMalloc(p, sizeof(double) * n) != cudaSuccess) { cudaGetLastError(); return false; }
       return cudaMemset(*p, 0, sizeof(double) * n) == cudaSuccess;
     };
-    bool ok = alloc(&c.x, vec) && alloc(&c.r, vec) && alloc(&c.p[0], vec) && alloc(&c.p[1], vec) && alloc(&c.b, vec) &&
+    bool ok = alloc(&c.x, vec) && alloc(&c.r, vec) && alloc(&c.z, vec) && alloc(&c.p[0], vec) && alloc(&c.p[1], vec) && alloc(&c.b, vec) &&
               alloc(&c.beta, beta_n) && alloc(&c.partials, part_n) &&
               alloc(&c.scratch1d, 3LL * (std::max(gf.n[0], std::max(gf.n[1], gf.n[2])) + 1)) &&
               alloc(&c.seeds, (long long)(gf.n[0] / 2 + 1) * (gf.n[1] / 2 + 1) * (gf.n[2] / 2 + 1)) &&
@@ -455,7 +459,7 @@ void slab_driver_destroy(SlabDriver* d) {
   if (!d) return;
   cudaDeviceSynchronize();
   for (auto& c : d->s) {
-    cudaFree(c.x); cudaFree(c.r); cudaFree(c.p[0]); cudaFree(c.p[1]); cudaFree(c.b); cudaFree(c.beta);
+    cudaFree(c.x); cudaFree(c.r); cudaFree(c.z); cudaFree(c.p[0]); cudaFree(c.p[1]); cudaFree(c.b); cudaFree(c.beta);
     cudaFree(c.partials); cudaFree(c.scratch1d); cudaFree(c.seeds); cudaFree(c.sc); cudaFree(c.ut);
     for (double* p : c.u) cudaFree(p);
   }

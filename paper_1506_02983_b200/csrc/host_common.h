@@ -19,7 +19,7 @@ inline LevelGeom make_geom(const ecmg_box& dom, const int n0[3], int k, const in
   }
   g.P = ((long long)std::max(1, g.nf[0]) + 31) / 32 * 32;
   g.S = g.P * std::max(1, g.nf[1]);
-  g.BP = g.n[0] + 4;
+  g.BP = ((long long)g.n[0] + 4 + 31) / 32 * 32;   // 256-B rows: TMA needs 16-B multiples
   g.BS = g.BP * (g.n[1] + 4);
   g.elem_path = elem_path;
   g.zoff = 0;
@@ -30,6 +30,8 @@ inline LevelGeom make_geom(const ecmg_box& dom, const int n0[3], int k, const in
   g.zhi = g.n[2] + 1;
   return g;
 }
+
+inline long long beta_doubles(const LevelGeom& g) { return g.BS * (g.n[2] + 4); }
 
 inline ElemStencil make_elem_stencil(const LevelGeom& g, const Problem& pb, int precond) {
   ElemStencil es{};
@@ -82,7 +84,7 @@ inline ConstStencil make_const_stencil(const LevelGeom& g, double beta, int prec
 
 inline int auto_zc(int zchunk, int elem_path, const LevelGeom& g) {
   if (zchunk > 0) return zchunk;
-  const int ty = elem_path ? 8 : 32;
+  const int ty = elem_path ? 16 : 32;   // JCG tiles: 32 x 16 (element path), 32 x 32 (constant stencil)
   const long long tiles = (long long)((g.nf[0] + 31) / 32) * ((g.nf[1] + ty - 1) / ty);
   const long long target = 148LL * 2 * 2;
   long long nchunks = (target + tiles - 1) / tiles;

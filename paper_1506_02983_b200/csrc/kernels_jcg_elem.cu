@@ -1,0 +1,456 @@
+// kernels_jcg_elem.cu -- TMA-fed z-marching JCG kernels for the element-beta operator: beta_e per
+// element and / or Robin / Neumann faces (C3, C5, P1-P3, the layered and Robin patch problems;
+// SURVEY.md §8a a4/a5). Same device-side CG recurrences as the constant-stencil kernels
+// (Alg. 4 l.7-9; textbook PCG, §8c O7).
+//
+// Operator (§8c A3): (A p)_i = sum_{e ni i} beta_e sum_{j in e} kappa[pat(i,j)] p_j
+//   + sum_{Robin faces F ni i} alpha_F h1 h2 sum_{face elements f ni i} sum_{j in f} m2[pat] p_j,
+// pat = bit d set if i, j differ along axis d (ElemStencil), m2 = {1/9, 1/18, 1/18, 1/36}.
+//
+// Element-layer split. The element layer between node planes d and u = d + 1 contributes to the
+// nodes of both planes. For a node column c and the four layer elements around it (betas
+// b_LB, b_RB, b_LA, b_RA: left / right in x, below / above in y), the beta-weighted in-plane sums
+// of a node plane v are
+//   G0(v) = B4 v_c,   G1(v) = W_x- v_x- + W_x+ v_x+,   G2(v) = W_y- v_y- + W_y+ v_y+,
+//   G3(v) = b_LB v_(x-,y-) + b_RB v_(x+,y-) + b_LA v_(x-,y+) + b_RA v_(x+,y+),
+// with B4 the sum of the four betas and W the sum of the two betas of the elements holding the edge.
+// The layer adds  sum_j kappa[j] G_j(p_d) + kappa[j+4] G_j(p_u)  to node (c, d) and
+//                 sum_j kappa[j] G_j(p_u) + kappa[j+4] G_j(p_d)  to node (c, u)
+// (pattern bit 4: the partner is in the other plane). A node completes once the layer above it is
+// added; the layer-below half rides in registers from the previous step. About 40 fp64 operations
+// per node instead of the 64 + 8 of the element-by-element form, and every beta is read once.
+//
+// CG data flow of this path: K2 / INIT also write z = D^-1 r (D = Jacobi diagonal
+// kappa_0 sum_{e ni i} beta_e + Robin diagonal, formed from the beta sums the kernel holds anyway), so
+// K1 needs only z and p_old on its halo (p = z + beta_cg p_old): no diagonal on halo nodes.
+// HBM per unknown and iteration: K1 reads z, p_old, beta, writes p (32 B); K2 reads p, beta, x, r and
+// writes x, r, z (56 B): 88 B.
+//
+// Data movement as in kernels_jcg_tma.cu: one cp.async.bulk.tensor.3d per CTA and vector per plane
+// into an NS-deep ring (mbarrier expect_tx), out-of-bounds boxes zero-filled (= p on Dirichlet /
+// outside nodes, beta outside the domain). Tile 32 x 16 nodes, 2 rows per warp.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <mutex>
+#include "ecmg_internal.cuh"
+#include "jcg_common.cuh"
+
+namespace ecmg {
+namespace {
+
+constexpr int RY = 2;                 // node rows per warp (two fp64 plane windows stay in registers)
+constexpr int TY = WARPS * RY;        // 16
+constexpr int HX = TX + 4;            // 36: node halo box x = X0-2 .. X0+33 (16-B aligned start)
+constexpr int XO = 2;                 // smem column of x = X0
+constexpr int HY = TY + 2;            // 18
+constexpr int HBYTES = HX * HY * 8;
+constexpr int HSTRIDE = (HBYTES + 127) / 128 * 128;
+constexpr int EBX = TX + 4;           // 36 element columns: beta-array index X0 .. X0+35
+constexpr int EBY = TY + 1;           // 17 element rows
+constexpr int EBYTES = EBX * EBY * 8;
+constexpr int ESTRIDE = (EBYTES + 127) / 128 * 128;
+constexpr int IBYTES = TX * TY * 8;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int MODE>
+struct ElemCfg {
+  static constexpr bool kH1 = (MODE == MODE_K1);
+  static constexpr int kNI = (MODE == MODE_K2) ? 2 : ((MODE == MODE_INIT || MODE == MODE_TRUE) ? 1 : 0);
+  static constexpr int OFF_E = HSTRIDE * (kH1 ? 2 : 1);
+  static constexpr int OFF_I = OFF_E + ESTRIDE;
+  static constexpr int SBYTES = OFF_I + IBYTES * kNI;
+};
+
+// loads of step t: node plane zh = z0-1+t (halo boxes), element layer (zh-1, zh), interior plane zh-1
+template <int MODE>
+__device__ __forceinline__ void issue_elem_stage(unsigned char* smem, uint64_t* full, int st, int t, int z0, int X0,
+                                                 int Y0, int ey0, int ez_base, uint32_t tx_bytes, bool first,
+                                                 const CUtensorMap* pH0, const CUtensorMap* pH1, const CUtensorMap* pE,
+                                                 const CUtensorMap* pI0, const CUtensorMap* pI1) {
+  using C = ElemCfg<MODE>;
+  unsigned char* base = smem + st * C::SBYTES;
+  mbar_expect_tx(&full[st], tx_bytes);
+  const int zh = z0 - 1 + t;
+  tma_load_3d(base, pH0, X0 - XO, Y0 - 1, zh, &full[st]);
+  if (C::kH1 && !first) tma_load_3d(base + HSTRIDE, pH1, X0 - XO, Y0 - 1, zh, &full[st]);
+  tma_load_3d(base + C::OFF_E, pE, X0, ey0, ez_base + zh, &full[st]);
+  if (C::kNI >= 1) tma_load_3d(base + C::OFF_I, pI0, X0, Y0, zh - 1, &full[st]);
+  if (C::kNI >= 2) tma_load_3d(base + C::OFF_I + IBYTES, pI1, X0, Y0, zh - 1, &full[st]);
+}
+
+template <int MODE, int NS>
+__global__ void __launch_bounds__(NTH, 2)
+    k_jcg_elem_tma(const LevelGeom g, const ElemStencil es, const KArgs a, const __grid_constant__ CUtensorMap mH0,
+                   const __grid_constant__ CUtensorMap mH1, const __grid_constant__ CUtensorMap mE,
+                   const __grid_constant__ CUtensorMap mI0, const __grid_constant__ CUtensorMap mI1) {
+  using C = ElemCfg<MODE>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full[NS];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  JcgScalars* sc = a.sc;
+  if (MODE == MODE_K1 || MODE == MODE_K2) {
+    if (*(volatile int*)&sc->done) return;
+  }
+  const int lane = threadIdx.x, w = threadIdx.y, tid = lane + TX * w;
+  const int nfx = g.nf[0], nfy = g.nf[1];
+  const long long S = g.S;
+  const int P = (int)g.P;
+  const int X0 = blockIdx.x * TX, Y0 = blockIdx.y * TY;
+  const int z0 = g.zbeg + blockIdx.z * a.zc;
+  const int z1 = min(z0 + a.zc, g.zend);
+  const int x = X0 + lane, yb = Y0 + RY * w;
+  const int nsteps = z1 - z0 + 2;
+
+  double bcg = 0.0, alpha = 0.0;
+  bool first = false;
+  if (MODE == MODE_K1) { bcg = sc->beta; first = (sc->iter == 0); }
+  if (MODE == MODE_K2) alpha = sc->alpha;
+  const uint32_t tx_bytes = HBYTES * ((C::kH1 && !first) ? 2 : 1) + EBYTES + IBYTES * C::kNI;
+  const int ey0 = g.flo[1] + Y0 + 1;               // beta-array row of the element below node row Y0
+  const int ez_base = g.flo[2] + g.zoff + 1;       // beta-array plane of the layer below node plane 0, + 1
+  const int eo = g.flo[0] + 1;                     // smem column of the left element of lane 0
+
+  const CUtensorMap* pH0 = &mH0;
+  const CUtensorMap* pH1 = &mH1;
+  const CUtensorMap* pE = &mE;
+  const CUtensorMap* pI0 = &mI0;
+  const CUtensorMap* pI1 = &mI1;
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) mbar_init(&full[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int t = 0; t < NS - 1 && t < nsteps; ++t)
+      issue_elem_stage<MODE>(smem, full, t % NS, t, z0, X0, Y0, ey0, ez_base, tx_bytes, first, pH0, pH1, pE, pI0, pI1);
+  }
+
+  // K1 halo ring slot of this thread (rows Y0-1, Y0+TY and columns X0-1, X0+32)
+  constexpr int RW = TX + 2;
+  int rhx = -1, rhy = -1;
+  if (tid < 2 * RW) { rhx = 1 + tid % RW; rhy = (tid < RW) ? 0 : HY - 1; }
+  else if (tid < 2 * RW + 2 * TY) { const int t = tid - 2 * RW; rhx = (t < TY) ? 1 : RW; rhy = 1 + (t % TY); }
+
+  bool own_ok[RY];
+  int own_off[RY];
+#pragma unroll
+  for (int j = 0; j < RY; ++j) {
+    own_ok[j] = (x < nfx) && (yb + j < nfy);
+    own_off[j] = own_ok[j] ? (yb + j) * P + x : 0;
+  }
+  // Robin faces (rare path): coefficient alpha_F h1 h2 of the x-face / y-face this node lies on and
+  // which in-plane face elements exist (index test on the box domain)
+  const int gx = g.flo[0] + x, gy0 = g.flo[1] + yb;
+  const bool edge = (gx == 0 && es.robin[0] != 0.0) || (gx == g.n[0] && es.robin[1] != 0.0) ||
+                    (gy0 <= 0 && gy0 + RY - 1 >= 0 && es.robin[2] != 0.0) ||
+                    (gy0 <= g.n[1] && gy0 + RY - 1 >= g.n[1] && es.robin[3] != 0.0);
+  const bool zrobin = es.robin[4] != 0.0 || es.robin[5] != 0.0;
+
+  double part[RY], dpart[RY];
+#pragma unroll
+  for (int j = 0; j < RY; ++j) { part[j] = 0.0; dpart[j] = 0.0; }
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+#define k0 es.kappa[0]
+#define k1 es.kappa[1]
+#define k2 es.kappa[2]
+#define k3 es.kappa[3]
+#define k4 es.kappa[4]
+#define k5 es.kappa[5]
+#define k6 es.kappa[6]
+#define k7 es.kappa[7]
+  constexpr double c9 = 1.0 / 9.0, c18 = 1.0 / 18.0, c36 = 1.0 / 36.0;
+
+  // one z step: node plane zl = z0-1+s arrives in wu; wd holds plane zl-1 (previous step)
+  auto step = [&](int s, double (&wd)[RY + 2][3], double (&wu)[RY + 2][3]) {
+    const int zl = z0 - 1 + s;
+    const int st = s % NS;
+    if (s > 0) __syncthreads();   // every thread is done with step s-1: its stage may be refilled
+    if (tid == 0 && s + NS - 1 < nsteps) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const int t = s + NS - 1;
+      issue_elem_stage<MODE>(smem, full, t % NS, t, z0, X0, Y0, ey0, ez_base, tx_bytes, first, pH0, pH1, pE, pI0, pI1);
+    }
+    mbar_wait(&full[st], (uint32_t)((s / NS) & 1));
+    unsigned char* stage = smem + st * C::SBYTES;
+    double* H = reinterpret_cast<double*>(stage);
+    if (MODE == MODE_K1) {   // p = z + beta_cg p_old on the own nodes and the halo ring, in place
+      const double* H1 = reinterpret_cast<const double*>(stage + HSTRIDE);
+      const bool halo_store = (zl == g.zbeg - 1 || zl == g.zend) && zl >= 0 && zl < g.nza;
+#pragma unroll
+      for (int j = 0; j < RY; ++j) {
+        const int o = (1 + RY * w + j) * HX + XO + lane;
+        H[o] = pcg_direction(1.0, H[o], bcg, H1[o], first);
+        if (halo_store && own_ok[j]) a.o0[(long long)zl * S + own_off[j]] = H[o];   // slab halo plane of p
+      }
+      if (rhx >= 0) {
+        const int o = rhy * HX + rhx;
+        H[o] = pcg_direction(1.0, H[o], bcg, H1[o], first);
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int r = 0; r < RY + 2; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) wu[r][c] = H[(RY * w + r) * HX + XO - 1 + lane + c];
+    if (s == 0) return;
+    const double* E = reinterpret_cast<const double*>(stage + C::OFF_E);
+    double bl[RY + 1][2];
+#pragma unroll
+    for (int r = 0; r < RY + 1; ++r)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) bl[r][c] = E[(RY * w + r) * EBX + eo + lane + c];
+    const double* I0 = reinterpret_cast<const double*>(stage + C::OFF_I);
+    const double* I1 = I0 + TX * TY;
+    const int d = zl - 1;   // node plane completed in this step
+    const int gzd = g.flo[2] + g.zoff + d;
+    const bool layer_ok = gzd >= 0 && gzd < g.n[2];
+    const double rz = zrobin ? ((gzd == 0 ? es.robin[4] : 0.0) + (gzd == g.n[2] ? es.robin[5] : 0.0)) : 0.0;
+    const bool rare = edge || rz != 0.0;
+#pragma unroll
+    for (int j = 0; j < RY; ++j) {
+      const double bLB = bl[j][0], bRB = bl[j][1], bLA = bl[j + 1][0], bRA = bl[j + 1][1];
+      const double Wxm = bLB + bLA, Wxp = bRB + bRA, Wym = bLB + bRB, Wyp = bLA + bRA;
+      const double B4 = Wxm + Wxp;
+      const double gd0 = B4 * wd[j + 1][1], gu0 = B4 * wu[j + 1][1];
+      const double gd1 = __fma_rn(Wxp, wd[j + 1][2], Wxm * wd[j + 1][0]);
+      const double gu1 = __fma_rn(Wxp, wu[j + 1][2], Wxm * wu[j + 1][0]);
+      const double gd2 = __fma_rn(Wyp, wd[j + 2][1], Wym * wd[j][1]);
+      const double gu2 = __fma_rn(Wyp, wu[j + 2][1], Wym * wu[j][1]);
+      const double gd3 = __fma_rn(bRA, wd[j + 2][2], __fma_rn(bLA, wd[j + 2][0], __fma_rn(bRB, wd[j][2], bLB * wd[j][0])));
+      const double gu3 = __fma_rn(bRA, wu[j + 2][2], __fma_rn(bLA, wu[j + 2][0], __fma_rn(bRB, wu[j][2], bLB * wu[j][0])));
+      double upd = __fma_rn(k0, gd0, __fma_rn(k1, gd1, __fma_rn(k2, gd2, __fma_rn(k3, gd3,
+                   __fma_rn(k4, gu0, __fma_rn(k5, gu1, __fma_rn(k6, gu2, k7 * gu3)))))));
+      double dnu = __fma_rn(k0, gu0, __fma_rn(k1, gu1, __fma_rn(k2, gu2, __fma_rn(k3, gu3,
+                   __fma_rn(k4, gd0, __fma_rn(k5, gd1, __fma_rn(k6, gd2, k7 * gd3)))))));
+      double diag_d = k0 * B4, diag_u = k0 * B4;
+      if (rare) {
+        // Robin face mass: x- / y-faces through this layer, z-face of plane d (in-plane)
+        double ad = 0.0, au = 0.0, gdg = 0.0;
+        const int gy = gy0 + j;
+        const double rx = (gx == 0 ? es.robin[0] : 0.0) + (gx == g.n[0] ? es.robin[1] : 0.0);
+        const double ryj = (gy == 0 ? es.robin[2] : 0.0) + (gy == g.n[1] ? es.robin[3] : 0.0);
+        const double cxm = gx >= 1 ? 1.0 : 0.0, cxp = gx < g.n[0] ? 1.0 : 0.0;
+        const double cym = gy >= 1 ? 1.0 : 0.0, cyp = gy < g.n[1] ? 1.0 : 0.0;
+        if (layer_ok && rx != 0.0) {   // face elements (y-1/2 | y+1/2) x (layer)
+          const double cm = cym, cp = cyp, c2 = cm + cp;
+          ad += rx * (c2 * (c9 * wd[j + 1][1] + c18 * wu[j + 1][1]) + cm * (c18 * wd[j][1] + c36 * wu[j][1]) +
+                      cp * (c18 * wd[j + 2][1] + c36 * wu[j + 2][1]));
+          au += rx * (c2 * (c9 * wu[j + 1][1] + c18 * wd[j + 1][1]) + cm * (c18 * wu[j][1] + c36 * wd[j][1]) +
+                      cp * (c18 * wu[j + 2][1] + c36 * wd[j + 2][1]));
+          gdg += rx * c2 * c9;
+        }
+        if (layer_ok && ryj != 0.0) {   // face elements (x-1/2 | x+1/2) x (layer)
+          const double cm = cxm, cp = cxp, c2 = cm + cp;
+          ad += ryj * (c2 * (c9 * wd[j + 1][1] + c18 * wu[j + 1][1]) + cm * (c18 * wd[j + 1][0] + c36 * wu[j + 1][0]) +
+                         cp * (c18 * wd[j + 1][2] + c36 * wu[j + 1][2]));
+          au += ryj * (c2 * (c9 * wu[j + 1][1] + c18 * wd[j + 1][1]) + cm * (c18 * wu[j + 1][0] + c36 * wd[j + 1][0]) +
+                         cp * (c18 * wu[j + 1][2] + c36 * wd[j + 1][2]));
+          gdg += ryj * c2 * c9;
+        }
+        diag_u += gdg;
+        diag_d += gdg;
+        if (rz != 0.0) {   // z-face through plane d: the in-plane elements (x+-1/2, y+-1/2)
+          const double sx = cxm + cxp, sy = cym + cyp;
+          ad += rz * (c9 * sx * sy * wd[j + 1][1] + c18 * (sy * (cxm * wd[j + 1][0] + cxp * wd[j + 1][2]) +
+                                                            sx * (cym * wd[j][1] + cyp * wd[j + 2][1])) +
+                      c36 * (cxm * cym * wd[j][0] + cxp * cym * wd[j][2] + cxm * cyp * wd[j + 2][0] +
+                             cxp * cyp * wd[j + 2][2]));
+          diag_d += rz * c9 * sx * sy;
+        }
+        upd += ad;
+        dnu += au;
+      }
+      if (s >= 2 && own_ok[j]) {
+        const double ap = part[j] + upd;
+        const double diag = dpart[j] + diag_d;
+        const double pc = wd[j + 1][1];
+        const long long off = (long long)d * S + own_off[j];
+        const int io = (RY * w + j) * TX + lane;
+        if (MODE == MODE_K1) {
+          acc0 = __fma_rn(pc, ap, acc0);
+          a.o0[off] = pc;
+        } else if (MODE == MODE_K2) {
+          const double dinv = es.precond ? (diag > 0.0 ? __drcp_rn(diag) : 0.0) : 1.0;
+          const double xn = __fma_rn(alpha, pc, I0[io]);
+          const double rn = __fma_rn(-alpha, ap, I1[io]);
+          const double zz = dinv * rn;
+          acc0 = __fma_rn(rn, zz, acc0);
+          acc1 = __fma_rn(rn, rn, acc1);
+          a.o0[off] = xn;
+          a.o1[off] = rn;
+          a.o2[off] = zz;
+        } else if (MODE == MODE_INIT) {
+          const double dinv = es.precond ? (diag > 0.0 ? __drcp_rn(diag) : 0.0) : 1.0;
+          const double bv = I0[io];
+          acc2 = __fma_rn(bv, bv, acc2);
+          const double rn = bv - ap;
+          const double zz = dinv * rn;
+          acc0 = __fma_rn(rn, zz, acc0);
+          acc1 = __fma_rn(rn, rn, acc1);
+          a.o0[off] = rn;
+          a.o1[off] = zz;
+        } else if (MODE == MODE_TRUE) {
+          const double rn = I0[io] - ap;
+          acc1 = __fma_rn(rn, rn, acc1);
+        } else {
+          a.o0[off] = ap;
+        }
+      }
+      part[j] = dnu;
+      dpart[j] = diag_u;
+    }
+  };
+
+  double wA[RY + 2][3], wB[RY + 2][3];
+  for (int s = 0; s < nsteps; s += 2) {   // unrolled by two: the two plane windows swap roles
+    step(s, wB, wA);
+    if (s + 1 < nsteps) step(s + 1, wA, wB);
+  }
+  if (MODE != MODE_APPLY) reduce_finalize(MODE, a, acc0, acc1, acc2);
+#undef k0
+#undef k1
+#undef k2
+#undef k3
+#undef k4
+#undef k5
+#undef k6
+#undef k7
+}
+
+template <int MODE, int NS>
+constexpr int elem_smem() { return ElemCfg<MODE>::SBYTES * NS + 128; }
+
+template <int MODE, int NS>
+cudaError_t set_elem_tma_attr() {
+  return cudaFuncSetAttribute(k_jcg_elem_tma<MODE, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, elem_smem<MODE, NS>());
+}
+
+template <int MODE, int NS>
+cudaError_t launch_elem_tma_mode(dim3 grid, const LevelGeom& g, const ElemStencil& es, const KArgs& a,
+                                 const CUtensorMap* m, cudaStream_t st) {
+  count_launch();
+  k_jcg_elem_tma<MODE, NS><<<grid, dim3(TX, WARPS), elem_smem<MODE, NS>(), st>>>(g, es, a, m[0], m[1], m[2], m[3], m[4]);
+  return cudaGetLastError();
+}
+
+// ---- tensor-map cache: (base, geometry, box) -> CUtensorMap; an entry is a pure function of its key
+struct MapKey {
+  const void* base;
+  long long d0, d1, d2, s1, s2;
+  int bx, by;
+  bool operator==(const MapKey& o) const {
+    return base == o.base && d0 == o.d0 && d1 == o.d1 && d2 == o.d2 && s1 == o.s1 && s2 == o.s2 && bx == o.bx &&
+           by == o.by;
+  }
+};
+struct MapEntry { MapKey k; CUtensorMap m; };
+constexpr int kMapCache = 64;
+
+bool encode_map(CUtensorMap* out, const MapKey& k) {
+  static std::mutex mu;
+  static MapEntry cache[kMapCache];
+  static int used = 0, next = 0;
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  for (int i = 0; i < used; ++i)
+    if (cache[i].k == k) { *out = cache[i].m; return true; }
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn) {
+      cudaGetLastError();
+      return false;
+    }
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  cuuint64_t dims[3] = {(cuuint64_t)k.d0, (cuuint64_t)k.d1, (cuuint64_t)k.d2};
+  cuuint64_t strides[2] = {(cuuint64_t)k.s1 * 8, (cuuint64_t)k.s2 * 8};
+  cuuint32_t box[3] = {(cuuint32_t)k.bx, (cuuint32_t)k.by, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUtensorMap m;
+  if (encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(k.base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  const int slot = used < kMapCache ? used++ : (next++ % kMapCache);
+  cache[slot].k = k;
+  cache[slot].m = m;
+  *out = m;
+  return true;
+}
+
+bool vec_map(CUtensorMap* m, const double* base, const LevelGeom& g, int bx, int by) {
+  const MapKey k{base, g.nf[0], g.nf[1], g.nza, g.P, g.S, bx, by};
+  return encode_map(m, k);
+}
+bool beta_map(CUtensorMap* m, const double* beta, const LevelGeom& g) {
+  const MapKey k{beta, g.n[0] + 4, g.n[1] + 4, g.n[2] + 4, g.BP, g.BS, EBX, EBY};
+  return encode_map(m, k);
+}
+
+}  // namespace
+
+cudaError_t init_elem_kernel_attributes() {
+  cudaError_t e = set_elem_tma_attr<MODE_K1, 3>();
+  if (e == cudaSuccess) e = set_elem_tma_attr<MODE_K2, 3>();
+  if (e == cudaSuccess) e = set_elem_tma_attr<MODE_INIT, 3>();
+  if (e == cudaSuccess) e = set_elem_tma_attr<MODE_TRUE, 3>();
+  if (e == cudaSuccess) e = set_elem_tma_attr<MODE_APPLY, 3>();
+  return e;
+}
+
+int elem_tile_rows() { return TY; }
+
+// K1: h0 = z, h1 = p_old, o0 = p. K2: h0 = p, i0 = x, i1 = r, o0 = x, o1 = r, o2 = z.
+// INIT: h0 = x, i0 = b, o0 = r, o1 = z. TRUE: h0 = x, i0 = b. APPLY: h0 = p, o0 = A p.
+cudaError_t launch_jcg_elem(int mode, const LevelGeom& g, const ElemStencil& es, const Problem&, const KArgs& a,
+                            cudaStream_t st) {
+  if (g.BP % 2 != 0 || !a.h0 || !a.beta) return cudaErrorInvalidValue;
+  CUtensorMap m[5];
+  bool ok = vec_map(&m[0], a.h0, g, HX, HY) && beta_map(&m[2], a.beta, g);
+  m[1] = m[0];
+  m[3] = m[0];
+  m[4] = m[0];
+  if (ok && mode == MODE_K1) ok = a.h1 && vec_map(&m[1], a.h1, g, HX, HY);
+  if (ok && (mode == MODE_K2 || mode == MODE_INIT || mode == MODE_TRUE)) ok = a.i0 && vec_map(&m[3], a.i0, g, TX, TY);
+  if (ok && mode == MODE_K2) ok = a.i1 && vec_map(&m[4], a.i1, g, TX, TY);
+  if (!ok) return cudaErrorInvalidValue;
+  dim3 grid((g.nf[0] + TX - 1) / TX, (g.nf[1] + TY - 1) / TY, (g.zend - g.zbeg + a.zc - 1) / a.zc);
+  switch (mode) {
+    case MODE_K1: return launch_elem_tma_mode<MODE_K1, 3>(grid, g, es, a, m, st);
+    case MODE_K2: return launch_elem_tma_mode<MODE_K2, 3>(grid, g, es, a, m, st);
+    case MODE_INIT: return launch_elem_tma_mode<MODE_INIT, 3>(grid, g, es, a, m, st);
+    case MODE_TRUE: return launch_elem_tma_mode<MODE_TRUE, 3>(grid, g, es, a, m, st);
+    case MODE_APPLY: return launch_elem_tma_mode<MODE_APPLY, 3>(grid, g, es, a, m, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace ecmg
