@@ -112,7 +112,9 @@ __global__ void __launch_bounds__(NTH, 2)
   using C = ElemCfg<MODE>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[NS];
-  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  // (offset from smem_raw, not a uintptr_t round trip: the pointer must stay in the shared window so
+  // the reads compile to LDS, not generic LD)
+  unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   JcgScalars* sc = a.sc;
   if (MODE == MODE_K1 || MODE == MODE_K2) {
     if (*(volatile int*)&sc->done) return;
@@ -417,12 +419,15 @@ bool beta_map(CUtensorMap* m, const double* beta, const LevelGeom& g) {
 
 }  // namespace
 
+// ring depth per mode: two CTAs per SM (register bound) leave ~110 KB of shared memory each
+constexpr int NS_K1 = 6, NS_K2 = 5, NS_OTHER = 4;
+
 cudaError_t init_elem_kernel_attributes() {
-  cudaError_t e = set_elem_tma_attr<MODE_K1, 3>();
-  if (e == cudaSuccess) e = set_elem_tma_attr<MODE_K2, 3>();
-  if (e == cudaSuccess) e = set_elem_tma_attr<MODE_INIT, 3>();
-  if (e == cudaSuccess) e = set_elem_tma_attr<MODE_TRUE, 3>();
-  if (e == cudaSuccess) e = set_elem_tma_attr<MODE_APPLY, 3>();
+  cudaError_t e = set_elem_tma_attr<MODE_K1, NS_K1>();
+  if (e == cudaSuccess) e = set_elem_tma_attr<MODE_K2, NS_K2>();
+  if (e == cudaSuccess) e = set_elem_tma_attr<MODE_INIT, NS_OTHER>();
+  if (e == cudaSuccess) e = set_elem_tma_attr<MODE_TRUE, NS_OTHER>();
+  if (e == cudaSuccess) e = set_elem_tma_attr<MODE_APPLY, NS_OTHER>();
   return e;
 }
 
@@ -444,11 +449,11 @@ cudaError_t launch_jcg_elem(int mode, const LevelGeom& g, const ElemStencil& es,
   if (!ok) return cudaErrorInvalidValue;
   dim3 grid((g.nf[0] + TX - 1) / TX, (g.nf[1] + TY - 1) / TY, (g.zend - g.zbeg + a.zc - 1) / a.zc);
   switch (mode) {
-    case MODE_K1: return launch_elem_tma_mode<MODE_K1, 3>(grid, g, es, a, m, st);
-    case MODE_K2: return launch_elem_tma_mode<MODE_K2, 3>(grid, g, es, a, m, st);
-    case MODE_INIT: return launch_elem_tma_mode<MODE_INIT, 3>(grid, g, es, a, m, st);
-    case MODE_TRUE: return launch_elem_tma_mode<MODE_TRUE, 3>(grid, g, es, a, m, st);
-    case MODE_APPLY: return launch_elem_tma_mode<MODE_APPLY, 3>(grid, g, es, a, m, st);
+    case MODE_K1: return launch_elem_tma_mode<MODE_K1, NS_K1>(grid, g, es, a, m, st);
+    case MODE_K2: return launch_elem_tma_mode<MODE_K2, NS_K2>(grid, g, es, a, m, st);
+    case MODE_INIT: return launch_elem_tma_mode<MODE_INIT, NS_OTHER>(grid, g, es, a, m, st);
+    case MODE_TRUE: return launch_elem_tma_mode<MODE_TRUE, NS_OTHER>(grid, g, es, a, m, st);
+    case MODE_APPLY: return launch_elem_tma_mode<MODE_APPLY, NS_OTHER>(grid, g, es, a, m, st);
     default: return cudaErrorInvalidValue;
   }
 }

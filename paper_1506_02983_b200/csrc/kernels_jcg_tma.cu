@@ -82,7 +82,9 @@ __global__ void __launch_bounds__(NTH, 2)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[NS];
   // TMA destinations must be 128-byte aligned in the shared window: align the stage base explicitly
-  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  // (offset from smem_raw, not a uintptr_t round trip: the pointer must stay in the shared window so
+  // the reads compile to LDS, not generic LD)
+  unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   JcgScalars* sc = a.sc;
   if (MODE == MODE_K1 || MODE == MODE_K2) {
     if (*(volatile int*)&sc->done) return;
