@@ -491,7 +491,8 @@ int ecmg_create_grid(const ecmg_box* dom, const int coarsest_cells[3], int num_l
   alloc(&G->p[1], G->vec_doubles);
   alloc(&G->b, G->vec_doubles);
   alloc(&G->partials, G->partial_doubles);
-  alloc(&G->scratch1d, 3LL * (std::max(gmax.n[0], std::max(gmax.n[1], gmax.n[2])) + 1));
+  alloc(&G->scratch1d, 15LL * (   // 1D Gauss loads: up to 5 separable terms x 3 axes
+      std::max(gmax.n[0], std::max(gmax.n[1], gmax.n[2])) + 1));
   alloc(&G->seeds, (long long)(gmax.n[0] / 2 + 1) * (gmax.n[1] / 2 + 1) * (gmax.n[2] / 2 + 1));
   if (st == ECMG_OK && cudaMalloc(&G->sc, sizeof(JcgScalars)) != cudaSuccess) st = ECMG_ENOMEM;
   if (st == ECMG_OK && cudaMemsetAsync(G->sc, 0, sizeof(JcgScalars), G->stream) != cudaSuccess) st = ECMG_ECUDA;

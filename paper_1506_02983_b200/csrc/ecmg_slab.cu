@@ -423,7 +423,7 @@ SlabDriver* slab_driver_create(const SlabCfg& cfg, int P, int rank, bool virt, c
     };
     bool ok = alloc(&c.x, vec) && alloc(&c.r, vec) && alloc(&c.z, vec) && alloc(&c.p[0], vec) && alloc(&c.p[1], vec) && alloc(&c.b, vec) &&
               alloc(&c.beta, beta_n) && alloc(&c.partials, part_n) &&
-              alloc(&c.scratch1d, 3LL * (std::max(gf.n[0], std::max(gf.n[1], gf.n[2])) + 1)) &&
+              alloc(&c.scratch1d, 15LL * (std::max(gf.n[0], std::max(gf.n[1], gf.n[2])) + 1)) &&
               alloc(&c.seeds, (long long)(gf.n[0] / 2 + 1) * (gf.n[1] / 2 + 1) * (gf.n[2] / 2 + 1)) &&
               alloc(&c.ut, level_nodes(gf));
     if (ok) {

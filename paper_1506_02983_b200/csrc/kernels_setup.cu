@@ -29,11 +29,12 @@ __global__ void k_beta(const LevelGeom g, const Problem pb, double* __restrict__
 
 // ---- right-hand side ---------------------------------------------------------------------------
 // b_f = F_f + G_f - A_fD g_D (§8c A2/A4/A5) in up to three passes:
-//  (1) volume load F by 2x2x2 Gauss. Separable f = A g_x(x) g_y(y) g_z(z) (C1, C2, C5, P1, P2, the
-//      patch tests): F_i = A L_x(i_x) L_y(i_y) L_z(i_z), with the 1D Gauss loads
-//      L_d(i) = sum_{e in {i-1,i}} (h_d/2) sum_{q=+-} g_d(x_q) N(xi_q) (the 3D rule factorises exactly).
-//      Otherwise (C3, C4, P3): z-marching CTAs evaluate f once per Gauss point of each element plane
-//      (shared memory), form the element load vectors, and every node gathers its 8 entries.
+//  (1) volume load F by 2x2x2 Gauss. Separable f = sum_k A_k g_k^x(x) g_k^y(y) g_k^z(z) (rank 1: C1, C2,
+//      C5, P1, P2, the patch tests; rank 5: C3): F_i = sum_k A_k L_kx(i_x) L_ky(i_y) L_kz(i_z), with the
+//      1D Gauss loads L_kd(i) = sum_{e in {i-1,i}} (h_d/2) sum_{q=+-} g_kd(x_q) N(xi_q) (the 3D rule
+//      factorises exactly). Otherwise (C4, P3): z-marching CTAs evaluate f once per Gauss point of
+//      each element plane (shared memory), form the element load vectors, and every node gathers its
+//      8 entries.
 //  (2) boundary shell of the free box: Robin face load G (2x2 Gauss) and the lifting -A_fD g_D.
 // ||b||^2 is accumulated by the JCG init pass, which reads b anyway.
 // node tile 31 x 7 -> element tile 32 x 8 = 256 = one element (and 8 Gauss points) per thread
@@ -41,18 +42,31 @@ constexpr int VX = 31, VY = 7, VNTH = 256;
 constexpr int VEX = VX + 1, VEY = VY + 1, VNE = VEX * VEY;     // 32 x 8 elements per plane
 constexpr int VSMEM = (VNE * 8 + 2 * VNE * 8) * (int)sizeof(double);
 
-// separable factor g_d and amplitude: returns false if f is not a product of 1D functions
-__host__ __device__ inline bool prob_separable(int id) {
+// f as a sum of R products of 1D functions, f = sum_k A_k g_k^x(x) g_k^y(y) g_k^z(z); R = 0: not
+// separable (volume kernel). C3's f = -beta Lap u - grad beta . grad u with beta = 1 + 1/2 sin(2 pi x)
+// cos(2 pi y) sin(2 pi z), u = cos(pi x) cos(pi y) e^z expands into 5 such terms:
+//   -(1 - 2 pi^2) [cx][cy][e^z]            -(1 - 2 pi^2)/2 [s2x cx][c2y cy][s2z e^z]   (-beta Lap u)
+//   +pi^2 [c2x sx][c2y cy][s2z e^z]        -pi^2 [s2x cx][s2y sy][s2z e^z]             (-beta_x u_x, -beta_y u_y)
+//   -pi [s2x cx][c2y cy][c2z e^z]                                                        (-beta_z u_z)
+// (sx = sin(pi x), s2x = sin(2 pi x), ...). The 2x2x2 Gauss rule factorises exactly per term.
+constexpr int kMaxSepRank = 5;
+__host__ __device__ inline int prob_sep_rank(int id) {
   switch (id) {
-    case 1: case 2: case 5: case 11: case 12: case 21: case 22: case 23: case 24: return true;
-    default: return false;
+    case 1: case 2: case 5: case 11: case 12: case 21: case 22: case 23: case 24: return 1;
+    case 3: return 5;
+    default: return 0;
   }
 }
-__device__ inline double sep_amp(const Problem& P) {
+__host__ __device__ inline bool prob_separable(int id) { return prob_sep_rank(id) > 0; }
+__device__ inline double sep_amp(const Problem& P, int k) {
   const double pi = kPi();
   switch (P.id) {
     case 1: return 3.0 * pi * pi;
     case 2: return -3.0;
+    case 3: {
+      const double A[5] = {-(1.0 - 2.0 * pi * pi), -0.5 * (1.0 - 2.0 * pi * pi), pi * pi, -pi * pi, -pi};
+      return A[k];
+    }
     case 5: return P.params[47];
     case 11: return 0.75 * pi * pi;
     case 12: return -(1.0 - 2.5 * pi * pi);
@@ -60,11 +74,21 @@ __device__ inline double sep_amp(const Problem& P) {
     default: return 0.0;   // patch tests: f = 0
   }
 }
-__device__ inline double sep_g(const Problem& P, int d, double t) {
+__device__ inline double sep_g(const Problem& P, int k, int d, double t) {
   const double pi = kPi();
   switch (P.id) {
     case 1: return sin(pi * t);
     case 2: return exp(t);
+    case 3: {
+      double s1, c1, s2, c2;
+      sincospi(t, &s1, &c1);
+      sincospi(2.0 * t, &s2, &c2);
+      if (d == 0) { const double gx[5] = {c1, s2 * c1, c2 * s1, s2 * c1, s2 * c1}; return gx[k]; }
+      if (d == 1) { const double gy[5] = {c1, c2 * c1, c2 * c1, s2 * s1, c2 * c1}; return gy[k]; }
+      const double e = exp(t);
+      const double gz[5] = {e, s2 * e, s2 * e, s2 * e, c2 * e};
+      return gz[k];
+    }
     case 5: { const double c = P.params[43 + d], s = P.params[46]; return exp(-(t - c) * (t - c) / (2.0 * s * s)); }
     case 11: return sin(0.5 * pi * t);
     case 12: return d == 0 ? sin(1.5 * pi * t) : (d == 1 ? sin(0.5 * pi * t) : exp(t));
@@ -72,28 +96,33 @@ __device__ inline double sep_g(const Problem& P, int d, double t) {
   }
 }
 
-// L_d(i), i = 0..n_d, for d = 0, 1, 2 stored at L[d * (nmax + 1) + i]
+// L_{k,d}(i), i = 0..n_d, for term k and axis d stored at L[(3 k + d) * (nmax + 1) + i]
 __global__ void k_load1d(const LevelGeom g, const Problem pb, double* __restrict__ L, int stride) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x, d = blockIdx.y;
-  if (i > g.n[d]) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x, d = blockIdx.y % 3, k = blockIdx.y / 3;
+  if (i > g.n[d] || k >= kMaxSepRank) return;
   double v = 0.0;
   for (int e = i - 1; e <= i; ++e) {
     if (e < 0 || e >= g.n[d]) continue;
     const double side = (e == i - 1) ? 1.0 : -1.0;   // node is local 1 (xi = +1) of e = i-1, local 0 of e = i
     for (int q = 0; q < 2; ++q) {
       const double xi = q ? kGauss : -kGauss;
-      v += sep_g(pb, d, g.lo[d] + (e + (1.0 + xi) / 2.0) * g.h[d]) * ((1.0 + side * xi) / 2.0) * (g.h[d] / 2.0);
+      v += sep_g(pb, k, d, g.lo[d] + (e + (1.0 + xi) / 2.0) * g.h[d]) * ((1.0 + side * xi) / 2.0) * (g.h[d] / 2.0);
     }
   }
-  L[(long long)d * stride + i] = v;
+  L[(long long)blockIdx.y * stride + i] = v;
 }
 
 __global__ void k_rhs_sep(const LevelGeom g, const Problem pb, const double* __restrict__ L, int stride,
                           double* __restrict__ b) {
   const int fx = blockIdx.x * blockDim.x + threadIdx.x, fy = blockIdx.y, lz = g.zbeg + blockIdx.z;
   if (fx >= g.nf[0]) return;
-  const double A = sep_amp(pb);
-  const double v = A * __ldg(L + g.flo[0] + fx) * __ldg(L + stride + g.flo[1] + fy) * __ldg(L + 2 * stride + g.flo[2] + g.zoff + lz);
+  const int R = prob_sep_rank(pb.id);
+  double v = 0.0;
+  for (int k = 0; k < R; ++k) {
+    const double* Lk = L + 3LL * k * stride;
+    v += sep_amp(pb, k) * __ldg(Lk + g.flo[0] + fx) * __ldg(Lk + stride + g.flo[1] + fy) *
+         __ldg(Lk + 2 * stride + g.flo[2] + g.zoff + lz);
+  }
   b[(long long)lz * g.S + (long long)fy * g.P + fx] = v;
 }
 
@@ -325,7 +354,7 @@ cudaError_t launch_rhs(const LevelGeom& g, const Problem& pb, const ElemStencil&
   if (prob_separable(pb.id)) {
     const int nmax = std::max(g.n[0], std::max(g.n[1], g.n[2]));
     const int stride = nmax + 1;
-    dim3 g1((stride + 127) / 128, 3);
+    dim3 g1((stride + 127) / 128, 3 * prob_sep_rank(pb.id));
     count_launch();
     k_load1d<<<g1, 128, 0, st>>>(g, pb, scratch, stride);
     dim3 g2((g.nf[0] + 127) / 128, g.nf[1], g.zend - g.zbeg);
