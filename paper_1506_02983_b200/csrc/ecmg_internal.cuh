@@ -62,6 +62,7 @@ struct ElemStencil {
   double kappa[8];
   double robin[6];     // alpha_F * h1 * h2 for Robin faces with alpha != 0, else 0
   int precond;         // 1 = Jacobi, 0 = plain CG (dinv = 1)
+  int cube;            // h_x = h_y = h_z: kappa = c{4,0,0,-1,0,-1,-1,-1} (the element kernel's short form)
 };
 
 // Device-resident CG scalars (no host round trip inside the iteration).

@@ -54,6 +54,7 @@ inline ElemStencil make_elem_stencil(const LevelGeom& g, const Problem& pb, int 
     es.robin[F] = (pb.face[F] == FACE_ROBIN && pb.alpha[F] != 0.0) ? pb.alpha[F] * g.h[d1] * g.h[d2] : 0.0;
   }
   es.precond = precond;
+  es.cube = g.h[0] == g.h[1] && g.h[0] == g.h[2];
   return es;
 }
 

@@ -102,13 +102,13 @@ __device__ __forceinline__ void issue_elem_stage(unsigned char* smem, uint64_t* 
   mbar_expect_tx(&full[st], tx_bytes);
   const int zh = z0 - 1 + t;
   tma_load_3d(base, pH0, X0 - XO, Y0 - 1, zh, &full[st]);
-  if (C::kH1 && !first) tma_load_3d(base + HSTRIDE, pH1, X0 - XO, Y0 - 1, zh, &full[st]);
+  if (C::kH1) tma_load_3d(base + HSTRIDE, pH1, X0 - XO, Y0 - 1, zh, &full[st]);
   tma_load_3d(base + C::OFF_E, pE, X0, ey0, ez_base + zh, &full[st]);
   if (C::kNI >= 1) tma_load_3d(base + C::OFF_I, pI0, X0, Y0, zh - 1, &full[st]);
   if (C::kNI >= 2) tma_load_3d(base + C::OFF_I + IBYTES, pI1, X0, Y0, zh - 1, &full[st]);
 }
 
-template <int MODE, int NS>
+template <int MODE, int NS, bool CUBE>
 __global__ void __launch_bounds__(NTH, ELEM_MINB)
     k_jcg_elem_tma(const LevelGeom g, const ElemStencil es, const KArgs a, const __grid_constant__ CUtensorMap mH0,
                    const __grid_constant__ CUtensorMap mH1, const __grid_constant__ CUtensorMap mE,
@@ -132,13 +132,16 @@ __global__ void __launch_bounds__(NTH, ELEM_MINB)
   bool first = false;
   if (MODE == MODE_K1) { bcg = sc->beta; first = (sc->iter == 0); }
   if (MODE == MODE_K2) alpha = sc->alpha;
-  const uint32_t tx_bytes = HBYTES * ((C::kH1 && !first) ? 2 : 1) + EBYTES + IBYTES * C::kNI;
+  // iteration 0 of K1 (p = z): the p_old slot is filled from z and beta_cg = 0 (exact for finite z), so
+  // the window update is one FMA with no per-element select
+  const double bcg_eff = first ? 0.0 : bcg;
+  const uint32_t tx_bytes = HBYTES * (C::kH1 ? 2 : 1) + EBYTES + IBYTES * C::kNI;
   const int ez_base = g.flo[2] + g.zoff + 1;       // beta-array plane of the layer below node plane 0, + 1
   const int eo = g.flo[0] + 1;                     // smem column of the left element of lane 0
   const bool zrobin = es.robin[4] != 0.0 || es.robin[5] != 0.0;
 
   const CUtensorMap* pH0 = &mH0;
-  const CUtensorMap* pH1 = &mH1;
+  const CUtensorMap* pH1 = (C::kH1 && first) ? &mH0 : &mH1;
   const CUtensorMap* pE = &mE;
   const CUtensorMap* pI0 = &mI0;
   const CUtensorMap* pI1 = &mI1;
@@ -217,7 +220,7 @@ __global__ void __launch_bounds__(NTH, ELEM_MINB)
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           const int o = (RY * w + r) * HX + XO - 1 + lane + c;
-          wu[r][c] = pcg_direction(1.0, H[o], bcg, H1[o], first);
+          wu[r][c] = __fma_rn(bcg_eff, H1[o], H[o]);
         }
       if ((zl == g.zbeg - 1 || zl == g.zend) && zl >= 0 && zl < g.nza) {
 #pragma unroll
@@ -249,6 +252,18 @@ __global__ void __launch_bounds__(NTH, ELEM_MINB)
       const double bLB = bl[j][0], bRB = bl[j][1], bLA = bl[j + 1][0], bRA = bl[j + 1][1];
       const double Wxm = bLB + bLA, Wxp = bRB + bRA, Wym = bLB + bRB, Wyp = bLA + bRA;
       const double B4 = Wxm + Wxp;
+      double upd, dnu;
+      if (CUBE) {
+        // cubic cells: kappa = {4c, 0, 0, -c, 0, -c, -c, -c} by pattern (K_e = c{4,0,-1,-1}), so
+        //   to d: kappa_0 G0(p_d) + kappa_7 (G3(p_d) + Sg(p_u)),  to u: kappa_0 G0(p_u) + kappa_7 (G3(p_u) + Sg(p_d))
+        // with Sg = G1 + G2 + G3 (the axis-weight zeros are dropped: |kappa_1| <= 1e-16 kappa_0 in fp64)
+        const double gd3 = __fma_rn(bRA, wd[j + 2][2], __fma_rn(bLA, wd[j + 2][0], __fma_rn(bRB, wd[j][2], bLB * wd[j][0])));
+        const double gu3 = __fma_rn(bRA, wu[j + 2][2], __fma_rn(bLA, wu[j + 2][0], __fma_rn(bRB, wu[j][2], bLB * wu[j][0])));
+        const double sd = __fma_rn(Wyp, wd[j + 2][1], __fma_rn(Wym, wd[j][1], __fma_rn(Wxp, wd[j + 1][2], __fma_rn(Wxm, wd[j + 1][0], gd3))));
+        const double su = __fma_rn(Wyp, wu[j + 2][1], __fma_rn(Wym, wu[j][1], __fma_rn(Wxp, wu[j + 1][2], __fma_rn(Wxm, wu[j + 1][0], gu3))));
+        upd = __fma_rn(k0, B4 * wd[j + 1][1], k7 * (gd3 + su));
+        dnu = __fma_rn(k0, B4 * wu[j + 1][1], k7 * (gu3 + sd));
+      } else {
       const double gd0 = B4 * wd[j + 1][1], gu0 = B4 * wu[j + 1][1];
       const double gd1 = __fma_rn(Wxp, wd[j + 1][2], Wxm * wd[j + 1][0]);
       const double gu1 = __fma_rn(Wxp, wu[j + 1][2], Wxm * wu[j + 1][0]);
@@ -256,10 +271,11 @@ __global__ void __launch_bounds__(NTH, ELEM_MINB)
       const double gu2 = __fma_rn(Wyp, wu[j + 2][1], Wym * wu[j][1]);
       const double gd3 = __fma_rn(bRA, wd[j + 2][2], __fma_rn(bLA, wd[j + 2][0], __fma_rn(bRB, wd[j][2], bLB * wd[j][0])));
       const double gu3 = __fma_rn(bRA, wu[j + 2][2], __fma_rn(bLA, wu[j + 2][0], __fma_rn(bRB, wu[j][2], bLB * wu[j][0])));
-      double upd = __fma_rn(k0, gd0, __fma_rn(k1, gd1, __fma_rn(k2, gd2, __fma_rn(k3, gd3,
-                   __fma_rn(k4, gu0, __fma_rn(k5, gu1, __fma_rn(k6, gu2, k7 * gu3)))))));
-      double dnu = __fma_rn(k0, gu0, __fma_rn(k1, gu1, __fma_rn(k2, gu2, __fma_rn(k3, gu3,
-                   __fma_rn(k4, gd0, __fma_rn(k5, gd1, __fma_rn(k6, gd2, k7 * gd3)))))));
+      upd = __fma_rn(k0, gd0, __fma_rn(k1, gd1, __fma_rn(k2, gd2, __fma_rn(k3, gd3,
+            __fma_rn(k4, gu0, __fma_rn(k5, gu1, __fma_rn(k6, gu2, k7 * gu3)))))));
+      dnu = __fma_rn(k0, gu0, __fma_rn(k1, gu1, __fma_rn(k2, gu2, __fma_rn(k3, gu3,
+            __fma_rn(k4, gd0, __fma_rn(k5, gd1, __fma_rn(k6, gd2, k7 * gd3)))))));
+      }
       double diag_d = k0 * B4, diag_u = k0 * B4;
       if (rare) {
         // Robin face mass: x- / y-faces through this layer, z-face of plane d (in-plane)
@@ -361,7 +377,11 @@ constexpr int elem_smem() { return ElemCfg<MODE>::SBYTES * NS + 128; }
 
 template <int MODE, int NS>
 cudaError_t set_elem_tma_attr() {
-  return cudaFuncSetAttribute(k_jcg_elem_tma<MODE, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, elem_smem<MODE, NS>());
+  cudaError_t e = cudaFuncSetAttribute(k_jcg_elem_tma<MODE, NS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       elem_smem<MODE, NS>());
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_jcg_elem_tma<MODE, NS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              elem_smem<MODE, NS>());
 }
 
 template <int MODE, int NS>
@@ -369,7 +389,10 @@ cudaError_t launch_elem_tma_mode(const LevelGeom& g, const ElemStencil& es, cons
                                  cudaStream_t st) {
   dim3 grid((g.nf[0] + TX - 1) / TX, (g.nf[1] + TY - 1) / TY, (g.zend - g.zbeg + a.zc - 1) / a.zc);
   count_launch();
-  k_jcg_elem_tma<MODE, NS><<<grid, dim3(TX, WARPS), elem_smem<MODE, NS>(), st>>>(g, es, a, m[0], m[1], m[2], m[3], m[4]);
+  if (es.cube)
+    k_jcg_elem_tma<MODE, NS, true><<<grid, dim3(TX, WARPS), elem_smem<MODE, NS>(), st>>>(g, es, a, m[0], m[1], m[2], m[3], m[4]);
+  else
+    k_jcg_elem_tma<MODE, NS, false><<<grid, dim3(TX, WARPS), elem_smem<MODE, NS>(), st>>>(g, es, a, m[0], m[1], m[2], m[3], m[4]);
   return cudaGetLastError();
 }
 

@@ -22,10 +22,16 @@ def main():
     ap.add_argument("--config", default="c4")
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--skip-run", action="store_true")
+    ap.add_argument("--host-loop", action="store_true",
+                    help="JCG loop driven from the host (same kernels): ncu does not list launches inside the "
+                         "CUDA graph's conditional WHILE body")
     a = ap.parse_args()
     pid, n0, levels, eps = {"c4": (PROB["C4"], 4, 8, 1e-9), "c3": (PROB["C3"], 4, 7, 1e-10),
                             "c2": (PROB["C2"], 4, 6, 1e-10)}[a.config]
     g = Grid(n0, levels, pid)
+    if a.host_loop:
+        from paper_1506_02983_b200 import ecmg
+        g.set_option(ecmg.OPT_GRAPH, 0)
     shape, nodes = g.shape(levels - 1)
     u = torch.empty(nodes, dtype=torch.float64, device="cuda")
     ut = torch.empty_like(u)
