@@ -58,7 +58,9 @@ struct ecmg_grid {
   bool ev_init = false;
   int kernel_variant = 1;   // ECMG_OPT_KERNEL
   int use_graph = 1;        // ECMG_OPT_GRAPH: device-driven JCG loop (CUDA graph, conditional WHILE node)
-  long long persistent_max = 5000;   // ECMG_OPT_PERSISTENT: one cooperative launch per solve up to this size
+  long long persistent_max = 40000;  // ECMG_OPT_PERSISTENT: one cooperative launch per solve up to this size (tools/tune_persistent.py)
+  double* aux[2] = {nullptr, nullptr};   // persistent element-path solve: w = A p and D^-1 (level-sized)
+  long long aux_doubles = 0;
   cudaStream_t cap_stream = nullptr;          // private stream used only for graph capture
   ParamHost* param_host = nullptr;   // pinned
   std::vector<cudaGraphExec_t> graphs;        // per level, lazily built
@@ -294,12 +296,38 @@ int run_jcg_graph(ecmg_grid* G, int k, double eps, ecmg_stats* st) {
   return fill_stats(G, g, eps, st);
 }
 
-// small constant-stencil levels: the whole solve in one cooperative launch (latency bound)
+bool use_persistent(const ecmg_grid* G, const LevelGeom& g) {
+  return !G->slab && G->persistent_max > 0 && free_count(g) <= G->persistent_max;
+}
+
+// the whole solve of a small level in one cooperative launch (kernels_jcg_persistent.cu)
+cudaError_t launch_persistent(ecmg_grid* G, const LevelGeom& g) {
+  const ConstStencil cs = make_const_stencil(g, 1.0, G->precond);
+  // w = A p (and on the element path D^-1) in scratch vectors sized for the level (grown on demand)
+  const long long need = g.S * g.nza + 64;
+  if (G->aux_doubles < need) {
+    cudaFree(G->aux[0]);
+    cudaFree(G->aux[1]);
+    G->aux[0] = G->aux[1] = nullptr;
+    G->aux_doubles = 0;
+    cudaError_t e = cudaMalloc(&G->aux[0], sizeof(double) * need);
+    if (e == cudaSuccess) e = cudaMalloc(&G->aux[1], sizeof(double) * need);
+    if (e != cudaSuccess) return e;
+    G->aux_doubles = need;
+  }
+  if (!G->elem_path)
+    return launch_jcg_persistent(g, cs, nullptr, G->x, G->r, nullptr, G->p[0], G->p[1], G->aux[0], nullptr, nullptr, G->b,
+                                 G->partials, G->sc, G->stream);
+  const ElemStencil es = make_elem_stencil(g, G->prob, G->precond);
+  return launch_jcg_persistent(g, cs, &es, G->x, G->r, G->zv, G->p[0], G->p[1], G->aux[0], G->aux[1], G->beta, G->b,
+                               G->partials, G->sc, G->stream);
+}
+
+// small levels: the whole solve in one cooperative launch (latency bound)
 int run_jcg_persistent(ecmg_grid* G, int k, double eps, ecmg_stats* st) {
   const LevelGeom& g = G->geom[k];
-  const ConstStencil cs = make_const_stencil(g, 1.0, G->precond);
   ECMG_CUDA(cudaEventRecord(G->ev[0], G->stream));
-  ECMG_CUDA(launch_jcg_persistent(g, cs, G->x, G->r, G->p[0], G->p[1], G->b, G->partials, G->sc, G->stream));
+  ECMG_CUDA(launch_persistent(G, g));
   ECMG_CUDA(cudaEventRecord(G->ev[1], G->stream));
   ECMG_CUDA(cudaMemcpyAsync(&G->sc_host[0], G->sc, sizeof(JcgScalars), cudaMemcpyDeviceToHost, G->stream));
   ECMG_CUDA(cudaStreamSynchronize(G->stream));
@@ -314,14 +342,13 @@ int run_jcg_persistent(ecmg_grid* G, int k, double eps, ecmg_stats* st) {
 // the level needs the host loop (ablation path).
 int enqueue_jcg(ecmg_grid* G, int k, double eps, int max_iter, ParamHost* param, JcgScalars* slot) {
   const LevelGeom& g = G->geom[k];
-  const bool persistent = !G->elem_path && G->persistent_max > 0 && free_count(g) <= G->persistent_max;
+  const bool persistent = use_persistent(G, g);
   if (!(eps > 0.0) || (!persistent && !G->use_graph)) return ECMG_EINVAL;
   param->eps = eps;
   param->max_iter = max_iter;
   ECMG_CUDA(cudaMemcpyAsync(&G->sc->eps_in, param, sizeof(double) + sizeof(int), cudaMemcpyHostToDevice, G->stream));
   if (persistent) {
-    ECMG_CUDA(launch_jcg_persistent(g, make_const_stencil(g, 1.0, G->precond), G->x, G->r, G->p[0], G->p[1], G->b,
-                                    G->partials, G->sc, G->stream));
+    ECMG_CUDA(launch_persistent(G, g));
   } else {
     if ((int)G->graphs.size() != G->L) G->graphs.assign(G->L, nullptr);
     if (!G->graphs[k]) ECMG_CUDA(build_level_graph(G, k, &G->graphs[k]));
@@ -345,8 +372,7 @@ int run_jcg(ecmg_grid* G, int k, double eps, int max_iter, ecmg_stats* st) {
   G->param_host->eps = eps;
   G->param_host->max_iter = max_iter;
   ECMG_CUDA(cudaMemcpyAsync(&G->sc->eps_in, G->param_host, sizeof(double) + sizeof(int), cudaMemcpyHostToDevice, G->stream));
-  if (!G->elem_path && G->persistent_max > 0 && free_count(g) <= G->persistent_max)
-    return run_jcg_persistent(G, k, eps, st);
+  if (use_persistent(G, g)) return run_jcg_persistent(G, k, eps, st);
   if (eps > 0.0 && G->use_graph) return run_jcg_graph(G, k, eps, st);
   // r = b - A x, rho = r.z, rr = r.r, stop test
   {
@@ -541,7 +567,7 @@ int ecmg_destroy_grid(ecmg_grid* G) {
   if (G->stream) cudaStreamSynchronize(G->stream); else cudaDeviceSynchronize();
   if (G->slab) slab_driver_destroy(G->slab);
   cudaFree(G->x); cudaFree(G->r); cudaFree(G->p[0]); cudaFree(G->p[1]); cudaFree(G->b);
-  cudaFree(G->beta); cudaFree(G->zv); cudaFree(G->partials); cudaFree(G->sc);
+  cudaFree(G->beta); cudaFree(G->zv); cudaFree(G->aux[0]); cudaFree(G->aux[1]); cudaFree(G->partials); cudaFree(G->sc);
   for (double* p : G->u) cudaFree(p);
   cudaFree(G->ut_tmp);
   cudaFree(G->scratch1d);

@@ -126,7 +126,8 @@ int make_vec_tensor_map(CUtensorMap* map, const double* base, const LevelGeom& g
 cudaError_t launch_finalize(int mode, const KArgs& a, cudaStream_t st);
 struct SlabScalars { JcgScalars* p[16]; int n; };
 cudaError_t launch_vsum(const SlabScalars& s, cudaStream_t st);
-cudaError_t launch_jcg_persistent(const LevelGeom& g, const ConstStencil& cs, double* x, double* r, double* p, double* w,
+cudaError_t launch_jcg_persistent(const LevelGeom& g, const ConstStencil& cs, const ElemStencil* es, double* x, double* r,
+                                  double* z, double* p0, double* p1, double* w, double* dinv, const double* beta,
                                   const double* b, double* partials, JcgScalars* sc, cudaStream_t st);
 cudaError_t init_tma_kernel_attributes();
 cudaError_t init_elem_kernel_attributes();

@@ -129,21 +129,6 @@ __global__ void k_rhs_sep(const LevelGeom g, const Problem pb, const double* __r
 // f specialised per problem at compile time (PID = 0: generic registry switch)
 template <int PID>
 __device__ __forceinline__ double f_at(const Problem& pb, double x, double y, double z) {
-  if (PID == 4) {   // C4: -(15/4) r^{-1/2} = -(15/4) (r^2)^{-1/4}
-    const double r2 = x * x + y * y + z * z;
-    if (r2 == 0.0) return 0.0;
-    if (r2 < 1e-30) return -3.75 * rsqrt(sqrt(r2));   // below the fp32 seed's range
-    // y = (r^2)^{-1/4}: fp32 seed (rel. error ~1e-7) + two fp64 Newton steps for y^-4 = r^2,
-    // y <- y (5 - r^2 y^4) / 4 (quadratic: 1e-7 -> 1e-14 -> rounding level); avoids the fp64
-    // MUFU sqrt / rsqrt sequences that bound this kernel
-    const float r2f = (float)r2;
-    double yv = (double)rsqrtf(sqrtf(r2f));
-    double y2 = yv * yv;
-    yv = yv * __fma_rn(-r2, y2 * y2, 5.0) * 0.25;
-    y2 = yv * yv;
-    yv = yv * __fma_rn(-r2, y2 * y2, 5.0) * 0.25;
-    return -3.75 * yv;
-  }
   return prob_f(pb, x, y, z);
 }
 
@@ -208,6 +193,86 @@ __global__ void __launch_bounds__(VNTH, 3) k_rhs_vol(const LevelGeom g, const Pr
       }
       b[(long long)fz * g.S + (long long)fy * g.P + fx] = v;
     }
+  }
+}
+
+// (r^2)^{-1/4} to fp64 accuracy: fp32 MUFU seed (rsqrt.approx, sqrt.approx: relative error ~3e-7),
+// then two Newton steps of y <- y (5 - r^2 y^4) / 4 (error e -> -5/2 e^2: 3e-7 -> 2e-13 -> rounding)
+__device__ __forceinline__ double rpow_m14(double r2) {
+  if (!(r2 >= 1e-30 && r2 <= 1e30)) return r2 == 0.0 ? 0.0 : rsqrt(sqrt(r2));   // outside the seed's range
+  float s;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"((float)r2));
+  asm("sqrt.approx.ftz.f32 %0, %0;" : "+f"(s));
+  double y = (double)s;
+  double y2 = y * y;
+  y = y * __fma_rn(-r2, y2 * y2, 5.0) * 0.25;
+  y2 = y * y;
+  y = y * __fma_rn(-r2, y2 * y2, 5.0) * 0.25;
+  return y;
+}
+
+// C4 volume load (f = -(15/4) r^{-1/2}, the corner singularity of u = r^{3/2}): element tile 32 x 8 =
+// one element per thread (node tile 31 x 7), z-marching over element layers. r^2 at a Gauss point is
+// (x^2 + y^2) + z^2 with the four in-plane sums fixed per thread and z^2 per layer, so a Gauss point
+// costs one add and the (r^2)^{-1/4} evaluation; the element vector F_e[a] = detJ sum_q f_q N_a(q) is
+// the same 2x2x2 tensor transform as k_rhs_vol. Per layer the z = 0 corners complete node plane fez
+// (with the z = 1 corners of the layer below carried in a register) through two shared-memory planes.
+__global__ void __launch_bounds__(VNTH, 3) k_rhs_c4(const LevelGeom g, double* __restrict__ b, int zc) {
+  __shared__ double F0[4][VEY][VEX];   // layer corner entries a = 0..3 (z = 0: node plane fez)
+  __shared__ double F1[4][VEY][VEX];   // a = 4..7 (z = 1: node plane fez + 1)
+  const int lane = threadIdx.x, w = threadIdx.y;
+  const int X0 = blockIdx.x * VX, Y0 = blockIdx.y * VY;
+  const int z0 = g.zbeg + blockIdx.z * zc, z1 = min(z0 + zc, g.zend);   // local planes
+  const int gex = g.flo[0] + X0 - 1 + lane, gey = g.flo[1] + Y0 - 1 + w;
+  const bool xy_in = gex >= 0 && gex < g.n[0] && gey >= 0 && gey < g.n[1];
+  const double ga = (1.0 - kGauss) / 2.0, gb = (1.0 + kGauss) / 2.0;   // Gauss points at xi = -+1/sqrt(3)
+  const double xa = g.lo[0] + (gex + ga) * g.h[0], xb = g.lo[0] + (gex + gb) * g.h[0];
+  const double ya = g.lo[1] + (gey + ga) * g.h[1], yb = g.lo[1] + (gey + gb) * g.h[1];
+  const double sxy[4] = {xa * xa + ya * ya, xb * xb + ya * ya, xa * xa + yb * yb, xb * xb + yb * yb};   // q bits x, y
+  const double detJ = -3.75 * (g.h[0] * g.h[1] * g.h[2] / 8.0);
+  const double wA = (1.0 + kGauss) / 2.0, wB = (1.0 - kGauss) / 2.0;   // N at the near / far Gauss point
+  const int fx = X0 + lane, fy = Y0 + w;
+  const bool node_ok = lane < VX && w < VY && fx < g.nf[0] && fy < g.nf[1];
+  double carry = 0.0;
+  for (int fez = z0 - 1; fez < z1; ++fez) {
+    const int gez = g.flo[2] + g.zoff + fez;
+    double F[8];
+    if (xy_in && gez >= 0 && gez < g.n[2]) {
+      const double za = g.lo[2] + (gez + ga) * g.h[2], zb = g.lo[2] + (gez + gb) * g.h[2];
+      const double z2[2] = {za * za, zb * zb};
+      double f[8], t1[8], t2[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) f[q] = rpow_m14(sxy[q & 3] + z2[q >> 2]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {   // along x: node bit 0 vs Gauss bit 0
+        const int qb = i & ~1;
+        t1[i] = (i & 1) ? (wB * f[qb] + wA * f[qb | 1]) : (wA * f[qb] + wB * f[qb | 1]);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {   // along y
+        const int qb = i & ~2;
+        t2[i] = (i & 2) ? (wB * t1[qb] + wA * t1[qb | 2]) : (wA * t1[qb] + wB * t1[qb | 2]);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {   // along z
+        const int qb = i & ~4;
+        F[i] = detJ * ((i & 4) ? (wB * t2[qb] + wA * t2[qb | 4]) : (wA * t2[qb] + wB * t2[qb | 4]));
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) F[i] = 0.0;
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) { F0[a][w][lane] = F[a]; F1[a][w][lane] = F[a + 4]; }
+    __syncthreads();
+    if (node_ok) {
+      // node (fx, fy) is corner (1 - ex, 1 - ey) of the elements at tile (lane + ex, w + ey)
+      const double v0 = (F0[3][w][lane] + F0[2][w][lane + 1]) + (F0[1][w + 1][lane] + F0[0][w + 1][lane + 1]);
+      const double v1 = (F1[3][w][lane] + F1[2][w][lane + 1]) + (F1[1][w + 1][lane] + F1[0][w + 1][lane + 1]);
+      if (fez >= z0) b[(long long)fez * g.S + (long long)fy * g.P + fx] = carry + v0;
+      carry = v1;
+    }
+    __syncthreads();
   }
 }
 
@@ -345,7 +410,6 @@ cudaError_t launch_beta(const LevelGeom& g, const Problem& pb, double* beta, cud
 
 cudaError_t init_setup_kernel_attributes() {
   cudaError_t e = cudaFuncSetAttribute(k_rhs_vol<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, VSMEM);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_rhs_vol<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, VSMEM);
   return e;
 }
 
@@ -364,7 +428,7 @@ cudaError_t launch_rhs(const LevelGeom& g, const Problem& pb, const ElemStencil&
     const int zc = 32;
     dim3 grid((g.nf[0] + VX - 1) / VX, (g.nf[1] + VY - 1) / VY, (g.zend - g.zbeg + zc - 1) / zc);
     count_launch();
-    if (pb.id == 4) k_rhs_vol<4><<<grid, dim3(32, 8), VSMEM, st>>>(g, pb, b, zc);
+    if (pb.id == 4) k_rhs_c4<<<grid, dim3(32, 8), 0, st>>>(g, b, zc);
     else k_rhs_vol<0><<<grid, dim3(32, 8), VSMEM, st>>>(g, pb, b, zc);
   }
   const int m = std::max(g.nf[0], std::max(g.nf[1], g.nf[2]));

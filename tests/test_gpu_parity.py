@@ -262,13 +262,15 @@ def test_graph_loop_equals_host_loop(pid, eps):
     assert np.array_equal(res[0][1], res[1][1]) and np.array_equal(res[0][2], res[1][2])
 
 
-@pytest.mark.parametrize("pid,eps", [(o.C1, 1e-8), (o.C2, 1e-10), (o.C4, 1e-9)])
+@pytest.mark.parametrize("pid,eps", [(o.C1, 1e-8), (o.C2, 1e-10), (o.C4, 1e-9), (o.C3, 1e-10), (o.C5, 1e-8),
+                                     (o.P1, 1e-9)])
 def test_persistent_small_levels_vs_graph(pid, eps):
-    # small constant-stencil levels run in one cooperative launch (ECMG_OPT_PERSISTENT); the
-    # z-marching graph path is the reference: same counts (+-1), iterates within rounding
+    # small levels run in one cooperative launch (ECMG_OPT_PERSISTENT; constant stencil and element
+    # beta + Robin / Neumann faces); the z-marching graph path is the reference: same counts (+-1),
+    # iterates within rounding
     res = []
     for pmax in (300000, 0):
-        g = Grid(4, 5, pid)
+        g = Grid(4, 5, pid, params_for(pid))
         g.set_option(ecmg.OPT_PERSISTENT, pmax)
         u = g.new_vec(4)
         st, stats = g.run(eps, u)
