@@ -104,8 +104,9 @@ typedef enum {
                                 0 register-prefetch loads (ablation) */
   ECMG_OPT_GRAPH = 5,        /* tolerance-stopped JCG loop: 1 (default) one CUDA graph per level with a
                                 device-set conditional WHILE node; 0 host loop with batched readbacks */
-  ECMG_OPT_PERSISTENT = 7,   /* constant-stencil levels with at most this many free unknowns run the
-                                whole JCG solve in one cooperative launch (default 5000, i.e. up to 16^3; 0 = off) */
+  ECMG_OPT_PERSISTENT = 7,   /* levels with at most this many free unknowns run the whole JCG solve in
+                                one cooperative launch, both operators (default 40000, i.e. up to 32^3
+                                cells; 0 = off; single GPU only) */
   ECMG_OPT_VIRTUAL_SLABS = 6 /* P in 2..16: run the z-slab decomposition with P slabs on this one GPU
                                 (device copies stand in for the NCCL halo messages, an in-order sum
                                 kernel for the allreduce; the multi-GPU test fixture); 0 or 1: off */
