@@ -37,7 +37,7 @@ struct PArgs {
 };
 
 // fixed-tree block sum of 3 values, result in every thread
-__device__ void block_sum3_all(double v[3]) {
+__device__ __forceinline__ void block_sum3_all(double v[3]) {
   __shared__ double red[3 * (PNTH / 32)];
   __shared__ double res[3];
   const int tid = threadIdx.x;
@@ -60,7 +60,7 @@ __device__ void block_sum3_all(double v[3]) {
 
 // grid-wide sum of 3 values: per-CTA partials, barrier, then every CTA reduces all partials in CTA
 // order with the same tree (bitwise identical in every CTA)
-__device__ void grid_sum3(double v[3], double* partials, int& buf, cg::grid_group& grid) {
+__device__ __forceinline__ void grid_sum3(double v[3], double* partials, int& buf, cg::grid_group& grid) {
   block_sum3_all(v);
   double* pb = partials + (size_t)buf * gridDim.x * 3;
   if (threadIdx.x == 0)
@@ -77,38 +77,6 @@ __device__ void grid_sum3(double v[3], double* partials, int& buf, cg::grid_grou
 struct Node {
   int fx, fy, fz, off;
 };
-__device__ __forceinline__ Node node_of(const LevelGeom& g, int i) {
-  const int nx = g.nf[0], nxy = g.nf[0] * g.nf[1];
-  Node n;
-  n.fz = i / nxy;
-  const int rem = i - n.fz * nxy;
-  n.fy = rem / nx;
-  n.fx = rem - n.fy * nx;
-  n.off = n.fz * (int)g.S + n.fy * (int)g.P + n.fx;
-  return n;
-}
-
-// the 27 values of v (or of p_new = zsrc + bcg p_old when FORM) around a node; 0 outside the free box
-template <bool FORM>
-__device__ __forceinline__ void gather27(const LevelGeom& g, const Node& n, const double* v, const double* pold,
-                                         double scale, double bcg, double p27[3][3][3]) {
-#pragma unroll
-  for (int dz = 0; dz < 3; ++dz)
-#pragma unroll
-    for (int dy = 0; dy < 3; ++dy)
-#pragma unroll
-      for (int dx = 0; dx < 3; ++dx) {
-        const int x = n.fx + dx - 1, y = n.fy + dy - 1, z = n.fz + dz - 1;
-        double val = 0.0;
-        if (x >= 0 && x < g.nf[0] && y >= 0 && y < g.nf[1] && z >= 0 && z < g.nf[2]) {
-          const int o = n.off + (dz - 1) * (int)g.S + (dy - 1) * (int)g.P + (dx - 1);
-          const double zv = FORM ? scale * __ldcg(v + o) : __ldcg(v + o);
-          val = (FORM && bcg != 0.0) ? __fma_rn(bcg, __ldcg(pold + o), zv) : zv;
-        }
-        p27[dz][dy][dx] = val;
-      }
-}
-
 __device__ __forceinline__ double apply_const(const ConstStencil& cs, const double p27[3][3][3]) {
   double acc = 0.0;
 #pragma unroll
@@ -125,19 +93,6 @@ __device__ __forceinline__ double apply_const(const ConstStencil& cs, const doub
   return acc;
 }
 
-// which Robin faces (alpha != 0) the node lies on: bit F
-__device__ __forceinline__ int robin_mask(const LevelGeom& g, const ElemStencil& es, const Node& n) {
-  const int gx = g.flo[0] + n.fx, gy = g.flo[1] + n.fy, gz = g.flo[2] + g.zoff + n.fz;
-  int m = 0;
-  if (gx == 0 && es.robin[0] != 0.0) m |= 1;
-  if (gx == g.n[0] && es.robin[1] != 0.0) m |= 2;
-  if (gy == 0 && es.robin[2] != 0.0) m |= 4;
-  if (gy == g.n[1] && es.robin[3] != 0.0) m |= 8;
-  if (gz == 0 && es.robin[4] != 0.0) m |= 16;
-  if (gz == g.n[2] && es.robin[5] != 0.0) m |= 32;
-  return m;
-}
-
 // betas of the 8 elements around the node (zero ring outside the domain)
 __device__ __forceinline__ void gather_beta(const LevelGeom& g, const Node& n, const double* beta, double b8[2][2][2]) {
   const int gx = g.flo[0] + n.fx, gy = g.flo[1] + n.fy, gz = g.flo[2] + g.zoff + n.fz;
@@ -150,9 +105,40 @@ __device__ __forceinline__ void gather_beta(const LevelGeom& g, const Node& n, c
         b8[ez][ey][ex] = __ldg(beta + (long long)(gz + 1 + ez) * g.BS + (long long)(gy + 1 + ey) * g.BP + (gx + 1 + ex));
 }
 
-// (A p)_i = sum_{e ni i} beta_e sum_{j in e} kappa[pat(i,j)] p_j + Robin face mass
-__device__ double apply_elem(const ElemStencil& es, int rm, const double b8[2][2][2], const double p27[3][3][3]) {
-  double ap = 0.0;
+// value of p27 at offset (o1, o2) along the two tangential axes of a face normal to axis D
+template <int D>
+__device__ __forceinline__ double face_at(const double p27[3][3][3], int o1, int o2) {
+  if (D == 0) return p27[1 + o2][1 + o1][1];   // tangential axes y, z
+  if (D == 1) return p27[1 + o2][1][1 + o1];   // x, z
+  return p27[1][1 + o2][1 + o1];               // x, y
+}
+
+// Robin face mass alpha h1 h2 (m (x) m) on the face normal to axis D through the node: the face
+// elements around it in the two tangential axes, present where the index range of the box domain has
+// them (cm / cp: element on the minus / plus side exists). Adds to (A p) and to the diagonal.
+template <int D>
+__device__ __forceinline__ void robin_face(double rf, const double p27[3][3][3], const double cm[3], const double cp[3],
+                                           double& ap, double& dg) {
+  constexpr int t1 = D == 0 ? 1 : 0, t2 = D == 2 ? 1 : 2;
+  double acc = 0.0, cnt = 0.0;
+#pragma unroll
+  for (int s2 = -1; s2 <= 1; s2 += 2)
+#pragma unroll
+    for (int s1 = -1; s1 <= 1; s1 += 2) {
+      const double chi = (s1 < 0 ? cm[t1] : cp[t1]) * (s2 < 0 ? cm[t2] : cp[t2]);
+      acc += chi * ((1.0 / 9.0) * face_at<D>(p27, 0, 0) + (1.0 / 18.0) * face_at<D>(p27, s1, 0) +
+                    (1.0 / 18.0) * face_at<D>(p27, 0, s2) + (1.0 / 36.0) * face_at<D>(p27, s1, s2));
+      cnt += chi;
+    }
+  ap += rf * acc;
+  dg += rf * cnt * (1.0 / 9.0);
+}
+
+// (A p)_i = sum_{e ni i} beta_e sum_{j in e} kappa[pat(i,j)] p_j + Robin face mass; the
+// Jacobi diagonal kappa_0 sum_e beta_e + Robin diagonal in *diag if asked
+__device__ __forceinline__ double apply_elem(const LevelGeom& g, const ElemStencil& es, const Node& nd,
+                                             const double b8[2][2][2], const double p27[3][3][3], double* diag) {
+  double ap = 0.0, sb = 0.0;
 #pragma unroll
   for (int ez = 0; ez < 2; ++ez)
 #pragma unroll
@@ -170,74 +156,115 @@ __device__ double apply_elem(const ElemStencil& es, int rm, const double b8[2][2
               t = __fma_rn(es.kappa[pat], p27[ez + bz][ey + by][ex + bx], t);
             }
         ap = __fma_rn(b8[ez][ey][ex], t, ap);
+        sb += b8[ez][ey][ex];
       }
-  if (rm) {   // Robin face mass alpha h1 h2 (m (x) m) of the face elements around the node
-    for (int F = 0; F < 6; ++F) {
-      if (!(rm & (1 << F))) continue;
-      const int d = F >> 1;
-      for (int ez = 0; ez < 2; ++ez)
-        for (int ey = 0; ey < 2; ++ey)
-          for (int ex = 0; ex < 2; ++ex) {
-            if (b8[ez][ey][ex] == 0.0) continue;   // element outside the domain
-            const int e3[3] = {ex, ey, ez};
-            for (int bb = 0; bb < 8; ++bb) {
-              const int b3[3] = {bb & 1, (bb >> 1) & 1, (bb >> 2) & 1};
-              if (b3[d] != 1 - e3[d]) continue;   // node of the element face on F
-              int nd = 0;
-              for (int t = 0; t < 3; ++t)
-                if (t != d && b3[t] != 1 - e3[t]) ++nd;
-              const double m2 = nd == 0 ? (1.0 / 9.0) : (nd == 1 ? (1.0 / 18.0) : (1.0 / 36.0));
-              ap += es.robin[F] * m2 * p27[ez + b3[2]][ey + b3[1]][ex + b3[0]];
-            }
-          }
-    }
+  double dg = es.kappa[0] * sb;
+  const int gx = g.flo[0] + nd.fx, gy = g.flo[1] + nd.fy, gz = g.flo[2] + g.zoff + nd.fz;
+  const double rfx = (gx == 0 ? es.robin[0] : 0.0) + (gx == g.n[0] ? es.robin[1] : 0.0);
+  const double rfy = (gy == 0 ? es.robin[2] : 0.0) + (gy == g.n[1] ? es.robin[3] : 0.0);
+  const double rfz = (gz == 0 ? es.robin[4] : 0.0) + (gz == g.n[2] ? es.robin[5] : 0.0);
+  if (rfx != 0.0 || rfy != 0.0 || rfz != 0.0) {
+    const double cm[3] = {gx >= 1 ? 1.0 : 0.0, gy >= 1 ? 1.0 : 0.0, gz >= 1 ? 1.0 : 0.0};
+    const double cp[3] = {gx < g.n[0] ? 1.0 : 0.0, gy < g.n[1] ? 1.0 : 0.0, gz < g.n[2] ? 1.0 : 0.0};
+    if (rfx != 0.0) robin_face<0>(rfx, p27, cm, cp, ap, dg);
+    if (rfy != 0.0) robin_face<1>(rfy, p27, cm, cp, ap, dg);
+    if (rfz != 0.0) robin_face<2>(rfz, p27, cm, cp, ap, dg);
   }
+  if (diag) *diag = dg;
   return ap;
 }
 
-__device__ double diag_elem(const ElemStencil& es, int rm, const double b8[2][2][2]) {
-  double sb = 0.0, rob = 0.0;
-#pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    const double be = b8[e >> 2][(e >> 1) & 1][e & 1];
-    sb += be;
-    if (rm && be != 0.0)
-      for (int F = 0; F < 6; ++F)
-        if (rm & (1 << F)) rob += es.robin[F] * (1.0 / 9.0);
+// Bricks of 8 x 8 x 4 nodes, one node per thread; the brick and its one-node halo (10 x 10 x 6) are staged
+// in shared memory with coalesced L2 loads whenever neighbours' values are needed (L1 is not coherent
+// across SMs, so data written by other CTAs in the previous phase is read with ld.cg). A node is always
+// handled by the same thread, so its own x, r, z, D^-1, p_new, w need no such care.
+constexpr int BX = 8, BY = 8, BZ = 4;
+constexpr int SX = BX + 2, SY = BY + 2, SZ = BZ + 2, SN = SX * SY * SZ;
+
+struct Brick {
+  int X0, Y0, Z0;
+};
+__device__ __forceinline__ Brick brick_of(const LevelGeom& g, int k) {
+  const int nbx = (g.nf[0] + BX - 1) / BX, nby = (g.nf[1] + BY - 1) / BY;
+  Brick br;
+  br.X0 = (k % nbx) * BX;
+  br.Y0 = ((k / nbx) % nby) * BY;
+  br.Z0 = (k / (nbx * nby)) * BZ;
+  return br;
+}
+
+// s[...] = FORM ? zscale * zsrc + bcg * pold : zsrc over the brick and its halo (0 outside the free box)
+template <bool FORM>
+__device__ __forceinline__ void stage(const LevelGeom& g, const Brick& br, const double* zsrc, const double* pold,
+                                      double zscale, double bcg, double* s) {
+  for (int t = threadIdx.x; t < SN; t += PNTH) {
+    const int hx = t % SX, hy = (t / SX) % SY, hz = t / (SX * SY);
+    const int x = br.X0 - 1 + hx, y = br.Y0 - 1 + hy, z = br.Z0 - 1 + hz;
+    double v = 0.0;
+    if (x >= 0 && x < g.nf[0] && y >= 0 && y < g.nf[1] && z >= 0 && z < g.nf[2]) {
+      const int o = z * (int)g.S + y * (int)g.P + x;
+      v = __ldcg(zsrc + o);
+      if (FORM) {
+        v *= zscale;
+        if (bcg != 0.0) v = __fma_rn(bcg, __ldcg(pold + o), v);
+      }
+    }
+    s[t] = v;
   }
-  return es.kappa[0] * sb + rob;
+}
+
+__device__ __forceinline__ void window27(const double* s, int lx, int ly, int lz, double p27[3][3][3]) {
+#pragma unroll
+  for (int dz = 0; dz < 3; ++dz)
+#pragma unroll
+    for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+      for (int dx = 0; dx < 3; ++dx) p27[dz][dy][dx] = s[((lz + dz) * SY + (ly + dy)) * SX + lx + dx];
 }
 
 template <bool ELEM>
-__global__ void __launch_bounds__(PNTH) k_jcg_persistent(const LevelGeom g, const ConstStencil cs, const ElemStencil es,
+__device__ __forceinline__ double apply_node(const LevelGeom& g, const ConstStencil& cs, const ElemStencil& es,
+                                             const double* beta, const Node& nd, const double p27[3][3][3], double* diag) {
+  if (ELEM) {
+    double b8[2][2][2];
+    gather_beta(g, nd, beta, b8);
+    return apply_elem(g, es, nd, b8, p27, diag);
+  }
+  return apply_const(cs, p27);
+}
+
+template <bool ELEM>
+__global__ void __launch_bounds__(PNTH, 2) k_jcg_persistent(const LevelGeom g, const ConstStencil cs, const ElemStencil es,
                                                          const PArgs a) {
+  __shared__ double sp[SN];
   cg::grid_group grid = cg::this_grid();
-  const int n = g.nf[0] * g.nf[1] * g.nf[2];   // small levels only: 32-bit index math
-  const int t0 = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+  const int nbricks = ((g.nf[0] + BX - 1) / BX) * ((g.nf[1] + BY - 1) / BY) * ((g.nf[2] + BZ - 1) / BZ);
+  const int lx = threadIdx.x % BX, ly = (threadIdx.x / BX) % BY, lz = threadIdx.x / (BX * BY);
   const double cdinv = cs.dinv;
   JcgScalars* sc = a.sc;
   const double eps = sc->eps_in;
   const int max_iter = sc->max_iter_in;
+  auto own = [&](const Brick& br, Node& nd) -> bool {
+    nd.fx = br.X0 + lx; nd.fy = br.Y0 + ly; nd.fz = br.Z0 + lz;
+    nd.off = nd.fz * (int)g.S + nd.fy * (int)g.P + nd.fx;
+    return nd.fx < g.nf[0] && nd.fy < g.nf[1] && nd.fz < g.nf[2];
+  };
   int buf = 0;
   // init: D^-1 (element path), r = b - A x, z = D^-1 r, rho = r.z, rr, ||b||^2
   double v[3] = {0.0, 0.0, 0.0};
-  for (int i = t0; i < n; i += stride) {
-    const Node nd = node_of(g, i);
+  for (int k = blockIdx.x; k < nbricks; k += gridDim.x) {
+    const Brick br = brick_of(g, k);
+    __syncthreads();
+    stage<false>(g, br, a.x, nullptr, 1.0, 0.0, sp);
+    __syncthreads();
+    Node nd;
+    if (!own(br, nd)) continue;
     double p27[3][3][3];
-    gather27<false>(g, nd, a.x, nullptr, 1.0, 0.0, p27);
-    double ax, di;
-    if (ELEM) {
-      double b8[2][2][2];
-      gather_beta(g, nd, a.beta, b8);
-      const int rm = robin_mask(g, es, nd);
-      ax = apply_elem(es, rm, b8, p27);
-      const double d = diag_elem(es, rm, b8);
-      di = es.precond ? (d > 0.0 ? 1.0 / d : 0.0) : 1.0;
-      a.dinv[nd.off] = di;
-    } else {
-      ax = apply_const(cs, p27);
-      di = cdinv;
-    }
+    window27(sp, lx, ly, lz, p27);
+    double d = 0.0;
+    const double ax = apply_node<ELEM>(g, cs, es, a.beta, nd, p27, &d);
+    const double di = ELEM ? (es.precond ? (d > 0.0 ? 1.0 / d : 0.0) : 1.0) : cdinv;
+    if (ELEM) a.dinv[nd.off] = di;
     const double bi = a.b[nd.off];
     const double rn = bi - ax;
     const double zz = di * rn;
@@ -258,25 +285,23 @@ __global__ void __launch_bounds__(PNTH) k_jcg_persistent(const LevelGeom g, cons
   if (!isfinite(rr)) { status = ST_EBREAKDOWN; done = true; }
   int cur = 0;   // a.p[cur] holds p_old
   while (!done) {
-    // phase 1: p_new = z + beta p_old around every node, w = A p_new, sigma = p_new . w
+    // phase 1: p_new = z + beta p_old on the brick and its halo, w = A p_new, sigma = p_new . w
     const double* zsrc = ELEM ? a.z : a.r;
     const double zscale = ELEM ? 1.0 : cdinv;
     const double bcg = iter == 0 ? 0.0 : beta;
     double* pnew = a.p[cur ^ 1];
     const double* pold = a.p[cur];
     v[0] = v[1] = v[2] = 0.0;
-    for (int i = t0; i < n; i += stride) {
-      const Node nd = node_of(g, i);
+    for (int k = blockIdx.x; k < nbricks; k += gridDim.x) {
+      const Brick br = brick_of(g, k);
+      __syncthreads();
+      stage<true>(g, br, zsrc, pold, zscale, bcg, sp);
+      __syncthreads();
+      Node nd;
+      if (!own(br, nd)) continue;
       double p27[3][3][3];
-      gather27<true>(g, nd, zsrc, pold, zscale, bcg, p27);
-      double wi;
-      if (ELEM) {
-        double b8[2][2][2];
-        gather_beta(g, nd, a.beta, b8);
-        wi = apply_elem(es, robin_mask(g, es, nd), b8, p27);
-      } else {
-        wi = apply_const(cs, p27);
-      }
+      window27(sp, lx, ly, lz, p27);
+      const double wi = apply_node<ELEM>(g, cs, es, a.beta, nd, p27, nullptr);
       const double pc = p27[1][1][1];
       pnew[nd.off] = pc;
       a.w[nd.off] = wi;
@@ -286,10 +311,11 @@ __global__ void __launch_bounds__(PNTH) k_jcg_persistent(const LevelGeom g, cons
     const double sigma = v[0];
     if (!(sigma > 0.0)) { status = ST_EBREAKDOWN; break; }
     const double alpha = rho / sigma;
-    // phase 2: x += alpha p, r -= alpha w, z = D^-1 r, rho' = r.z, rr = r.r
+    // phase 2 (own nodes only): x += alpha p, r -= alpha w, z = D^-1 r, rho' = r.z, rr = r.r
     v[0] = v[1] = v[2] = 0.0;
-    for (int i = t0; i < n; i += stride) {
-      const Node nd = node_of(g, i);
+    for (int k = blockIdx.x; k < nbricks; k += gridDim.x) {
+      Node nd;
+      if (!own(brick_of(g, k), nd)) continue;
       const int o = nd.off;
       a.x[o] = __fma_rn(alpha, pnew[o], a.x[o]);
       const double rn = __fma_rn(-alpha, a.w[o], a.r[o]);
@@ -310,19 +336,16 @@ __global__ void __launch_bounds__(PNTH) k_jcg_persistent(const LevelGeom g, cons
   }
   // true residual ||b - A x||
   v[0] = v[1] = v[2] = 0.0;
-  for (int i = t0; i < n; i += stride) {
-    const Node nd = node_of(g, i);
+  for (int k = blockIdx.x; k < nbricks; k += gridDim.x) {
+    const Brick br = brick_of(g, k);
+    __syncthreads();
+    stage<false>(g, br, a.x, nullptr, 1.0, 0.0, sp);
+    __syncthreads();
+    Node nd;
+    if (!own(br, nd)) continue;
     double p27[3][3][3];
-    gather27<false>(g, nd, a.x, nullptr, 1.0, 0.0, p27);
-    double ax;
-    if (ELEM) {
-      double b8[2][2][2];
-      gather_beta(g, nd, a.beta, b8);
-      ax = apply_elem(es, robin_mask(g, es, nd), b8, p27);
-    } else {
-      ax = apply_const(cs, p27);
-    }
-    const double rn = a.b[nd.off] - ax;
+    window27(sp, lx, ly, lz, p27);
+    const double rn = a.b[nd.off] - apply_node<ELEM>(g, cs, es, a.beta, nd, p27, nullptr);
     v[1] = __fma_rn(rn, rn, v[1]);
   }
   grid_sum3(v, a.partials, buf, grid);
@@ -352,8 +375,8 @@ int persistent_grid(int want) {
 cudaError_t launch_jcg_persistent(const LevelGeom& g, const ConstStencil& cs, const ElemStencil* es, double* x, double* r,
                                   double* z, double* p0, double* p1, double* w, double* dinv, const double* beta,
                                   const double* b, double* partials, JcgScalars* sc, cudaStream_t st) {
-  const long long n = (long long)g.nf[0] * g.nf[1] * g.nf[2];
-  const int want = (int)std::min<long long>((n + PNTH - 1) / PNTH, 1 << 20);
+  const long long nbricks = (long long)((g.nf[0] + BX - 1) / BX) * ((g.nf[1] + BY - 1) / BY) * ((g.nf[2] + BZ - 1) / BZ);
+  const int want = (int)std::min<long long>(nbricks, 1 << 20);
   PArgs a{x, r, z, {p0, p1}, w, b, dinv, beta, partials, sc};
   const ElemStencil e = es ? *es : ElemStencil{};
   void* args[] = {(void*)&g, (void*)&cs, (void*)&e, (void*)&a};
