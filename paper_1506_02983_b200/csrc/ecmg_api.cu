@@ -25,7 +25,7 @@ using namespace ecmg;
 static std::atomic<long long> g_launches{0};
 namespace ecmg { void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); } }
 
-struct ParamHost { double eps; int max_iter; int pad; };
+using ParamHost = JcgParams;
 
 struct ecmg_grid {
   int device = 0;
@@ -340,13 +340,14 @@ int run_jcg_persistent(ecmg_grid* G, int k, double eps, ecmg_stats* st) {
 // Enqueue a device-driven JCG solve (graph or persistent path) without any host synchronisation;
 // the final scalars land in *slot (pinned) when the stream reaches them. Returns ECMG_EINVAL if
 // the level needs the host loop (ablation path).
-int enqueue_jcg(ecmg_grid* G, int k, double eps, int max_iter, ParamHost* param, JcgScalars* slot) {
+int enqueue_jcg(ecmg_grid* G, int k, double eps, int max_iter, double* u_out, ParamHost* param, JcgScalars* slot) {
   const LevelGeom& g = G->geom[k];
   const bool persistent = use_persistent(G, g);
   if (!(eps > 0.0) || (!persistent && !G->use_graph)) return ECMG_EINVAL;
   param->eps = eps;
   param->max_iter = max_iter;
-  ECMG_CUDA(cudaMemcpyAsync(&G->sc->eps_in, param, sizeof(double) + sizeof(int), cudaMemcpyHostToDevice, G->stream));
+  param->u_out = u_out;
+  ECMG_CUDA(cudaMemcpyAsync(&G->sc->in, param, sizeof(JcgParams), cudaMemcpyHostToDevice, G->stream));
   if (persistent) {
     ECMG_CUDA(launch_persistent(G, g));
   } else {
@@ -358,8 +359,9 @@ int enqueue_jcg(ecmg_grid* G, int k, double eps, int max_iter, ParamHost* param,
   return ECMG_OK;
 }
 
-// JCG on the level whose RHS is in G->b, starting from G->x. Fills stats (except timings).
-int run_jcg(ecmg_grid* G, int k, double eps, int max_iter, ecmg_stats* st) {
+// JCG on the level whose RHS is in G->b, starting from G->x. Fills stats (except timings). The true
+// residual pass writes the solution into the free nodes of the full-layout vector u_out (if not null).
+int run_jcg(ecmg_grid* G, int k, double eps, int max_iter, double* u_out, ecmg_stats* st) {
   const LevelGeom& g = G->geom[k];
   if (max_iter <= 0 && eps > 0) max_iter = 10000;
   if (max_iter < 0) max_iter = 0;
@@ -371,7 +373,8 @@ int run_jcg(ecmg_grid* G, int k, double eps, int max_iter, ecmg_stats* st) {
   // eps and max_iter reach the init pass through the device scalars
   G->param_host->eps = eps;
   G->param_host->max_iter = max_iter;
-  ECMG_CUDA(cudaMemcpyAsync(&G->sc->eps_in, G->param_host, sizeof(double) + sizeof(int), cudaMemcpyHostToDevice, G->stream));
+  G->param_host->u_out = u_out;
+  ECMG_CUDA(cudaMemcpyAsync(&G->sc->in, G->param_host, sizeof(JcgParams), cudaMemcpyHostToDevice, G->stream));
   if (use_persistent(G, g)) return run_jcg_persistent(G, k, eps, st);
   if (eps > 0.0 && G->use_graph) return run_jcg_graph(G, k, eps, st);
   // r = b - A x, rho = r.z, rr = r.r, stop test
@@ -678,9 +681,8 @@ int ecmg_solve_level(ecmg_grid* G, int level, double eps, int max_iter, double* 
   if (G->setup_level != level) { int s = setup_level(G, level); if (s) return s; }
   ECMG_CUDA(cudaEventRecord(G->ev[5], G->stream));
   ECMG_CUDA(launch_gather(g, u, G->x, G->stream));
-  const int st = run_jcg(G, level, eps, max_iter, stats);
+  const int st = run_jcg(G, level, eps, max_iter, u, stats);   // the true-residual pass fills u's free nodes
   if (st == ECMG_ECUDA || st == ECMG_ENOMEM) return st;
-  ECMG_CUDA(launch_scatter(g, G->x, u, G->stream));
   ECMG_CUDA(launch_dirichlet_fill(g, G->prob, u, 0.0, 0, G->stream));
   ECMG_CUDA(cudaEventRecord(G->ev[6], G->stream));
   ECMG_CUDA(cudaStreamSynchronize(G->stream));
@@ -736,7 +738,7 @@ int ecmg_level_rhs(ecmg_grid* G, int level, double* bout, double* norm_b) {
   {
     KArgs a{};
     a.partials = G->partials; a.sc = G->sc; a.zc = auto_zc(G->zchunk, G->elem_path, g); a.beta = G->beta;
-    a.h0 = G->x; a.i0 = G->b; a.o0 = G->r; a.o1 = G->zv; a.eps = 0.0; a.max_iter = 0;
+    a.h0 = G->x; a.i0 = G->b; a.o0 = G->r; a.o1 = G->zv;
     ECMG_CUDA(launch_mode(G, MODE_INIT, g, a));
   }
   ECMG_CUDA(cudaMemcpyAsync(&G->sc_host[0], G->sc, sizeof(JcgScalars), cudaMemcpyDeviceToHost, G->stream));
@@ -797,26 +799,28 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
     ECMG_CUDA(cudaEventRecord(e[2], G->stream));
     const double eps_k = k < 2 ? 1e-14 : eps_lv[k];   // JCG from W_h (l.7-9)
     const int maxit_k = k < 2 ? 10000 : maxit_lv[k];
-    int s = enqueue_jcg(G, k, eps_k, maxit_k, &G->lvl_param[k], &G->lvl_sc[k]);
+    // u_k: the finest level goes straight into the caller's device buffer (no copy at the end); the
+    // true-residual pass of the solve writes its free nodes (fused scatter)
+    double* uk = (k == G->L - 1 && u_dev) ? u_fine : G->u[k];
+    int s = enqueue_jcg(G, k, eps_k, maxit_k, uk, &G->lvl_param[k], &G->lvl_sc[k]);
     if (s == ECMG_OK) {
       async[k] = 1;
     } else if (s == ECMG_EINVAL) {
-      s = run_jcg(G, k, eps_k, maxit_k, &st);   // host loop (ablation path / fixed counts)
+      s = run_jcg(G, k, eps_k, maxit_k, uk, &st);   // host loop (ablation path / fixed counts)
       if (k < 2 && s == ECMG_ENOTCONV) s = ECMG_OK;
       if (s != ECMG_OK && status == ECMG_OK) status = s;
     }
     if (s == ECMG_ECUDA || s == ECMG_ENOMEM) return s;
-    ECMG_CUDA(launch_scatter(g, G->x, G->u[k], G->stream));
-    ECMG_CUDA(launch_dirichlet_fill(g, G->prob, G->u[k], 0.0, 0, G->stream));
+    ECMG_CUDA(launch_dirichlet_fill(g, G->prob, uk, 0.0, 0, G->stream));
     ECMG_CUDA(cudaEventRecord(e[3], G->stream));
     if (k >= 2 && k == G->L - 1 && ut_fine) {
       // u~_h = EXP_true(u_h, u_2h) (Alg. 4 l.10) on the finest level
-      ECMG_CUDA(launch_exp_true(g, G->prob, G->u[k], G->u[k - 1], ut_dev ? ut_fine : G->ut_tmp, G->stream));
+      ECMG_CUDA(launch_exp_true(g, G->prob, uk, G->u[k - 1], ut_dev ? ut_fine : G->ut_tmp, G->stream));
     }
     ECMG_CUDA(cudaEventRecord(e[4], G->stream));
   }
-  ECMG_CUDA(cudaMemcpyAsync(u_fine, G->u[G->L - 1], sizeof(double) * Nf,
-                            u_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, G->stream));
+  if (!u_dev)
+    ECMG_CUDA(cudaMemcpyAsync(u_fine, G->u[G->L - 1], sizeof(double) * Nf, cudaMemcpyDeviceToHost, G->stream));
   if (ut_fine && !ut_dev)
     ECMG_CUDA(cudaMemcpyAsync(ut_fine, G->ut_tmp, sizeof(double) * Nf, cudaMemcpyDeviceToHost, G->stream));
   ECMG_CUDA(cudaStreamSynchronize(G->stream));

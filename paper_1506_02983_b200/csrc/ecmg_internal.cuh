@@ -65,6 +65,15 @@ struct ElemStencil {
   int cube;            // h_x = h_y = h_z: kappa = c{4,0,0,-1,0,-1,-1,-1} (the element kernel's short form)
 };
 
+// Per-solve inputs, written by one host-to-device copy before the init pass (pinned host copy).
+struct JcgParams {
+  double eps;        // requested eps (<= 0: exactly max_iter iterations)
+  double* u_out;     // single GPU: full-layout nodal vector whose free nodes the true-residual pass
+                     // fills with the solution (fused scatter); nullptr: no write
+  int max_iter;      // requested max_iter
+  int pad_;
+};
+
 // Device-resident CG scalars (no host round trip inside the iteration).
 struct JcgScalars {
   double rho;        // r.z
@@ -73,8 +82,7 @@ struct JcgScalars {
   double bb;         // ||b||^2 (set by the RHS kernel)
   double rr_true;    // ||b - A x||^2 (set by the true-residual pass)
   double thresh;     // eps * ||b|| (or eps if ||b|| = 0); <= 0: fixed-iteration mode
-  double eps_in;     // requested eps (written by the host before the init pass)
-  int max_iter_in;   // requested max_iter (idem)
+  JcgParams in;      // eps, max_iter, u_out of the current solve (written by the host before the init pass)
   int iter, max_iter, done, status;
   unsigned int counter;   // last-block-done counter (reset by the last block)
   int pad_;
@@ -83,6 +91,12 @@ struct JcgScalars {
 };
 
 enum KMode { MODE_K1 = 1, MODE_K2 = 2, MODE_INIT = 3, MODE_TRUE = 4, MODE_APPLY = 5 };
+
+// index of free node (fx, fy, local plane fz) in the caller-visible full-layout vector (single GPU)
+__host__ __device__ inline long long full_index(const LevelGeom& g, int fx, int fy, int fz) {
+  const long long nx = g.n[0] + 1, ny = g.n[1] + 1;
+  return (long long)(g.flo[2] + g.zoff + fz) * nx * ny + (long long)(g.flo[1] + fy) * nx + (g.flo[0] + fx);
+}
 
 struct KArgs {
   const double* h0;   // halo-read vector (K1: r (element path: z), K2: p, INIT/TRUE: x, APPLY: p)
@@ -96,8 +110,6 @@ struct KArgs {
   double* partials;   // per-block partial dot products (2 per block)
   JcgScalars* sc;
   int zc;             // planes per CTA
-  double eps;         // unused (eps / max_iter are read from JcgScalars::eps_in / max_iter_in)
-  int max_iter;
   cudaGraphConditionalHandle cond;   // CUDA-graph WHILE condition (device-driven JCG loop)
   int use_cond;                      // 1: the init / K2 passes set `cond` = !done
   int local_only;                    // z-slabs: write this slab's sums to sc->loc, finalize later

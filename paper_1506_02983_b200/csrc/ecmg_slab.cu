@@ -104,7 +104,7 @@ struct SlabDriver {
   std::vector<SlabCtx> s;    // local slabs: all P (virtual) or this rank's one (NCCL)
   ncclComm_t comm = nullptr;
   JcgScalars* sc_host = nullptr;
-  struct ParamHost { double eps; int max_iter; int pad; }* param_host = nullptr;
+  JcgParams* param_host = nullptr;   // u_out stays null: slabs scatter separately
   cudaEvent_t ev[4];
   SlabCfg cfg{};
   int L = 0;
@@ -297,8 +297,9 @@ int slab_jcg(SlabDriver* d, int k, double eps, int max_iter, ecmg_stats* st, cud
   const int nloc = (sh || !d->virt) ? (int)d->s.size() : 1;
   d->param_host->eps = eps;
   d->param_host->max_iter = max_iter;
+  d->param_host->u_out = nullptr;
   for (int i = 0; i < nloc; ++i)
-    SL_CUDA(cudaMemcpyAsync(&d->s[i].sc->eps_in, d->param_host, sizeof(double) + sizeof(int), cudaMemcpyHostToDevice, stream));
+    SL_CUDA(cudaMemcpyAsync(&d->s[i].sc->in, d->param_host, sizeof(JcgParams), cudaMemcpyHostToDevice, stream));
   // one pass of `mode` over all local slabs (+ allreduce and finalize when sharded)
   auto pass = [&](int mode, auto fill) -> int {
     for (int i = 0; i < nloc; ++i) {

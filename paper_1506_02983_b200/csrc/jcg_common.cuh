@@ -49,8 +49,8 @@ __device__ void finalize(int mode, const KArgs& a, double s0, double s1, double 
     case MODE_INIT: {
       sc->bb = s2;   // ||b||^2 of the lifted right-hand side (read by this pass anyway)
       sc->rho = s0; sc->rr = s1; sc->alpha = 0.0; sc->beta = 0.0; sc->sigma = 0.0;
-      const double eps = sc->eps_in;
-      const int max_iter = sc->max_iter_in;
+      const double eps = sc->in.eps;
+      const int max_iter = sc->in.max_iter;
       sc->iter = 0; sc->status = ST_OK; sc->max_iter = max_iter;
       const double nb = sqrt(sc->bb);
       const double nbe = nb > 0.0 ? nb : 1.0;             // ||f|| = 0: absolute residual (§8c A11)

@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(NTH, 2) k_jcg_const(const LevelGeom g, const C
   bool first = false;
   if (MODE == MODE_K1) { bcg = sc->beta; first = (sc->iter == 0); }
   if (MODE == MODE_K2) alpha = sc->alpha;
+  double* const u_out = (MODE == MODE_TRUE) ? sc->in.u_out : nullptr;
   const double dinv = cs.dinv;
   constexpr bool kTwoHalo = (MODE == MODE_K1);
   constexpr bool kInt0 = (MODE == MODE_K2 || MODE == MODE_INIT || MODE == MODE_TRUE);
@@ -166,6 +167,7 @@ __global__ void __launch_bounds__(NTH, 2) k_jcg_const(const LevelGeom g, const C
         } else if (MODE == MODE_TRUE) {
           const double rn = ii0[j] - ap;
           acc1 = __fma_rn(rn, rn, acc1);
+          if (u_out) u_out[full_index(g, x, yb + j, z)] = pp[j];   // fused scatter of u_h
         } else {
           a.o0[off] = ap;
         }

@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(NTH, ELEM_MINB)
   bool first = false;
   if (MODE == MODE_K1) { bcg = sc->beta; first = (sc->iter == 0); }
   if (MODE == MODE_K2) alpha = sc->alpha;
+  double* const u_out = (MODE == MODE_TRUE) ? sc->in.u_out : nullptr;
   // iteration 0 of K1 (p = z): the p_old slot is filled from z and beta_cg = 0 (exact for finite z), so
   // the window update is one FMA with no per-element select
   const double bcg_eff = first ? 0.0 : bcg;
@@ -346,6 +347,7 @@ __global__ void __launch_bounds__(NTH, ELEM_MINB)
         } else if (MODE == MODE_TRUE) {
           const double rn = I0[io] - ap;
           acc1 = __fma_rn(rn, rn, acc1);
+          if (u_out) u_out[full_index(g, x, yb + j, d)] = pc;   // fused scatter of u_h
         } else {
           a.o0[off] = ap;
         }

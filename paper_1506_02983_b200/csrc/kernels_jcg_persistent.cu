@@ -242,8 +242,9 @@ __global__ void __launch_bounds__(PNTH, 2) k_jcg_persistent(const LevelGeom g, c
   const int lx = threadIdx.x % BX, ly = (threadIdx.x / BX) % BY, lz = threadIdx.x / (BX * BY);
   const double cdinv = cs.dinv;
   JcgScalars* sc = a.sc;
-  const double eps = sc->eps_in;
-  const int max_iter = sc->max_iter_in;
+  const double eps = sc->in.eps;
+  const int max_iter = sc->in.max_iter;
+  double* const u_out = sc->in.u_out;
   auto own = [&](const Brick& br, Node& nd) -> bool {
     nd.fx = br.X0 + lx; nd.fy = br.Y0 + ly; nd.fz = br.Z0 + lz;
     nd.off = nd.fz * (int)g.S + nd.fy * (int)g.P + nd.fx;
@@ -347,6 +348,7 @@ __global__ void __launch_bounds__(PNTH, 2) k_jcg_persistent(const LevelGeom g, c
     window27(sp, lx, ly, lz, p27);
     const double rn = a.b[nd.off] - apply_node<ELEM>(g, cs, es, a.beta, nd, p27, nullptr);
     v[1] = __fma_rn(rn, rn, v[1]);
+    if (u_out) u_out[full_index(g, nd.fx, nd.fy, nd.fz)] = p27[1][1][1];   // fused scatter of u_h
   }
   grid_sum3(v, a.partials, buf, grid);
   if (blockIdx.x == 0 && threadIdx.x == 0) {

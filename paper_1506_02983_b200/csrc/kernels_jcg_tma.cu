@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(NTH, 2)
   bool first = false;
   if (MODE == MODE_K1) { bcg = sc->beta; first = (sc->iter == 0); }
   if (MODE == MODE_K2) alpha = sc->alpha;
+  double* const u_out = (MODE == MODE_TRUE) ? sc->in.u_out : nullptr;
   const double dinv = cs.dinv;
   const uint32_t tx_bytes = HBYTES + ((kH1 && !first) ? HBYTES : 0) + IBYTES * kNI;
 
@@ -207,6 +208,7 @@ __global__ void __launch_bounds__(NTH, 2)
         } else if (MODE == MODE_TRUE) {
           const double rn = I0[io] - ap;
           acc1 = __fma_rn(rn, rn, acc1);
+          if (u_out) u_out[full_index(g, x, yb + j, z)] = pp[j];   // fused scatter of u_h
         } else {
           a.o0[off] = ap;
         }

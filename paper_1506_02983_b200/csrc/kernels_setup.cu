@@ -196,19 +196,20 @@ __global__ void __launch_bounds__(VNTH, 3) k_rhs_vol(const LevelGeom g, const Pr
   }
 }
 
-// (r^2)^{-1/4} to fp64 accuracy: fp32 MUFU seed (rsqrt.approx, sqrt.approx: relative error ~3e-7),
-// then two Newton steps of y <- y (5 - r^2 y^4) / 4 (error e -> -5/2 e^2: 3e-7 -> 2e-13 -> rounding)
+// (r^2)^{-1/4} to fp64 accuracy: fp32 MUFU seed (rsqrt.approx, sqrt.approx: relative error ~3e-7) and
+// one fp32 Newton step (to ~1e-7, the fp32 rounding level) on the fp32 pipe, then one fp64 Newton step of
+// y <- y (5 - r^2 y^4) / 4 (error e -> -5/2 e^2: ~1e-7 -> ~3e-14)
 __device__ __forceinline__ double rpow_m14(double r2) {
   if (!(r2 >= 1e-30 && r2 <= 1e30)) return r2 == 0.0 ? 0.0 : rsqrt(sqrt(r2));   // outside the seed's range
+  const float rf = (float)r2;
   float s;
-  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"((float)r2));
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"(rf));
   asm("sqrt.approx.ftz.f32 %0, %0;" : "+f"(s));
+  float s2 = s * s;
+  s = s * fmaf(-rf, s2 * s2, 5.0f) * 0.25f;
   double y = (double)s;
-  double y2 = y * y;
-  y = y * __fma_rn(-r2, y2 * y2, 5.0) * 0.25;
-  y2 = y * y;
-  y = y * __fma_rn(-r2, y2 * y2, 5.0) * 0.25;
-  return y;
+  const double y2 = y * y;
+  return y * __fma_rn(-r2, y2 * y2, 5.0) * 0.25;
 }
 
 // C4 volume load (f = -(15/4) r^{-1/2}, the corner singularity of u = r^{3/2}): element tile 32 x 8 =
@@ -231,6 +232,7 @@ __global__ void __launch_bounds__(VNTH, 3) k_rhs_c4(const LevelGeom g, double* _
   const double sxy[4] = {xa * xa + ya * ya, xb * xb + ya * ya, xa * xa + yb * yb, xb * xb + yb * yb};   // q bits x, y
   const double detJ = -3.75 * (g.h[0] * g.h[1] * g.h[2] / 8.0);
   const double wA = (1.0 + kGauss) / 2.0, wB = (1.0 - kGauss) / 2.0;   // N at the near / far Gauss point
+  const double dA = detJ * wA, dB = detJ * wB;
   const int fx = X0 + lane, fy = Y0 + w;
   const bool node_ok = lane < VX && w < VY && fx < g.nf[0] && fy < g.nf[1];
   double carry = 0.0;
@@ -254,9 +256,9 @@ __global__ void __launch_bounds__(VNTH, 3) k_rhs_c4(const LevelGeom g, double* _
         t2[i] = (i & 2) ? (wB * t1[qb] + wA * t1[qb | 2]) : (wA * t1[qb] + wB * t1[qb | 2]);
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {   // along z
+      for (int i = 0; i < 8; ++i) {   // along z, with detJ folded into the weights
         const int qb = i & ~4;
-        F[i] = detJ * ((i & 4) ? (wB * t2[qb] + wA * t2[qb | 4]) : (wA * t2[qb] + wB * t2[qb | 4]));
+        F[i] = (i & 4) ? (dB * t2[qb] + dA * t2[qb | 4]) : (dA * t2[qb] + dB * t2[qb | 4]);
       }
     } else {
 #pragma unroll
