@@ -272,7 +272,7 @@ def main():
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "jcg_traffic.json")) as f:
-            traffic = json.load(f).get("bytes_per_iteration_k1_k2")
+            traffic = json.load(f)[args.config]["bytes_per_iteration_k1_k2"]   # ncu, per K1 + K2 pair
     except Exception:
         pass
 
