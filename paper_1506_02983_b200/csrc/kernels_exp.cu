@@ -22,8 +22,8 @@
 // EXP_true (l.10): u~ = u_h + (1/3) I_trilinear(u_h|_2h - u_2h), which equals
 // Eq. (t1) at 2h nodes, Eq. (chenlin) at 2h edge centres and the mean of Eq. (chenlin) over the
 // 2 face diagonals / 4 space diagonals at face / cell centres (reading §8c A13; derived identity,
-// DESIGN.md). One thread per 2h cell computes its (up to 27) owned fine nodes from the 8 corner
-// differences. Dirichlet nodes take g_D.
+// DESIGN.md). A z-march over 64 x 8 fine tiles (coalesced rows) with the corner differences of two 2h
+// planes in shared memory. Dirichlet nodes take g_D.
 #include <algorithm>
 #include "ecmg_internal.cuh"
 #include "problems.cuh"
@@ -31,9 +31,9 @@
 namespace ecmg {
 namespace {
 
-__device__ __forceinline__ bool is_free(const LevelGeom& g, int gx, int gy, int gz) {
-  return gx >= g.flo[0] && gx < g.flo[0] + g.nf[0] && gy >= g.flo[1] && gy < g.flo[1] + g.nf[1] &&
-         gz >= g.flo[2] && gz < g.flo[2] + g.nf[2];
+// g_D at fine node (fx, fy, fz): kept out of line (boundary faces only) so the marching loops stay lean
+__device__ __noinline__ double gD_at(const LevelGeom& gf, const Problem& pb, int fx, int fy, int fz) {
+  return prob_gD(pb, gf.lo[0] + fx * gf.h[0], gf.lo[1] + fy * gf.h[1], gf.lo[2] + fz * gf.h[2]);
 }
 
 // (1) extrapolated values at all 2h nodes of the fine level gf (2h grid: n/2 cells per axis)
@@ -152,74 +152,109 @@ __global__ void __launch_bounds__(64) k_exp_interp(const LevelGeom gf, const Pro
       if (FREEBOX) {
         if (fr) out[(long long)(fz - gf.flo[2] - gf.zoff) * gf.S + (long long)(fy - gf.flo[1]) * gf.P + (fx - gf.flo[0])] = W;
       } else {
-        if (!fr) W = prob_gD(pb, gf.lo[0] + fx * gf.h[0], gf.lo[1] + fy * gf.h[1], gf.lo[2] + fz * gf.h[2]);
+        if (!fr) W = gD_at(gf, pb, fx, fy, fz);
         out[(long long)fx + nx * ((long long)fy + ny * fz)] = W;
       }
     }
   }
 }
 
-// EXP_true, one thread per 2h cell (cx, cy, cz); owned fine nodes 2c + {0,1} per axis (+2 in the
-// last cell along an axis). Cells whose owned nodes are all free take the fast path (no Dirichlet
-// tests, pointer increments only).
-__global__ void __launch_bounds__(128, 6) k_exp_true(const LevelGeom gf, const Problem pb, const double* __restrict__ uh,
-                                                  const double* __restrict__ u2h, double* __restrict__ ut) {
+// EXP_true as a z-march over a 64 x 8 fine tile (threads 32 x 8; thread (lane, w) owns the nodes
+// X0 + lane and X0 + 32 + lane of fine row Y0 + w, so every load / store instruction of a warp covers
+// 256 contiguous bytes). Per 2h plane K: (a) the tile's 33 x 5 corner differences
+// d = u_h|_2h - u_2h of plane K go to a two-plane shared ring; (b) fine plane 2K-1 is written from
+// d planes K-1, K and (c) fine plane 2K from d plane K: u~ = u_h + (1/3) I_trilinear(d), where the
+// trilinear interpolant at a fine node is d at the 2h node it sits on, or the mean of the two / four /
+// eight 2h nodes around it (reading A13). Dirichlet nodes take g_D (A15).
+constexpr int ETX = 64, ETY = 8, EDX = ETX / 2 + 1, EDY = ETY / 2 + 1;   // 33 x 5 corner values per plane
+
+__global__ void __launch_bounds__(256) k_exp_true(const LevelGeom gf, const Problem pb, const double* __restrict__ uh,
+                                                  const double* __restrict__ u2h, double* __restrict__ ut, int c0,
+                                                  int cchunk) {
+  __shared__ double D[2][EDY][EDX];
+  const int lane = threadIdx.x, w = threadIdx.y, tid = lane + 32 * w;
   const int n2x = gf.n[0] / 2, n2y = gf.n[1] / 2, n2z = gf.n[2] / 2;
-  const int cx = blockIdx.x * blockDim.x + threadIdx.x, cy = blockIdx.y, cz = gf.zlo / 2 + blockIdx.z;
-  if (cx >= n2x) return;
+  const int X0 = blockIdx.x * ETX, Y0 = blockIdx.y * ETY;
+  const int I0 = X0 / 2, J0 = Y0 / 2;
+  const int Ca = c0 + blockIdx.z * cchunk, Cb = min(Ca + cchunk, min(gf.zhi / 2, n2z));   // 2h cells [Ca, Cb)
+  if (Ca >= Cb) return;
   const long long nx = gf.n[0] + 1, ny = gf.n[1] + 1, pl = nx * ny;
   const long long nx2 = n2x + 1, pl2 = nx2 * (n2y + 1);
-  const long long c0 = 2LL * cx + nx * 2LL * cy + pl * 2LL * cz;     // fine index of the cell's first node
-  const long long k0 = (long long)cx + nx2 * cy + pl2 * cz;          // 2h index of the cell's first corner
-  double d[2][2][2];
-#pragma unroll
-  for (int c = 0; c < 2; ++c)
-#pragma unroll
-    for (int b = 0; b < 2; ++b)
-#pragma unroll
-      for (int a = 0; a < 2; ++a)
-        d[c][b][a] = __ldg(uh + c0 + 2 * (a + nx * b + pl * c)) - __ldg(u2h + k0 + a + nx2 * b + pl2 * c);
-  const bool last = (cx == n2x - 1) || (cy == n2y - 1) || (cz == n2z - 1);
-  const bool inner = !last && 2 * cx >= gf.flo[0] && 2 * cy >= gf.flo[1] && 2 * cz >= gf.flo[2] &&
-                     2 * cx + 1 < gf.flo[0] + gf.nf[0] && 2 * cy + 1 < gf.flo[1] + gf.nf[1] && 2 * cz + 1 < gf.flo[2] + gf.nf[2];
-  if (inner) {
-#pragma unroll
-    for (int c = 0; c < 2; ++c)
-#pragma unroll
-      for (int b = 0; b < 2; ++b) {
-        const double wz1 = 0.5 * c, wz0 = 1.0 - wz1, wy1 = 0.5 * b, wy0 = 1.0 - wy1;
-        const double r0 = wz0 * (wy0 * d[0][0][0] + wy1 * d[0][1][0]) + wz1 * (wy0 * d[1][0][0] + wy1 * d[1][1][0]);
-        const double r1 = wz0 * (wy0 * d[0][0][1] + wy1 * d[0][1][1]) + wz1 * (wy0 * d[1][0][1] + wy1 * d[1][1][1]);
-        const long long i = c0 + nx * b + pl * c;
-        ut[i] = __ldg(uh + i) + r0 / 3.0;
-        ut[i + 1] = __ldg(uh + i + 1) + (0.5 * r0 + 0.5 * r1) / 3.0;
-      }
-    return;
-  }
-  const int ea = (cx == n2x - 1) ? 3 : 2, eb = (cy == n2y - 1) ? 3 : 2, ec = (cz == n2z - 1) ? 3 : 2;
-  for (int c = 0; c < ec; ++c) {
-    const double wz[2] = {1.0 - 0.5 * c, 0.5 * c};
-    const int fz = 2 * cz + c;
-    for (int b = 0; b < eb; ++b) {
-      const double wy[2] = {1.0 - 0.5 * b, 0.5 * b};
-      const int fy = 2 * cy + b;
-      const double r0 = wz[0] * (wy[0] * d[0][0][0] + wy[1] * d[0][1][0]) + wz[1] * (wy[0] * d[1][0][0] + wy[1] * d[1][1][0]);
-      const double r1 = wz[0] * (wy[0] * d[0][0][1] + wy[1] * d[0][1][1]) + wz[1] * (wy[0] * d[1][0][1] + wy[1] * d[1][1][1]);
-      for (int a = 0; a < ea; ++a) {
-        const int fx = 2 * cx + a;
-        const long long i = (long long)fx + nx * ((long long)fy + ny * fz);
-        double v;
-        if (!is_free(gf, fx, fy, fz)) {
-          v = prob_gD(pb, gf.lo[0] + fx * gf.h[0], gf.lo[1] + fy * gf.h[1], gf.lo[2] + fz * gf.h[2]);
-        } else {
-          const double I = (1.0 - 0.5 * a) * r0 + 0.5 * a * r1;
-          v = __ldg(uh + i) + I / 3.0;
-        }
-        ut[i] = v;
-      }
+  const int fy = Y0 + w;
+  const bool row_ok = fy <= gf.n[1];
+  const int fxa = X0 + lane, fxb = X0 + 32 + lane;
+  // interpolation stencil of the thread's nodes: 2h column(s) and row(s) below / above
+  const int ia = lane >> 1, iaw = lane & 1;                 // node fxa: d column ia (+1 if odd)
+  const int ib = 16 + (lane >> 1);                          // node fxb: d column ib (+1 if odd)
+  const int jr = w >> 1, jw = w & 1;                        // row: d row jr (+1 if odd)
+  // (y, x)-interpolated d of plane slot s at the two nodes of this thread
+  auto dxy = [&](int s, double& va, double& vb) {
+    double a = D[s][jr][ia], b = D[s][jr][ib];
+    if (iaw) { a = 0.5 * (a + D[s][jr][ia + 1]); b = 0.5 * (b + D[s][jr][ib + 1]); }
+    if (jw) {
+      double a2 = D[s][jr + 1][ia], b2 = D[s][jr + 1][ib];
+      if (iaw) { a2 = 0.5 * (a2 + D[s][jr + 1][ia + 1]); b2 = 0.5 * (b2 + D[s][jr + 1][ib + 1]); }
+      a = 0.5 * (a + a2);
+      b = 0.5 * (b + b2);
+    }
+    va = a;
+    vb = b;
+  };
+  // loads are issued one step ahead (registers), so the global latency overlaps the barrier and the
+  // shared-memory interpolation of the current step
+  const bool dthr = tid < EDX * EDY;
+  const int di = tid % EDX, dj = tid / EDX;
+  const bool d_ok = dthr && I0 + di <= n2x && J0 + dj <= n2y;
+  auto load_d = [&](int K, double& a, double& b) {   // u_h at the 2h node and u_2h, plane K
+    a = b = 0.0;
+    if (d_ok) {
+      a = __ldg(uh + (long long)(2 * K) * pl + (long long)(2 * (J0 + dj)) * nx + 2 * (I0 + di));
+      b = __ldg(u2h + (long long)K * pl2 + (J0 + dj) * nx2 + (I0 + di));
+    }
+  };
+  const bool okA = row_ok && fxa <= gf.n[0], okB = row_ok && fxb <= gf.n[0];
+  auto load_u = [&](int fz, double& a, double& b) {
+    const long long row = (long long)fz * pl + (long long)fy * nx;
+    a = okA ? __ldg(uh + row + fxa) : 0.0;
+    b = okB ? __ldg(uh + row + fxb) : 0.0;
+  };
+  auto put = [&](int fz, double ua, double ub, double ia_, double ib_) {   // u~ on plane fz, this thread's nodes
+    const long long row = (long long)fz * pl + (long long)fy * nx;
+    const bool zf = fz >= gf.flo[2] && fz < gf.flo[2] + gf.nf[2], yf = fy >= gf.flo[1] && fy < gf.flo[1] + gf.nf[1];
+    if (okA) {
+      const bool fr = zf && yf && fxa >= gf.flo[0] && fxa < gf.flo[0] + gf.nf[0];
+      ut[row + fxa] = fr ? ua + ia_ / 3.0 : gD_at(gf, pb, fxa, fy, fz);
+    }
+    if (okB) {
+      const bool fr = zf && yf && fxb >= gf.flo[0] && fxb < gf.flo[0] + gf.nf[0];
+      ut[row + fxb] = fr ? ub + ib_ / 3.0 : gD_at(gf, pb, fxb, fy, fz);
+    }
+  };
+  double dh, d2;
+  load_d(Ca, dh, d2);
+  for (int K = Ca; K <= Cb; ++K) {
+    __syncthreads();   // the slot of plane K (plane K-2's) is free
+    if (dthr) D[K & 1][dj][di] = dh - d2;   // (a) corner differences of 2h plane K
+    if (K < Cb) load_d(K + 1, dh, d2);
+    double uoa = 0.0, uob = 0.0, uea = 0.0, ueb = 0.0;
+    const bool odd = K > Ca, even = K < Cb || K == n2z;
+    if (odd) load_u(2 * K - 1, uoa, uob);
+    if (even) load_u(2 * K, uea, ueb);
+    __syncthreads();
+    if (odd) {   // (b) odd fine plane 2K-1 between d planes K-1 and K
+      double a0, b0, a1, b1;
+      dxy((K - 1) & 1, a0, b0);
+      dxy(K & 1, a1, b1);
+      put(2 * K - 1, uoa, uob, 0.5 * (a0 + a1), 0.5 * (b0 + b1));
+    }
+    if (even) {   // (c) even fine plane 2K (the last 2h plane also ends the level)
+      double a0, b0;
+      dxy(K & 1, a0, b0);
+      put(2 * K, uea, ueb, a0, b0);
     }
   }
 }
+
 
 }  // namespace
 
@@ -246,9 +281,10 @@ cudaError_t launch_exp_true(const LevelGeom& gf, const Problem& pb, const double
                             cudaStream_t st) {
   const int c0 = gf.zlo / 2, c1 = std::min(gf.zhi / 2, gf.n[2] / 2);   // 2h cells owning this rank's planes
   if (c1 <= c0) return cudaSuccess;
-  dim3 grid((gf.n[0] / 2 + 127) / 128, gf.n[1] / 2, c1 - c0);
+  const int cchunk = 32;   // 2h cells (64 fine planes) per CTA
+  dim3 grid((gf.n[0] + 1 + ETX - 1) / ETX, (gf.n[1] + 1 + ETY - 1) / ETY, (c1 - c0 + cchunk - 1) / cchunk);
   count_launch();
-  k_exp_true<<<grid, 128, 0, st>>>(gf, pb, uh, u2h, ut);
+  k_exp_true<<<grid, dim3(32, 8), 0, st>>>(gf, pb, uh, u2h, ut, c0, cchunk);
   return cudaGetLastError();
 }
 
