@@ -196,21 +196,30 @@ __global__ void __launch_bounds__(VNTH, 3) k_rhs_vol(const LevelGeom g, const Pr
   }
 }
 
-// (r^2)^{-1/4} to fp64 accuracy: fp32 MUFU seed (rsqrt.approx, sqrt.approx: relative error ~3e-7) and
-// one fp32 Newton step (to ~1e-7, the fp32 rounding level) on the fp32 pipe, then one fp64 Newton step of
-// y <- y (5 - r^2 y^4) / 4 (error e -> -5/2 e^2: ~1e-7 -> ~3e-14)
-__device__ __forceinline__ double rpow_m14(double r2) {
-  if (!(r2 >= 1e-30 && r2 <= 1e30)) return r2 == 0.0 ? 0.0 : rsqrt(sqrt(r2));   // outside the seed's range
-  const float rf = (float)r2;
+// 4 (r^2)^{-1/4} to fp64 accuracy (the factor 1/4 of the last Newton step is folded into the caller's
+// weights): fp32 MUFU seed (rsqrt.approx, sqrt.approx: relative error ~3e-7) and one fp32 Newton step
+// (to ~1e-7, the fp32 rounding level) on the fp32 pipe, then one fp64 Newton step of
+// y <- y (5 - r^2 y^4) / 4 (error e -> -5/2 e^2: ~1e-7 -> ~3e-14). r^2 > 0 at every Gauss point (they
+// are interior to the elements); the fp32 clamp only keeps the seed finite.
+__device__ __forceinline__ double rpow_m14_x4(double r2, double five) {
+  const float rf = fmaxf((float)r2, 1e-30f);
   float s;
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"(rf));
   asm("sqrt.approx.ftz.f32 %0, %0;" : "+f"(s));
   float s2 = s * s;
   s = s * fmaf(-rf, s2 * s2, 5.0f) * 0.25f;
-  double y = (double)s;
+  const double y = (double)s;
   const double y2 = y * y;
-  return y * __fma_rn(-r2, y2 * y2, 5.0) * 0.25;
+  return y * __fma_rn(-r2, y2 * y2, five);
 }
+
+// fp64 constants of k_rhs_c4 as kernel parameters (constant bank operands instead of per-use
+// immediate materialisation)
+struct RhsC4Consts {
+  double wA, wB;   // N at the near / far Gauss point
+  double dA, dB;   // detJ * (-15/4) * (1/4) * wA, wB: the z pass of the tensor transform
+  double five;
+};
 
 // C4 volume load (f = -(15/4) r^{-1/2}, the corner singularity of u = r^{3/2}): element tile 32 x 8 =
 // one element per thread (node tile 31 x 7), z-marching over element layers. r^2 at a Gauss point is
@@ -218,7 +227,8 @@ __device__ __forceinline__ double rpow_m14(double r2) {
 // costs one add and the (r^2)^{-1/4} evaluation; the element vector F_e[a] = detJ sum_q f_q N_a(q) is
 // the same 2x2x2 tensor transform as k_rhs_vol. Per layer the z = 0 corners complete node plane fez
 // (with the z = 1 corners of the layer below carried in a register) through two shared-memory planes.
-__global__ void __launch_bounds__(VNTH, 3) k_rhs_c4(const LevelGeom g, double* __restrict__ b, int zc) {
+__global__ void __launch_bounds__(VNTH, 3) k_rhs_c4(const LevelGeom g, double* __restrict__ b, int zc,
+                                                   const RhsC4Consts k) {
   __shared__ double F0[4][VEY][VEX];   // layer corner entries a = 0..3 (z = 0: node plane fez)
   __shared__ double F1[4][VEY][VEX];   // a = 4..7 (z = 1: node plane fez + 1)
   const int lane = threadIdx.x, w = threadIdx.y;
@@ -230,9 +240,7 @@ __global__ void __launch_bounds__(VNTH, 3) k_rhs_c4(const LevelGeom g, double* _
   const double xa = g.lo[0] + (gex + ga) * g.h[0], xb = g.lo[0] + (gex + gb) * g.h[0];
   const double ya = g.lo[1] + (gey + ga) * g.h[1], yb = g.lo[1] + (gey + gb) * g.h[1];
   const double sxy[4] = {xa * xa + ya * ya, xb * xb + ya * ya, xa * xa + yb * yb, xb * xb + yb * yb};   // q bits x, y
-  const double detJ = -3.75 * (g.h[0] * g.h[1] * g.h[2] / 8.0);
-  const double wA = (1.0 + kGauss) / 2.0, wB = (1.0 - kGauss) / 2.0;   // N at the near / far Gauss point
-  const double dA = detJ * wA, dB = detJ * wB;
+  const double wA = k.wA, wB = k.wB, dA = k.dA, dB = k.dB;
   const int fx = X0 + lane, fy = Y0 + w;
   const bool node_ok = lane < VX && w < VY && fx < g.nf[0] && fy < g.nf[1];
   double carry = 0.0;
@@ -244,7 +252,7 @@ __global__ void __launch_bounds__(VNTH, 3) k_rhs_c4(const LevelGeom g, double* _
       const double z2[2] = {za * za, zb * zb};
       double f[8], t1[8], t2[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) f[q] = rpow_m14(sxy[q & 3] + z2[q >> 2]);
+      for (int q = 0; q < 8; ++q) f[q] = rpow_m14_x4(sxy[q & 3] + z2[q >> 2], k.five);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {   // along x: node bit 0 vs Gauss bit 0
         const int qb = i & ~1;
@@ -430,7 +438,16 @@ cudaError_t launch_rhs(const LevelGeom& g, const Problem& pb, const ElemStencil&
     const int zc = 32;
     dim3 grid((g.nf[0] + VX - 1) / VX, (g.nf[1] + VY - 1) / VY, (g.zend - g.zbeg + zc - 1) / zc);
     count_launch();
-    if (pb.id == 4) k_rhs_c4<<<grid, dim3(32, 8), 0, st>>>(g, b, zc);
+    if (pb.id == 4) {
+      RhsC4Consts k;
+      k.wA = (1.0 + kGauss) / 2.0;
+      k.wB = (1.0 - kGauss) / 2.0;
+      const double detJ = -3.75 * (g.h[0] * g.h[1] * g.h[2] / 8.0) * 0.25;   // f = -15/4 (r^2)^{-1/4}
+      k.dA = detJ * k.wA;
+      k.dB = detJ * k.wB;
+      k.five = 5.0;
+      k_rhs_c4<<<grid, dim3(32, 8), 0, st>>>(g, b, zc, k);
+    }
     else k_rhs_vol<0><<<grid, dim3(32, 8), VSMEM, st>>>(g, pb, b, zc);
   }
   const int m = std::max(g.nf[0], std::max(g.nf[1], g.nf[2]));
