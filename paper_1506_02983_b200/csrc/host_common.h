@@ -101,6 +101,19 @@ inline int device_sm_count() {
 inline int auto_zc(int zchunk, int elem_path, const LevelGeom& g) {
   if (zchunk > 0) return zchunk;
   const int nz = g.zend - g.zbeg;
+  const double slots = device_sm_count() * 2.0;   // both JCG kernels: 2 CTAs per SM (register bound)
+  {
+    // small levels (latency bound: a pass takes ~zc+2 dependent plane steps plus a fixed launch and
+    // reduction cost): about 256 CTAs with chunks of >= 3 planes (tools/tune_zc_levels.py: 64^3 best at
+    // zc 3-4, 128^3 at zc 8 (constant) / 16 (element), 20 % faster than 2 waves of 4-plane chunks)
+    const double tiles = elem_path ? (double)((g.nf[0] + 31) / 32) * ((g.nf[1] + 15) / 16)
+                                   : (double)((g.nf[0] + 31) / 32) * ((g.nf[1] + 31) / 32);
+    if (tiles * (nz / 16) < 1.5 * slots) {
+      long long nchunks = (long long)std::ceil(256.0 / tiles);
+      nchunks = std::max(1LL, std::min(nchunks, (long long)std::max(1, nz / 3)));
+      return (int)((nz + nchunks - 1) / nchunks);
+    }
+  }
   if (!elem_path) {   // constant stencil, 32 x 32 tiles: about 4 CTAs per SM in total (tools/tune_jcg.py)
     const long long tiles = (long long)((g.nf[0] + 31) / 32) * ((g.nf[1] + 31) / 32);
     const long long target = (long long)device_sm_count() * 2 * 2;
@@ -113,14 +126,6 @@ inline int auto_zc(int zchunk, int elem_path, const LevelGeom& g) {
   // (a partial last wave idles SMs; fewer than ~1.5 waves cannot saturate HBM; every chunk re-reads
   // two halo planes). Measured on C3 256^3: the sweep is flat at the optimum and 10 % worse at 2.2 waves.
   const double tiles = (double)((g.nf[0] + 31) / 32) * ((g.nf[1] + 15) / 16);
-  const double slots = device_sm_count() * 2.0;
-  if (tiles * (nz / 16) < 1.5 * slots) {
-    // small level (latency bound: the pass takes ~zc+2 dependent plane steps): as many chunks of >= 4
-    // planes as give about 2 waves
-    long long nchunks = (long long)std::ceil(2.0 * slots / tiles);
-    nchunks = std::max(1LL, std::min(nchunks, (long long)std::max(1, nz / 4)));
-    return (int)((nz + nchunks - 1) / nchunks);
-  }
   int best_zc = std::max(1, nz);
   double best = -1.0;
   for (int k = 1; k <= std::max(1, nz / 16); ++k) {
