@@ -104,9 +104,10 @@ typedef enum {
                                 0 register-prefetch loads (ablation) */
   ECMG_OPT_GRAPH = 5,        /* tolerance-stopped JCG loop: 1 (default) one CUDA graph per level with a
                                 device-set conditional WHILE node; 0 host loop with batched readbacks */
-  ECMG_OPT_PERSISTENT = 7,   /* levels with at most this many free unknowns run the whole JCG solve in
-                                one cooperative launch, both operators (default 40000, i.e. up to 32^3
-                                cells; 0 = off; single GPU only) */
+  ECMG_OPT_PERSISTENT = 7,   /* levels with at most this many free unknowns (and at most 4 bricks of
+                                8x8x4 nodes per resident CTA) run the whole JCG solve in one cooperative
+                                launch, both operators (default 300000, i.e. up to 64^3 cells; 0 = off;
+                                single GPU only) */
   ECMG_OPT_VIRTUAL_SLABS = 6 /* P in 2..16: run the z-slab decomposition with P slabs on this one GPU
                                 (device copies stand in for the NCCL halo messages, an in-order sum
                                 kernel for the allreduce; the multi-GPU test fixture); 0 or 1: off */

@@ -58,7 +58,7 @@ struct ecmg_grid {
   bool ev_init = false;
   int kernel_variant = 1;   // ECMG_OPT_KERNEL
   int use_graph = 1;        // ECMG_OPT_GRAPH: device-driven JCG loop (CUDA graph, conditional WHILE node)
-  long long persistent_max = 40000;  // ECMG_OPT_PERSISTENT: one cooperative launch per solve up to this size (tools/tune_persistent.py)
+  long long persistent_max = 300000;  // ECMG_OPT_PERSISTENT: one cooperative launch per solve up to this size (tools/tune_persistent.py)
   double* aux[2] = {nullptr, nullptr};   // persistent element-path solve: w = A p and D^-1 (level-sized)
   long long aux_doubles = 0;
   cudaStream_t cap_stream = nullptr;          // private stream used only for graph capture
@@ -297,7 +297,9 @@ int run_jcg_graph(ecmg_grid* G, int k, double eps, ecmg_stats* st) {
 }
 
 bool use_persistent(const ecmg_grid* G, const LevelGeom& g) {
-  return !G->slab && G->persistent_max > 0 && free_count(g) <= G->persistent_max;
+  if (G->slab || G->persistent_max <= 0 || free_count(g) > G->persistent_max) return false;
+  const long long nbricks = (long long)((g.nf[0] + 7) / 8) * ((g.nf[1] + 7) / 8) * ((g.nf[2] + 3) / 4);
+  return nbricks <= persistent_max_bricks(G->elem_path);   // every brick's nodes stay in registers
 }
 
 // the whole solve of a small level in one cooperative launch (kernels_jcg_persistent.cu)

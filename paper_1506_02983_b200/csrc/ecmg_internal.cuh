@@ -141,6 +141,7 @@ cudaError_t launch_vsum(const SlabScalars& s, cudaStream_t st);
 cudaError_t launch_jcg_persistent(const LevelGeom& g, const ConstStencil& cs, const ElemStencil* es, double* x, double* r,
                                   double* z, double* p0, double* p1, double* w, double* dinv, const double* beta,
                                   const double* b, double* partials, JcgScalars* sc, cudaStream_t st);
+long long persistent_max_bricks(int elem_path);
 cudaError_t init_tma_kernel_attributes();
 cudaError_t init_elem_kernel_attributes();
 int elem_tile_rows();

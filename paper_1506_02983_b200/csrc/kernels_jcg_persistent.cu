@@ -233,6 +233,12 @@ __device__ __forceinline__ double apply_node(const LevelGeom& g, const ConstSten
   return apply_const(cs, p27);
 }
 
+// Each CTA owns at most MAXB bricks (k = blockIdx.x + i gridDim.x) for the whole solve, and each thread
+// keeps its nodes' x, r, D^-1, p_new and A p_new in registers: phase 2 needs no global loads, A p is never
+// stored, x is stored once at the end. Only the halo exchange goes through L2: z (element path) or r
+// (constant path, z = D^-1 r with D constant) and p_new.
+constexpr int MAXB = 4;
+
 template <bool ELEM>
 __global__ void __launch_bounds__(PNTH, 2) k_jcg_persistent(const LevelGeom g, const ConstStencil cs, const ElemStencil es,
                                                          const PArgs a) {
@@ -245,32 +251,45 @@ __global__ void __launch_bounds__(PNTH, 2) k_jcg_persistent(const LevelGeom g, c
   const double eps = sc->in.eps;
   const int max_iter = sc->in.max_iter;
   double* const u_out = sc->in.u_out;
-  auto own = [&](const Brick& br, Node& nd) -> bool {
-    nd.fx = br.X0 + lx; nd.fy = br.Y0 + ly; nd.fz = br.Z0 + lz;
-    nd.off = nd.fz * (int)g.S + nd.fy * (int)g.P + nd.fx;
-    return nd.fx < g.nf[0] && nd.fy < g.nf[1] && nd.fz < g.nf[2];
-  };
+  double* const zsrc = ELEM ? a.z : a.r;   // what neighbours stage: p_new = zscale * zsrc + beta p_old
+  const double zscale = ELEM ? 1.0 : cdinv;
+
+  bool act[MAXB], own[MAXB];
+  Brick br[MAXB];
+  Node nd[MAXB];
+#pragma unroll
+  for (int i = 0; i < MAXB; ++i) {
+    const int k = blockIdx.x + i * gridDim.x;
+    act[i] = k < nbricks;   // uniform over the CTA
+    br[i] = brick_of(g, act[i] ? k : 0);
+    nd[i].fx = br[i].X0 + lx; nd[i].fy = br[i].Y0 + ly; nd[i].fz = br[i].Z0 + lz;
+    nd[i].off = nd[i].fz * (int)g.S + nd[i].fy * (int)g.P + nd[i].fx;
+    own[i] = act[i] && nd[i].fx < g.nf[0] && nd[i].fy < g.nf[1] && nd[i].fz < g.nf[2];
+  }
+  double xr[MAXB], rr_[MAXB], di[MAXB], pc[MAXB], wv[MAXB];
   int buf = 0;
   // init: D^-1 (element path), r = b - A x, z = D^-1 r, rho = r.z, rr, ||b||^2
   double v[3] = {0.0, 0.0, 0.0};
-  for (int k = blockIdx.x; k < nbricks; k += gridDim.x) {
-    const Brick br = brick_of(g, k);
+#pragma unroll
+  for (int i = 0; i < MAXB; ++i) {
+    xr[i] = rr_[i] = pc[i] = wv[i] = 0.0;
+    di[i] = cdinv;
+    if (!act[i]) continue;
     __syncthreads();
-    stage<false>(g, br, a.x, nullptr, 1.0, 0.0, sp);
+    stage<false>(g, br[i], a.x, nullptr, 1.0, 0.0, sp);
     __syncthreads();
-    Node nd;
-    if (!own(br, nd)) continue;
+    if (!own[i]) continue;
     double p27[3][3][3];
     window27(sp, lx, ly, lz, p27);
     double d = 0.0;
-    const double ax = apply_node<ELEM>(g, cs, es, a.beta, nd, p27, &d);
-    const double di = ELEM ? (es.precond ? (d > 0.0 ? 1.0 / d : 0.0) : 1.0) : cdinv;
-    if (ELEM) a.dinv[nd.off] = di;
-    const double bi = a.b[nd.off];
+    const double ax = apply_node<ELEM>(g, cs, es, a.beta, nd[i], p27, &d);
+    if (ELEM) di[i] = es.precond ? (d > 0.0 ? 1.0 / d : 0.0) : 1.0;
+    xr[i] = p27[1][1][1];
+    const double bi = a.b[nd[i].off];
     const double rn = bi - ax;
-    const double zz = di * rn;
-    a.r[nd.off] = rn;
-    if (ELEM) a.z[nd.off] = zz;
+    const double zz = di[i] * rn;
+    rr_[i] = rn;
+    zsrc[nd[i].off] = ELEM ? zz : rn;
     v[0] = __fma_rn(rn, zz, v[0]);
     v[1] = __fma_rn(rn, rn, v[1]);
     v[2] = __fma_rn(bi, bi, v[2]);
@@ -287,42 +306,38 @@ __global__ void __launch_bounds__(PNTH, 2) k_jcg_persistent(const LevelGeom g, c
   int cur = 0;   // a.p[cur] holds p_old
   while (!done) {
     // phase 1: p_new = z + beta p_old on the brick and its halo, w = A p_new, sigma = p_new . w
-    const double* zsrc = ELEM ? a.z : a.r;
-    const double zscale = ELEM ? 1.0 : cdinv;
     const double bcg = iter == 0 ? 0.0 : beta;
     double* pnew = a.p[cur ^ 1];
     const double* pold = a.p[cur];
     v[0] = v[1] = v[2] = 0.0;
-    for (int k = blockIdx.x; k < nbricks; k += gridDim.x) {
-      const Brick br = brick_of(g, k);
+#pragma unroll
+    for (int i = 0; i < MAXB; ++i) {
+      if (!act[i]) continue;
       __syncthreads();
-      stage<true>(g, br, zsrc, pold, zscale, bcg, sp);
+      stage<true>(g, br[i], zsrc, pold, zscale, bcg, sp);
       __syncthreads();
-      Node nd;
-      if (!own(br, nd)) continue;
+      if (!own[i]) continue;
       double p27[3][3][3];
       window27(sp, lx, ly, lz, p27);
-      const double wi = apply_node<ELEM>(g, cs, es, a.beta, nd, p27, nullptr);
-      const double pc = p27[1][1][1];
-      pnew[nd.off] = pc;
-      a.w[nd.off] = wi;
-      v[0] = __fma_rn(pc, wi, v[0]);
+      wv[i] = apply_node<ELEM>(g, cs, es, a.beta, nd[i], p27, nullptr);
+      pc[i] = p27[1][1][1];
+      pnew[nd[i].off] = pc[i];
+      v[0] = __fma_rn(pc[i], wv[i], v[0]);
     }
     grid_sum3(v, a.partials, buf, grid);
     const double sigma = v[0];
     if (!(sigma > 0.0)) { status = ST_EBREAKDOWN; break; }
     const double alpha = rho / sigma;
-    // phase 2 (own nodes only): x += alpha p, r -= alpha w, z = D^-1 r, rho' = r.z, rr = r.r
+    // phase 2 (own nodes, registers): x += alpha p, r -= alpha w, z = D^-1 r, rho' = r.z, rr = r.r
     v[0] = v[1] = v[2] = 0.0;
-    for (int k = blockIdx.x; k < nbricks; k += gridDim.x) {
-      Node nd;
-      if (!own(brick_of(g, k), nd)) continue;
-      const int o = nd.off;
-      a.x[o] = __fma_rn(alpha, pnew[o], a.x[o]);
-      const double rn = __fma_rn(-alpha, a.w[o], a.r[o]);
-      a.r[o] = rn;
-      const double zz = (ELEM ? a.dinv[o] : cdinv) * rn;
-      if (ELEM) a.z[o] = zz;
+#pragma unroll
+    for (int i = 0; i < MAXB; ++i) {
+      if (!own[i]) continue;
+      xr[i] = __fma_rn(alpha, pc[i], xr[i]);
+      const double rn = __fma_rn(-alpha, wv[i], rr_[i]);
+      rr_[i] = rn;
+      const double zz = di[i] * rn;
+      zsrc[nd[i].off] = ELEM ? zz : rn;
       v[0] = __fma_rn(rn, zz, v[0]);
       v[1] = __fma_rn(rn, rn, v[1]);
     }
@@ -335,20 +350,24 @@ __global__ void __launch_bounds__(PNTH, 2) k_jcg_persistent(const LevelGeom g, c
     done = (iter >= max_iter) || (thresh > 0.0 && !(sqrt(rr) > thresh));
     if (!isfinite(rr)) { status = ST_EBREAKDOWN; done = true; }
   }
-  // true residual ||b - A x||
+  // x (and r, for the caller's inspection) back to memory, then the true residual ||b - A x||
+#pragma unroll
+  for (int i = 0; i < MAXB; ++i)
+    if (own[i]) { a.x[nd[i].off] = xr[i]; a.r[nd[i].off] = rr_[i]; }
+  grid.sync();
   v[0] = v[1] = v[2] = 0.0;
-  for (int k = blockIdx.x; k < nbricks; k += gridDim.x) {
-    const Brick br = brick_of(g, k);
+#pragma unroll
+  for (int i = 0; i < MAXB; ++i) {
+    if (!act[i]) continue;
     __syncthreads();
-    stage<false>(g, br, a.x, nullptr, 1.0, 0.0, sp);
+    stage<false>(g, br[i], a.x, nullptr, 1.0, 0.0, sp);
     __syncthreads();
-    Node nd;
-    if (!own(br, nd)) continue;
+    if (!own[i]) continue;
     double p27[3][3][3];
     window27(sp, lx, ly, lz, p27);
-    const double rn = a.b[nd.off] - apply_node<ELEM>(g, cs, es, a.beta, nd, p27, nullptr);
+    const double rn = a.b[nd[i].off] - apply_node<ELEM>(g, cs, es, a.beta, nd[i], p27, nullptr);
     v[1] = __fma_rn(rn, rn, v[1]);
-    if (u_out) u_out[full_index(g, nd.fx, nd.fy, nd.fz)] = p27[1][1][1];   // fused scatter of u_h
+    if (u_out) u_out[full_index(g, nd[i].fx, nd[i].fy, nd[i].fz)] = xr[i];   // fused scatter of u_h
   }
   grid_sum3(v, a.partials, buf, grid);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -372,13 +391,21 @@ int persistent_grid(int want) {
 
 }  // namespace
 
+// largest level (in bricks of 8 x 8 x 4 nodes) the persistent kernel takes: MAXB bricks per resident CTA
+long long persistent_max_bricks(int elem_path) {
+  return (long long)MAXB * (elem_path ? persistent_grid<true>(1 << 30) : persistent_grid<false>(1 << 30));
+}
+
 // One cooperative launch: the whole solve. Element path (es != nullptr): z, dinv and w are scratch
 // vectors of the level's size; beta as in KArgs. Constant path: z, dinv, beta unused.
 cudaError_t launch_jcg_persistent(const LevelGeom& g, const ConstStencil& cs, const ElemStencil* es, double* x, double* r,
                                   double* z, double* p0, double* p1, double* w, double* dinv, const double* beta,
                                   const double* b, double* partials, JcgScalars* sc, cudaStream_t st) {
   const long long nbricks = (long long)((g.nf[0] + BX - 1) / BX) * ((g.nf[1] + BY - 1) / BY) * ((g.nf[2] + BZ - 1) / BZ);
-  const int want = (int)std::min<long long>(nbricks, 1 << 20);
+  // one brick per CTA while the CTAs fit (parallelism), up to MAXB per CTA beyond that
+  const int slots = es ? persistent_grid<true>(1 << 30) : persistent_grid<false>(1 << 30);
+  if (nbricks > (long long)MAXB * slots) return cudaErrorInvalidValue;
+  const int want = (int)std::min<long long>(nbricks, slots);
   PArgs a{x, r, z, {p0, p1}, w, b, dinv, beta, partials, sc};
   const ElemStencil e = es ? *es : ElemStencil{};
   void* args[] = {(void*)&g, (void*)&cs, (void*)&e, (void*)&a};
