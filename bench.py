@@ -308,7 +308,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (analytic C4 problem; no dataset)",
+            "data": f"synthetic (analytic {args.config.upper()} problem; no dataset)",
             "config": {"workload": desc, "levels": levels, "finest_cells": list(shape), "eps": eps,
                        "free_unknowns_finest": int(nf_j),
                        "parallelism": f"z-slabs over {ws} NCCL ranks (levels with n % 4P == 0 and n/P >= 16 sharded)"
