@@ -108,6 +108,9 @@ typedef enum {
                                 8x8x4 nodes per resident CTA) run the whole JCG solve in one cooperative
                                 launch, both operators (default 300000, i.e. up to 64^3 cells; 0 = off;
                                 single GPU only) */
+  ECMG_OPT_PDL = 8,          /* 1: the JCG kernels use programmatic dependent launch (the next kernel's
+                                launch overlaps the previous one's tail); 0 (default): plain launches
+                                (measured on B200: no difference inside the per-level CUDA graphs) */
   ECMG_OPT_VIRTUAL_SLABS = 6 /* P in 2..16: run the z-slab decomposition with P slabs on this one GPU
                                 (device copies stand in for the NCCL halo messages, an in-order sum
                                 kernel for the allreduce; the multi-GPU test fixture); 0 or 1: off */

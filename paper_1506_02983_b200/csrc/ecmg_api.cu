@@ -58,6 +58,8 @@ struct ecmg_grid {
   bool ev_init = false;
   int kernel_variant = 1;   // ECMG_OPT_KERNEL
   int use_graph = 1;        // ECMG_OPT_GRAPH: device-driven JCG loop (CUDA graph, conditional WHILE node)
+  int pdl = 0;              // ECMG_OPT_PDL: programmatic dependent launch between the JCG kernels (measured: no gain
+                            // inside the CUDA graphs, tools/tune_pdl.py; off by default)
   long long persistent_max = 300000;  // ECMG_OPT_PERSISTENT: one cooperative launch per solve up to this size (tools/tune_persistent.py)
   double* aux[2] = {nullptr, nullptr};   // persistent element-path solve: w = A p and D^-1 (level-sized)
   long long aux_doubles = 0;
@@ -228,7 +230,7 @@ cudaError_t build_level_graph(ecmg_grid* G, int k, cudaGraphExec_t* out) {
   cudaGraphConditionalHandle h;
   e = cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault);
   KArgs a{};
-  a.partials = G->partials; a.sc = G->sc; a.zc = auto_zc(G->zchunk, G->elem_path, g); a.beta = G->beta;
+  a.partials = G->partials; a.sc = G->sc; a.pdl = G->pdl; a.zc = auto_zc(G->zchunk, G->elem_path, g); a.beta = G->beta;
   a.cond = h; a.use_cond = 1;
   const long long launches_before = ecmg_kernel_launches();
   cudaStream_t user = G->stream;
@@ -370,6 +372,7 @@ int run_jcg(ecmg_grid* G, int k, double eps, int max_iter, double* u_out, ecmg_s
   KArgs a{};
   a.partials = G->partials;
   a.sc = G->sc;
+  a.pdl = G->pdl;
   a.zc = auto_zc(G->zchunk, G->elem_path, g);
   a.beta = G->beta;
   // eps and max_iter reach the init pass through the device scalars
@@ -640,6 +643,7 @@ int ecmg_set_option(ecmg_grid* G, int option, int value) {
     case ECMG_OPT_KERNEL: if (value != 0 && value != 1) return ECMG_EINVAL; G->kernel_variant = value; clear_graphs(G); break;
     case ECMG_OPT_GRAPH: if (value != 0 && value != 1) return ECMG_EINVAL; G->use_graph = value; break;
     case ECMG_OPT_PERSISTENT: if (value < 0) return ECMG_EINVAL; G->persistent_max = value; break;
+    case ECMG_OPT_PDL: if (value != 0 && value != 1) return ECMG_EINVAL; G->pdl = value; clear_graphs(G); break;
     case ECMG_OPT_VIRTUAL_SLABS: {
       if (value < 0 || value > 16 || G->nranks > 1) return ECMG_EINVAL;
       if (G->slab) { slab_driver_destroy(G->slab); G->slab = nullptr; }
@@ -720,7 +724,7 @@ int ecmg_apply_operator(ecmg_grid* G, int level, const double* p, double* q) {
   if (G->elem_path && G->setup_level != level) { int s = setup_level(G, level); if (s) return s; }
   ECMG_CUDA(launch_gather(g, p, G->p[0], G->stream));
   KArgs a{};
-  a.partials = G->partials; a.sc = G->sc; a.zc = auto_zc(G->zchunk, G->elem_path, g); a.beta = G->beta;
+  a.partials = G->partials; a.sc = G->sc; a.pdl = G->pdl; a.zc = auto_zc(G->zchunk, G->elem_path, g); a.beta = G->beta;
   a.h0 = G->p[0]; a.o0 = G->r;
   ECMG_CUDA(launch_mode(G, MODE_APPLY, g, a));
   ECMG_CUDA(cudaMemsetAsync(q, 0, sizeof(double) * level_nodes(g), G->stream));
@@ -739,7 +743,7 @@ int ecmg_level_rhs(ecmg_grid* G, int level, double* bout, double* norm_b) {
   ECMG_CUDA(launch_zero_vec(g, G->x, G->stream));
   {
     KArgs a{};
-    a.partials = G->partials; a.sc = G->sc; a.zc = auto_zc(G->zchunk, G->elem_path, g); a.beta = G->beta;
+    a.partials = G->partials; a.sc = G->sc; a.pdl = G->pdl; a.zc = auto_zc(G->zchunk, G->elem_path, g); a.beta = G->beta;
     a.h0 = G->x; a.i0 = G->b; a.o0 = G->r; a.o1 = G->zv;
     ECMG_CUDA(launch_mode(G, MODE_INIT, g, a));
   }

@@ -12,6 +12,7 @@
 //    beta_e = 0 outside the domain, which truncates the stencil at Robin / Neumann faces.
 #pragma once
 #include <cstdint>
+#include <utility>
 #include <cuda_runtime.h>
 
 namespace ecmg {
@@ -113,7 +114,25 @@ struct KArgs {
   cudaGraphConditionalHandle cond;   // CUDA-graph WHILE condition (device-driven JCG loop)
   int use_cond;                      // 1: the init / K2 passes set `cond` = !done
   int local_only;                    // z-slabs: write this slab's sums to sc->loc, finalize later
+  int pdl;                           // launch with programmatic stream serialization (ECMG_OPT_PDL)
 };
+
+// launch kernel<<<grid, block, smem, st>>>(args...), with programmatic dependent launch if pdl
+template <typename... KArgsT, typename... Act>
+inline cudaError_t launch_maybe_pdl(void (*kernel)(KArgsT...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, int pdl,
+                                    Act&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Act>(args)...);
+}
 
 // status codes (mirror of ecmg_status)
 enum { ST_OK = 0, ST_EINVAL = -1, ST_ENOMEM = -2, ST_ENOTCONV = -3, ST_EBREAKDOWN = -4, ST_EDIAG = -5,

@@ -10,6 +10,12 @@ constexpr int TX = 32;
 constexpr int WARPS = 8;
 constexpr int NTH = TX * WARPS;
 
+// ---- programmatic dependent launch (sm_90+): a JCG kernel lets the next one in the stream start
+// launching as soon as all its CTAs run, and waits for its predecessor's completion (and memory) before
+// it reads the CG scalars or any vector. Without the launch attribute both are no-ops.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ---- deterministic reductions and the device-side CG scalar updates -----------------------
 
 // ---- the per-node arithmetic of the constant-stencil kernels, with explicit rounding ------------

@@ -120,6 +120,8 @@ __global__ void __launch_bounds__(NTH, ELEM_MINB)
   // the reads compile to LDS, not generic LD)
   unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   JcgScalars* sc = a.sc;
+  pdl_trigger();
+  pdl_wait();
   if (MODE == MODE_K1 || MODE == MODE_K2) {
     if (*(volatile int*)&sc->done) return;
   }
@@ -392,10 +394,10 @@ cudaError_t launch_elem_tma_mode(const LevelGeom& g, const ElemStencil& es, cons
   dim3 grid((g.nf[0] + TX - 1) / TX, (g.nf[1] + TY - 1) / TY, (g.zend - g.zbeg + a.zc - 1) / a.zc);
   count_launch();
   if (es.cube)
-    k_jcg_elem_tma<MODE, NS, true><<<grid, dim3(TX, WARPS), elem_smem<MODE, NS>(), st>>>(g, es, a, m[0], m[1], m[2], m[3], m[4]);
-  else
-    k_jcg_elem_tma<MODE, NS, false><<<grid, dim3(TX, WARPS), elem_smem<MODE, NS>(), st>>>(g, es, a, m[0], m[1], m[2], m[3], m[4]);
-  return cudaGetLastError();
+    return launch_maybe_pdl(k_jcg_elem_tma<MODE, NS, true>, grid, dim3(TX, WARPS), elem_smem<MODE, NS>(), st, a.pdl, g, es,
+                            a, m[0], m[1], m[2], m[3], m[4]);
+  return launch_maybe_pdl(k_jcg_elem_tma<MODE, NS, false>, grid, dim3(TX, WARPS), elem_smem<MODE, NS>(), st, a.pdl, g, es,
+                          a, m[0], m[1], m[2], m[3], m[4]);
 }
 
 // ---- tensor-map cache: (base, geometry, box) -> CUtensorMap; an entry is a pure function of its key

@@ -86,6 +86,8 @@ __global__ void __launch_bounds__(NTH, 2)
   // the reads compile to LDS, not generic LD)
   unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   JcgScalars* sc = a.sc;
+  pdl_trigger();
+  pdl_wait();
   if (MODE == MODE_K1 || MODE == MODE_K2) {
     if (*(volatile int*)&sc->done) return;
   }
@@ -229,8 +231,8 @@ cudaError_t launch_tma_mode(dim3 grid, dim3 block, const LevelGeom& g, const Con
   constexpr int SBYTES = HSTRIDE * (kH1 ? 2 : 1) + IBYTES * kNI;
   constexpr int SMEM = SBYTES * NS + 128;
   count_launch();
-  k_jcg_const_tma<MODE, NS><<<grid, block, SMEM, st>>>(g, cs, a, maps[0], maps[1], maps[2], maps[3]);
-  return cudaGetLastError();
+  return launch_maybe_pdl(k_jcg_const_tma<MODE, NS>, grid, block, SMEM, st, a.pdl, g, cs, a, maps[0], maps[1], maps[2],
+                          maps[3]);
 }
 
 template <int MODE, int NS>
