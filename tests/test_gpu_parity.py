@@ -291,3 +291,19 @@ def test_alg3_fixed_schedule(pid, precond):
     assert [s["iterations"] for s in stats[2:]] == [int(v) for v in ostats[2:, 0]] == [12, 6, 3]
     assert np.max(np.abs(host(u) - ou)) <= 1e-11 * np.max(np.abs(ou))
     assert np.max(np.abs(host(ut) - out)) <= 1e-11 * np.max(np.abs(out))
+
+
+@pytest.mark.parametrize("pid,eps", [(o.C2, 1e-10), (o.C3, 1e-10)])
+def test_pdl_launch_bitwise(pid, eps):
+    # ECMG_OPT_PDL changes only how the JCG kernels are launched: iterates are bitwise identical
+    res = []
+    for pdl in (0, 1):
+        g = Grid(4, 5, pid, params_for(pid))
+        g.set_option(ecmg.OPT_PDL, pdl)
+        g.set_option(ecmg.OPT_PERSISTENT, 0)   # the z-marching kernels are the ones launched with PDL
+        u = g.new_vec(4)
+        st, stats = g.run(eps, u)
+        assert st == 0
+        res.append(([s["iterations"] for s in stats], host(u)))
+    assert res[0][0] == res[1][0]
+    assert np.array_equal(res[0][1], res[1][1])
