@@ -111,6 +111,11 @@ typedef enum {
   ECMG_OPT_PDL = 8,          /* 1: the JCG kernels use programmatic dependent launch (the next kernel's
                                 launch overlaps the previous one's tail); 0 (default): plain launches
                                 (measured on B200: no difference inside the per-level CUDA graphs) */
+  ECMG_OPT_FUSED_HALO = 9,   /* z-slabs: 1 (default) the K2 / init passes store their boundary planes of
+                                the vector the next K1 reads straight into the neighbours' halo planes
+                                (another slab on this GPU, or the neighbour rank's buffer mapped with
+                                CUDA IPC over NVLink; ranks fall back to 0 together if any mapping
+                                fails); 0: halo planes by device copy / ncclSend-ncclRecv */
   ECMG_OPT_VIRTUAL_SLABS = 6 /* P in 2..16: run the z-slab decomposition with P slabs on this one GPU
                                 (device copies stand in for the NCCL halo messages, an in-order sum
                                 kernel for the allreduce; the multi-GPU test fixture); 0 or 1: off */

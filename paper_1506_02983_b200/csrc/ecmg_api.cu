@@ -58,6 +58,7 @@ struct ecmg_grid {
   bool ev_init = false;
   int kernel_variant = 1;   // ECMG_OPT_KERNEL
   int use_graph = 1;        // ECMG_OPT_GRAPH: device-driven JCG loop (CUDA graph, conditional WHILE node)
+  int fused_halo = 1;       // ECMG_OPT_FUSED_HALO: z-slab halo planes stored by K2 / init into the neighbours
   int pdl = 0;              // ECMG_OPT_PDL: programmatic dependent launch between the JCG kernels (measured: no gain
                             // inside the CUDA graphs, tools/tune_pdl.py; off by default)
   long long persistent_max = 300000;  // ECMG_OPT_PERSISTENT: one cooperative launch per solve up to this size (tools/tune_persistent.py)
@@ -115,6 +116,7 @@ SlabCfg slab_cfg(const ecmg_grid* G) {
   c.precond = G->precond;
   c.kernel_variant = G->kernel_variant;
   c.zchunk = G->zchunk;
+  c.fused_halo = G->fused_halo;
   return c;
 }
 
@@ -644,6 +646,7 @@ int ecmg_set_option(ecmg_grid* G, int option, int value) {
     case ECMG_OPT_GRAPH: if (value != 0 && value != 1) return ECMG_EINVAL; G->use_graph = value; break;
     case ECMG_OPT_PERSISTENT: if (value < 0) return ECMG_EINVAL; G->persistent_max = value; break;
     case ECMG_OPT_PDL: if (value != 0 && value != 1) return ECMG_EINVAL; G->pdl = value; clear_graphs(G); break;
+    case ECMG_OPT_FUSED_HALO: if (value != 0 && value != 1) return ECMG_EINVAL; G->fused_halo = value; break;
     case ECMG_OPT_VIRTUAL_SLABS: {
       if (value < 0 || value > 16 || G->nranks > 1) return ECMG_EINVAL;
       if (G->slab) { slab_driver_destroy(G->slab); G->slab = nullptr; }

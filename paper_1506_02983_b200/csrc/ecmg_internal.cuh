@@ -115,6 +115,13 @@ struct KArgs {
   int use_cond;                      // 1: the init / K2 passes set `cond` = !done
   int local_only;                    // z-slabs: write this slab's sums to sc->loc, finalize later
   int pdl;                           // launch with programmatic stream serialization (ECMG_OPT_PDL)
+  // z-slabs, fused halo exchange (K2 and init passes): the neighbours' halo planes of the vector the
+  // next K1 reads (r, or z on the element path): peer_lo receives this slab's first owned plane (it is
+  // the lower neighbour's upper halo plane), peer_hi its last. Same (P, S) layout on every slab; a
+  // device pointer of another slab on this GPU (virtual slabs) or a CUDA-IPC mapping of the
+  // neighbour rank's buffer over NVLink. nullptr: no fused store (halo by copy / NCCL).
+  double* peer_lo;
+  double* peer_hi;
 };
 
 // launch kernel<<<grid, block, smem, st>>>(args...), with programmatic dependent launch if pdl

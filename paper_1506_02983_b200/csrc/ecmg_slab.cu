@@ -43,6 +43,7 @@ struct NcclApi {
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
 };
 
 static NcclApi& nccl() {
@@ -61,8 +62,9 @@ static NcclApi& nccl() {
   api.Recv = (decltype(api.Recv))dlsym(h, "ncclRecv");
   api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
   api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
+  api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
   api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.Send && api.Recv &&
-           api.GroupStart && api.GroupEnd;
+           api.GroupStart && api.GroupEnd && api.AllGather;
   return api;
 }
 
@@ -96,6 +98,13 @@ struct SlabCtx {
   int maps_level = -1;
   bool maps_ok = false;
   CUtensorMap xh, xi, rh, ri, ph[2], bi;
+  // fused halo exchange: base pointers of the lower [0] / upper [1] neighbour's r and z buffers (another
+  // slab on this GPU, or a CUDA-IPC mapping of the neighbour rank's buffers), and per level the local
+  // plane index of the neighbour's halo plane that receives this slab's boundary plane
+  double* peer_r[2] = {nullptr, nullptr};
+  double* peer_z[2] = {nullptr, nullptr};
+  bool peer_ipc = false;                 // the peer pointers are IPC mappings (closed at destroy)
+  std::vector<int> nb_lo_zend, nb_hi_zbeg;
 };
 
 struct SlabDriver {
@@ -330,20 +339,39 @@ int slab_jcg(SlabDriver* d, int k, double eps, int max_iter, ecmg_stats* st, cud
     }
   }
   if (sh && (rc = comm_halo(d, k, 0, stream))) return rc;
-  // K1 reads r (constant stencil) or z = D^-1 r (element path) on its halo planes
+  // K1 reads r (constant stencil) or z = D^-1 r (element path) on its halo planes. Fused halo: the init
+  // and K2 passes store their boundary planes of that vector straight into the neighbours' halo planes
+  // (peer memory); the allreduce that follows every pass orders those stores before the next K1.
   const bool elem = d->cfg.elem_path != 0;
   const int k1_vec = elem ? 2 : 1;
-  if ((rc = pass(MODE_INIT, [&](SlabCtx& c, KArgs& a) { a.h0 = c.x; a.i0 = c.b; a.o0 = c.r; a.o1 = c.z; }))) return rc;
-  if (sh && (rc = comm_halo(d, k, k1_vec, stream))) return rc;   // halo planes for the first K1
+  bool fused = sh && d->cfg.fused_halo != 0;
+  for (int i = 0; i < nloc && fused; ++i) {
+    const SlabCtx& c = d->s[i];
+    if ((c.rank > 0 && !c.peer_r[0]) || (c.rank + 1 < d->P && !c.peer_r[1])) fused = false;
+  }
+  auto set_peers = [&](SlabCtx& c, KArgs& a) {
+    if (!fused) return;
+    const LevelGeom& g = c.geom[k];
+    double* const* base = elem ? c.peer_z : c.peer_r;
+    a.peer_lo = c.rank > 0 ? base[0] + (long long)c.nb_lo_zend[k] * g.S : nullptr;
+    a.peer_hi = c.rank + 1 < d->P ? base[1] + (long long)(c.nb_hi_zbeg[k] - 1) * g.S : nullptr;
+  };
+  if ((rc = pass(MODE_INIT, [&](SlabCtx& c, KArgs& a) {
+         a.h0 = c.x; a.i0 = c.b; a.o0 = c.r; a.o1 = c.z;
+         set_peers(c, a);
+       })))
+    return rc;
+  if (sh && !fused && (rc = comm_halo(d, k, k1_vec, stream))) return rc;   // halo planes for the first K1
   long long it = 0;
   auto iteration = [&]() -> int {
     int q = pass(MODE_K1, [&](SlabCtx& c, KArgs& a) { a.h0 = elem ? c.z : c.r; a.h1 = c.p[it & 1]; a.o0 = c.p[(it + 1) & 1]; });
     if (q) return q;
     q = pass(MODE_K2, [&](SlabCtx& c, KArgs& a) {
       a.h0 = c.p[(it + 1) & 1]; a.i0 = c.x; a.i1 = c.r; a.o0 = c.x; a.o1 = c.r; a.o2 = c.z;
+      set_peers(c, a);
     });
     if (q) return q;
-    if (sh && (q = comm_halo(d, k, k1_vec, stream))) return q;
+    if (sh && !fused && (q = comm_halo(d, k, k1_vec, stream))) return q;
     ++it;
     return ECMG_OK;
   };
@@ -384,6 +412,76 @@ int slab_jcg(SlabDriver* d, int k, double eps, int max_iter, ecmg_stats* st, cud
 }
 
 }  // namespace
+
+// CUDA-IPC mappings of the neighbour ranks' r and z buffers (NVLink peer memory): every rank exports
+// the two handles, an ncclAllGather distributes them, ranks r-1 and r+1 open theirs. Any failure
+// (no P2P path, IPC unsupported) leaves the pointers null and the NCCL halo path in use; the outcome
+// is agreed on by all ranks (an allreduce of the success flags), so every rank takes the same path.
+void exchange_ipc(SlabDriver* d) {
+  NcclApi& n = nccl();
+  SlabCtx& c = d->s[0];
+  const int P = d->P, me = d->rank;
+  constexpr size_t H = sizeof(cudaIpcMemHandle_t);
+  std::vector<unsigned char> mine(2 * H, 0), all((size_t)P * 2 * H, 0);
+  int ok = 1;
+  cudaIpcMemHandle_t hr, hz;
+  if (cudaIpcGetMemHandle(&hr, c.r) != cudaSuccess || cudaIpcGetMemHandle(&hz, c.z) != cudaSuccess) ok = 0;
+  std::memcpy(mine.data(), &hr, H);
+  std::memcpy(mine.data() + H, &hz, H);
+  unsigned char* dbuf = nullptr;
+  double* flag = nullptr;
+  cudaStream_t st = nullptr;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMalloc(&dbuf, (size_t)(P + 1) * 2 * H) != cudaSuccess || cudaMalloc(&flag, sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    ok = 0;
+  }
+  bool gathered = false;
+  if (dbuf && flag && st) {
+    cudaMemcpy(dbuf + (size_t)P * 2 * H, mine.data(), 2 * H, cudaMemcpyHostToDevice);
+    gathered = n.AllGather(dbuf + (size_t)P * 2 * H, dbuf, 2 * H, ncclUint8, d->comm, st) == ncclSuccess &&
+               cudaStreamSynchronize(st) == cudaSuccess &&
+               cudaMemcpy(all.data(), dbuf, (size_t)P * 2 * H, cudaMemcpyDeviceToHost) == cudaSuccess;
+  }
+  if (!gathered) ok = 0;
+  for (int s = 0; s < 2 && ok; ++s) {
+    const int nb = me + (s ? 1 : -1);
+    if (nb < 0 || nb >= P) continue;
+    cudaIpcMemHandle_t h[2];
+    std::memcpy(&h[0], all.data() + (size_t)nb * 2 * H, H);
+    std::memcpy(&h[1], all.data() + (size_t)nb * 2 * H + H, H);
+    void* pr = nullptr;
+    void* pz = nullptr;
+    if (cudaIpcOpenMemHandle(&pr, h[0], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+        cudaIpcOpenMemHandle(&pz, h[1], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      ok = 0;
+      break;
+    }
+    c.peer_r[s] = static_cast<double*>(pr);
+    c.peer_z[s] = static_cast<double*>(pz);
+    c.peer_ipc = true;
+  }
+  // every rank must agree: min over ranks of ok (sum of failures == 0)
+  double fail_local = ok ? 0.0 : 1.0, fail_sum = 1.0;
+  if (flag && st) {
+    cudaMemcpy(flag, &fail_local, sizeof(double), cudaMemcpyHostToDevice);
+    if (n.AllReduce(flag, flag, 1, ncclDouble, ncclSum, d->comm, st) == ncclSuccess && cudaStreamSynchronize(st) == cudaSuccess)
+      cudaMemcpy(&fail_sum, flag, sizeof(double), cudaMemcpyDeviceToHost);
+  }
+  if (fail_sum != 0.0) {   // someone failed: nobody uses peer stores
+    for (int s = 0; s < 2; ++s) {
+      if (c.peer_ipc && c.peer_r[s]) cudaIpcCloseMemHandle(c.peer_r[s]);
+      if (c.peer_ipc && c.peer_z[s]) cudaIpcCloseMemHandle(c.peer_z[s]);
+      c.peer_r[s] = c.peer_z[s] = nullptr;
+    }
+    c.peer_ipc = false;
+  }
+  if (dbuf) cudaFree(dbuf);
+  if (flag) cudaFree(flag);
+  if (st) cudaStreamDestroy(st);
+  cudaGetLastError();
+}
 
 // ---- driver lifecycle ------------------------------------------------------------------------
 SlabDriver* slab_driver_create(const SlabCfg& cfg, int P, int rank, bool virt, const unsigned char* nccl_id, int* status) {
@@ -438,6 +536,15 @@ SlabDriver* slab_driver_create(const SlabCfg& cfg, int P, int rank, bool virt, c
       cudaHostAlloc(&d->param_host, sizeof(*d->param_host), cudaHostAllocDefault) != cudaSuccess)
     return fail(ECMG_ENOMEM);
   for (int i = 0; i < 4; ++i) cudaEventCreate(&d->ev[i]);
+  if (virt) {
+    for (int i = 0; i < nloc; ++i) {   // neighbours are slabs of this process
+      SlabCtx& c = d->s[i];
+      if (i > 0) { c.peer_r[0] = d->s[i - 1].r; c.peer_z[0] = d->s[i - 1].z; }
+      if (i + 1 < nloc) { c.peer_r[1] = d->s[i + 1].r; c.peer_z[1] = d->s[i + 1].z; }
+    }
+  } else {
+    exchange_ipc(d);   // best effort: without peer mappings the halo goes through ncclSend / ncclRecv
+  }
   slab_driver_configure(d, cfg);
   return d;
 }
@@ -447,10 +554,16 @@ void slab_driver_configure(SlabDriver* d, const SlabCfg& cfg) {
   for (auto& c : d->s) {
     c.geom.clear();
     c.sharded.clear();
+    c.nb_lo_zend.assign(cfg.L, 0);
+    c.nb_hi_zbeg.assign(cfg.L, 0);
     for (int k = 0; k < cfg.L; ++k) {
       bool sh;
-      c.geom.push_back(slab_geom(make_geom(cfg.dom, cfg.n0, k, cfg.prob.face, cfg.elem_path), d->P, c.rank, &sh));
+      const LevelGeom gk = make_geom(cfg.dom, cfg.n0, k, cfg.prob.face, cfg.elem_path);
+      c.geom.push_back(slab_geom(gk, d->P, c.rank, &sh));
       c.sharded.push_back(sh ? 1 : 0);
+      bool s2;   // the neighbours' level geometries follow from the same partition
+      if (c.rank > 0) c.nb_lo_zend[k] = slab_geom(gk, d->P, c.rank - 1, &s2).zend;
+      if (c.rank + 1 < d->P) c.nb_hi_zbeg[k] = slab_geom(gk, d->P, c.rank + 1, &s2).zbeg;
     }
     c.maps_level = -1;
   }
@@ -460,6 +573,11 @@ void slab_driver_destroy(SlabDriver* d) {
   if (!d) return;
   cudaDeviceSynchronize();
   for (auto& c : d->s) {
+    if (c.peer_ipc)
+      for (int s = 0; s < 2; ++s) {
+        if (c.peer_r[s]) cudaIpcCloseMemHandle(c.peer_r[s]);
+        if (c.peer_z[s]) cudaIpcCloseMemHandle(c.peer_z[s]);
+      }
     cudaFree(c.x); cudaFree(c.r); cudaFree(c.z); cudaFree(c.p[0]); cudaFree(c.p[1]); cudaFree(c.b); cudaFree(c.beta);
     cudaFree(c.partials); cudaFree(c.scratch1d); cudaFree(c.seeds); cudaFree(c.sc); cudaFree(c.ut);
     for (double* p : c.u) cudaFree(p);

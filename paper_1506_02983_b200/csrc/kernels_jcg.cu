@@ -157,6 +157,8 @@ __global__ void __launch_bounds__(NTH, 2) k_jcg_const(const LevelGeom g, const C
           acc1 = __fma_rn(rn, rn, acc1);
           a.o0[off] = xn;
           a.o1[off] = rn;
+          if (z == g.zbeg && a.peer_lo) a.peer_lo[own_off[j]] = rn;      // fused halo exchange
+          if (z == g.zend - 1 && a.peer_hi) a.peer_hi[own_off[j]] = rn;
         } else if (MODE == MODE_INIT) {
           acc2 = __fma_rn(ii0[j], ii0[j], acc2);
           const double rn = ii0[j] - ap;
@@ -164,6 +166,8 @@ __global__ void __launch_bounds__(NTH, 2) k_jcg_const(const LevelGeom g, const C
           acc0 = __fma_rn(rn, zz, acc0);
           acc1 = __fma_rn(rn, rn, acc1);
           a.o0[off] = rn;
+          if (z == g.zbeg && a.peer_lo) a.peer_lo[own_off[j]] = rn;      // fused halo exchange
+          if (z == g.zend - 1 && a.peer_hi) a.peer_hi[own_off[j]] = rn;
         } else if (MODE == MODE_TRUE) {
           const double rn = ii0[j] - ap;
           acc1 = __fma_rn(rn, rn, acc1);
@@ -177,6 +181,7 @@ __global__ void __launch_bounds__(NTH, 2) k_jcg_const(const LevelGeom g, const C
       pp[j] = cc;
     }
   }
+  if ((MODE == MODE_K2 || MODE == MODE_INIT) && (a.peer_lo || a.peer_hi)) __threadfence_system();   // peer stores
   if (MODE != MODE_APPLY) reduce_finalize(MODE, a, acc0, acc1, acc2);
 }
 

@@ -336,6 +336,8 @@ __global__ void __launch_bounds__(NTH, ELEM_MINB)
           a.o0[off] = xn;
           a.o1[off] = rn;
           a.o2[off] = zz;
+          if (d == g.zbeg && a.peer_lo) a.peer_lo[own_off[j]] = zz;      // fused halo exchange (z)
+          if (d == g.zend - 1 && a.peer_hi) a.peer_hi[own_off[j]] = zz;
         } else if (MODE == MODE_INIT) {
           const double dinv = es.precond ? (diag > 0.0 ? __drcp_rn(diag) : 0.0) : 1.0;
           const double bv = I0[io];
@@ -346,6 +348,8 @@ __global__ void __launch_bounds__(NTH, ELEM_MINB)
           acc1 = __fma_rn(rn, rn, acc1);
           a.o0[off] = rn;
           a.o1[off] = zz;
+          if (d == g.zbeg && a.peer_lo) a.peer_lo[own_off[j]] = zz;      // fused halo exchange (z)
+          if (d == g.zend - 1 && a.peer_hi) a.peer_hi[own_off[j]] = zz;
         } else if (MODE == MODE_TRUE) {
           const double rn = I0[io] - ap;
           acc1 = __fma_rn(rn, rn, acc1);
@@ -365,6 +369,7 @@ __global__ void __launch_bounds__(NTH, ELEM_MINB)
     if (s + 1 < nsteps) step(s + 1, wA, wB);
   }
   }
+  if ((MODE == MODE_K2 || MODE == MODE_INIT) && (a.peer_lo || a.peer_hi)) __threadfence_system();   // peer stores
   if (MODE != MODE_APPLY) reduce_finalize(MODE, a, acc0, acc1, acc2);
 #undef k0
 #undef k1

@@ -200,6 +200,8 @@ __global__ void __launch_bounds__(NTH, 2)
           acc1 = __fma_rn(rn, rn, acc1);
           a.o0[off] = xn;
           a.o1[off] = rn;
+          if (z == g.zbeg && a.peer_lo) a.peer_lo[own_off[j]] = rn;      // fused halo exchange
+          if (z == g.zend - 1 && a.peer_hi) a.peer_hi[own_off[j]] = rn;
         } else if (MODE == MODE_INIT) {
           acc2 = __fma_rn(I0[io], I0[io], acc2);
           const double rn = I0[io] - ap;
@@ -207,6 +209,8 @@ __global__ void __launch_bounds__(NTH, 2)
           acc0 = __fma_rn(rn, zz, acc0);
           acc1 = __fma_rn(rn, rn, acc1);
           a.o0[off] = rn;
+          if (z == g.zbeg && a.peer_lo) a.peer_lo[own_off[j]] = rn;      // fused halo exchange
+          if (z == g.zend - 1 && a.peer_hi) a.peer_hi[own_off[j]] = rn;
         } else if (MODE == MODE_TRUE) {
           const double rn = I0[io] - ap;
           acc1 = __fma_rn(rn, rn, acc1);
@@ -220,6 +224,7 @@ __global__ void __launch_bounds__(NTH, 2)
       pp[j] = cc;
     }
   }
+  if ((MODE == MODE_K2 || MODE == MODE_INIT) && (a.peer_lo || a.peer_hi)) __threadfence_system();   // peer stores
   if (MODE != MODE_APPLY) reduce_finalize(MODE, a, acc0, acc1, acc2);
 }
 

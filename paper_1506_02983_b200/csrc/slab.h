@@ -11,6 +11,7 @@ struct SlabCfg {
   int L;
   Problem prob;
   int elem_path, exp_variant, precond, kernel_variant, zchunk;
+  int fused_halo;   // 1: K2 / init store their boundary planes into the neighbours' halo planes
 };
 
 struct SlabDriver;

@@ -98,3 +98,22 @@ print(json.dumps(dict(st=[st1, stn], it1=[s["iterations"] for s in s1], itn=[s["
     assert r["st"] == [0, 0]
     assert r["it1"] == r["itn"]
     assert r["d"] <= 1e-13
+
+
+@pytest.mark.parametrize("pid,levels,eps,P", [(o.C2, 5, 1e-10, 2), (o.C3, 5, 1e-10, 2), (o.C5, 6, 1e-8, 4),
+                                              (o.C4, 6, 1e-9, 8)])
+def test_fused_halo_equals_copied_halo(pid, levels, eps, P):
+    # ECMG_OPT_FUSED_HALO: the K2 / init passes store their boundary planes straight into the neighbour
+    # slabs' halo planes (the kernel code the NCCL ranks run over CUDA-IPC peer memory) instead of a
+    # copy after the pass; the halo values are the same, so every iterate is bitwise identical
+    res = []
+    for fused in (0, 1):
+        g = Grid(4, levels, pid, params_for(pid))
+        g.set_option(ecmg.OPT_VIRTUAL_SLABS, P)
+        g.set_option(ecmg.OPT_FUSED_HALO, fused)
+        u, ut = g.new_vec(levels - 1), g.new_vec(levels - 1)
+        st, stats = g.run(eps, u, ut)
+        assert st == 0
+        res.append(([s["iterations"] for s in stats], host(u), host(ut)))
+    assert res[0][0] == res[1][0]
+    assert np.array_equal(res[0][1], res[1][1]) and np.array_equal(res[0][2], res[1][2])
