@@ -435,8 +435,12 @@ cudaError_t launch_rhs(const LevelGeom& g, const Problem& pb, const ElemStencil&
     count_launch();
     k_rhs_sep<<<g2, 128, 0, st>>>(g, pb, scratch, stride, b);
   } else {
-    const int zc = 32;
-    dim3 grid((g.nf[0] + VX - 1) / VX, (g.nf[1] + VY - 1) / VY, (g.zend - g.zbeg + zc - 1) / zc);
+    // element planes per CTA: 32 on large levels (a chunk re-evaluates one element plane), shorter on
+    // small ones so that the grid has ~1000 CTAs instead of a few long serial chains
+    const long long tiles = (long long)((g.nf[0] + VX - 1) / VX) * ((g.nf[1] + VY - 1) / VY);
+    const int nz = g.zend - g.zbeg;
+    const int zc = (int)std::max(4LL, std::min(32LL, tiles * nz / 1000));
+    dim3 grid((g.nf[0] + VX - 1) / VX, (g.nf[1] + VY - 1) / VY, (nz + zc - 1) / zc);
     count_launch();
     if (pb.id == 4) {
       RhsC4Consts k;
