@@ -24,7 +24,7 @@ LIB = os.path.join(HERE, "liboracle.so")
 # problem ids / face kinds (interface numbers; the CUDA registry declares the same ids itself)
 C1, C2, C3, C4, C5 = 1, 2, 3, 4, 5
 P1, P2, P3 = 11, 12, 13
-PATCH_TRILINEAR, PATCH_LAYERED, PATCH_ROBIN, CONST_F = 21, 22, 23, 24
+PATCH_TRILINEAR, PATCH_LAYERED, PATCH_ROBIN, CONST_F, PATCH_ROBIN_XY = 21, 22, 23, 24, 25
 DIRICHLET, ROBIN = 0, 1
 
 NSTAT = 17
@@ -107,6 +107,8 @@ def default_faces(problem_id: int):
         f[1] = f[3] = f[5] = ROBIN
     elif problem_id == P2:
         f[1] = f[3] = ROBIN
+    elif problem_id == PATCH_ROBIN_XY:
+        f[0] = f[1] = f[2] = f[3] = ROBIN
     return f
 
 

@@ -53,6 +53,7 @@ enum {
   PROB_C1 = 1, PROB_C2 = 2, PROB_C3 = 3, PROB_C4 = 4, PROB_C5 = 5,
   PROB_P1 = 11, PROB_P2 = 12, PROB_P3 = 13,
   PROB_PATCH_TRILINEAR = 21, PROB_PATCH_LAYERED = 22, PROB_PATCH_ROBIN = 23, PROB_CONST_F = 24,
+  PROB_PATCH_ROBIN_XY = 25,
 };
 
 const double PI = 3.14159265358979323846;
@@ -101,7 +102,7 @@ struct Problem {
       case PROB_P3: { double r2 = x * x + y * y + z * z; if (r2 == 0.0) return 0.0; return x * y * z / std::pow(r2, 0.75); }
       case PROB_PATCH_TRILINEAR: return 1.0 + x + 2.0 * y - z + x * y + 3.0 * x * y * z;
       case PROB_PATCH_LAYERED: return 0.5 + 1.5 * x - 0.75 * y;
-      case PROB_PATCH_ROBIN: return 0.3 + 0.7 * x - 0.4 * y + 0.9 * z;
+      case PROB_PATCH_ROBIN: case PROB_PATCH_ROBIN_XY: return 0.3 + 0.7 * x - 0.4 * y + 0.9 * z;
       default: return 0.0;
     }
   }
@@ -148,9 +149,12 @@ struct Problem {
   double gD(double x, double y, double z) const { return exact(x, y, z); }
 
   double alpha(int face_id) const {
-    (void)face_id;
     switch (id) {
       case PROB_C3: case PROB_PATCH_ROBIN: return 1.0;
+      case PROB_PATCH_ROBIN_XY: {   // Robin on x-, x+, y-, y+ with a different alpha each
+        const double a[6] = {2.0, 0.5, 1.5, 3.0, 0.0, 0.0};
+        return a[face_id];
+      }
       default: return 0.0;  // P1, P2: Neumann = Robin with alpha = 0
     }
   }
@@ -160,6 +164,10 @@ struct Problem {
     switch (id) {
       case PROB_C3: return (alpha(face_id) + beta(x, y, z)) * exact(x, y, z);  // du/dz = u, n = +z
       case PROB_PATCH_ROBIN: return alpha(face_id) * exact(x, y, z) + 1.0 * 0.9;
+      case PROB_PATCH_ROBIN_XY: {   // beta du/dn with grad u = (0.7, -0.4, 0.9) and the outward normal
+        const double dudn[6] = {-0.7, 0.7, 0.4, -0.4, -0.9, 0.9};
+        return alpha(face_id) * exact(x, y, z) + dudn[face_id];
+      }
       default: return 0.0;  // P1, P2: homogeneous Neumann
     }
   }
@@ -174,6 +182,8 @@ bool make_problem(int id, const double* params, int nparams, const int* face_in,
       P->has_exact = true; break;
     case PROB_C3: case PROB_PATCH_ROBIN:
       P->has_exact = true; P->face[5] = FACE_ROBIN; break;
+    case PROB_PATCH_ROBIN_XY:
+      P->has_exact = true; P->face[0] = P->face[1] = P->face[2] = P->face[3] = FACE_ROBIN; break;
     case PROB_P1:
       P->has_exact = true; P->face[1] = P->face[3] = P->face[5] = FACE_ROBIN; break;
     case PROB_P2:

@@ -145,6 +145,10 @@ inline bool problem_faces(int id, int face[6], double alpha[6], int* nparams_req
   switch (id) {
     case 1: case 2: case 4: case 13: case 21: case 24: break;
     case 3: case 23: face[ZP] = FACE_ROBIN; alpha[ZP] = 1.0; break;
+    case 25:   // Robin patch on the four side faces, a different alpha on each (face indexing pin)
+      face[XM] = face[XP] = face[YM] = face[YP] = FACE_ROBIN;
+      alpha[XM] = 2.0; alpha[XP] = 0.5; alpha[YM] = 1.5; alpha[YP] = 3.0;
+      break;
     case 11: face[XP] = face[YP] = face[ZP] = FACE_ROBIN; break;   // Neumann (alpha = 0)
     case 12: face[XP] = face[YP] = FACE_ROBIN; break;
     case 5: *nparams_required = 48; break;

@@ -52,7 +52,7 @@ constexpr int VSMEM = (VNE * 8 + 2 * VNE * 8) * (int)sizeof(double);
 constexpr int kMaxSepRank = 5;
 __host__ __device__ inline int prob_sep_rank(int id) {
   switch (id) {
-    case 1: case 2: case 5: case 11: case 12: case 21: case 22: case 23: case 24: return 1;
+    case 1: case 2: case 5: case 11: case 12: case 21: case 22: case 23: case 24: case 25: return 1;
     case 3: return 5;
     default: return 0;
   }

@@ -44,7 +44,7 @@ __host__ __device__ inline double prob_exact(const Problem& P, double x, double 
     case 13: { double r2 = x * x + y * y + z * z; if (r2 == 0.0) return 0.0; return x * y * z / (sqrt(r2) * sqrt(sqrt(r2))); }
     case 21: return 1.0 + x + 2.0 * y - z + x * y + 3.0 * x * y * z;
     case 22: return 0.5 + 1.5 * x - 0.75 * y;
-    case 23: return 0.3 + 0.7 * x - 0.4 * y + 0.9 * z;
+    case 23: case 25: return 0.3 + 0.7 * x - 0.4 * y + 0.9 * z;
     default: return 0.0;
   }
 }
@@ -100,6 +100,10 @@ __host__ __device__ inline double prob_gR(const Problem& P, int face, double x, 
   switch (P.id) {
     case 3: return (P.alpha[face] + prob_beta(P, x, y, z)) * prob_exact(P, x, y, z);  // du/dz = u on z = 1
     case 23: return P.alpha[face] * prob_exact(P, x, y, z) + 0.9;
+    case 25: {   // Robin on the four side faces: alpha_F u + du/dn_F, grad u = (0.7, -0.4, 0.9)
+      const double dudn[6] = {-0.7, 0.7, 0.4, -0.4, -0.9, 0.9};
+      return P.alpha[face] * prob_exact(P, x, y, z) + dudn[face];
+    }
     default: return 0.0;  // P1, P2: homogeneous Neumann
   }
 }

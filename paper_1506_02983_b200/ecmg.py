@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(HERE, "libecmg.so")
 OK, EINVAL, ENOMEM, ENOTCONV, EBREAKDOWN, EDIAG, EMISMATCH, ECUDA, ENCCL = 0, -1, -2, -3, -4, -5, -6, -7, -8
 DIRICHLET, ROBIN = 0, 1
 PROB = dict(C1=1, C2=2, C3=3, C4=4, C5=5, P1=11, P2=12, P3=13,
-            PATCH_TRILINEAR=21, PATCH_LAYERED=22, PATCH_ROBIN=23, CONST_F=24)
+            PATCH_TRILINEAR=21, PATCH_LAYERED=22, PATCH_ROBIN=23, CONST_F=24, PATCH_ROBIN_XY=25)
 OPT_EXP_VARIANT, OPT_PRECOND, OPT_ZCHUNK, OPT_KERNEL, OPT_GRAPH, OPT_VIRTUAL_SLABS, OPT_PERSISTENT, OPT_PDL = 1, 2, 3, 4, 5, 6, 7, 8
 OPT_FUSED_HALO = 9
 
@@ -229,6 +229,8 @@ def default_faces(problem_id: int):
         f[1] = f[3] = f[5] = ROBIN
     elif problem_id == PROB["P2"]:
         f[1] = f[3] = ROBIN
+    elif problem_id == PROB["PATCH_ROBIN_XY"]:
+        f[0] = f[1] = f[2] = f[3] = ROBIN
     return f
 
 

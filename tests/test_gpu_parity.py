@@ -46,7 +46,7 @@ def free_box(L):
 # PATCH_LAYERED, PATCH_ROBIN. Free boxes of 15, 31, 63 (ragged 32-wide tiles), box cells for P2.
 OPERATORS = [(o.C1, 4, 2), (o.C2, 4, 4), (o.C4, 4, 4), (o.PATCH_TRILINEAR, 4, 3),
              (o.C3, 4, 2), (o.C3, 4, 4), (o.C5, 4, 4), (o.P1, 4, 3), (o.P2, (10, 4, 5), 2),
-             (o.PATCH_LAYERED, 4, 3), (o.PATCH_ROBIN, 4, 3)]
+             (o.PATCH_LAYERED, 4, 3), (o.PATCH_ROBIN, 4, 3), (o.PATCH_ROBIN_XY, 4, 3), (o.PATCH_ROBIN_XY, 4, 4)]
 
 
 @pytest.mark.parametrize("pid,n0,level", OPERATORS)
@@ -139,7 +139,7 @@ def test_fixed_iterations(pid, k):
 
 
 @pytest.mark.parametrize("pid,eps", [(o.C1, 1e-8), (o.C2, 1e-10), (o.C3, 1e-10), (o.C4, 1e-9), (o.C5, 1e-8),
-                                     (o.P1, 1e-9), (o.P3, 1e-11)])
+                                     (o.P1, 1e-9), (o.P3, 1e-11), (o.PATCH_ROBIN_XY, 1e-10)])
 def test_tolerance_stopped_solve(pid, eps):
     level = 3
     g = Grid(4, level + 1, pid, params_for(pid))
@@ -263,7 +263,7 @@ def test_graph_loop_equals_host_loop(pid, eps):
 
 
 @pytest.mark.parametrize("pid,eps", [(o.C1, 1e-8), (o.C2, 1e-10), (o.C4, 1e-9), (o.C3, 1e-10), (o.C5, 1e-8),
-                                     (o.P1, 1e-9)])
+                                     (o.P1, 1e-9), (o.PATCH_ROBIN_XY, 1e-10)])
 def test_persistent_small_levels_vs_graph(pid, eps):
     # small levels run in one cooperative launch (ECMG_OPT_PERSISTENT; constant stencil and element
     # beta + Robin / Neumann faces); the z-marching graph path is the reference: same counts (+-1),
@@ -307,3 +307,17 @@ def test_pdl_launch_bitwise(pid, eps):
         res.append(([s["iterations"] for s in stats], host(u)))
     assert res[0][0] == res[1][0]
     assert np.array_equal(res[0][1], res[1][1])
+
+
+@pytest.mark.parametrize("persistent", [0, 300000])
+def test_robin_side_faces_patch_exact(persistent):
+    # Galerkin exactness on the GPU: u = 0.3 + 0.7x - 0.4y + 0.9z is in the Q1 space, so with Robin data
+    # alpha_F u + du/dn on the four side faces (four different alphas; edge nodes on two Robin faces) the
+    # discrete solution is u at every node, through both JCG kernel families (z-marching / persistent)
+    g = Grid(4, 5, o.PATCH_ROBIN_XY)
+    g.set_option(ecmg.OPT_PERSISTENT, persistent)
+    u = g.new_vec(4)
+    st, stats = g.run(1e-13, u)
+    assert st == 0
+    ue = o.Level((64,) * 3, o.PATCH_ROBIN_XY).exact()
+    assert np.max(np.abs(host(u) - ue)) <= 1e-11 * np.max(np.abs(ue))

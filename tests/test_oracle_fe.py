@@ -154,6 +154,7 @@ def test_spd_small():
     (o.PATCH_TRILINEAR, None),
     (o.PATCH_LAYERED, synth.layered_only(0)),
     (o.PATCH_ROBIN, None),
+    (o.PATCH_ROBIN_XY, None),   # Robin on the four side faces, four different alphas, edges shared by two
 ])
 def test_patch_exact(pid, params):
     L = o.Level((8, 8, 8), pid, params=params)
