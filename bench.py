@@ -266,6 +266,16 @@ def main():
     torch.cuda.synchronize()
     tts_hostloop = max_over_ranks(ev_h[0].elapsed_time(ev_h[1]))
     grid.set_option(ecmg.OPT_GRAPH, 1)
+    # ablation: every level's setup in line before its solve instead of ahead on a low-priority stream
+    grid.set_option(ecmg.OPT_SETUP_AHEAD, 0)
+    grid.run(eps, u, ut)
+    ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev_s[0].record(stream)
+    grid.run(eps, u, ut)
+    ev_s[1].record(stream)
+    torch.cuda.synchronize()
+    tts_inline = max_over_ranks(ev_s[0].elapsed_time(ev_s[1]))
+    grid.set_option(ecmg.OPT_SETUP_AHEAD, 1)
     peak, peak_src = load_peaks()
     bpu = BYTES_PER_UNKNOWN_ITER_ELEM if pid in (3, 5) else BYTES_PER_UNKNOWN_ITER
     achieved = bpu * nf_j * it_j / (ms_j / 1e3) / 1e9 / ws   # per GPU
@@ -317,6 +327,7 @@ def main():
                        "iterations_per_level": [s["iterations"] for s in per_level]},
             "ecmg_tts_ms": ms_per_step,
             "ecmg_tts_ms_ablation_hostloop": tts_hostloop,
+            "ecmg_tts_ms_ablation_setup_inline": tts_inline,
             "fine_grid_jcg_in_run": {"value": fine_units / (fine_ms / 1e3), "unit": UNIT,
                                      "iterations": int(per_level[-1]["iterations"])},
             "jcg_fixed": {"value": jcg_ups, "unit": UNIT, "iterations": it_j, "ms": ms_j,

@@ -116,6 +116,12 @@ typedef enum {
                                 (another slab on this GPU, or the neighbour rank's buffer mapped with
                                 CUDA IPC over NVLink; ranks fall back to 0 together if any mapping
                                 fails); 0: halo planes by device copy / ncclSend-ncclRecv */
+  ECMG_OPT_SETUP_AHEAD = 10, /* ecmg_run / ecmg_run_fixed: 1 (default) every level's setup (element beta,
+                                lifted right-hand side, g_D on the Dirichlet nodes of u_k; row a1 depends
+                                on no solution) is enqueued up front on a low-priority internal stream and
+                                overlaps the latency-bound coarse solves, which run on a high-priority
+                                internal stream (both forked from and joined back into the grid's stream);
+                                0: each level's setup runs in line before its solve */
   ECMG_OPT_VIRTUAL_SLABS = 6 /* P in 2..16: run the z-slab decomposition with P slabs on this one GPU
                                 (device copies stand in for the NCCL halo messages, an in-order sum
                                 kernel for the allreduce; the multi-GPU test fixture); 0 or 1: off */

@@ -42,18 +42,23 @@ struct ecmg_grid {
   double* x = nullptr;
   double* r = nullptr;
   double* p[2] = {nullptr, nullptr};
-  double* b = nullptr;
+  double* b = nullptr;             // finest level's right-hand side (bl[L-1])
+  std::vector<double*> bl;         // per-level right-hand sides (setup of every level can run ahead)
+  std::vector<double*> betal;      // per-level element beta (element path)
+  std::vector<double*> s1d;        // per-level 1D Gauss load tables (separable right-hand sides)
+  std::vector<char> setup_ok;      // level k's b / beta hold the current problem's data
+  int setup_ahead = 1;             // ECMG_OPT_SETUP_AHEAD
+  cudaStream_t hi_stream = nullptr, lo_stream = nullptr;   // ecmg_run: solves (high) / level setup (low priority)
+  std::vector<cudaEvent_t> setup_ev;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   double* zv = nullptr;            // element path: z = D^-1 r (K2 / INIT write it, K1 reads it)
-  double* beta = nullptr;
   double* partials = nullptr;
   JcgScalars* sc = nullptr;
   JcgScalars* sc_host = nullptr;   // pinned, 2 slots
   std::vector<double*> u;          // per-level full nodal vectors (ecmg_run)
   double* ut_tmp = nullptr;
-  double* scratch1d = nullptr;     // 1D Gauss load tables (separable right-hand sides)
   double* seeds = nullptr;         // EXP_finite: extrapolated values on the 2h grid of the finest level
   long long vec_doubles = 0, beta_doubles = 0, partial_doubles = 0;
-  int setup_level = -1;
   cudaEvent_t ev[16];
   bool ev_init = false;
   int kernel_variant = 1;   // ECMG_OPT_KERNEL
@@ -128,7 +133,7 @@ bool ensure_maps(ecmg_grid* G, const LevelGeom& g, int level) {
   M.ok = make_vec_tensor_map(&M.xh, G->x, g, hx, hy) == 0 && make_vec_tensor_map(&M.xi, G->x, g, ix, iy) == 0 &&
          make_vec_tensor_map(&M.rh, G->r, g, hx, hy) == 0 && make_vec_tensor_map(&M.ri, G->r, g, ix, iy) == 0 &&
          make_vec_tensor_map(&M.ph[0], G->p[0], g, hx, hy) == 0 && make_vec_tensor_map(&M.ph[1], G->p[1], g, hx, hy) == 0 &&
-         make_vec_tensor_map(&M.bi, G->b, g, ix, iy) == 0;
+         make_vec_tensor_map(&M.bi, G->bl[level], g, ix, iy) == 0;
   M.level = level;
   return M.ok;
 }
@@ -145,7 +150,7 @@ const CUtensorMap* int_map(ecmg_grid* G, const double* p) {
   auto& M = G->maps;
   if (p == G->x) return &M.xi;
   if (p == G->r) return &M.ri;
-  if (p == G->b) return &M.bi;
+  if (M.level >= 0 && p == G->bl[M.level]) return &M.bi;
   return nullptr;
 }
 
@@ -173,14 +178,18 @@ cudaError_t launch_mode(ecmg_grid* G, int mode, const LevelGeom& g, const KArgs&
   return launch_jcg_const(mode, g, cs, a, G->stream);
 }
 
-int setup_level(ecmg_grid* G, int k) {
+// Level setup (row a1): element beta, lifted right-hand side b_k. Independent of every solution, so
+// ecmg_run enqueues it for all levels up front on a low-priority stream (ECMG_OPT_SETUP_AHEAD).
+int setup_level_on(ecmg_grid* G, int k, cudaStream_t st) {
   const LevelGeom& g = G->geom[k];
   const ElemStencil es = make_elem_stencil(g, G->prob, G->precond);
-  if (G->elem_path) ECMG_CUDA(launch_beta(g, G->prob, G->beta, G->stream));
-  ECMG_CUDA(launch_rhs(g, G->prob, es, 1.0, G->elem_path ? G->beta : nullptr, G->b, G->scratch1d, G->stream));
-  G->setup_level = k;
+  if (G->elem_path) ECMG_CUDA(launch_beta(g, G->prob, G->betal[k], st));
+  ECMG_CUDA(launch_rhs(g, G->prob, es, 1.0, G->elem_path ? G->betal[k] : nullptr, G->bl[k], G->s1d[k], st));
+  G->setup_ok[k] = 1;
   return ECMG_OK;
 }
+int setup_level(ecmg_grid* G, int k) { return setup_level_on(G, k, G->stream); }
+void invalidate_setup(ecmg_grid* G) { std::fill(G->setup_ok.begin(), G->setup_ok.end(), 0); }
 
 
 int stats_from(const JcgScalars& s, double eps, ecmg_stats* st) {
@@ -232,7 +241,7 @@ cudaError_t build_level_graph(ecmg_grid* G, int k, cudaGraphExec_t* out) {
   cudaGraphConditionalHandle h;
   e = cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault);
   KArgs a{};
-  a.partials = G->partials; a.sc = G->sc; a.pdl = G->pdl; a.zc = auto_zc(G->zchunk, G->elem_path, g); a.beta = G->beta;
+  a.partials = G->partials; a.sc = G->sc; a.pdl = G->pdl; a.zc = auto_zc(G->zchunk, G->elem_path, g); a.beta = G->betal[k];
   a.cond = h; a.use_cond = 1;
   const long long launches_before = ecmg_kernel_launches();
   cudaStream_t user = G->stream;
@@ -243,7 +252,7 @@ cudaError_t build_level_graph(ecmg_grid* G, int k, cudaGraphExec_t* out) {
   // init pass
   e = cudaStreamBeginCaptureToGraph(G->cap_stream, graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
   if (e != cudaSuccess) return done(e);
-  { KArgs ai = a; ai.h0 = G->x; ai.i0 = G->b; ai.o0 = G->r; ai.o1 = G->zv; e = launch_mode(G, MODE_INIT, g, ai); }
+  { KArgs ai = a; ai.h0 = G->x; ai.i0 = G->bl[k]; ai.o0 = G->r; ai.o1 = G->zv; e = launch_mode(G, MODE_INIT, g, ai); }
   cudaError_t e2 = cudaStreamEndCapture(G->cap_stream, &graph);
   if (e != cudaSuccess || e2 != cudaSuccess) return done(e != cudaSuccess ? e : e2);
   size_t nn = 1;
@@ -274,7 +283,7 @@ cudaError_t build_level_graph(ecmg_grid* G, int k, cudaGraphExec_t* out) {
   // true residual after the loop
   e = cudaStreamBeginCaptureToGraph(G->cap_stream, graph, &cond_node, nullptr, 1, cudaStreamCaptureModeThreadLocal);
   if (e != cudaSuccess) return done(e);
-  { KArgs at = a; at.use_cond = 0; at.h0 = G->x; at.i0 = G->b; e = launch_mode(G, MODE_TRUE, g, at); }
+  { KArgs at = a; at.use_cond = 0; at.h0 = G->x; at.i0 = G->bl[k]; e = launch_mode(G, MODE_TRUE, g, at); }
   e2 = cudaStreamEndCapture(G->cap_stream, &graph);
   if (e != cudaSuccess || e2 != cudaSuccess) return done(e != cudaSuccess ? e : e2);
   e = cudaGraphInstantiate(out, graph, 0);
@@ -308,6 +317,7 @@ bool use_persistent(const ecmg_grid* G, const LevelGeom& g) {
 
 // the whole solve of a small level in one cooperative launch (kernels_jcg_persistent.cu)
 cudaError_t launch_persistent(ecmg_grid* G, const LevelGeom& g) {
+  const int k = level_of(G, g);
   const ConstStencil cs = make_const_stencil(g, 1.0, G->precond);
   // w = A p (and on the element path D^-1) in scratch vectors sized for the level (grown on demand)
   const long long need = g.S * g.nza + 64;
@@ -322,10 +332,10 @@ cudaError_t launch_persistent(ecmg_grid* G, const LevelGeom& g) {
     G->aux_doubles = need;
   }
   if (!G->elem_path)
-    return launch_jcg_persistent(g, cs, nullptr, G->x, G->r, nullptr, G->p[0], G->p[1], G->aux[0], nullptr, nullptr, G->b,
+    return launch_jcg_persistent(g, cs, nullptr, G->x, G->r, nullptr, G->p[0], G->p[1], G->aux[0], nullptr, nullptr, G->bl[k],
                                  G->partials, G->sc, G->stream);
   const ElemStencil es = make_elem_stencil(g, G->prob, G->precond);
-  return launch_jcg_persistent(g, cs, &es, G->x, G->r, G->zv, G->p[0], G->p[1], G->aux[0], G->aux[1], G->beta, G->b,
+  return launch_jcg_persistent(g, cs, &es, G->x, G->r, G->zv, G->p[0], G->p[1], G->aux[0], G->aux[1], G->betal[k], G->bl[k],
                                G->partials, G->sc, G->stream);
 }
 
@@ -365,7 +375,7 @@ int enqueue_jcg(ecmg_grid* G, int k, double eps, int max_iter, double* u_out, Pa
   return ECMG_OK;
 }
 
-// JCG on the level whose RHS is in G->b, starting from G->x. Fills stats (except timings). The true
+// JCG on level k (right-hand side in G->bl[k]), starting from G->x. Fills stats (except timings). The true
 // residual pass writes the solution into the free nodes of the full-layout vector u_out (if not null).
 int run_jcg(ecmg_grid* G, int k, double eps, int max_iter, double* u_out, ecmg_stats* st) {
   const LevelGeom& g = G->geom[k];
@@ -376,7 +386,7 @@ int run_jcg(ecmg_grid* G, int k, double eps, int max_iter, double* u_out, ecmg_s
   a.sc = G->sc;
   a.pdl = G->pdl;
   a.zc = auto_zc(G->zchunk, G->elem_path, g);
-  a.beta = G->beta;
+  a.beta = G->betal[k];
   // eps and max_iter reach the init pass through the device scalars
   G->param_host->eps = eps;
   G->param_host->max_iter = max_iter;
@@ -387,7 +397,7 @@ int run_jcg(ecmg_grid* G, int k, double eps, int max_iter, double* u_out, ecmg_s
   // r = b - A x, rho = r.z, rr = r.r, stop test
   {
     KArgs ai = a;
-    ai.h0 = G->x; ai.i0 = G->b; ai.o0 = G->r; ai.o1 = G->zv;
+    ai.h0 = G->x; ai.i0 = G->bl[k]; ai.o0 = G->r; ai.o1 = G->zv;
     ECMG_CUDA(launch_mode(G, MODE_INIT, g, ai));
   }
   long long it = 0;
@@ -431,7 +441,7 @@ int run_jcg(ecmg_grid* G, int k, double eps, int max_iter, double* u_out, ecmg_s
   // true residual RRe = ||b - A x|| / ||b||
   {
     KArgs at = a;
-    at.h0 = G->x; at.i0 = G->b;
+    at.h0 = G->x; at.i0 = G->bl[k];
     ECMG_CUDA(launch_mode(G, MODE_TRUE, g, at));
   }
   ECMG_CUDA(cudaMemcpyAsync(&G->sc_host[0], G->sc, sizeof(JcgScalars), cudaMemcpyDeviceToHost, G->stream));
@@ -525,16 +535,37 @@ int ecmg_create_grid(const ecmg_box* dom, const int coarsest_cells[3], int num_l
   alloc(&G->r, G->vec_doubles);
   alloc(&G->p[0], G->vec_doubles);
   alloc(&G->p[1], G->vec_doubles);
-  alloc(&G->b, G->vec_doubles);
   alloc(&G->partials, G->partial_doubles);
-  alloc(&G->scratch1d, 15LL * (   // 1D Gauss loads: up to 5 separable terms x 3 axes
-      std::max(gmax.n[0], std::max(gmax.n[1], gmax.n[2])) + 1));
+  // per-level right-hand sides and 1D load tables (the finest level's b is the full-size G->b)
+  G->bl.assign(num_levels, nullptr);
+  G->betal.assign(num_levels, nullptr);
+  G->s1d.assign(num_levels, nullptr);
+  G->setup_ok.assign(num_levels, 0);
+  for (int k = 0; k < num_levels; ++k) {
+    const LevelGeom gk = make_geom(*dom, coarsest_cells, std::min(k, size_level), face_none, 1);
+    alloc(&G->bl[k], k == num_levels - 1 ? G->vec_doubles : gk.S * gk.nf[2] + 64);
+    alloc(&G->s1d[k], 15LL * (   // 1D Gauss loads: up to 5 separable terms x 3 axes
+        std::max(gk.n[0], std::max(gk.n[1], gk.n[2])) + 1));
+  }
+  G->b = G->bl[num_levels - 1];
   alloc(&G->seeds, (long long)(gmax.n[0] / 2 + 1) * (gmax.n[1] / 2 + 1) * (gmax.n[2] / 2 + 1));
   if (st == ECMG_OK && cudaMalloc(&G->sc, sizeof(JcgScalars)) != cudaSuccess) st = ECMG_ENOMEM;
   if (st == ECMG_OK && cudaMemsetAsync(G->sc, 0, sizeof(JcgScalars), G->stream) != cudaSuccess) st = ECMG_ECUDA;
   if (st == ECMG_OK && cudaHostAlloc(&G->sc_host, 2 * sizeof(JcgScalars), cudaHostAllocDefault) != cudaSuccess) st = ECMG_ENOMEM;
   if (st == ECMG_OK && cudaHostAlloc(&G->param_host, sizeof(*G->param_host), cudaHostAllocDefault) != cudaSuccess) st = ECMG_ENOMEM;
   if (st == ECMG_OK && cudaStreamCreateWithFlags(&G->cap_stream, cudaStreamNonBlocking) != cudaSuccess) st = ECMG_ECUDA;
+  if (st == ECMG_OK) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);   // lo = least priority, hi = greatest
+    if (cudaStreamCreateWithPriority(&G->hi_stream, cudaStreamNonBlocking, hi) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&G->lo_stream, cudaStreamNonBlocking, lo) != cudaSuccess ||
+        cudaEventCreateWithFlags(&G->fork_ev, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&G->join_ev, cudaEventDisableTiming) != cudaSuccess)
+      st = ECMG_ECUDA;
+    G->setup_ev.assign(num_levels, nullptr);
+    for (auto& e : G->setup_ev)
+      if (st == ECMG_OK && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) st = ECMG_ECUDA;
+  }
   G->graphs.assign(num_levels, nullptr);
   if (st == ECMG_OK && cudaHostAlloc(&G->lvl_param, sizeof(ParamHost) * num_levels, cudaHostAllocDefault) != cudaSuccess) st = ECMG_ENOMEM;
   if (st == ECMG_OK && cudaHostAlloc(&G->lvl_sc, sizeof(JcgScalars) * num_levels, cudaHostAllocDefault) != cudaSuccess) st = ECMG_ENOMEM;
@@ -576,11 +607,18 @@ int ecmg_destroy_grid(ecmg_grid* G) {
   if (!G) return ECMG_EINVAL;
   if (G->stream) cudaStreamSynchronize(G->stream); else cudaDeviceSynchronize();
   if (G->slab) slab_driver_destroy(G->slab);
-  cudaFree(G->x); cudaFree(G->r); cudaFree(G->p[0]); cudaFree(G->p[1]); cudaFree(G->b);
-  cudaFree(G->beta); cudaFree(G->zv); cudaFree(G->aux[0]); cudaFree(G->aux[1]); cudaFree(G->partials); cudaFree(G->sc);
+  cudaFree(G->x); cudaFree(G->r); cudaFree(G->p[0]); cudaFree(G->p[1]);
+  for (double* p : G->bl) cudaFree(p);
+  for (double* p : G->betal) cudaFree(p);
+  for (double* p : G->s1d) cudaFree(p);
+  cudaFree(G->zv); cudaFree(G->aux[0]); cudaFree(G->aux[1]); cudaFree(G->partials); cudaFree(G->sc);
   for (double* p : G->u) cudaFree(p);
   cudaFree(G->ut_tmp);
-  cudaFree(G->scratch1d);
+  for (auto& e : G->setup_ev) if (e) cudaEventDestroy(e);
+  if (G->fork_ev) cudaEventDestroy(G->fork_ev);
+  if (G->join_ev) cudaEventDestroy(G->join_ev);
+  if (G->hi_stream) cudaStreamDestroy(G->hi_stream);
+  if (G->lo_stream) cudaStreamDestroy(G->lo_stream);
   cudaFree(G->seeds);
   if (G->sc_host) cudaFreeHost(G->sc_host);
   if (G->param_host) cudaFreeHost(G->param_host);
@@ -617,8 +655,13 @@ int ecmg_set_coeffs(ecmg_grid* G, const ecmg_problem* pr) {
   bool all_dir = true;
   for (int f = 0; f < 6; ++f) all_dir = all_dir && pb.face[f] == FACE_DIRICHLET;
   const int elem_path = !(prob_beta_is_one(pb.id) && all_dir);
-  if (elem_path && !G->beta) {
-    if (cudaMalloc(&G->beta, sizeof(double) * G->beta_doubles) != cudaSuccess) { cudaGetLastError(); return ECMG_ENOMEM; }
+  if (elem_path && !G->betal.back()) {
+    const int size_level = G->nranks > 1 ? 0 : G->L - 1;
+    int face_none[6] = {FACE_ROBIN, FACE_ROBIN, FACE_ROBIN, FACE_ROBIN, FACE_ROBIN, FACE_ROBIN};
+    for (int k = 0; k < G->L; ++k) {
+      const LevelGeom gk = make_geom(G->dom, G->n0, std::min(k, size_level), face_none, 1);
+      if (cudaMalloc(&G->betal[k], sizeof(double) * beta_doubles(gk)) != cudaSuccess) { cudaGetLastError(); return ECMG_ENOMEM; }
+    }
   }
   if (elem_path && !G->zv) {
     if (cudaMalloc(&G->zv, sizeof(double) * G->vec_doubles) != cudaSuccess) { cudaGetLastError(); return ECMG_ENOMEM; }
@@ -629,7 +672,7 @@ int ecmg_set_coeffs(ecmg_grid* G, const ecmg_problem* pr) {
   G->geom.clear();
   for (int k = 0; k < G->L; ++k) G->geom.push_back(make_geom(G->dom, G->n0, k, pb.face, elem_path));
   G->has_problem = true;
-  G->setup_level = -1;
+  invalidate_setup(G);
   G->maps.level = -1;
   clear_graphs(G);
   if (G->slab) slab_driver_configure(G->slab, slab_cfg(G));
@@ -640,7 +683,8 @@ int ecmg_set_option(ecmg_grid* G, int option, int value) {
   if (!G) return ECMG_EINVAL;
   switch (option) {
     case ECMG_OPT_EXP_VARIANT: if (value != 0 && value != 1) return ECMG_EINVAL; G->exp_variant = value; break;
-    case ECMG_OPT_PRECOND: if (value != 0 && value != 1) return ECMG_EINVAL; G->precond = value; G->setup_level = -1; clear_graphs(G); break;
+    case ECMG_OPT_PRECOND: if (value != 0 && value != 1) return ECMG_EINVAL; G->precond = value; invalidate_setup(G); clear_graphs(G); break;
+    case ECMG_OPT_SETUP_AHEAD: if (value != 0 && value != 1) return ECMG_EINVAL; G->setup_ahead = value; break;
     case ECMG_OPT_ZCHUNK: if (value < 0) return ECMG_EINVAL; G->zchunk = value; clear_graphs(G); break;
     case ECMG_OPT_KERNEL: if (value != 0 && value != 1) return ECMG_EINVAL; G->kernel_variant = value; clear_graphs(G); break;
     case ECMG_OPT_GRAPH: if (value != 0 && value != 1) return ECMG_EINVAL; G->use_graph = value; break;
@@ -687,7 +731,7 @@ int ecmg_solve_level(ecmg_grid* G, int level, double eps, int max_iter, double* 
   }
   const LevelGeom& g = G->geom[level];
   ECMG_CUDA(cudaEventRecord(G->ev[4], G->stream));
-  if (G->setup_level != level) { int s = setup_level(G, level); if (s) return s; }
+  if (!G->setup_ok[level]) { int s = setup_level(G, level); if (s) return s; }
   ECMG_CUDA(cudaEventRecord(G->ev[5], G->stream));
   ECMG_CUDA(launch_gather(g, u, G->x, G->stream));
   const int st = run_jcg(G, level, eps, max_iter, u, stats);   // the true-residual pass fills u's free nodes
@@ -724,10 +768,10 @@ int ecmg_richardson(ecmg_grid* G, int level, const double* uh, const double* u2h
 int ecmg_apply_operator(ecmg_grid* G, int level, const double* p, double* q) {
   if (!G || !p || !q || !G->has_problem || level < 0 || level >= G->L || G->nranks > 1) return ECMG_EINVAL;
   const LevelGeom& g = G->geom[level];
-  if (G->elem_path && G->setup_level != level) { int s = setup_level(G, level); if (s) return s; }
+  if (G->elem_path && !G->setup_ok[level]) { int s = setup_level(G, level); if (s) return s; }
   ECMG_CUDA(launch_gather(g, p, G->p[0], G->stream));
   KArgs a{};
-  a.partials = G->partials; a.sc = G->sc; a.pdl = G->pdl; a.zc = auto_zc(G->zchunk, G->elem_path, g); a.beta = G->beta;
+  a.partials = G->partials; a.sc = G->sc; a.pdl = G->pdl; a.zc = auto_zc(G->zchunk, G->elem_path, g); a.beta = G->betal[level];
   a.h0 = G->p[0]; a.o0 = G->r;
   ECMG_CUDA(launch_mode(G, MODE_APPLY, g, a));
   ECMG_CUDA(cudaMemsetAsync(q, 0, sizeof(double) * level_nodes(g), G->stream));
@@ -739,15 +783,15 @@ int ecmg_apply_operator(ecmg_grid* G, int level, const double* p, double* q) {
 int ecmg_level_rhs(ecmg_grid* G, int level, double* bout, double* norm_b) {
   if (!G || !bout || !G->has_problem || level < 0 || level >= G->L || G->nranks > 1) return ECMG_EINVAL;
   const LevelGeom& g = G->geom[level];
-  if (G->setup_level != level) { int s = setup_level(G, level); if (s) return s; }
+  if (!G->setup_ok[level]) { int s = setup_level(G, level); if (s) return s; }
   ECMG_CUDA(cudaMemsetAsync(bout, 0, sizeof(double) * level_nodes(g), G->stream));
-  ECMG_CUDA(launch_scatter(g, G->b, bout, G->stream));
+  ECMG_CUDA(launch_scatter(g, G->bl[level], bout, G->stream));
   // ||b||^2 is accumulated by the JCG init pass; run it at x = 0
   ECMG_CUDA(launch_zero_vec(g, G->x, G->stream));
   {
     KArgs a{};
-    a.partials = G->partials; a.sc = G->sc; a.pdl = G->pdl; a.zc = auto_zc(G->zchunk, G->elem_path, g); a.beta = G->beta;
-    a.h0 = G->x; a.i0 = G->b; a.o0 = G->r; a.o1 = G->zv;
+    a.partials = G->partials; a.sc = G->sc; a.pdl = G->pdl; a.zc = auto_zc(G->zchunk, G->elem_path, g); a.beta = G->betal[level];
+    a.h0 = G->x; a.i0 = G->bl[level]; a.o0 = G->r; a.o1 = G->zv;
     ECMG_CUDA(launch_mode(G, MODE_INIT, g, a));
   }
   ECMG_CUDA(cudaMemcpyAsync(&G->sc_host[0], G->sc, sizeof(JcgScalars), cudaMemcpyDeviceToHost, G->stream));
@@ -790,13 +834,33 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
   std::vector<ecmg_stats> stv(G->L);
   std::vector<char> async(G->L, 0);
   for (auto& st : stv) std::memset(&st, 0, sizeof(st));
+  auto level_u = [&](int k) { return (k == G->L - 1 && u_dev) ? u_fine : G->u[k]; };
+  // Setup ahead (ECMG_OPT_SETUP_AHEAD): the level setups (row a1: beta, lifted b, g_D on the Dirichlet
+  // nodes of u_k) depend on no solution, so they are all enqueued up front on a low-priority stream and
+  // run under the latency-bound coarse solves, which go to a high-priority stream; level k's solve
+  // waits for its setup event only. The caller's stream forks into both and joins at the end.
+  const bool ahead = G->setup_ahead != 0;
+  cudaStream_t user = G->stream;
+  struct Restore { ecmg_grid* G; cudaStream_t s; ~Restore() { G->stream = s; } } restore{G, user};
+  if (ahead) {
+    ECMG_CUDA(cudaEventRecord(G->fork_ev, user));
+    ECMG_CUDA(cudaStreamWaitEvent(G->hi_stream, G->fork_ev, 0));
+    ECMG_CUDA(cudaStreamWaitEvent(G->lo_stream, G->fork_ev, 0));
+    for (int k = 0; k < G->L; ++k) {
+      { int s = setup_level_on(G, k, G->lo_stream); if (s) return s; }
+      ECMG_CUDA(launch_dirichlet_fill(G->geom[k], G->prob, level_u(k), 0.0, 0, G->lo_stream));
+      ECMG_CUDA(cudaEventRecord(G->setup_ev[k], G->lo_stream));
+    }
+    G->stream = G->hi_stream;
+  }
   // the whole cascade is enqueued without host synchronisation when every solve is device driven
   for (int k = 0; k < G->L; ++k) {
     const LevelGeom& g = G->geom[k];
     ecmg_stats& st = stv[k];
     cudaEvent_t* e = &G->lvl_ev[5 * k];
     ECMG_CUDA(cudaEventRecord(e[0], G->stream));
-    { int s = setup_level(G, k); if (s) return s; }
+    if (ahead) ECMG_CUDA(cudaStreamWaitEvent(G->stream, G->setup_ev[k], 0));
+    else { int s = setup_level(G, k); if (s) return s; }
     ECMG_CUDA(cudaEventRecord(e[1], G->stream));
     if (k < 2) {
       // DSOLVE (Alg. 4 l.1-2): JCG from a zero free guess to 1e-14 (reading §8c A12)
@@ -810,7 +874,7 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
     const int maxit_k = k < 2 ? 10000 : maxit_lv[k];
     // u_k: the finest level goes straight into the caller's device buffer (no copy at the end); the
     // true-residual pass of the solve writes its free nodes (fused scatter)
-    double* uk = (k == G->L - 1 && u_dev) ? u_fine : G->u[k];
+    double* uk = level_u(k);
     int s = enqueue_jcg(G, k, eps_k, maxit_k, uk, &G->lvl_param[k], &G->lvl_sc[k]);
     if (s == ECMG_OK) {
       async[k] = 1;
@@ -820,7 +884,7 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
       if (s != ECMG_OK && status == ECMG_OK) status = s;
     }
     if (s == ECMG_ECUDA || s == ECMG_ENOMEM) return s;
-    ECMG_CUDA(launch_dirichlet_fill(g, G->prob, uk, 0.0, 0, G->stream));
+    if (!ahead) ECMG_CUDA(launch_dirichlet_fill(g, G->prob, uk, 0.0, 0, G->stream));
     ECMG_CUDA(cudaEventRecord(e[3], G->stream));
     if (k >= 2 && k == G->L - 1 && ut_fine) {
       // u~_h = EXP_true(u_h, u_2h) (Alg. 4 l.10) on the finest level
@@ -832,6 +896,10 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
     ECMG_CUDA(cudaMemcpyAsync(u_fine, G->u[G->L - 1], sizeof(double) * Nf, cudaMemcpyDeviceToHost, G->stream));
   if (ut_fine && !ut_dev)
     ECMG_CUDA(cudaMemcpyAsync(ut_fine, G->ut_tmp, sizeof(double) * Nf, cudaMemcpyDeviceToHost, G->stream));
+  if (ahead) {   // join: the caller's stream continues after everything enqueued here
+    ECMG_CUDA(cudaEventRecord(G->join_ev, G->stream));
+    ECMG_CUDA(cudaStreamWaitEvent(user, G->join_ev, 0));
+  }
   ECMG_CUDA(cudaStreamSynchronize(G->stream));
   for (int k = 0; k < G->L; ++k) {
     ecmg_stats& st = stv[k];

@@ -22,6 +22,7 @@ PROB = dict(C1=1, C2=2, C3=3, C4=4, C5=5, P1=11, P2=12, P3=13,
             PATCH_TRILINEAR=21, PATCH_LAYERED=22, PATCH_ROBIN=23, CONST_F=24, PATCH_ROBIN_XY=25)
 OPT_EXP_VARIANT, OPT_PRECOND, OPT_ZCHUNK, OPT_KERNEL, OPT_GRAPH, OPT_VIRTUAL_SLABS, OPT_PERSISTENT, OPT_PDL = 1, 2, 3, 4, 5, 6, 7, 8
 OPT_FUSED_HALO = 9
+OPT_SETUP_AHEAD = 10
 
 EXPORTS = ["ecmg_create_grid", "ecmg_set_coeffs", "ecmg_set_option", "ecmg_solve_level",
            "ecmg_prolongate_extrapolate", "ecmg_richardson", "ecmg_run", "ecmg_run_fixed", "ecmg_apply_operator",

@@ -321,3 +321,24 @@ def test_robin_side_faces_patch_exact(persistent):
     assert st == 0
     ue = o.Level((64,) * 3, o.PATCH_ROBIN_XY).exact()
     assert np.max(np.abs(host(u) - ue)) <= 1e-11 * np.max(np.abs(ue))
+
+
+@pytest.mark.parametrize("pid,eps", [(o.C2, 1e-10), (o.C3, 1e-10), (o.C4, 1e-9), (o.C5, 1e-8)])
+def test_setup_ahead_bitwise(pid, eps):
+    # ECMG_OPT_SETUP_AHEAD moves every level's setup (beta, b, g_D of u_k) to a low-priority stream that
+    # runs ahead of the solves: same kernels on the same data, so iterates are bitwise identical; the
+    # caller's stream is joined (u and u~ read on torch's stream right after the call), and a second run
+    # on the same grid reuses nothing stale
+    res = []
+    for ahead in (0, 1, 1):
+        g = Grid(4, 5, pid, params_for(pid))
+        g.set_option(ecmg.OPT_SETUP_AHEAD, ahead)
+        u, ut = g.new_vec(4), g.new_vec(4)
+        for _ in range(2 if ahead else 1):
+            u.fill_(7.0)
+            st, stats = g.run(eps, u, ut)
+            assert st == 0
+        res.append(([s["iterations"] for s in stats], u.cpu().numpy(), ut.cpu().numpy()))
+    for r in res[1:]:
+        assert r[0] == res[0][0]
+        assert np.array_equal(r[1], res[0][1]) and np.array_equal(r[2], res[0][2])
