@@ -122,6 +122,14 @@ typedef enum {
                                 overlaps the latency-bound coarse solves, which run on a high-priority
                                 internal stream (both forked from and joined back into the grid's stream);
                                 0: each level's setup runs in line before its solve */
+  ECMG_OPT_EXP_KERNEL = 12,  /* EXP_finite: 1 (default) one fused pass (seeds formed per 4h layer in shared
+                                memory, fine level written once); 0: seed pass + interpolation pass
+                                (ablation; bitwise the same results) */
+  ECMG_OPT_CTA_SOLVE = 13,   /* levels with at most this many free unknowns (default 1000, at most 4096)
+                                are solved by ONE CTA with every vector in shared memory (no grid barrier);
+                                0: off (the cooperative persistent kernel takes them) */
+  ECMG_OPT_SETUP_CTAS = 11,  /* tuning: CTAs per SM of the fp64-ALU-bound volume-load kernel when it runs
+                                ahead (0 = one CTA per work item, the full grid) */
   ECMG_OPT_VIRTUAL_SLABS = 6 /* P in 2..16: run the z-slab decomposition with P slabs on this one GPU
                                 (device copies stand in for the NCCL halo messages, an in-order sum
                                 kernel for the allreduce; the multi-GPU test fixture); 0 or 1: off */

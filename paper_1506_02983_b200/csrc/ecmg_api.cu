@@ -48,7 +48,11 @@ struct ecmg_grid {
   std::vector<double*> s1d;        // per-level 1D Gauss load tables (separable right-hand sides)
   std::vector<char> setup_ok;      // level k's b / beta hold the current problem's data
   int setup_ahead = 1;             // ECMG_OPT_SETUP_AHEAD
+  int exp_fused = 1;               // ECMG_OPT_EXP_KERNEL: 1 fused one-pass EXP_finite, 0 seeds + interpolation passes
+  int setup_ctas = 0;              // ECMG_OPT_SETUP_CTAS: CTAs per SM of the ALU-bound RHS kernel when run ahead
   cudaStream_t hi_stream = nullptr, lo_stream = nullptr;   // ecmg_run: solves (high) / level setup (low priority)
+  cudaStream_t lo2_stream = nullptr;                        // the finest level's setup (starts at once, beside lo_stream)
+  int setup_ahead_prio = 1;   // the coarse levels' setups at the solves' priority (they are short and needed soon)
   std::vector<cudaEvent_t> setup_ev;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   double* zv = nullptr;            // element path: z = D^-1 r (K2 / INIT write it, K1 reads it)
@@ -66,6 +70,7 @@ struct ecmg_grid {
   int fused_halo = 1;       // ECMG_OPT_FUSED_HALO: z-slab halo planes stored by K2 / init into the neighbours
   int pdl = 0;              // ECMG_OPT_PDL: programmatic dependent launch between the JCG kernels (measured: no gain
                             // inside the CUDA graphs, tools/tune_pdl.py; off by default)
+  long long cta_max = 1000;           // ECMG_OPT_CTA_SOLVE: one-CTA solve up to this many free unknowns (0: off)
   long long persistent_max = 300000;  // ECMG_OPT_PERSISTENT: one cooperative launch per solve up to this size (tools/tune_persistent.py)
   double* aux[2] = {nullptr, nullptr};   // persistent element-path solve: w = A p and D^-1 (level-sized)
   long long aux_doubles = 0;
@@ -180,11 +185,11 @@ cudaError_t launch_mode(ecmg_grid* G, int mode, const LevelGeom& g, const KArgs&
 
 // Level setup (row a1): element beta, lifted right-hand side b_k. Independent of every solution, so
 // ecmg_run enqueues it for all levels up front on a low-priority stream (ECMG_OPT_SETUP_AHEAD).
-int setup_level_on(ecmg_grid* G, int k, cudaStream_t st) {
+int setup_level_on(ecmg_grid* G, int k, cudaStream_t st, int ctas_per_sm = 0) {
   const LevelGeom& g = G->geom[k];
   const ElemStencil es = make_elem_stencil(g, G->prob, G->precond);
   if (G->elem_path) ECMG_CUDA(launch_beta(g, G->prob, G->betal[k], st));
-  ECMG_CUDA(launch_rhs(g, G->prob, es, 1.0, G->elem_path ? G->betal[k] : nullptr, G->bl[k], G->s1d[k], st));
+  ECMG_CUDA(launch_rhs(g, G->prob, es, 1.0, G->elem_path ? G->betal[k] : nullptr, G->bl[k], G->s1d[k], st, ctas_per_sm));
   G->setup_ok[k] = 1;
   return ECMG_OK;
 }
@@ -309,7 +314,13 @@ int run_jcg_graph(ecmg_grid* G, int k, double eps, ecmg_stats* st) {
   return fill_stats(G, g, eps, st);
 }
 
+// the smallest levels: the whole solve in one CTA with every vector in shared memory
+bool use_cta(const ecmg_grid* G, const LevelGeom& g) {
+  return !G->slab && G->cta_max > 0 && cta_solve_fits(g, G->elem_path, G->cta_max);
+}
+
 bool use_persistent(const ecmg_grid* G, const LevelGeom& g) {
+  if (use_cta(G, g)) return true;
   if (G->slab || G->persistent_max <= 0 || free_count(g) > G->persistent_max) return false;
   const long long nbricks = (long long)((g.nf[0] + 7) / 8) * ((g.nf[1] + 7) / 8) * ((g.nf[2] + 3) / 4);
   return nbricks <= persistent_max_bricks(G->elem_path);   // every brick's nodes stay in registers
@@ -319,6 +330,11 @@ bool use_persistent(const ecmg_grid* G, const LevelGeom& g) {
 cudaError_t launch_persistent(ecmg_grid* G, const LevelGeom& g) {
   const int k = level_of(G, g);
   const ConstStencil cs = make_const_stencil(g, 1.0, G->precond);
+  if (use_cta(G, g)) {
+    if (!G->elem_path) return launch_jcg_cta(g, cs, nullptr, G->x, G->r, nullptr, G->bl[k], G->sc, G->stream);
+    const ElemStencil es = make_elem_stencil(g, G->prob, G->precond);
+    return launch_jcg_cta(g, cs, &es, G->x, G->r, G->betal[k], G->bl[k], G->sc, G->stream);
+  }
   // w = A p (and on the element path D^-1) in scratch vectors sized for the level (grown on demand)
   const long long need = g.S * g.nza + 64;
   if (G->aux_doubles < need) {
@@ -558,7 +574,8 @@ int ecmg_create_grid(const ecmg_box* dom, const int coarsest_cells[3], int num_l
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);   // lo = least priority, hi = greatest
     if (cudaStreamCreateWithPriority(&G->hi_stream, cudaStreamNonBlocking, hi) != cudaSuccess ||
-        cudaStreamCreateWithPriority(&G->lo_stream, cudaStreamNonBlocking, lo) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&G->lo_stream, cudaStreamNonBlocking, G->setup_ahead_prio ? hi : lo) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&G->lo2_stream, cudaStreamNonBlocking, lo) != cudaSuccess ||
         cudaEventCreateWithFlags(&G->fork_ev, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&G->join_ev, cudaEventDisableTiming) != cudaSuccess)
       st = ECMG_ECUDA;
@@ -574,7 +591,7 @@ int ecmg_create_grid(const ecmg_box* dom, const int coarsest_cells[3], int num_l
     for (auto& e : G->lvl_ev) cudaEventCreate(&e);
   }
   if (st == ECMG_OK && (init_tma_kernel_attributes() != cudaSuccess || init_elem_kernel_attributes() != cudaSuccess ||
-                        init_setup_kernel_attributes() != cudaSuccess))
+                        init_setup_kernel_attributes() != cudaSuccess || init_cta_kernel_attributes() != cudaSuccess))
     st = ECMG_ECUDA;
   if (st == ECMG_OK) {
     for (int i = 0; i < 16; ++i) cudaEventCreate(&G->ev[i]);
@@ -619,6 +636,7 @@ int ecmg_destroy_grid(ecmg_grid* G) {
   if (G->join_ev) cudaEventDestroy(G->join_ev);
   if (G->hi_stream) cudaStreamDestroy(G->hi_stream);
   if (G->lo_stream) cudaStreamDestroy(G->lo_stream);
+  if (G->lo2_stream) cudaStreamDestroy(G->lo2_stream);
   cudaFree(G->seeds);
   if (G->sc_host) cudaFreeHost(G->sc_host);
   if (G->param_host) cudaFreeHost(G->param_host);
@@ -684,11 +702,14 @@ int ecmg_set_option(ecmg_grid* G, int option, int value) {
   switch (option) {
     case ECMG_OPT_EXP_VARIANT: if (value != 0 && value != 1) return ECMG_EINVAL; G->exp_variant = value; break;
     case ECMG_OPT_PRECOND: if (value != 0 && value != 1) return ECMG_EINVAL; G->precond = value; invalidate_setup(G); clear_graphs(G); break;
-    case ECMG_OPT_SETUP_AHEAD: if (value != 0 && value != 1) return ECMG_EINVAL; G->setup_ahead = value; break;
+    case ECMG_OPT_SETUP_AHEAD: if (value < 0 || value > 3) return ECMG_EINVAL; G->setup_ahead = value; break;
+    case ECMG_OPT_EXP_KERNEL: if (value != 0 && value != 1) return ECMG_EINVAL; G->exp_fused = value; break;
+    case ECMG_OPT_SETUP_CTAS: if (value < 0) return ECMG_EINVAL; G->setup_ctas = value; break;
     case ECMG_OPT_ZCHUNK: if (value < 0) return ECMG_EINVAL; G->zchunk = value; clear_graphs(G); break;
     case ECMG_OPT_KERNEL: if (value != 0 && value != 1) return ECMG_EINVAL; G->kernel_variant = value; clear_graphs(G); break;
     case ECMG_OPT_GRAPH: if (value != 0 && value != 1) return ECMG_EINVAL; G->use_graph = value; break;
     case ECMG_OPT_PERSISTENT: if (value < 0) return ECMG_EINVAL; G->persistent_max = value; break;
+    case ECMG_OPT_CTA_SOLVE: if (value < 0) return ECMG_EINVAL; G->cta_max = value; break;
     case ECMG_OPT_PDL: if (value != 0 && value != 1) return ECMG_EINVAL; G->pdl = value; clear_graphs(G); break;
     case ECMG_OPT_FUSED_HALO: if (value != 0 && value != 1) return ECMG_EINVAL; G->fused_halo = value; break;
     case ECMG_OPT_VIRTUAL_SLABS: {
@@ -751,7 +772,7 @@ int ecmg_prolongate_extrapolate(ecmg_grid* G, int level, const double* u2h, cons
   if (!G || !u2h || !u4h || !w || !G->has_problem || level < 2 || level >= G->L || G->nranks > 1) return ECMG_EINVAL;
   const LevelGeom& g = G->geom[level];
   for (int d = 0; d < 3; ++d) if (g.n[d] % 4) return ECMG_EMISMATCH;
-  ECMG_CUDA(launch_exp_finite(g, G->prob, u2h, u4h, w, G->exp_variant, G->seeds, 0, G->stream));
+  ECMG_CUDA(launch_exp_finite(g, G->prob, u2h, u4h, w, G->exp_variant, G->seeds, 0, G->stream, G->exp_fused));
   ECMG_CUDA(cudaStreamSynchronize(G->stream));
   return ECMG_OK;
 }
@@ -846,10 +867,14 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
     ECMG_CUDA(cudaEventRecord(G->fork_ev, user));
     ECMG_CUDA(cudaStreamWaitEvent(G->hi_stream, G->fork_ev, 0));
     ECMG_CUDA(cudaStreamWaitEvent(G->lo_stream, G->fork_ev, 0));
+    ECMG_CUDA(cudaStreamWaitEvent(G->lo2_stream, G->fork_ev, 0));
+    // the finest level's setup (most of the work) on its own stream, so that it starts at once; the
+    // coarser levels' setups in level order beside it
     for (int k = 0; k < G->L; ++k) {
-      { int s = setup_level_on(G, k, G->lo_stream); if (s) return s; }
-      ECMG_CUDA(launch_dirichlet_fill(G->geom[k], G->prob, level_u(k), 0.0, 0, G->lo_stream));
-      ECMG_CUDA(cudaEventRecord(G->setup_ev[k], G->lo_stream));
+      cudaStream_t s_k = (k == G->L - 1 && G->setup_ahead != 2) ? G->lo2_stream : G->lo_stream;
+      { int s = setup_level_on(G, k, s_k, G->setup_ctas); if (s) return s; }
+      ECMG_CUDA(launch_dirichlet_fill(G->geom[k], G->prob, level_u(k), 0.0, 0, s_k));
+      ECMG_CUDA(cudaEventRecord(G->setup_ev[k], s_k));
     }
     G->stream = G->hi_stream;
   }
@@ -859,7 +884,12 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
     ecmg_stats& st = stv[k];
     cudaEvent_t* e = &G->lvl_ev[5 * k];
     ECMG_CUDA(cudaEventRecord(e[0], G->stream));
-    if (ahead) ECMG_CUDA(cudaStreamWaitEvent(G->stream, G->setup_ev[k], 0));
+    if (ahead) {
+      ECMG_CUDA(cudaStreamWaitEvent(G->stream, G->setup_ev[k], 0));
+      // mode 3: the z-marching (non-persistent) solves wait until the finest level's setup is done too,
+      // instead of sharing the SMs with it
+      if (G->setup_ahead == 3 && !use_persistent(G, g)) ECMG_CUDA(cudaStreamWaitEvent(G->stream, G->setup_ev[G->L - 1], 0));
+    }
     else { int s = setup_level(G, k); if (s) return s; }
     ECMG_CUDA(cudaEventRecord(e[1], G->stream));
     if (k < 2) {
@@ -867,7 +897,7 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
       ECMG_CUDA(launch_zero_vec(g, G->x, G->stream));
     } else {
       // W_h = EXP_finite(u_2h, u_4h) (Alg. 4 l.6), written straight into the free-box work vector
-      ECMG_CUDA(launch_exp_finite(g, G->prob, G->u[k - 1], G->u[k - 2], G->x, G->exp_variant, G->seeds, 1, G->stream));
+      ECMG_CUDA(launch_exp_finite(g, G->prob, G->u[k - 1], G->u[k - 2], G->x, G->exp_variant, G->seeds, 1, G->stream, G->exp_fused));
     }
     ECMG_CUDA(cudaEventRecord(e[2], G->stream));
     const double eps_k = k < 2 ? 1e-14 : eps_lv[k];   // JCG from W_h (l.7-9)

@@ -168,6 +168,10 @@ cudaError_t launch_jcg_persistent(const LevelGeom& g, const ConstStencil& cs, co
                                   double* z, double* p0, double* p1, double* w, double* dinv, const double* beta,
                                   const double* b, double* partials, JcgScalars* sc, cudaStream_t st);
 long long persistent_max_bricks(int elem_path);
+bool cta_solve_fits(const LevelGeom& g, int elem_path, long long max_nodes);
+cudaError_t init_cta_kernel_attributes();
+cudaError_t launch_jcg_cta(const LevelGeom& g, const ConstStencil& cs, const ElemStencil* es, double* x, double* r,
+                           const double* beta, const double* b, JcgScalars* sc, cudaStream_t st);
 cudaError_t init_tma_kernel_attributes();
 cudaError_t init_elem_kernel_attributes();
 int elem_tile_rows();
@@ -179,13 +183,13 @@ int tma_int_box_y();
 
 cudaError_t launch_beta(const LevelGeom& g, const Problem& pb, double* beta, cudaStream_t st);
 cudaError_t launch_rhs(const LevelGeom& g, const Problem& pb, const ElemStencil& es, double beta_const,
-                       const double* beta, double* b, double* scratch, cudaStream_t st);
+                       const double* beta, double* b, double* scratch, cudaStream_t st, int ctas_per_sm = 0);
 cudaError_t launch_gather(const LevelGeom& g, const double* u, double* x, cudaStream_t st);
 cudaError_t launch_scatter(const LevelGeom& g, const double* x, double* u, cudaStream_t st);
 cudaError_t launch_dirichlet_fill(const LevelGeom& g, const Problem& pb, double* u, double value_if_none,
                                   int zero_instead, cudaStream_t st);
 cudaError_t launch_exp_finite(const LevelGeom& gf, const Problem& pb, const double* u2h, const double* u4h,
-                              double* w, int variant, double* seeds, int freebox, cudaStream_t st);
+                              double* w, int variant, double* seeds, int freebox, cudaStream_t st, int fused = 1);
 cudaError_t launch_exp_true(const LevelGeom& gf, const Problem& pb, const double* uh, const double* u2h,
                             double* ut, cudaStream_t st);
 cudaError_t launch_zero_vec(const LevelGeom& g, double* v, cudaStream_t st);

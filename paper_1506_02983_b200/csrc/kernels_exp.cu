@@ -159,6 +159,228 @@ __global__ void __launch_bounds__(64) k_exp_interp(const LevelGeom gf, const Pro
   }
 }
 
+// (1+2) fused: EXP_finite as one z-march over 4h block layers. A CTA owns XB x YB 4h blocks in (x, y)
+// (64 x 8 fine nodes, plus the domain's last node row / column) and a chunk of 4h layers. Per layer it
+// stages the three 2h planes of u_2h and the two 4h planes of u_4h it touches in shared memory, forms
+// the seeds of the layer's blocks there (the same expressions as k_exp_seeds), evaluates the
+// interpolant per (block, fine row, fine plane) with the per-row coefficients of k_exp_interp into a
+// shared output tile, and writes the tile with coalesced row stores. HBM traffic: the fine level
+// written once (8 B / node) plus ~1/8 + 1/64 of it read, instead of a seed array written and re-read.
+// Results are bitwise those of k_exp_seeds + k_exp_interp (same operations in the same order).
+constexpr int XB = 16, YB = 2;                                 // 4h blocks per tile
+constexpr int FXT = 4 * XB + 1, FYT = 4 * YB + 1;              // fine nodes per tile incl. the last node
+constexpr int S2X = 2 * XB + 1, S2Y = 2 * YB + 1;              // 2h nodes per tile plane
+constexpr int FNTH = 256;
+
+template <bool FREEBOX>
+__global__ void __launch_bounds__(FNTH, 3) k_exp_fused(const LevelGeom gf, const Problem pb, const double* __restrict__ u2h,
+                                                       const double* __restrict__ u4h, double* __restrict__ out, int variant,
+                                                       int F0, int F1, int bzA, int lchunk) {
+  __shared__ double U1s[3][S2Y][S2X];          // u_2h on 2h planes 2bz .. 2bz+2
+  __shared__ double U0s[2][YB + 1][XB + 1];    // u_4h on 4h planes bz, bz+1
+  __shared__ double Ss[3][S2Y][S2X];           // seeds of the layer
+  __shared__ double Os[5][FYT][FXT];           // fine output tile, planes 4bz .. 4bz+4
+  __shared__ double Wq[5][3], Wl[5][2];        // 1D quadratic / linear weights at xi = (l - 2) / 2
+  const int tid = threadIdx.x;
+  if (tid < 5) { quad_w(tid, Wq[tid]); lin_w(tid, Wl[tid]); }
+  const int n4x = gf.n[0] / 4, n4y = gf.n[1] / 4, n4z = gf.n[2] / 4;
+  const int n2x = gf.n[0] / 2, n2y = gf.n[1] / 2;
+  const long long nn2x = n2x + 1, nn2y = n2y + 1;
+  const long long nn4x = n4x + 1, nn4y = n4y + 1;
+  const int bx0 = blockIdx.x * XB, by0 = blockIdx.y * YB;
+  const int nbx = min(XB, n4x - bx0), nby = min(YB, n4y - by0);   // blocks in this tile
+  const int X0 = 4 * bx0, Y0 = 4 * by0;
+  const int nfx = 4 * nbx + (bx0 + nbx == n4x ? 1 : 0);          // fine nodes of the tile along x
+  const int nfy = 4 * nby + (by0 + nby == n4y ? 1 : 0);
+  const int I0 = 2 * bx0, J0 = 2 * by0;
+  const long long nx = gf.n[0] + 1, ny = gf.n[1] + 1;
+  const int bzs = bzA + blockIdx.z * lchunk, bze = min(bzs + lchunk, n4z);
+  // staging assignments (compile-time index maps): each thread loads at most 2 u_2h and 1 u_4h values
+  constexpr int N1 = 3 * S2Y * S2X, N0 = 2 * (YB + 1) * (XB + 1);
+  long long o1[2];
+  bool v1[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int t = tid + r * FNTH;
+    const int i = t % S2X, j = (t / S2X) % S2Y, k = t / (S2X * S2Y);
+    v1[r] = t < N1 && I0 + i <= n2x && J0 + j <= n2y;
+    o1[r] = (I0 + i) + nn2x * ((J0 + j) + nn2y * (long long)k);   // + (2 bz) nn2x nn2y per layer
+  }
+  const int i0 = tid % (XB + 1), j0 = (tid / (XB + 1)) % (YB + 1), k0 = tid / ((XB + 1) * (YB + 1));
+  const bool v0 = tid < N0 && bx0 + i0 <= n4x && by0 + j0 <= n4y;
+  const long long o0 = (bx0 + i0) + nn4x * ((by0 + j0) + nn4y * (long long)k0);
+  const long long pl2 = nn2x * nn2y, pl4 = nn4x * nn4y;
+  double r1[2] = {0.0, 0.0}, r0 = 0.0;
+  auto fetch = [&](int bz) {
+#pragma unroll
+    for (int r = 0; r < 2; ++r) r1[r] = v1[r] ? __ldg(u2h + o1[r] + 2LL * bz * pl2) : 0.0;
+    r0 = v0 ? __ldg(u4h + o0 + (long long)bz * pl4) : 0.0;
+  };
+  // regular stores (free-box output): thread -> column st_lx, rows st_row and st_row + 4 of the tile
+  const int st_lx = tid & 63, st_row = tid >> 6;
+  bool st_ok[2];
+  long long st_off[2];
+#pragma unroll
+  for (int r2 = 0; r2 < 2; ++r2) {
+    const int fx = X0 + st_lx, fy = Y0 + st_row + 4 * r2;
+    st_ok[r2] = st_lx < nfx && st_row + 4 * r2 < nfy && fx >= gf.flo[0] && fx < gf.flo[0] + gf.nf[0] &&
+                fy >= gf.flo[1] && fy < gf.flo[1] + gf.nf[1];
+    st_off[r2] = (long long)(fy - gf.flo[1]) * gf.P + (fx - gf.flo[0]);
+  }
+  if (bzs < bze) fetch(bzs);
+  for (int bz = bzs; bz < bze; ++bz) {
+    const int fz0 = 4 * bz, nfz = (bz == n4z - 1) ? 5 : 4;
+    const int pz0 = max(fz0, F0), pz1 = min(fz0 + nfz, F1);   // fine planes of this layer to write
+    __syncthreads();   // previous layer's tiles consumed
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+      if (tid + r * FNTH < N1) (&U1s[0][0][0])[tid + r * FNTH] = r1[r];
+    if (tid < N0) (&U0s[0][0][0])[tid] = r0;
+    if (bz + 1 < bze) fetch(bz + 1);   // next layer's loads in flight during this layer's work
+    __syncthreads();
+    if (pz0 >= pz1) continue;
+    // seeds (k_exp_seeds' expressions; (i, j, k) tile-local 2h indices, even = 4h-coincident)
+    auto U1 = [&](int i, int j, int k) { return U1s[k][j][i]; };
+    auto U0 = [&](int i, int j, int k) { return U0s[k >> 1][j >> 1][i >> 1]; };
+    auto D = [&](int i, int j, int k) { return U1(i, j, k) - U0(i, j, k); };
+    for (int t = tid; t < N1; t += FNTH) {
+      const int i = t % S2X, j = (t / S2X) % S2Y, k = t / (S2X * S2Y);
+      double v = 0.0;
+      const int oi = i & 1, oj = j & 1, ok = k & 1;
+      const int nodd = oi + oj + ok;
+      if (nodd == 0) {
+        v = (5.0 * U1(i, j, k) - U0(i, j, k)) / 4.0;                              // Eq. (jiedian)
+      } else if (nodd == 1) {
+        v = U1(i, j, k) + (D(i - oi, j - oj, k - ok) + D(i + oi, j + oj, k + ok)) / 8.0;   // Eq. (zhongdian)
+      } else if (variant == 1) {   // Remark 2: mean of Eq. (zhongdian) over the diagonals
+        const int odd[3] = {oi, oj, ok};
+        double sum = 0.0;
+        int ax[3], na = 0;
+        for (int d = 0; d < 3; ++d) if (odd[d]) ax[na++] = d;
+        const int nseg = 1 << (na - 1);
+        for (int sgn = 0; sgn < nseg; ++sgn) {
+          int oa[3] = {0, 0, 0};
+          oa[ax[0]] = -1;
+          for (int q = 1; q < na; ++q) oa[ax[q]] = ((sgn >> (q - 1)) & 1) ? -1 : 1;
+          sum += U1(i, j, k) + (D(i + oa[0], j + oa[1], k + oa[2]) + D(i - oa[0], j - oa[1], k - oa[2])) / 8.0;
+        }
+        v = sum / nseg;
+      }
+      (&Ss[0][0][0])[t] = v;   // outside the tile's blocks: never read
+    }
+    __syncthreads();
+    // interpolation: one item per (fine row, block, fine plane) of the tile, k_exp_interp's expressions.
+    // The 4 x 8 x 16 regular items map to threads at compile time (row fastest: conflict-free shared
+    // stores, row stride 65 doubles); the domain's last row (row 8) and last plane (lz 4) follow as extras.
+    auto interp_item = [&](int row, int lb, int lz) {
+      const int lby = min(row >> 2, nby - 1), ly = row - 4 * lby;
+      const double qz[3] = {Wq[lz][0], Wq[lz][1], Wq[lz][2]}, lz2[2] = {Wl[lz][0], Wl[lz][1]};
+      const double qy[3] = {Wq[ly][0], Wq[ly][1], Wq[ly][2]}, ly2[2] = {Wl[ly][0], Wl[ly][1]};
+      auto s = [&](int k, int j, int i) { return Ss[k][2 * lby + j][2 * lb + i]; };
+      double C[3], E[2];
+      if (variant == 1) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          double tt = 0.0;
+#pragma unroll
+          for (int k = 0; k < 3; ++k) tt += qz[k] * (qy[0] * s(k, 0, i) + qy[1] * s(k, 1, i) + qy[2] * s(k, 2, i));
+          C[i] = tt;
+        }
+        E[0] = E[1] = 0.0;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+          C[i] = ly2[0] * (lz2[0] * s(0, 0, i) + lz2[1] * s(2, 0, i)) + ly2[1] * (lz2[0] * s(0, 2, i) + lz2[1] * s(2, 2, i));
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+          const int A = 2 * a;
+          const double Py = lz2[0] * (qy[0] * s(0, 0, A) + qy[1] * s(0, 1, A) + qy[2] * s(0, 2, A)) +
+                            lz2[1] * (qy[0] * s(2, 0, A) + qy[1] * s(2, 1, A) + qy[2] * s(2, 2, A));
+          const double Pz = ly2[0] * (qz[0] * s(0, 0, A) + qz[1] * s(1, 0, A) + qz[2] * s(2, 0, A)) +
+                            ly2[1] * (qz[0] * s(0, 2, A) + qz[1] * s(1, 2, A) + qz[2] * s(2, 2, A));
+          const double T = ly2[0] * (lz2[0] * s(0, 0, A) + lz2[1] * s(2, 0, A)) + ly2[1] * (lz2[0] * s(0, 2, A) + lz2[1] * s(2, 2, A));
+          E[a] = Py + Pz - 2.0 * T;
+        }
+      }
+      double* orow = &Os[lz][row][4 * lb];
+#pragma unroll
+      for (int l = 0; l < 4; ++l) {
+        double qx[3], lx[2];
+        quad_w(l, qx); lin_w(l, lx);
+        orow[l] = qx[0] * C[0] + qx[1] * C[1] + qx[2] * C[2] + lx[0] * E[0] + lx[1] * E[1];
+      }
+      if (bx0 + lb == n4x - 1) {   // the domain's last node column (l = 4)
+        double qx[3], lx[2];
+        quad_w(4, qx); lin_w(4, lx);
+        orow[4] = qx[0] * C[0] + qx[1] * C[1] + qx[2] * C[2] + lx[0] * E[0] + lx[1] * E[1];
+      }
+    };
+    const int lzs = pz0 - fz0, lze = pz1 - fz0;   // planes of the layer to produce
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int t = tid + r * FNTH;
+      const int row = t & 7, lb = (t >> 3) & 15, lz = t >> 7;
+      if (lb < nbx && row < nfy && lz >= lzs && lz < lze) interp_item(row, lb, lz);
+    }
+    if (nfy > 8 || lze > 4) {   // extras: row 8 of the domain's last block row, plane 4 of the last layer
+      const int nx8 = (nfy > 8) ? 4 * XB : 0;                     // (row 8, lb, lz < 4)
+      const int n4p = (lze > 4) ? FYT * XB : 0;                   // (row, lb, lz = 4)
+      for (int t = tid; t < nx8 + n4p; t += FNTH) {
+        int row, lb, lz;
+        if (t < nx8) { row = 8; lb = t & 15; lz = t >> 4; }
+        else { const int u = t - nx8; row = u % FYT; lb = u / FYT; lz = 4; }
+        if (lb < nbx && row < nfy && lz >= lzs && lz < lze) interp_item(row, lb, lz);
+      }
+    }
+    __syncthreads();
+    // stores: the 4 x 8 x 64 regular nodes map to threads at compile time (coalesced rows), then the
+    // domain's last column / row / plane as extras
+    auto put = [&](int lz, int row, int lx) {
+      const int fx = X0 + lx, fy = Y0 + row, fz = fz0 + lz;
+      double W = Os[lz][row][lx];
+      const bool fr = fz >= gf.flo[2] && fz < gf.flo[2] + gf.nf[2] && fy >= gf.flo[1] && fy < gf.flo[1] + gf.nf[1] &&
+                      fx >= gf.flo[0] && fx < gf.flo[0] + gf.nf[0];
+      if (FREEBOX) {
+        if (fr) out[(long long)(fz - gf.flo[2] - gf.zoff) * gf.S + (long long)(fy - gf.flo[1]) * gf.P + (fx - gf.flo[0])] = W;
+      } else {
+        if (!fr) W = gD_at(gf, pb, fx, fy, fz);
+        out[(long long)fx + nx * ((long long)fy + ny * fz)] = W;
+      }
+    };
+    if (FREEBOX) {   // free-box output: per-thread (x, y) offsets fixed, the plane term per layer
+#pragma unroll
+      for (int lz = 0; lz < 4; ++lz) {
+        const int fz = fz0 + lz;
+        if (lz < lzs || lz >= lze || fz < gf.flo[2] || fz >= gf.flo[2] + gf.nf[2]) continue;
+        const long long zt = (long long)(fz - gf.flo[2] - gf.zoff) * gf.S;
+#pragma unroll
+        for (int r2 = 0; r2 < 2; ++r2)
+          if (st_ok[r2]) out[zt + st_off[r2]] = Os[lz][st_row + 4 * r2][st_lx];
+      }
+    } else {
+      const int lx = tid & 63, row0 = tid >> 6;
+      if (lx < nfx) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const int row = row0 + 4 * (r & 1), lz = r >> 1;
+          if (row < nfy && lz >= lzs && lz < lze) put(lz, row, lx);
+        }
+      }
+    }
+    if (nfx > 64 || nfy > 8 || lze > 4) {
+      // extras: A = column 64 (rows < 8, planes < 4), B = row 8 (planes < 4), C = plane 4
+      const int nA = nfx > 64 ? 32 : 0, nB = nfy > 8 ? 4 * FXT : 0, nC = lze > 4 ? FYT * FXT : 0;
+      for (int t = tid; t < nA + nB + nC; t += FNTH) {
+        int lx, row, lz;
+        if (t < nA) { lx = 64; row = t & 7; lz = t >> 3; }
+        else if (t < nA + nB) { const int u = t - nA; lx = u % FXT; row = 8; lz = u / FXT; }
+        else { const int u = t - nA - nB; lx = u % FXT; row = u / FXT; lz = 4; }
+        if (lx < nfx && row < nfy && lz >= lzs && lz < lze) put(lz, row, lx);
+      }
+    }
+  }
+}
+
 // EXP_true as a z-march over a 64 x 8 fine tile (threads 32 x 8; thread (lane, w) owns the nodes
 // X0 + lane and X0 + 32 + lane of fine row Y0 + w, so every load / store instruction of a warp covers
 // 256 contiguous bytes). Per 2h plane K: (a) the tile's 33 x 5 corner differences
@@ -170,7 +392,7 @@ constexpr int ETX = 64, ETY = 8, EDX = ETX / 2 + 1, EDY = ETY / 2 + 1;   // 33 x
 
 __global__ void __launch_bounds__(256) k_exp_true(const LevelGeom gf, const Problem pb, const double* __restrict__ uh,
                                                   const double* __restrict__ u2h, double* __restrict__ ut, int c0,
-                                                  int cchunk) {
+                                                  int cchunk, double third) {
   __shared__ double D[2][EDY][EDX];
   const int lane = threadIdx.x, w = threadIdx.y, tid = lane + 32 * w;
   const int n2x = gf.n[0] / 2, n2y = gf.n[1] / 2, n2z = gf.n[2] / 2;
@@ -183,52 +405,49 @@ __global__ void __launch_bounds__(256) k_exp_true(const LevelGeom gf, const Prob
   const int fy = Y0 + w;
   const bool row_ok = fy <= gf.n[1];
   const int fxa = X0 + lane, fxb = X0 + 32 + lane;
-  // interpolation stencil of the thread's nodes: 2h column(s) and row(s) below / above
-  const int ia = lane >> 1, iaw = lane & 1;                 // node fxa: d column ia (+1 if odd)
-  const int ib = 16 + (lane >> 1);                          // node fxb: d column ib (+1 if odd)
-  const int jr = w >> 1, jw = w & 1;                        // row: d row jr (+1 if odd)
-  // (y, x)-interpolated d of plane slot s at the two nodes of this thread
-  auto dxy = [&](int s, double& va, double& vb) {
-    double a = D[s][jr][ia], b = D[s][jr][ib];
-    if (iaw) { a = 0.5 * (a + D[s][jr][ia + 1]); b = 0.5 * (b + D[s][jr][ib + 1]); }
-    if (jw) {
-      double a2 = D[s][jr + 1][ia], b2 = D[s][jr + 1][ib];
-      if (iaw) { a2 = 0.5 * (a2 + D[s][jr + 1][ia + 1]); b2 = 0.5 * (b2 + D[s][jr + 1][ib + 1]); }
-      a = 0.5 * (a + a2);
-      b = 0.5 * (b + b2);
-    }
-    va = a;
-    vb = b;
+  // interpolation stencil of the thread's nodes: 2h column(s) and row(s) below / above, as weights
+  // (1, 0) on a 2h node or (1/2, 1/2) between two: the products are exact, so w0 d0 + w1 d1 equals the
+  // mean (d0 + d1) / 2 bit for bit and the interpolation needs no branches
+  const int ia = lane >> 1, ib = 16 + (lane >> 1), jr = w >> 1;
+  const double wx1 = (lane & 1) ? 0.5 : 0.0, wx0 = 1.0 - wx1;
+  const double wy1 = (w & 1) ? 0.5 : 0.0, wy0 = 1.0 - wy1;
+  auto dxy = [&](int s, double& va, double& vb) {   // (y, x)-interpolated d of plane slot s
+    const double a0 = wx0 * D[s][jr][ia] + wx1 * D[s][jr][ia + 1];
+    const double b0 = wx0 * D[s][jr][ib] + wx1 * D[s][jr][ib + 1];
+    const double a1 = wx0 * D[s][jr + 1][ia] + wx1 * D[s][jr + 1][ia + 1];
+    const double b1 = wx0 * D[s][jr + 1][ib] + wx1 * D[s][jr + 1][ib + 1];
+    va = wy0 * a0 + wy1 * a1;
+    vb = wy0 * b0 + wy1 * b1;
   };
   // loads are issued one step ahead (registers), so the global latency overlaps the barrier and the
   // shared-memory interpolation of the current step
   const bool dthr = tid < EDX * EDY;
   const int di = tid % EDX, dj = tid / EDX;
   const bool d_ok = dthr && I0 + di <= n2x && J0 + dj <= n2y;
+  const long long doff_h = (long long)(2 * (J0 + dj)) * nx + 2 * (I0 + di), doff_2 = (long long)(J0 + dj) * nx2 + (I0 + di);
   auto load_d = [&](int K, double& a, double& b) {   // u_h at the 2h node and u_2h, plane K
     a = b = 0.0;
     if (d_ok) {
-      a = __ldg(uh + (long long)(2 * K) * pl + (long long)(2 * (J0 + dj)) * nx + 2 * (I0 + di));
-      b = __ldg(u2h + (long long)K * pl2 + (J0 + dj) * nx2 + (I0 + di));
+      a = __ldg(uh + (long long)(2 * K) * pl + doff_h);
+      b = __ldg(u2h + (long long)K * pl2 + doff_2);
     }
   };
   const bool okA = row_ok && fxa <= gf.n[0], okB = row_ok && fxb <= gf.n[0];
+  const long long rowoff = (long long)fy * nx;
   auto load_u = [&](int fz, double& a, double& b) {
-    const long long row = (long long)fz * pl + (long long)fy * nx;
+    const long long row = (long long)fz * pl + rowoff;
     a = okA ? __ldg(uh + row + fxa) : 0.0;
     b = okB ? __ldg(uh + row + fxb) : 0.0;
   };
+  // free (x, y) flags of the thread's two nodes; the plane decides the rest
+  const bool yf = fy >= gf.flo[1] && fy < gf.flo[1] + gf.nf[1];
+  const bool xyfA = yf && fxa >= gf.flo[0] && fxa < gf.flo[0] + gf.nf[0];
+  const bool xyfB = yf && fxb >= gf.flo[0] && fxb < gf.flo[0] + gf.nf[0];
   auto put = [&](int fz, double ua, double ub, double ia_, double ib_) {   // u~ on plane fz, this thread's nodes
-    const long long row = (long long)fz * pl + (long long)fy * nx;
-    const bool zf = fz >= gf.flo[2] && fz < gf.flo[2] + gf.nf[2], yf = fy >= gf.flo[1] && fy < gf.flo[1] + gf.nf[1];
-    if (okA) {
-      const bool fr = zf && yf && fxa >= gf.flo[0] && fxa < gf.flo[0] + gf.nf[0];
-      ut[row + fxa] = fr ? ua + ia_ / 3.0 : gD_at(gf, pb, fxa, fy, fz);
-    }
-    if (okB) {
-      const bool fr = zf && yf && fxb >= gf.flo[0] && fxb < gf.flo[0] + gf.nf[0];
-      ut[row + fxb] = fr ? ub + ib_ / 3.0 : gD_at(gf, pb, fxb, fy, fz);
-    }
+    const long long row = (long long)fz * pl + rowoff;
+    const bool zf = fz >= gf.flo[2] && fz < gf.flo[2] + gf.nf[2];
+    if (okA) ut[row + fxa] = (zf && xyfA) ? __fma_rn(ia_, third, ua) : gD_at(gf, pb, fxa, fy, fz);
+    if (okB) ut[row + fxb] = (zf && xyfB) ? __fma_rn(ib_, third, ub) : gD_at(gf, pb, fxb, fy, fz);
   };
   double dh, d2;
   load_d(Ca, dh, d2);
@@ -259,13 +478,23 @@ __global__ void __launch_bounds__(256) k_exp_true(const LevelGeom gf, const Prob
 }  // namespace
 
 cudaError_t launch_exp_finite(const LevelGeom& gf, const Problem& pb, const double* u2h, const double* u4h, double* w,
-                              int variant, double* seeds, int freebox, cudaStream_t st) {
+                              int variant, double* seeds, int freebox, cudaStream_t st, int fused) {
   // fine planes produced: the rank's free planes (free-box output) or its owned node planes (full output)
   const int F0 = freebox ? gf.flo[2] + gf.zoff + gf.zbeg : gf.zlo;
   const int F1 = freebox ? gf.flo[2] + gf.zoff + gf.zend : gf.zhi;
   if (F1 <= F0) return cudaSuccess;
   const int n4z = gf.n[2] / 4;
   const int bz0 = std::min(F0 / 4, n4z - 1), bz1 = std::min((F1 - 1) / 4, n4z - 1);
+  if (fused) {
+    const int nl = bz1 - bz0 + 1;
+    const int tiles = ((gf.n[0] / 4 + XB - 1) / XB) * ((gf.n[1] / 4 + YB - 1) / YB);
+    const int lchunk = std::max(1, std::min(8, tiles * nl / 2000));   // >= ~2000 CTAs where the level allows
+    dim3 g((gf.n[0] / 4 + XB - 1) / XB, (gf.n[1] / 4 + YB - 1) / YB, (nl + lchunk - 1) / lchunk);
+    count_launch();
+    if (freebox) k_exp_fused<true><<<g, FNTH, 0, st>>>(gf, pb, u2h, u4h, w, variant, F0, F1, bz0, lchunk);
+    else k_exp_fused<false><<<g, FNTH, 0, st>>>(gf, pb, u2h, u4h, w, variant, F0, F1, bz0, lchunk);
+    return cudaGetLastError();
+  }
   const int K0 = 2 * bz0, K1 = 2 * bz1 + 2;   // 2h planes of the touched 4h blocks
   dim3 g1((gf.n[0] / 2 + 1 + 127) / 128, gf.n[1] / 2 + 1, K1 - K0 + 1);
   count_launch();
@@ -284,7 +513,7 @@ cudaError_t launch_exp_true(const LevelGeom& gf, const Problem& pb, const double
   const int cchunk = 32;   // 2h cells (64 fine planes) per CTA
   dim3 grid((gf.n[0] + 1 + ETX - 1) / ETX, (gf.n[1] + 1 + ETY - 1) / ETY, (c1 - c0 + cchunk - 1) / cchunk);
   count_launch();
-  k_exp_true<<<grid, dim3(32, 8), 0, st>>>(gf, pb, uh, u2h, ut, c0, cchunk);
+  k_exp_true<<<grid, dim3(32, 8), 0, st>>>(gf, pb, uh, u2h, ut, c0, cchunk, 1.0 / 3.0);
   return cudaGetLastError();
 }
 

@@ -12,6 +12,7 @@
 // init phase (kappa_0 sum_e beta_e + Robin diagonal) into a scratch vector.
 // Reductions are deterministic and identical in every CTA: each CTA writes its partial, and after the
 // barrier every CTA reduces all partials with the same fixed tree (ping-pong partial buffers).
+#include <algorithm>
 #include <cooperative_groups.h>
 #include "ecmg_internal.cuh"
 #include "jcg_common.cuh"
@@ -376,6 +377,187 @@ __global__ void __launch_bounds__(PNTH, 2) k_jcg_persistent(const LevelGeom g, c
   }
 }
 
+// ---- the smallest levels: the whole solve in ONE CTA, every vector in shared memory -------------------
+// Levels of at most CNODES free unknowns (4^3 .. 16^3) do not need a grid: one CTA of CNTH threads keeps
+// p (with a zero halo ring), x, r, w = A p and (element path) D^-1 in shared memory, so an iteration is
+// two block reductions and a few barriers with no L2 round trip and no grid barrier. Each thread owns
+// the nodes t, t + CNTH, ... (x fastest) for the whole solve; the arithmetic per node is the persistent
+// kernel's (apply_const / apply_elem on a 27-value window).
+constexpr int CNTH = 512, CMAXN = 8, CNODES = CNTH * CMAXN;
+
+__device__ __forceinline__ void cta_sum3(double v[3], double* red) {
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_down_sync(0xffffffffu, v[k], o);
+  if ((tid & 31) == 0)
+    for (int k = 0; k < 3; ++k) red[3 * (tid >> 5) + k] = v[k];
+  __syncthreads();
+  if (tid < 3) {
+    double sum = 0.0;
+    for (int w = 0; w < CNTH / 32; ++w) sum += red[3 * w + tid];
+    red[3 * (CNTH / 32) + tid] = sum;
+  }
+  __syncthreads();
+  v[0] = red[3 * (CNTH / 32)]; v[1] = red[3 * (CNTH / 32) + 1]; v[2] = red[3 * (CNTH / 32) + 2];
+  __syncthreads();   // red reusable
+}
+
+template <bool ELEM>
+__global__ void __launch_bounds__(CNTH, 1) k_jcg_cta(const LevelGeom g, const ConstStencil cs, const ElemStencil es,
+                                                   const PArgs a) {
+  extern __shared__ double csm[];
+  const int nfx = g.nf[0], nfy = g.nf[1], nfz = g.nf[2];
+  const int n = nfx * nfy * nfz;
+  const int hx = nfx + 2, hxy = hx * (nfy + 2);
+  const int nh = hxy * (nfz + 2);
+  double* P = csm;              // p with a zero halo ring, index ((z+1) hxy + (y+1) hx + x+1)
+  double* X = P + nh;
+  double* R = X + n;
+  double* W = R + n;
+  double* DI = W + n;           // element path only
+  double* red = DI + (ELEM ? n : 0);
+  const int tid = threadIdx.x;
+  JcgScalars* sc = a.sc;
+  const double eps = sc->in.eps;
+  const int max_iter = sc->in.max_iter;
+  double* const u_out = sc->in.u_out;
+  const double cdinv = cs.dinv;
+  Node nd[CMAXN];
+  int hp[CMAXN];
+  bool own[CMAXN];
+#pragma unroll
+  for (int q = 0; q < CMAXN; ++q) {
+    const int i = tid + q * CNTH;
+    own[q] = i < n;
+    const int ii = own[q] ? i : 0;
+    nd[q].fx = ii % nfx; nd[q].fy = (ii / nfx) % nfy; nd[q].fz = ii / (nfx * nfy);
+    nd[q].off = nd[q].fz * (int)g.S + nd[q].fy * (int)g.P + nd[q].fx;
+    hp[q] = (nd[q].fz + 1) * hxy + (nd[q].fy + 1) * hx + nd[q].fx + 1;
+  }
+  auto win = [&](int h, double p27[3][3][3]) {
+#pragma unroll
+    for (int dz = 0; dz < 3; ++dz)
+#pragma unroll
+      for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx) p27[dz][dy][dx] = P[h + (dz - 1) * hxy + (dy - 1) * hx + (dx - 1)];
+  };
+  auto applyq = [&](int q, double* diag) {
+    double p27[3][3][3];
+    win(hp[q], p27);
+    return apply_node<ELEM>(g, cs, es, a.beta, nd[q], p27, diag);
+  };
+  // init: P = x (zero halo), r = b - A x, D^-1, z = D^-1 r, rho = r.z, rr, ||b||^2
+  for (int t = tid; t < nh; t += CNTH) P[t] = 0.0;
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < CMAXN; ++q)
+    if (own[q]) P[hp[q]] = a.x[nd[q].off];
+  __syncthreads();
+  double v[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int q = 0; q < CMAXN; ++q) {
+    if (!own[q]) continue;
+    const int i = tid + q * CNTH;
+    double d = 0.0;
+    const double ax = applyq(q, &d);
+    const double di = ELEM ? (es.precond ? (d > 0.0 ? 1.0 / d : 0.0) : 1.0) : cdinv;
+    if (ELEM) DI[i] = di;
+    const double bi = a.b[nd[q].off];
+    const double rn = bi - ax;
+    X[i] = P[hp[q]];
+    R[i] = rn;
+    const double zz = di * rn;
+    v[0] = __fma_rn(rn, zz, v[0]);
+    v[1] = __fma_rn(rn, rn, v[1]);
+    v[2] = __fma_rn(bi, bi, v[2]);
+  }
+  cta_sum3(v, red);
+  double rho = v[0], rr = v[1];
+  const double bb = v[2];
+  const double nb = sqrt(bb), nbe = nb > 0.0 ? nb : 1.0;
+  const double thresh = eps > 0.0 ? eps * nbe : -1.0;
+  int status = ST_OK, iter = 0;
+  double beta = 0.0;
+  bool done = (max_iter <= 0) || (thresh > 0.0 && !(sqrt(rr) > thresh));
+  if (!isfinite(rr)) { status = ST_EBREAKDOWN; done = true; }
+  while (!done) {
+    // p_new = z + beta p_old (pointwise, in place), then w = A p_new, sigma = p.w
+#pragma unroll
+    for (int q = 0; q < CMAXN; ++q) {
+      if (!own[q]) continue;
+      const int i = tid + q * CNTH;
+      const double zz = (ELEM ? DI[i] : cdinv) * R[i];
+      P[hp[q]] = iter == 0 ? zz : __fma_rn(beta, P[hp[q]], zz);
+    }
+    __syncthreads();
+    v[0] = v[1] = v[2] = 0.0;
+#pragma unroll
+    for (int q = 0; q < CMAXN; ++q) {
+      if (!own[q]) continue;
+      const int i = tid + q * CNTH;
+      const double w = applyq(q, nullptr);
+      W[i] = w;
+      v[0] = __fma_rn(P[hp[q]], w, v[0]);
+    }
+    cta_sum3(v, red);
+    const double sigma = v[0];
+    if (!(sigma > 0.0)) { status = ST_EBREAKDOWN; break; }
+    const double alpha = rho / sigma;
+    v[0] = v[1] = v[2] = 0.0;
+#pragma unroll
+    for (int q = 0; q < CMAXN; ++q) {
+      if (!own[q]) continue;
+      const int i = tid + q * CNTH;
+      X[i] = __fma_rn(alpha, P[hp[q]], X[i]);
+      const double rn = __fma_rn(-alpha, W[i], R[i]);
+      R[i] = rn;
+      const double zz = (ELEM ? DI[i] : cdinv) * rn;
+      v[0] = __fma_rn(rn, zz, v[0]);
+      v[1] = __fma_rn(rn, rn, v[1]);
+    }
+    cta_sum3(v, red);
+    beta = v[0] / rho;
+    rho = v[0];
+    rr = v[1];
+    ++iter;
+    done = (iter >= max_iter) || (thresh > 0.0 && !(sqrt(rr) > thresh));
+    if (!isfinite(rr)) { status = ST_EBREAKDOWN; done = true; }
+  }
+  // x, r back to memory; true residual ||b - A x|| with x staged in P; fused scatter of u_h
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < CMAXN; ++q) {
+    if (!own[q]) continue;
+    const int i = tid + q * CNTH;
+    a.x[nd[q].off] = X[i];
+    a.r[nd[q].off] = R[i];
+    P[hp[q]] = X[i];
+  }
+  __syncthreads();
+  v[0] = v[1] = v[2] = 0.0;
+#pragma unroll
+  for (int q = 0; q < CMAXN; ++q) {
+    if (!own[q]) continue;
+    const double rn = a.b[nd[q].off] - applyq(q, nullptr);
+    v[1] = __fma_rn(rn, rn, v[1]);
+    if (u_out) u_out[full_index(g, nd[q].fx, nd[q].fy, nd[q].fz)] = P[hp[q]];
+  }
+  cta_sum3(v, red);
+  if (tid == 0) {
+    sc->rho = rho; sc->rr = rr; sc->bb = bb; sc->rr_true = v[1]; sc->beta = beta;
+    sc->iter = iter; sc->max_iter = max_iter; sc->thresh = thresh; sc->status = status; sc->done = 1;
+  }
+}
+
+size_t cta_smem_bytes(const LevelGeom& g, bool elem) {
+  const long long n = (long long)g.nf[0] * g.nf[1] * g.nf[2];
+  const long long nh = (long long)(g.nf[0] + 2) * (g.nf[1] + 2) * (g.nf[2] + 2);
+  return sizeof(double) * (size_t)(nh + (elem ? 4 : 3) * n + 3 * (CNTH / 32) + 3);
+}
+
 template <bool ELEM>
 int persistent_grid(int want) {
   static int slots = 0;
@@ -390,6 +572,32 @@ int persistent_grid(int want) {
 }
 
 }  // namespace
+
+// the single-CTA solve takes the level if its free box fits (nodes and shared memory; not z-slabs)
+bool cta_solve_fits(const LevelGeom& g, int elem_path, long long max_nodes) {
+  const long long n = (long long)g.nf[0] * g.nf[1] * g.nf[2];
+  if (n > std::min<long long>(max_nodes, CNODES) || g.nza != g.nf[2] || g.zoff != 0) return false;
+  return cta_smem_bytes(g, elem_path != 0) <= 200 * 1024;
+}
+
+cudaError_t init_cta_kernel_attributes() {
+  cudaError_t e = cudaFuncSetAttribute(k_jcg_cta<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_jcg_cta<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  return e;
+}
+
+// One launch of one CTA: the whole solve of a small level (cta_solve_fits). Arguments as
+// launch_jcg_persistent (z and w unused).
+cudaError_t launch_jcg_cta(const LevelGeom& g, const ConstStencil& cs, const ElemStencil* es, double* x, double* r,
+                           const double* beta, const double* b, JcgScalars* sc, cudaStream_t st) {
+  PArgs a{x, r, nullptr, {nullptr, nullptr}, nullptr, b, nullptr, beta, nullptr, sc};
+  const ElemStencil e = es ? *es : ElemStencil{};
+  const size_t smem = cta_smem_bytes(g, es != nullptr);
+  count_launch();
+  if (es) k_jcg_cta<true><<<1, CNTH, smem, st>>>(g, cs, e, a);
+  else k_jcg_cta<false><<<1, CNTH, smem, st>>>(g, cs, e, a);
+  return cudaGetLastError();
+}
 
 // largest level (in bricks of 8 x 8 x 4 nodes) the persistent kernel takes: MAXB bricks per resident CTA
 long long persistent_max_bricks(int elem_path) {

@@ -196,93 +196,107 @@ __global__ void __launch_bounds__(VNTH, 3) k_rhs_vol(const LevelGeom g, const Pr
   }
 }
 
-// 4 (r^2)^{-1/4} to fp64 accuracy (the factor 1/4 of the last Newton step is folded into the caller's
-// weights): fp32 MUFU seed (rsqrt.approx, sqrt.approx: relative error ~3e-7) and one fp32 Newton step
-// (to ~1e-7, the fp32 rounding level) on the fp32 pipe, then one fp64 Newton step of
-// y <- y (5 - r^2 y^4) / 4 (error e -> -5/2 e^2: ~1e-7 -> ~3e-14). r^2 > 0 at every Gauss point (they
-// are interior to the elements); the fp32 clamp only keeps the seed finite.
-__device__ __forceinline__ double rpow_m14_x4(double r2, double five) {
-  const float rf = fmaxf((float)r2, 1e-30f);
-  float s;
-  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"(rf));
-  asm("sqrt.approx.ftz.f32 %0, %0;" : "+f"(s));
-  float s2 = s * s;
-  s = s * fmaf(-rf, s2 * s2, 5.0f) * 0.25f;
-  const double y = (double)s;
-  const double y2 = y * y;
-  return y * __fma_rn(-r2, y2 * y2, five);
-}
-
 // fp64 constants of k_rhs_c4 as kernel parameters (constant bank operands instead of per-use
 // immediate materialisation)
 struct RhsC4Consts {
   double wA, wB;   // N at the near / far Gauss point
-  double dA, dB;   // detJ * (-15/4) * (1/4) * wA, wB: the z pass of the tensor transform
-  double five;
+  double dA, dB;   // detJ * (-15/4) * wA, wB: the z pass of the contraction
+  double one, c3;   // 1, 1/4: y (1 + e/4)
 };
 
-// C4 volume load (f = -(15/4) r^{-1/2}, the corner singularity of u = r^{3/2}): element tile 32 x 8 =
-// one element per thread (node tile 31 x 7), z-marching over element layers. r^2 at a Gauss point is
-// (x^2 + y^2) + z^2 with the four in-plane sums fixed per thread and z^2 per layer, so a Gauss point
-// costs one add and the (r^2)^{-1/4} evaluation; the element vector F_e[a] = detJ sum_q f_q N_a(q) is
-// the same 2x2x2 tensor transform as k_rhs_vol. Per layer the z = 0 corners complete node plane fez
-// (with the z = 1 corners of the layer below carried in a register) through two shared-memory planes.
-__global__ void __launch_bounds__(VNTH, 3) k_rhs_c4(const LevelGeom g, double* __restrict__ b, int zc,
-                                                   const RhsC4Consts k) {
-  __shared__ double F0[4][VEY][VEX];   // layer corner entries a = 0..3 (z = 0: node plane fez)
-  __shared__ double F1[4][VEY][VEX];   // a = 4..7 (z = 1: node plane fez + 1)
-  const int lane = threadIdx.x, w = threadIdx.y;
-  const int X0 = blockIdx.x * VX, Y0 = blockIdx.y * VY;
-  const int z0 = g.zbeg + blockIdx.z * zc, z1 = min(z0 + zc, g.zend);   // local planes
-  const int gex = g.flo[0] + X0 - 1 + lane, gey = g.flo[1] + Y0 - 1 + w;
-  const bool xy_in = gex >= 0 && gex < g.n[0] && gey >= 0 && gey < g.n[1];
+// (r^2)^{-1/4} to fp64 accuracy. fp32 seed: r^2 rounded to fp32 (F2F), rsqrt.approx and sqrt.approx (MUFU,
+// relative error ~3e-7) and one fp32 Newton step of y <- y (5 - x y^4) / 4 (to ~1e-7, the fp32 rounding
+// level); y widened to fp64 exactly by bit operations (no second F2F: the XU pipe that executes MUFU and
+// F2F is this kernel's limit, 3 instead of 4 XU instructions per Gauss point); then one fp64 step in the
+// form y (1 + e/4), e = 1 - r^2 y^4 (error 5e^2/32: ~3e-14). r^2 > 0 at every Gauss point (interior to
+// the elements) and stays in the normal fp32 range on every level.
+__device__ __forceinline__ double rpow_m14(double r2, const RhsC4Consts& k) {
+  const float xf = (float)r2;
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(xf));
+  asm("sqrt.approx.ftz.f32 %0, %0;" : "+f"(y));
+  const float y2f = y * y;
+  y = (y * 0.25f) * fmaf(-xf, y2f * y2f, 5.0f);
+  const unsigned yb = __float_as_uint(y);
+  const double yd = __hiloint2double((int)((yb >> 3) + ((1023u - 127u) << 20)), (int)(yb << 29));
+  const double y2 = yd * yd;
+  const double e = __fma_rn(-r2, y2 * y2, k.one);
+  return __fma_rn(yd * k.c3, e, yd);
+}
+
+// C4 volume load (f = -(15/4) r^{-1/2}, the corner singularity of u = r^{3/2}). 512 threads = 32 x 16
+// elements per plane (node tile 31 x 15), one element per thread, z-marching over element layers. r^2 at a
+// Gauss point is (x^2 + y^2) + z^2 with the four in-plane sums fixed per thread and z^2 per layer, so a
+// Gauss point costs one add and the (r^2)^{-1/4} evaluation. The 2x2x2 Gauss load of node i,
+// F_i = detJ sum_{q} f_q N_i(q) over the 64 Gauss points of its 8 elements, factorises per axis (the 1D
+// weight of a Gauss point is wA at the point nearer the node, wB at the farther one) and is contracted
+// axis by axis: x within the thread, then the right node column takes its left neighbour element's
+// share by a warp shuffle; y the same across warps through shared memory; z with the lower layer's share
+// carried in a register. ~75 fp64 operations per element instead of ~113 for the 8 x 8 element-vector
+// transform. Work items (tile, z chunk) are linear, taken by a grid-stride loop.
+constexpr int C4X = 31, C4Y = 15, C4NTH = 512;
+__global__ void __launch_bounds__(C4NTH, 2) k_rhs_c4(const LevelGeom g, double* __restrict__ b, int zc,
+                                                    const RhsC4Consts k, int tx, int ty, int items) {
+  __shared__ double lo_s[2][2][16][32];   // [layer parity][qz][element row][lane]: y share of the row below
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const double ga = (1.0 - kGauss) / 2.0, gb = (1.0 + kGauss) / 2.0;   // Gauss points at xi = -+1/sqrt(3)
-  const double xa = g.lo[0] + (gex + ga) * g.h[0], xb = g.lo[0] + (gex + gb) * g.h[0];
-  const double ya = g.lo[1] + (gey + ga) * g.h[1], yb = g.lo[1] + (gey + gb) * g.h[1];
-  const double sxy[4] = {xa * xa + ya * ya, xb * xb + ya * ya, xa * xa + yb * yb, xb * xb + yb * yb};   // q bits x, y
   const double wA = k.wA, wB = k.wB, dA = k.dA, dB = k.dB;
-  const int fx = X0 + lane, fy = Y0 + w;
-  const bool node_ok = lane < VX && w < VY && fx < g.nf[0] && fy < g.nf[1];
-  double carry = 0.0;
-  for (int fez = z0 - 1; fez < z1; ++fez) {
-    const int gez = g.flo[2] + g.zoff + fez;
-    double F[8];
-    if (xy_in && gez >= 0 && gez < g.n[2]) {
-      const double za = g.lo[2] + (gez + ga) * g.h[2], zb = g.lo[2] + (gez + gb) * g.h[2];
-      const double z2[2] = {za * za, zb * zb};
-      double f[8], t1[8], t2[8];
+  for (int item = blockIdx.x; item < items; item += gridDim.x) {
+    const int X0 = (item % tx) * C4X, Y0 = ((item / tx) % ty) * C4Y;
+    const int z0 = g.zbeg + (item / (tx * ty)) * zc, z1 = min(z0 + zc, g.zend);   // local planes
+    const int gex = g.flo[0] + X0 - 1 + lane, gey = g.flo[1] + Y0 - 1 + w;
+    const bool xy_in = gex >= 0 && gex < g.n[0] && gey >= 0 && gey < g.n[1];
+    const double xa = g.lo[0] + (gex + ga) * g.h[0], xb = g.lo[0] + (gex + gb) * g.h[0];
+    const double ya = g.lo[1] + (gey + ga) * g.h[1], yb = g.lo[1] + (gey + gb) * g.h[1];
+    const double sxy[2][2] = {{xa * xa + ya * ya, xb * xb + ya * ya}, {xa * xa + yb * yb, xb * xb + yb * yb}};   // [qy][qx]
+    const int fx = X0 + lane, fy = Y0 + w;
+    const bool node_ok = lane < C4X && w < C4Y && fx < g.nf[0] && fy < g.nf[1];
+    double carry = 0.0;
+    int par = 0;
+    for (int fez = z0 - 1; fez < z1; ++fez, par ^= 1) {
+      const int gez = g.flo[2] + g.zoff + fez;
+      double X[2][2];   // [qy][qz]: x-contracted load of node column fx (this element's right node)
+      {
+        double h0[2][2], h1[2][2];
+        if (xy_in && gez >= 0 && gez < g.n[2]) {
+          const double za = g.lo[2] + (gez + ga) * g.h[2], zb = g.lo[2] + (gez + gb) * g.h[2];
+          const double z2[2] = {za * za, zb * zb};
 #pragma unroll
-      for (int q = 0; q < 8; ++q) f[q] = rpow_m14_x4(sxy[q & 3] + z2[q >> 2], k.five);
+          for (int qy = 0; qy < 2; ++qy)
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {   // along x: node bit 0 vs Gauss bit 0
-        const int qb = i & ~1;
-        t1[i] = (i & 1) ? (wB * f[qb] + wA * f[qb | 1]) : (wA * f[qb] + wB * f[qb | 1]);
+            for (int qz = 0; qz < 2; ++qz) {
+              const double fa = rpow_m14(sxy[qy][0] + z2[qz], k);
+              const double fb = rpow_m14(sxy[qy][1] + z2[qz], k);
+              h0[qy][qz] = __fma_rn(wA, fa, wB * fb);   // to the element's left node
+              h1[qy][qz] = __fma_rn(wB, fa, wA * fb);   // to its right node
+            }
+        } else {
+#pragma unroll
+          for (int qy = 0; qy < 2; ++qy)
+#pragma unroll
+            for (int qz = 0; qz < 2; ++qz) h0[qy][qz] = h1[qy][qz] = 0.0;
+        }
+#pragma unroll
+        for (int qy = 0; qy < 2; ++qy)
+#pragma unroll
+          for (int qz = 0; qz < 2; ++qz) X[qy][qz] = h1[qy][qz] + __shfl_down_sync(0xffffffffu, h0[qy][qz], 1);
       }
+      // y: node row fy = element row + 1 takes hi of this row and lo of the row above
+      double hi[2];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {   // along y
-        const int qb = i & ~2;
-        t2[i] = (i & 2) ? (wB * t1[qb] + wA * t1[qb | 2]) : (wA * t1[qb] + wB * t1[qb | 2]);
+      for (int qz = 0; qz < 2; ++qz) {
+        lo_s[par][qz][w][lane] = __fma_rn(wA, X[0][qz], wB * X[1][qz]);
+        hi[qz] = __fma_rn(wB, X[0][qz], wA * X[1][qz]);
       }
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {   // along z, with detJ folded into the weights
-        const int qb = i & ~4;
-        F[i] = (i & 4) ? (dB * t2[qb] + dA * t2[qb | 4]) : (dA * t2[qb] + dB * t2[qb | 4]);
+      __syncthreads();
+      if (node_ok) {
+        const double Ya = hi[0] + lo_s[par][0][w + 1][lane];
+        const double Yb = hi[1] + lo_s[par][1][w + 1][lane];
+        if (fez >= z0) b[(long long)fez * g.S + (long long)fy * g.P + fx] = carry + __fma_rn(dA, Ya, dB * Yb);
+        carry = __fma_rn(dB, Ya, dA * Yb);
       }
-    } else {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) F[i] = 0.0;
     }
-#pragma unroll
-    for (int a = 0; a < 4; ++a) { F0[a][w][lane] = F[a]; F1[a][w][lane] = F[a + 4]; }
-    __syncthreads();
-    if (node_ok) {
-      // node (fx, fy) is corner (1 - ex, 1 - ey) of the elements at tile (lane + ex, w + ey)
-      const double v0 = (F0[3][w][lane] + F0[2][w][lane + 1]) + (F0[1][w + 1][lane] + F0[0][w + 1][lane + 1]);
-      const double v1 = (F1[3][w][lane] + F1[2][w][lane + 1]) + (F1[1][w + 1][lane] + F1[0][w + 1][lane + 1]);
-      if (fez >= z0) b[(long long)fez * g.S + (long long)fy * g.P + fx] = carry + v0;
-      carry = v1;
-    }
-    __syncthreads();
+    __syncthreads();   // lo_s of this item's last layers consumed before the next item
   }
 }
 
@@ -424,7 +438,7 @@ cudaError_t init_setup_kernel_attributes() {
 }
 
 cudaError_t launch_rhs(const LevelGeom& g, const Problem& pb, const ElemStencil& es, double beta_const, const double* beta,
-                       double* b, double* scratch, cudaStream_t st) {
+                       double* b, double* scratch, cudaStream_t st, int ctas_per_sm) {
   if (prob_separable(pb.id)) {
     const int nmax = std::max(g.n[0], std::max(g.n[1], g.n[2]));
     const int stride = nmax + 1;
@@ -437,20 +451,30 @@ cudaError_t launch_rhs(const LevelGeom& g, const Problem& pb, const ElemStencil&
   } else {
     // element planes per CTA: 32 on large levels (a chunk re-evaluates one element plane), shorter on
     // small ones so that the grid has ~1000 CTAs instead of a few long serial chains
-    const long long tiles = (long long)((g.nf[0] + VX - 1) / VX) * ((g.nf[1] + VY - 1) / VY);
+    const bool c4 = pb.id == 4;
+    const int TX = c4 ? C4X : VX, TY = c4 ? C4Y : VY;
+    const long long tiles = (long long)((g.nf[0] + TX - 1) / TX) * ((g.nf[1] + TY - 1) / TY);
     const int nz = g.zend - g.zbeg;
-    const int zc = (int)std::max(4LL, std::min(32LL, tiles * nz / 1000));
-    dim3 grid((g.nf[0] + VX - 1) / VX, (g.nf[1] + VY - 1) / VY, (nz + zc - 1) / zc);
+    const int zc = (int)std::max(4LL, std::min(32LL, tiles * nz / (c4 ? 500 : 1000)));
+    dim3 grid((g.nf[0] + TX - 1) / TX, (g.nf[1] + TY - 1) / TY, (nz + zc - 1) / zc);
     count_launch();
-    if (pb.id == 4) {
+    if (c4) {
       RhsC4Consts k;
       k.wA = (1.0 + kGauss) / 2.0;
       k.wB = (1.0 - kGauss) / 2.0;
-      const double detJ = -3.75 * (g.h[0] * g.h[1] * g.h[2] / 8.0) * 0.25;   // f = -15/4 (r^2)^{-1/4}
+      const double detJ = -3.75 * (g.h[0] * g.h[1] * g.h[2] / 8.0);   // f = -15/4 (r^2)^{-1/4}
       k.dA = detJ * k.wA;
       k.dB = detJ * k.wB;
-      k.five = 5.0;
-      k_rhs_c4<<<grid, dim3(32, 8), 0, st>>>(g, b, zc, k);
+      k.one = 1.0; k.c3 = 0.25;
+      const int items = (int)(grid.x * grid.y * grid.z);
+      int nblk = items;
+      if (ctas_per_sm > 0) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        nblk = std::min(items, sms * ctas_per_sm);
+      }
+      k_rhs_c4<<<nblk, C4NTH, 0, st>>>(g, b, zc, k, (int)grid.x, (int)grid.y, items);
     }
     else k_rhs_vol<0><<<grid, dim3(32, 8), VSMEM, st>>>(g, pb, b, zc);
   }

@@ -23,6 +23,9 @@ PROB = dict(C1=1, C2=2, C3=3, C4=4, C5=5, P1=11, P2=12, P3=13,
 OPT_EXP_VARIANT, OPT_PRECOND, OPT_ZCHUNK, OPT_KERNEL, OPT_GRAPH, OPT_VIRTUAL_SLABS, OPT_PERSISTENT, OPT_PDL = 1, 2, 3, 4, 5, 6, 7, 8
 OPT_FUSED_HALO = 9
 OPT_SETUP_AHEAD = 10
+OPT_SETUP_CTAS = 11
+OPT_EXP_KERNEL = 12
+OPT_CTA_SOLVE = 13
 
 EXPORTS = ["ecmg_create_grid", "ecmg_set_coeffs", "ecmg_set_option", "ecmg_solve_level",
            "ecmg_prolongate_extrapolate", "ecmg_richardson", "ecmg_run", "ecmg_run_fixed", "ecmg_apply_operator",

@@ -84,7 +84,8 @@ def test_rhs(pid, n0, level):
 
 
 @pytest.mark.parametrize("variant", [0, 1])
-@pytest.mark.parametrize("pid,n0,level", [(o.C1, 4, 3), (o.C3, 4, 4), (o.P1, 4, 3), (o.P2, (10, 4, 5), 2)])
+@pytest.mark.parametrize("pid,n0,level", [(o.C1, 4, 3), (o.C3, 4, 4), (o.P1, 4, 3), (o.P2, (10, 4, 5), 2),
+                                          (o.C2, 4, 5), (o.P2, (10, 4, 5), 3)])
 def test_exp_finite(pid, n0, level, variant):
     n0 = (n0,) * 3 if np.isscalar(n0) else n0
     g = Grid(n0, level + 1, pid, params_for(pid), exp_variant=variant)
@@ -272,6 +273,7 @@ def test_persistent_small_levels_vs_graph(pid, eps):
     for pmax in (300000, 0):
         g = Grid(4, 5, pid, params_for(pid))
         g.set_option(ecmg.OPT_PERSISTENT, pmax)
+        g.set_option(ecmg.OPT_CTA_SOLVE, 4096 if pmax else 0)
         u = g.new_vec(4)
         st, stats = g.run(eps, u)
         assert st == 0
@@ -342,3 +344,51 @@ def test_setup_ahead_bitwise(pid, eps):
     for r in res[1:]:
         assert r[0] == res[0][0]
         assert np.array_equal(r[1], res[0][1]) and np.array_equal(r[2], res[0][2])
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("pid,n0,levels", [(o.C2, 4, 6), (o.C3, 4, 5), (o.P2, (10, 4, 5), 4), (o.P1, 4, 5)])
+def test_exp_fused_equals_two_pass(pid, n0, levels, variant):
+    # ECMG_OPT_EXP_KERNEL: the fused one-pass EXP_finite evaluates the same expressions as the seed and
+    # interpolation passes, so both the full-vector output (ecmg_prolongate_extrapolate, g_D on Dirichlet
+    # nodes) and the free-box output inside ecmg_run are bitwise equal
+    n0 = (n0,) * 3 if np.isscalar(n0) else n0
+    level = levels - 1
+    n = tuple(c << level for c in n0)
+    u2 = dev(synth.random_nodal(13, tuple(c // 2 for c in n)))
+    u4 = dev(synth.random_nodal(12, tuple(c // 4 for c in n)))
+    res = []
+    for fused in (0, 1):
+        g = Grid(n0, levels, pid, params_for(pid), exp_variant=variant)
+        g.set_option(ecmg.OPT_EXP_KERNEL, fused)
+        w = g.new_vec(level)
+        g.prolongate_extrapolate(level, u2, u4, w)
+        u, ut = g.new_vec(level), g.new_vec(level)
+        st, stats = g.run(1e-9, u, ut)
+        assert st == 0
+        res.append((host(w), [s["iterations"] for s in stats], host(u), host(ut)))
+    assert np.array_equal(res[0][0], res[1][0])
+    assert res[0][1] == res[1][1]
+    assert np.array_equal(res[0][2], res[1][2]) and np.array_equal(res[0][3], res[1][3])
+
+
+@pytest.mark.parametrize("pid,eps", [(o.C1, 1e-8), (o.C2, 1e-10), (o.C3, 1e-10), (o.C5, 1e-8), (o.P1, 1e-9),
+                                     (o.PATCH_ROBIN_XY, 1e-10)])
+def test_cta_solve_vs_persistent(pid, eps):
+    # levels of <= 4096 free unknowns (4^3 .. 16^3) are solved by one CTA with every vector in shared
+    # memory (ECMG_OPT_CTA_SOLVE); the cooperative persistent kernel is the reference: same counts (+-1)
+    # per level, solutions within rounding; and the one-CTA levels against the oracle's DSOLVE / JCG
+    res = []
+    for cta in (4096, 0):
+        g = Grid(4, 4, pid, params_for(pid))
+        g.set_option(ecmg.OPT_CTA_SOLVE, cta)
+        u = g.new_vec(3)
+        st, stats = g.run(eps, u)
+        assert st == 0
+        res.append(([s["iterations"] for s in stats], host(u)))
+    assert all(abs(a - b) <= 1 for a, b in zip(res[0][0], res[1][0]))
+    assert np.max(np.abs(res[0][1] - res[1][1])) <= 1e-9 * np.max(np.abs(res[1][1]))
+    ost, ostats, ou, _ = o.ecmg(4, 4, pid, eps, params=params_for(pid))
+    assert ost == 0
+    assert all(abs(a - int(b)) <= 1 for a, b in zip(res[0][0][2:], ostats[2:, 0]))
+    assert np.max(np.abs(res[0][1] - ou)) <= 1e-9 * np.max(np.abs(ou))
