@@ -128,6 +128,10 @@ typedef enum {
   ECMG_OPT_CTA_SOLVE = 13,   /* levels with at most this many free unknowns (default 1000, at most 4096)
                                 are solved by ONE CTA with every vector in shared memory (no grid barrier);
                                 0: off (the cooperative persistent kernel takes them) */
+  ECMG_OPT_PERS_TMA = 14,    /* constant-stencil levels with at most this many free unknowns (default
+                                3000000, i.e. up to 128^3) and more than ECMG_OPT_PERSISTENT run the whole
+                                tolerance-stopped solve as ONE cooperative launch of TMA z-marching passes
+                                (no per-iteration kernel launches); 0: the CUDA-graph loop of K1 / K2 */
   ECMG_OPT_SETUP_CTAS = 11,  /* tuning: CTAs per SM of the fp64-ALU-bound volume-load kernel when it runs
                                 ahead (0 = one CTA per work item, the full grid) */
   ECMG_OPT_VIRTUAL_SLABS = 6 /* P in 2..16: run the z-slab decomposition with P slabs on this one GPU

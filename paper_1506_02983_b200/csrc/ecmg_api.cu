@@ -71,6 +71,7 @@ struct ecmg_grid {
   int pdl = 0;              // ECMG_OPT_PDL: programmatic dependent launch between the JCG kernels (measured: no gain
                             // inside the CUDA graphs, tools/tune_pdl.py; off by default)
   long long cta_max = 1000;           // ECMG_OPT_CTA_SOLVE: one-CTA solve up to this many free unknowns (0: off)
+  long long pers_tma_max = 3000000;   // ECMG_OPT_PERS_TMA: constant stencil, one cooperative TMA solve up to this size
   long long persistent_max = 300000;  // ECMG_OPT_PERSISTENT: one cooperative launch per solve up to this size (tools/tune_persistent.py)
   double* aux[2] = {nullptr, nullptr};   // persistent element-path solve: w = A p and D^-1 (level-sized)
   long long aux_doubles = 0;
@@ -326,6 +327,22 @@ bool use_persistent(const ecmg_grid* G, const LevelGeom& g) {
   return nbricks <= persistent_max_bricks(G->elem_path);   // every brick's nodes stay in registers
 }
 
+// mid-size levels, constant stencil: the whole solve in one cooperative launch of TMA z-marching passes
+bool use_pers_tma(ecmg_grid* G, const LevelGeom& g) {
+  if (G->slab || G->elem_path || G->kernel_variant != 1 || G->pers_tma_max <= 0 || free_count(g) > G->pers_tma_max)
+    return false;
+  return ensure_maps(G, g, level_of(G, g));
+}
+
+cudaError_t launch_pers_tma(ecmg_grid* G, const LevelGeom& g) {
+  const int k = level_of(G, g);
+  const ConstStencil cs = make_const_stencil(g, 1.0, G->precond);
+  const auto& M = G->maps;
+  CUtensorMap maps[7] = {M.xh, M.rh, M.ph[0], M.ph[1], M.xi, M.ri, M.bi};
+  (void)k;
+  return launch_jcg_const_pers(g, cs, G->x, G->r, G->p[0], G->p[1], G->partials, G->sc, maps, G->stream);
+}
+
 // the whole solve of a small level in one cooperative launch (kernels_jcg_persistent.cu)
 cudaError_t launch_persistent(ecmg_grid* G, const LevelGeom& g) {
   const int k = level_of(G, g);
@@ -382,6 +399,8 @@ int enqueue_jcg(ecmg_grid* G, int k, double eps, int max_iter, double* u_out, Pa
   ECMG_CUDA(cudaMemcpyAsync(&G->sc->in, param, sizeof(JcgParams), cudaMemcpyHostToDevice, G->stream));
   if (persistent) {
     ECMG_CUDA(launch_persistent(G, g));
+  } else if (use_pers_tma(G, g)) {
+    ECMG_CUDA(launch_pers_tma(G, g));
   } else {
     if ((int)G->graphs.size() != G->L) G->graphs.assign(G->L, nullptr);
     if (!G->graphs[k]) ECMG_CUDA(build_level_graph(G, k, &G->graphs[k]));
@@ -409,6 +428,17 @@ int run_jcg(ecmg_grid* G, int k, double eps, int max_iter, double* u_out, ecmg_s
   G->param_host->u_out = u_out;
   ECMG_CUDA(cudaMemcpyAsync(&G->sc->in, G->param_host, sizeof(JcgParams), cudaMemcpyHostToDevice, G->stream));
   if (use_persistent(G, g)) return run_jcg_persistent(G, k, eps, st);
+  if (eps > 0.0 && G->use_graph && use_pers_tma(G, g)) {
+    ECMG_CUDA(cudaEventRecord(G->ev[0], G->stream));
+    ECMG_CUDA(launch_pers_tma(G, g));
+    ECMG_CUDA(cudaEventRecord(G->ev[1], G->stream));
+    ECMG_CUDA(cudaMemcpyAsync(&G->sc_host[0], G->sc, sizeof(JcgScalars), cudaMemcpyDeviceToHost, G->stream));
+    ECMG_CUDA(cudaStreamSynchronize(G->stream));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, G->ev[0], G->ev[1]);
+    G->last_jcg_ms = ms;
+    return fill_stats(G, g, eps, st);
+  }
   if (eps > 0.0 && G->use_graph) return run_jcg_graph(G, k, eps, st);
   // r = b - A x, rho = r.z, rr = r.r, stop test
   {
@@ -591,7 +621,8 @@ int ecmg_create_grid(const ecmg_box* dom, const int coarsest_cells[3], int num_l
     for (auto& e : G->lvl_ev) cudaEventCreate(&e);
   }
   if (st == ECMG_OK && (init_tma_kernel_attributes() != cudaSuccess || init_elem_kernel_attributes() != cudaSuccess ||
-                        init_setup_kernel_attributes() != cudaSuccess || init_cta_kernel_attributes() != cudaSuccess))
+                        init_setup_kernel_attributes() != cudaSuccess || init_cta_kernel_attributes() != cudaSuccess ||
+                        init_pers_kernel_attributes() != cudaSuccess))
     st = ECMG_ECUDA;
   if (st == ECMG_OK) {
     for (int i = 0; i < 16; ++i) cudaEventCreate(&G->ev[i]);
@@ -709,6 +740,7 @@ int ecmg_set_option(ecmg_grid* G, int option, int value) {
     case ECMG_OPT_KERNEL: if (value != 0 && value != 1) return ECMG_EINVAL; G->kernel_variant = value; clear_graphs(G); break;
     case ECMG_OPT_GRAPH: if (value != 0 && value != 1) return ECMG_EINVAL; G->use_graph = value; break;
     case ECMG_OPT_PERSISTENT: if (value < 0) return ECMG_EINVAL; G->persistent_max = value; break;
+    case ECMG_OPT_PERS_TMA: if (value < 0) return ECMG_EINVAL; G->pers_tma_max = value; break;
     case ECMG_OPT_CTA_SOLVE: if (value < 0) return ECMG_EINVAL; G->cta_max = value; break;
     case ECMG_OPT_PDL: if (value != 0 && value != 1) return ECMG_EINVAL; G->pdl = value; clear_graphs(G); break;
     case ECMG_OPT_FUSED_HALO: if (value != 0 && value != 1) return ECMG_EINVAL; G->fused_halo = value; break;

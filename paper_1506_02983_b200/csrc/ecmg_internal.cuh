@@ -159,6 +159,9 @@ namespace ecmg {
 cudaError_t launch_jcg_const_tma(int mode, const LevelGeom& g, const ConstStencil& cs, const KArgs& a,
                                  const CUtensorMap* maps, cudaStream_t st);
 int make_vec_tensor_map(CUtensorMap* map, const double* base, const LevelGeom& g, int bx, int by);
+cudaError_t init_pers_kernel_attributes();
+cudaError_t launch_jcg_const_pers(const LevelGeom& g, const ConstStencil& cs, double* x, double* r, double* p0, double* p1,
+                                  double* partials, JcgScalars* sc, const CUtensorMap* maps, cudaStream_t st);
 // z-slabs: finalize pass after the allreduce, and the in-order sum of P slabs' partial dots
 // (virtual slabs on one GPU; NCCL's allreduce on real ranks)
 cudaError_t launch_finalize(int mode, const KArgs& a, cudaStream_t st);

@@ -12,6 +12,9 @@
 // __syncthreads, so no separate "empty" barrier is needed.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cooperative_groups.h>
+#include <type_traits>
+#include <algorithm>
 #include "ecmg_internal.cuh"
 #include "jcg_common.cuh"
 
@@ -71,57 +74,31 @@ __device__ __forceinline__ void issue_stage(unsigned char* smem, uint64_t* full,
   if (kNI >= 2) tma_load_3d(base + HSTRIDE * (kH1 ? 2 : 1) + IBYTES, pI1, X0, Y0, zh - 1, &full[st]);
 }
 
-template <int MODE, int NS>
-__global__ void __launch_bounds__(NTH, 2)
-    k_jcg_const_tma(const LevelGeom g, const ConstStencil cs, const KArgs a, const __grid_constant__ CUtensorMap mH0,
-                    const __grid_constant__ CUtensorMap mH1, const __grid_constant__ CUtensorMap mI0,
-                    const __grid_constant__ CUtensorMap mI1) {
+// One z-march of the CTA over its (tile, z chunk) in mode MODE: the per-plane TMA pipeline of the kernels
+// below, with the stage ring continuing at the running step count gstep (stage (gstep + s) % NS, parity
+// ((gstep + s) / NS) & 1), so that a persistent CTA can run several passes over the same mbarriers.
+// Returns the thread's partial sums in acc0..acc2. The caller has initialised the mbarriers and
+// synchronised the CTA since its previous pass.
+template <int MODE, int NS, int SBYTES>
+__device__ __forceinline__ void tma_pass(const LevelGeom& g, const ConstStencil& cs, const KArgs& a, int X0, int Y0, int z0,
+                                         int z1, double bcg, bool first, double alpha, double* u_out,
+                                         const CUtensorMap* pH0, const CUtensorMap* pH1, const CUtensorMap* pI0,
+                                         const CUtensorMap* pI1, unsigned char* smem, uint64_t* full, uint32_t gstep,
+                                         double& acc0, double& acc1, double& acc2) {
   constexpr bool kH1 = (MODE == MODE_K1);
   constexpr int kNI = (MODE == MODE_K2) ? 2 : ((MODE == MODE_INIT || MODE == MODE_TRUE) ? 1 : 0);
-  constexpr int SBYTES = HSTRIDE * (kH1 ? 2 : 1) + IBYTES * kNI;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t full[NS];
-  // TMA destinations must be 128-byte aligned in the shared window: align the stage base explicitly
-  // (offset from smem_raw, not a uintptr_t round trip: the pointer must stay in the shared window so
-  // the reads compile to LDS, not generic LD)
-  unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
-  JcgScalars* sc = a.sc;
-  pdl_trigger();
-  pdl_wait();
-  if (MODE == MODE_K1 || MODE == MODE_K2) {
-    if (*(volatile int*)&sc->done) return;
-  }
   const int lane = threadIdx.x, w = threadIdx.y, tid = lane + TX * w;
   const int nfx = g.nf[0], nfy = g.nf[1];
   const long long P = g.P, S = g.S;
-  const int X0 = blockIdx.x * TX, Y0 = blockIdx.y * TY;
-  const int z0 = g.zbeg + blockIdx.z * a.zc;
-  const int z1 = min(z0 + a.zc, g.zend);
   const int x = X0 + lane, yb = Y0 + RY * w;
   const int nsteps = z1 - z0 + 2;
-
-  double bcg = 0.0, alpha = 0.0;
-  bool first = false;
-  if (MODE == MODE_K1) { bcg = sc->beta; first = (sc->iter == 0); }
-  if (MODE == MODE_K2) alpha = sc->alpha;
-  double* const u_out = (MODE == MODE_TRUE) ? sc->in.u_out : nullptr;
   const double dinv = cs.dinv;
   const uint32_t tx_bytes = HBYTES + ((kH1 && !first) ? HBYTES : 0) + IBYTES * kNI;
-
   auto stage_ptr = [&](int st) { return smem + st * SBYTES; };
-  // descriptor addresses taken directly from the __grid_constant__ parameters (param space)
-  const CUtensorMap* pH0 = &mH0;
-  const CUtensorMap* pH1 = &mH1;
-  const CUtensorMap* pI0 = &mI0;
-  const CUtensorMap* pI1 = &mI1;
   if (tid == 0) {
-    for (int i = 0; i < NS; ++i) mbar_init(&full[i], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (tid == 0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic accesses before async-proxy writes
     for (int t = 0; t < NS - 1 && t < nsteps; ++t)
-      issue_stage<kH1, kNI, SBYTES>(smem, full, t % NS, t, z0, X0, Y0, tx_bytes, first, pH0, pH1, pI0, pI1);
+      issue_stage<kH1, kNI, SBYTES>(smem, full, (gstep + t) % NS, t, z0, X0, Y0, tx_bytes, first, pH0, pH1, pI0, pI1);
   }
 
   // halo ring slot of this thread (transform in place, K1 only): rows y = Y0-1, Y0+32 (x = X0-1 ..
@@ -141,18 +118,17 @@ __global__ void __launch_bounds__(NTH, 2)
   double part[RY], q1p[RY], pp[RY];
 #pragma unroll
   for (int j = 0; j < RY; ++j) { part[j] = q1p[j] = pp[j] = 0.0; }
-  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
 
   for (int s = 0; s < nsteps; ++s) {
     const int zl = z0 - 1 + s;
-    const int st = s % NS;
+    const int st = (gstep + s) % NS;
     if (s > 0) __syncthreads();   // every thread is done with step s-1: its stage may be refilled
     if (tid == 0 && s + NS - 1 < nsteps) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes before async-proxy writes
       const int t = s + NS - 1;                                      // into stage (s-1) % NS
-      issue_stage<kH1, kNI, SBYTES>(smem, full, t % NS, t, z0, X0, Y0, tx_bytes, first, pH0, pH1, pI0, pI1);
+      issue_stage<kH1, kNI, SBYTES>(smem, full, (gstep + t) % NS, t, z0, X0, Y0, tx_bytes, first, pH0, pH1, pI0, pI1);
     }
-    mbar_wait(&full[st], (uint32_t)((s / NS) & 1));
+    mbar_wait(&full[st], (uint32_t)(((gstep + s) / NS) & 1));
     double* H = reinterpret_cast<double*>(stage_ptr(st));
     if (MODE == MODE_K1) {
       const double* H1 = reinterpret_cast<const double*>(stage_ptr(st) + HSTRIDE);
@@ -224,8 +200,160 @@ __global__ void __launch_bounds__(NTH, 2)
       pp[j] = cc;
     }
   }
+}
+
+template <int MODE, int NS>
+__global__ void __launch_bounds__(NTH, 2)
+    k_jcg_const_tma(const LevelGeom g, const ConstStencil cs, const KArgs a, const __grid_constant__ CUtensorMap mH0,
+                    const __grid_constant__ CUtensorMap mH1, const __grid_constant__ CUtensorMap mI0,
+                    const __grid_constant__ CUtensorMap mI1) {
+  constexpr bool kH1 = (MODE == MODE_K1);
+  constexpr int kNI = (MODE == MODE_K2) ? 2 : ((MODE == MODE_INIT || MODE == MODE_TRUE) ? 1 : 0);
+  constexpr int SBYTES = HSTRIDE * (kH1 ? 2 : 1) + IBYTES * kNI;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full[NS];
+  // TMA destinations must be 128-byte aligned in the shared window: align the stage base explicitly
+  // (offset from smem_raw, not a uintptr_t round trip: the pointer must stay in the shared window so
+  // the reads compile to LDS, not generic LD)
+  unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  JcgScalars* sc = a.sc;
+  pdl_trigger();
+  pdl_wait();
+  if (MODE == MODE_K1 || MODE == MODE_K2) {
+    if (*(volatile int*)&sc->done) return;
+  }
+  const int tid = threadIdx.x + TX * threadIdx.y;
+  const int X0 = blockIdx.x * TX, Y0 = blockIdx.y * TY;
+  const int z0 = g.zbeg + blockIdx.z * a.zc;
+  const int z1 = min(z0 + a.zc, g.zend);
+  double bcg = 0.0, alpha = 0.0;
+  bool first = false;
+  if (MODE == MODE_K1) { bcg = sc->beta; first = (sc->iter == 0); }
+  if (MODE == MODE_K2) alpha = sc->alpha;
+  double* const u_out = (MODE == MODE_TRUE) ? sc->in.u_out : nullptr;
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) mbar_init(&full[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+  tma_pass<MODE, NS, SBYTES>(g, cs, a, X0, Y0, z0, z1, bcg, first, alpha, u_out, &mH0, &mH1, &mI0, &mI1, smem, full, 0u,
+                             acc0, acc1, acc2);
   if ((MODE == MODE_K2 || MODE == MODE_INIT) && (a.peer_lo || a.peer_hi)) __threadfence_system();   // peer stores
   if (MODE != MODE_APPLY) reduce_finalize(MODE, a, acc0, acc1, acc2);
+}
+
+// ---- the whole JCG solve of a level in ONE cooperative launch, TMA z-marching passes -------------
+// (mid-size levels, e.g. 128^3: a launched K1/K2 pair costs ~36 us there, mostly launch, pipeline fill
+// and tail, against ~20 us of traffic). Each CTA owns a fixed list of (tile, z chunk) items and runs
+// init -> { K1 pass, grid sum, K2 pass, grid sum } -> true residual; the grid sums are deterministic
+// (per-CTA partials, grid barrier, every CTA reduces all partials in CTA order), so every CTA holds the
+// same CG scalars and takes the same stop decision. Same per-node arithmetic as the kernels above.
+constexpr int PS_NS = 3;
+constexpr int PS_SBYTES = HSTRIDE + 2 * IBYTES;   // the largest stage (K2: p halo + x, r interior)
+static_assert(PS_SBYTES >= 2 * HSTRIDE, "K1 stage (r and p_old halo boxes) must fit");
+
+struct PersMaps { CUtensorMap xh, rh, ph0, ph1, xi, ri, bi; };
+
+__device__ __forceinline__ void pers_grid_sum3(double v[3], double* partials, int& buf, double* red,
+                                               cooperative_groups::grid_group& grid) {
+  block_sum3(v[0], v[1], v[2], red);   // thread 0 holds the CTA sums
+  const int tid = threadIdx.x + TX * threadIdx.y;
+  double* pb = partials + (size_t)buf * gridDim.x * 3;
+  if (tid == 0)
+    for (int k = 0; k < 3; ++k) pb[3 * blockIdx.x + k] = v[k];
+  grid.sync();
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  for (unsigned c = tid; c < gridDim.x; c += NTH) {
+    s0 += __ldcg(pb + 3 * c);
+    s1 += __ldcg(pb + 3 * c + 1);
+    s2 += __ldcg(pb + 3 * c + 2);
+  }
+  block_sum3(s0, s1, s2, red);
+  __shared__ double bc[3];
+  if (tid == 0) { bc[0] = s0; bc[1] = s1; bc[2] = s2; }
+  __syncthreads();
+  v[0] = bc[0]; v[1] = bc[1]; v[2] = bc[2];
+  __syncthreads();
+  buf ^= 1;
+}
+
+__global__ void __launch_bounds__(NTH, 2)
+    k_jcg_const_pers(const LevelGeom g, const ConstStencil cs, double* x, double* r, double* p0, double* p1, double* partials,
+                     JcgScalars* sc, int zc, int ntx, int nty, int items, const __grid_constant__ PersMaps M) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full[PS_NS];
+  __shared__ double red[3 * (NTH / 32)];
+  unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  const int tid = threadIdx.x + TX * threadIdx.y;
+  if (tid == 0) {
+    for (int i = 0; i < PS_NS; ++i) mbar_init(&full[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const double eps = sc->in.eps;
+  const int max_iter = sc->in.max_iter;
+  double* const u_out = sc->in.u_out;
+  uint32_t gstep = 0;
+  int buf = 0;
+  KArgs a{};
+  // one pass of MODE over this CTA's items
+  auto pass = [&](auto mode_tag, const CUtensorMap* h0, const CUtensorMap* h1, const CUtensorMap* i0, const CUtensorMap* i1,
+                  double bcg, bool first, double alpha, double v[3]) {
+    constexpr int MODE = decltype(mode_tag)::value;
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+    for (int it = blockIdx.x; it < items; it += gridDim.x) {
+      const int X0 = (it % ntx) * TX, Y0 = ((it / ntx) % nty) * TY;
+      const int z0 = (it / (ntx * nty)) * zc, z1 = min(z0 + zc, g.zend);
+      tma_pass<MODE, PS_NS, PS_SBYTES>(g, cs, a, X0, Y0, z0, z1, bcg, first, alpha, u_out, h0, h1, i0, i1, smem, full,
+                                       gstep, acc0, acc1, acc2);
+      gstep += (uint32_t)(z1 - z0 + 2);
+      __syncthreads();   // every stage consumed before the next pass's prefill
+    }
+    // this pass's global stores are read by other CTAs' TMA (async proxy) in the next pass
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    v[0] = acc0; v[1] = acc1; v[2] = acc2;
+    pers_grid_sum3(v, partials, buf, red, grid);
+    if (tid == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
+  };
+  // init: r = b - A x, rho = r.z, rr, ||b||^2
+  double v[3];
+  a.o0 = r;
+  pass(std::integral_constant<int, MODE_INIT>{}, &M.xh, &M.xh, &M.bi, &M.bi, 0.0, false, 0.0, v);
+  double rho = v[0], rr = v[1];
+  const double bb = v[2];
+  const double nb = sqrt(bb), nbe = nb > 0.0 ? nb : 1.0;
+  const double thresh = eps > 0.0 ? eps * nbe : -1.0;
+  int status = ST_OK, iter = 0;
+  double beta = 0.0;
+  bool done = (max_iter <= 0) || (thresh > 0.0 && !(sqrt(rr) > thresh));
+  if (!isfinite(rr)) { status = ST_EBREAKDOWN; done = true; }
+  int cur = 0;   // p_cur holds p_old
+  while (!done) {
+    double* pnew = cur ? p0 : p1;
+    a.o0 = pnew;
+    pass(std::integral_constant<int, MODE_K1>{}, &M.rh, cur ? &M.ph1 : &M.ph0, &M.rh, &M.rh, beta, iter == 0, 0.0, v);
+    const double sigma = v[0];
+    if (!(sigma > 0.0)) { status = ST_EBREAKDOWN; break; }
+    const double alpha = rho / sigma;
+    a.o0 = x; a.o1 = r;
+    pass(std::integral_constant<int, MODE_K2>{}, cur ? &M.ph0 : &M.ph1, &M.rh, &M.xi, &M.ri, 0.0, false, alpha, v);
+    beta = v[0] / rho;
+    rho = v[0];
+    rr = v[1];
+    cur ^= 1;
+    ++iter;
+    done = (iter >= max_iter) || (thresh > 0.0 && !(sqrt(rr) > thresh));
+    if (!isfinite(rr)) { status = ST_EBREAKDOWN; done = true; }
+  }
+  // true residual ||b - A x|| and the fused scatter of u_h
+  pass(std::integral_constant<int, MODE_TRUE>{}, &M.xh, &M.xh, &M.bi, &M.bi, 0.0, false, 0.0, v);
+  if (blockIdx.x == 0 && tid == 0) {
+    sc->rho = rho; sc->rr = rr; sc->bb = bb; sc->rr_true = v[1]; sc->beta = beta;
+    sc->iter = iter; sc->max_iter = max_iter; sc->thresh = thresh; sc->status = status; sc->done = 1;
+    sc->counter = 0;
+  }
 }
 
 template <int MODE, int NS>
@@ -297,6 +425,44 @@ int make_vec_tensor_map(CUtensorMap* map, const double* base, const LevelGeom& g
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : -1;
+}
+
+// grid of the persistent TMA solve: at most the co-resident CTAs (2 per SM); z chunks sized so that the
+// (tile, chunk) items come to about one per CTA
+static int pers_slots() {
+  static int slots = 0;
+  if (!slots) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jcg_const_pers, NTH, PS_SBYTES * PS_NS + 128);
+    slots = sms * std::max(1, per_sm);
+  }
+  return slots;
+}
+
+cudaError_t init_pers_kernel_attributes() {
+  return cudaFuncSetAttribute(k_jcg_const_pers, cudaFuncAttributeMaxDynamicSharedMemorySize, PS_SBYTES * PS_NS + 128);
+}
+
+// maps: x halo, r halo, p0 halo, p1 halo, x interior, r interior, b interior (make_vec_tensor_map)
+cudaError_t launch_jcg_const_pers(const LevelGeom& g, const ConstStencil& cs, double* x, double* r, double* p0, double* p1,
+                                  double* partials, JcgScalars* sc, const CUtensorMap* maps, cudaStream_t st) {
+  const int ntx = (g.nf[0] + TX - 1) / TX, nty = (g.nf[1] + TY - 1) / TY;
+  const int nz = g.zend - g.zbeg;
+  const int slots = pers_slots();
+  const long long tiles = (long long)ntx * nty;
+  if (tiles > slots || g.zbeg != 0) return cudaErrorInvalidValue;
+  const int nch = (int)std::max(1LL, slots / tiles);          // z chunks per tile
+  const int zc = (nz + nch - 1) / nch;
+  const int items = (int)(tiles * ((nz + zc - 1) / zc));
+  PersMaps M{maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6]};
+  int grid = std::min(items, slots);
+  void* args[] = {(void*)&g, (void*)&cs, (void*)&x, (void*)&r, (void*)&p0, (void*)&p1, (void*)&partials, (void*)&sc,
+                  (void*)&zc, (void*)&ntx, (void*)&nty, (void*)&items, (void*)&M};
+  count_launch();
+  return cudaLaunchCooperativeKernel((const void*)k_jcg_const_pers, dim3(grid), dim3(TX, WARPS), args,
+                                     PS_SBYTES * PS_NS + 128, st);
 }
 
 int tma_halo_box_x() { return HX; }

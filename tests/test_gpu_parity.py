@@ -160,6 +160,7 @@ def test_tolerance_stopped_solve(pid, eps):
 
 @pytest.mark.parametrize("pid,levels,eps,variant", [
     (o.C1, 4, 1e-8, 0), (o.C2, 5, 1e-10, 0), (o.C3, 5, 1e-10, 0), (o.C4, 5, 1e-9, 0), (o.C5, 5, 1e-8, 0),
+    (o.C2, 6, 1e-10, 0), (o.C4, 6, 1e-9, 0),
     (o.P1, 4, 1e-9, 1), (o.P1, 4, 1e-9, 0), (o.P2, 4, 1e-12, 1), (o.P3, 4, 1e-11, 0)])
 def test_ecmg_run(pid, levels, eps, variant):
     n0 = (10, 4, 5) if pid == o.P2 else ((8,) * 3 if pid in (o.P1, o.P3) else (4,) * 3)
@@ -392,3 +393,25 @@ def test_cta_solve_vs_persistent(pid, eps):
     assert ost == 0
     assert all(abs(a - int(b)) <= 1 for a, b in zip(res[0][0][2:], ostats[2:, 0]))
     assert np.max(np.abs(res[0][1] - ou)) <= 1e-9 * np.max(np.abs(ou))
+
+
+@pytest.mark.parametrize("pid,eps", [(o.C2, 1e-10), (o.C4, 1e-9), (o.C1, 1e-8)])
+def test_persistent_tma_vs_graph(pid, eps):
+    # constant-stencil levels between ECMG_OPT_PERSISTENT and ECMG_OPT_PERS_TMA (here 128^3) run the
+    # whole solve as one cooperative launch of the TMA z-marching passes; the CUDA-graph K1/K2 loop is
+    # the reference: same per-node arithmetic, reductions in another order -> counts +-1, solutions within
+    # rounding; also a tolerance-stopped solve_level from a seeded guess
+    res = []
+    for pt in (3000000, 0):
+        g = Grid(4, 6, pid, params_for(pid))
+        g.set_option(ecmg.OPT_PERS_TMA, pt)
+        u, ut = g.new_vec(5), g.new_vec(5)
+        st, stats = g.run(eps, u, ut)
+        assert st == 0
+        x = dev(synth.random_nodal(14, (128,) * 3, (1, 1, 1), (127,) * 3))
+        sst = g.solve_level(5, eps, 10000, x)
+        res.append(([s["iterations"] for s in stats], host(u), host(ut), sst, host(x)))
+    assert all(abs(a - b) <= 1 for a, b in zip(res[0][0], res[1][0]))
+    for k in (1, 2, 4):
+        assert np.max(np.abs(res[0][k] - res[1][k])) <= 1e-9 * np.max(np.abs(res[1][k]))
+    assert abs(res[0][3][1]["iterations"] - res[1][3][1]["iterations"]) <= 1
