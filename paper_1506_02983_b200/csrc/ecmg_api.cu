@@ -48,6 +48,7 @@ struct ecmg_grid {
   std::vector<double*> s1d;        // per-level 1D Gauss load tables (separable right-hand sides)
   std::vector<char> setup_ok;      // level k's b / beta hold the current problem's data
   int setup_ahead = 1;             // ECMG_OPT_SETUP_AHEAD
+  int beta_fly = 1;                // ECMG_OPT_BETA_FLY: element kernels form analytic beta from axis tables
   int exp_fused = 1;               // ECMG_OPT_EXP_KERNEL: 1 fused one-pass EXP_finite, 0 seeds + interpolation passes
   int setup_ctas = 0;              // ECMG_OPT_SETUP_CTAS: CTAs per SM of the ALU-bound RHS kernel when run ahead
   cudaStream_t hi_stream = nullptr, lo_stream = nullptr;   // ecmg_run: solves (high) / level setup (low priority)
@@ -128,6 +129,7 @@ SlabCfg slab_cfg(const ecmg_grid* G) {
   c.kernel_variant = G->kernel_variant;
   c.zchunk = G->zchunk;
   c.fused_halo = G->fused_halo;
+  c.beta_fly = G->beta_fly;
   return c;
 }
 
@@ -167,7 +169,8 @@ int level_of(const ecmg_grid* G, const LevelGeom& g) {
 
 cudaError_t launch_mode(ecmg_grid* G, int mode, const LevelGeom& g, const KArgs& a) {
   if (G->elem_path) {
-    const ElemStencil es = make_elem_stencil(g, G->prob, G->precond);
+    ElemStencil es = make_elem_stencil(g, G->prob, G->precond);
+    if (G->beta_fly && a.beta) set_beta_fly(es, g, G->prob, a.beta);
     return launch_jcg_elem(mode, g, es, G->prob, a, G->stream);
   }
   const ConstStencil cs = make_const_stencil(g, 1.0, G->precond);
@@ -329,17 +332,22 @@ bool use_persistent(const ecmg_grid* G, const LevelGeom& g) {
 
 // mid-size levels, constant stencil: the whole solve in one cooperative launch of TMA z-marching passes
 bool use_pers_tma(ecmg_grid* G, const LevelGeom& g) {
-  if (G->slab || G->elem_path || G->kernel_variant != 1 || G->pers_tma_max <= 0 || free_count(g) > G->pers_tma_max)
-    return false;
-  return ensure_maps(G, g, level_of(G, g));
+  if (G->slab || G->pers_tma_max <= 0 || free_count(g) > G->pers_tma_max) return false;
+  if (G->elem_path) return true;
+  return G->kernel_variant == 1 && ensure_maps(G, g, level_of(G, g));
 }
 
 cudaError_t launch_pers_tma(ecmg_grid* G, const LevelGeom& g) {
   const int k = level_of(G, g);
   const ConstStencil cs = make_const_stencil(g, 1.0, G->precond);
+  if (G->elem_path) {
+    ElemStencil es = make_elem_stencil(g, G->prob, G->precond);
+    if (G->beta_fly) set_beta_fly(es, g, G->prob, G->betal[k]);
+    return launch_jcg_elem_pers(g, es, G->x, G->r, G->zv, G->p[0], G->p[1], G->bl[k], G->betal[k], G->partials, G->sc,
+                                G->stream);
+  }
   const auto& M = G->maps;
   CUtensorMap maps[7] = {M.xh, M.rh, M.ph[0], M.ph[1], M.xi, M.ri, M.bi};
-  (void)k;
   return launch_jcg_const_pers(g, cs, G->x, G->r, G->p[0], G->p[1], G->partials, G->sc, maps, G->stream);
 }
 
@@ -622,7 +630,7 @@ int ecmg_create_grid(const ecmg_box* dom, const int coarsest_cells[3], int num_l
   }
   if (st == ECMG_OK && (init_tma_kernel_attributes() != cudaSuccess || init_elem_kernel_attributes() != cudaSuccess ||
                         init_setup_kernel_attributes() != cudaSuccess || init_cta_kernel_attributes() != cudaSuccess ||
-                        init_pers_kernel_attributes() != cudaSuccess))
+                        init_pers_kernel_attributes() != cudaSuccess || init_elem_pers_attributes() != cudaSuccess))
     st = ECMG_ECUDA;
   if (st == ECMG_OK) {
     for (int i = 0; i < 16; ++i) cudaEventCreate(&G->ev[i]);
@@ -734,6 +742,7 @@ int ecmg_set_option(ecmg_grid* G, int option, int value) {
     case ECMG_OPT_EXP_VARIANT: if (value != 0 && value != 1) return ECMG_EINVAL; G->exp_variant = value; break;
     case ECMG_OPT_PRECOND: if (value != 0 && value != 1) return ECMG_EINVAL; G->precond = value; invalidate_setup(G); clear_graphs(G); break;
     case ECMG_OPT_SETUP_AHEAD: if (value < 0 || value > 3) return ECMG_EINVAL; G->setup_ahead = value; break;
+    case ECMG_OPT_BETA_FLY: if (value != 0 && value != 1) return ECMG_EINVAL; G->beta_fly = value; clear_graphs(G); break;
     case ECMG_OPT_EXP_KERNEL: if (value != 0 && value != 1) return ECMG_EINVAL; G->exp_fused = value; break;
     case ECMG_OPT_SETUP_CTAS: if (value < 0) return ECMG_EINVAL; G->setup_ctas = value; break;
     case ECMG_OPT_ZCHUNK: if (value < 0) return ECMG_EINVAL; G->zchunk = value; clear_graphs(G); break;

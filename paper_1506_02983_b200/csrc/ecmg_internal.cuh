@@ -64,7 +64,39 @@ struct ElemStencil {
   double robin[6];     // alpha_F * h1 * h2 for Robin faces with alpha != 0, else 0
   int precond;         // 1 = Jacobi, 0 = plain CG (dinv = 1)
   int cube;            // h_x = h_y = h_z: kappa = c{4,0,0,-1,0,-1,-1,-1} (the element kernel's short form)
+  // beta on the fly (analytic beta, BETA_KIND_*): the element kernels form beta_e from per-axis tables in
+  // registers instead of reading the beta array (8 B per unknown less in each of K1 and K2). bkind < 0:
+  // read the array. baxes: the tables of the level (beta_axes_* below), written by launch_beta.
+  int bkind;
+  int bw;              // table row width W = max_d n_d + 4
+  const double* baxes;
 };
+
+// Analytic beta at element centroids (Eq. bvp, reading A3) from per-axis tables, so that the beta array
+// (k_beta) and the element kernels' on-the-fly values are the same function of the same table entries:
+//   kind 0 (beta = 1): valid ? 1 : 0
+//   kind 1 (C3: 1 + 1/2 sin 2pi x cos 2pi y sin 2pi z): valid ? fma(Ax Ay, Az, 1) : 0, Ax = sin(2pi x)/2, Ay = cos, Az = sin
+//   kind 2 (layers in z): valid ? Az : 0, Az = layer beta at the centroid's z
+//   kind 3 (C5: layers + 4 boxes, a later box overriding an earlier one): the highest box whose x, y and z
+//          ranges all contain the centroid, else the layer value
+// Tables at baxes: A[3][W] doubles, then M[3][W] ints (bit 4: the element exists, bits 0-3: inside box k
+// along that axis), then the 4 box betas; entry (d, e) for element index e in [-2, n_d + 1] at e + 2.
+enum { BETA_KIND_ONE = 0, BETA_KIND_C3 = 1, BETA_KIND_LAYERS = 2, BETA_KIND_C5 = 3 };
+__host__ __device__ inline long long beta_axes_doubles(int W) { return 3LL * W + (3LL * W + 1) / 2 + 4 + 1; }
+__device__ __forceinline__ double beta_combine(int kind, double ax, double ay, double az, int mx, int my, int mz,
+                                               const double* boxb) {
+  const int m = mx & my & mz;
+  if (!(m & 16)) return 0.0;
+  switch (kind) {
+    case BETA_KIND_C3: return __fma_rn(ax * ay, az, 1.0);
+    case BETA_KIND_LAYERS: return az;
+    case BETA_KIND_C5: {
+      const int bits = m & 15;
+      return bits ? boxb[31 - __clz(bits)] : az;
+    }
+    default: return 1.0;
+  }
+}
 
 // Per-solve inputs, written by one host-to-device copy before the init pass (pinned host copy).
 struct JcgParams {
@@ -160,6 +192,10 @@ cudaError_t launch_jcg_const_tma(int mode, const LevelGeom& g, const ConstStenci
                                  const CUtensorMap* maps, cudaStream_t st);
 int make_vec_tensor_map(CUtensorMap* map, const double* base, const LevelGeom& g, int bx, int by);
 cudaError_t init_pers_kernel_attributes();
+cudaError_t init_elem_pers_attributes();
+cudaError_t launch_jcg_elem_pers(const LevelGeom& g, const ElemStencil& es, double* x, double* r, double* z, double* p0,
+                                 double* p1, const double* b, const double* beta, double* partials, JcgScalars* sc,
+                                 cudaStream_t st);
 cudaError_t launch_jcg_const_pers(const LevelGeom& g, const ConstStencil& cs, double* x, double* r, double* p0, double* p1,
                                   double* partials, JcgScalars* sc, const CUtensorMap* maps, cudaStream_t st);
 // z-slabs: finalize pass after the allreduce, and the in-order sum of P slabs' partial dots

@@ -227,7 +227,11 @@ bool slab_maps(SlabDriver* d, SlabCtx& c, int k) {
 cudaError_t slab_launch(SlabDriver* d, SlabCtx& c, int mode, int k, const KArgs& a, cudaStream_t st) {
   const SlabCfg& cf = d->cfg;
   const LevelGeom& g = c.geom[k];
-  if (cf.elem_path) return launch_jcg_elem(mode, g, make_elem_stencil(g, cf.prob, cf.precond), cf.prob, a, st);
+  if (cf.elem_path) {
+    ElemStencil es = make_elem_stencil(g, cf.prob, cf.precond);
+    if (cf.beta_fly && a.beta) set_beta_fly(es, g, cf.prob, a.beta);
+    return launch_jcg_elem(mode, g, es, cf.prob, a, st);
+  }
   const ConstStencil cs = make_const_stencil(g, 1.0, cf.precond);
   if (cf.kernel_variant == 1 && slab_maps(d, c, k)) {
     auto halo = [&](const double* p) -> const CUtensorMap* {

@@ -32,7 +32,18 @@ inline LevelGeom make_geom(const ecmg_box& dom, const int n0[3], int k, const in
   return g;
 }
 
-inline long long beta_doubles(const LevelGeom& g) { return g.BS * (g.n[2] + 4); }
+inline int beta_axes_w(const LevelGeom& g) { return std::max(g.n[0], std::max(g.n[1], g.n[2])) + 4; }
+// the element-beta array (zero ring of 2) followed by the per-axis tables of beta_combine
+inline long long beta_doubles(const LevelGeom& g) { return g.BS * (g.n[2] + 4) + beta_axes_doubles(beta_axes_w(g)); }
+inline const double* beta_axes_ptr(const LevelGeom& g, const double* beta) { return beta + g.BS * (g.n[2] + 4); }
+inline int beta_kind(int problem_id) {
+  switch (problem_id) {
+    case 3: return BETA_KIND_C3;
+    case 5: return BETA_KIND_C5;
+    case 22: return BETA_KIND_LAYERS;
+    default: return BETA_KIND_ONE;
+  }
+}
 
 inline ElemStencil make_elem_stencil(const LevelGeom& g, const Problem& pb, int precond) {
   ElemStencil es{};
@@ -55,6 +66,9 @@ inline ElemStencil make_elem_stencil(const LevelGeom& g, const Problem& pb, int 
   }
   es.precond = precond;
   es.cube = g.h[0] == g.h[1] && g.h[0] == g.h[2];
+  es.bkind = -1;   // the caller enables beta on the fly (set_beta_fly) where the tables exist
+  es.bw = 0;
+  es.baxes = nullptr;
   return es;
 }
 
@@ -194,4 +208,13 @@ inline LevelGeom slab_geom(LevelGeom g, int P, int r, bool* sharded) {
   return g;
 }
 
+}  // namespace ecmg
+
+namespace ecmg {
+// element kernels form beta from the level's axis tables (analytic beta) instead of reading the array
+inline void set_beta_fly(ElemStencil& es, const LevelGeom& g, const Problem& pb, const double* beta) {
+  es.bkind = beta_kind(pb.id);
+  es.bw = beta_axes_w(g);
+  es.baxes = beta_axes_ptr(g, beta);
+}
 }  // namespace ecmg

@@ -33,6 +33,8 @@
 #include <cudaTypedefs.h>
 #include <algorithm>
 #include <mutex>
+#include <type_traits>
+#include <cooperative_groups.h>
 #include "ecmg_internal.cuh"
 #include "jcg_common.cuh"
 
@@ -92,69 +94,43 @@ struct ElemCfg {
 };
 
 // loads of step t: node plane zh = z0-1+t (halo boxes), element layer (zh-1, zh), interior plane zh-1
-template <int MODE>
+template <int MODE, int SB, int BF>
 __device__ __forceinline__ void issue_elem_stage(unsigned char* smem, uint64_t* full, int st, int t, int z0, int X0,
                                                  int Y0, int ey0, int ez_base, uint32_t tx_bytes, bool first,
                                                  const CUtensorMap* pH0, const CUtensorMap* pH1, const CUtensorMap* pE,
                                                  const CUtensorMap* pI0, const CUtensorMap* pI1) {
   using C = ElemCfg<MODE>;
-  unsigned char* base = smem + st * C::SBYTES;
+  unsigned char* base = smem + st * SB;
   mbar_expect_tx(&full[st], tx_bytes);
   const int zh = z0 - 1 + t;
   tma_load_3d(base, pH0, X0 - XO, Y0 - 1, zh, &full[st]);
   if (C::kH1) tma_load_3d(base + HSTRIDE, pH1, X0 - XO, Y0 - 1, zh, &full[st]);
-  tma_load_3d(base + C::OFF_E, pE, X0, ey0, ez_base + zh, &full[st]);
+  if (BF == 0) tma_load_3d(base + C::OFF_E, pE, X0, ey0, ez_base + zh, &full[st]);   // else: beta on the fly
   if (C::kNI >= 1) tma_load_3d(base + C::OFF_I, pI0, X0, Y0, zh - 1, &full[st]);
   if (C::kNI >= 2) tma_load_3d(base + C::OFF_I + IBYTES, pI1, X0, Y0, zh - 1, &full[st]);
 }
 
-template <int MODE, int NS, bool CUBE>
-__global__ void __launch_bounds__(NTH, ELEM_MINB)
-    k_jcg_elem_tma(const LevelGeom g, const ElemStencil es, const KArgs a, const __grid_constant__ CUtensorMap mH0,
-                   const __grid_constant__ CUtensorMap mH1, const __grid_constant__ CUtensorMap mE,
-                   const __grid_constant__ CUtensorMap mI0, const __grid_constant__ CUtensorMap mI1) {
+// One z-march of the CTA over its (tile, z chunk) in mode MODE (the body of k_jcg_elem_tma): the stage
+// ring continues at the running step count G (stage (G + s) % NS, parity ((G + s) / NS) & 1), so that a
+// persistent CTA can run several passes over the same mbarriers. Adds the thread's partial sums to
+// acc0..acc2. The caller has initialised the mbarriers and synchronised the CTA since its previous pass.
+// BF: 0 = beta from the array (TMA box per layer); 1 = on the fly, product kind (C3); 2 = on the fly,
+// bit-mask kinds (beta = 1, layers, C5 boxes) -- see beta_combine
+template <int MODE, int NS, bool CUBE, int SB, int BF>
+__device__ __forceinline__ void elem_pass(const LevelGeom& g, const ElemStencil& es, const KArgs& a, int X0, int Y0, int z0,
+                                          int z1, double bcg_eff, bool first, double alpha, double* u_out,
+                                          const CUtensorMap* pH0, const CUtensorMap* pH1, const CUtensorMap* pE,
+                                          const CUtensorMap* pI0, const CUtensorMap* pI1, unsigned char* smem, uint64_t* full,
+                                          const uint32_t G, double& acc0, double& acc1, double& acc2) {
   using C = ElemCfg<MODE>;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t full[NS];
-  // (offset from smem_raw, not a uintptr_t round trip: the pointer must stay in the shared window so
-  // the reads compile to LDS, not generic LD)
-  unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
-  JcgScalars* sc = a.sc;
-  pdl_trigger();
-  pdl_wait();
-  if (MODE == MODE_K1 || MODE == MODE_K2) {
-    if (*(volatile int*)&sc->done) return;
-  }
   const int lane = threadIdx.x, w = threadIdx.y, tid = lane + TX * w;
   const int nfx = g.nf[0], nfy = g.nf[1];
   const long long S = g.S;
   const int P = (int)g.P;
-
-  double bcg = 0.0, alpha = 0.0;
-  bool first = false;
-  if (MODE == MODE_K1) { bcg = sc->beta; first = (sc->iter == 0); }
-  if (MODE == MODE_K2) alpha = sc->alpha;
-  double* const u_out = (MODE == MODE_TRUE) ? sc->in.u_out : nullptr;
-  // iteration 0 of K1 (p = z): the p_old slot is filled from z and beta_cg = 0 (exact for finite z), so
-  // the window update is one FMA with no per-element select
-  const double bcg_eff = first ? 0.0 : bcg;
-  const uint32_t tx_bytes = HBYTES * (C::kH1 ? 2 : 1) + EBYTES + IBYTES * C::kNI;
+  const uint32_t tx_bytes = HBYTES * (C::kH1 ? 2 : 1) + (BF ? 0 : EBYTES) + IBYTES * C::kNI;
   const int ez_base = g.flo[2] + g.zoff + 1;       // beta-array plane of the layer below node plane 0, + 1
   const int eo = g.flo[0] + 1;                     // smem column of the left element of lane 0
   const bool zrobin = es.robin[4] != 0.0 || es.robin[5] != 0.0;
-
-  const CUtensorMap* pH0 = &mH0;
-  const CUtensorMap* pH1 = (C::kH1 && first) ? &mH0 : &mH1;
-  const CUtensorMap* pE = &mE;
-  const CUtensorMap* pI0 = &mI0;
-  const CUtensorMap* pI1 = &mI1;
-  if (tid == 0) {
-    for (int i = 0; i < NS; ++i) mbar_init(&full[i], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-
-  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
 #define k0 es.kappa[0]
 #define k1 es.kappa[1]
 #define k2 es.kappa[2]
@@ -164,23 +140,13 @@ __global__ void __launch_bounds__(NTH, ELEM_MINB)
 #define k6 es.kappa[6]
 #define k7 es.kappa[7]
   constexpr double c9 = 1.0 / 9.0, c18 = 1.0 / 18.0, c36 = 1.0 / 36.0;
-
-  // Work distribution: grid (x tiles, y tiles, z chunks of a.zc planes). All tiles of a z chunk march
-  // side by side, so the halo rows / columns that neighbouring CTAs both read (boxes are 1.2-1.27x the
-  // tile) are L2 hits. (Measured: giving each of 2 x 148 persistent CTAs an equal contiguous range of
-  // the tile-major (tile, plane) space removes the partial last wave but de-phases neighbouring
-  // tiles, and costs 40 % at 256^3: 0.444 vs 0.315 ms per iteration.)
-  {
-  const uint32_t G = 0;
-  const int X0 = blockIdx.x * TX, Y0 = blockIdx.y * TY;
-  const int z0 = g.zbeg + blockIdx.z * a.zc;
-  const int z1 = min(z0 + a.zc, g.zend);
+  if (tid == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   const int x = X0 + lane, yb = Y0 + RY * w;
   const int nsteps = z1 - z0 + 2;
   const int ey0 = g.flo[1] + Y0 + 1;               // beta-array row of the element below node row Y0
   if (tid == 0) {
     for (int t = 0; t < NS - 1 && t < nsteps; ++t)
-      issue_elem_stage<MODE>(smem, full, (G + t) % NS, t, z0, X0, Y0, ey0, ez_base, tx_bytes, first, pH0, pH1, pE, pI0,
+      issue_elem_stage<MODE, SB, BF>(smem, full, (G + t) % NS, t, z0, X0, Y0, ey0, ez_base, tx_bytes, first, pH0, pH1, pE, pI0,
                              pI1);
   }
 
@@ -200,6 +166,39 @@ __global__ void __launch_bounds__(NTH, ELEM_MINB)
   double part[RY], dpart[RY];
 #pragma unroll
   for (int j = 0; j < RY; ++j) { part[j] = 0.0; dpart[j] = 0.0; }
+  // beta on the fly: the thread's 2 element columns x 3 element rows are fixed for the pass; per layer
+  // one (uniform) table entry. pk: 5 bits (exists, boxes) per (row, column); bt: products Ax Ay (C3)
+  const int BW = es.bw;
+  const double* tA = es.baxes;
+  const int* tM = reinterpret_cast<const int*>(es.baxes + 3LL * BW);
+  const double* boxb = es.baxes + 3LL * BW + (3LL * BW + 1) / 2;
+  int pk = 0;
+  double bt[RY + 1][2];
+  if (BF) {
+    double axc[2], ayr[RY + 1];
+    int mxc[2], myr[RY + 1];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int ex = X0 + g.flo[0] - 1 + lane + c;
+      const bool in = ex >= -2 && ex < g.n[0] + 2;
+      axc[c] = (BF == 1 && in) ? tA[ex + 2] : 0.0;
+      mxc[c] = in ? tM[ex + 2] : 0;
+    }
+#pragma unroll
+    for (int r = 0; r < RY + 1; ++r) {
+      const int ey = g.flo[1] + Y0 - 1 + RY * w + r;
+      const bool in = ey >= -2 && ey < g.n[1] + 2;
+      ayr[r] = (BF == 1 && in) ? tA[BW + ey + 2] : 0.0;
+      myr[r] = in ? tM[BW + ey + 2] : 0;
+    }
+#pragma unroll
+    for (int r = 0; r < RY + 1; ++r)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        pk |= ((mxc[c] & myr[r]) & 31) << (5 * (2 * r + c));
+        bt[r][c] = BF == 1 ? axc[c] * ayr[r] : 0.0;
+      }
+  }
 
   // one z step: node plane zl = z0-1+s arrives in wu; wd holds plane zl-1 (previous step)
   auto step = [&](int s, double (&wd)[RY + 2][3], double (&wu)[RY + 2][3]) {
@@ -210,11 +209,11 @@ __global__ void __launch_bounds__(NTH, ELEM_MINB)
     if (tid == 0 && s + NS - 1 < nsteps) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       const int t = s + NS - 1;
-      issue_elem_stage<MODE>(smem, full, (G + t) % NS, t, z0, X0, Y0, ey0, ez_base, tx_bytes, first, pH0, pH1, pE,
+      issue_elem_stage<MODE, SB, BF>(smem, full, (G + t) % NS, t, z0, X0, Y0, ey0, ez_base, tx_bytes, first, pH0, pH1, pE,
                              pI0, pI1);
     }
     mbar_wait(&full[st], (gs / NS) & 1u);
-    unsigned char* stage = smem + st * C::SBYTES;
+    unsigned char* stage = smem + st * SB;
     const double* H = reinterpret_cast<const double*>(stage);
     if (MODE == MODE_K1) {   // p = z + beta_cg p_old, formed per thread for its whole window
       const double* H1 = reinterpret_cast<const double*>(stage + HSTRIDE);
@@ -237,12 +236,27 @@ __global__ void __launch_bounds__(NTH, ELEM_MINB)
         for (int c = 0; c < 3; ++c) wu[r][c] = H[(RY * w + r) * HX + XO - 1 + lane + c];
     }
     if (s == 0) return;
-    const double* E = reinterpret_cast<const double*>(stage + C::OFF_E);
     double bl[RY + 1][2];
+    if (BF) {   // beta_combine on the layer's table entry (same function and inputs as the array, k_beta)
+      const int ez = g.flo[2] + g.zoff - 1 + zl;
+      const bool in = ez >= -2 && ez < g.n[2] + 2;
+      const double az = in ? tA[2 * BW + ez + 2] : 0.0;
+      const int mz = in ? tM[2 * BW + ez + 2] : 0;
 #pragma unroll
-    for (int r = 0; r < RY + 1; ++r)
+      for (int r = 0; r < RY + 1; ++r)
 #pragma unroll
-      for (int c = 0; c < 2; ++c) bl[r][c] = E[(RY * w + r) * EBX + eo + lane + c];
+        for (int c = 0; c < 2; ++c) {
+          const int m = (pk >> (5 * (2 * r + c))) & mz;
+          if (BF == 1) bl[r][c] = (m & 16) ? __fma_rn(bt[r][c], az, 1.0) : 0.0;
+          else bl[r][c] = beta_combine(es.bkind, 0.0, 0.0, az, m, 31, 31, boxb);
+        }
+    } else {
+      const double* E = reinterpret_cast<const double*>(stage + C::OFF_E);
+#pragma unroll
+      for (int r = 0; r < RY + 1; ++r)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) bl[r][c] = E[(RY * w + r) * EBX + eo + lane + c];
+    }
     const double* I0 = reinterpret_cast<const double*>(stage + C::OFF_I);
     const double* I1 = I0 + TX * TY;
     const int d = zl - 1;   // node plane completed in this step
@@ -368,9 +382,6 @@ __global__ void __launch_bounds__(NTH, ELEM_MINB)
     step(s, wB, wA);
     if (s + 1 < nsteps) step(s + 1, wA, wB);
   }
-  }
-  if ((MODE == MODE_K2 || MODE == MODE_INIT) && (a.peer_lo || a.peer_hi)) __threadfence_system();   // peer stores
-  if (MODE != MODE_APPLY) reduce_finalize(MODE, a, acc0, acc1, acc2);
 #undef k0
 #undef k1
 #undef k2
@@ -381,16 +392,179 @@ __global__ void __launch_bounds__(NTH, ELEM_MINB)
 #undef k7
 }
 
+template <int MODE, int NS, bool CUBE, int BF>
+__global__ void __launch_bounds__(NTH, ELEM_MINB)
+    k_jcg_elem_tma(const LevelGeom g, const ElemStencil es, const KArgs a, const __grid_constant__ CUtensorMap mH0,
+                   const __grid_constant__ CUtensorMap mH1, const __grid_constant__ CUtensorMap mE,
+                   const __grid_constant__ CUtensorMap mI0, const __grid_constant__ CUtensorMap mI1) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full[NS];
+  // (offset from smem_raw, not a uintptr_t round trip: the pointer must stay in the shared window so
+  // the reads compile to LDS, not generic LD)
+  unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  JcgScalars* sc = a.sc;
+  pdl_trigger();
+  pdl_wait();
+  if (MODE == MODE_K1 || MODE == MODE_K2) {
+    if (*(volatile int*)&sc->done) return;
+  }
+  const int tid = threadIdx.x + TX * threadIdx.y;
+  double bcg = 0.0, alpha = 0.0;
+  bool first = false;
+  if (MODE == MODE_K1) { bcg = sc->beta; first = (sc->iter == 0); }
+  if (MODE == MODE_K2) alpha = sc->alpha;
+  double* const u_out = (MODE == MODE_TRUE) ? sc->in.u_out : nullptr;
+  // iteration 0 of K1 (p = z): the p_old slot is filled from z and beta_cg = 0 (exact for finite z), so
+  // the window update is one FMA with no per-element select
+  const double bcg_eff = first ? 0.0 : bcg;
+  const CUtensorMap* pH1 = (MODE == MODE_K1 && first) ? &mH0 : &mH1;
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) mbar_init(&full[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // Work distribution: grid (x tiles, y tiles, z chunks of a.zc planes). All tiles of a z chunk march
+  // side by side, so the halo rows / columns that neighbouring CTAs both read (boxes are 1.2-1.27x the
+  // tile) are L2 hits. (Measured: giving each of 2 x 148 persistent CTAs an equal contiguous range of
+  // the tile-major (tile, plane) space removes the partial last wave but de-phases neighbouring
+  // tiles, and costs 40 % at 256^3: 0.444 vs 0.315 ms per iteration.)
+  const int X0 = blockIdx.x * TX, Y0 = blockIdx.y * TY;
+  const int z0 = g.zbeg + blockIdx.z * a.zc;
+  const int z1 = min(z0 + a.zc, g.zend);
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+  elem_pass<MODE, NS, CUBE, ElemCfg<MODE>::SBYTES, BF>(g, es, a, X0, Y0, z0, z1, bcg_eff, first, alpha, u_out, &mH0, pH1, &mE, &mI0, &mI1, smem, full,
+                            0u, acc0, acc1, acc2);
+  if ((MODE == MODE_K2 || MODE == MODE_INIT) && (a.peer_lo || a.peer_hi)) __threadfence_system();   // peer stores
+  if (MODE != MODE_APPLY) reduce_finalize(MODE, a, acc0, acc1, acc2);
+}
+
+// ---- the whole JCG solve of a level in ONE cooperative launch (element path), as k_jcg_const_pers in
+// kernels_jcg_tma.cu: each CTA owns a fixed list of (tile, z chunk) items and runs init -> { K1 pass,
+// grid sum, K2 pass, grid sum } -> true residual with deterministic grid sums (every CTA reduces all
+// partials in CTA order and holds the same CG scalars).
+constexpr int EP_NS = 5;
+constexpr int EP_SB = ElemCfg<MODE_K2>::SBYTES > ElemCfg<MODE_K1>::SBYTES ? ElemCfg<MODE_K2>::SBYTES : ElemCfg<MODE_K1>::SBYTES;
+constexpr int EP_SMEM = EP_SB * EP_NS + 128;
+
+struct ElemPersMaps { CUtensorMap xh, zh, ph0, ph1, be, xi, ri, bi; };
+
+__device__ __forceinline__ void elem_grid_sum3(double v[3], double* partials, int& buf, double* red,
+                                               cooperative_groups::grid_group& grid) {
+  block_sum3(v[0], v[1], v[2], red);   // thread 0 holds the CTA sums
+  const int tid = threadIdx.x + TX * threadIdx.y;
+  double* pb = partials + (size_t)buf * gridDim.x * 3;
+  if (tid == 0)
+    for (int k = 0; k < 3; ++k) pb[3 * blockIdx.x + k] = v[k];
+  grid.sync();
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  for (unsigned c = tid; c < gridDim.x; c += NTH) {
+    s0 += __ldcg(pb + 3 * c);
+    s1 += __ldcg(pb + 3 * c + 1);
+    s2 += __ldcg(pb + 3 * c + 2);
+  }
+  block_sum3(s0, s1, s2, red);
+  __shared__ double bc[3];
+  if (tid == 0) { bc[0] = s0; bc[1] = s1; bc[2] = s2; }
+  __syncthreads();
+  v[0] = bc[0]; v[1] = bc[1]; v[2] = bc[2];
+  __syncthreads();
+  buf ^= 1;
+}
+
+template <bool CUBE, int BF>
+__global__ void __launch_bounds__(NTH, ELEM_MINB)
+    k_jcg_elem_pers(const LevelGeom g, const ElemStencil es, double* x, double* r, double* z, double* p0, double* p1,
+                    double* partials, JcgScalars* sc, int zc, int ntx, int nty, int items,
+                    const __grid_constant__ ElemPersMaps M) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full[EP_NS];
+  __shared__ double red[3 * (NTH / 32)];
+  unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  const int tid = threadIdx.x + TX * threadIdx.y;
+  if (tid == 0) {
+    for (int i = 0; i < EP_NS; ++i) mbar_init(&full[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const double eps = sc->in.eps;
+  const int max_iter = sc->in.max_iter;
+  double* const u_out = sc->in.u_out;
+  uint32_t gstep = 0;
+  int buf = 0;
+  KArgs a{};
+  auto pass = [&](auto mode_tag, const CUtensorMap* h0, const CUtensorMap* h1, const CUtensorMap* i0, const CUtensorMap* i1,
+                  double bcg, bool first, double alpha, double v[3]) {
+    constexpr int MODE = decltype(mode_tag)::value;
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+    for (int it = blockIdx.x; it < items; it += gridDim.x) {
+      const int X0 = (it % ntx) * TX, Y0 = ((it / ntx) % nty) * TY;
+      const int z0 = (it / (ntx * nty)) * zc, z1 = min(z0 + zc, g.zend);
+      elem_pass<MODE, EP_NS, CUBE, EP_SB, BF>(g, es, a, X0, Y0, z0, z1, bcg, first, alpha, u_out, h0, h1, &M.be, i0, i1, smem,
+                                          full, gstep, acc0, acc1, acc2);
+      gstep += (uint32_t)(z1 - z0 + 2);
+      __syncthreads();   // every stage consumed before the next pass's prefill
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");   // stores read by other CTAs' TMA next pass
+    v[0] = acc0; v[1] = acc1; v[2] = acc2;
+    elem_grid_sum3(v, partials, buf, red, grid);
+    if (tid == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
+  };
+  double v[3];
+  a.o0 = r; a.o1 = z;   // init: r = b - A x, z = D^-1 r, rho = r.z, rr, ||b||^2
+  pass(std::integral_constant<int, MODE_INIT>{}, &M.xh, &M.xh, &M.bi, &M.bi, 0.0, false, 0.0, v);
+  double rho = v[0], rr = v[1];
+  const double bb = v[2];
+  const double nb = sqrt(bb), nbe = nb > 0.0 ? nb : 1.0;
+  const double thresh = eps > 0.0 ? eps * nbe : -1.0;
+  int status = ST_OK, iter = 0;
+  double beta = 0.0;
+  bool done = (max_iter <= 0) || (thresh > 0.0 && !(sqrt(rr) > thresh));
+  if (!isfinite(rr)) { status = ST_EBREAKDOWN; done = true; }
+  int cur = 0;   // p_cur holds p_old
+  while (!done) {
+    a.o0 = cur ? p0 : p1;
+    // iteration 0: p = z (the p_old slot is filled from z and beta_cg = 0, as in k_jcg_elem_tma)
+    pass(std::integral_constant<int, MODE_K1>{}, &M.zh, iter == 0 ? &M.zh : (cur ? &M.ph1 : &M.ph0), &M.zh, &M.zh,
+         iter == 0 ? 0.0 : beta, iter == 0, 0.0, v);
+    const double sigma = v[0];
+    if (!(sigma > 0.0)) { status = ST_EBREAKDOWN; break; }
+    const double alpha = rho / sigma;
+    a.o0 = x; a.o1 = r; a.o2 = z;
+    pass(std::integral_constant<int, MODE_K2>{}, cur ? &M.ph0 : &M.ph1, &M.zh, &M.xi, &M.ri, 0.0, false, alpha, v);
+    beta = v[0] / rho;
+    rho = v[0];
+    rr = v[1];
+    cur ^= 1;
+    ++iter;
+    done = (iter >= max_iter) || (thresh > 0.0 && !(sqrt(rr) > thresh));
+    if (!isfinite(rr)) { status = ST_EBREAKDOWN; done = true; }
+  }
+  pass(std::integral_constant<int, MODE_TRUE>{}, &M.xh, &M.xh, &M.bi, &M.bi, 0.0, false, 0.0, v);
+  if (blockIdx.x == 0 && tid == 0) {
+    sc->rho = rho; sc->rr = rr; sc->bb = bb; sc->rr_true = v[1]; sc->beta = beta;
+    sc->iter = iter; sc->max_iter = max_iter; sc->thresh = thresh; sc->status = status; sc->done = 1;
+    sc->counter = 0;
+  }
+}
+
 template <int MODE, int NS>
 constexpr int elem_smem() { return ElemCfg<MODE>::SBYTES * NS + 128; }
 
 template <int MODE, int NS>
 cudaError_t set_elem_tma_attr() {
-  cudaError_t e = cudaFuncSetAttribute(k_jcg_elem_tma<MODE, NS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       elem_smem<MODE, NS>());
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_jcg_elem_tma<MODE, NS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              elem_smem<MODE, NS>());
+  const int sm = elem_smem<MODE, NS>();
+  cudaError_t e = cudaFuncSetAttribute(k_jcg_elem_tma<MODE, NS, false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_jcg_elem_tma<MODE, NS, true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_jcg_elem_tma<MODE, NS, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_jcg_elem_tma<MODE, NS, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  return e;
+}
+
+// beta on the fly for cubic cells with the level's tables (ElemStencil::bkind >= 0): 1 = product kind
+inline int beta_fly_variant(const ElemStencil& es) {
+  if (!es.cube || es.bkind < 0 || !es.baxes) return 0;
+  return es.bkind == BETA_KIND_C3 ? 1 : 2;
 }
 
 template <int MODE, int NS>
@@ -398,11 +572,14 @@ cudaError_t launch_elem_tma_mode(const LevelGeom& g, const ElemStencil& es, cons
                                  cudaStream_t st) {
   dim3 grid((g.nf[0] + TX - 1) / TX, (g.nf[1] + TY - 1) / TY, (g.zend - g.zbeg + a.zc - 1) / a.zc);
   count_launch();
-  if (es.cube)
-    return launch_maybe_pdl(k_jcg_elem_tma<MODE, NS, true>, grid, dim3(TX, WARPS), elem_smem<MODE, NS>(), st, a.pdl, g, es,
-                            a, m[0], m[1], m[2], m[3], m[4]);
-  return launch_maybe_pdl(k_jcg_elem_tma<MODE, NS, false>, grid, dim3(TX, WARPS), elem_smem<MODE, NS>(), st, a.pdl, g, es,
-                          a, m[0], m[1], m[2], m[3], m[4]);
+  const int sm = elem_smem<MODE, NS>();
+  const dim3 blk(TX, WARPS);
+  switch (es.cube ? 1 + beta_fly_variant(es) : 0) {
+    case 1: return launch_maybe_pdl(k_jcg_elem_tma<MODE, NS, true, 0>, grid, blk, sm, st, a.pdl, g, es, a, m[0], m[1], m[2], m[3], m[4]);
+    case 2: return launch_maybe_pdl(k_jcg_elem_tma<MODE, NS, true, 1>, grid, blk, sm, st, a.pdl, g, es, a, m[0], m[1], m[2], m[3], m[4]);
+    case 3: return launch_maybe_pdl(k_jcg_elem_tma<MODE, NS, true, 2>, grid, blk, sm, st, a.pdl, g, es, a, m[0], m[1], m[2], m[3], m[4]);
+    default: return launch_maybe_pdl(k_jcg_elem_tma<MODE, NS, false, 0>, grid, blk, sm, st, a.pdl, g, es, a, m[0], m[1], m[2], m[3], m[4]);
+  }
 }
 
 // ---- tensor-map cache: (base, geometry, box) -> CUtensorMap; an entry is a pure function of its key
@@ -482,6 +659,58 @@ cudaError_t init_elem_kernel_attributes() {
 }
 
 int elem_tile_rows() { return TY; }
+
+static int elem_pers_slots() {
+  static int slots = 0;
+  if (!slots) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jcg_elem_pers<true, 0>, NTH, EP_SMEM);
+    slots = sms * std::max(1, per_sm);
+  }
+  return slots;
+}
+
+cudaError_t init_elem_pers_attributes() {
+  cudaError_t e = cudaFuncSetAttribute(k_jcg_elem_pers<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, EP_SMEM);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_jcg_elem_pers<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, EP_SMEM);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_jcg_elem_pers<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, EP_SMEM);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_jcg_elem_pers<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, EP_SMEM);
+  return e;
+}
+
+// the whole tolerance-stopped solve of an element-path level in one cooperative launch (single GPU)
+cudaError_t launch_jcg_elem_pers(const LevelGeom& g, const ElemStencil& es, double* x, double* r, double* z, double* p0,
+                                 double* p1, const double* b, const double* beta, double* partials, JcgScalars* sc,
+                                 cudaStream_t st) {
+  if (g.BP % 2 != 0 || g.zbeg != 0) return cudaErrorInvalidValue;
+  const int ntx = (g.nf[0] + TX - 1) / TX, nty = (g.nf[1] + TY - 1) / TY;
+  const int nz = g.zend - g.zbeg;
+  const int slots = elem_pers_slots();
+  const long long tiles = (long long)ntx * nty;
+  if (tiles > slots) return cudaErrorInvalidValue;
+  const int nch = (int)std::max(1LL, slots / tiles);
+  const int zc = (nz + nch - 1) / nch;
+  const int items = (int)(tiles * ((nz + zc - 1) / zc));
+  ElemPersMaps M;
+  const bool ok = vec_map(&M.xh, x, g, HX, HY) && vec_map(&M.zh, z, g, HX, HY) && vec_map(&M.ph0, p0, g, HX, HY) &&
+                  vec_map(&M.ph1, p1, g, HX, HY) && beta_map(&M.be, beta, g) && vec_map(&M.xi, x, g, TX, TY) &&
+                  vec_map(&M.ri, r, g, TX, TY) && vec_map(&M.bi, b, g, TX, TY);
+  if (!ok) return cudaErrorInvalidValue;
+  const int grid = std::min(items, slots);
+  void* args[] = {(void*)&g, (void*)&es, (void*)&x, (void*)&r, (void*)&z, (void*)&p0, (void*)&p1, (void*)&partials,
+                  (void*)&sc, (void*)&zc, (void*)&ntx, (void*)&nty, (void*)&items, (void*)&M};
+  count_launch();
+  const void* fn = (const void*)k_jcg_elem_pers<false, 0>;
+  switch (es.cube ? 1 + beta_fly_variant(es) : 0) {
+    case 1: fn = (const void*)k_jcg_elem_pers<true, 0>; break;
+    case 2: fn = (const void*)k_jcg_elem_pers<true, 1>; break;
+    case 3: fn = (const void*)k_jcg_elem_pers<true, 2>; break;
+    default: break;
+  }
+  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(TX, WARPS), args, EP_SMEM, st);
+}
 
 // K1: h0 = z, h1 = p_old, o0 = p. K2: h0 = p, i0 = x, i1 = r, o0 = x, o1 = r, o2 = z.
 // INIT: h0 = x, i0 = b, o0 = r, o1 = z. TRUE: h0 = x, i0 = b. APPLY: h0 = p, o0 = A p.

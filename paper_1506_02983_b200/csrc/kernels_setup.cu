@@ -4,6 +4,7 @@
 // caller-visible nodal vectors and the free-box work vectors.
 #include <algorithm>
 #include "ecmg_internal.cuh"
+#include "host_common.h"
 #include "problems.cuh"
 
 namespace ecmg {
@@ -12,17 +13,46 @@ namespace {
 constexpr double kGauss = 0.57735026918962576451;  // 1/sqrt(3)
 
 // ---- element coefficients beta_e = beta(centroid) (§8c A3), zero outside the domain ----------
-__global__ void k_beta(const LevelGeom g, const Problem pb, double* __restrict__ beta) {
+// Per-axis tables of beta_combine (ecmg_internal.cuh) at the element centroids lo + (e + 1/2) h, e in
+// [-2, n_d + 1]: the factor / layer value A and the bits M (element exists; inside box k along the axis).
+__global__ void k_beta_axes(const LevelGeom g, const Problem pb, double* __restrict__ tab, int W, int kind) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  double* A = tab;
+  int* M = reinterpret_cast<int*>(tab + 3LL * W);
+  double* boxb = tab + 3LL * W + (3LL * W + 1) / 2;
+  if (t < 4) boxb[t] = (kind == BETA_KIND_C5) ? pb.params[15 + 7 * t + 6] : 0.0;
+  if (t >= 3 * W) return;
+  const int d = t / W, e = t % W - 2;
+  double a = 0.0;
+  int m = 0;
+  if (e >= -2 && e < g.n[d] + 2) {
+    const double c = g.lo[d] + (e + 0.5) * g.h[d];
+    if (e >= 0 && e < g.n[d]) m |= 16;
+    const double tp = 2.0 * kPi() * c;
+    if (kind == BETA_KIND_C3) a = d == 0 ? 0.5 * sin(tp) : (d == 1 ? cos(tp) : sin(tp));
+    if ((kind == BETA_KIND_LAYERS || kind == BETA_KIND_C5) && d == 2) a = layer_beta(pb, c);
+    if (kind == BETA_KIND_C5)
+      for (int k = 0; k < 4; ++k) {
+        const double* q = &pb.params[15 + 7 * k];
+        if (fabs(c - q[d]) < q[3 + d]) m |= 1 << k;
+      }
+  }
+  A[t] = a;
+  M[t] = m;
+}
+
+__global__ void k_beta(const LevelGeom g, double* __restrict__ beta, const double* __restrict__ tab, int W, int kind) {
   // element planes this rank's work vectors touch: [flo+zoff-2, flo+zoff+nza] (all planes on one GPU)
   const int e0 = max(-2, g.flo[2] + g.zoff - 2), e1 = min(g.n[2] + 1, g.flo[2] + g.zoff + g.nza);
   const long long ne0 = g.n[0] + 4, ne1 = g.n[1] + 4, ne2 = e1 - e0 + 1;
   const long long total = ne0 * ne1 * ne2;
+  const double* A = tab;
+  const int* M = reinterpret_cast<const int*>(tab + 3LL * W);
+  const double* boxb = tab + 3LL * W + (3LL * W + 1) / 2;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
     const int ex = (int)(t % ne0) - 2, ey = (int)((t / ne0) % ne1) - 2, ez = (int)(t / (ne0 * ne1)) + e0;
-    double v = 0.0;
-    if (ex >= 0 && ex < g.n[0] && ey >= 0 && ey < g.n[1] && ez >= 0 && ez < g.n[2]) {
-      v = prob_beta(pb, g.lo[0] + (ex + 0.5) * g.h[0], g.lo[1] + (ey + 0.5) * g.h[1], g.lo[2] + (ez + 0.5) * g.h[2]);
-    }
+    const double v = beta_combine(kind, A[ex + 2], A[W + ey + 2], A[2 * W + ez + 2], M[ex + 2], M[W + ey + 2],
+                                  M[2 * W + ez + 2], boxb);
     beta[(long long)(ez + 2) * g.BS + (long long)(ey + 2) * g.BP + (ex + 2)] = v;
   }
 }
@@ -424,11 +454,16 @@ __global__ void k_zero_free(const LevelGeom g, double* __restrict__ v) {
 
 }  // namespace
 
+// beta array of the level and, behind it, the per-axis tables it is formed from (beta_combine)
 cudaError_t launch_beta(const LevelGeom& g, const Problem& pb, double* beta, cudaStream_t st) {
+  const int W = beta_axes_w(g), kind = beta_kind(pb.id);
+  double* tab = beta + g.BS * (g.n[2] + 4);
+  count_launch();
+  k_beta_axes<<<(3 * W + 127) / 128, 128, 0, st>>>(g, pb, tab, W, kind);
   const long long total = (long long)(g.n[0] + 4) * (g.n[1] + 4) * (g.n[2] + 4);
   const int nb = (int)std::min<long long>((total + 255) / 256, 148LL * 32);
   count_launch();
-  k_beta<<<nb, 256, 0, st>>>(g, pb, beta);
+  k_beta<<<nb, 256, 0, st>>>(g, beta, tab, W, kind);
   return cudaGetLastError();
 }
 

@@ -12,6 +12,7 @@ struct SlabCfg {
   Problem prob;
   int elem_path, exp_variant, precond, kernel_variant, zchunk;
   int fused_halo;   // 1: K2 / init store their boundary planes into the neighbours' halo planes
+  int beta_fly;     // 1: element kernels form analytic beta from the level's axis tables
 };
 
 struct SlabDriver;

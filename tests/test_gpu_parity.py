@@ -160,7 +160,7 @@ def test_tolerance_stopped_solve(pid, eps):
 
 @pytest.mark.parametrize("pid,levels,eps,variant", [
     (o.C1, 4, 1e-8, 0), (o.C2, 5, 1e-10, 0), (o.C3, 5, 1e-10, 0), (o.C4, 5, 1e-9, 0), (o.C5, 5, 1e-8, 0),
-    (o.C2, 6, 1e-10, 0), (o.C4, 6, 1e-9, 0),
+    (o.C2, 6, 1e-10, 0), (o.C4, 6, 1e-9, 0), (o.C3, 6, 1e-10, 0),
     (o.P1, 4, 1e-9, 1), (o.P1, 4, 1e-9, 0), (o.P2, 4, 1e-12, 1), (o.P3, 4, 1e-11, 0)])
 def test_ecmg_run(pid, levels, eps, variant):
     n0 = (10, 4, 5) if pid == o.P2 else ((8,) * 3 if pid in (o.P1, o.P3) else (4,) * 3)
@@ -395,7 +395,8 @@ def test_cta_solve_vs_persistent(pid, eps):
     assert np.max(np.abs(res[0][1] - ou)) <= 1e-9 * np.max(np.abs(ou))
 
 
-@pytest.mark.parametrize("pid,eps", [(o.C2, 1e-10), (o.C4, 1e-9), (o.C1, 1e-8)])
+@pytest.mark.parametrize("pid,eps", [(o.C2, 1e-10), (o.C4, 1e-9), (o.C1, 1e-8), (o.C3, 1e-10), (o.C5, 1e-8),
+                                     (o.PATCH_ROBIN_XY, 1e-10)])
 def test_persistent_tma_vs_graph(pid, eps):
     # constant-stencil levels between ECMG_OPT_PERSISTENT and ECMG_OPT_PERS_TMA (here 128^3) run the
     # whole solve as one cooperative launch of the TMA z-marching passes; the CUDA-graph K1/K2 loop is
@@ -415,3 +416,25 @@ def test_persistent_tma_vs_graph(pid, eps):
     for k in (1, 2, 4):
         assert np.max(np.abs(res[0][k] - res[1][k])) <= 1e-9 * np.max(np.abs(res[1][k]))
     assert abs(res[0][3][1]["iterations"] - res[1][3][1]["iterations"]) <= 1
+
+
+@pytest.mark.parametrize("pid,eps", [(o.C3, 1e-10), (o.C5, 1e-8), (o.P1, 1e-9), (o.PATCH_LAYERED, 1e-12),
+                                     (o.PATCH_ROBIN_XY, 1e-10)])
+def test_beta_on_the_fly_bitwise(pid, eps):
+    # ECMG_OPT_BETA_FLY: the element kernels form beta_e from the per-axis tables with the same function the
+    # beta array is filled with, so every iterate is bitwise that of the array-reading kernels (graph loop,
+    # persistent TMA solve and the init / true-residual passes, up to 128^3)
+    res = []
+    for fly in (0, 1):
+        g = Grid(4, 6, pid, params_for(pid))
+        g.set_option(ecmg.OPT_BETA_FLY, fly)
+        u, ut = g.new_vec(5), g.new_vec(5)
+        st, stats = g.run(eps, u, ut)
+        assert st == 0
+        p = dev(synth.random_nodal(11, (128,) * 3))
+        q = g.new_vec(5)
+        g.apply_operator(5, p, q)
+        res.append(([s["iterations"] for s in stats], host(u), host(ut), host(q)))
+    assert res[0][0] == res[1][0]
+    for k in (1, 2, 3):
+        assert np.array_equal(res[0][k], res[1][k])
