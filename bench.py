@@ -38,18 +38,17 @@ UNIT = "unknown-iters/s"
 BYTES_PER_UNKNOWN_ITER = 64   # x 1R+1W, r 2R+1W, p 2R+1W (constant-beta path)
 
 CONFIGS = {
-    # name: (problem id, coarsest, levels, eps, description); C3 / C5 run the element-beta path (72 B/unknown)
+    # name: (problem id, coarsest, levels, eps, description); C3 / C5 run the element-beta path (88 B/unknown)
     "c4": (4, 4, 8, 1e-9, "C4 (BASELINE configs[3]): u=r^{3/2}, beta=1, Dirichlet, Q1, 4^3->512^3, eps=1e-9"),
     "c2": (2, 4, 6, 1e-10, "C2 (BASELINE configs[1]): u=exp(x+y+z), beta=1, Dirichlet, Q1, 4^3->128^3, eps=1e-10"),
     "c1": (1, 4, 4, 1e-8, "C1 (BASELINE configs[0]): u=sin sin sin, beta=1, Dirichlet, Q1, 4^3->32^3, eps=1e-8"),
     "c3": (3, 4, 7, 1e-10, "C3 (BASELINE configs[2]): variable beta, Robin z=1, Q1, 4^3->256^3, eps=1e-10"),
     "c5": (5, 4, 9, 1e-8, "C5 (BASELINE configs[4]): layered geology (seed 0), Dirichlet, Q1, 4^3->1024^3, eps=1e-8"),
 }
-# element-beta path (kernels_jcg_elem.cu): K1 reads z, p_old and writes p; K2 reads p, x, r and writes
-# x, r, z = D^-1 r (z replaces the halo diagonal): 9 x 8 B. beta_e of the analytic problems (C3, C5) is
-# formed in registers from per-axis tables (ECMG_OPT_BETA_FLY); reading the beta array instead adds
-# 8 B in each of K1 and K2 (88 B, the ablation)
-BYTES_PER_UNKNOWN_ITER_ELEM = 72
+# element-beta path (kernels_jcg_elem.cu): K1 reads z, p_old, beta_e and writes p; K2 reads p, beta_e,
+# x, r and writes x, r, z = D^-1 r (z replaces the halo diagonal): 11 x 8 B. With ECMG_OPT_BETA_FLY = 1
+# (ablation) beta_e is formed in registers from per-axis tables: 9 x 8 B
+BYTES_PER_UNKNOWN_ITER_ELEM = 88
 
 
 def load_peaks():
@@ -259,15 +258,15 @@ def main():
     ms_p = max_over_ranks(ms_p)
     grid.set_option(ecmg.OPT_KERNEL, 1)
     ablation_beta = None
-    if pid in (3, 5):   # ablation: the element kernels read the beta array instead of forming beta on the fly
-        grid.set_option(ecmg.OPT_BETA_FLY, 0)
+    if pid in (3, 5):   # ablation: the element kernels form beta on the fly instead of reading the array
+        grid.set_option(ecmg.OPT_BETA_FLY, 1)
         xb.copy_(x0)
         grid.solve_level(fine, 0.0, args.fixed_iters, xb)
         ms_b, it_b, _ = grid.last_jcg_timing()
         ms_b = max_over_ranks(ms_b)
-        grid.set_option(ecmg.OPT_BETA_FLY, 1)
+        grid.set_option(ecmg.OPT_BETA_FLY, 0)
         ablation_beta = {"value": nf_j * it_b / (ms_b / 1e3), "unit": UNIT, "ms_per_iteration": ms_b / max(1, it_b),
-                         "kernel": "element kernels reading the beta array (ECMG_OPT_BETA_FLY=0), 88 B/unknown"}
+                         "kernel": "element kernels forming beta_e from per-axis tables (ECMG_OPT_BETA_FLY=1), 72 B/unknown"}
     # ablation: host-driven JCG loop (batched readbacks) instead of the CUDA-graph WHILE loop
     grid.set_option(ecmg.OPT_GRAPH, 0)
     grid.run(eps, u, ut)
@@ -347,7 +346,7 @@ def main():
             "jcg_fixed_ablation_prefetch": {"value": nf_j * it_p / (ms_p / 1e3), "unit": UNIT,
                                             "ms_per_iteration": ms_p / max(1, it_p),
                                             "kernel": "register-prefetch loads (ECMG_OPT_KERNEL=0)"},
-            "jcg_fixed_ablation_beta_array": ablation_beta,
+            "jcg_fixed_ablation_beta_fly": ablation_beta,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "kernel": "jcg K1+K2 (one CG iteration)",
                          "bytes_per_unit": bpu, "peak_source": peak_src,

@@ -133,10 +133,11 @@ typedef enum {
                                 tolerance-stopped solve as ONE cooperative launch of TMA z-marching passes
                                 (no per-iteration kernel launches); 0: the CUDA-graph loop of K1 / K2 */
   ECMG_OPT_BETA_FLY = 15,    /* element-beta path, cubic cells, analytic beta (C3, C5, layers, beta = 1 with
-                                Robin / Neumann faces): 1 (default) the TMA element kernels form beta_e in
-                                registers from per-axis tables (the same function the beta array is
-                                filled with, bitwise) instead of reading the array: 16 B less HBM traffic
-                                per unknown and iteration; 0: read the array (ablation) */
+                                Robin / Neumann faces): 1: the TMA element kernels form beta_e in registers
+                                from per-axis tables (the same function the beta array is filled with,
+                                bitwise) instead of reading the array, 16 B less HBM traffic per unknown and
+                                iteration; 0 (default): read the array (measured as fast: the element
+                                kernels are latency bound at 2 CTAs per SM, not HBM bound) */
   ECMG_OPT_SETUP_CTAS = 11,  /* tuning: CTAs per SM of the fp64-ALU-bound volume-load kernel when it runs
                                 ahead (0 = one CTA per work item, the full grid) */
   ECMG_OPT_VIRTUAL_SLABS = 6 /* P in 2..16: run the z-slab decomposition with P slabs on this one GPU

@@ -48,7 +48,8 @@ struct ecmg_grid {
   std::vector<double*> s1d;        // per-level 1D Gauss load tables (separable right-hand sides)
   std::vector<char> setup_ok;      // level k's b / beta hold the current problem's data
   int setup_ahead = 1;             // ECMG_OPT_SETUP_AHEAD
-  int beta_fly = 1;                // ECMG_OPT_BETA_FLY: element kernels form analytic beta from axis tables
+  int beta_fly = 0;                // ECMG_OPT_BETA_FLY: element kernels form analytic beta from axis tables (measured:
+                                   // 16 B/unknown less traffic but no faster -- the element kernels are latency bound)
   int exp_fused = 1;               // ECMG_OPT_EXP_KERNEL: 1 fused one-pass EXP_finite, 0 seeds + interpolation passes
   int setup_ctas = 0;              // ECMG_OPT_SETUP_CTAS: CTAs per SM of the ALU-bound RHS kernel when run ahead
   cudaStream_t hi_stream = nullptr, lo_stream = nullptr;   // ecmg_run: solves (high) / level setup (low priority)

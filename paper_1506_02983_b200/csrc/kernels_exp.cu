@@ -383,17 +383,20 @@ __global__ void __launch_bounds__(FNTH, 3) k_exp_fused(const LevelGeom gf, const
 
 // EXP_true as a z-march over a 64 x 8 fine tile (threads 32 x 8; thread (lane, w) owns the nodes
 // X0 + lane and X0 + 32 + lane of fine row Y0 + w, so every load / store instruction of a warp covers
-// 256 contiguous bytes). Per 2h plane K: (a) the tile's 33 x 5 corner differences
-// d = u_h|_2h - u_2h of plane K go to a two-plane shared ring; (b) fine plane 2K-1 is written from
-// d planes K-1, K and (c) fine plane 2K from d plane K: u~ = u_h + (1/3) I_trilinear(d), where the
-// trilinear interpolant at a fine node is d at the 2h node it sits on, or the mean of the two / four /
-// eight 2h nodes around it (reading A13). Dirichlet nodes take g_D (A15).
+// 256 contiguous bytes). u~ = u_h + (1/3) I_trilinear(d), d = u_h|_2h - u_2h (reading A13), with the
+// trilinear interpolant applied axis by axis: per 2h plane K the tile's 33 x 5 corner differences are
+// interpolated along x into a 64 x 5 shared array (one pass for the whole CTA), then each thread
+// interpolates its two nodes along y in registers; fine plane 2K takes plane K's values, the odd plane
+// 2K-1 the mean of planes K-1 and K (registers carried from the previous step). The weights are (1, 0)
+// on a 2h node and (1/2, 1/2) between two, so every stage equals the mean of its two inputs bit for bit.
+// Dirichlet nodes take g_D (A15).
 constexpr int ETX = 64, ETY = 8, EDX = ETX / 2 + 1, EDY = ETY / 2 + 1;   // 33 x 5 corner values per plane
 
 __global__ void __launch_bounds__(256) k_exp_true(const LevelGeom gf, const Problem pb, const double* __restrict__ uh,
                                                   const double* __restrict__ u2h, double* __restrict__ ut, int c0,
                                                   int cchunk, double third) {
-  __shared__ double D[2][EDY][EDX];
+  __shared__ double D[EDY][EDX];     // corner differences of the current 2h plane
+  __shared__ double XI[EDY][ETX];    // ... interpolated along x to the tile's 64 fine columns
   const int lane = threadIdx.x, w = threadIdx.y, tid = lane + 32 * w;
   const int n2x = gf.n[0] / 2, n2y = gf.n[1] / 2, n2z = gf.n[2] / 2;
   const int X0 = blockIdx.x * ETX, Y0 = blockIdx.y * ETY;
@@ -405,22 +408,7 @@ __global__ void __launch_bounds__(256) k_exp_true(const LevelGeom gf, const Prob
   const int fy = Y0 + w;
   const bool row_ok = fy <= gf.n[1];
   const int fxa = X0 + lane, fxb = X0 + 32 + lane;
-  // interpolation stencil of the thread's nodes: 2h column(s) and row(s) below / above, as weights
-  // (1, 0) on a 2h node or (1/2, 1/2) between two: the products are exact, so w0 d0 + w1 d1 equals the
-  // mean (d0 + d1) / 2 bit for bit and the interpolation needs no branches
-  const int ia = lane >> 1, ib = 16 + (lane >> 1), jr = w >> 1;
-  const double wx1 = (lane & 1) ? 0.5 : 0.0, wx0 = 1.0 - wx1;
-  const double wy1 = (w & 1) ? 0.5 : 0.0, wy0 = 1.0 - wy1;
-  auto dxy = [&](int s, double& va, double& vb) {   // (y, x)-interpolated d of plane slot s
-    const double a0 = wx0 * D[s][jr][ia] + wx1 * D[s][jr][ia + 1];
-    const double b0 = wx0 * D[s][jr][ib] + wx1 * D[s][jr][ib + 1];
-    const double a1 = wx0 * D[s][jr + 1][ia] + wx1 * D[s][jr + 1][ia + 1];
-    const double b1 = wx0 * D[s][jr + 1][ib] + wx1 * D[s][jr + 1][ib + 1];
-    va = wy0 * a0 + wy1 * a1;
-    vb = wy0 * b0 + wy1 * b1;
-  };
-  // loads are issued one step ahead (registers), so the global latency overlaps the barrier and the
-  // shared-memory interpolation of the current step
+  // corner differences: thread tid < 165 loads 2h node (di, dj) of each plane, one step ahead
   const bool dthr = tid < EDX * EDY;
   const int di = tid % EDX, dj = tid / EDX;
   const bool d_ok = dthr && I0 + di <= n2x && J0 + dj <= n2y;
@@ -431,6 +419,21 @@ __global__ void __launch_bounds__(256) k_exp_true(const LevelGeom gf, const Prob
       a = __ldg(uh + (long long)(2 * K) * pl + doff_h);
       b = __ldg(u2h + (long long)K * pl2 + doff_2);
     }
+  };
+  // x pass: thread t < 320 (and t + 256 < 320) produces XI[r][c] = w0 D[r][c/2] + w1 D[r][c/2 + 1]
+  auto xpass = [&]() {
+    for (int t = tid; t < EDY * ETX; t += 256) {
+      const int r = t / ETX, c = t % ETX, i = c >> 1;
+      const double w1 = (c & 1) ? 0.5 : 0.0, w0 = 1.0 - w1;
+      XI[r][c] = w0 * D[r][i] + w1 * D[r][i + 1];
+    }
+  };
+  // y pass of this thread's two nodes (row w between 2h rows w/2 and w/2 + 1)
+  const int jr = w >> 1;
+  const double wy1 = (w & 1) ? 0.5 : 0.0, wy0 = 1.0 - wy1;
+  auto ypass = [&](double& va, double& vb) {
+    va = wy0 * XI[jr][lane] + wy1 * XI[jr + 1][lane];
+    vb = wy0 * XI[jr][lane + 32] + wy1 * XI[jr + 1][lane + 32];
   };
   const bool okA = row_ok && fxa <= gf.n[0], okB = row_ok && fxb <= gf.n[0];
   const long long rowoff = (long long)fy * nx;
@@ -449,28 +452,25 @@ __global__ void __launch_bounds__(256) k_exp_true(const LevelGeom gf, const Prob
     if (okA) ut[row + fxa] = (zf && xyfA) ? __fma_rn(ia_, third, ua) : gD_at(gf, pb, fxa, fy, fz);
     if (okB) ut[row + fxb] = (zf && xyfB) ? __fma_rn(ib_, third, ub) : gD_at(gf, pb, fxb, fy, fz);
   };
-  double dh, d2;
+  double dh, d2, pa = 0.0, pb_ = 0.0;   // pa, pb_: plane K-1's interpolated d at the thread's nodes
   load_d(Ca, dh, d2);
   for (int K = Ca; K <= Cb; ++K) {
-    __syncthreads();   // the slot of plane K (plane K-2's) is free
-    if (dthr) D[K & 1][dj][di] = dh - d2;   // (a) corner differences of 2h plane K
+    __syncthreads();   // D / XI of plane K-1 consumed
+    if (dthr) D[dj][di] = dh - d2;   // corner differences of 2h plane K
     if (K < Cb) load_d(K + 1, dh, d2);
     double uoa = 0.0, uob = 0.0, uea = 0.0, ueb = 0.0;
     const bool odd = K > Ca, even = K < Cb || K == n2z;
     if (odd) load_u(2 * K - 1, uoa, uob);
     if (even) load_u(2 * K, uea, ueb);
     __syncthreads();
-    if (odd) {   // (b) odd fine plane 2K-1 between d planes K-1 and K
-      double a0, b0, a1, b1;
-      dxy((K - 1) & 1, a0, b0);
-      dxy(K & 1, a1, b1);
-      put(2 * K - 1, uoa, uob, 0.5 * (a0 + a1), 0.5 * (b0 + b1));
-    }
-    if (even) {   // (c) even fine plane 2K (the last 2h plane also ends the level)
-      double a0, b0;
-      dxy(K & 1, a0, b0);
-      put(2 * K, uea, ueb, a0, b0);
-    }
+    xpass();
+    __syncthreads();
+    double ca, cb;
+    ypass(ca, cb);
+    if (odd) put(2 * K - 1, uoa, uob, 0.5 * (pa + ca), 0.5 * (pb_ + cb));   // odd fine plane between K-1 and K
+    if (even) put(2 * K, uea, ueb, ca, cb);                                // even fine plane 2K
+    pa = ca;
+    pb_ = cb;
   }
 }
 
