@@ -138,6 +138,10 @@ typedef enum {
                                 bitwise) instead of reading the array, 16 B less HBM traffic per unknown and
                                 iteration; 0 (default): read the array (measured as fast: the element
                                 kernels are latency bound at 2 CTAs per SM, not HBM bound) */
+  ECMG_OPT_SLAB_HYBRID = 16, /* z-slabs: 1 (default) the replicated levels (before the first sharded one)
+                                run through the single-GPU path (one-CTA / persistent / CUDA-graph solves,
+                                setup ahead) on every rank, then the slab driver takes over; 0: the slab
+                                driver's host-driven loop for every level (ablation) */
   ECMG_OPT_SETUP_CTAS = 11,  /* tuning: CTAs per SM of the fp64-ALU-bound volume-load kernel when it runs
                                 ahead (0 = one CTA per work item, the full grid) */
   ECMG_OPT_VIRTUAL_SLABS = 6 /* P in 2..16: run the z-slab decomposition with P slabs on this one GPU

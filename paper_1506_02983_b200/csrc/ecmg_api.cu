@@ -69,6 +69,7 @@ struct ecmg_grid {
   bool ev_init = false;
   int kernel_variant = 1;   // ECMG_OPT_KERNEL
   int use_graph = 1;        // ECMG_OPT_GRAPH: device-driven JCG loop (CUDA graph, conditional WHILE node)
+  int hybrid = 1;           // ECMG_OPT_SLAB_HYBRID: z-slabs, replicated levels through the single-GPU path
   int fused_halo = 1;       // ECMG_OPT_FUSED_HALO: z-slab halo planes stored by K2 / init into the neighbours
   int pdl = 0;              // ECMG_OPT_PDL: programmatic dependent launch between the JCG kernels (measured: no gain
                             // inside the CUDA graphs, tools/tune_pdl.py; off by default)
@@ -86,6 +87,7 @@ struct ecmg_grid {
   long long last_free = 0;
   // z-slabs: NCCL ranks (dist) or virtual slabs on this GPU (ECMG_OPT_VIRTUAL_SLABS)
   int nranks = 1, rank = 0;
+  int size_level = 0;   // the single-GPU workspace covers levels <= size_level (z-slabs: the replicated ones)
   unsigned char nccl_id[128] = {0};
   int virt_slabs = 0;
   SlabDriver* slab = nullptr;
@@ -319,21 +321,23 @@ int run_jcg_graph(ecmg_grid* G, int k, double eps, ecmg_stats* st) {
   return fill_stats(G, g, eps, st);
 }
 
+// (these selectors act on this grid's own single-GPU buffers; on z-slab grids only the replicated levels
+// of the hybrid cascade reach them)
 // the smallest levels: the whole solve in one CTA with every vector in shared memory
 bool use_cta(const ecmg_grid* G, const LevelGeom& g) {
-  return !G->slab && G->cta_max > 0 && cta_solve_fits(g, G->elem_path, G->cta_max);
+  return G->cta_max > 0 && cta_solve_fits(g, G->elem_path, G->cta_max);
 }
 
 bool use_persistent(const ecmg_grid* G, const LevelGeom& g) {
   if (use_cta(G, g)) return true;
-  if (G->slab || G->persistent_max <= 0 || free_count(g) > G->persistent_max) return false;
+  if (G->persistent_max <= 0 || free_count(g) > G->persistent_max) return false;
   const long long nbricks = (long long)((g.nf[0] + 7) / 8) * ((g.nf[1] + 7) / 8) * ((g.nf[2] + 3) / 4);
   return nbricks <= persistent_max_bricks(G->elem_path);   // every brick's nodes stay in registers
 }
 
 // mid-size levels, constant stencil: the whole solve in one cooperative launch of TMA z-marching passes
 bool use_pers_tma(ecmg_grid* G, const LevelGeom& g) {
-  if (G->slab || G->pers_tma_max <= 0 || free_count(g) > G->pers_tma_max) return false;
+  if (G->pers_tma_max <= 0 || free_count(g) > G->pers_tma_max) return false;
   if (G->elem_path) return true;
   return G->kernel_variant == 1 && ensure_maps(G, g, level_of(G, g));
 }
@@ -573,7 +577,18 @@ int ecmg_create_grid(const ecmg_box* dom, const int coarsest_cells[3], int num_l
   // size workspace for the finest level with the largest possible free box (no Dirichlet faces)
   int face_none[6] = {FACE_ROBIN, FACE_ROBIN, FACE_ROBIN, FACE_ROBIN, FACE_ROBIN, FACE_ROBIN};
   // NCCL ranks keep their work vectors in the slab driver: size the single-GPU workspace minimally
-  const int size_level = (dist && dist->nranks > 1) ? 0 : num_levels - 1;
+  // NCCL ranks keep the sharded levels' work vectors in the slab driver; the levels below the first
+  // sharded one are solved replicated by this grid's single-GPU kernels (ecmg_run), so size for those
+  int size_level = num_levels - 1;
+  if (dist && dist->nranks > 1) {
+    size_level = 0;
+    for (int k = 0; k < num_levels; ++k) {
+      int zlo, zhi;
+      if (slab_partition((coarsest_cells[2]) << k, dist->nranks, 0, &zlo, &zhi)) break;
+      size_level = k;
+    }
+  }
+  G->size_level = size_level;
   LevelGeom gmax = make_geom(*dom, coarsest_cells, size_level, face_none, 1);
   G->vec_doubles = gmax.S * gmax.nf[2] + 64;
   G->beta_doubles = beta_doubles(gmax);
@@ -714,7 +729,7 @@ int ecmg_set_coeffs(ecmg_grid* G, const ecmg_problem* pr) {
   for (int f = 0; f < 6; ++f) all_dir = all_dir && pb.face[f] == FACE_DIRICHLET;
   const int elem_path = !(prob_beta_is_one(pb.id) && all_dir);
   if (elem_path && !G->betal.back()) {
-    const int size_level = G->nranks > 1 ? 0 : G->L - 1;
+    const int size_level = G->size_level;
     int face_none[6] = {FACE_ROBIN, FACE_ROBIN, FACE_ROBIN, FACE_ROBIN, FACE_ROBIN, FACE_ROBIN};
     for (int k = 0; k < G->L; ++k) {
       const LevelGeom gk = make_geom(G->dom, G->n0, std::min(k, size_level), face_none, 1);
@@ -751,6 +766,7 @@ int ecmg_set_option(ecmg_grid* G, int option, int value) {
     case ECMG_OPT_GRAPH: if (value != 0 && value != 1) return ECMG_EINVAL; G->use_graph = value; break;
     case ECMG_OPT_PERSISTENT: if (value < 0) return ECMG_EINVAL; G->persistent_max = value; break;
     case ECMG_OPT_PERS_TMA: if (value < 0) return ECMG_EINVAL; G->pers_tma_max = value; break;
+    case ECMG_OPT_SLAB_HYBRID: if (value != 0 && value != 1) return ECMG_EINVAL; G->hybrid = value; break;
     case ECMG_OPT_CTA_SOLVE: if (value < 0) return ECMG_EINVAL; G->cta_max = value; break;
     case ECMG_OPT_PDL: if (value != 0 && value != 1) return ECMG_EINVAL; G->pdl = value; clear_graphs(G); break;
     case ECMG_OPT_FUSED_HALO: if (value != 0 && value != 1) return ECMG_EINVAL; G->fused_halo = value; break;
@@ -875,20 +891,28 @@ int ecmg_last_jcg_timing(const ecmg_grid* G, double* ms, int* iterations, long l
 
 // Alg. 4 / Alg. 3 cascade with per-level (eps, max_iter) for the ECMG levels k >= 2 (eps <= 0:
 // exactly max_iter iterations). Levels 0, 1: DSOLVE.
+// k_end < L: only levels [0, k_end) (z-slabs: the replicated levels before the first sharded one); u_k
+// of every level stays in G->u and u_fine / ut_fine are not written.
 static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const std::vector<int>& maxit_lv,
-                       ecmg_stats* per_level, double* u_fine, double* ut_fine) {
+                       ecmg_stats* per_level, double* u_fine, double* ut_fine, int k_end = -1) {
   const double eps = eps_lv.back();
-  if (!G || !G->has_problem || !u_fine) return ECMG_EINVAL;
+  if (k_end < 0) k_end = G ? G->L : 0;
+  const bool partial = G && k_end < G->L;
+  if (!G || !G->has_problem || (!u_fine && !partial)) return ECMG_EINVAL;
+  if (partial) { u_fine = nullptr; ut_fine = nullptr; }
   for (int k = 2; k < G->L; ++k)
     for (int d = 0; d < 3; ++d) if (G->geom[k].n[d] % 4) return ECMG_EMISMATCH;
   if ((int)G->u.size() != G->L) {
     for (double* p : G->u) cudaFree(p);
     G->u.assign(G->L, nullptr);
-    for (int k = 0; k < G->L; ++k)
-      if (cudaMalloc(&G->u[k], sizeof(double) * level_nodes(G->geom[k])) != cudaSuccess) { cudaGetLastError(); return ECMG_ENOMEM; }
   }
+  for (int k = 0; k < k_end; ++k)   // per-level solutions, allocated on first use
+    if (!G->u[k] && cudaMalloc(&G->u[k], sizeof(double) * level_nodes(G->geom[k])) != cudaSuccess) {
+      cudaGetLastError();
+      return ECMG_ENOMEM;
+    }
   const bool ut_dev = ut_fine && is_device_ptr(ut_fine);
-  const bool u_dev = is_device_ptr(u_fine);
+  const bool u_dev = u_fine && is_device_ptr(u_fine);
   const long long Nf = level_nodes(G->geom[G->L - 1]);
   if (ut_fine && !ut_dev && !G->ut_tmp) {
     if (cudaMalloc(&G->ut_tmp, sizeof(double) * Nf) != cudaSuccess) { cudaGetLastError(); return ECMG_ENOMEM; }
@@ -898,6 +922,7 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
   std::vector<char> async(G->L, 0);
   for (auto& st : stv) std::memset(&st, 0, sizeof(st));
   auto level_u = [&](int k) { return (k == G->L - 1 && u_dev) ? u_fine : G->u[k]; };
+  const int L_run = k_end;
   // Setup ahead (ECMG_OPT_SETUP_AHEAD): the level setups (row a1: beta, lifted b, g_D on the Dirichlet
   // nodes of u_k) depend on no solution, so they are all enqueued up front on a low-priority stream and
   // run under the latency-bound coarse solves, which go to a high-priority stream; level k's solve
@@ -912,8 +937,8 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
     ECMG_CUDA(cudaStreamWaitEvent(G->lo2_stream, G->fork_ev, 0));
     // the finest level's setup (most of the work) on its own stream, so that it starts at once; the
     // coarser levels' setups in level order beside it
-    for (int k = 0; k < G->L; ++k) {
-      cudaStream_t s_k = (k == G->L - 1 && G->setup_ahead != 2) ? G->lo2_stream : G->lo_stream;
+    for (int k = 0; k < L_run; ++k) {
+      cudaStream_t s_k = (k == L_run - 1 && G->setup_ahead != 2) ? G->lo2_stream : G->lo_stream;
       { int s = setup_level_on(G, k, s_k, G->setup_ctas); if (s) return s; }
       ECMG_CUDA(launch_dirichlet_fill(G->geom[k], G->prob, level_u(k), 0.0, 0, s_k));
       ECMG_CUDA(cudaEventRecord(G->setup_ev[k], s_k));
@@ -921,7 +946,7 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
     G->stream = G->hi_stream;
   }
   // the whole cascade is enqueued without host synchronisation when every solve is device driven
-  for (int k = 0; k < G->L; ++k) {
+  for (int k = 0; k < L_run; ++k) {
     const LevelGeom& g = G->geom[k];
     ecmg_stats& st = stv[k];
     cudaEvent_t* e = &G->lvl_ev[5 * k];
@@ -930,7 +955,7 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
       ECMG_CUDA(cudaStreamWaitEvent(G->stream, G->setup_ev[k], 0));
       // mode 3: the z-marching (non-persistent) solves wait until the finest level's setup is done too,
       // instead of sharing the SMs with it
-      if (G->setup_ahead == 3 && !use_persistent(G, g)) ECMG_CUDA(cudaStreamWaitEvent(G->stream, G->setup_ev[G->L - 1], 0));
+      if (G->setup_ahead == 3 && !use_persistent(G, g)) ECMG_CUDA(cudaStreamWaitEvent(G->stream, G->setup_ev[L_run - 1], 0));
     }
     else { int s = setup_level(G, k); if (s) return s; }
     ECMG_CUDA(cudaEventRecord(e[1], G->stream));
@@ -964,7 +989,7 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
     }
     ECMG_CUDA(cudaEventRecord(e[4], G->stream));
   }
-  if (!u_dev)
+  if (u_fine && !u_dev)
     ECMG_CUDA(cudaMemcpyAsync(u_fine, G->u[G->L - 1], sizeof(double) * Nf, cudaMemcpyDeviceToHost, G->stream));
   if (ut_fine && !ut_dev)
     ECMG_CUDA(cudaMemcpyAsync(ut_fine, G->ut_tmp, sizeof(double) * Nf, cudaMemcpyDeviceToHost, G->stream));
@@ -973,7 +998,7 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
     ECMG_CUDA(cudaStreamWaitEvent(user, G->join_ev, 0));
   }
   ECMG_CUDA(cudaStreamSynchronize(G->stream));
-  for (int k = 0; k < G->L; ++k) {
+  for (int k = 0; k < L_run; ++k) {
     ecmg_stats& st = stv[k];
     if (async[k]) {
       int s = stats_from(G->lvl_sc[k], k < 2 ? 1e-14 : eps_lv[k], &st);
@@ -986,12 +1011,12 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
     st.ms_solve = elapsed(e[2], e[3]);
     st.ms_rich = elapsed(e[3], e[4]);
   }
-  if (async[G->L - 1]) {
-    G->last_jcg_iters = G->lvl_sc[G->L - 1].iter;
-    G->last_free = free_count(G->geom[G->L - 1]);
-    G->last_jcg_ms = elapsed(G->lvl_ev[5 * (G->L - 1) + 2], G->lvl_ev[5 * (G->L - 1) + 3]);
+  if (async[L_run - 1]) {
+    G->last_jcg_iters = G->lvl_sc[L_run - 1].iter;
+    G->last_free = free_count(G->geom[L_run - 1]);
+    G->last_jcg_ms = elapsed(G->lvl_ev[5 * (L_run - 1) + 2], G->lvl_ev[5 * (L_run - 1) + 3]);
   }
-  if (per_level) for (int k = 0; k < G->L; ++k) per_level[k] = stv[k];
+  if (per_level) for (int k = 0; k < L_run; ++k) per_level[k] = stv[k];
   (void)eps;
   return status;
 }
@@ -1004,8 +1029,27 @@ int ecmg_run(ecmg_grid* G, double eps, ecmg_stats* per_level, double* u_fine, do
     for (int k = 2; k < G->L; ++k)
       for (int d = 0; d < 3; ++d) if (G->geom[k].n[d] % 4) return ECMG_EMISMATCH;
     std::vector<ecmg_stats> stv(G->L);
+    // Hybrid cascade: the levels before the first sharded one are replicated (every rank solves them
+    // whole, with no communication), so they run through this grid's single-GPU path (one-CTA /
+    // persistent / graph solves, setup ahead); their last two solutions seed the first sharded level's
+    // EXP_finite in every local slab, and the slab driver takes over from there.
+    int kc = slab_first_sharded(G->slab);
+    if (G->hybrid && kc >= 2 && kc <= G->size_level + 1) {
+      int s0 = run_cascade(G, std::vector<double>(G->L, eps), std::vector<int>(G->L, 10000), stv.data(), nullptr,
+                           nullptr, kc);
+      if (s0 == ECMG_ECUDA || s0 == ECMG_ENOMEM) return s0;
+      for (int k = kc - 2; k < kc; ++k) {
+        const int r = slab_import_u(G->slab, k, G->u[k], G->stream);
+        if (r) return r;
+      }
+      const int s = slab_run(G->slab, eps, stv.data(), u_fine, is_device_ptr(u_fine), ut_fine,
+                             ut_fine ? is_device_ptr(ut_fine) : false, G->stream, kc);
+      slab_last_timing(G->slab, &G->last_jcg_ms, &G->last_jcg_iters, &G->last_free);
+      if (per_level) for (int k = 0; k < G->L; ++k) per_level[k] = stv[k];
+      return s != ECMG_OK ? s : s0;
+    }
     const int s = slab_run(G->slab, eps, stv.data(), u_fine, is_device_ptr(u_fine), ut_fine,
-                           ut_fine ? is_device_ptr(ut_fine) : false, G->stream);
+                           ut_fine ? is_device_ptr(ut_fine) : false, G->stream, 0);
     slab_last_timing(G->slab, &G->last_jcg_ms, &G->last_jcg_iters, &G->last_free);
     if (per_level) for (int k = 0; k < G->L; ++k) per_level[k] = stv[k];
     return s;

@@ -609,12 +609,25 @@ void slab_last_timing(const SlabDriver* d, double* ms, int* it, long long* nfree
 // ---- Alg. 4 over slabs -------------------------------------------------------------------------
 // u_out / ut_out: virtual slabs -> full-layout finest vectors (device or host); NCCL ranks -> this
 // rank's owned planes [zlo, zhi) of the finest level.
+int slab_first_sharded(const SlabDriver* d) {
+  const auto& sh = d->s[0].sharded;
+  for (int k = 0; k < (int)sh.size(); ++k)
+    if (sh[k]) return k;
+  return (int)sh.size();
+}
+
+int slab_import_u(SlabDriver* d, int k, const double* u_full, cudaStream_t stream) {
+  for (auto& c : d->s)
+    SL_CUDA(cudaMemcpyAsync(c.u[k], u_full, sizeof(double) * level_nodes(c.geom[k]), cudaMemcpyDeviceToDevice, stream));
+  return ECMG_OK;
+}
+
 int slab_run(SlabDriver* d, double eps, ecmg_stats* per_level, double* u_out, bool u_dev, double* ut_out, bool ut_dev,
-             cudaStream_t stream) {
+             cudaStream_t stream, int k_begin) {
   const SlabCfg& cf = d->cfg;
   const int L = cf.L;
   int status = ECMG_OK;
-  for (int k = 0; k < L; ++k) {
+  for (int k = k_begin; k < L; ++k) {
     ecmg_stats st{};
     const bool sh = d->s[0].sharded[k];
     const int nloc = (sh || !d->virt) ? (int)d->s.size() : 1;

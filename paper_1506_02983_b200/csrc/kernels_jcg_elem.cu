@@ -41,7 +41,10 @@
 namespace ecmg {
 namespace {
 
-constexpr int RY = 2;                 // node rows per warp (two fp64 plane windows stay in registers)
+#ifndef ELEM_RY
+#define ELEM_RY 2
+#endif
+constexpr int RY = ELEM_RY;           // node rows per warp (two fp64 plane windows stay in registers)
 constexpr int TY = WARPS * RY;        // 16
 constexpr int HX = TX + 4;            // 36: node halo box x = X0-2 .. X0+33 (16-B aligned start)
 constexpr int XO = 2;                 // smem column of x = X0

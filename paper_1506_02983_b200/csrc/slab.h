@@ -21,8 +21,13 @@ struct SlabDriver;
 SlabDriver* slab_driver_create(const SlabCfg& cfg, int P, int rank, bool virt, const unsigned char* nccl_id, int* status);
 void slab_driver_configure(SlabDriver* d, const SlabCfg& cfg);
 void slab_driver_destroy(SlabDriver* d);
+// levels [k_begin, L) (levels below k_begin: u_k imported with slab_import_u, per_level left untouched)
 int slab_run(SlabDriver* d, double eps, ecmg_stats* per_level, double* u_out, bool u_dev, double* ut_out, bool ut_dev,
-             cudaStream_t stream);
+             cudaStream_t stream, int k_begin);
+// first sharded level (L if none); every level below it is replicated
+int slab_first_sharded(const SlabDriver* d);
+// copy a full-layout level-k solution into every local slab's u_k (the replicated levels' solutions)
+int slab_import_u(SlabDriver* d, int k, const double* u_full, cudaStream_t stream);
 int slab_solve_level(SlabDriver* d, int k, double eps, int max_iter, double* u, ecmg_stats* st, cudaStream_t stream);
 void slab_level_range(const SlabDriver* d, int k, int* zlo, int* zhi);
 void slab_last_timing(const SlabDriver* d, double* ms, int* it, long long* nfree);

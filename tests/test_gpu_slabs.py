@@ -117,3 +117,25 @@ def test_fused_halo_equals_copied_halo(pid, levels, eps, P):
         res.append(([s["iterations"] for s in stats], host(u), host(ut)))
     assert res[0][0] == res[1][0]
     assert np.array_equal(res[0][1], res[1][1]) and np.array_equal(res[0][2], res[1][2])
+
+
+@pytest.mark.parametrize("pid,levels,eps,P", [(o.C2, 6, 1e-10, 2), (o.C4, 6, 1e-9, 8), (o.C3, 5, 1e-10, 2),
+                                              (o.C5, 6, 1e-8, 4)])
+def test_hybrid_cascade_vs_slab_loop(pid, levels, eps, P):
+    # ECMG_OPT_SLAB_HYBRID: the replicated levels (before the first sharded one) run through the single-GPU
+    # path (one-CTA / persistent / graph solves, setup ahead), then their last two solutions seed the slab
+    # driver; the slab driver's host loop for every level is the reference: counts +-1, solutions within
+    # rounding, and the per-level statistics of every level are filled
+    res = []
+    for hyb in (1, 0):
+        g = Grid(4, levels, pid, params_for(pid))
+        g.set_option(ecmg.OPT_VIRTUAL_SLABS, P)
+        g.set_option(ecmg.OPT_SLAB_HYBRID, hyb)
+        u, ut = g.new_vec(levels - 1), g.new_vec(levels - 1)
+        st, stats = g.run(eps, u, ut)
+        assert st == 0
+        assert all(s["iterations"] > 0 and s["rel_res_true"] > 0 for s in stats)
+        res.append(([s["iterations"] for s in stats], host(u), host(ut)))
+    assert all(abs(a - b) <= 1 for a, b in zip(res[0][0], res[1][0])), (res[0][0], res[1][0])
+    for k in (1, 2):
+        assert np.max(np.abs(res[0][k] - res[1][k])) <= 1e-9 * np.max(np.abs(res[1][k]))

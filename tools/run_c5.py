@@ -14,7 +14,10 @@ from paper_1506_02983_b200 import Grid, PROB  # noqa: E402
 
 def main():
     levels = int(sys.argv[1]) if len(sys.argv) > 1 else 9
+    fly = int(sys.argv[2]) if len(sys.argv) > 2 else 0
     g = Grid(4, levels, PROB["C5"], synth.c5_geometry(0))
+    from paper_1506_02983_b200 import ecmg
+    g.set_option(ecmg.OPT_BETA_FLY, fly)
     shape, nodes = g.shape(levels - 1)
     u = torch.empty(nodes, dtype=torch.float64, device="cuda")
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -23,7 +26,7 @@ def main():
     st, stats = g.run(1e-8, u)
     ev[1].record()
     torch.cuda.synchronize()
-    out = dict(config="C5 4^3->%d^3" % (4 << (levels - 1)), status=st, tts_ms=ev[0].elapsed_time(ev[1]),
+    out = dict(config="C5 4^3->%d^3" % (4 << (levels - 1)), beta_fly=fly, status=st, tts_ms=ev[0].elapsed_time(ev[1]),
                wall_s=time.time() - t0, iterations=[s["iterations"] for s in stats],
                solve_ms=[round(s["ms_solve"], 2) for s in stats], rel_true=[s["rel_res_true"] for s in stats],
                mem_gb=torch.cuda.max_memory_allocated() / 1e9)
