@@ -74,6 +74,11 @@ def lib():
             L.orc_exp_true.restype = C.c_int
             L.orc_exp_true.argtypes = [vp, dp, dp, dp]
             L.orc_norms.argtypes = [vp, dp, dp, dp]
+            llp = C.POINTER(C.c_longlong)
+            L.orc_rows.argtypes = [dp, dp, ip, C.c_int, dp, C.c_int, ip, llp, C.c_long, dp, dp, dp, dp]
+            L.orc_rows.restype = C.c_int
+            L.orc_exp_nodes.argtypes = [dp, dp, ip, C.c_int, dp, C.c_int, ip, C.c_int, dp, dp, llp, C.c_long, dp]
+            L.orc_exp_nodes.restype = C.c_int
             L.orc_element_stiffness.argtypes = [dp, C.c_double, dp]
             L.orc_face_integrals.argtypes = [C.c_double, C.c_double, dp, dp, dp, dp]
             L.orc_serendipity_weights.argtypes = [C.c_double, C.c_double, C.c_double, dp]
@@ -266,3 +271,47 @@ def ecmg_fixed(n0, levels, problem_id, m_L, ratio, params=None, lo=(0, 0, 0), hi
                               _d(w) if w is not None else None)
     stats = stats.reshape(levels, NSTAT)
     return (st, stats, u, ut, w) if want_w else (st, stats, u, ut)
+
+
+# ---- sampled evaluation without assembling the level (parity at full size) -------------------------
+def _nodes(nodes):
+    a = np.ascontiguousarray(np.asarray(nodes, dtype=np.int64).reshape(-1, 3))
+    return a, a.ctypes.data_as(C.POINTER(C.c_longlong))
+
+
+def rows(n_cells, problem_id, nodes, p=None, params=None, lo=(0, 0, 0), hi=(1, 1, 1), faces=None, diag=False):
+    """(A_ff p)_i and the lifted b_f,i at the given (ix, iy, iz) nodes, each row accumulated from the
+    element (and Robin face) matrices around the node in build_level's order; with diag=True also A_ii."""
+    nd, ndp = _nodes(nodes)
+    n = np.array([int(v) for v in n_cells], dtype=np.int32)
+    prm = _f64(params if params is not None else np.zeros(1))
+    fc = np.array(faces if faces is not None else default_faces(problem_id), dtype=np.int32)
+    q = np.empty(len(nd))
+    b = np.empty(len(nd))
+    pp = _f64(p) if p is not None else None
+    dg = np.empty(len(nd)) if diag else None
+    st = lib().orc_rows(_d(_f64(lo)), _d(_f64(hi)), _i(n), problem_id, _d(prm),
+                        int(prm.size if params is not None else 0), _i(fc), ndp, len(nd),
+                        _d(pp) if pp is not None else None, _d(q) if pp is not None else None, _d(b),
+                        _d(dg) if diag else None)
+    if st != 0:
+        raise ValueError(f"oracle rows: {st}")
+    if diag:
+        return (q if pp is not None else None), b, dg
+    return (q if pp is not None else None), b
+
+
+def exp_nodes(n_cells, problem_id, which, a, c, nodes, params=None, lo=(0, 0, 0), hi=(1, 1, 1), faces=None):
+    """which 0: EXP_finite (Serendipity), 1: EXP_finite (Remark 2 Lagrange), 2: EXP_true, at the given
+    fine nodes; a, c = (u_2h, u_4h) or (u_h, u_2h) as full nodal vectors."""
+    nd, ndp = _nodes(nodes)
+    n = np.array([int(v) for v in n_cells], dtype=np.int32)
+    prm = _f64(params if params is not None else np.zeros(1))
+    fc = np.array(faces if faces is not None else default_faces(problem_id), dtype=np.int32)
+    out = np.empty(len(nd))
+    st = lib().orc_exp_nodes(_d(_f64(lo)), _d(_f64(hi)), _i(n), problem_id, _d(prm),
+                             int(prm.size if params is not None else 0), _i(fc), int(which), _d(_f64(a)),
+                             _d(_f64(c)), ndp, len(nd), _d(out))
+    if st != 0:
+        raise ValueError(f"oracle exp_nodes: {st}")
+    return out

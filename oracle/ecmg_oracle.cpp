@@ -580,46 +580,52 @@ double serendipity_N(int label, double xi, double eta, double zeta) {
   return 0.0;
 }
 
-// EXP_finite (Alg. 4 l.6 "w_h = EXP_finite(u_2h, u_4h)"; §4.3)
-void exp_finite(const Level& Lf, const double* u2h, const double* u4h, double* w) {
-  const long n4[3] = {Lf.n[0] / 4, Lf.n[1] / 4, Lf.n[2] / 4};
-  const long nn2[3] = {Lf.n[0] / 2 + 1, Lf.n[1] / 2 + 1, Lf.n[2] / 2 + 1};
+// EXP_finite (Alg. 4 l.6 "w_h = EXP_finite(u_2h, u_4h)"; §4.3) at fine node
+// (ix, iy, iz) of a level with n cells per axis (before the Dirichlet overwrite): the owner 4h block's
+// 20 seeds by Eqs. (jiedian) / (zhongdian), then W = sum_i N_i W_i (Eq. inter) in label order.
+double exp_finite_node(const int n[3], const double* u2h, const double* u4h, long ix, long iy, long iz) {
+  const long n4[3] = {n[0] / 4, n[1] / 4, n[2] / 4};
+  const long nn2[3] = {n[0] / 2 + 1, n[1] / 2 + 1, n[2] / 2 + 1};
   const long nn4[3] = {n4[0] + 1, n4[1] + 1, n4[2] + 1};
   auto U1 = [&](long i, long j, long k) { return u2h[i + nn2[0] * (j + nn2[1] * k)]; };
   auto U0 = [&](long i, long j, long k) { return u4h[i + nn4[0] * (j + nn4[1] * k)]; };
+  long id[3] = {ix, iy, iz}, b[3], l[3];
+  for (int d = 0; d < 3; ++d) { b[d] = std::min(id[d] / 4, n4[d] - 1); l[d] = id[d] - 4 * b[d]; }
+  // the 20 seeds of block b, in label order
+  double seed[20];
+  for (int s = 0; s < 20; ++s) {
+    int ls[3]; label_local(SEED_LABEL[s], ls);
+    int nmid = (ls[0] == 2) + (ls[1] == 2) + (ls[2] == 2);
+    if (nmid == 0) {
+      // corner: W = (5 U^1 - U^0)/4, Eq. (jiedian)
+      double u1 = U1(2 * b[0] + ls[0] / 2, 2 * b[1] + ls[1] / 2, 2 * b[2] + ls[2] / 2);
+      double u0 = U0(b[0] + ls[0] / 4, b[1] + ls[1] / 4, b[2] + ls[2] / 4);
+      seed[s] = (5.0 * u1 - u0) / 4.0;
+    } else {
+      // edge midpoint: W = U^1_mid + (1/8)(U^1_a - U^0_a + U^1_b - U^0_b), Eq. (zhongdian)
+      int dm = (ls[0] == 2) ? 0 : (ls[1] == 2 ? 1 : 2);
+      long la[3] = {ls[0], ls[1], ls[2]}, lb[3] = {ls[0], ls[1], ls[2]};
+      la[dm] = 0; lb[dm] = 4;
+      double um = U1(2 * b[0] + ls[0] / 2, 2 * b[1] + ls[1] / 2, 2 * b[2] + ls[2] / 2);
+      double u1a = U1(2 * b[0] + la[0] / 2, 2 * b[1] + la[1] / 2, 2 * b[2] + la[2] / 2);
+      double u0a = U0(b[0] + la[0] / 4, b[1] + la[1] / 4, b[2] + la[2] / 4);
+      double u1b = U1(2 * b[0] + lb[0] / 2, 2 * b[1] + lb[1] / 2, 2 * b[2] + lb[2] / 2);
+      double u0b = U0(b[0] + lb[0] / 4, b[1] + lb[1] / 4, b[2] + lb[2] / 4);
+      seed[s] = um + (1.0 / 8.0) * (u1a - u0a + u1b - u0b);
+    }
+  }
+  double xi = (l[0] - 2) / 2.0, eta = (l[1] - 2) / 2.0, zeta = (l[2] - 2) / 2.0;
+  double W = 0.0;
+  for (int s = 0; s < 20; ++s) W += serendipity_N(SEED_LABEL[s], xi, eta, zeta) * seed[s];
+  return W;
+}
+
+void exp_finite(const Level& Lf, const double* u2h, const double* u4h, double* w) {
   for (long iz = 0; iz < Lf.nn[2]; ++iz)
     for (long iy = 0; iy < Lf.nn[1]; ++iy)
       for (long ix = 0; ix < Lf.nn[0]; ++ix) {
-        long id[3] = {ix, iy, iz}, b[3], l[3];
-        for (int d = 0; d < 3; ++d) { b[d] = std::min(id[d] / 4, n4[d] - 1); l[d] = id[d] - 4 * b[d]; }
-        // the 20 seeds of block b, in label order
-        double seed[20];
-        for (int s = 0; s < 20; ++s) {
-          int ls[3]; label_local(SEED_LABEL[s], ls);
-          int nmid = (ls[0] == 2) + (ls[1] == 2) + (ls[2] == 2);
-          if (nmid == 0) {
-            // corner: W = (5 U^1 - U^0)/4, Eq. (jiedian)
-            double u1 = U1(2 * b[0] + ls[0] / 2, 2 * b[1] + ls[1] / 2, 2 * b[2] + ls[2] / 2);
-            double u0 = U0(b[0] + ls[0] / 4, b[1] + ls[1] / 4, b[2] + ls[2] / 4);
-            seed[s] = (5.0 * u1 - u0) / 4.0;
-          } else {
-            // edge midpoint: W = U^1_mid + (1/8)(U^1_a - U^0_a + U^1_b - U^0_b), Eq. (zhongdian)
-            int dm = (ls[0] == 2) ? 0 : (ls[1] == 2 ? 1 : 2);
-            long la[3] = {ls[0], ls[1], ls[2]}, lb[3] = {ls[0], ls[1], ls[2]};
-            la[dm] = 0; lb[dm] = 4;
-            double um = U1(2 * b[0] + ls[0] / 2, 2 * b[1] + ls[1] / 2, 2 * b[2] + ls[2] / 2);
-            double u1a = U1(2 * b[0] + la[0] / 2, 2 * b[1] + la[1] / 2, 2 * b[2] + la[2] / 2);
-            double u0a = U0(b[0] + la[0] / 4, b[1] + la[1] / 4, b[2] + la[2] / 4);
-            double u1b = U1(2 * b[0] + lb[0] / 2, 2 * b[1] + lb[1] / 2, 2 * b[2] + lb[2] / 2);
-            double u0b = U0(b[0] + lb[0] / 4, b[1] + lb[1] / 4, b[2] + lb[2] / 4);
-            seed[s] = um + (1.0 / 8.0) * (u1a - u0a + u1b - u0b);
-          }
-        }
-        double xi = (l[0] - 2) / 2.0, eta = (l[1] - 2) / 2.0, zeta = (l[2] - 2) / 2.0;
-        double W = 0.0;
-        for (int s = 0; s < 20; ++s) W += serendipity_N(SEED_LABEL[s], xi, eta, zeta) * seed[s];
         long i = Lf.idx(ix, iy, iz);
-        w[i] = Lf.dir[i] ? Lf.gDv[i] : W;  // Dirichlet overwrite (§8c A15)
+        w[i] = Lf.dir[i] ? Lf.gDv[i] : exp_finite_node(Lf.n, u2h, u4h, ix, iy, iz);  // Dirichlet overwrite (§8c A15)
       }
 }
 
@@ -633,97 +639,172 @@ double lagrange_quadratic(int node, double t) {  // node in {0,1,2} at t = -1, 0
   return t * (t + 1.0) / 2.0;
 }
 
-void exp_finite_lagrange(const Level& Lf, const double* u2h, const double* u4h, double* w) {
-  const long n4[3] = {Lf.n[0] / 4, Lf.n[1] / 4, Lf.n[2] / 4};
-  const long nn2[3] = {Lf.n[0] / 2 + 1, Lf.n[1] / 2 + 1, Lf.n[2] / 2 + 1};
+double exp_finite_lagrange_node(const int n[3], const double* u2h, const double* u4h, long ix, long iy, long iz) {
+  const long n4[3] = {n[0] / 4, n[1] / 4, n[2] / 4};
+  const long nn2[3] = {n[0] / 2 + 1, n[1] / 2 + 1, n[2] / 2 + 1};
   const long nn4[3] = {n4[0] + 1, n4[1] + 1, n4[2] + 1};
   auto U1 = [&](long i, long j, long k) { return u2h[i + nn2[0] * (j + nn2[1] * k)]; };
   auto U0 = [&](long i, long j, long k) { return u4h[i + nn4[0] * (j + nn4[1] * k)]; };
+  long id[3] = {ix, iy, iz}, b[3], l[3];
+  for (int d = 0; d < 3; ++d) { b[d] = std::min(id[d] / 4, n4[d] - 1); l[d] = id[d] - 4 * b[d]; }
+  double seed[3][3][3];  // [k][j][i] local 2h offsets 0..2 in the block
+  for (int k = 0; k < 3; ++k)
+    for (int j = 0; j < 3; ++j)
+      for (int i = 0; i < 3; ++i) {
+        int c[3] = {i, j, k};
+        int ax[3], na = 0;
+        for (int d = 0; d < 3; ++d) if (c[d] == 1) ax[na++] = d;
+        long g[3] = {2 * b[0] + i, 2 * b[1] + j, 2 * b[2] + k};  // 2h index
+        if (na == 0) {
+          seed[k][j][i] = (5.0 * U1(g[0], g[1], g[2]) - U0(b[0] + i / 2, b[1] + j / 2, b[2] + k / 2)) / 4.0;
+          continue;
+        }
+        int nseg = 1 << (na - 1);
+        double sum = 0.0;
+        for (int s = 0; s < nseg; ++s) {
+          int ca[3] = {i, j, k}, cb[3] = {i, j, k};
+          ca[ax[0]] = 0; cb[ax[0]] = 2;
+          for (int t = 1; t < na; ++t) {
+            bool plus = (s >> (t - 1)) & 1;
+            ca[ax[t]] = plus ? 0 : 2; cb[ax[t]] = plus ? 2 : 0;
+          }
+          double ua1 = U1(2 * b[0] + ca[0], 2 * b[1] + ca[1], 2 * b[2] + ca[2]);
+          double ua0 = U0(b[0] + ca[0] / 2, b[1] + ca[1] / 2, b[2] + ca[2] / 2);
+          double ub1 = U1(2 * b[0] + cb[0], 2 * b[1] + cb[1], 2 * b[2] + cb[2]);
+          double ub0 = U0(b[0] + cb[0] / 2, b[1] + cb[1] / 2, b[2] + cb[2] / 2);
+          sum += U1(g[0], g[1], g[2]) + (1.0 / 8.0) * (ua1 - ua0 + ub1 - ub0);  // Eq. (zhongdian)
+        }
+        seed[k][j][i] = sum / nseg;
+      }
+  double xi = (l[0] - 2) / 2.0, eta = (l[1] - 2) / 2.0, zeta = (l[2] - 2) / 2.0;
+  double W = 0.0;
+  for (int k = 0; k < 3; ++k)
+    for (int j = 0; j < 3; ++j)
+      for (int i = 0; i < 3; ++i)
+        W += lagrange_quadratic(i, xi) * lagrange_quadratic(j, eta) * lagrange_quadratic(k, zeta) * seed[k][j][i];
+  return W;
+}
+
+void exp_finite_lagrange(const Level& Lf, const double* u2h, const double* u4h, double* w) {
   for (long iz = 0; iz < Lf.nn[2]; ++iz)
     for (long iy = 0; iy < Lf.nn[1]; ++iy)
       for (long ix = 0; ix < Lf.nn[0]; ++ix) {
-        long id[3] = {ix, iy, iz}, b[3], l[3];
-        for (int d = 0; d < 3; ++d) { b[d] = std::min(id[d] / 4, n4[d] - 1); l[d] = id[d] - 4 * b[d]; }
-        double seed[3][3][3];  // [k][j][i] local 2h offsets 0..2 in the block
-        for (int k = 0; k < 3; ++k)
-          for (int j = 0; j < 3; ++j)
-            for (int i = 0; i < 3; ++i) {
-              int c[3] = {i, j, k};
-              int ax[3], na = 0;
-              for (int d = 0; d < 3; ++d) if (c[d] == 1) ax[na++] = d;
-              long g[3] = {2 * b[0] + i, 2 * b[1] + j, 2 * b[2] + k};  // 2h index
-              if (na == 0) {
-                seed[k][j][i] = (5.0 * U1(g[0], g[1], g[2]) - U0(b[0] + i / 2, b[1] + j / 2, b[2] + k / 2)) / 4.0;
-                continue;
-              }
-              int nseg = 1 << (na - 1);
-              double sum = 0.0;
-              for (int s = 0; s < nseg; ++s) {
-                int ca[3] = {i, j, k}, cb[3] = {i, j, k};
-                ca[ax[0]] = 0; cb[ax[0]] = 2;
-                for (int t = 1; t < na; ++t) {
-                  bool plus = (s >> (t - 1)) & 1;
-                  ca[ax[t]] = plus ? 0 : 2; cb[ax[t]] = plus ? 2 : 0;
-                }
-                double ua1 = U1(2 * b[0] + ca[0], 2 * b[1] + ca[1], 2 * b[2] + ca[2]);
-                double ua0 = U0(b[0] + ca[0] / 2, b[1] + ca[1] / 2, b[2] + ca[2] / 2);
-                double ub1 = U1(2 * b[0] + cb[0], 2 * b[1] + cb[1], 2 * b[2] + cb[2]);
-                double ub0 = U0(b[0] + cb[0] / 2, b[1] + cb[1] / 2, b[2] + cb[2] / 2);
-                sum += U1(g[0], g[1], g[2]) + (1.0 / 8.0) * (ua1 - ua0 + ub1 - ub0);  // Eq. (zhongdian)
-              }
-              seed[k][j][i] = sum / nseg;
-            }
-        double xi = (l[0] - 2) / 2.0, eta = (l[1] - 2) / 2.0, zeta = (l[2] - 2) / 2.0;
-        double W = 0.0;
-        for (int k = 0; k < 3; ++k)
-          for (int j = 0; j < 3; ++j)
-            for (int i = 0; i < 3; ++i)
-              W += lagrange_quadratic(i, xi) * lagrange_quadratic(j, eta) * lagrange_quadratic(k, zeta) * seed[k][j][i];
         long ii = Lf.idx(ix, iy, iz);
-        w[ii] = Lf.dir[ii] ? Lf.gDv[ii] : W;
+        w[ii] = Lf.dir[ii] ? Lf.gDv[ii] : exp_finite_lagrange_node(Lf.n, u2h, u4h, ix, iy, iz);
       }
 }
 
-// EXP_true (Alg. 4 l.10 "u~_h = EXP_true(u_h, u_2h)")
-void exp_true(const Level& Lf, const double* uh, const double* u2h, double* ut) {
-  const long nn2[3] = {Lf.n[0] / 2 + 1, Lf.n[1] / 2 + 1, Lf.n[2] / 2 + 1};
-  auto U1 = [&](long i, long j, long k) { return uh[Lf.idx(i, j, k)]; };
+// EXP_true (Alg. 4 l.10 "u~_h = EXP_true(u_h, u_2h)") at fine node (ix, iy, iz)
+// of a level with n cells per axis, before the Dirichlet overwrite
+double exp_true_node(const int n[3], const double* uh, const double* u2h, long ix, long iy, long iz) {
+  const long nn[3] = {n[0] + 1L, n[1] + 1L, n[2] + 1L};
+  const long nn2[3] = {n[0] / 2 + 1, n[1] / 2 + 1, n[2] / 2 + 1};
+  auto U1 = [&](long i, long j, long k) { return uh[i + nn[0] * (j + nn[1] * k)]; };
   auto U0 = [&](long i, long j, long k) { return u2h[(i / 2) + nn2[0] * ((j / 2) + nn2[1] * (k / 2))]; };
   // Chen-Lin value at midpoint m of the segment a..b (a, b coarse-coincident), Eq. (chenlin)
   auto chenlin = [&](const long m[3], const long a[3], const long b[3]) {
     return U1(m[0], m[1], m[2]) + (1.0 / 6.0) * (U1(a[0], a[1], a[2]) - U0(a[0], a[1], a[2]) +
                                                    U1(b[0], b[1], b[2]) - U0(b[0], b[1], b[2]));
   };
+  long m[3] = {ix, iy, iz};
+  int odd[3] = {(int)(ix & 1), (int)(iy & 1), (int)(iz & 1)};
+  int nodd = odd[0] + odd[1] + odd[2];
+  if (nodd == 0) return (4.0 * U1(ix, iy, iz) - U0(ix, iy, iz)) / 3.0;  // Eq. (t1)
+  // enumerate the diagonals through m: sign patterns over the odd axes with the first odd
+  // axis fixed to -1 (a) / +1 (b): 1 segment (edge), 2 (face), 4 (cell)
+  int ax[3], na = 0;
+  for (int d = 0; d < 3; ++d) if (odd[d]) ax[na++] = d;
+  int nseg = 1 << (na - 1);
+  double sum = 0.0;
+  for (int s = 0; s < nseg; ++s) {
+    long a[3] = {ix, iy, iz}, b[3] = {ix, iy, iz};
+    a[ax[0]] -= 1; b[ax[0]] += 1;
+    for (int t = 1; t < na; ++t) {
+      int sg = ((s >> (t - 1)) & 1) ? 1 : -1;
+      a[ax[t]] -= sg; b[ax[t]] += sg;
+    }
+    sum += chenlin(m, a, b);
+  }
+  return sum / nseg;  // arithmetic mean over the diagonals (§8c A13)
+}
+
+void exp_true(const Level& Lf, const double* uh, const double* u2h, double* ut) {
   for (long iz = 0; iz < Lf.nn[2]; ++iz)
     for (long iy = 0; iy < Lf.nn[1]; ++iy)
       for (long ix = 0; ix < Lf.nn[0]; ++ix) {
-        long m[3] = {ix, iy, iz};
-        int odd[3] = {(int)(ix & 1), (int)(iy & 1), (int)(iz & 1)};
-        int nodd = odd[0] + odd[1] + odd[2];
-        double v;
-        if (nodd == 0) {
-          v = (4.0 * U1(ix, iy, iz) - U0(ix, iy, iz)) / 3.0;  // Eq. (t1)
-        } else {
-          // enumerate the diagonals through m: sign patterns over the odd axes with the first odd
-          // axis fixed to -1 (a) / +1 (b): 1 segment (edge), 2 (face), 4 (cell)
-          int ax[3], na = 0;
-          for (int d = 0; d < 3; ++d) if (odd[d]) ax[na++] = d;
-          int nseg = 1 << (na - 1);
-          double sum = 0.0;
-          for (int s = 0; s < nseg; ++s) {
-            long a[3] = {ix, iy, iz}, b[3] = {ix, iy, iz};
-            a[ax[0]] -= 1; b[ax[0]] += 1;
-            for (int t = 1; t < na; ++t) {
-              int sg = ((s >> (t - 1)) & 1) ? 1 : -1;
-              a[ax[t]] -= sg; b[ax[t]] += sg;
-            }
-            sum += chenlin(m, a, b);
-          }
-          v = sum / nseg;  // arithmetic mean over the diagonals (§8c A13)
-        }
         long i = Lf.idx(ix, iy, iz);
-        ut[i] = Lf.dir[i] ? Lf.gDv[i] : v;
+        ut[i] = Lf.dir[i] ? Lf.gDv[i] : exp_true_node(Lf.n, uh, u2h, ix, iy, iz);
       }
+}
+
+// ---- one row at a time (parity at full size on sampled nodes: no global matrix) -------------
+// Row i = (ix, iy, iz) of the assembled matrix (27 entries by neighbour offset, before elimination)
+// and its load F_i, accumulated exactly as build_level does: the (up to 8) elements around the node
+// in the same lexicographic element order, then the Robin faces in face and face-element order. Every
+// entry is therefore the same sum in the same order as build_level's.
+bool node_is_dirichlet(const Problem& P, const int n[3], long ix, long iy, long iz) {
+  long id[3] = {ix, iy, iz};
+  for (int d = 0; d < 3; ++d) {
+    if (id[d] == 0 && P.face[2 * d] == FACE_DIRICHLET) return true;
+    if (id[d] == n[d] && P.face[2 * d + 1] == FACE_DIRICHLET) return true;
+  }
+  return false;
+}
+
+void assemble_row(const Problem& P, const double lo[3], const double h[3], const int n[3], long ix, long iy, long iz,
+                  double A27[27], double* F) {
+  for (int t = 0; t < 27; ++t) A27[t] = 0.0;
+  *F = 0.0;
+  double K[8][8], Fe[8];
+  const long id[3] = {ix, iy, iz};
+  for (long ez = iz - 1; ez <= iz; ++ez)
+    for (long ey = iy - 1; ey <= iy; ++ey)
+      for (long ex = ix - 1; ex <= ix; ++ex) {
+        if (ex < 0 || ey < 0 || ez < 0 || ex >= n[0] || ey >= n[1] || ez >= n[2]) continue;
+        double cx = lo[0] + (ex + 0.5) * h[0];
+        double cy = lo[1] + (ey + 0.5) * h[1];
+        double cz = lo[2] + (ez + 0.5) * h[2];
+        element_stiffness(h, P.beta(cx, cy, cz), K);
+        int e[3] = {(int)ex, (int)ey, (int)ez};
+        element_load(P, lo, h, e, Fe);
+        const int a = (int)(ix - ex) + 2 * (int)(iy - ey) + 4 * (int)(iz - ez);
+        *F += Fe[a];
+        for (int bb = 0; bb < 8; ++bb) {
+          int dx = (bb & 1) - (a & 1), dy = ((bb >> 1) & 1) - ((a >> 1) & 1), dz = ((bb >> 2) & 1) - ((a >> 2) & 1);
+          A27[slot(dx, dy, dz)] += K[a][bb];
+        }
+      }
+  for (int face = 0; face < 6; ++face) {
+    if (P.face[face] != FACE_ROBIN) continue;
+    const int d = face / 2, side = face % 2;
+    const int d1 = (d == 0) ? 1 : 0, d2 = (d == 2) ? 1 : 2;
+    const long fixed = side ? n[d] : 0;
+    if (id[d] != fixed) continue;
+    for (long e2 = id[d2] - 1; e2 <= id[d2]; ++e2)
+      for (long e1 = id[d1] - 1; e1 <= id[d1]; ++e1) {
+        if (e1 < 0 || e2 < 0 || e1 >= n[d1] || e2 >= n[d2]) continue;
+        double aq[4], gq[4];
+        for (int q = 0; q < 4; ++q) {
+          double xi1 = sgn(q, 0) * GAUSS, xi2 = sgn(q, 1) * GAUSS;
+          double x[3];
+          x[d] = lo[d] + fixed * h[d];
+          x[d1] = lo[d1] + (e1 + (1.0 + xi1) / 2.0) * h[d1];
+          x[d2] = lo[d2] + (e2 + (1.0 + xi2) / 2.0) * h[d2];
+          aq[q] = P.alpha(face);
+          gq[q] = P.gR(face, x[0], x[1], x[2]);
+        }
+        double M[4][4], G[4];
+        face_integrals(h[d1], h[d2], aq, gq, M, G);
+        const int c = (int)(id[d1] - e1) + 2 * (int)(id[d2] - e2);
+        *F += G[c];
+        for (int c2 = 0; c2 < 4; ++c2) {
+          int off[3] = {0, 0, 0};
+          off[d1] = (c2 & 1) - (c & 1);
+          off[d2] = ((c2 >> 1) & 1) - ((c >> 1) & 1);
+          A27[slot(off[0], off[1], off[2])] += M[c][c2];
+        }
+      }
+  }
 }
 
 void norms(const Level& L, const double* e, double* l2, double* linf) {
@@ -801,6 +882,75 @@ int orc_exp_true(const orc_level* fine, const double* uh, const double* u2h, dou
 }
 
 void orc_norms(const orc_level* h, const double* e, double* l2, double* linf) { norms(h->L, e, l2, linf); }
+
+// Sampled rows of a level without assembling it: for node k of `nodes` (ix, iy, iz triples),
+// q[k] = (A_ff p)_i (0 on Dirichlet rows; p a full nodal vector, free entries used) and b[k] = the lifted
+// right-hand side b_f,i = F_i - sum_{j Dirichlet} A_ij g_D(x_j) (0 on Dirichlet rows), with the
+// neighbour loops in apply_ff's / build_level's order; dg[k] = A_ii. p, q, b, dg may be NULL.
+int orc_rows(const double* lo, const double* hi, const int* n, int problem_id, const double* params, int nparams,
+             const int* face, const long long* nodes, long count, const double* p, double* q, double* b, double* dg) {
+  Problem P;
+  if (!make_problem(problem_id, params, nparams, face, &P)) return ORC_EINVAL;
+  double h[3];
+  long nn[3];
+  for (int d = 0; d < 3; ++d) {
+    if (n[d] < 1 || !(hi[d] > lo[d])) return ORC_EINVAL;
+    h[d] = (hi[d] - lo[d]) / n[d];
+    nn[d] = n[d] + 1;
+  }
+  auto idx = [&](long x, long y, long z) { return x + nn[0] * (y + nn[1] * z); };
+  auto coord = [&](int d, long i) { return lo[d] + i * h[d]; };
+  for (long k = 0; k < count; ++k) {
+    const long ix = nodes[3 * k], iy = nodes[3 * k + 1], iz = nodes[3 * k + 2];
+    if (ix < 0 || iy < 0 || iz < 0 || ix > n[0] || iy > n[1] || iz > n[2]) return ORC_EINVAL;
+    if (node_is_dirichlet(P, n, ix, iy, iz)) {
+      if (q) q[k] = 0.0;
+      if (b) b[k] = 0.0;
+      if (dg) dg[k] = 0.0;
+      continue;
+    }
+    double A27[27], F;
+    assemble_row(P, lo, h, n, ix, iy, iz, A27, &F);
+    if (dg) dg[k] = A27[slot(0, 0, 0)];   // the Jacobi diagonal A_ii
+    double sq = 0.0, sb = F;
+    for (int dz = -1; dz <= 1; ++dz)
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx) {
+          long jx = ix + dx, jy = iy + dy, jz = iz + dz;
+          if (jx < 0 || jy < 0 || jz < 0 || jx >= nn[0] || jy >= nn[1] || jz >= nn[2]) continue;
+          if (node_is_dirichlet(P, n, jx, jy, jz)) {
+            sb -= A27[slot(dx, dy, dz)] * P.gD(coord(0, jx), coord(1, jy), coord(2, jz));
+          } else if (p) {
+            sq += A27[slot(dx, dy, dz)] * p[idx(jx, jy, jz)];
+          }
+        }
+    if (q) q[k] = sq;
+    if (b) b[k] = sb;
+  }
+  return ORC_OK;
+}
+
+// EXP_finite / EXP_true at sampled fine nodes (with the Dirichlet overwrite by g_D), per-node bodies
+// of exp_finite / exp_finite_lagrange / exp_true
+int orc_exp_nodes(const double* lo, const double* hi, const int* n, int problem_id, const double* params, int nparams,
+                  const int* face, int which /* 0 Serendipity, 1 Lagrange, 2 EXP_true */, const double* a,
+                  const double* c, const long long* nodes, long count, double* out) {
+  Problem P;
+  if (!make_problem(problem_id, params, nparams, face, &P)) return ORC_EINVAL;
+  for (int d = 0; d < 3; ++d) if (n[d] % (which == 2 ? 2 : 4)) return ORC_EMISMATCH;
+  for (long k = 0; k < count; ++k) {
+    const long ix = nodes[3 * k], iy = nodes[3 * k + 1], iz = nodes[3 * k + 2];
+    if (ix < 0 || iy < 0 || iz < 0 || ix > n[0] || iy > n[1] || iz > n[2]) return ORC_EINVAL;
+    if (node_is_dirichlet(P, n, ix, iy, iz)) {
+      const double h0 = (hi[0] - lo[0]) / n[0], h1 = (hi[1] - lo[1]) / n[1], h2 = (hi[2] - lo[2]) / n[2];
+      out[k] = P.gD(lo[0] + ix * h0, lo[1] + iy * h1, lo[2] + iz * h2);
+      continue;
+    }
+    out[k] = which == 2 ? exp_true_node(n, a, c, ix, iy, iz)
+                        : (which == 1 ? exp_finite_lagrange_node(n, a, c, ix, iy, iz) : exp_finite_node(n, a, c, ix, iy, iz));
+  }
+  return ORC_OK;
+}
 
 void orc_element_stiffness(const double* h, double beta, double* K) {
   double Kl[8][8];
