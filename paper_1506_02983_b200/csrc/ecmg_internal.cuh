@@ -187,6 +187,11 @@ cudaError_t launch_jcg_elem(int mode, const LevelGeom& g, const ElemStencil& es,
 int jcg_num_blocks(const LevelGeom& g, int elem_path, int zc);
 }  // namespace ecmg
 #include <cuda.h>
+// L2 promotion of the TMA loads (tuning macro): none measured 0.7 % faster than 256 B on the C4 JCG
+// iteration (1.460 vs 1.471 ms at 512^3, tools/build_full_variants.sh + tools/tune_elem.py), equal on C3
+#ifndef ECMG_TMA_PROMO
+#define ECMG_TMA_PROMO CU_TENSOR_MAP_L2_PROMOTION_NONE
+#endif
 namespace ecmg {
 cudaError_t launch_jcg_const_tma(int mode, const LevelGeom& g, const ConstStencil& cs, const KArgs& a,
                                  const CUtensorMap* maps, cudaStream_t st);

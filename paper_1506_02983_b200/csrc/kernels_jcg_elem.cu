@@ -622,7 +622,7 @@ bool encode_map(CUtensorMap* out, const MapKey& k) {
   cuuint32_t estr[3] = {1, 1, 1};
   CUtensorMap m;
   if (encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(k.base), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, ECMG_TMA_PROMO,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return false;
   const int slot = used < kMapCache ? used++ : (next++ % kMapCache);
