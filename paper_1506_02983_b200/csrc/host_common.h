@@ -128,10 +128,12 @@ inline int auto_zc(int zchunk, int elem_path, const LevelGeom& g) {
       return (int)((nz + nchunks - 1) / nchunks);
     }
   }
-  if (!elem_path) {   // constant stencil, 32 x 32 tiles: about 4 CTAs per SM in total (tools/tune_jcg.py)
+  if (!elem_path) {   // constant stencil, 32 x 32 tiles: at least ~4 CTAs per SM in total and chunks of at
+    // most ~32 planes. Measured at 512^3 (TMA loads without L2 promotion, tools/tune_elem.py --zc): zc 171
+    // (3 chunks, 2.6 waves) 1.47 ms per iteration, zc 24-57 (8-22 waves) 1.36-1.41 ms
     const long long tiles = (long long)((g.nf[0] + 31) / 32) * ((g.nf[1] + 31) / 32);
     const long long target = (long long)device_sm_count() * 2 * 2;
-    long long nchunks = (target + tiles - 1) / tiles;
+    long long nchunks = std::max((target + tiles - 1) / tiles, (long long)(nz + 31) / 32);
     nchunks = std::max(1LL, std::min(nchunks, (long long)std::max(1, nz / 4)));
     return (int)((nz + nchunks - 1) / nchunks);
   }
