@@ -54,6 +54,7 @@ struct ecmg_grid {
   int setup_ctas = 0;              // ECMG_OPT_SETUP_CTAS: CTAs per SM of the ALU-bound RHS kernel when run ahead
   cudaStream_t hi_stream = nullptr, lo_stream = nullptr;   // ecmg_run: solves (high) / level setup (low priority)
   cudaStream_t lo2_stream = nullptr;                        // the finest level's setup (starts at once, beside lo_stream)
+  cudaStream_t hi2_stream = nullptr;                        // mode 4: the finest level's setup at the solves' priority
   int setup_ahead_prio = 1;   // the coarse levels' setups at the solves' priority (they are short and needed soon)
   std::vector<cudaEvent_t> setup_ev;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
@@ -630,6 +631,7 @@ int ecmg_create_grid(const ecmg_box* dom, const int coarsest_cells[3], int num_l
     if (cudaStreamCreateWithPriority(&G->hi_stream, cudaStreamNonBlocking, hi) != cudaSuccess ||
         cudaStreamCreateWithPriority(&G->lo_stream, cudaStreamNonBlocking, G->setup_ahead_prio ? hi : lo) != cudaSuccess ||
         cudaStreamCreateWithPriority(&G->lo2_stream, cudaStreamNonBlocking, lo) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&G->hi2_stream, cudaStreamNonBlocking, hi) != cudaSuccess ||
         cudaEventCreateWithFlags(&G->fork_ev, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&G->join_ev, cudaEventDisableTiming) != cudaSuccess)
       st = ECMG_ECUDA;
@@ -692,6 +694,7 @@ int ecmg_destroy_grid(ecmg_grid* G) {
   if (G->hi_stream) cudaStreamDestroy(G->hi_stream);
   if (G->lo_stream) cudaStreamDestroy(G->lo_stream);
   if (G->lo2_stream) cudaStreamDestroy(G->lo2_stream);
+  if (G->hi2_stream) cudaStreamDestroy(G->hi2_stream);
   cudaFree(G->seeds);
   if (G->sc_host) cudaFreeHost(G->sc_host);
   if (G->param_host) cudaFreeHost(G->param_host);
@@ -757,7 +760,7 @@ int ecmg_set_option(ecmg_grid* G, int option, int value) {
   switch (option) {
     case ECMG_OPT_EXP_VARIANT: if (value != 0 && value != 1) return ECMG_EINVAL; G->exp_variant = value; break;
     case ECMG_OPT_PRECOND: if (value != 0 && value != 1) return ECMG_EINVAL; G->precond = value; invalidate_setup(G); clear_graphs(G); break;
-    case ECMG_OPT_SETUP_AHEAD: if (value < 0 || value > 3) return ECMG_EINVAL; G->setup_ahead = value; break;
+    case ECMG_OPT_SETUP_AHEAD: if (value < 0 || value > 4) return ECMG_EINVAL; G->setup_ahead = value; break;
     case ECMG_OPT_BETA_FLY: if (value != 0 && value != 1) return ECMG_EINVAL; G->beta_fly = value; clear_graphs(G); break;
     case ECMG_OPT_EXP_KERNEL: if (value != 0 && value != 1) return ECMG_EINVAL; G->exp_fused = value; break;
     case ECMG_OPT_SETUP_CTAS: if (value < 0) return ECMG_EINVAL; G->setup_ctas = value; break;
@@ -935,10 +938,12 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
     ECMG_CUDA(cudaStreamWaitEvent(G->hi_stream, G->fork_ev, 0));
     ECMG_CUDA(cudaStreamWaitEvent(G->lo_stream, G->fork_ev, 0));
     ECMG_CUDA(cudaStreamWaitEvent(G->lo2_stream, G->fork_ev, 0));
+    ECMG_CUDA(cudaStreamWaitEvent(G->hi2_stream, G->fork_ev, 0));
     // the finest level's setup (most of the work) on its own stream, so that it starts at once; the
     // coarser levels' setups in level order beside it
     for (int k = 0; k < L_run; ++k) {
-      cudaStream_t s_k = (k == L_run - 1 && G->setup_ahead != 2) ? G->lo2_stream : G->lo_stream;
+      cudaStream_t s_k = (k == L_run - 1 && G->setup_ahead != 2) ? (G->setup_ahead == 4 ? G->hi2_stream : G->lo2_stream)
+                                                                 : G->lo_stream;
       { int s = setup_level_on(G, k, s_k, G->setup_ctas); if (s) return s; }
       ECMG_CUDA(launch_dirichlet_fill(G->geom[k], G->prob, level_u(k), 0.0, 0, s_k));
       ECMG_CUDA(cudaEventRecord(G->setup_ev[k], s_k));
