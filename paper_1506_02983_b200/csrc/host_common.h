@@ -128,11 +128,11 @@ inline int auto_zc(int zchunk, int elem_path, const LevelGeom& g) {
       return (int)((nz + nchunks - 1) / nchunks);
     }
   }
-  if (!elem_path) {   // constant stencil, 32 x 32 tiles: at least ~4 CTAs per SM in total and chunks of at
-    // most ~32 planes. Measured at 512^3 (TMA loads without L2 promotion, tools/tune_elem.py --zc): zc 171
-    // (3 chunks, 2.6 waves) 1.47 ms per iteration, zc 24-57 (8-22 waves) 1.36-1.41 ms
+  if (!elem_path) {   // constant stencil, 32 x 32 tiles: chunks of at most ~32 planes and at least 1.5 waves.
+    // Measured (TMA loads without L2 promotion, tools/tune_elem.py --zc): 512^3 zc 171 (3 chunks, 2.6 waves)
+    // 1.47 ms per iteration, zc 24-57 (8-22 waves) 1.36-1.41 ms; 256^3 zc 26 0.205 ms, zc 16-32 0.199 ms
     const long long tiles = (long long)((g.nf[0] + 31) / 32) * ((g.nf[1] + 31) / 32);
-    const long long target = (long long)device_sm_count() * 2 * 2;
+    const long long target = (long long)(device_sm_count() * 2 * 1.5);   // >= 1.5 waves
     long long nchunks = std::max((target + tiles - 1) / tiles, (long long)(nz + 31) / 32);
     nchunks = std::max(1LL, std::min(nchunks, (long long)std::max(1, nz / 4)));
     return (int)((nz + nchunks - 1) / nchunks);
@@ -141,10 +141,12 @@ inline int auto_zc(int zchunk, int elem_path, const LevelGeom& g) {
   //   (fill of the last wave) x min(1, waves / 1.5) x zc / (zc + 2)
   // (a partial last wave idles SMs; fewer than ~1.5 waves cannot saturate HBM; every chunk re-reads
   // two halo planes). Measured on C3 256^3: the sweep is flat at the optimum and 10 % worse at 2.2 waves.
+  // Chunks are capped at 64 planes: at 1024^3 (C5) the score above picks whole-z chunks (2048 CTAs,
+  // zc 1023: 18.2 ms per iteration) while zc 32-64 measured 17.2-17.3 ms (tools/tune_elem.py --zc).
   const double tiles = (double)((g.nf[0] + 31) / 32) * ((g.nf[1] + 15) / 16);
   int best_zc = std::max(1, nz);
   double best = -1.0;
-  for (int k = 1; k <= std::max(1, nz / 16); ++k) {
+  for (int k = std::max(1, (nz + 63) / 64); k <= std::max(1, nz / 16); ++k) {
     const int zc = (nz + k - 1) / k;
     const int kk = (nz + zc - 1) / zc;
     const double waves = tiles * kk / slots;

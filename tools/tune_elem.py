@@ -15,8 +15,9 @@ def one(path, cfg, zcs=(0,)):
     import synth
     from paper_1506_02983_b200 import Grid, PROB, ecmg
     ecmg.LIB_PATH = os.path.abspath(path)
-    pid, n0, levels = {"c3": (PROB["C3"], 4, 7), "c4": (PROB["C4"], 4, 8)}[cfg]
-    g = Grid(n0, levels, pid)
+    pid, n0, levels = {"c3": (PROB["C3"], 4, 7), "c4": (PROB["C4"], 4, 8), "c4_256": (PROB["C4"], 4, 7),
+                       "c5": (PROB["C5"], 4, 9), "c3_128": (PROB["C3"], 4, 6)}[cfg]
+    g = Grid(n0, levels, pid, synth.c5_geometry(0) if cfg == "c5" else None)
     k = levels - 1
     shape, nodes = g.shape(k)
     x0 = torch.from_numpy(synth.random_nodal(14, shape, (1, 1, 1), tuple(v - 1 for v in shape))).cuda()
@@ -30,7 +31,7 @@ def one(path, cfg, zcs=(0,)):
             g.solve_level(k, 0.0, 40, xb)
             ms, it, nf = g.last_jcg_timing()
             best = min(best, ms / it)
-        bpu = 88 if cfg == "c3" else 64
+        bpu = 88 if cfg in ("c3", "c5", "c3_128") else 64
         print(json.dumps(dict(lib=os.path.basename(path), cfg=cfg, zc=zc, ms_per_iter=round(best, 5),
                               frac=round(bpu * nf / (best / 1e3) / 1e9 / 6538.9, 4))), flush=True)
 
