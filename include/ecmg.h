@@ -106,8 +106,10 @@ typedef enum {
                                 device-set conditional WHILE node; 0 host loop with batched readbacks */
   ECMG_OPT_PERSISTENT = 7,   /* levels with at most this many free unknowns (and at most 4 bricks of
                                 8x8x4 nodes per resident CTA) run the whole JCG solve in one cooperative
-                                launch, both operators (default 300000, i.e. up to 64^3 cells; 0 = off;
-                                single GPU only) */
+                                launch with the nodes' values in registers, both operators (default
+                                40000, i.e. up to 32^3 cells; 0 = off; larger levels up to
+                                ECMG_OPT_PERS_TMA take the cooperative TMA solve: measured 64^3 0.82 ->
+                                0.67 ms on C4) */
   ECMG_OPT_PDL = 8,          /* 1: the JCG kernels use programmatic dependent launch (the next kernel's
                                 launch overlaps the previous one's tail); 0 (default): plain launches
                                 (measured on B200: no difference inside the per-level CUDA graphs) */
@@ -128,8 +130,8 @@ typedef enum {
   ECMG_OPT_CTA_SOLVE = 13,   /* levels with at most this many free unknowns (default 1000, at most 4096)
                                 are solved by ONE CTA with every vector in shared memory (no grid barrier);
                                 0: off (the cooperative persistent kernel takes them) */
-  ECMG_OPT_PERS_TMA = 14,    /* constant-stencil levels with at most this many free unknowns (default
-                                3000000, i.e. up to 128^3) and more than ECMG_OPT_PERSISTENT run the whole
+  ECMG_OPT_PERS_TMA = 14,    /* levels with at most this many free unknowns (default 3000000, i.e. up to
+                                128^3; both operators) and more than ECMG_OPT_PERSISTENT run the whole
                                 tolerance-stopped solve as ONE cooperative launch of TMA z-marching passes
                                 (no per-iteration kernel launches); 0: the CUDA-graph loop of K1 / K2 */
   ECMG_OPT_BETA_FLY = 15,    /* element-beta path, cubic cells, analytic beta (C3, C5, layers, beta = 1 with

@@ -76,7 +76,8 @@ struct ecmg_grid {
                             // inside the CUDA graphs, tools/tune_pdl.py; off by default)
   long long cta_max = 1000;           // ECMG_OPT_CTA_SOLVE: one-CTA solve up to this many free unknowns (0: off)
   long long pers_tma_max = 3000000;   // ECMG_OPT_PERS_TMA: constant stencil, one cooperative TMA solve up to this size
-  long long persistent_max = 300000;  // ECMG_OPT_PERSISTENT: one cooperative launch per solve up to this size (tools/tune_persistent.py)
+  long long persistent_max = 40000;   // ECMG_OPT_PERSISTENT: register-resident cooperative solve up to this size (tools/tune_persistent.py:
+                                      // 64^3 is faster as the cooperative TMA solve, 0.67 vs 0.82 ms on C4)
   double* aux[2] = {nullptr, nullptr};   // persistent element-path solve: w = A p and D^-1 (level-sized)
   long long aux_doubles = 0;
   cudaStream_t cap_stream = nullptr;          // private stream used only for graph capture
