@@ -397,6 +397,7 @@ __global__ void __launch_bounds__(256) k_exp_true(const LevelGeom gf, const Prob
                                                   int cchunk, double third) {
   __shared__ double D[EDY][EDX];     // corner differences of the current 2h plane
   __shared__ double XI[EDY][ETX];    // ... interpolated along x to the tile's 64 fine columns
+  __shared__ double UB[3][2][ETY][ETX];   // u_h of fine planes 2K-1, 2K: cp.async ring, two steps ahead
   const int lane = threadIdx.x, w = threadIdx.y, tid = lane + 32 * w;
   const int n2x = gf.n[0] / 2, n2y = gf.n[1] / 2, n2z = gf.n[2] / 2;
   const int X0 = blockIdx.x * ETX, Y0 = blockIdx.y * ETY;
@@ -437,10 +438,26 @@ __global__ void __launch_bounds__(256) k_exp_true(const LevelGeom gf, const Prob
   };
   const bool okA = row_ok && fxa <= gf.n[0], okB = row_ok && fxb <= gf.n[0];
   const long long rowoff = (long long)fy * nx;
-  auto load_u = [&](int fz, double& a, double& b) {
-    const long long row = (long long)fz * pl + rowoff;
-    a = okA ? __ldg(uh + row + fxa) : 0.0;
-    b = okB ? __ldg(uh + row + fxb) : 0.0;
+  // u_h rows of the thread's two nodes go to shared memory with cp.async (8-byte, cached), two steps
+  // ahead, one commit group per step: the loads are in flight without holding registers
+  auto cp8 = [&](double* dst, const double* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+                 : "memory");
+  };
+  auto issue_u = [&](int K) {   // fine planes 2K-1 (if K > Ca) and 2K (if even_of(K)) into slot (K - Ca) % 3
+    double* u0 = &UB[(K - Ca) % 3][0][w][0];
+    double* u1 = &UB[(K - Ca) % 3][1][w][0];
+    if (K > Ca) {
+      const double* row = uh + (long long)(2 * K - 1) * pl + rowoff;
+      if (okA) cp8(u0 + lane, row + fxa);
+      if (okB) cp8(u0 + 32 + lane, row + fxb);
+    }
+    if (K < Cb || K == n2z) {
+      const double* row = uh + (long long)(2 * K) * pl + rowoff;
+      if (okA) cp8(u1 + lane, row + fxa);
+      if (okB) cp8(u1 + 32 + lane, row + fxb);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   };
   // free (x, y) flags of the thread's two nodes; the plane decides the rest
   const bool yf = fy >= gf.flo[1] && fy < gf.flo[1] + gf.nf[1];
@@ -454,14 +471,18 @@ __global__ void __launch_bounds__(256) k_exp_true(const LevelGeom gf, const Prob
   };
   double dh, d2, pa = 0.0, pb_ = 0.0;   // pa, pb_: plane K-1's interpolated d at the thread's nodes
   load_d(Ca, dh, d2);
+  issue_u(Ca);
+  if (Ca + 1 <= Cb) issue_u(Ca + 1); else asm volatile("cp.async.commit_group;" ::: "memory");
   for (int K = Ca; K <= Cb; ++K) {
     __syncthreads();   // D / XI of plane K-1 consumed
     if (dthr) D[dj][di] = dh - d2;   // corner differences of 2h plane K
     if (K < Cb) load_d(K + 1, dh, d2);
-    double uoa = 0.0, uob = 0.0, uea = 0.0, ueb = 0.0;
+    if (K + 2 <= Cb) issue_u(K + 2); else asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 2;" ::: "memory");   // this step's group (own slots only: no barrier)
+    const int sl = (K - Ca) % 3;
+    const double uoa = UB[sl][0][w][lane], uob = UB[sl][0][w][lane + 32];
+    const double uea = UB[sl][1][w][lane], ueb = UB[sl][1][w][lane + 32];
     const bool odd = K > Ca, even = K < Cb || K == n2z;
-    if (odd) load_u(2 * K - 1, uoa, uob);
-    if (even) load_u(2 * K, uea, ueb);
     __syncthreads();
     xpass();
     __syncthreads();
