@@ -395,8 +395,8 @@ constexpr int ETX = 64, ETY = 8, EDX = ETX / 2 + 1, EDY = ETY / 2 + 1;   // 33 x
 __global__ void __launch_bounds__(256) k_exp_true(const LevelGeom gf, const Problem pb, const double* __restrict__ uh,
                                                   const double* __restrict__ u2h, double* __restrict__ ut, int c0,
                                                   int cchunk, double third) {
-  __shared__ double D[EDY][EDX];     // corner differences of the current 2h plane
-  __shared__ double XI[EDY][ETX];    // ... interpolated along x to the tile's 64 fine columns
+  __shared__ double D[2][EDY][EDX];     // corner differences of 2h plane K (slot K & 1)
+  __shared__ double XI[2][EDY][ETX];    // ... interpolated along x to the tile's 64 fine columns
   __shared__ double UB[3][2][ETY][ETX];   // u_h of fine planes 2K-1, 2K: cp.async ring, two steps ahead
   const int lane = threadIdx.x, w = threadIdx.y, tid = lane + 32 * w;
   const int n2x = gf.n[0] / 2, n2y = gf.n[1] / 2, n2z = gf.n[2] / 2;
@@ -422,19 +422,19 @@ __global__ void __launch_bounds__(256) k_exp_true(const LevelGeom gf, const Prob
     }
   };
   // x pass: thread t < 320 (and t + 256 < 320) produces XI[r][c] = w0 D[r][c/2] + w1 D[r][c/2 + 1]
-  auto xpass = [&]() {
+  auto xpass = [&](int sl) {
     for (int t = tid; t < EDY * ETX; t += 256) {
       const int r = t / ETX, c = t % ETX, i = c >> 1;
       const double w1 = (c & 1) ? 0.5 : 0.0, w0 = 1.0 - w1;
-      XI[r][c] = w0 * D[r][i] + w1 * D[r][i + 1];
+      XI[sl][r][c] = w0 * D[sl][r][i] + w1 * D[sl][r][i + 1];
     }
   };
   // y pass of this thread's two nodes (row w between 2h rows w/2 and w/2 + 1)
   const int jr = w >> 1;
   const double wy1 = (w & 1) ? 0.5 : 0.0, wy0 = 1.0 - wy1;
-  auto ypass = [&](double& va, double& vb) {
-    va = wy0 * XI[jr][lane] + wy1 * XI[jr + 1][lane];
-    vb = wy0 * XI[jr][lane + 32] + wy1 * XI[jr + 1][lane + 32];
+  auto ypass = [&](int sl, double& va, double& vb) {
+    va = wy0 * XI[sl][jr][lane] + wy1 * XI[sl][jr + 1][lane];
+    vb = wy0 * XI[sl][jr][lane + 32] + wy1 * XI[sl][jr + 1][lane + 32];
   };
   const bool okA = row_ok && fxa <= gf.n[0], okB = row_ok && fxb <= gf.n[0];
   const long long rowoff = (long long)fy * nx;
@@ -473,9 +473,11 @@ __global__ void __launch_bounds__(256) k_exp_true(const LevelGeom gf, const Prob
   load_d(Ca, dh, d2);
   issue_u(Ca);
   if (Ca + 1 <= Cb) issue_u(Ca + 1); else asm volatile("cp.async.commit_group;" ::: "memory");
+  // D and XI are double buffered by plane parity: two barriers per step (D written -> x pass -> y pass);
+  // slot K & 1 was last read in step K - 2, which every thread finished before step K - 1's barriers
   for (int K = Ca; K <= Cb; ++K) {
-    __syncthreads();   // D / XI of plane K-1 consumed
-    if (dthr) D[dj][di] = dh - d2;   // corner differences of 2h plane K
+    const int pk = K & 1;
+    if (dthr) D[pk][dj][di] = dh - d2;   // corner differences of 2h plane K
     if (K < Cb) load_d(K + 1, dh, d2);
     if (K + 2 <= Cb) issue_u(K + 2); else asm volatile("cp.async.commit_group;" ::: "memory");
     asm volatile("cp.async.wait_group 2;" ::: "memory");   // this step's group (own slots only: no barrier)
@@ -484,10 +486,10 @@ __global__ void __launch_bounds__(256) k_exp_true(const LevelGeom gf, const Prob
     const double uea = UB[sl][1][w][lane], ueb = UB[sl][1][w][lane + 32];
     const bool odd = K > Ca, even = K < Cb || K == n2z;
     __syncthreads();
-    xpass();
+    xpass(pk);
     __syncthreads();
     double ca, cb;
-    ypass(ca, cb);
+    ypass(pk, ca, cb);
     if (odd) put(2 * K - 1, uoa, uob, 0.5 * (pa + ca), 0.5 * (pb_ + cb));   // odd fine plane between K-1 and K
     if (even) put(2 * K, uea, ueb, ca, cb);                                // even fine plane 2K
     pa = ca;
