@@ -257,6 +257,16 @@ def main():
     ms_p, it_p, _ = grid.last_jcg_timing()
     ms_p = max_over_ranks(ms_p)
     grid.set_option(ecmg.OPT_KERNEL, 1)
+    ablation_unfused = None
+    if pid not in (3, 5):   # ablation: the unfused textbook PCG sequence (nine passes, 144 B/unknown)
+        grid.set_option(ecmg.OPT_UNFUSED, 1)
+        xb.copy_(x0)
+        grid.solve_level(fine, 0.0, 20, xb)
+        ms_u, it_u, _ = grid.last_jcg_timing()
+        ms_u = max_over_ranks(ms_u)
+        grid.set_option(ecmg.OPT_UNFUSED, 0)
+        ablation_unfused = {"value": nf_j * it_u / (ms_u / 1e3), "unit": UNIT, "ms_per_iteration": ms_u / max(1, it_u),
+                            "kernel": "unfused textbook PCG (ECMG_OPT_UNFUSED=1): 9 passes, 144 B/unknown"}
     ablation_beta = None
     if pid in (3, 5):   # ablation: the element kernels form beta on the fly instead of reading the array
         grid.set_option(ecmg.OPT_BETA_FLY, 1)
@@ -349,6 +359,7 @@ def main():
                                             "ms_per_iteration": ms_p / max(1, it_p),
                                             "kernel": "register-prefetch loads (ECMG_OPT_KERNEL=0)"},
             "jcg_fixed_ablation_beta_fly": ablation_beta,
+            "jcg_fixed_ablation_unfused": ablation_unfused,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "kernel": "jcg K1+K2 (one CG iteration)",
                          "bytes_per_unit": bpu, "peak_source": peak_src,

@@ -144,6 +144,10 @@ typedef enum {
                                 run through the single-GPU path (one-CTA / persistent / CUDA-graph solves,
                                 setup ahead) on every rank, then the slab driver takes over; 0: the slab
                                 driver's host-driven loop for every level (ablation) */
+  ECMG_OPT_UNFUSED = 17,     /* ablation: 1 = fixed-count (eps <= 0) constant-stencil solves run the unfused
+                                textbook PCG sequence -- w = A p, p.w, two axpys, z = D^-1 r, r.z, r.r and the
+                                p update as separate passes (144 B per unknown and iteration instead of the
+                                fused 64 B); 0 (default): the fused K1 / K2 kernels */
   ECMG_OPT_SETUP_CTAS = 11,  /* tuning: CTAs per SM of the fp64-ALU-bound volume-load kernel when it runs
                                 ahead (0 = one CTA per work item, the full grid) */
   ECMG_OPT_VIRTUAL_SLABS = 6 /* P in 2..16: run the z-slab decomposition with P slabs on this one GPU

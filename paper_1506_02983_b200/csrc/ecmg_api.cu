@@ -70,6 +70,7 @@ struct ecmg_grid {
   bool ev_init = false;
   int kernel_variant = 1;   // ECMG_OPT_KERNEL
   int use_graph = 1;        // ECMG_OPT_GRAPH: device-driven JCG loop (CUDA graph, conditional WHILE node)
+  int unfused = 0;          // ECMG_OPT_UNFUSED: fixed-count constant-stencil solves by the textbook sequence
   int hybrid = 1;           // ECMG_OPT_SLAB_HYBRID: z-slabs, replicated levels through the single-GPU path
   int fused_halo = 1;       // ECMG_OPT_FUSED_HALO: z-slab halo planes stored by K2 / init into the neighbours
   int pdl = 0;              // ECMG_OPT_PDL: programmatic dependent launch between the JCG kernels (measured: no gain
@@ -474,7 +475,39 @@ int run_jcg(ecmg_grid* G, int k, double eps, int max_iter, double* u_out, ecmg_s
     return e;
   };
   ECMG_CUDA(cudaEventRecord(G->ev[0], G->stream));
-  if (eps <= 0.0) {
+  if (eps <= 0.0 && G->unfused && !G->elem_path) {
+    // ablation: the unfused textbook sequence (kernels_textbook.cu), nine passes per iteration
+    const long long need = g.S * g.nza + 64;
+    if (G->aux_doubles < need) {
+      cudaFree(G->aux[0]); cudaFree(G->aux[1]);
+      G->aux[0] = G->aux[1] = nullptr;
+      G->aux_doubles = 0;
+      ECMG_CUDA(cudaMalloc(&G->aux[0], sizeof(double) * need));
+      ECMG_CUDA(cudaMalloc(&G->aux[1], sizeof(double) * need));
+      G->aux_doubles = need;
+    }
+    double* z = G->aux[0];
+    double* p = G->p[0];
+    double* w = G->p[1];
+    const double dinv = make_const_stencil(g, 1.0, G->precond).dinv;
+    ECMG_CUDA(launch_textbook(3, g, z, G->r, nullptr, G->sc, dinv, G->stream));   // z0 = D^-1 r0
+    ECMG_CUDA(launch_textbook(4, g, p, z, nullptr, G->sc, 1.0, G->stream));       // p0 = z0
+    for (int i = 0; i < max_iter; ++i) {
+      if (i > 0) ECMG_CUDA(launch_textbook(4, g, p, z, nullptr, G->sc, 0.0, G->stream));   // p = z + beta p
+      KArgs aa = a;
+      aa.h0 = p; aa.o0 = w;
+      ECMG_CUDA(launch_mode(G, MODE_APPLY, g, aa));                                           // w = A p
+      ECMG_CUDA(launch_textbook(0, g, p, w, G->partials, G->sc, 0.0, G->stream));             // p.w
+      ECMG_CUDA(launch_textbook(1, g, nullptr, nullptr, G->partials, G->sc, 0.0, G->stream)); // alpha
+      ECMG_CUDA(launch_textbook(2, g, G->x, p, nullptr, G->sc, 1.0, G->stream));              // x += alpha p
+      ECMG_CUDA(launch_textbook(2, g, G->r, w, nullptr, G->sc, -1.0, G->stream));             // r -= alpha w
+      ECMG_CUDA(launch_textbook(3, g, z, G->r, nullptr, G->sc, dinv, G->stream));             // z = D^-1 r
+      ECMG_CUDA(launch_textbook(0, g, G->r, z, G->partials, G->sc, 0.0, G->stream));          // r.z
+      ECMG_CUDA(launch_textbook(1, g, nullptr, nullptr, G->partials, G->sc, 1.0, G->stream)); // beta, rho
+      ECMG_CUDA(launch_textbook(0, g, G->r, G->r, G->partials, G->sc, 0.0, G->stream));       // r.r
+      ECMG_CUDA(launch_textbook(1, g, nullptr, nullptr, G->partials, G->sc, 2.0, G->stream)); // rr, iter
+    }
+  } else if (eps <= 0.0) {
     for (int i = 0; i < max_iter; ++i) ECMG_CUDA(launch_iter());
   } else {
     const long long nfree = free_count(g);
@@ -770,6 +803,7 @@ int ecmg_set_option(ecmg_grid* G, int option, int value) {
     case ECMG_OPT_GRAPH: if (value != 0 && value != 1) return ECMG_EINVAL; G->use_graph = value; break;
     case ECMG_OPT_PERSISTENT: if (value < 0) return ECMG_EINVAL; G->persistent_max = value; break;
     case ECMG_OPT_PERS_TMA: if (value < 0) return ECMG_EINVAL; G->pers_tma_max = value; break;
+    case ECMG_OPT_UNFUSED: if (value != 0 && value != 1) return ECMG_EINVAL; G->unfused = value; break;
     case ECMG_OPT_SLAB_HYBRID: if (value != 0 && value != 1) return ECMG_EINVAL; G->hybrid = value; break;
     case ECMG_OPT_CTA_SOLVE: if (value < 0) return ECMG_EINVAL; G->cta_max = value; break;
     case ECMG_OPT_PDL: if (value != 0 && value != 1) return ECMG_EINVAL; G->pdl = value; clear_graphs(G); break;

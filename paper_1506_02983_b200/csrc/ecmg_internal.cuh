@@ -197,6 +197,11 @@ cudaError_t launch_jcg_const_tma(int mode, const LevelGeom& g, const ConstStenci
                                  const CUtensorMap* maps, cudaStream_t st);
 int make_vec_tensor_map(CUtensorMap* map, const double* base, const LevelGeom& g, int bx, int by);
 cudaError_t init_pers_kernel_attributes();
+// the unfused textbook PCG sequence (ablation, kernels_textbook.cu): step 0 dot(y, x) -> partials,
+// 1 finish(arg = op), 2 y += arg * alpha x, 3 y = arg * x, 4 y(p) = x(z) + beta p (arg = first)
+long long textbook_partials(const LevelGeom& g);
+cudaError_t launch_textbook(int step, const LevelGeom& g, double* y, const double* x, double* partials, JcgScalars* sc,
+                            double arg, cudaStream_t st);
 cudaError_t init_elem_pers_attributes();
 cudaError_t launch_jcg_elem_pers(const LevelGeom& g, const ElemStencil& es, double* x, double* r, double* z, double* p0,
                                  double* p1, const double* b, const double* beta, double* partials, JcgScalars* sc,

@@ -29,6 +29,7 @@ OPT_CTA_SOLVE = 13
 OPT_PERS_TMA = 14
 OPT_BETA_FLY = 15
 OPT_SLAB_HYBRID = 16
+OPT_UNFUSED = 17
 
 EXPORTS = ["ecmg_create_grid", "ecmg_set_coeffs", "ecmg_set_option", "ecmg_solve_level",
            "ecmg_prolongate_extrapolate", "ecmg_richardson", "ecmg_run", "ecmg_run_fixed", "ecmg_apply_operator",

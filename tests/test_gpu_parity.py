@@ -438,3 +438,26 @@ def test_beta_on_the_fly_bitwise(pid, eps):
     assert res[0][0] == res[1][0]
     for k in (1, 2, 3):
         assert np.array_equal(res[0][k], res[1][k])
+
+
+@pytest.mark.parametrize("pid,level", [(o.C2, 4), (o.C4, 5), (o.C1, 3)])
+def test_unfused_textbook_equals_fused(pid, level):
+    # ECMG_OPT_UNFUSED (the ablation of the fused K1 / K2 kernels): the textbook PCG sequence as separate
+    # passes gives the same iterates up to the summation order of the dot products
+    n = (4 << level,) * 3
+    L = o.Level(n, pid)
+    m, _ = L.dirichlet()
+    x0 = np.where(~m, synth.random_nodal(14, n), 0.0)
+    res = []
+    for unf in (0, 1):
+        g = Grid(4, level + 1, pid)
+        g.set_option(ecmg.OPT_UNFUSED, unf)
+        x = dev(x0)
+        st, s = g.solve_level(level, 0.0, 10, x)
+        assert st == 0 and s["iterations"] == 10
+        res.append((host(x), s["rel_res_recur"], s["rel_res_true"]))
+    assert rel(res[1][0], res[0][0]) <= 1e-12
+    assert abs(res[1][1] - res[0][1]) <= 1e-9 * res[0][1]
+    xo, _ = L.jcg(x0, 0.0, 10)
+    fr = ~m
+    assert rel(res[1][0][fr], xo[fr]) <= 1e-12

@@ -2,6 +2,7 @@
 # captures + launch lists (tools/gpu_profiles.sh), setup / EXP kernel captures at 512^3, and the ncu
 # launch list of the bench command itself
 mkdir -p gpurun_out
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo exit=$? >> gpurun_out/smoke.log
 timeout 1800 python -m pytest tests -m gpu -q --timeout 600 > gpurun_out/gpu_tests.log 2>&1; echo tests_exit=$? >> gpurun_out/gpu_tests.log
 timeout 900 python bench.py > gpurun_out/bench_default.log 2>&1; echo exit=$? >> gpurun_out/bench_default.log
 timeout 900 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_reference.log 2>&1; echo exit=$? >> gpurun_out/bench_reference.log

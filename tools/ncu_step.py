@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--host-loop", action="store_true",
                     help="JCG loop driven from the host (same kernels): ncu does not list launches inside the "
                          "CUDA graph's conditional WHILE body")
+    ap.add_argument("--unfused", action="store_true",
+                    help="the fixed iterations run the unfused textbook PCG sequence (ECMG_OPT_UNFUSED ablation)")
     a = ap.parse_args()
     pid, n0, levels, eps = {"c4": (PROB["C4"], 4, 8, 1e-9), "c3": (PROB["C3"], 4, 7, 1e-10),
                             "c2": (PROB["C2"], 4, 6, 1e-10)}[a.config]
@@ -37,6 +39,9 @@ def main():
     ut = torch.empty_like(u)
     g.run(eps, u, ut)
     x0 = torch.from_numpy(synth.random_nodal(14, shape, (1, 1, 1), tuple(v - 1 for v in shape))).cuda()
+    if a.unfused:
+        from paper_1506_02983_b200 import ecmg as _e
+        g.set_option(_e.OPT_UNFUSED, 1)
     g.solve_level(levels - 1, 0.0, 2, x0.clone())
     torch.cuda.synchronize()
     torch.cuda.profiler.start()
