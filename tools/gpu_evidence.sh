@@ -12,3 +12,6 @@ timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_ex
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_rhs_c4 -c 1 -o gpurun_out/rhs_c4 python tools/exp_timing.py 8 rhs > gpurun_out/ncu_rhs.log 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_exp_true -c 1 -o gpurun_out/exp_true python tools/exp_timing.py 8 rich > gpurun_out/ncu_rich.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_lbench.log 2>&1
+# the fusion ablation: per-launch time and DRAM bytes of 3 fused and 3 unfused (textbook) 512^3 iterations
+timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_c4_fused3.csv python tools/ncu_step.py --config c4 --skip-run --iters 3 > gpurun_out/ncu_lf.log 2>&1
+timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_c4_unfused3.csv python tools/ncu_step.py --config c4 --skip-run --iters 3 --unfused > gpurun_out/ncu_lu.log 2>&1
