@@ -344,7 +344,7 @@ def main():
             "data": f"synthetic (analytic {args.config.upper()} problem; no dataset)",
             "config": {"workload": desc, "levels": levels, "finest_cells": list(shape), "eps": eps,
                        "free_unknowns_finest": int(nf_j),
-                       "parallelism": f"z-slabs over {ws} NCCL ranks (levels with n % 4P == 0 and n/P >= 16 sharded)"
+                       "parallelism": f"z-slabs over {ws} NCCL ranks (levels with n >= 256, n % 4P == 0 and n/P >= 16 sharded; smaller levels replicated)"
                        if ws > 1 else "single GPU",
                        "l2": "inputs larger than L2 (no flush)",
                        "iterations_per_level": [s["iterations"] for s in per_level]},

@@ -148,6 +148,11 @@ typedef enum {
                                 textbook PCG sequence -- w = A p, p.w, two axpys, z = D^-1 r, r.z, r.r and the
                                 p update as separate passes (144 B per unknown and iteration instead of the
                                 fused 64 B); 0 (default): the fused K1 / K2 kernels */
+  ECMG_OPT_SHARD_MIN = 18,   /* z-slabs: a level is split across the ranks only if its z extent n satisfies
+                                n % 4P == 0, n / P >= 16 (ecmg_slab_partition) and n >= this value (default
+                                256); smaller levels are solved replicated on every rank. A split level pays
+                                two allreduces and two finalize launches per iteration (~35-50 us), more
+                                than a whole 128^3 iteration on one GPU (~29 us) */
   ECMG_OPT_SETUP_CTAS = 11,  /* tuning: CTAs per SM of the fp64-ALU-bound volume-load kernel when it runs
                                 ahead (0 = one CTA per work item, the full grid) */
   ECMG_OPT_VIRTUAL_SLABS = 6 /* P in 2..16: run the z-slab decomposition with P slabs on this one GPU
@@ -219,9 +224,10 @@ int ecmg_level_rhs(ecmg_grid* grid, int level, double* b, double* norm_b);
 int ecmg_level_shape(const ecmg_grid* grid, int level, int n_cells3[3], long long* nodes, int* z_lo, int* z_hi);
 
 /* z-slab partition, a pure host function usable without a GPU: a level with
- * n_cells_z cells is sharded over nranks iff n % (4 nranks) == 0 and n / nranks >= 16; then rank r
+ * n_cells_z cells can be sharded over nranks iff n % (4 nranks) == 0 and n / nranks >= 16; then rank r
  * owns node planes [r n/P, (r+1) n/P) (the last rank also plane n). Returns 1 (sharded, range
- * filled), 0 (replicated: [0, n+1)), or ECMG_EINVAL. */
+ * filled), 0 (replicated: [0, n+1)), or ECMG_EINVAL. A grid additionally keeps levels with
+ * n < ECMG_OPT_SHARD_MIN (default 256) replicated; ecmg_level_shape reports the layout it uses. */
 int ecmg_slab_partition(int n_cells_z, int nranks, int rank, int* z_lo, int* z_hi);
 
 /* NCCL unique id for ecmg_dist.nccl_id: rank 0 calls this and broadcasts the 128 bytes (e.g. with

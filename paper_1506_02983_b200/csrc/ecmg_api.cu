@@ -71,6 +71,7 @@ struct ecmg_grid {
   int kernel_variant = 1;   // ECMG_OPT_KERNEL
   int use_graph = 1;        // ECMG_OPT_GRAPH: device-driven JCG loop (CUDA graph, conditional WHILE node)
   int unfused = 0;          // ECMG_OPT_UNFUSED: fixed-count constant-stencil solves by the textbook sequence
+  int shard_min = kShardMinDefault;   // ECMG_OPT_SHARD_MIN: z-slabs split only levels with >= this many z cells
   int hybrid = 1;           // ECMG_OPT_SLAB_HYBRID: z-slabs, replicated levels through the single-GPU path
   int fused_halo = 1;       // ECMG_OPT_FUSED_HALO: z-slab halo planes stored by K2 / init into the neighbours
   int pdl = 0;              // ECMG_OPT_PDL: programmatic dependent launch between the JCG kernels (measured: no gain
@@ -136,6 +137,7 @@ SlabCfg slab_cfg(const ecmg_grid* G) {
   c.zchunk = G->zchunk;
   c.fused_halo = G->fused_halo;
   c.beta_fly = G->beta_fly;
+  c.shard_min = G->shard_min;
   return c;
 }
 
@@ -619,7 +621,7 @@ int ecmg_create_grid(const ecmg_box* dom, const int coarsest_cells[3], int num_l
     size_level = 0;
     for (int k = 0; k < num_levels; ++k) {
       int zlo, zhi;
-      if (slab_partition((coarsest_cells[2]) << k, dist->nranks, 0, &zlo, &zhi)) break;
+      if (slab_partition((coarsest_cells[2]) << k, dist->nranks, 0, &zlo, &zhi, kShardMinDefault)) break;
       size_level = k;
     }
   }
@@ -804,6 +806,7 @@ int ecmg_set_option(ecmg_grid* G, int option, int value) {
     case ECMG_OPT_PERSISTENT: if (value < 0) return ECMG_EINVAL; G->persistent_max = value; break;
     case ECMG_OPT_PERS_TMA: if (value < 0) return ECMG_EINVAL; G->pers_tma_max = value; break;
     case ECMG_OPT_UNFUSED: if (value != 0 && value != 1) return ECMG_EINVAL; G->unfused = value; break;
+    case ECMG_OPT_SHARD_MIN: if (value < 0) return ECMG_EINVAL; G->shard_min = value; break;
     case ECMG_OPT_SLAB_HYBRID: if (value != 0 && value != 1) return ECMG_EINVAL; G->hybrid = value; break;
     case ECMG_OPT_CTA_SOLVE: if (value < 0) return ECMG_EINVAL; G->cta_max = value; break;
     case ECMG_OPT_PDL: if (value != 0 && value != 1) return ECMG_EINVAL; G->pdl = value; clear_graphs(G); break;

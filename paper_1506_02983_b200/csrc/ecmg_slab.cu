@@ -514,7 +514,7 @@ SlabDriver* slab_driver_create(const SlabCfg& cfg, int P, int rank, bool virt, c
     long long vec = 64;
     for (int k = 0; k < cfg.L; ++k) {
       bool sh;
-      LevelGeom g = slab_geom(make_geom(cfg.dom, cfg.n0, k, face_none, 1), P, c.rank, &sh);
+      LevelGeom g = slab_geom(make_geom(cfg.dom, cfg.n0, k, face_none, 1), P, c.rank, &sh, cfg.shard_min);
       vec = std::max(vec, g.S * (long long)g.nza + 64);
     }
     const LevelGeom gf = make_geom(cfg.dom, cfg.n0, cfg.L - 1, face_none, 1);
@@ -563,11 +563,11 @@ void slab_driver_configure(SlabDriver* d, const SlabCfg& cfg) {
     for (int k = 0; k < cfg.L; ++k) {
       bool sh;
       const LevelGeom gk = make_geom(cfg.dom, cfg.n0, k, cfg.prob.face, cfg.elem_path);
-      c.geom.push_back(slab_geom(gk, d->P, c.rank, &sh));
+      c.geom.push_back(slab_geom(gk, d->P, c.rank, &sh, cfg.shard_min));
       c.sharded.push_back(sh ? 1 : 0);
       bool s2;   // the neighbours' level geometries follow from the same partition
-      if (c.rank > 0) c.nb_lo_zend[k] = slab_geom(gk, d->P, c.rank - 1, &s2).zend;
-      if (c.rank + 1 < d->P) c.nb_hi_zbeg[k] = slab_geom(gk, d->P, c.rank + 1, &s2).zbeg;
+      if (c.rank > 0) c.nb_lo_zend[k] = slab_geom(gk, d->P, c.rank - 1, &s2, cfg.shard_min).zend;
+      if (c.rank + 1 < d->P) c.nb_hi_zbeg[k] = slab_geom(gk, d->P, c.rank + 1, &s2, cfg.shard_min).zbeg;
     }
     c.maps_level = -1;
   }

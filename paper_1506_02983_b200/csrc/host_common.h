@@ -188,8 +188,10 @@ inline bool& slab_force_single() {   // test only: shard even with P = 1 (single
   return f;
 }
 
-inline bool slab_partition(int n, int P, int r, int* zlo, int* zhi) {
-  const bool sharded = (P > 1 || slab_force_single()) && n % (4 * P) == 0 && n / P >= 16;
+// min_n: levels with fewer z cells stay replicated even where they could be split (the driver's
+// ECMG_OPT_SHARD_MIN: a split level pays two allreduces and two finalize launches per iteration)
+inline bool slab_partition(int n, int P, int r, int* zlo, int* zhi, int min_n = 0) {
+  const bool sharded = (P > 1 || slab_force_single()) && n % (4 * P) == 0 && n / P >= 16 && n >= min_n;
   if (!sharded) { *zlo = 0; *zhi = n + 1; return false; }
   *zlo = r * (n / P);
   *zhi = (r == P - 1) ? n + 1 : (r + 1) * (n / P);
@@ -197,9 +199,9 @@ inline bool slab_partition(int n, int P, int r, int* zlo, int* zhi) {
 }
 
 // geometry of rank r's slab of a level (work vectors: owned free planes + one halo plane per side)
-inline LevelGeom slab_geom(LevelGeom g, int P, int r, bool* sharded) {
+inline LevelGeom slab_geom(LevelGeom g, int P, int r, bool* sharded, int min_n = 0) {
   int zlo, zhi;
-  *sharded = slab_partition(g.n[2], P, r, &zlo, &zhi);
+  *sharded = slab_partition(g.n[2], P, r, &zlo, &zhi, min_n);
   if (!*sharded) return g;
   g.zlo = zlo;
   g.zhi = zhi;

@@ -13,7 +13,9 @@ struct SlabCfg {
   int elem_path, exp_variant, precond, kernel_variant, zchunk;
   int fused_halo;   // 1: K2 / init store their boundary planes into the neighbours' halo planes
   int beta_fly;     // 1: element kernels form analytic beta from the level's axis tables
+  int shard_min;    // levels with fewer z cells are replicated (ECMG_OPT_SHARD_MIN)
 };
+constexpr int kShardMinDefault = 256;
 
 struct SlabDriver;
 // P slabs; virt = all P in this process on one GPU (test fixture), else this process is `rank` of P

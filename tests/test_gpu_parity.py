@@ -255,6 +255,7 @@ def test_graph_loop_equals_host_loop(pid, eps):
     for use_graph in (1, 0):
         g = Grid(4, 5, pid, params_for(pid))
         g.set_option(ecmg.OPT_GRAPH, use_graph)
+        g.set_option(ecmg.OPT_PERS_TMA, 0)   # 64^3 through the graph / host loop of the same K1 / K2
         u = g.new_vec(4)
         ut = g.new_vec(4)
         st, stats = g.run(eps, u, ut)

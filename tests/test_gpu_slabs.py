@@ -32,6 +32,7 @@ def test_virtual_slab_run(pid, levels, eps, P):
     st1, s1 = g1.run(eps, u1, ut1)
     gp = Grid(4, levels, pid, params_for(pid))
     gp.set_option(ecmg.OPT_VIRTUAL_SLABS, P)
+    gp.set_option(ecmg.OPT_SHARD_MIN, 16)   # split the small test levels too
     n_fine = 4 << (levels - 1)
     assert ecmg.slab_partition(n_fine, P, 0)[0]   # the finest level is sharded
     up, utp = gp.new_vec(levels - 1), gp.new_vec(levels - 1)
@@ -61,6 +62,7 @@ def test_virtual_slab_fixed_iterations(pid, P):
         g = Grid(4, level + 1, pid, params_for(pid))
         if p > 1:
             g.set_option(ecmg.OPT_VIRTUAL_SLABS, p)
+            g.set_option(ecmg.OPT_SHARD_MIN, 16)   # split the small test levels too
         u = torch.from_numpy(x0.copy()).cuda()
         st, s = g.solve_level(level, 0.0, 20, u)
         assert st == 0 and s["iterations"] == 20
@@ -84,7 +86,7 @@ from paper_1506_02983_b200 import Grid, ecmg, PROB
 nid = ecmg.nccl_unique_id()
 g1 = Grid(4, 5, PROB["C2"]); u1 = g1.new_vec(4); st1, s1 = g1.run(1e-10, u1)
 d = ecmg.make_dist(0, 1, nid)
-gn = Grid(4, 5, PROB["C2"], dist=d); un = gn.new_vec(4); stn, sn = gn.run(1e-10, un)
+gn = Grid(4, 5, PROB["C2"], dist=d); gn.set_option(ecmg.OPT_SHARD_MIN, 16); un = gn.new_vec(4); stn, sn = gn.run(1e-10, un)
 torch.cuda.synchronize()
 a, b = un.cpu().numpy(), u1.cpu().numpy()
 print(json.dumps(dict(st=[st1, stn], it1=[s["iterations"] for s in s1], itn=[s["iterations"] for s in sn],
@@ -110,6 +112,7 @@ def test_fused_halo_equals_copied_halo(pid, levels, eps, P):
     for fused in (0, 1):
         g = Grid(4, levels, pid, params_for(pid))
         g.set_option(ecmg.OPT_VIRTUAL_SLABS, P)
+        g.set_option(ecmg.OPT_SHARD_MIN, 16)   # split the small test levels too
         g.set_option(ecmg.OPT_FUSED_HALO, fused)
         u, ut = g.new_vec(levels - 1), g.new_vec(levels - 1)
         st, stats = g.run(eps, u, ut)
@@ -130,6 +133,7 @@ def test_hybrid_cascade_vs_slab_loop(pid, levels, eps, P):
     for hyb in (1, 0):
         g = Grid(4, levels, pid, params_for(pid))
         g.set_option(ecmg.OPT_VIRTUAL_SLABS, P)
+        g.set_option(ecmg.OPT_SHARD_MIN, 16)   # split the small test levels too
         g.set_option(ecmg.OPT_SLAB_HYBRID, hyb)
         u, ut = g.new_vec(levels - 1), g.new_vec(levels - 1)
         st, stats = g.run(eps, u, ut)
