@@ -258,7 +258,7 @@ def main():
     ms_p = max_over_ranks(ms_p)
     grid.set_option(ecmg.OPT_KERNEL, 1)
     ablation_unfused = None
-    if pid not in (3, 5):   # ablation: the unfused textbook PCG sequence (nine passes, 144 B/unknown)
+    if pid not in (3, 5) and ws == 1:   # ablation: the unfused textbook PCG sequence (9 passes, 144 B/unknown)
         grid.set_option(ecmg.OPT_UNFUSED, 1)
         xb.copy_(x0)
         grid.solve_level(fine, 0.0, 20, xb)
