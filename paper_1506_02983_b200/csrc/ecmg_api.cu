@@ -979,14 +979,35 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
     ECMG_CUDA(cudaStreamWaitEvent(G->hi2_stream, G->fork_ev, 0));
     // the finest level's setup (most of the work) on its own stream, so that it starts at once; the
     // coarser levels' setups in level order beside it
-    for (int k = 0; k < L_run; ++k) {
-      cudaStream_t s_k = (k == L_run - 1 && G->setup_ahead != 2) ? (G->setup_ahead == 4 ? G->hi2_stream : G->lo2_stream)
-                                                                 : G->lo_stream;
-      { int s = setup_level_on(G, k, s_k, G->setup_ctas); if (s) return s; }
-      ECMG_CUDA(launch_dirichlet_fill(G->geom[k], G->prob, level_u(k), 0.0, 0, s_k));
-      ECMG_CUDA(cudaEventRecord(G->setup_ev[k], s_k));
-    }
     G->stream = G->hi_stream;
+  }
+  // host enqueue order: the finest level's setup first (it starts at once on its own stream), then the
+  // coarse setups two levels ahead of the solves, so that the first solve is enqueued after a handful of
+  // launches instead of every level's setup
+  int next_setup = 0;
+  auto enqueue_setup = [&](int k) -> int {
+    cudaStream_t s_k = (k == L_run - 1 && G->setup_ahead != 2) ? (G->setup_ahead == 4 ? G->hi2_stream : G->lo2_stream)
+                                                               : G->lo_stream;
+    { int s = setup_level_on(G, k, s_k, G->setup_ctas); if (s) return s; }
+    ECMG_CUDA(launch_dirichlet_fill(G->geom[k], G->prob, level_u(k), 0.0, 0, s_k));
+    ECMG_CUDA(cudaEventRecord(G->setup_ev[k], s_k));
+    return ECMG_OK;
+  };
+  auto setups_until = [&](int k_last) -> int {   // enqueue the coarse setups up to level k_last
+    for (; next_setup <= std::min(k_last, L_run - 2); ++next_setup) {
+      const int s = enqueue_setup(next_setup);
+      if (s) return s;
+    }
+    return ECMG_OK;
+  };
+  if (ahead) {
+    if (G->setup_ahead == 2) {   // tuning mode: every setup on one stream, in level order
+      { int s = setups_until(L_run - 2); if (s) return s; }
+      { int s = enqueue_setup(L_run - 1); if (s) return s; }
+    } else {
+      { int s = enqueue_setup(L_run - 1); if (s) return s; }
+      { int s = setups_until(1); if (s) return s; }
+    }
   }
   // the whole cascade is enqueued without host synchronisation when every solve is device driven
   for (int k = 0; k < L_run; ++k) {
@@ -1031,6 +1052,7 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
       ECMG_CUDA(launch_exp_true(g, G->prob, uk, G->u[k - 1], ut_dev ? ut_fine : G->ut_tmp, G->stream));
     }
     ECMG_CUDA(cudaEventRecord(e[4], G->stream));
+    if (ahead) { int s = setups_until(k + 2); if (s) return s; }
   }
   if (u_fine && !u_dev)
     ECMG_CUDA(cudaMemcpyAsync(u_fine, G->u[G->L - 1], sizeof(double) * Nf, cudaMemcpyDeviceToHost, G->stream));

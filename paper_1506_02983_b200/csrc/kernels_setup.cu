@@ -429,9 +429,12 @@ __global__ void k_scatter(const LevelGeom g, const double* __restrict__ x, doubl
   u[gi] = x[(long long)lz * g.S + (long long)fy * g.P + fx];
 }
 
-// Dirichlet nodes (outside the free box) of a full nodal vector := g_D (or 0). One launch per
-// boundary face; nodes on shared edges are written twice with the same value.
-__global__ void k_dirichlet_face(const LevelGeom g, const Problem pb, double* __restrict__ u, int F, int zero) {
+// Dirichlet nodes (outside the free box) of a full nodal vector := g_D (or 0). One launch for all
+// faces: blockIdx.z = face (non-Dirichlet faces return); nodes on shared edges are written twice with
+// the same value.
+__global__ void k_dirichlet_face(const LevelGeom g, const Problem pb, double* __restrict__ u, int zero) {
+  const int F = blockIdx.z;
+  if (pb.face[F] != FACE_DIRICHLET) return;
   const int d = F >> 1, side = F & 1;
   const int d1 = (d == 0) ? 1 : 0, d2 = (d == 2) ? 1 : 2;
   const int i1 = blockIdx.x * blockDim.x + threadIdx.x, i2 = blockIdx.y;
@@ -536,14 +539,13 @@ cudaError_t launch_scatter(const LevelGeom& g, const double* x, double* u, cudaS
 
 cudaError_t launch_dirichlet_fill(const LevelGeom& g, const Problem& pb, double* u, double, int zero_instead,
                                   cudaStream_t st) {
-  for (int F = 0; F < 6; ++F) {
-    if (pb.face[F] != FACE_DIRICHLET) continue;
-    const int d = F >> 1;
-    const int d1 = (d == 0) ? 1 : 0, d2 = (d == 2) ? 1 : 2;
-    dim3 grid((g.n[d1] + 1 + 127) / 128, g.n[d2] + 1);
-    count_launch();
-    k_dirichlet_face<<<grid, 128, 0, st>>>(g, pb, u, F, zero_instead);
-  }
+  bool any = false;
+  for (int F = 0; F < 6; ++F) any = any || pb.face[F] == FACE_DIRICHLET;
+  if (!any) return cudaSuccess;
+  const int m = std::max(g.n[0], std::max(g.n[1], g.n[2])) + 1;
+  dim3 grid((m + 127) / 128, m, 6);
+  count_launch();
+  k_dirichlet_face<<<grid, 128, 0, st>>>(g, pb, u, zero_instead);
   return cudaGetLastError();
 }
 

@@ -30,7 +30,7 @@ def main():
         shape, nodes = g.shape(levels - 1)
         u = torch.empty(nodes, dtype=torch.float64, device="cuda")
         ut = torch.empty(nodes, dtype=torch.float64, device="cuda")
-        for ahead, c in [(0, 0), (1, 0), (4, 0), (3, 0), (1, 0), (4, 0), (3, 0), (1, 0), (4, 0)]:
+        for ahead, c in [(0, 0), (1, 0), (0, 0), (1, 0), (1, 0)]:
             g.set_option(ecmg.OPT_SETUP_AHEAD, ahead)
             g.set_option(ecmg.OPT_SETUP_CTAS, c)
             g.run(eps, u, ut)
