@@ -265,7 +265,10 @@ __device__ __forceinline__ double rpow_m14(double r2, const RhsC4Consts& k) {
 // carried in a register. ~75 fp64 operations per element instead of ~113 for the 8 x 8 element-vector
 // transform. Work items (tile, z chunk) are linear, taken by a grid-stride loop.
 constexpr int C4X = 31, C4Y = 15, C4NTH = 512;
-__global__ void __launch_bounds__(C4NTH, 2) k_rhs_c4(const LevelGeom g, double* __restrict__ b, int zc,
+#ifndef RHS_C4_MINB
+#define RHS_C4_MINB 2
+#endif
+__global__ void __launch_bounds__(C4NTH, RHS_C4_MINB) k_rhs_c4(const LevelGeom g, double* __restrict__ b, int zc,
                                                     const RhsC4Consts k, int tx, int ty, int items) {
   __shared__ double lo_s[2][2][16][32];   // [layer parity][qz][element row][lane]: y share of the row below
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -493,7 +496,10 @@ cudaError_t launch_rhs(const LevelGeom& g, const Problem& pb, const ElemStencil&
     const int TX = c4 ? C4X : VX, TY = c4 ? C4Y : VY;
     const long long tiles = (long long)((g.nf[0] + TX - 1) / TX) * ((g.nf[1] + TY - 1) / TY);
     const int nz = g.zend - g.zbeg;
-    const int zc = (int)std::max(4LL, std::min(32LL, tiles * nz / (c4 ? 500 : 1000)));
+#ifndef RHS_ZC_MAX
+#define RHS_ZC_MAX 32
+#endif
+    const int zc = (int)std::max(4LL, std::min((long long)RHS_ZC_MAX, tiles * nz / (c4 ? 500 : 1000)));
     dim3 grid((g.nf[0] + TX - 1) / TX, (g.nf[1] + TY - 1) / TY, (nz + zc - 1) / zc);
     count_launch();
     if (c4) {
