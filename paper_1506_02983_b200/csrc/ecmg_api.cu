@@ -1099,7 +1099,12 @@ int ecmg_run(ecmg_grid* G, double eps, ecmg_stats* per_level, double* u_fine, do
     // persistent / graph solves, setup ahead); their last two solutions seed the first sharded level's
     // EXP_finite in every local slab, and the slab driver takes over from there.
     int kc = slab_first_sharded(G->slab);
-    if (G->hybrid && kc >= 2 && kc <= G->size_level + 1) {
+    if (G->hybrid && kc >= G->L && G->size_level >= G->L - 1) {   // nothing split: the single-GPU run
+      return run_cascade(G, std::vector<double>(G->L, eps), std::vector<int>(G->L, 10000), per_level, u_fine, ut_fine);
+    }
+    if (G->hybrid && kc >= 2 && kc < G->L && kc <= G->size_level + 1) {
+      // the finest (split) level's setup runs ahead on the slab driver's stream meanwhile
+      if (G->setup_ahead) { const int r = slab_setup_ahead(G->slab, G->stream); if (r) return r; }
       int s0 = run_cascade(G, std::vector<double>(G->L, eps), std::vector<int>(G->L, 10000), stv.data(), nullptr,
                            nullptr, kc);
       if (s0 == ECMG_ECUDA || s0 == ECMG_ENOMEM) return s0;

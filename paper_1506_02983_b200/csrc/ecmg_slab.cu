@@ -89,6 +89,9 @@ struct SlabCtx {
   double* p[2] = {nullptr, nullptr};
   double* b = nullptr;
   double* beta = nullptr;
+  double* b_fin = nullptr;      // the finest level's b / beta / 1D tables (its setup can run ahead)
+  double* beta_fin = nullptr;
+  double* s1d_fin = nullptr;
   double* partials = nullptr;
   double* scratch1d = nullptr;
   double* seeds = nullptr;
@@ -120,6 +123,10 @@ struct SlabDriver {
   double last_jcg_ms = 0.0;
   int last_jcg_iters = 0;
   long long last_free = 0;
+  // the finest level's setup run ahead (hybrid cascade): its event, and whether it is pending
+  cudaStream_t ahead_stream = nullptr;
+  cudaEvent_t ahead_ev = nullptr, fork_ev = nullptr;
+  bool fin_ahead = false;
 };
 
 namespace {
@@ -211,6 +218,12 @@ int comm_u_halo(SlabDriver* d, int k, cudaStream_t st) {
 }
 
 // ---- per-slab kernels ------------------------------------------------------------------------
+// right-hand side / element beta / 1D tables of level k: the finest level has its own (its setup can
+// run ahead while the replicated levels are solved); the other sharded levels share one set
+inline double* bvec(const SlabDriver* d, SlabCtx& c, int k) { return k == d->L - 1 ? c.b_fin : c.b; }
+inline double* betavec(const SlabDriver* d, SlabCtx& c, int k) { return k == d->L - 1 ? c.beta_fin : c.beta; }
+inline double* s1dvec(const SlabDriver* d, SlabCtx& c, int k) { return k == d->L - 1 ? c.s1d_fin : c.scratch1d; }
+
 bool slab_maps(SlabDriver* d, SlabCtx& c, int k) {
   if (c.maps_level == k) return c.maps_ok;
   const LevelGeom& g = c.geom[k];
@@ -218,9 +231,8 @@ bool slab_maps(SlabDriver* d, SlabCtx& c, int k) {
   c.maps_ok = make_vec_tensor_map(&c.xh, c.x, g, hx, hy) == 0 && make_vec_tensor_map(&c.xi, c.x, g, ix, iy) == 0 &&
               make_vec_tensor_map(&c.rh, c.r, g, hx, hy) == 0 && make_vec_tensor_map(&c.ri, c.r, g, ix, iy) == 0 &&
               make_vec_tensor_map(&c.ph[0], c.p[0], g, hx, hy) == 0 &&
-              make_vec_tensor_map(&c.ph[1], c.p[1], g, hx, hy) == 0 && make_vec_tensor_map(&c.bi, c.b, g, ix, iy) == 0;
+              make_vec_tensor_map(&c.ph[1], c.p[1], g, hx, hy) == 0 && make_vec_tensor_map(&c.bi, bvec(d, c, k), g, ix, iy) == 0;
   c.maps_level = k;
-  (void)d;
   return c.maps_ok;
 }
 
@@ -244,7 +256,7 @@ cudaError_t slab_launch(SlabDriver* d, SlabCtx& c, int mode, int k, const KArgs&
     auto inter = [&](const double* p) -> const CUtensorMap* {
       if (p == c.x) return &c.xi;
       if (p == c.r) return &c.ri;
-      if (p == c.b) return &c.bi;
+      if (p == bvec(d, c, k)) return &c.bi;
       return nullptr;
     };
     const CUtensorMap* h0 = halo(a.h0);
@@ -264,7 +276,7 @@ KArgs base_args(SlabDriver* d, SlabCtx& c, int k, bool local_only) {
   a.partials = c.partials;
   a.sc = c.sc;
   a.zc = auto_zc(d->cfg.zchunk, d->cfg.elem_path, c.geom[k]);
-  a.beta = c.beta;
+  a.beta = betavec(d, c, k);
   a.local_only = local_only ? 1 : 0;
   return a;
 }
@@ -273,8 +285,8 @@ int setup_slab_level(SlabDriver* d, SlabCtx& c, int k, cudaStream_t st) {
   const SlabCfg& cf = d->cfg;
   const LevelGeom& g = c.geom[k];
   const ElemStencil es = make_elem_stencil(g, cf.prob, cf.precond);
-  if (cf.elem_path) SL_CUDA(launch_beta(g, cf.prob, c.beta, st));
-  SL_CUDA(launch_rhs(g, cf.prob, es, 1.0, cf.elem_path ? c.beta : nullptr, c.b, c.scratch1d, st));
+  if (cf.elem_path) SL_CUDA(launch_beta(g, cf.prob, betavec(d, c, k), st));
+  SL_CUDA(launch_rhs(g, cf.prob, es, 1.0, cf.elem_path ? betavec(d, c, k) : nullptr, bvec(d, c, k), s1dvec(d, c, k), st));
   return ECMG_OK;
 }
 
@@ -361,7 +373,7 @@ int slab_jcg(SlabDriver* d, int k, double eps, int max_iter, ecmg_stats* st, cud
     a.peer_hi = c.rank + 1 < d->P ? base[1] + (long long)(c.nb_hi_zbeg[k] - 1) * g.S : nullptr;
   };
   if ((rc = pass(MODE_INIT, [&](SlabCtx& c, KArgs& a) {
-         a.h0 = c.x; a.i0 = c.b; a.o0 = c.r; a.o1 = c.z;
+         a.h0 = c.x; a.i0 = bvec(d, c, k); a.o0 = c.r; a.o1 = c.z;
          set_peers(c, a);
        })))
     return rc;
@@ -407,7 +419,7 @@ int slab_jcg(SlabDriver* d, int k, double eps, int max_iter, ecmg_stats* st, cud
   }
   SL_CUDA(cudaEventRecord(d->ev[1], stream));
   if (sh && (rc = comm_halo(d, k, 0, stream))) return rc;
-  if ((rc = pass(MODE_TRUE, [&](SlabCtx& c, KArgs& a) { a.h0 = c.x; a.i0 = c.b; }))) return rc;
+  if ((rc = pass(MODE_TRUE, [&](SlabCtx& c, KArgs& a) { a.h0 = c.x; a.i0 = bvec(d, c, k); }))) return rc;
   const int status = read_stats(d, k, eps, st, stream);
   float ms = 0.f;
   cudaEventElapsedTime(&ms, d->ev[0], d->ev[1]);
@@ -525,7 +537,8 @@ SlabDriver* slab_driver_create(const SlabCfg& cfg, int P, int rank, bool virt, c
       return cudaMemset(*p, 0, sizeof(double) * n) == cudaSuccess;
     };
     bool ok = alloc(&c.x, vec) && alloc(&c.r, vec) && alloc(&c.z, vec) && alloc(&c.p[0], vec) && alloc(&c.p[1], vec) && alloc(&c.b, vec) &&
-              alloc(&c.beta, beta_n) && alloc(&c.partials, part_n) &&
+              alloc(&c.beta, beta_n) && alloc(&c.partials, part_n) && alloc(&c.b_fin, vec) && alloc(&c.beta_fin, beta_n) &&
+              alloc(&c.s1d_fin, 15LL * (std::max(gf.n[0], std::max(gf.n[1], gf.n[2])) + 1)) &&
               alloc(&c.scratch1d, 15LL * (std::max(gf.n[0], std::max(gf.n[1], gf.n[2])) + 1)) &&
               alloc(&c.seeds, (long long)(gf.n[0] / 2 + 1) * (gf.n[1] / 2 + 1) * (gf.n[2] / 2 + 1)) &&
               alloc(&c.ut, level_nodes(gf));
@@ -555,6 +568,7 @@ SlabDriver* slab_driver_create(const SlabCfg& cfg, int P, int rank, bool virt, c
 
 void slab_driver_configure(SlabDriver* d, const SlabCfg& cfg) {
   d->cfg = cfg;
+  d->fin_ahead = false;   // a pending ahead setup belongs to the previous configuration
   for (auto& c : d->s) {
     c.geom.clear();
     c.sharded.clear();
@@ -583,6 +597,7 @@ void slab_driver_destroy(SlabDriver* d) {
         if (c.peer_z[s]) cudaIpcCloseMemHandle(c.peer_z[s]);
       }
     cudaFree(c.x); cudaFree(c.r); cudaFree(c.z); cudaFree(c.p[0]); cudaFree(c.p[1]); cudaFree(c.b); cudaFree(c.beta);
+    cudaFree(c.b_fin); cudaFree(c.beta_fin); cudaFree(c.s1d_fin);
     cudaFree(c.partials); cudaFree(c.scratch1d); cudaFree(c.seeds); cudaFree(c.sc); cudaFree(c.ut);
     for (double* p : c.u) cudaFree(p);
   }
@@ -590,6 +605,9 @@ void slab_driver_destroy(SlabDriver* d) {
   if (d->sc_host) cudaFreeHost(d->sc_host);
   if (d->param_host) cudaFreeHost(d->param_host);
   cudaGetLastError();
+  if (d->ahead_stream) cudaStreamDestroy(d->ahead_stream);
+  if (d->ahead_ev) cudaEventDestroy(d->ahead_ev);
+  if (d->fork_ev) cudaEventDestroy(d->fork_ev);
   delete d;
 }
 
@@ -609,6 +627,27 @@ void slab_last_timing(const SlabDriver* d, double* ms, int* it, long long* nfree
 // ---- Alg. 4 over slabs -------------------------------------------------------------------------
 // u_out / ut_out: virtual slabs -> full-layout finest vectors (device or host); NCCL ranks -> this
 // rank's owned planes [zlo, zhi) of the finest level.
+// the finest level's setup (every local slab) on the driver's low-priority stream, forked from `stream`;
+// slab_run's finest level waits for it instead of setting up in line
+int slab_setup_ahead(SlabDriver* d, cudaStream_t stream) {
+  const int k = d->L - 1;
+  if (!d->ahead_stream) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    SL_CUDA(cudaStreamCreateWithPriority(&d->ahead_stream, cudaStreamNonBlocking, lo));
+    SL_CUDA(cudaEventCreateWithFlags(&d->ahead_ev, cudaEventDisableTiming));
+    SL_CUDA(cudaEventCreateWithFlags(&d->fork_ev, cudaEventDisableTiming));
+  }
+  SL_CUDA(cudaEventRecord(d->fork_ev, stream));
+  SL_CUDA(cudaStreamWaitEvent(d->ahead_stream, d->fork_ev, 0));
+  const bool sh = d->s[0].sharded[k];
+  const int nloc = (sh || !d->virt) ? (int)d->s.size() : 1;
+  for (int i = 0; i < nloc; ++i) { int r = setup_slab_level(d, d->s[i], k, d->ahead_stream); if (r) return r; }
+  SL_CUDA(cudaEventRecord(d->ahead_ev, d->ahead_stream));
+  d->fin_ahead = true;
+  return ECMG_OK;
+}
+
 int slab_first_sharded(const SlabDriver* d) {
   const auto& sh = d->s[0].sharded;
   for (int k = 0; k < (int)sh.size(); ++k)
@@ -634,7 +673,12 @@ int slab_run(SlabDriver* d, double eps, ecmg_stats* per_level, double* u_out, bo
     cudaEvent_t e0, e1, e2, e3;
     cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&e2); cudaEventCreate(&e3);
     SL_CUDA(cudaEventRecord(e0, stream));
-    for (int i = 0; i < nloc; ++i) { int r = setup_slab_level(d, d->s[i], k, stream); if (r) return r; }
+    if (k == L - 1 && d->fin_ahead) {   // set up ahead (slab_setup_ahead) while the replicated levels ran
+      SL_CUDA(cudaStreamWaitEvent(stream, d->ahead_ev, 0));
+      d->fin_ahead = false;
+    } else {
+      for (int i = 0; i < nloc; ++i) { int r = setup_slab_level(d, d->s[i], k, stream); if (r) return r; }
+    }
     SL_CUDA(cudaEventRecord(e1, stream));
     for (int i = 0; i < nloc; ++i) {
       SlabCtx& c = d->s[i];

@@ -26,6 +26,9 @@ void slab_driver_destroy(SlabDriver* d);
 // levels [k_begin, L) (levels below k_begin: u_k imported with slab_import_u, per_level left untouched)
 int slab_run(SlabDriver* d, double eps, ecmg_stats* per_level, double* u_out, bool u_dev, double* ut_out, bool ut_dev,
              cudaStream_t stream, int k_begin);
+// the finest level's setup on the driver's own low-priority stream (forked from `stream`); the next
+// slab_run waits for it instead of setting the finest level up in line
+int slab_setup_ahead(SlabDriver* d, cudaStream_t stream);
 // first sharded level (L if none); every level below it is replicated
 int slab_first_sharded(const SlabDriver* d);
 // copy a full-layout level-k solution into every local slab's u_k (the replicated levels' solutions)

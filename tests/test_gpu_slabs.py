@@ -143,3 +143,23 @@ def test_hybrid_cascade_vs_slab_loop(pid, levels, eps, P):
     assert all(abs(a - b) <= 1 for a, b in zip(res[0][0], res[1][0])), (res[0][0], res[1][0])
     for k in (1, 2):
         assert np.max(np.abs(res[0][k] - res[1][k])) <= 1e-9 * np.max(np.abs(res[1][k]))
+
+
+@pytest.mark.parametrize("pid,levels,eps,P", [(o.C2, 6, 1e-10, 2), (o.C5, 6, 1e-8, 4), (o.C3, 5, 1e-10, 2)])
+def test_slab_finest_setup_ahead_bitwise(pid, levels, eps, P):
+    # in the hybrid cascade the finest (split) level's setup runs ahead on the slab driver's stream while
+    # the replicated levels are solved (own b / beta buffers); same kernels on the same data as the in-line
+    # setup, so every iterate is bitwise equal; the second run on the same grid sets up ahead again
+    res = []
+    for ahead in (0, 1):
+        g = Grid(4, levels, pid, params_for(pid))
+        g.set_option(ecmg.OPT_VIRTUAL_SLABS, P)
+        g.set_option(ecmg.OPT_SHARD_MIN, 16)
+        g.set_option(ecmg.OPT_SETUP_AHEAD, ahead)
+        u, ut = g.new_vec(levels - 1), g.new_vec(levels - 1)
+        for _ in range(2):
+            st, stats = g.run(eps, u, ut)
+            assert st == 0
+        res.append(([s["iterations"] for s in stats], host(u), host(ut)))
+    assert res[0][0] == res[1][0]
+    assert np.array_equal(res[0][1], res[1][1]) and np.array_equal(res[0][2], res[1][2])
