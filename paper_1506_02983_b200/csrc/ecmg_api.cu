@@ -99,6 +99,7 @@ struct ecmg_grid {
   ParamHost* lvl_param = nullptr;
   JcgScalars* lvl_sc = nullptr;
   std::vector<cudaEvent_t> lvl_ev;
+  std::vector<char> lvl_graph;     // the level's last async solve ran its CUDA graph (launch count from iterations)
 };
 
 namespace {
@@ -424,6 +425,8 @@ int enqueue_jcg(ecmg_grid* G, int k, double eps, int max_iter, double* u_out, Pa
     if (!G->graphs[k]) ECMG_CUDA(build_level_graph(G, k, &G->graphs[k]));
     ECMG_CUDA(cudaGraphLaunch(G->graphs[k], G->stream));
   }
+  if ((int)G->lvl_graph.size() != G->L) G->lvl_graph.assign(G->L, 0);
+  G->lvl_graph[k] = (!persistent && !use_pers_tma(G, g)) ? 1 : 0;
   ECMG_CUDA(cudaMemcpyAsync(slot, G->sc, sizeof(JcgScalars), cudaMemcpyDeviceToHost, G->stream));
   return ECMG_OK;
 }
@@ -1066,6 +1069,8 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
   for (int k = 0; k < L_run; ++k) {
     ecmg_stats& st = stv[k];
     if (async[k]) {
+      // kernels the level's graph ran: init + true residual + the executed two-iteration loop bodies
+      if ((int)G->lvl_graph.size() == G->L && G->lvl_graph[k]) count_launch(2 + 4 * ((G->lvl_sc[k].iter + 1) / 2));
       int s = stats_from(G->lvl_sc[k], k < 2 ? 1e-14 : eps_lv[k], &st);
       if (k < 2 && s == ECMG_ENOTCONV) s = ECMG_OK;
       if (s != ECMG_OK && status == ECMG_OK) status = s;
