@@ -25,6 +25,7 @@ LIB = os.path.join(HERE, "liboracle.so")
 C1, C2, C3, C4, C5 = 1, 2, 3, 4, 5
 P1, P2, P3 = 11, 12, 13
 PATCH_TRILINEAR, PATCH_LAYERED, PATCH_ROBIN, CONST_F, PATCH_ROBIN_XY = 21, 22, 23, 24, 25
+ARRAYS = 100   # caller data per level: beta_e, f at the Gauss points, g_D per node, g_R at the face Gauss points
 DIRICHLET, ROBIN = 0, 1
 
 NSTAT = 17
@@ -85,6 +86,11 @@ def lib():
             L.orc_ecmg.restype = C.c_int
             L.orc_ecmg.argtypes = [dp, dp, ip, C.c_int, C.c_int, dp, C.c_int, ip, C.c_double, C.c_int,
                                    C.c_int, C.c_int, dp, dp, dp, dp]
+            L.orc_build_level_arrays.restype = vp
+            L.orc_build_level_arrays.argtypes = [dp, dp, ip, ip, dp, dp, dp, dp, dp]
+            L.orc_ecmg_arrays.restype = C.c_int
+            L.orc_ecmg_arrays.argtypes = [dp, dp, ip, C.c_int, dp, ip, C.POINTER(dp), C.c_double, C.c_int,
+                                          C.c_int, C.c_int, dp, dp, dp, dp]
             L.orc_ecmg_fixed.restype = C.c_int
             L.orc_ecmg_fixed.argtypes = [dp, dp, ip, C.c_int, C.c_int, dp, C.c_int, ip, C.c_int, C.c_double,
                                          C.c_int, C.c_int, dp, dp, dp, dp]
@@ -134,6 +140,28 @@ class Level:
                                     int(self.params.size if params is not None else 0), _i(self.faces))
         if not self._h:
             raise ValueError("oracle: invalid level / problem")
+
+    @classmethod
+    def from_arrays(cls, n_cells, faces, alpha, beta_e=None, f_q=None, gD=None, gR=None, lo=(0, 0, 0), hi=(1, 1, 1)):
+        """A level of the ARRAYS problem: beta_e[n_x n_y n_z] (x fastest), f_q[8 per element] (Gauss point
+        q = q_x + 2 q_y + 4 q_z, bit set = +1/sqrt(3)), gD[(n_x+1)(n_y+1)(n_z+1)], gR[per face x-..z+ a block of
+        4 n_d1 n_d2: 4 (e1 + n_d1 e2) + q], alpha[6]; None = beta 1 / f 0 / g_D 0 / g_R 0."""
+        self = cls.__new__(cls)
+        L = lib()
+        self.n = tuple(int(v) for v in n_cells)
+        self.shape = (self.n[2] + 1, self.n[1] + 1, self.n[0] + 1)
+        self.N = self.shape[0] * self.shape[1] * self.shape[2]
+        self.problem_id = ARRAYS
+        self.params = _f64(alpha)
+        self.faces = np.array(faces, dtype=np.int32)
+        self.lo, self.hi = _f64(lo), _f64(hi)
+        self._arrays = [None if a is None else _f64(a).reshape(-1) for a in (beta_e, f_q, gD, gR)]
+        n = np.array(self.n, dtype=np.int32)
+        ptr = [_d(a) if a is not None else None for a in self._arrays]
+        self._h = L.orc_build_level_arrays(_d(self.lo), _d(self.hi), _i(n), _i(self.faces), _d(self.params), *ptr)
+        if not self._h:
+            raise ValueError("oracle: invalid ARRAYS level")
+        return self
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -248,6 +276,28 @@ def ecmg(n0, levels, problem_id, eps, params=None, lo=(0, 0, 0), hi=(1, 1, 1), f
                         int(prm.size if params is not None else 0), _i(fc), float(eps), int(max_iter),
                         1 if precond else 0, int(exp_variant), _d(stats), _d(u), _d(ut),
                         _d(w) if w is not None else None)
+    stats = stats.reshape(levels, NSTAT)
+    if want_w:
+        return st, stats, u, ut, w
+    return st, stats, u, ut
+
+
+def ecmg_arrays(n0, levels, faces, alpha, level_arrays, eps, lo=(0, 0, 0), hi=(1, 1, 1), max_iter=100000,
+                precond=True, want_w=False, exp_variant=0):
+    """Alg. 4 on ARRAYS data: level_arrays[k] = (beta_e, f_q, gD, gR) of level k (layouts: Level.from_arrays)."""
+    n0 = np.array([n0] * 3 if np.isscalar(n0) else list(n0), dtype=np.int32)
+    nf = n0 * (1 << (levels - 1))
+    N = int(np.prod(nf + 1))
+    stats = np.empty(levels * NSTAT)
+    u, ut = np.empty(N), np.empty(N)
+    w = np.empty(N) if want_w else None
+    keep = [None if a is None else _f64(a).reshape(-1) for lv in level_arrays for a in lv]
+    ptrs = (C.POINTER(C.c_double) * len(keep))(*[_d(a) if a is not None else None for a in keep])
+    fc = np.array(faces, dtype=np.int32)
+    st = lib().orc_ecmg_arrays(_d(_f64(lo)), _d(_f64(hi)), _i(n0), int(levels), _d(_f64(alpha)), _i(fc), ptrs,
+                               float(eps), int(max_iter), 1 if precond else 0, int(exp_variant), _d(stats), _d(u),
+                               _d(ut), _d(w) if w is not None else None)
+    del keep
     stats = stats.reshape(levels, NSTAT)
     if want_w:
         return st, stats, u, ut, w

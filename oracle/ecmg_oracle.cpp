@@ -54,6 +54,7 @@ enum {
   PROB_P1 = 11, PROB_P2 = 12, PROB_P3 = 13,
   PROB_PATCH_TRILINEAR = 21, PROB_PATCH_LAYERED = 22, PROB_PATCH_ROBIN = 23, PROB_CONST_F = 24,
   PROB_PATCH_ROBIN_XY = 25,
+  PROB_ARRAYS = 100,   // caller data per level (SURVEY.md §8b ECMG_PROB_ARRAYS; reading R8)
 };
 
 const double PI = 3.14159265358979323846;
@@ -66,6 +67,13 @@ struct Problem {
   int face[6] = {0, 0, 0, 0, 0, 0};  // x-, x+, y-, y+, z-, z+
   std::vector<double> params;
   bool has_exact = false;
+  // PROB_ARRAYS: the data of Eq. (bvp) given on one level at the quadrature / nodal points the
+  // discretisation reads: beta_e per element (element e = ex + n_x (ey + n_y ez)), f at the 8
+  // Gauss points of each element (index 8 e + q, q = q_x + 2 q_y + 4 q_z, bit set = +1/sqrt(3)), g_D per
+  // node, g_R at the 4 Gauss points of each Robin face element (per face F in order x-..z+ a block of
+  // n_d1 n_d2 4 values, index 4 (e1 + n_d1 e2) + q, q = q_1 + 2 q_2, d1 < d2 the in-face axes); alpha
+  // per face = params[F]. A null array means beta = 1, f = 0, g_D = 0, g_R = 0.
+  const double *a_beta = nullptr, *a_f = nullptr, *a_gD = nullptr, *a_gR = nullptr;
 
   // C5 / layered geometry (params layout documented in synth/__init__.py)
   double layer_beta_at(double z) const {
@@ -150,6 +158,7 @@ struct Problem {
 
   double alpha(int face_id) const {
     switch (id) {
+      case PROB_ARRAYS: return params[face_id];
       case PROB_C3: case PROB_PATCH_ROBIN: return 1.0;
       case PROB_PATCH_ROBIN_XY: {   // Robin on x-, x+, y-, y+ with a different alpha each
         const double a[6] = {2.0, 0.5, 1.5, 3.0, 0.0, 0.0};
@@ -196,6 +205,10 @@ bool make_problem(int id, const double* params, int nparams, const int* face_in,
       P->has_exact = true; break;
     case PROB_CONST_F:
       P->has_exact = false; break;
+    case PROB_ARRAYS:
+      if (nparams < 6) return false;
+      for (int f = 0; f < 6; ++f) if (!(params[f] >= 0.0)) return false;
+      P->has_exact = false; break;
     default: return false;
   }
   if (face_in) for (int f = 0; f < 6; ++f) P->face[f] = face_in[f];
@@ -233,14 +246,15 @@ void element_stiffness(const double h[3], double beta, double K[8][8]) {
 }
 
 // F_e[a] = sum_q f(x_q) N_a(xi_q) detJ, element with lower corner node index (ex,ey,ez)
-void element_load(const Problem& P, const double lo[3], const double h[3], const int e[3], double F[8]) {
+void element_load(const Problem& P, const double lo[3], const double h[3], const int e[3], double F[8],
+                  const double* f_arr = nullptr /* PROB_ARRAYS: f at this element's 8 Gauss points */) {
   for (int a = 0; a < 8; ++a) F[a] = 0.0;
   const double detJ = h[0] * h[1] * h[2] / 8.0;
   for (int q = 0; q < 8; ++q) {
     double xi[3] = {sgn(q, 0) * GAUSS, sgn(q, 1) * GAUSS, sgn(q, 2) * GAUSS};
     double x[3];
     for (int d = 0; d < 3; ++d) x[d] = lo[d] + (e[d] + (1.0 + xi[d]) / 2.0) * h[d];
-    double fq = P.f(x[0], x[1], x[2]);
+    double fq = P.id == PROB_ARRAYS ? (f_arr ? f_arr[q] : 0.0) : P.f(x[0], x[1], x[2]);
     for (int a = 0; a < 8; ++a) {
       double N = 1.0;
       for (int d = 0; d < 3; ++d) N *= (1.0 + sgn(a, d) * xi[d]) / 2.0;
@@ -317,7 +331,8 @@ bool build_level(Level* L, const double lo[3], const double hi[3], const int n[3
         }
         long i = L->idx(ix, iy, iz);
         L->dir[i] = D ? 1 : 0;
-        if (D) L->gDv[i] = P.gD(L->coord(0, ix), L->coord(1, iy), L->coord(2, iz));
+        if (D) L->gDv[i] = P.id == PROB_ARRAYS ? (P.a_gD ? P.a_gD[i] : 0.0)
+                                               : P.gD(L->coord(0, ix), L->coord(1, iy), L->coord(2, iz));
       }
 
   // volume terms, elements in lexicographic order
@@ -330,9 +345,11 @@ bool build_level(Level* L, const double lo[3], const double hi[3], const int n[3
         double cx = L->lo[0] + (ex + 0.5) * L->h[0];
         double cy = L->lo[1] + (ey + 0.5) * L->h[1];
         double cz = L->lo[2] + (ez + 0.5) * L->h[2];
-        element_stiffness(Kh, P.beta(cx, cy, cz), K);
+        const long el = ex + (long)n[0] * (ey + (long)n[1] * ez);
+        const double be = P.id == PROB_ARRAYS ? (P.a_beta ? P.a_beta[el] : 1.0) : P.beta(cx, cy, cz);
+        element_stiffness(Kh, be, K);
         int e[3] = {ex, ey, ez};
-        element_load(P, L->lo, L->h, e, Fe);
+        element_load(P, L->lo, L->h, e, Fe, P.a_f ? P.a_f + 8 * el : nullptr);
         for (int a = 0; a < 8; ++a) {
           long ia = L->idx(ex + (a & 1), ey + ((a >> 1) & 1), ez + ((a >> 2) & 1));
           L->F[ia] += Fe[a];
@@ -344,10 +361,13 @@ bool build_level(Level* L, const double lo[3], const double hi[3], const int n[3
       }
 
   // Robin faces (a(u,v) gets int alpha u v, f(v) gets int g_R v)
+  long gR_block = 0;   // PROB_ARRAYS: offset of this face's block of g_R values
   for (int face = 0; face < 6; ++face) {
-    if (P.face[face] != FACE_ROBIN) continue;
     const int d = face / 2, side = face % 2;
     const int d1 = (d == 0) ? 1 : 0, d2 = (d == 2) ? 1 : 2;
+    const long block = gR_block;
+    gR_block += 4L * n[d1] * n[d2];
+    if (P.face[face] != FACE_ROBIN) continue;
     const long fixed = side ? L->n[d] : 0;
     for (int e2 = 0; e2 < n[d2]; ++e2)
       for (int e1 = 0; e1 < n[d1]; ++e1) {
@@ -359,7 +379,8 @@ bool build_level(Level* L, const double lo[3], const double hi[3], const int n[3
           x[d1] = L->lo[d1] + (e1 + (1.0 + xi1) / 2.0) * L->h[d1];
           x[d2] = L->lo[d2] + (e2 + (1.0 + xi2) / 2.0) * L->h[d2];
           aq[q] = P.alpha(face);
-          gq[q] = P.gR(face, x[0], x[1], x[2]);
+          gq[q] = P.id == PROB_ARRAYS ? (P.a_gR ? P.a_gR[block + 4L * (e1 + (long)n[d1] * e2) + q] : 0.0)
+                                      : P.gR(face, x[0], x[1], x[2]);
         }
         double M[4][4], G[4];
         face_integrals(L->h[d1], L->h[d2], aq, gq, M, G);
@@ -834,7 +855,19 @@ struct orc_level { Level L; };
 orc_level* orc_build_level(const double* lo, const double* hi, const int* n, int problem_id,
                            const double* params, int nparams, const int* face) {
   Problem P;
-  if (!make_problem(problem_id, params, nparams, face, &P)) return nullptr;
+  if (problem_id == PROB_ARRAYS || !make_problem(problem_id, params, nparams, face, &P)) return nullptr;
+  orc_level* h = new orc_level;
+  if (!build_level(&h->L, lo, hi, n, P)) { delete h; return nullptr; }
+  return h;
+}
+
+// PROB_ARRAYS level: alpha[6] per face, arrays as documented at Problem::a_beta (each may be NULL)
+orc_level* orc_build_level_arrays(const double* lo, const double* hi, const int* n, const int* face,
+                                  const double* alpha, const double* beta_e, const double* f_q, const double* gD_n,
+                                  const double* gR_q) {
+  Problem P;
+  if (!make_problem(PROB_ARRAYS, alpha, 6, face, &P)) return nullptr;
+  P.a_beta = beta_e; P.a_f = f_q; P.a_gD = gD_n; P.a_gR = gR_q;
   orc_level* h = new orc_level;
   if (!build_level(&h->L, lo, hi, n, P)) { delete h; return nullptr; }
   return h;
@@ -889,6 +922,7 @@ void orc_norms(const orc_level* h, const double* e, double* l2, double* linf) { 
 // neighbour loops in apply_ff's / build_level's order; dg[k] = A_ii. p, q, b, dg may be NULL.
 int orc_rows(const double* lo, const double* hi, const int* n, int problem_id, const double* params, int nparams,
              const int* face, const long long* nodes, long count, const double* p, double* q, double* b, double* dg) {
+  if (problem_id == PROB_ARRAYS) return ORC_EINVAL;   // per-level arrays: orc_build_level_arrays
   Problem P;
   if (!make_problem(problem_id, params, nparams, face, &P)) return ORC_EINVAL;
   double h[3];
@@ -935,6 +969,7 @@ int orc_rows(const double* lo, const double* hi, const int* n, int problem_id, c
 int orc_exp_nodes(const double* lo, const double* hi, const int* n, int problem_id, const double* params, int nparams,
                   const int* face, int which /* 0 Serendipity, 1 Lagrange, 2 EXP_true */, const double* a,
                   const double* c, const long long* nodes, long count, double* out) {
+  if (problem_id == PROB_ARRAYS) return ORC_EINVAL;   // per-level arrays: orc_build_level_arrays
   Problem P;
   if (!make_problem(problem_id, params, nparams, face, &P)) return ORC_EINVAL;
   for (int d = 0; d < 3; ++d) if (n[d] % (which == 2 ? 2 : 4)) return ORC_EMISMATCH;
@@ -982,7 +1017,8 @@ void orc_serendipity_weights(double xi, double eta, double zeta, double* w20) {
 // means exactly maxit_k[k] CG / JCG iterations (Alg. 3's fixed counts).
 static int ecmg_impl(const double* lo, const double* hi, const int* coarsest, int num_levels, int problem_id,
                      const double* params, int nparams, const int* face, const double* eps_k, const int* maxit_k,
-                     int precond, int exp_variant, double* stats, double* u_fine, double* ut_fine, double* w_fine) {
+                     int precond, int exp_variant, double* stats, double* u_fine, double* ut_fine, double* w_fine,
+                     const double* const* level_arrays = nullptr /* PROB_ARRAYS: 4 per level */) {
   Problem P;
   if (!make_problem(problem_id, params, nparams, face, &P)) return ORC_EINVAL;
   if (num_levels < 3) return ORC_EINVAL;
@@ -995,6 +1031,11 @@ static int ecmg_impl(const double* lo, const double* hi, const int* coarsest, in
     int n[3] = {coarsest[0] << k, coarsest[1] << k, coarsest[2] << k};
     double t0 = now_s();
     Level* L = new Level;
+    if (problem_id == PROB_ARRAYS) {
+      if (!level_arrays) { delete L; return ORC_EINVAL; }
+      P.a_beta = level_arrays[4 * k]; P.a_f = level_arrays[4 * k + 1];
+      P.a_gD = level_arrays[4 * k + 2]; P.a_gR = level_arrays[4 * k + 3];
+    }
     if (!build_level(L, lo, hi, n, P)) { delete L; return ORC_EINVAL; }
     double t1 = now_s();
     row[11] = t1 - t0;
@@ -1078,6 +1119,17 @@ int orc_ecmg(const double* lo, const double* hi, const int* coarsest, int num_le
 // Alg. 3: the original ECMG with a fixed number of iterations per level, Eq. (ee)
 // (P:290-295): m_j = ceil(m_L * ratio^(L-j)) on the j-th ECMG level (j = 1..L, L = num_levels - 2;
 // reading R4 in DESIGN.md), plain CG by default (precond = 0). Levels 0, 1: DSOLVE.
+// Alg. 4 on PROB_ARRAYS data: level_arrays[4 k + {0, 1, 2, 3}] = beta_e, f_q, gD_n, gR_q of level k
+int orc_ecmg_arrays(const double* lo, const double* hi, const int* coarsest, int num_levels, const double* alpha,
+                    const int* face, const double* const* level_arrays, double eps, int max_iter, int precond,
+                    int exp_variant, double* stats, double* u_fine, double* ut_fine, double* w_fine) {
+  if (num_levels < 3 || num_levels > 16 || !level_arrays) return ORC_EINVAL;
+  std::vector<double> e(num_levels, eps);
+  std::vector<int> m(num_levels, max_iter);
+  return ecmg_impl(lo, hi, coarsest, num_levels, PROB_ARRAYS, alpha, 6, face, e.data(), m.data(), precond,
+                   exp_variant, stats, u_fine, ut_fine, w_fine, level_arrays);
+}
+
 int orc_ecmg_fixed(const double* lo, const double* hi, const int* coarsest, int num_levels, int problem_id,
                    const double* params, int nparams, const int* face, int m_L, double ratio, int precond,
                    int exp_variant, double* stats, double* u_fine, double* ut_fine, double* w_fine) {

@@ -101,3 +101,24 @@ def c5_geometry(seed: int = 0) -> np.ndarray:
 def layered_only(seed: int = 0) -> np.ndarray:
     """The C5 layer set with no boxes (for the layered-beta patch test)."""
     return c5_geometry(seed)[:15].copy()
+
+
+def face_gauss_count(n_cells) -> int:
+    """Length of a g_R array of the ARRAYS problem: 4 Gauss points per face element, all six faces."""
+    nx, ny, nz = (int(v) for v in n_cells)
+    return 4 * 2 * (ny * nz + nx * nz + nx * ny)
+
+
+def random_problem_arrays(seed: int, n_cells, beta=True):
+    """Seeded data of the ARRAYS problem on one level (SURVEY.md §8b ECMG_PROB_ARRAYS; layouts in
+    include/ecmg.h): beta_e in [0.5, 2) per element (None if beta is False: beta = 1), f at the 8 Gauss
+    points of each element in [-1, 1), g_D per node in [-1, 1), g_R at the 4 Gauss points of every face
+    element in [-1, 1)."""
+    nx, ny, nz = (int(v) for v in n_cells)
+    ne, nn = nx * ny * nz, (nx + 1) * (ny + 1) * (nz + 1)
+    u = counter_uniform(seed, ne + 8 * ne + nn + face_gauss_count(n_cells))
+    b = 0.5 + 1.5 * u[:ne] if beta else None
+    f = 2.0 * u[ne:9 * ne] - 1.0
+    g = 2.0 * u[9 * ne:9 * ne + nn] - 1.0
+    r = 2.0 * u[9 * ne + nn:] - 1.0
+    return b, f, g, r

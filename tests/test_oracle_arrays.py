@@ -1,0 +1,77 @@
+"""The oracle's ARRAYS problem (SURVEY.md §8b ECMG_PROB_ARRAYS: beta_e, f at the Gauss points, g_D per node,
+g_R at the face Gauss points, given by the caller per level) pinned against what fixes it independently:
+(1) C3's data sampled at those points gives the level the analytic C3 registry builds (matrix, load, lifted
+right-hand side, Dirichlet values), which test_oracle_fe.py pins to closed forms; a transposed array
+index (element order, Gauss point order, face block or in-face order) moves values by O(h) and fails it;
+(2) a layered-beta linear patch with Robin faces of four different alphas is solved exactly (Galerkin
+exactness: u is in the Q1 space and beta grad u is divergence free), which fails for a wrong beta layer or a
+misplaced g_R block; (3) Alg. 4 on the sampled C3 reproduces Alg. 4 on the analytic C3."""
+import numpy as np
+import pytest
+
+import oracle as o
+import synth
+from arrays_data import C3_ALPHA, C3_FACES, PATCH_ALPHA, PATCH_FACES, c3_arrays, patch_arrays, patch_u, node_points
+
+
+def rel(a, b):
+    return np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300)
+
+
+@pytest.mark.parametrize("n,lo,hi", [((6, 5, 4), (0, 0, 0), (1, 1, 1)), ((4, 6, 8), (-0.5, 0.0, 0.25), (1.5, 0.75, 1.0))])
+def test_sampled_c3_equals_registry(n, lo, hi):
+    ref = o.Level(n, o.C3, lo=lo, hi=hi)
+    arr = o.Level.from_arrays(n, C3_FACES, C3_ALPHA, *c3_arrays(n, lo, hi), lo=lo, hi=hi)
+    assert rel(arr.matrix(), ref.matrix()) <= 1e-14
+    assert rel(arr.load(), ref.load()) <= 1e-13
+    (ba, na), (br, nr) = arr.rhs(), ref.rhs()
+    assert rel(ba, br) <= 1e-13 and abs(na - nr) <= 1e-13 * nr
+    (ma, ga), (mr, gr) = arr.dirichlet(), ref.dirichlet()
+    assert np.array_equal(ma, mr) and rel(ga, gr) <= 1e-15
+
+
+def test_arrays_none_defaults():
+    # beta = 1, f = g_D = g_R = 0 when the arrays are absent: the Laplacian with a zero right-hand side
+    n = (4, 3, 5)
+    a = o.Level.from_arrays(n, [0, 1, 0, 0, 1, 0], [0, 0.5, 0, 0, 2.0, 0])
+    assert np.max(np.abs(a.rhs()[0])) == 0.0 and np.max(np.abs(a.load())) == 0.0
+    one = o.Level.from_arrays(n, [0, 1, 0, 0, 1, 0], [0, 0.5, 0, 0, 2.0, 0], beta_e=np.ones(60))
+    assert np.array_equal(a.matrix(), one.matrix())
+
+
+def test_arrays_reject():
+    with pytest.raises(ValueError):
+        o.Level.from_arrays((4, 4, 4), [0] * 6, [0, 0, -1.0, 0, 0, 0])   # alpha < 0
+
+
+@pytest.mark.parametrize("n", [(4, 4, 4), (6, 5, 7)])
+def test_layered_patch_exact(n):
+    layer = 0.5 + 1.5 * synth.counter_uniform(31, n[2])
+    L = o.Level.from_arrays(n, PATCH_FACES, PATCH_ALPHA, *patch_arrays(n, layer))
+    x, s = L.jcg(np.zeros(L.N), 1e-14, 10000)
+    assert s["status"] == 0
+    free = L.dirichlet()[0] == 0
+    ue = patch_u(*node_points(n, (0, 0, 0), (1, 1, 1))).reshape(-1)
+    assert np.max(np.abs(x - ue)[free]) <= 1e-11
+
+
+def test_layered_patch_wrong_layer_order_fails():
+    # the same data with the element layers reversed is a different problem: the patch is no longer exact
+    n = (4, 4, 6)
+    layer = 0.5 + 1.5 * synth.counter_uniform(31, n[2])
+    b, f, g, r = patch_arrays(n, layer)
+    L = o.Level.from_arrays(n, PATCH_FACES, PATCH_ALPHA, b.reshape(n[2], -1)[::-1].reshape(-1), f, g, r)
+    x, _ = L.jcg(np.zeros(L.N), 1e-14, 10000)
+    free = L.dirichlet()[0] == 0
+    ue = patch_u(*node_points(n, (0, 0, 0), (1, 1, 1))).reshape(-1)
+    assert np.max(np.abs(x - ue)[free]) > 1e-6
+
+
+def test_ecmg_arrays_equals_registry():
+    lv = 4
+    arrays = [c3_arrays((4 << k,) * 3) for k in range(lv)]
+    sa, ta, ua, uta = o.ecmg_arrays(4, lv, C3_FACES, C3_ALPHA, arrays, 1e-10)
+    sr, tr, ur, utr = o.ecmg(4, lv, o.C3, 1e-10)
+    assert sa == 0 and sr == 0
+    assert list(ta[:, 0]) == list(tr[:, 0])
+    assert rel(ua, ur) <= 1e-11 and rel(uta, utr) <= 1e-11
