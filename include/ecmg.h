@@ -57,7 +57,9 @@ typedef enum {
   ECMG_PROB_PATCH_TRILINEAR = 21,
   ECMG_PROB_PATCH_LAYERED = 22, /* params[15]: the C5 layer set */
   ECMG_PROB_PATCH_ROBIN = 23,
-  ECMG_PROB_CONST_F = 24
+  ECMG_PROB_CONST_F = 24,
+  ECMG_PROB_PATCH_ROBIN_XY = 25, /* linear patch, Robin on x-, x+, y-, y+ with alpha 2, 0.5, 1.5, 3 */
+  ECMG_PROB_ARRAYS = 100  /* the caller's data per level (ecmg_problem.level_arrays), any face kinds */
 } ecmg_problem_id;
 
 typedef struct { double lo[3], hi[3]; } ecmg_box;  /* domain Omega = [lo, hi]; hi > lo */
@@ -84,8 +86,25 @@ int ecmg_create_grid(const ecmg_box* dom, const int coarsest_cells[3], int num_l
 typedef struct {
   ecmg_face_kind face[6];   /* x-, x+, y-, y+, z-, z+; must equal the problem's own boundary kinds */
   int problem_id;           /* ecmg_problem_id */
-  const double* params;     /* host array, problem parameters (C5: 48 doubles, PATCH_LAYERED: 15) */
+  const double* params;     /* host array, problem parameters (C5: 48 doubles, PATCH_LAYERED: 15,
+                               ARRAYS: 6 = alpha per face, read on Robin faces, >= 0) */
   int n_params;
+  /* ECMG_PROB_ARRAYS only (else NULL / 0): n_level_arrays = 4 * num_levels device pointers, level k's
+   * data of Eq. (bvp) at the points the discretisation reads:
+   *   [4k+0] beta_e   n_x n_y n_z doubles, element e = ex + n_x (ey + n_y ez); beta > 0 (not checked);
+   *                   NULL on every level = beta 1 (then all-Dirichlet problems take the constant stencil)
+   *   [4k+1] f_q      8 per element, index 8 e + q, q = q_x + 2 q_y + 4 q_z: the 2x2x2 Gauss point
+   *                   lo + (e + (1 +- 1/sqrt(3)) / 2) h per axis, bit set = the + point; NULL = f 0
+   *   [4k+2] gD       (n_x+1)(n_y+1)(n_z+1) nodes, x fastest, read on Dirichlet nodes only; NULL = 0
+   *   [4k+3] gR       per face F = x-, x+, y-, y+, z-, z+ a block of 4 n_d1 n_d2 values (d1 < d2 the in-face
+   *                   axes), index 4 (e1 + n_d1 e2) + q, q = q_1 + 2 q_2 the 2x2 face Gauss point; read on
+   *                   Robin faces only; NULL = 0
+   * The grid keeps the pointers: the arrays are read by every call that runs a level's setup or a
+   * Dirichlet fill (ecmg_run, ecmg_run_fixed, ecmg_solve_level, ecmg_level_rhs, the EXP calls) and must stay
+   * valid and unchanged until the next ecmg_set_coeffs or ecmg_destroy_grid (reading R8).
+   * Single GPU only (ECMG_EINVAL with dist / virtual slabs). */
+  const double* const* level_arrays;
+  int n_level_arrays;
 } ecmg_problem;
 
 /* Bind the problem of Eq. (bvp) to the grid. Level operators are matrix-free; the

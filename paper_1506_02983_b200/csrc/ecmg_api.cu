@@ -47,6 +47,7 @@ struct ecmg_grid {
   std::vector<double*> betal;      // per-level element beta (element path)
   std::vector<double*> s1d;        // per-level 1D Gauss load tables (separable right-hand sides)
   std::vector<char> setup_ok;      // level k's b / beta hold the current problem's data
+  std::vector<const double*> arrays;   // ECMG_PROB_ARRAYS: the caller's 4 device arrays per level
   int setup_ahead = 1;             // ECMG_OPT_SETUP_AHEAD
   int beta_fly = 0;                // ECMG_OPT_BETA_FLY: element kernels form analytic beta from axis tables (measured:
                                    // 16 B/unknown less traffic but no faster -- the element kernels are latency bound)
@@ -198,11 +199,20 @@ cudaError_t launch_mode(ecmg_grid* G, int mode, const LevelGeom& g, const KArgs&
 
 // Level setup (row a1): element beta, lifted right-hand side b_k. Independent of every solution, so
 // ecmg_run enqueues it for all levels up front on a low-priority stream (ECMG_OPT_SETUP_AHEAD).
+// the problem as level k's kernels see it (ECMG_PROB_ARRAYS: with that level's caller arrays)
+Problem level_prob(const ecmg_grid* G, int k) {
+  Problem p = G->prob;
+  if (p.id == PROB_ARRAYS && (int)G->arrays.size() == 4 * G->L)
+    for (int j = 0; j < 4; ++j) p.arr[j] = G->arrays[4 * k + j];
+  return p;
+}
+
 int setup_level_on(ecmg_grid* G, int k, cudaStream_t st, int ctas_per_sm = 0) {
   const LevelGeom& g = G->geom[k];
-  const ElemStencil es = make_elem_stencil(g, G->prob, G->precond);
-  if (G->elem_path) ECMG_CUDA(launch_beta(g, G->prob, G->betal[k], st));
-  ECMG_CUDA(launch_rhs(g, G->prob, es, 1.0, G->elem_path ? G->betal[k] : nullptr, G->bl[k], G->s1d[k], st, ctas_per_sm));
+  const Problem pk = level_prob(G, k);
+  const ElemStencil es = make_elem_stencil(g, pk, G->precond);
+  if (G->elem_path) ECMG_CUDA(launch_beta(g, pk, G->betal[k], st));
+  ECMG_CUDA(launch_rhs(g, pk, es, 1.0, G->elem_path ? G->betal[k] : nullptr, G->bl[k], G->s1d[k], st, ctas_per_sm));
   G->setup_ok[k] = 1;
   return ECMG_OK;
 }
@@ -752,7 +762,21 @@ int ecmg_set_coeffs(ecmg_grid* G, const ecmg_problem* pr) {
   if (!G || !pr) return ECMG_EINVAL;
   Problem pb{};
   int need = 0;
-  if (!problem_faces(pr->problem_id, pb.face, pb.alpha, &need)) return ECMG_EINVAL;
+  bool arrays_beta = false;
+  if (pr->problem_id == ECMG_PROB_ARRAYS) {
+    // caller data per level: single grid only, alpha per face in params[0..5]
+    if (G->slab || G->nranks > 1) return ECMG_EINVAL;
+    if (!pr->level_arrays || pr->n_level_arrays != 4 * G->L || pr->n_params != 6 || !pr->params) return ECMG_EINVAL;
+    for (int f = 0; f < 6; ++f) {
+      if (pr->face[f] != ECMG_DIRICHLET && pr->face[f] != ECMG_ROBIN) return ECMG_EINVAL;
+      pb.face[f] = pr->face[f];
+      pb.alpha[f] = pr->face[f] == ECMG_ROBIN ? pr->params[f] : 0.0;
+      if (!(pr->params[f] >= 0.0)) return ECMG_EINVAL;   // alpha >= 0
+    }
+    arrays_beta = pr->level_arrays[0] != nullptr;
+    for (int k = 0; k < G->L; ++k)
+      if ((pr->level_arrays[4 * k] != nullptr) != arrays_beta) return ECMG_EINVAL;   // beta on every level or none
+  } else if (!problem_faces(pr->problem_id, pb.face, pb.alpha, &need)) return ECMG_EINVAL;
   for (int f = 0; f < 6; ++f)
     if ((int)pr->face[f] != pb.face[f]) return ECMG_EINVAL;
   if (pr->n_params < need || pr->n_params > kMaxParams || (need > 0 && !pr->params)) return ECMG_EINVAL;
@@ -769,7 +793,7 @@ int ecmg_set_coeffs(ecmg_grid* G, const ecmg_problem* pr) {
   for (int f = 0; f < 6; ++f) if (pb.alpha[f] < 0.0) return ECMG_EINVAL;   // alpha >= 0
   bool all_dir = true;
   for (int f = 0; f < 6; ++f) all_dir = all_dir && pb.face[f] == FACE_DIRICHLET;
-  const int elem_path = !(prob_beta_is_one(pb.id) && all_dir);
+  const int elem_path = pb.id == PROB_ARRAYS ? (arrays_beta || !all_dir) : !(prob_beta_is_one(pb.id) && all_dir);
   if (elem_path && !G->betal.back()) {
     const int size_level = G->size_level;
     int face_none[6] = {FACE_ROBIN, FACE_ROBIN, FACE_ROBIN, FACE_ROBIN, FACE_ROBIN, FACE_ROBIN};
@@ -784,6 +808,8 @@ int ecmg_set_coeffs(ecmg_grid* G, const ecmg_problem* pr) {
   }
   G->prob = pb;
   G->elem_path = elem_path;
+  if (pb.id == PROB_ARRAYS) G->arrays.assign(pr->level_arrays, pr->level_arrays + 4 * G->L);
+  else G->arrays.clear();
   G->geom.clear();
   for (int k = 0; k < G->L; ++k) G->geom.push_back(make_geom(G->dom, G->n0, k, pb.face, elem_path));
   G->has_problem = true;
@@ -815,7 +841,7 @@ int ecmg_set_option(ecmg_grid* G, int option, int value) {
     case ECMG_OPT_PDL: if (value != 0 && value != 1) return ECMG_EINVAL; G->pdl = value; clear_graphs(G); break;
     case ECMG_OPT_FUSED_HALO: if (value != 0 && value != 1) return ECMG_EINVAL; G->fused_halo = value; break;
     case ECMG_OPT_VIRTUAL_SLABS: {
-      if (value < 0 || value > 16 || G->nranks > 1) return ECMG_EINVAL;
+      if (value < 0 || value > 16 || G->nranks > 1 || (value > 1 && G->prob.id == PROB_ARRAYS)) return ECMG_EINVAL;
       if (G->slab) { slab_driver_destroy(G->slab); G->slab = nullptr; }
       G->virt_slabs = value > 1 ? value : 0;
       if (G->virt_slabs) {
@@ -859,7 +885,7 @@ int ecmg_solve_level(ecmg_grid* G, int level, double eps, int max_iter, double* 
   ECMG_CUDA(launch_gather(g, u, G->x, G->stream));
   const int st = run_jcg(G, level, eps, max_iter, u, stats);   // the true-residual pass fills u's free nodes
   if (st == ECMG_ECUDA || st == ECMG_ENOMEM) return st;
-  ECMG_CUDA(launch_dirichlet_fill(g, G->prob, u, 0.0, 0, G->stream));
+  ECMG_CUDA(launch_dirichlet_fill(g, level_prob(G, level), u, 0.0, 0, G->stream));
   ECMG_CUDA(cudaEventRecord(G->ev[6], G->stream));
   ECMG_CUDA(cudaStreamSynchronize(G->stream));
   if (stats) {
@@ -874,7 +900,7 @@ int ecmg_prolongate_extrapolate(ecmg_grid* G, int level, const double* u2h, cons
   if (!G || !u2h || !u4h || !w || !G->has_problem || level < 2 || level >= G->L || G->nranks > 1) return ECMG_EINVAL;
   const LevelGeom& g = G->geom[level];
   for (int d = 0; d < 3; ++d) if (g.n[d] % 4) return ECMG_EMISMATCH;
-  ECMG_CUDA(launch_exp_finite(g, G->prob, u2h, u4h, w, G->exp_variant, G->seeds, 0, G->stream, G->exp_fused));
+  ECMG_CUDA(launch_exp_finite(g, level_prob(G, level), u2h, u4h, w, G->exp_variant, G->seeds, 0, G->stream, G->exp_fused));
   ECMG_CUDA(cudaStreamSynchronize(G->stream));
   return ECMG_OK;
 }
@@ -883,7 +909,7 @@ int ecmg_richardson(ecmg_grid* G, int level, const double* uh, const double* u2h
   if (!G || !uh || !u2h || !ut || !G->has_problem || level < 1 || level >= G->L || G->nranks > 1) return ECMG_EINVAL;
   const LevelGeom& g = G->geom[level];
   for (int d = 0; d < 3; ++d) if (g.n[d] % 2) return ECMG_EMISMATCH;
-  ECMG_CUDA(launch_exp_true(g, G->prob, uh, u2h, ut, G->stream));
+  ECMG_CUDA(launch_exp_true(g, level_prob(G, level), uh, u2h, ut, G->stream));
   ECMG_CUDA(cudaStreamSynchronize(G->stream));
   return ECMG_OK;
 }
@@ -992,7 +1018,7 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
     cudaStream_t s_k = (k == L_run - 1 && G->setup_ahead != 2) ? (G->setup_ahead == 4 ? G->hi2_stream : G->lo2_stream)
                                                                : G->lo_stream;
     { int s = setup_level_on(G, k, s_k, G->setup_ctas); if (s) return s; }
-    ECMG_CUDA(launch_dirichlet_fill(G->geom[k], G->prob, level_u(k), 0.0, 0, s_k));
+    ECMG_CUDA(launch_dirichlet_fill(G->geom[k], level_prob(G, k), level_u(k), 0.0, 0, s_k));
     ECMG_CUDA(cudaEventRecord(G->setup_ev[k], s_k));
     return ECMG_OK;
   };
@@ -1031,7 +1057,7 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
       ECMG_CUDA(launch_zero_vec(g, G->x, G->stream));
     } else {
       // W_h = EXP_finite(u_2h, u_4h) (Alg. 4 l.6), written straight into the free-box work vector
-      ECMG_CUDA(launch_exp_finite(g, G->prob, G->u[k - 1], G->u[k - 2], G->x, G->exp_variant, G->seeds, 1, G->stream, G->exp_fused));
+      ECMG_CUDA(launch_exp_finite(g, level_prob(G, k), G->u[k - 1], G->u[k - 2], G->x, G->exp_variant, G->seeds, 1, G->stream, G->exp_fused));
     }
     ECMG_CUDA(cudaEventRecord(e[2], G->stream));
     const double eps_k = k < 2 ? 1e-14 : eps_lv[k];   // JCG from W_h (l.7-9)
@@ -1048,11 +1074,11 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
       if (s != ECMG_OK && status == ECMG_OK) status = s;
     }
     if (s == ECMG_ECUDA || s == ECMG_ENOMEM) return s;
-    if (!ahead) ECMG_CUDA(launch_dirichlet_fill(g, G->prob, uk, 0.0, 0, G->stream));
+    if (!ahead) ECMG_CUDA(launch_dirichlet_fill(g, level_prob(G, k), uk, 0.0, 0, G->stream));
     ECMG_CUDA(cudaEventRecord(e[3], G->stream));
     if (k >= 2 && k == G->L - 1 && ut_fine) {
       // u~_h = EXP_true(u_h, u_2h) (Alg. 4 l.10) on the finest level
-      ECMG_CUDA(launch_exp_true(g, G->prob, uk, G->u[k - 1], ut_dev ? ut_fine : G->ut_tmp, G->stream));
+      ECMG_CUDA(launch_exp_true(g, level_prob(G, k), uk, G->u[k - 1], ut_dev ? ut_fine : G->ut_tmp, G->stream));
     }
     ECMG_CUDA(cudaEventRecord(e[4], G->stream));
     if (ahead) { int s = setups_until(k + 2); if (s) return s; }

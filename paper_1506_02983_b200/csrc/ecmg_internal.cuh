@@ -29,7 +29,11 @@ struct Problem {
   double alpha[6];        // Robin alpha per face (0 = Neumann)
   double params[kMaxParams];
   int n_params;
+  // PROB_ARRAYS: the caller's device arrays of ONE level (beta_e, f at the Gauss points, g_D per node, g_R at
+  // the face Gauss points; layouts in include/ecmg.h), set per launch by the host (level_prob); null = 0 / 1
+  const double* arr[4];
 };
+constexpr int PROB_ARRAYS = 100;
 
 struct LevelGeom {
   int n[3];          // cells per axis

@@ -219,6 +219,7 @@ inline LevelGeom slab_geom(LevelGeom g, int P, int r, bool* sharded, int min_n =
 namespace ecmg {
 // element kernels form beta from the level's axis tables (analytic beta) instead of reading the array
 inline void set_beta_fly(ElemStencil& es, const LevelGeom& g, const Problem& pb, const double* beta) {
+  if (pb.id == PROB_ARRAYS) return;   // caller beta: no analytic axis tables, the kernels read the array
   es.bkind = beta_kind(pb.id);
   es.bw = beta_axes_w(g);
   es.baxes = beta_axes_ptr(g, beta);

@@ -33,7 +33,7 @@ namespace {
 
 // g_D at fine node (fx, fy, fz): kept out of line (boundary faces only) so the marching loops stay lean
 __device__ __noinline__ double gD_at(const LevelGeom& gf, const Problem& pb, int fx, int fy, int fz) {
-  return prob_gD(pb, gf.lo[0] + fx * gf.h[0], gf.lo[1] + fy * gf.h[1], gf.lo[2] + fz * gf.h[2]);
+  return prob_gD_node(pb, gf, fx, fy, fz);
 }
 
 // (1) extrapolated values at all 2h nodes of the fine level gf (2h grid: n/2 cells per axis)

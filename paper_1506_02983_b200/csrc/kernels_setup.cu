@@ -57,6 +57,19 @@ __global__ void k_beta(const LevelGeom g, double* __restrict__ beta, const doubl
   }
 }
 
+// PROB_ARRAYS: beta_e from the caller's element array (x fastest), 1 if absent, 0 on the ring
+__global__ void k_beta_arr(const LevelGeom g, double* __restrict__ beta, const double* __restrict__ be) {
+  const int e0 = max(-2, g.flo[2] + g.zoff - 2), e1 = min(g.n[2] + 1, g.flo[2] + g.zoff + g.nza);
+  const long long ne0 = g.n[0] + 4, ne1 = g.n[1] + 4, ne2 = e1 - e0 + 1;
+  const long long total = ne0 * ne1 * ne2;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    const int ex = (int)(t % ne0) - 2, ey = (int)((t / ne0) % ne1) - 2, ez = (int)(t / (ne0 * ne1)) + e0;
+    const bool in = ex >= 0 && ex < g.n[0] && ey >= 0 && ey < g.n[1] && ez >= 0 && ez < g.n[2];
+    const double v = !in ? 0.0 : (be ? be[(long long)ex + g.n[0] * ((long long)ey + (long long)g.n[1] * ez)] : 1.0);
+    beta[(long long)(ez + 2) * g.BS + (long long)(ey + 2) * g.BP + (ex + 2)] = v;
+  }
+}
+
 // ---- right-hand side ---------------------------------------------------------------------------
 // b_f = F_f + G_f - A_fD g_D (§8c A2/A4/A5) in up to three passes:
 //  (1) volume load F by 2x2x2 Gauss. Separable f = sum_k A_k g_k^x(x) g_k^y(y) g_k^z(z) (rank 1: C1, C2,
@@ -180,7 +193,10 @@ __global__ void __launch_bounds__(VNTH, 3) k_rhs_vol(const LevelGeom g, const Pr
       const int q = t / VNE, e = t - q * VNE;
       const int gex = g.flo[0] + X0 - 1 + e % VEX, gey = g.flo[1] + Y0 - 1 + e / VEX;
       double v = 0.0;
-      if (gex >= 0 && gex < g.n[0] && gey >= 0 && gey < g.n[1] && gez >= 0 && gez < g.n[2]) {
+      if (PID == PROB_ARRAYS) {   // the caller's f at Gauss point q of the element
+        if (gex >= 0 && gex < g.n[0] && gey >= 0 && gey < g.n[1] && gez >= 0 && gez < g.n[2] && pb.arr[1])
+          v = pb.arr[1][8 * ((long long)gex + g.n[0] * ((long long)gey + (long long)g.n[1] * gez)) + q];
+      } else if (gex >= 0 && gex < g.n[0] && gey >= 0 && gey < g.n[1] && gez >= 0 && gez < g.n[2]) {
         const double xi = (q & 1) ? kGauss : -kGauss, eta = (q & 2) ? kGauss : -kGauss, ze = (q & 4) ? kGauss : -kGauss;
         v = f_at<PID>(pb, g.lo[0] + (gex + (1.0 + xi) / 2.0) * g.h[0], g.lo[1] + (gey + (1.0 + eta) / 2.0) * g.h[1],
                       g.lo[2] + (gez + (1.0 + ze) / 2.0) * g.h[2]);
@@ -365,6 +381,11 @@ __global__ void k_rhs_shell(const LevelGeom g, const Problem pb, const ElemStenc
     if (gi[dF] != ((F & 1) ? g.n[dF] : 0)) continue;
     const int e1d = (dF == 0) ? 1 : 0, e2d = (dF == 2) ? 1 : 2;
     const double hh = g.h[e1d] * g.h[e2d] / 4.0;
+    long long gR_block = 0;   // PROB_ARRAYS: this face's block of g_R values (faces in order, 4 n_d1 n_d2 each)
+    for (int F2 = 0; F2 < F; ++F2) {
+      const int a = F2 >> 1;
+      gR_block += 4LL * g.n[(a == 0) ? 1 : 0] * g.n[(a == 2) ? 1 : 2];
+    }
     for (int e2 = -1; e2 <= 0; ++e2)
       for (int e1 = -1; e1 <= 0; ++e1) {
         const int f1 = gi[e1d] + e1, f2 = gi[e2d] + e2;
@@ -376,7 +397,10 @@ __global__ void k_rhs_shell(const LevelGeom g, const Problem pb, const ElemStenc
           xq[e1d] = g.lo[e1d] + (f1 + (1.0 + xi1) / 2.0) * g.h[e1d];
           xq[e2d] = g.lo[e2d] + (f2 + (1.0 + xi2) / 2.0) * g.h[e2d];
           const double N = ((1.0 + (e1 ? xi1 : -xi1)) / 2.0) * ((1.0 + (e2 ? xi2 : -xi2)) / 2.0);
-          v += prob_gR(pb, F, xq[0], xq[1], xq[2]) * N * hh;
+          const double gR = pb.id == PROB_ARRAYS
+                                ? (pb.arr[3] ? pb.arr[3][gR_block + 4LL * (f1 + (long long)g.n[e1d] * f2) + q] : 0.0)
+                                : prob_gR(pb, F, xq[0], xq[1], xq[2]);
+          v += gR * N * hh;
         }
       }
   }
@@ -393,7 +417,7 @@ __global__ void k_rhs_shell(const LevelGeom g, const Problem pb, const ElemStenc
       const bool jfree = jx >= g.flo[0] && jx < g.flo[0] + g.nf[0] && jy >= g.flo[1] && jy < g.flo[1] + g.nf[1] &&
                          jz >= g.flo[2] && jz < g.flo[2] + g.nf[2];
       if (jfree) continue;
-      const double gD = prob_gD(pb, g.lo[0] + jx * g.h[0], g.lo[1] + jy * g.h[1], g.lo[2] + jz * g.h[2]);
+      const double gD = prob_gD_node(pb, g, jx, jy, jz);
       const int pat = ((ex + bx) != 1 ? 1 : 0) | ((ey + by) != 1 ? 2 : 0) | ((ez + bz) != 1 ? 4 : 0);
       sub += be * es.kappa[pat] * gD;
       // Robin face mass between this node and the Dirichlet node j on a common Robin face
@@ -448,7 +472,7 @@ __global__ void k_dirichlet_face(const LevelGeom g, const Problem pb, double* __
   gi[d2] = i2;
   if (gi[2] < g.zlo || gi[2] >= g.zhi) return;   // only this rank's planes
   const long long nx = g.n[0] + 1, ny = g.n[1] + 1;
-  const double v = zero ? 0.0 : prob_gD(pb, g.lo[0] + gi[0] * g.h[0], g.lo[1] + gi[1] * g.h[1], g.lo[2] + gi[2] * g.h[2]);
+  const double v = zero ? 0.0 : prob_gD_node(pb, g, gi[0], gi[1], gi[2]);
   u[(long long)gi[0] + nx * ((long long)gi[1] + ny * gi[2])] = v;
 }
 
@@ -462,6 +486,12 @@ __global__ void k_zero_free(const LevelGeom g, double* __restrict__ v) {
 
 // beta array of the level and, behind it, the per-axis tables it is formed from (beta_combine)
 cudaError_t launch_beta(const LevelGeom& g, const Problem& pb, double* beta, cudaStream_t st) {
+  if (pb.id == PROB_ARRAYS) {
+    const long long total = (long long)(g.n[0] + 4) * (g.n[1] + 4) * (g.n[2] + 4);
+    count_launch();
+    k_beta_arr<<<(int)std::min<long long>((total + 255) / 256, 148LL * 32), 256, 0, st>>>(g, beta, pb.arr[0]);
+    return cudaGetLastError();
+  }
   const int W = beta_axes_w(g), kind = beta_kind(pb.id);
   double* tab = beta + g.BS * (g.n[2] + 4);
   count_launch();
@@ -475,6 +505,7 @@ cudaError_t launch_beta(const LevelGeom& g, const Problem& pb, double* beta, cud
 
 cudaError_t init_setup_kernel_attributes() {
   cudaError_t e = cudaFuncSetAttribute(k_rhs_vol<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, VSMEM);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_rhs_vol<PROB_ARRAYS>, cudaFuncAttributeMaxDynamicSharedMemorySize, VSMEM);
   return e;
 }
 
@@ -520,6 +551,7 @@ cudaError_t launch_rhs(const LevelGeom& g, const Problem& pb, const ElemStencil&
       }
       k_rhs_c4<<<nblk, C4NTH, 0, st>>>(g, b, zc, k, (int)grid.x, (int)grid.y, items);
     }
+    else if (pb.id == PROB_ARRAYS) k_rhs_vol<PROB_ARRAYS><<<grid, dim3(32, 8), VSMEM, st>>>(g, pb, b, zc);
     else k_rhs_vol<0><<<grid, dim3(32, 8), VSMEM, st>>>(g, pb, b, zc);
   }
   const int m = std::max(g.nf[0], std::max(g.nf[1], g.nf[2]));

@@ -95,6 +95,13 @@ __host__ __device__ inline double prob_gD(const Problem& P, double x, double y, 
   return prob_exact(P, x, y, z);
 }
 
+// g_D at global node (ix, iy, iz) of level g: the caller's nodal array (PROB_ARRAYS) or the registry's g_D
+__device__ inline double prob_gD_node(const Problem& P, const LevelGeom& g, int ix, int iy, int iz) {
+  if (P.id == PROB_ARRAYS)
+    return P.arr[2] ? P.arr[2][(long long)ix + (g.n[0] + 1LL) * ((long long)iy + (g.n[1] + 1LL) * iz)] : 0.0;
+  return prob_gD(P, g.lo[0] + ix * g.h[0], g.lo[1] + iy * g.h[1], g.lo[2] + iz * g.h[2]);
+}
+
 // Robin data g_R = alpha u + beta du/dn on face `face`
 __host__ __device__ inline double prob_gR(const Problem& P, int face, double x, double y, double z) {
   switch (P.id) {

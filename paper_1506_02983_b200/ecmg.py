@@ -19,7 +19,8 @@ LIB_PATH = os.path.join(HERE, "libecmg.so")
 OK, EINVAL, ENOMEM, ENOTCONV, EBREAKDOWN, EDIAG, EMISMATCH, ECUDA, ENCCL = 0, -1, -2, -3, -4, -5, -6, -7, -8
 DIRICHLET, ROBIN = 0, 1
 PROB = dict(C1=1, C2=2, C3=3, C4=4, C5=5, P1=11, P2=12, P3=13,
-            PATCH_TRILINEAR=21, PATCH_LAYERED=22, PATCH_ROBIN=23, CONST_F=24, PATCH_ROBIN_XY=25)
+            PATCH_TRILINEAR=21, PATCH_LAYERED=22, PATCH_ROBIN=23, CONST_F=24, PATCH_ROBIN_XY=25,
+            ARRAYS=100)
 OPT_EXP_VARIANT, OPT_PRECOND, OPT_ZCHUNK, OPT_KERNEL, OPT_GRAPH, OPT_VIRTUAL_SLABS, OPT_PERSISTENT, OPT_PDL = 1, 2, 3, 4, 5, 6, 7, 8
 OPT_FUSED_HALO = 9
 OPT_SETUP_AHEAD = 10
@@ -48,7 +49,8 @@ class ecmg_dist(C.Structure):
 
 class ecmg_problem(C.Structure):
     _fields_ = [("face", C.c_int * 6), ("problem_id", C.c_int), ("params", C.POINTER(C.c_double)),
-                ("n_params", C.c_int)]
+                ("n_params", C.c_int), ("level_arrays", C.POINTER(C.POINTER(C.c_double))),
+                ("n_level_arrays", C.c_int)]
 
 
 class ecmg_stats(C.Structure):
@@ -130,7 +132,9 @@ def create_grid(lo, hi, coarsest_cells, num_levels, stream=None, dist=None):
     return st, out
 
 
-def set_coeffs(grid, problem_id, faces, params=None):
+def set_coeffs(grid, problem_id, faces, params=None, level_arrays=None):
+    """level_arrays (ECMG_PROB_ARRAYS): 4 device arrays (or None) per level, flattened in level order; the
+    library keeps the pointers, the caller keeps the arrays alive (include/ecmg.h)."""
     pr = ecmg_problem()
     for i, f in enumerate(faces):
         pr.face[i] = int(f)
@@ -140,6 +144,12 @@ def set_coeffs(grid, problem_id, faces, params=None):
         keep = (C.c_double * len(params))(*[float(v) for v in params])
         pr.params = C.cast(keep, C.POINTER(C.c_double))
         pr.n_params = len(params)
+    if level_arrays is not None:
+        dp = C.POINTER(C.c_double)
+        arr = (dp * len(level_arrays))(*[C.cast(_ptr(a), dp) if a is not None else dp()
+                                         for a in level_arrays])
+        pr.level_arrays = C.cast(arr, C.POINTER(dp))
+        pr.n_level_arrays = len(level_arrays)
     return lib().ecmg_set_coeffs(grid, C.byref(pr))
 
 
@@ -247,7 +257,7 @@ class Grid:
     """Owning wrapper: Grid(coarsest, levels, problem_id, params) on the current torch stream."""
 
     def __init__(self, coarsest, num_levels, problem_id, params=None, lo=(0.0, 0.0, 0.0), hi=(1.0, 1.0, 1.0),
-                 stream=None, exp_variant=0, precond=True, dist=None):
+                 stream=None, exp_variant=0, precond=True, dist=None, faces=None, level_arrays=None):
         import torch
         if stream is None:
             stream = torch.cuda.current_stream().cuda_stream
@@ -256,7 +266,10 @@ class Grid:
         st, self.h = create_grid(lo, hi, coarsest, num_levels, stream, dist)
         if st != OK:
             raise EcmgError(st, "ecmg_create_grid")
-        self._check(set_coeffs(self.h, problem_id, default_faces(problem_id), params), "ecmg_set_coeffs")
+        # ARRAYS: level_arrays[k] = (beta_e, f_q, gD, gR) device float64 tensors (or None), kept alive here
+        self._arrays = [a for lv in level_arrays for a in lv] if level_arrays is not None else None
+        self._check(set_coeffs(self.h, problem_id, faces if faces is not None else default_faces(problem_id), params,
+                               self._arrays), "ecmg_set_coeffs")
         self._check(set_option(self.h, OPT_EXP_VARIANT, exp_variant), "ecmg_set_option")
         self._check(set_option(self.h, OPT_PRECOND, 1 if precond else 0), "ecmg_set_option")
 

@@ -1,0 +1,129 @@
+"""ECMG_PROB_ARRAYS (the caller's beta_e, f at the Gauss points, g_D per node and g_R at the
+face Gauss points, per level) through the C ABI against the oracle's ARRAYS problem (pinned in
+test_oracle_arrays.py), on seeded random data (synth.random_problem_arrays): lifted right-hand side and
+operator 1e-13, Alg. 4 iterations +-1 and u, u~ within 1e-9 ||u||_inf (the tolerances of
+test_gpu_parity.py). Cases: the element path (random beta, Robin faces with four alphas, a Neumann face),
+all-Dirichlet with beta (element path), all-Dirichlet without beta (constant-stencil path); box cells with
+free boxes spanning several 32-wide tiles and ragged tails. Also: C3's data sampled into arrays gives the
+registry C3's right-hand side on the GPU, and a run is bitwise reproducible."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as o
+import synth
+from arrays_data import C3_ALPHA, C3_FACES, c3_arrays
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_1506_02983_b200 import Grid, PROB
+
+
+def rel(a, b):
+    return np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300)
+
+
+def dev(a):
+    return None if a is None else torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+CASES = {
+    "robin": ([1, 1, 1, 1, 0, 0], [2.0, 0.5, 1.5, 3.0, 0.0, 0.0], True),
+    "neumann_z": ([0, 0, 0, 1, 0, 1], [0.0, 0.0, 0.0, 0.7, 0.0, 0.0], True),
+    "dirichlet_beta": ([0] * 6, [0.0] * 6, True),
+    "dirichlet_const": ([0] * 6, [0.0] * 6, False),
+}
+
+
+def level_data(n0, levels, with_beta, seed=40):
+    return [synth.random_problem_arrays(seed + k, tuple(c << k for c in n0), beta=with_beta) for k in range(levels)]
+
+
+def make(n0, levels, case, data):
+    faces, alpha, _ = CASES[case]
+    dv = [tuple(dev(a) for a in lv) for lv in data]
+    g = Grid(n0, levels, PROB["ARRAYS"], params=alpha, faces=faces, level_arrays=dv)
+    return g, dv
+
+
+@pytest.mark.parametrize("case", list(CASES))
+def test_arrays_rhs_and_operator(case):
+    n0, levels = (5, 3, 4), 4          # finest 40 x 24 x 32 cells
+    faces, alpha, wb = CASES[case]
+    data = level_data(n0, levels, wb)
+    g, _ = make(n0, levels, case, data)
+    for k in (2, 3):
+        n = tuple(c << k for c in n0)
+        L = o.Level.from_arrays(n, faces, alpha, *data[k])
+        free = L.dirichlet()[0] == 0
+        b = g.new_vec(k)
+        g.level_rhs(k, b)
+        bo, _ = L.rhs()
+        assert rel(host(b)[free], bo[free]) <= 1e-13
+        p = np.where(free, synth.random_nodal(11, n), 0.0)
+        q = g.new_vec(k)
+        g.apply_operator(k, dev(p), q)
+        assert rel(host(q)[free], L.apply(p)[free]) <= 1e-13
+    g.close()
+
+
+@pytest.mark.parametrize("case", list(CASES))
+def test_arrays_ecmg_run(case):
+    n0, levels, eps = (5, 3, 4), 4, 1e-10
+    faces, alpha, wb = CASES[case]
+    data = level_data(n0, levels, wb, seed=60)
+    g, _ = make(n0, levels, case, data)
+    u, ut = g.new_vec(levels - 1), g.new_vec(levels - 1)
+    st, stats = g.run(eps, u, ut)
+    ost, ostats, ou, out = o.ecmg_arrays(n0, levels, faces, alpha, data, eps)
+    assert st == 0 and ost == 0
+    it_g = [s["iterations"] for s in stats[2:]]
+    it_o = [int(v) for v in ostats[2:, 0]]
+    assert all(abs(a - b) <= 1 for a, b in zip(it_g, it_o)), (it_g, it_o)
+    assert np.max(np.abs(host(u) - ou)) <= 1e-9 * np.max(np.abs(ou))
+    assert np.max(np.abs(host(ut) - out)) <= 1e-9 * np.max(np.abs(out))
+    # bitwise reproducible
+    u2, ut2 = g.new_vec(levels - 1), g.new_vec(levels - 1)
+    g.run(eps, u2, ut2)
+    assert torch.equal(u, u2) and torch.equal(ut, ut2)
+    g.close()
+
+
+def test_arrays_sampled_c3_equals_registry():
+    n0, levels = (4, 4, 4), 5           # finest 64^3
+    data = [c3_arrays((4 << k,) * 3) for k in range(levels)]
+    dv = [tuple(dev(a) for a in lv) for lv in data]
+    ga = Grid(n0, levels, PROB["ARRAYS"], params=C3_ALPHA, faces=C3_FACES, level_arrays=dv)
+    gr = Grid(n0, levels, PROB["C3"])
+    k = levels - 1
+    ba, br = ga.new_vec(k), gr.new_vec(k)
+    ga.level_rhs(k, ba)
+    gr.level_rhs(k, br)
+    assert rel(host(ba), host(br)) <= 1e-13
+    ua, ur = ga.new_vec(k), gr.new_vec(k)
+    sa, st_a = ga.run(1e-10, ua)
+    sr, st_r = gr.run(1e-10, ur)
+    assert sa == 0 and sr == 0
+    assert [s["iterations"] for s in st_a] == [s["iterations"] for s in st_r]
+    assert rel(host(ua), host(ur)) <= 1e-11
+    ga.close()
+    gr.close()
+
+
+def test_arrays_rejects():
+    from paper_1506_02983_b200 import ecmg
+    data = level_data((4, 4, 4), 3, True)
+    dv = [tuple(dev(a) for a in lv) for lv in data]
+    with pytest.raises(ecmg.EcmgError):      # alpha < 0
+        Grid(4, 3, PROB["ARRAYS"], params=[-1.0, 0, 0, 0, 0, 0], faces=[1, 0, 0, 0, 0, 0], level_arrays=dv)
+    with pytest.raises(ecmg.EcmgError):      # beta on some levels only
+        dv2 = [dv[0], (None,) + dv[1][1:], dv[2]]
+        Grid(4, 3, PROB["ARRAYS"], params=[0.0] * 6, faces=[0] * 6, level_arrays=dv2)
+    with pytest.raises(ecmg.EcmgError):      # wrong number of arrays
+        Grid(4, 3, PROB["ARRAYS"], params=[0.0] * 6, faces=[0] * 6, level_arrays=dv[:2])
