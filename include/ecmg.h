@@ -101,7 +101,7 @@ typedef struct {
    *                   Robin faces only; NULL = 0
    * The grid keeps the pointers: the arrays are read by every call that runs a level's setup or a
    * Dirichlet fill (ecmg_run, ecmg_run_fixed, ecmg_solve_level, ecmg_level_rhs, the EXP calls) and must stay
-   * valid and unchanged until the next ecmg_set_coeffs or ecmg_destroy_grid (reading R8).
+   * valid and unchanged until the next ecmg_set_coeffs or ecmg_destroy_grid (reading R6).
    * Single GPU only (ECMG_EINVAL with dist / virtual slabs). */
   const double* const* level_arrays;
   int n_level_arrays;

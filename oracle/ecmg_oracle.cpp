@@ -54,7 +54,7 @@ enum {
   PROB_P1 = 11, PROB_P2 = 12, PROB_P3 = 13,
   PROB_PATCH_TRILINEAR = 21, PROB_PATCH_LAYERED = 22, PROB_PATCH_ROBIN = 23, PROB_CONST_F = 24,
   PROB_PATCH_ROBIN_XY = 25,
-  PROB_ARRAYS = 100,   // caller data per level (SURVEY.md §8b ECMG_PROB_ARRAYS; reading R8)
+  PROB_ARRAYS = 100,   // caller data per level (SURVEY.md §8b ECMG_PROB_ARRAYS; reading R6)
 };
 
 const double PI = 3.14159265358979323846;
