@@ -173,7 +173,10 @@ constexpr int S2X = 2 * XB + 1, S2Y = 2 * YB + 1;              // 2h nodes per t
 constexpr int FNTH = 256;
 
 template <bool FREEBOX>
-__global__ void __launch_bounds__(FNTH, 3) k_exp_fused(const LevelGeom gf, const Problem pb, const double* __restrict__ u2h,
+#ifndef EXP_FUSED_MINB
+#define EXP_FUSED_MINB 3
+#endif
+__global__ void __launch_bounds__(FNTH, EXP_FUSED_MINB) k_exp_fused(const LevelGeom gf, const Problem pb, const double* __restrict__ u2h,
                                                        const double* __restrict__ u4h, double* __restrict__ out, int variant,
                                                        int F0, int F1, int bzA, int lchunk) {
   __shared__ double U1s[3][S2Y][S2X];          // u_2h on 2h planes 2bz .. 2bz+2
@@ -392,7 +395,10 @@ __global__ void __launch_bounds__(FNTH, 3) k_exp_fused(const LevelGeom gf, const
 // Dirichlet nodes take g_D (A15).
 constexpr int ETX = 64, ETY = 8, EDX = ETX / 2 + 1, EDY = ETY / 2 + 1;   // 33 x 5 corner values per plane
 
-__global__ void __launch_bounds__(256) k_exp_true(const LevelGeom gf, const Problem pb, const double* __restrict__ uh,
+#ifndef EXP_TRUE_MINB
+#define EXP_TRUE_MINB 1
+#endif
+__global__ void __launch_bounds__(256, EXP_TRUE_MINB) k_exp_true(const LevelGeom gf, const Problem pb, const double* __restrict__ uh,
                                                   const double* __restrict__ u2h, double* __restrict__ ut, int c0,
                                                   int cchunk, double third) {
   __shared__ double D[2][EDY][EDX];     // corner differences of 2h plane K (slot K & 1)
