@@ -174,7 +174,7 @@ constexpr int FNTH = 256;
 
 template <bool FREEBOX>
 #ifndef EXP_FUSED_MINB
-#define EXP_FUSED_MINB 3
+#define EXP_FUSED_MINB 3   // 4 (64 registers): 0.54 -> 0.61 ms inside ecmg_run at 512^3
 #endif
 __global__ void __launch_bounds__(FNTH, EXP_FUSED_MINB) k_exp_fused(const LevelGeom gf, const Problem pb, const double* __restrict__ u2h,
                                                        const double* __restrict__ u4h, double* __restrict__ out, int variant,
@@ -395,10 +395,9 @@ __global__ void __launch_bounds__(FNTH, EXP_FUSED_MINB) k_exp_fused(const LevelG
 // Dirichlet nodes take g_D (A15).
 constexpr int ETX = 64, ETY = 8, EDX = ETX / 2 + 1, EDY = ETY / 2 + 1;   // 33 x 5 corner values per plane
 
-#ifndef EXP_TRUE_MINB
-#define EXP_TRUE_MINB 1
-#endif
-__global__ void __launch_bounds__(256, EXP_TRUE_MINB) k_exp_true(const LevelGeom gf, const Problem pb, const double* __restrict__ uh,
+// no min-blocks hint: ptxas picks 72 registers (3 CTAs / SM); measured at 512^3: hint 1 -> 102 registers,
+// 0.71 ms; hint 3 -> 80, 0.60 ms; hint 4 -> 64, 0.67 ms; none 0.60 ms
+__global__ void __launch_bounds__(256) k_exp_true(const LevelGeom gf, const Problem pb, const double* __restrict__ uh,
                                                   const double* __restrict__ u2h, double* __restrict__ ut, int c0,
                                                   int cchunk, double third) {
   __shared__ double D[2][EDY][EDX];     // corner differences of 2h plane K (slot K & 1)
