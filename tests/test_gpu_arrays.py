@@ -127,3 +127,21 @@ def test_arrays_rejects():
         Grid(4, 3, PROB["ARRAYS"], params=[0.0] * 6, faces=[0] * 6, level_arrays=dv2)
     with pytest.raises(ecmg.EcmgError):      # wrong number of arrays
         Grid(4, 3, PROB["ARRAYS"], params=[0.0] * 6, faces=[0] * 6, level_arrays=dv[:2])
+
+
+def test_arrays_setup_ahead_bitwise_and_slabs_rejected():
+    from paper_1506_02983_b200 import ecmg
+    n0, levels = (5, 3, 4), 4
+    data = level_data(n0, levels, True, seed=80)
+    g, _ = make(n0, levels, "robin", data)
+    outs = []
+    for ahead in (1, 0):
+        g.set_option(ecmg.OPT_SETUP_AHEAD, ahead)
+        u, ut = g.new_vec(levels - 1), g.new_vec(levels - 1)
+        st, _ = g.run(1e-10, u, ut)
+        assert st == 0
+        outs.append((u, ut))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    # the z-slab driver does not take caller arrays
+    assert ecmg.set_option(g.h, ecmg.OPT_VIRTUAL_SLABS, 2) == ecmg.EINVAL
+    g.close()
