@@ -1,6 +1,7 @@
 """Parity at BASELINE.json's full sizes, in the launch configuration bench.py times: C4 (configs[3],
-4^3 -> 512^3, the default bench line; constant-stencil TMA kernels) and C3 (configs[2], 256^3; element-beta
-kernels with a Robin face). The assembled oracle does not fit in host memory at these sizes, so outputs are
+4^3 -> 512^3, the default bench line; constant-stencil TMA kernels), C3 (configs[2], 256^3; element-beta
+kernels with a Robin face) and C5 (configs[4], 1024^3, layered geology: right-hand side, EXP_finite, operator,
+one JCG iteration). The assembled oracle does not fit in host memory at these sizes, so outputs are
 sampled (random nodes plus the domain faces and the 32-wide tile seams of the kernels) and the oracle
 computes them one row / node at a time (oracle.rows, oracle.exp_nodes: pinned bitwise to the assembled
 oracle in test_oracle_rows.py). Where an output depends on global sums (a CG step, a whole solve), the
@@ -179,3 +180,50 @@ def test_fullsize_orders():
     assert 1.8 <= np.log2(eu2 / eu1) <= 2.2, rms
     assert np.log2(et2 / et1) >= 2.6, rms
     assert et1 < 0.05 * eu1, rms
+
+
+def test_fullsize_c5():
+    # C5 (configs[4], layered geology, 4^3 -> 1024^3, element beta): the finest right-hand side, EXP_finite,
+    # the operator and one JCG iteration on sampled nodes against the oracle's one-row / one-node evaluations
+    pid, levels = o.C5, 9
+    n = (1024,) * 3
+    prm = synth.c5_geometry(0)
+    g = Grid(4, levels, pid, prm)
+    nodes = sample_nodes(n, 2000, 9)
+    idx = lin(n, nodes)
+    b = g.new_vec(levels - 1)
+    g.level_rhs(levels - 1, b)
+    _, bo = o.rows(n, pid, nodes, params=prm)
+    assert rel(host_at(b, idx), bo) <= 1e-13
+    del b
+    n2, n4 = tuple(c // 2 for c in n), tuple(c // 4 for c in n)
+    u2, u4 = synth.random_nodal(13, n2), synth.random_nodal(12, n4)
+    w = g.new_vec(levels - 1)
+    g.prolongate_extrapolate(levels - 1, dev(u2), dev(u4), w)
+    wo = o.exp_nodes(n, pid, 0, u2, u4, nodes, params=prm)
+    assert rel(host_at(w, idx), wo) <= 1e-14
+    del w, u2, u4
+    # the element operator and one JCG iteration at 1024^3 (the bench's --config c5 kernels), if the host
+    # can hold the seeded 8.6 GB input and its generator's temporaries
+    import psutil
+    if psutil.virtual_memory().available >= 96 << 30:
+        p = synth.random_nodal(11, n)
+        q = g.new_vec(levels - 1)
+        g.apply_operator(levels - 1, dev(p), q)
+        qo, _ = o.rows(n, pid, nodes, p, params=prm)
+        assert rel(host_at(q, idx), qo) <= 1e-13
+        del q
+        x = dev(p)
+        st, s = g.solve_level(levels - 1, 0.0, 1, x)
+        assert st == 0 and s["iterations"] == 1
+        ax, bb, dg = o.rows(n, pid, nodes, p, params=prm, diag=True)
+        free = dg > 0
+        p0 = (bb[free] - ax[free]) / dg[free]
+        dx = host_at(x, idx)[free] - p[idx][free]
+        big = np.abs(p0) >= 1e-2 * np.max(np.abs(p0))
+        alpha = dx[big] / p0[big]
+        a0 = np.median(alpha)
+        assert alpha.size > 100 and np.max(np.abs(alpha - a0)) <= 1e-10 * abs(a0)
+        del x, p
+    g.close()
+    torch.cuda.empty_cache()
