@@ -1,7 +1,7 @@
 """Parity at BASELINE.json's full sizes, in the launch configuration bench.py times: C4 (configs[3],
 4^3 -> 512^3, the default bench line; constant-stencil TMA kernels), C3 (configs[2], 256^3; element-beta
 kernels with a Robin face) and C5 (configs[4], 1024^3, layered geology: right-hand side, EXP_finite, operator,
-one JCG iteration). The assembled oracle does not fit in host memory at these sizes, so outputs are
+one JCG iteration, EXP_true). The assembled oracle does not fit in host memory at these sizes, so outputs are
 sampled (random nodes plus the domain faces and the 32-wide tile seams of the kernels) and the oracle
 computes them one row / node at a time (oracle.rows, oracle.exp_nodes: pinned bitwise to the assembled
 oracle in test_oracle_rows.py). Where an output depends on global sums (a CG step, a whole solve), the
@@ -184,7 +184,7 @@ def test_fullsize_orders():
 
 def test_fullsize_c5():
     # C5 (configs[4], layered geology, 4^3 -> 1024^3, element beta): the finest right-hand side, EXP_finite,
-    # the operator and one JCG iteration on sampled nodes against the oracle's one-row / one-node evaluations
+    # the operator, one JCG iteration and EXP_true on sampled nodes against the oracle's one-row / one-node evaluations
     pid, levels = o.C5, 9
     n = (1024,) * 3
     prm = synth.c5_geometry(0)
@@ -224,6 +224,12 @@ def test_fullsize_c5():
         alpha = dx[big] / p0[big]
         a0 = np.median(alpha)
         assert alpha.size > 100 and np.max(np.abs(alpha - a0)) <= 1e-10 * abs(a0)
-        del x, p
+        del x
+        u2 = synth.random_nodal(13, n2)
+        ut = g.new_vec(levels - 1)
+        g.richardson(levels - 1, dev(p), dev(u2), ut)
+        uto = o.exp_nodes(n, pid, 2, p, u2, nodes, params=prm)
+        assert rel(host_at(ut, idx), uto) <= 1e-14
+        del ut, u2, p
     g.close()
     torch.cuda.empty_cache()
