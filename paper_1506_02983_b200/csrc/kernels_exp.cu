@@ -464,15 +464,13 @@ __global__ void __launch_bounds__(256) k_exp_true(const LevelGeom gf, const Prob
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  // free (x, y) flags of the thread's two nodes; the plane decides the rest
-  const bool yf = fy >= gf.flo[1] && fy < gf.flo[1] + gf.nf[1];
-  const bool xyfA = yf && fxa >= gf.flo[0] && fxa < gf.flo[0] + gf.nf[0];
-  const bool xyfB = yf && fxb >= gf.flo[0] && fxb < gf.flo[0] + gf.nf[0];
-  auto put = [&](int fz, double ua, double ub, double ia_, double ib_) {   // u~ on plane fz, this thread's nodes
+  // u~ on plane fz at this thread's nodes, every node by the formula: the Dirichlet nodes are overwritten with
+  // g_D by the face kernel launched after this one (launch_exp_true), which keeps the rare g_D evaluation
+  // (an out-of-line call with its stack frame) out of this loop
+  auto put = [&](int fz, double ua, double ub, double ia_, double ib_) {
     const long long row = (long long)fz * pl + rowoff;
-    const bool zf = fz >= gf.flo[2] && fz < gf.flo[2] + gf.nf[2];
-    if (okA) ut[row + fxa] = (zf && xyfA) ? __fma_rn(ia_, third, ua) : gD_at(gf, pb, fxa, fy, fz);
-    if (okB) ut[row + fxb] = (zf && xyfB) ? __fma_rn(ib_, third, ub) : gD_at(gf, pb, fxb, fy, fz);
+    if (okA) ut[row + fxa] = __fma_rn(ia_, third, ua);
+    if (okB) ut[row + fxb] = __fma_rn(ib_, third, ub);
   };
   double dh, d2, pa = 0.0, pb_ = 0.0;   // pa, pb_: plane K-1's interpolated d at the thread's nodes
   load_d(Ca, dh, d2);
@@ -542,7 +540,9 @@ cudaError_t launch_exp_true(const LevelGeom& gf, const Problem& pb, const double
   dim3 grid((gf.n[0] + 1 + ETX - 1) / ETX, (gf.n[1] + 1 + ETY - 1) / ETY, (c1 - c0 + cchunk - 1) / cchunk);
   count_launch();
   k_exp_true<<<grid, dim3(32, 8), 0, st>>>(gf, pb, uh, u2h, ut, c0, cchunk, 1.0 / 3.0);
-  return cudaGetLastError();
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return launch_dirichlet_fill(gf, pb, ut, 0.0, 0, st);   // Dirichlet overwrite (§8c A15): u~ = g_D there
 }
 
 }  // namespace ecmg
