@@ -23,18 +23,14 @@
 // Eq. (t1) at 2h nodes, Eq. (chenlin) at 2h edge centres and the mean of Eq. (chenlin) over the
 // 2 face diagonals / 4 space diagonals at face / cell centres (reading §8c A13; derived identity,
 // DESIGN.md). A z-march over 64 x 8 fine tiles (coalesced rows) with the corner differences of two 2h
-// planes in shared memory. Dirichlet nodes take g_D.
+// planes in shared memory. Dirichlet nodes take g_D (A15) from the face kernel launched after the full-layout
+// outputs (launch_dirichlet_fill), so that no g_D evaluation sits in the marching loops.
 #include <algorithm>
 #include "ecmg_internal.cuh"
 #include "problems.cuh"
 
 namespace ecmg {
 namespace {
-
-// g_D at fine node (fx, fy, fz): kept out of line (boundary faces only) so the marching loops stay lean
-__device__ __noinline__ double gD_at(const LevelGeom& gf, const Problem& pb, int fx, int fy, int fz) {
-  return prob_gD_node(pb, gf, fx, fy, fz);
-}
 
 // (1) extrapolated values at all 2h nodes of the fine level gf (2h grid: n/2 cells per axis)
 __global__ void k_exp_seeds(const LevelGeom gf, const double* __restrict__ u2h, const double* __restrict__ u4h,
@@ -152,8 +148,7 @@ __global__ void __launch_bounds__(64) k_exp_interp(const LevelGeom gf, const Pro
       if (FREEBOX) {
         if (fr) out[(long long)(fz - gf.flo[2] - gf.zoff) * gf.S + (long long)(fy - gf.flo[1]) * gf.P + (fx - gf.flo[0])] = W;
       } else {
-        if (!fr) W = gD_at(gf, pb, fx, fy, fz);
-        out[(long long)fx + nx * ((long long)fy + ny * fz)] = W;
+        out[(long long)fx + nx * ((long long)fy + ny * fz)] = W;   // Dirichlet nodes: launch_exp_finite's face fill
       }
     }
   }
@@ -346,8 +341,7 @@ __global__ void __launch_bounds__(FNTH, EXP_FUSED_MINB) k_exp_fused(const LevelG
       if (FREEBOX) {
         if (fr) out[(long long)(fz - gf.flo[2] - gf.zoff) * gf.S + (long long)(fy - gf.flo[1]) * gf.P + (fx - gf.flo[0])] = W;
       } else {
-        if (!fr) W = gD_at(gf, pb, fx, fy, fz);
-        out[(long long)fx + nx * ((long long)fy + ny * fz)] = W;
+        out[(long long)fx + nx * ((long long)fy + ny * fz)] = W;   // Dirichlet nodes: launch_exp_finite's face fill
       }
     };
     if (FREEBOX) {   // free-box output: per-thread (x, y) offsets fixed, the plane term per layer
@@ -392,7 +386,7 @@ __global__ void __launch_bounds__(FNTH, EXP_FUSED_MINB) k_exp_fused(const LevelG
 // interpolates its two nodes along y in registers; fine plane 2K takes plane K's values, the odd plane
 // 2K-1 the mean of planes K-1 and K (registers carried from the previous step). The weights are (1, 0)
 // on a 2h node and (1/2, 1/2) between two, so every stage equals the mean of its two inputs bit for bit.
-// Dirichlet nodes take g_D (A15).
+// Dirichlet nodes: overwritten with g_D (A15) by the face kernel launched after this one.
 constexpr int ETX = 64, ETY = 8, EDX = ETX / 2 + 1, EDY = ETY / 2 + 1;   // 33 x 5 corner values per plane
 
 // no min-blocks hint: ptxas picks 72 registers (3 CTAs / SM); measured at 512^3: hint 1 -> 102 registers,
@@ -519,7 +513,9 @@ cudaError_t launch_exp_finite(const LevelGeom& gf, const Problem& pb, const doub
     count_launch();
     if (freebox) k_exp_fused<true><<<g, FNTH, 0, st>>>(gf, pb, u2h, u4h, w, variant, F0, F1, bz0, lchunk);
     else k_exp_fused<false><<<g, FNTH, 0, st>>>(gf, pb, u2h, u4h, w, variant, F0, F1, bz0, lchunk);
-    return cudaGetLastError();
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess || freebox) return e;
+    return launch_dirichlet_fill(gf, pb, w, 0.0, 0, st);   // full output: g_D on the Dirichlet nodes (§8c A15)
   }
   const int K0 = 2 * bz0, K1 = 2 * bz1 + 2;   // 2h planes of the touched 4h blocks
   dim3 g1((gf.n[0] / 2 + 1 + 127) / 128, gf.n[1] / 2 + 1, K1 - K0 + 1);
@@ -529,7 +525,9 @@ cudaError_t launch_exp_finite(const LevelGeom& gf, const Problem& pb, const doub
   count_launch();
   if (freebox) k_exp_interp<true><<<g2, 64, 0, st>>>(gf, pb, seeds, w, variant, F0);
   else k_exp_interp<false><<<g2, 64, 0, st>>>(gf, pb, seeds, w, variant, F0);
-  return cudaGetLastError();
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || freebox) return e;
+  return launch_dirichlet_fill(gf, pb, w, 0.0, 0, st);
 }
 
 cudaError_t launch_exp_true(const LevelGeom& gf, const Problem& pb, const double* uh, const double* u2h, double* ut,
