@@ -474,8 +474,11 @@ __device__ __forceinline__ void elem_grid_sum3(double v[3], double* partials, in
   buf ^= 1;
 }
 
+#ifndef ELEM_PERS_MINB   // 2 CTAs / SM spill ~200 B per thread; 1 (no spills, half the CTAs) measured on C3:
+#define ELEM_PERS_MINB ELEM_MINB   // 64^3 1.24 -> 1.15 ms but 128^3 4.72 -> 5.2 ms, TTS 40.4 -> 40.8 ms
+#endif
 template <bool CUBE, int BF>
-__global__ void __launch_bounds__(NTH, ELEM_MINB)
+__global__ void __launch_bounds__(NTH, ELEM_PERS_MINB)
     k_jcg_elem_pers(const LevelGeom g, const ElemStencil es, double* x, double* r, double* z, double* p0, double* p1,
                     double* partials, JcgScalars* sc, int zc, int ntx, int nty, int items,
                     const __grid_constant__ ElemPersMaps M) {
