@@ -91,6 +91,9 @@ def lib():
             L.orc_ecmg_arrays.restype = C.c_int
             L.orc_ecmg_arrays.argtypes = [dp, dp, ip, C.c_int, dp, ip, C.POINTER(dp), C.c_double, C.c_int,
                                           C.c_int, C.c_int, dp, dp, dp, dp]
+            L.orc_ecmg_fixed_arrays.restype = C.c_int
+            L.orc_ecmg_fixed_arrays.argtypes = [dp, dp, ip, C.c_int, dp, ip, C.POINTER(dp), C.c_int, C.c_double,
+                                                C.c_int, C.c_int, dp, dp, dp, dp]
             L.orc_ecmg_fixed.restype = C.c_int
             L.orc_ecmg_fixed.argtypes = [dp, dp, ip, C.c_int, C.c_int, dp, C.c_int, ip, C.c_int, C.c_double,
                                          C.c_int, C.c_int, dp, dp, dp, dp]
@@ -302,6 +305,22 @@ def ecmg_arrays(n0, levels, faces, alpha, level_arrays, eps, lo=(0, 0, 0), hi=(1
     if want_w:
         return st, stats, u, ut, w
     return st, stats, u, ut
+
+
+def ecmg_fixed_arrays(n0, levels, faces, alpha, level_arrays, m_L, ratio, lo=(0, 0, 0), hi=(1, 1, 1), precond=False,
+                      exp_variant=0):
+    """Alg. 3 on ARRAYS data (level_arrays as in ecmg_arrays)."""
+    n0 = np.array([n0] * 3 if np.isscalar(n0) else list(n0), dtype=np.int32)
+    N = int(np.prod(n0 * (1 << (levels - 1)) + 1))
+    stats = np.empty(levels * NSTAT)
+    u, ut = np.empty(N), np.empty(N)
+    keep = [None if a is None else _f64(a).reshape(-1) for lv in level_arrays for a in lv]
+    ptrs = (C.POINTER(C.c_double) * len(keep))(*[_d(a) if a is not None else None for a in keep])
+    st = lib().orc_ecmg_fixed_arrays(_d(_f64(lo)), _d(_f64(hi)), _i(n0), int(levels), _d(_f64(alpha)),
+                                     _i(np.array(faces, dtype=np.int32)), ptrs, int(m_L), float(ratio),
+                                     1 if precond else 0, int(exp_variant), _d(stats), _d(u), _d(ut), None)
+    del keep
+    return st, stats.reshape(levels, NSTAT), u, ut
 
 
 def ecmg_fixed(n0, levels, problem_id, m_L, ratio, params=None, lo=(0, 0, 0), hi=(1, 1, 1), faces=None,

@@ -1130,9 +1130,10 @@ int orc_ecmg_arrays(const double* lo, const double* hi, const int* coarsest, int
                    exp_variant, stats, u_fine, ut_fine, w_fine, level_arrays);
 }
 
-int orc_ecmg_fixed(const double* lo, const double* hi, const int* coarsest, int num_levels, int problem_id,
-                   const double* params, int nparams, const int* face, int m_L, double ratio, int precond,
-                   int exp_variant, double* stats, double* u_fine, double* ut_fine, double* w_fine) {
+static int ecmg_fixed_impl(const double* lo, const double* hi, const int* coarsest, int num_levels, int problem_id,
+                           const double* params, int nparams, const int* face, int m_L, double ratio, int precond,
+                           int exp_variant, double* stats, double* u_fine, double* ut_fine, double* w_fine,
+                           const double* const* level_arrays) {
   if (num_levels < 3 || num_levels > 16 || m_L < 0 || !(ratio > 0.0)) return ORC_EINVAL;
   const int Lc = num_levels - 2;
   std::vector<double> e(num_levels, 0.0);
@@ -1142,7 +1143,24 @@ int orc_ecmg_fixed(const double* lo, const double* hi, const int* coarsest, int 
     m[k] = (int)std::ceil(m_L * std::pow(ratio, (double)(Lc - j)) - 1e-12);
   }
   return ecmg_impl(lo, hi, coarsest, num_levels, problem_id, params, nparams, face, e.data(), m.data(), precond,
-                   exp_variant, stats, u_fine, ut_fine, w_fine);
+                   exp_variant, stats, u_fine, ut_fine, w_fine, level_arrays);
+}
+
+int orc_ecmg_fixed(const double* lo, const double* hi, const int* coarsest, int num_levels, int problem_id,
+                   const double* params, int nparams, const int* face, int m_L, double ratio, int precond,
+                   int exp_variant, double* stats, double* u_fine, double* ut_fine, double* w_fine) {
+  return ecmg_fixed_impl(lo, hi, coarsest, num_levels, problem_id, params, nparams, face, m_L, ratio, precond,
+                         exp_variant, stats, u_fine, ut_fine, w_fine, nullptr);
+}
+
+// Alg. 3 on PROB_ARRAYS data (level_arrays as in orc_ecmg_arrays)
+int orc_ecmg_fixed_arrays(const double* lo, const double* hi, const int* coarsest, int num_levels,
+                          const double* alpha, const int* face, const double* const* level_arrays, int m_L,
+                          double ratio, int precond, int exp_variant, double* stats, double* u_fine, double* ut_fine,
+                          double* w_fine) {
+  if (!level_arrays) return ORC_EINVAL;
+  return ecmg_fixed_impl(lo, hi, coarsest, num_levels, PROB_ARRAYS, alpha, 6, face, m_L, ratio, precond,
+                         exp_variant, stats, u_fine, ut_fine, w_fine, level_arrays);
 }
 
 }  // extern "C"

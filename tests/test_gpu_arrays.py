@@ -145,3 +145,20 @@ def test_arrays_setup_ahead_bitwise_and_slabs_rejected():
     # the z-slab driver does not take caller arrays
     assert ecmg.set_option(g.h, ecmg.OPT_VIRTUAL_SLABS, 2) == ecmg.EINVAL
     g.close()
+
+
+def test_arrays_alg3_fixed_schedule():
+    # Alg. 3 (Eq. (ee) counts with m_L = 3, ratio 2, plain CG) on ARRAYS data against the oracle
+    n0, levels = (5, 3, 4), 4
+    faces, alpha, _ = CASES["robin"]
+    data = level_data(n0, levels, True, seed=90)
+    dv = [tuple(dev(a) for a in lv) for lv in data]
+    g = Grid(n0, levels, PROB["ARRAYS"], params=alpha, faces=faces, level_arrays=dv, precond=False)
+    u, ut = g.new_vec(levels - 1), g.new_vec(levels - 1)
+    st, stats = g.run_fixed(3, 2.0, u, ut)
+    ost, ostats, ou, out = o.ecmg_fixed_arrays(n0, levels, faces, alpha, data, 3, 2.0)
+    assert st == 0 and ost == 0
+    assert [s["iterations"] for s in stats[2:]] == [int(v) for v in ostats[2:, 0]] == [6, 3]
+    assert np.max(np.abs(host(u) - ou)) <= 1e-11 * np.max(np.abs(ou))
+    assert np.max(np.abs(host(ut) - out)) <= 1e-11 * np.max(np.abs(out))
+    g.close()

@@ -75,3 +75,14 @@ def test_ecmg_arrays_equals_registry():
     assert sa == 0 and sr == 0
     assert list(ta[:, 0]) == list(tr[:, 0])
     assert rel(ua, ur) <= 1e-11 and rel(uta, utr) <= 1e-11
+
+
+def test_ecmg_fixed_arrays_equals_registry():
+    # Alg. 3 (fixed counts, plain CG) on the sampled C3 = Alg. 3 on the registry C3
+    lv = 4
+    arrays = [c3_arrays((4 << k,) * 3) for k in range(lv)]
+    sa, ta, ua, uta = o.ecmg_fixed_arrays(4, lv, C3_FACES, C3_ALPHA, arrays, 3, 2.0)
+    sr, tr, ur, utr = o.ecmg_fixed(4, lv, o.C3, 3, 2.0)
+    assert sa == 0 and sr == 0
+    assert list(ta[:, 0]) == list(tr[:, 0])
+    assert rel(ua, ur) <= 1e-11 and rel(uta, utr) <= 1e-11
