@@ -162,3 +162,23 @@ def test_arrays_alg3_fixed_schedule():
     assert np.max(np.abs(host(u) - ou)) <= 1e-11 * np.max(np.abs(ou))
     assert np.max(np.abs(host(ut) - out)) <= 1e-11 * np.max(np.abs(out))
     g.close()
+
+
+def test_arrays_zero_data():
+    # no f, g_D, g_R (beta given): b = 0 on every level, so every solve stops before its first iteration
+    # (§8c A10) and u = u~ = 0; the oracle agrees
+    n0, levels = (4, 4, 4), 4
+    faces, alpha = [0, 1, 0, 0, 0, 1], [0.0, 1.5, 0.0, 0.0, 0.0, 0.0]
+    data = [(synth.random_problem_arrays(5 + k, (4 << k,) * 3)[0], None, None, None) for k in range(levels)]
+    dv = [tuple(dev(a) for a in lv) for lv in data]
+    g = Grid(n0, levels, PROB["ARRAYS"], params=alpha, faces=faces, level_arrays=dv)
+    u, ut = g.new_vec(levels - 1), g.new_vec(levels - 1)
+    u.fill_(1.0)
+    ut.fill_(1.0)
+    st, stats = g.run(1e-10, u, ut)
+    ost, ostats, ou, out = o.ecmg_arrays(n0, levels, faces, alpha, data, 1e-10)
+    assert st == 0 and ost == 0
+    assert [s["iterations"] for s in stats[2:]] == [int(v) for v in ostats[2:, 0]] == [0, 0]
+    assert float(u.abs().max()) == 0.0 and float(ut.abs().max()) == 0.0
+    assert np.max(np.abs(ou)) == 0.0
+    g.close()
