@@ -68,3 +68,27 @@ def test_invalid_arguments(libpath):
     st, h = ecmg.create_grid((0, 0, 0), (0, 1, 1), (4, 4, 4), 4)     # empty extent
     assert st == ecmg.EINVAL
     assert ecmg.lib().ecmg_destroy_grid(None) == ecmg.EINVAL
+
+
+def test_struct_layouts_match_header(tmp_path):
+    # the ctypes mirrors of the ABI structs (ecmg.py) have the header's sizes and field offsets (compiled with gcc)
+    import ctypes as C
+    import subprocess
+    from paper_1506_02983_b200 import ecmg as E
+    structs = {"ecmg_problem": E.ecmg_problem, "ecmg_stats": E.ecmg_stats, "ecmg_box": E.ecmg_box,
+               "ecmg_dist": E.ecmg_dist}
+    src = ['#include <stdio.h>', '#include <stddef.h>', '#include "ecmg.h"', "int main(void) {"]
+    for name, cls in structs.items():
+        src.append(f'  printf("{name} %zu\\n", sizeof({name}));')
+        for f, _ in cls._fields_:
+            src.append(f'  printf("{name}.{f} %zu\\n", offsetof({name}, {f}));')
+    src.append("  return 0; }")
+    c = tmp_path / "layout.c"
+    c.write_text("\n".join(src))
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(c), "-o", str(exe)])
+    out = dict(line.rsplit(" ", 1) for line in subprocess.check_output([str(exe)], text=True).splitlines())
+    for name, cls in structs.items():
+        assert int(out[name]) == C.sizeof(cls), name
+        for f, _ in cls._fields_:
+            assert int(out[f"{name}.{f}"]) == getattr(cls, f).offset, (name, f)
