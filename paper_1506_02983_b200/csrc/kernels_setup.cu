@@ -349,6 +349,8 @@ __global__ void __launch_bounds__(C4NTH, RHS_C4_MINB) k_rhs_c4(const LevelGeom g
   }
 }
 
+__device__ __forceinline__ int sel3(int d, int a, int b, int c) { return d == 0 ? a : (d == 1 ? b : c); }
+
 // Boundary shell of the free box: Robin load G and lifting -A_fD g_D, added to b.
 // blockIdx.z = face of the free box (axis d = face/2, side = face&1); a node is handled by the
 // lowest-numbered free-box face it lies on.
@@ -362,23 +364,25 @@ __global__ void k_rhs_shell(const LevelGeom g, const Problem pb, const ElemStenc
   const int ext2 = (d2 == 2) ? ze - zb : g.nf[d2], off2 = (d2 == 2) ? zb : 0;
   const int i1 = blockIdx.x * blockDim.x + threadIdx.x, i2 = blockIdx.y;
   if (i1 >= ext1 || i2 >= ext2) return;
-  int f[3];
-  f[d] = side ? g.nf[d] - 1 : 0;
-  f[d1] = off1 + i1;
-  f[d2] = off2 + i2;
-  if (d == 2 && (f[2] < zb || f[2] >= ze)) return;   // z face not in this slab
-  for (int fc = 0; fc < face; ++fc) {   // owned by a lower face?
+  // free-box coordinates of the node (scalars: no dynamically indexed local arrays)
+  const int fx = d == 0 ? (side ? g.nf[0] - 1 : 0) : off1 + i1;
+  const int fy = d == 1 ? (side ? g.nf[1] - 1 : 0) : (d == 0 ? off1 + i1 : off2 + i2);
+  const int fz = d == 2 ? (side ? g.nf[2] - 1 : 0) : off2 + i2;
+  if (d == 2 && (fz < zb || fz >= ze)) return;   // z face not in this slab
+#pragma unroll
+  for (int fc = 0; fc < 5; ++fc) {   // owned by a lower face?
+    if (fc >= face) break;
     const int dd = fc >> 1;
-    if (f[dd] == ((fc & 1) ? g.nf[dd] - 1 : 0)) return;
+    if (sel3(dd, fx, fy, fz) == ((fc & 1) ? g.nf[dd] - 1 : 0)) return;
   }
-  const int gi[3] = {g.flo[0] + f[0], g.flo[1] + f[1], g.flo[2] + f[2]};
-  const int gx = gi[0], gy = gi[1], gz = gi[2];
+  const int gx = g.flo[0] + fx, gy = g.flo[1] + fy, gz = g.flo[2] + fz;
   double v = 0.0;
   // Robin face load G = sum_q g_R(x_q) N_c h1 h2 / 4 on every Robin face through the node
+#pragma unroll
   for (int F = 0; F < 6; ++F) {
     if (pb.face[F] != FACE_ROBIN) continue;
     const int dF = F >> 1;
-    if (gi[dF] != ((F & 1) ? g.n[dF] : 0)) continue;
+    if (sel3(dF, gx, gy, gz) != ((F & 1) ? g.n[dF] : 0)) continue;
     const int e1d = (dF == 0) ? 1 : 0, e2d = (dF == 2) ? 1 : 2;
     const double hh = g.h[e1d] * g.h[e2d] / 4.0;
     long long gR_block = 0;   // PROB_ARRAYS: this face's block of g_R values (faces in order, 4 n_d1 n_d2 each)
@@ -388,12 +392,12 @@ __global__ void k_rhs_shell(const LevelGeom g, const Problem pb, const ElemStenc
     }
     for (int e2 = -1; e2 <= 0; ++e2)
       for (int e1 = -1; e1 <= 0; ++e1) {
-        const int f1 = gi[e1d] + e1, f2 = gi[e2d] + e2;
+        const int f1 = sel3(e1d, gx, gy, gz) + e1, f2 = sel3(e2d, gx, gy, gz) + e2;
         if (f1 < 0 || f1 >= g.n[e1d] || f2 < 0 || f2 >= g.n[e2d]) continue;
         for (int q = 0; q < 4; ++q) {
           const double xi1 = (q & 1) ? kGauss : -kGauss, xi2 = (q & 2) ? kGauss : -kGauss;
           double xq[3];
-          xq[dF] = g.lo[dF] + gi[dF] * g.h[dF];
+          xq[dF] = g.lo[dF] + sel3(dF, gx, gy, gz) * g.h[dF];
           xq[e1d] = g.lo[e1d] + (f1 + (1.0 + xi1) / 2.0) * g.h[e1d];
           xq[e2d] = g.lo[e2d] + (f2 + (1.0 + xi2) / 2.0) * g.h[e2d];
           const double N = ((1.0 + (e1 ? xi1 : -xi1)) / 2.0) * ((1.0 + (e2 ? xi2 : -xi2)) / 2.0);
@@ -421,20 +425,18 @@ __global__ void k_rhs_shell(const LevelGeom g, const Problem pb, const ElemStenc
       const int pat = ((ex + bx) != 1 ? 1 : 0) | ((ey + by) != 1 ? 2 : 0) | ((ez + bz) != 1 ? 4 : 0);
       sub += be * es.kappa[pat] * gD;
       // Robin face mass between this node and the Dirichlet node j on a common Robin face
+#pragma unroll
       for (int F = 0; F < 6; ++F) {
         if (es.robin[F] == 0.0) continue;
         const int dF = F >> 1;
         const int plane = (F & 1) ? g.n[dF] : 0;
-        if (gi[dF] != plane) continue;
-        const int jj[3] = {jx, jy, jz};
-        if (jj[dF] != plane) continue;
-        int nd = 0;
-        for (int t = 0; t < 3; ++t) if (t != dF && jj[t] != gi[t]) ++nd;
+        if (sel3(dF, gx, gy, gz) != plane || sel3(dF, jx, jy, jz) != plane) continue;
+        const int nd = (dF != 0 && jx != gx) + (dF != 1 && jy != gy) + (dF != 2 && jz != gz);
         sub += es.robin[F] * (nd == 0 ? (1.0 / 9.0) : (nd == 1 ? (1.0 / 18.0) : (1.0 / 36.0))) * gD;
       }
     }
   }
-  if (v != 0.0 || sub != 0.0) b[(long long)(f[2] - g.zoff) * g.S + (long long)f[1] * g.P + f[0]] += v - sub;
+  if (v != 0.0 || sub != 0.0) b[(long long)(fz - g.zoff) * g.S + (long long)fy * g.P + fx] += v - sub;
 }
 
 // ---- gather / scatter between full nodal vectors and the free box ------------------------------
