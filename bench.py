@@ -61,10 +61,13 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled during the timed region. The sampler is started and its
+    first (idle) sample awaited before the region opens, so that nvidia-smi's start-up does not eat a short
+    region; samples are kept by arrival time (every 20 ms) from the region's start to just after its end."""
 
     def __init__(self, index: int):
         self.index, self.samples, self.proc = index, [], None
+        self.t0, self.t1 = None, None
 
     def __enter__(self):
         try:
@@ -72,20 +75,29 @@ class ClockSampler:
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            t_wait = time.monotonic()
+            while not self.samples and time.monotonic() - t_wait < 5.0:
+                time.sleep(0.005)
         except Exception:
             self.proc = None
+        self.t0 = time.monotonic()
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.samples.append([s.strip() for s in line.split(",")])
+            self.samples.append((time.monotonic(), [s.strip() for s in line.split(",")]))
 
     def __exit__(self, *exc):
+        self.t1 = time.monotonic()
         if self.proc:
+            t_wait = time.monotonic()
+            while (not any(t >= self.t0 for t, _ in self.samples)) and time.monotonic() - t_wait < 0.5:
+                time.sleep(0.005)
+            time.sleep(0.05)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=2)
@@ -93,14 +105,19 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        if not self.samples:
+        inside = [v for t, v in self.samples if self.t0 <= t <= self.t1 + 0.06]
+        window = "timed region"
+        if not inside:   # a region shorter than one sampling period: the first sample after it
+            inside = [v for t, v in self.samples if t >= self.t0][:1]
+            window = "first sample after the timed region"
+        if not inside:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        sm = [float(s[0]) for s in inside if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in inside if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and s[3 + i] == "Active"})
+        reasons = sorted({names[i] for s in inside for i in range(4) if len(s) > 3 + i and s[3 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(inside), "window": window}
 
 
 def dist_env():
