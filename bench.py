@@ -226,6 +226,7 @@ def main():
     units_total, fine_units, fine_ms = 0.0, 0.0, 0.0
     per_level = None
     with ClockSampler(local) as clk:
+        barrier()   # the ranks' samplers have started: open the region together
         evs[0].record(stream)
         for _ in range(args.steps):
             st, stats = grid.run(eps, u, ut)
