@@ -157,7 +157,7 @@ def run_reference(args):
     v = statistics.mean(s["value"] for s in samples)
     ms = statistics.mean(s["wall_s"] for s in samples) * 1e3
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (analytic problem, no dataset)",
             "config": {"workload": cfg[4], "sample": samples[-1]["sample"]},
             "cpu_baseline": {k: samples[-1][k] for k in ("value", "unit", "cores", "kind", "sample")},
