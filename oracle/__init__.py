@@ -41,7 +41,7 @@ def build(force: bool = False) -> str:
     """Compile liboracle.so with g++ -O2 -ffp-contract=off."""
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
         tmp = LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["g++", "-std=c++17", "-O2", "-ffp-contract=off", "-shared", "-fPIC",
+        subprocess.check_call(["g++", "-std=c++17", "-O2", "-ffp-contract=off", "-fopenmp", "-shared", "-fPIC",
                                "-o", tmp, SRC])
         os.replace(tmp, LIB)
     return LIB
@@ -97,8 +97,26 @@ def lib():
             L.orc_ecmg_fixed.restype = C.c_int
             L.orc_ecmg_fixed.argtypes = [dp, dp, ip, C.c_int, C.c_int, dp, C.c_int, ip, C.c_int, C.c_double,
                                          C.c_int, C.c_int, dp, dp, dp, dp]
+            L.orc_set_threads.restype = C.c_int
+            L.orc_set_threads.argtypes = [C.c_int]
+            L.orc_get_threads.restype = C.c_int
+            L.orc_max_threads.restype = C.c_int
             _lib = L
     return _lib
+
+
+def set_threads(t: int) -> int:
+    """Threads of the oracle's row loops (1 = serial). Results are bitwise the same for every t
+    (tests/test_oracle_threads.py); only the wall time changes. Returns the previous value."""
+    prev = lib().orc_get_threads()
+    if lib().orc_set_threads(int(t)) != 0:
+        raise ValueError(f"oracle: bad thread count {t}")
+    return prev
+
+
+def max_threads() -> int:
+    """Host processors available to the oracle (omp_get_num_procs)."""
+    return int(lib().orc_max_threads())
 
 
 def _d(a):

@@ -27,7 +27,13 @@
 //   * Alg. 4 level by level, with the diagnostics of Tables 4-10 (errors, r_h,
 //     P:725-729; norms per §8c A21).
 //
-// Built with -O2 -ffp-contract=off (§8c A23). Single threaded.
+// Built with -O2 -ffp-contract=off (§8c A23). Single threaded by default. orc_set_threads(T > 1) runs the
+// node-row loops (assembly scatter, lifting, A_ff p, the vector updates, EXP_finite, EXP_true) over T
+// OpenMP threads so that the full-size configs (C3 256^3, C4 512^3, C5 to 512^3) finish in minutes. Every
+// result is BITWISE the single-threaded one: each row / node is still computed by the same expression from
+// the same operands in the same order (the element contributions to a row keep the lexicographic element
+// order, see build_level), and every reduction -- dot products, ||b||^2, norms -- stays one serial loop in
+// node order (pinned: tests/test_oracle_threads.py).
 
 #include <cmath>
 #include <cstdint>
@@ -38,7 +44,11 @@
 #include <chrono>
 #include <vector>
 
+#include <omp.h>
+
 namespace {
+
+int g_threads = 1;   // orc_set_threads; 1 = the plain serial program
 
 // ----------------------------------------------------------------------------------------------
 // Status codes (same numeric meaning as the product ABI, declared independently here).
@@ -320,6 +330,7 @@ bool build_level(Level* L, const double lo[3], const double hi[3], const int n[3
   L->b.assign(N, 0.0);
 
   // node classes: Dirichlet dominates on shared edges (§8c A6)
+#pragma omp parallel for schedule(static) num_threads(g_threads) if (g_threads > 1)
   for (long iz = 0; iz < L->nn[2]; ++iz)
     for (long iy = 0; iy < L->nn[1]; ++iy)
       for (long ix = 0; ix < L->nn[0]; ++ix) {
@@ -336,29 +347,63 @@ bool build_level(Level* L, const double lo[3], const double hi[3], const int n[3
       }
 
   // volume terms, elements in lexicographic order
-  double K[8][8], Fe[8];
   const double Kh[3] = {L->h[0], L->h[1], L->h[2]};
-  for (int ez = 0; ez < n[2]; ++ez)
-    for (int ey = 0; ey < n[1]; ++ey)
-      for (int ex = 0; ex < n[0]; ++ex) {
-        // beta_e = beta at the element centroid (§8c A3)
-        double cx = L->lo[0] + (ex + 0.5) * L->h[0];
-        double cy = L->lo[1] + (ey + 0.5) * L->h[1];
-        double cz = L->lo[2] + (ez + 0.5) * L->h[2];
-        const long el = ex + (long)n[0] * (ey + (long)n[1] * ez);
-        const double be = P.id == PROB_ARRAYS ? (P.a_beta ? P.a_beta[el] : 1.0) : P.beta(cx, cy, cz);
-        element_stiffness(Kh, be, K);
-        int e[3] = {ex, ey, ez};
-        element_load(P, L->lo, L->h, e, Fe, P.a_f ? P.a_f + 8 * el : nullptr);
-        for (int a = 0; a < 8; ++a) {
-          long ia = L->idx(ex + (a & 1), ey + ((a >> 1) & 1), ez + ((a >> 2) & 1));
-          L->F[ia] += Fe[a];
-          for (int bb = 0; bb < 8; ++bb) {
-            int dx = (bb & 1) - (a & 1), dy = ((bb >> 1) & 1) - ((a >> 1) & 1), dz = ((bb >> 2) & 1) - ((a >> 2) & 1);
-            L->A[ia * 27 + slot(dx, dy, dz)] += K[a][bb];
-          }
+  auto element_terms = [&](int ex, int ey, int ez, double K[8][8], double Fe[8]) {
+    // beta_e = beta at the element centroid (§8c A3)
+    double cx = L->lo[0] + (ex + 0.5) * L->h[0];
+    double cy = L->lo[1] + (ey + 0.5) * L->h[1];
+    double cz = L->lo[2] + (ez + 0.5) * L->h[2];
+    const long el = ex + (long)n[0] * (ey + (long)n[1] * ez);
+    const double be = P.id == PROB_ARRAYS ? (P.a_beta ? P.a_beta[el] : 1.0) : P.beta(cx, cy, cz);
+    element_stiffness(Kh, be, K);
+    int e[3] = {ex, ey, ez};
+    element_load(P, L->lo, L->h, e, Fe, P.a_f ? P.a_f + 8 * el : nullptr);
+  };
+  // add element (ex, ey, ez)'s row a to the global row of its local node a
+  auto scatter_row = [&](int ex, int ey, int ez, int a, const double K[8][8], const double Fe[8]) {
+    long ia = L->idx(ex + (a & 1), ey + ((a >> 1) & 1), ez + ((a >> 2) & 1));
+    L->F[ia] += Fe[a];
+    for (int bb = 0; bb < 8; ++bb) {
+      int dx = (bb & 1) - (a & 1), dy = ((bb >> 1) & 1) - ((a >> 1) & 1), dz = ((bb >> 2) & 1) - ((a >> 2) & 1);
+      L->A[ia * 27 + slot(dx, dy, dz)] += K[a][bb];
+    }
+  };
+  if (g_threads <= 1) {
+    double K[8][8], Fe[8];
+    for (int ez = 0; ez < n[2]; ++ez)
+      for (int ey = 0; ey < n[1]; ++ey)
+        for (int ex = 0; ex < n[0]; ++ex) {
+          element_terms(ex, ey, ez, K, Fe);
+          for (int a = 0; a < 8; ++a) scatter_row(ex, ey, ez, a, K, Fe);
         }
+  } else {
+    // Threaded: one element plane at a time. The plane's element matrices are formed in parallel, then
+    // every node row of the two node planes it touches adds its (up to 4) elements of this plane in
+    // lexicographic (ey, ex) order. Planes go in ez order, so each row receives the same terms in the
+    // same order as in the serial loop above: bitwise the same sums.
+    const long npl = (long)n[0] * n[1];
+    std::vector<double> Kp((size_t)npl * 64), Fp((size_t)npl * 8);
+    for (int ez = 0; ez < n[2]; ++ez) {
+#pragma omp parallel for schedule(static) num_threads(g_threads)
+      for (long t = 0; t < npl; ++t)
+        element_terms((int)(t % n[0]), (int)(t / n[0]), ez, reinterpret_cast<double(*)[8]>(&Kp[(size_t)t * 64]),
+                      &Fp[(size_t)t * 8]);
+      const long rows_pl = L->nn[0] * L->nn[1];
+#pragma omp parallel for schedule(static) num_threads(g_threads)
+      for (long t = 0; t < 2 * rows_pl; ++t) {
+        const int az = (int)(t / rows_pl);
+        const long ix = (t % rows_pl) % L->nn[0], iy = (t % rows_pl) / L->nn[0];
+        for (long ey = iy - 1; ey <= iy; ++ey)
+          for (long ex = ix - 1; ex <= ix; ++ex) {
+            if (ex < 0 || ey < 0 || ex >= n[0] || ey >= n[1]) continue;
+            const long e = ex + (long)n[0] * ey;
+            const int a = (int)(ix - ex) + 2 * (int)(iy - ey) + 4 * az;
+            scatter_row((int)ex, (int)ey, ez, a, reinterpret_cast<const double(*)[8]>(&Kp[(size_t)e * 64]),
+                        &Fp[(size_t)e * 8]);
+          }
       }
+    }
+  }
 
   // Robin faces (a(u,v) gets int alpha u v, f(v) gets int g_R v)
   long gR_block = 0;   // PROB_ARRAYS: offset of this face's block of g_R values
@@ -399,7 +444,7 @@ bool build_level(Level* L, const double lo[3], const double hi[3], const int n[3
   }
 
   // symmetric Dirichlet elimination (lifting): b_f = F_f - A_fD g_D (§8c A5)
-  double bb = 0.0;
+#pragma omp parallel for schedule(static) num_threads(g_threads) if (g_threads > 1)
   for (long iz = 0; iz < L->nn[2]; ++iz)
     for (long iy = 0; iy < L->nn[1]; ++iy)
       for (long ix = 0; ix < L->nn[0]; ++ix) {
@@ -415,14 +460,17 @@ bool build_level(Level* L, const double lo[3], const double hi[3], const int n[3
               if (L->dir[j]) s -= L->A[i * 27 + slot(dx, dy, dz)] * L->gDv[j];
             }
         L->b[i] = s;
-        bb += s * s;
       }
+  double bb = 0.0;   // ||b||^2, serial in node order
+  for (long i = 0; i < N; ++i)
+    if (!L->dir[i]) bb += L->b[i] * L->b[i];
   L->normb = std::sqrt(bb);
   return true;
 }
 
 // q_f = A_ff p_f on free rows (only free columns), q = 0 on Dirichlet rows
 void apply_ff(const Level& L, const double* p, double* q) {
+#pragma omp parallel for schedule(static) num_threads(g_threads) if (g_threads > 1)
   for (long iz = 0; iz < L.nn[2]; ++iz)
     for (long iy = 0; iy < L.nn[1]; ++iy)
       for (long ix = 0; ix < L.nn[0]; ++ix) {
@@ -481,7 +529,9 @@ SolveStats jcg(const Level& L, double* x, double eps, int max_iter, int precond,
     dinv[i] = precond ? 1.0 / d : 1.0;
   }
   apply_ff(L, x, w.data());  // A_ff x_f (Dirichlet columns are skipped by apply_ff)
+#pragma omp parallel for schedule(static) num_threads(g_threads) if (g_threads > 1)
   for (long i = 0; i < N; ++i) if (!L.dir[i]) r[i] = L.b[i] - w[i];
+#pragma omp parallel for schedule(static) num_threads(g_threads) if (g_threads > 1)
   for (long i = 0; i < N; ++i) if (!L.dir[i]) { z[i] = dinv[i] * r[i]; p[i] = z[i]; }
   double rho = dot_free(L, r.data(), z.data());
   double rr = dot_free(L, r.data(), r.data());
@@ -493,12 +543,15 @@ SolveStats jcg(const Level& L, double* x, double eps, int max_iter, int precond,
     double sigma = dot_free(L, p.data(), w.data());
     if (!(sigma > 0.0)) { st.status = ORC_EBREAKDOWN; break; }
     double alpha = rho / sigma;
+#pragma omp parallel for schedule(static) num_threads(g_threads) if (g_threads > 1)
     for (long i = 0; i < N; ++i)
       if (!L.dir[i]) { x[i] = x[i] + alpha * p[i]; r[i] = r[i] - alpha * w[i]; }
+#pragma omp parallel for schedule(static) num_threads(g_threads) if (g_threads > 1)
     for (long i = 0; i < N; ++i) if (!L.dir[i]) z[i] = dinv[i] * r[i];
     double rho_new = dot_free(L, r.data(), z.data());
     double beta = rho_new / rho;
     rho = rho_new;
+#pragma omp parallel for schedule(static) num_threads(g_threads) if (g_threads > 1)
     for (long i = 0; i < N; ++i) if (!L.dir[i]) p[i] = z[i] + beta * p[i];
     rr = dot_free(L, r.data(), r.data());
     ++k;
@@ -506,7 +559,7 @@ SolveStats jcg(const Level& L, double* x, double eps, int max_iter, int precond,
   st.iterations = k;
   st.rel_recur = std::sqrt(rr) / nb;
   apply_ff(L, x, w.data());
-  double tr = 0.0;
+  double tr = 0.0;   // serial in node order
   for (long i = 0; i < N; ++i) if (!L.dir[i]) { double t = L.b[i] - w[i]; tr += t * t; }
   st.rel_true = std::sqrt(tr) / nb;
   if (st.status == ORC_OK && eps > 0.0 && std::sqrt(rr) > eps * nb) st.status = ORC_ENOTCONV;
@@ -642,6 +695,7 @@ double exp_finite_node(const int n[3], const double* u2h, const double* u4h, lon
 }
 
 void exp_finite(const Level& Lf, const double* u2h, const double* u4h, double* w) {
+#pragma omp parallel for schedule(static) num_threads(g_threads) if (g_threads > 1)
   for (long iz = 0; iz < Lf.nn[2]; ++iz)
     for (long iy = 0; iy < Lf.nn[1]; ++iy)
       for (long ix = 0; ix < Lf.nn[0]; ++ix) {
@@ -707,6 +761,7 @@ double exp_finite_lagrange_node(const int n[3], const double* u2h, const double*
 }
 
 void exp_finite_lagrange(const Level& Lf, const double* u2h, const double* u4h, double* w) {
+#pragma omp parallel for schedule(static) num_threads(g_threads) if (g_threads > 1)
   for (long iz = 0; iz < Lf.nn[2]; ++iz)
     for (long iy = 0; iy < Lf.nn[1]; ++iy)
       for (long ix = 0; ix < Lf.nn[0]; ++ix) {
@@ -750,6 +805,7 @@ double exp_true_node(const int n[3], const double* uh, const double* u2h, long i
 }
 
 void exp_true(const Level& Lf, const double* uh, const double* u2h, double* ut) {
+#pragma omp parallel for schedule(static) num_threads(g_threads) if (g_threads > 1)
   for (long iz = 0; iz < Lf.nn[2]; ++iz)
     for (long iy = 0; iy < Lf.nn[1]; ++iy)
       for (long ix = 0; ix < Lf.nn[0]; ++ix) {
@@ -874,6 +930,15 @@ orc_level* orc_build_level_arrays(const double* lo, const double* hi, const int*
 }
 
 void orc_free_level(orc_level* h) { delete h; }
+
+// Threads of the row loops (1 = serial, the default); results are bitwise independent of it.
+int orc_set_threads(int t) {
+  if (t < 1) return ORC_EINVAL;
+  g_threads = t;
+  return ORC_OK;
+}
+int orc_get_threads(void) { return g_threads; }
+int orc_max_threads(void) { return omp_get_num_procs(); }
 long orc_num_nodes(const orc_level* h) { return h->L.N; }
 void orc_get_matrix(const orc_level* h, double* band) { std::memcpy(band, h->L.A.data(), sizeof(double) * h->L.N * 27); }
 void orc_get_load(const orc_level* h, double* F) { std::memcpy(F, h->L.F.data(), sizeof(double) * h->L.N); }
@@ -895,6 +960,7 @@ int orc_dsolve(const orc_level* h, double* x) { return dsolve(h->L, x); }
 
 void orc_exact(const orc_level* h, double* u) {
   const Level& L = h->L;
+#pragma omp parallel for schedule(static) num_threads(g_threads) if (g_threads > 1)
   for (long iz = 0; iz < L.nn[2]; ++iz)
     for (long iy = 0; iy < L.nn[1]; ++iy)
       for (long ix = 0; ix < L.nn[0]; ++ix)
@@ -1077,6 +1143,7 @@ static int ecmg_impl(const double* lo, const double* hi, const int* coarsest, in
     }
     if (P.has_exact) {
       std::vector<double> ex(L->N), e(L->N);
+#pragma omp parallel for schedule(static) num_threads(g_threads) if (g_threads > 1)
       for (long iz = 0; iz < L->nn[2]; ++iz)
         for (long iy = 0; iy < L->nn[1]; ++iy)
           for (long ix = 0; ix < L->nn[0]; ++ix)

@@ -55,7 +55,6 @@ struct ecmg_grid {
   int setup_ctas = 0;              // ECMG_OPT_SETUP_CTAS: CTAs per SM of the ALU-bound RHS kernel when run ahead
   cudaStream_t hi_stream = nullptr, lo_stream = nullptr;   // ecmg_run: solves (high) / level setup (low priority)
   cudaStream_t lo2_stream = nullptr;                        // the finest level's setup (starts at once, beside lo_stream)
-  cudaStream_t hi2_stream = nullptr;                        // mode 4: the finest level's setup at the solves' priority
   int setup_ahead_prio = 1;   // the coarse levels' setups at the solves' priority (they are short and needed soon)
   std::vector<cudaEvent_t> setup_ev;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
@@ -354,8 +353,10 @@ bool use_persistent(const ecmg_grid* G, const LevelGeom& g) {
 // mid-size levels, constant stencil: the whole solve in one cooperative launch of TMA z-marching passes
 bool use_pers_tma(ecmg_grid* G, const LevelGeom& g) {
   if (G->pers_tma_max <= 0 || free_count(g) > G->pers_tma_max) return false;
-  if (G->elem_path) return true;
-  return G->kernel_variant == 1 && ensure_maps(G, g, level_of(G, g));
+  // the cooperative launch needs every (x, y) tile resident at once: wide, flat levels (or a GPU with
+  // fewer SMs) take the graph path instead
+  if (G->elem_path) return elem_pers_fits(g);
+  return const_pers_fits(g) && G->kernel_variant == 1 && ensure_maps(G, g, level_of(G, g));
 }
 
 cudaError_t launch_pers_tma(ecmg_grid* G, const LevelGeom& g) {
@@ -561,6 +562,17 @@ int run_jcg(ecmg_grid* G, int k, double eps, int max_iter, double* u_out, ecmg_s
   return fill_stats(G, g, eps, st);
 }
 
+// DSOLVE (Alg. 4 l.1-2) runs JCG from zero to 1e-14 (reading A12), a target rounding may keep the recurrence
+// residual just above on an ill-conditioned coarse grid. The direct-solve contract is the TRUE residual:
+// rel_res_true <= 1e-12 is a solved level (status OK), anything above is reported as ENOTCONV (it would signal
+// an assembly bug: SPEC coarse_solve).
+constexpr double kDsolveTrueTol = 1e-12;
+int dsolve_status(int s, ecmg_stats& st) {
+  if (s != ECMG_ENOTCONV) return s;
+  if (st.rel_res_true <= kDsolveTrueTol) { st.converged = 1; st.status = ECMG_OK; return ECMG_OK; }
+  return ECMG_ENOTCONV;
+}
+
 bool is_device_ptr(const void* p) {
   cudaPointerAttributes at;
   if (cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return false; }
@@ -644,7 +656,7 @@ int ecmg_create_grid(const ecmg_box* dom, const int coarsest_cells[3], int num_l
   G->beta_doubles = beta_doubles(gmax);
   const long long rhs_blocks = (long long)((gmax.nf[0] + 7) / 8) * ((gmax.nf[1] + 7) / 8) * ((gmax.nf[2] + 3) / 4);
   const long long jcg_blocks = (long long)((gmax.nf[0] + 31) / 32) * ((gmax.nf[1] + 7) / 8) * gmax.nf[2];
-  G->partial_doubles = 3 * std::max(rhs_blocks, jcg_blocks) + 64;
+  G->partial_doubles = 3 * std::max(rhs_blocks, jcg_blocks) + 64;   // grown below for the cooperative solves
   int st = ECMG_OK;
   auto alloc = [&](double** p, long long n) {
     if (st != ECMG_OK) return;
@@ -655,7 +667,6 @@ int ecmg_create_grid(const ecmg_box* dom, const int coarsest_cells[3], int num_l
   alloc(&G->r, G->vec_doubles);
   alloc(&G->p[0], G->vec_doubles);
   alloc(&G->p[1], G->vec_doubles);
-  alloc(&G->partials, G->partial_doubles);
   // per-level right-hand sides and 1D load tables (the finest level's b is the full-size G->b)
   G->bl.assign(num_levels, nullptr);
   G->betal.assign(num_levels, nullptr);
@@ -680,7 +691,6 @@ int ecmg_create_grid(const ecmg_box* dom, const int coarsest_cells[3], int num_l
     if (cudaStreamCreateWithPriority(&G->hi_stream, cudaStreamNonBlocking, hi) != cudaSuccess ||
         cudaStreamCreateWithPriority(&G->lo_stream, cudaStreamNonBlocking, G->setup_ahead_prio ? hi : lo) != cudaSuccess ||
         cudaStreamCreateWithPriority(&G->lo2_stream, cudaStreamNonBlocking, lo) != cudaSuccess ||
-        cudaStreamCreateWithPriority(&G->hi2_stream, cudaStreamNonBlocking, hi) != cudaSuccess ||
         cudaEventCreateWithFlags(&G->fork_ev, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&G->join_ev, cudaEventDisableTiming) != cudaSuccess)
       st = ECMG_ECUDA;
@@ -699,13 +709,21 @@ int ecmg_create_grid(const ecmg_box* dom, const int coarsest_cells[3], int num_l
                         init_setup_kernel_attributes() != cudaSuccess || init_cta_kernel_attributes() != cudaSuccess ||
                         init_pers_kernel_attributes() != cudaSuccess || init_elem_pers_attributes() != cudaSuccess))
     st = ECMG_ECUDA;
+  // the partial sums: per-CTA triples of the z-marching passes, or the two ping-pong buffers of the
+  // cooperative solves (6 doubles per co-resident CTA), whichever is larger
+  if (st == ECMG_OK) G->partial_doubles = std::max(G->partial_doubles, coop_partials_doubles());
+  alloc(&G->partials, G->partial_doubles);
   if (st == ECMG_OK) {
     for (int i = 0; i < 16; ++i) cudaEventCreate(&G->ev[i]);
     G->ev_init = true;
   }
   if (st == ECMG_OK && cudaStreamSynchronize(G->stream) != cudaSuccess) st = ECMG_ECUDA;
-  // test only: ECMG_TEST_NCCL_SINGLE=1 with nranks == 1 runs the NCCL slab path on one rank
+#ifdef ECMG_TESTING
+  // test build only (libecmg_test.so): ECMG_TEST_NCCL_SINGLE=1 with nranks == 1 runs the NCCL slab path on one rank
   const bool nccl_single = dist && dist->nranks == 1 && std::getenv("ECMG_TEST_NCCL_SINGLE") != nullptr;
+#else
+  const bool nccl_single = false;
+#endif
   if (nccl_single) slab_force_single() = true;
   if (st == ECMG_OK && dist && (dist->nranks > 1 || nccl_single)) {
     // NCCL ranks: the communicator is created here (collective over all ranks)
@@ -743,7 +761,6 @@ int ecmg_destroy_grid(ecmg_grid* G) {
   if (G->hi_stream) cudaStreamDestroy(G->hi_stream);
   if (G->lo_stream) cudaStreamDestroy(G->lo_stream);
   if (G->lo2_stream) cudaStreamDestroy(G->lo2_stream);
-  if (G->hi2_stream) cudaStreamDestroy(G->hi2_stream);
   cudaFree(G->seeds);
   if (G->sc_host) cudaFreeHost(G->sc_host);
   if (G->param_host) cudaFreeHost(G->param_host);
@@ -825,7 +842,7 @@ int ecmg_set_option(ecmg_grid* G, int option, int value) {
   switch (option) {
     case ECMG_OPT_EXP_VARIANT: if (value != 0 && value != 1) return ECMG_EINVAL; G->exp_variant = value; break;
     case ECMG_OPT_PRECOND: if (value != 0 && value != 1) return ECMG_EINVAL; G->precond = value; invalidate_setup(G); clear_graphs(G); break;
-    case ECMG_OPT_SETUP_AHEAD: if (value < 0 || value > 4) return ECMG_EINVAL; G->setup_ahead = value; break;
+    case ECMG_OPT_SETUP_AHEAD: if (value != 0 && value != 1) return ECMG_EINVAL; G->setup_ahead = value; break;
     case ECMG_OPT_BETA_FLY: if (value != 0 && value != 1) return ECMG_EINVAL; G->beta_fly = value; clear_graphs(G); break;
     case ECMG_OPT_EXP_KERNEL: if (value != 0 && value != 1) return ECMG_EINVAL; G->exp_fused = value; break;
     case ECMG_OPT_SETUP_CTAS: if (value < 0) return ECMG_EINVAL; G->setup_ctas = value; break;
@@ -999,13 +1016,24 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
   // waits for its setup event only. The caller's stream forks into both and joins at the end.
   const bool ahead = G->setup_ahead != 0;
   cudaStream_t user = G->stream;
-  struct Restore { ecmg_grid* G; cudaStream_t s; ~Restore() { G->stream = s; } } restore{G, user};
+  // On every exit (the error returns included) the caller's stream is joined after all the work forked
+  // from it -- kernels still writing b_k / beta_k / u_k must not outlive the call on the caller's
+  // ordering -- and G->stream is restored.
+  struct Join {
+    ecmg_grid* G; cudaStream_t user; bool forked = false;
+    ~Join() {
+      if (forked)
+        for (cudaStream_t s : {G->hi_stream, G->lo_stream, G->lo2_stream})
+          if (cudaEventRecord(G->join_ev, s) == cudaSuccess) cudaStreamWaitEvent(user, G->join_ev, 0);
+      G->stream = user;
+    }
+  } join{G, user};
   if (ahead) {
     ECMG_CUDA(cudaEventRecord(G->fork_ev, user));
+    join.forked = true;
     ECMG_CUDA(cudaStreamWaitEvent(G->hi_stream, G->fork_ev, 0));
     ECMG_CUDA(cudaStreamWaitEvent(G->lo_stream, G->fork_ev, 0));
     ECMG_CUDA(cudaStreamWaitEvent(G->lo2_stream, G->fork_ev, 0));
-    ECMG_CUDA(cudaStreamWaitEvent(G->hi2_stream, G->fork_ev, 0));
     // the finest level's setup (most of the work) on its own stream, so that it starts at once; the
     // coarser levels' setups in level order beside it
     G->stream = G->hi_stream;
@@ -1015,8 +1043,7 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
   // launches instead of every level's setup
   int next_setup = 0;
   auto enqueue_setup = [&](int k) -> int {
-    cudaStream_t s_k = (k == L_run - 1 && G->setup_ahead != 2) ? (G->setup_ahead == 4 ? G->hi2_stream : G->lo2_stream)
-                                                               : G->lo_stream;
+    cudaStream_t s_k = k == L_run - 1 ? G->lo2_stream : G->lo_stream;
     { int s = setup_level_on(G, k, s_k, G->setup_ctas); if (s) return s; }
     ECMG_CUDA(launch_dirichlet_fill(G->geom[k], level_prob(G, k), level_u(k), 0.0, 0, s_k));
     ECMG_CUDA(cudaEventRecord(G->setup_ev[k], s_k));
@@ -1030,13 +1057,8 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
     return ECMG_OK;
   };
   if (ahead) {
-    if (G->setup_ahead == 2) {   // tuning mode: every setup on one stream, in level order
-      { int s = setups_until(L_run - 2); if (s) return s; }
-      { int s = enqueue_setup(L_run - 1); if (s) return s; }
-    } else {
-      { int s = enqueue_setup(L_run - 1); if (s) return s; }
-      { int s = setups_until(1); if (s) return s; }
-    }
+    { int s = enqueue_setup(L_run - 1); if (s) return s; }
+    { int s = setups_until(1); if (s) return s; }
   }
   // the whole cascade is enqueued without host synchronisation when every solve is device driven
   for (int k = 0; k < L_run; ++k) {
@@ -1044,12 +1066,7 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
     ecmg_stats& st = stv[k];
     cudaEvent_t* e = &G->lvl_ev[5 * k];
     ECMG_CUDA(cudaEventRecord(e[0], G->stream));
-    if (ahead) {
-      ECMG_CUDA(cudaStreamWaitEvent(G->stream, G->setup_ev[k], 0));
-      // mode 3: the z-marching (non-persistent) solves wait until the finest level's setup is done too,
-      // instead of sharing the SMs with it
-      if (G->setup_ahead == 3 && !use_persistent(G, g)) ECMG_CUDA(cudaStreamWaitEvent(G->stream, G->setup_ev[L_run - 1], 0));
-    }
+    if (ahead) ECMG_CUDA(cudaStreamWaitEvent(G->stream, G->setup_ev[k], 0));
     else { int s = setup_level(G, k); if (s) return s; }
     ECMG_CUDA(cudaEventRecord(e[1], G->stream));
     if (k < 2) {
@@ -1070,7 +1087,7 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
       async[k] = 1;
     } else if (s == ECMG_EINVAL) {
       s = run_jcg(G, k, eps_k, maxit_k, uk, &st);   // host loop (ablation path / fixed counts)
-      if (k < 2 && s == ECMG_ENOTCONV) s = ECMG_OK;
+      if (k < 2) s = dsolve_status(s, st);
       if (s != ECMG_OK && status == ECMG_OK) status = s;
     }
     if (s == ECMG_ECUDA || s == ECMG_ENOMEM) return s;
@@ -1087,18 +1104,14 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
     ECMG_CUDA(cudaMemcpyAsync(u_fine, G->u[G->L - 1], sizeof(double) * Nf, cudaMemcpyDeviceToHost, G->stream));
   if (ut_fine && !ut_dev)
     ECMG_CUDA(cudaMemcpyAsync(ut_fine, G->ut_tmp, sizeof(double) * Nf, cudaMemcpyDeviceToHost, G->stream));
-  if (ahead) {   // join: the caller's stream continues after everything enqueued here
-    ECMG_CUDA(cudaEventRecord(G->join_ev, G->stream));
-    ECMG_CUDA(cudaStreamWaitEvent(user, G->join_ev, 0));
-  }
-  ECMG_CUDA(cudaStreamSynchronize(G->stream));
+  ECMG_CUDA(cudaStreamSynchronize(G->stream));   // (the caller's stream is joined by `join` on return)
   for (int k = 0; k < L_run; ++k) {
     ecmg_stats& st = stv[k];
     if (async[k]) {
       // kernels the level's graph ran: init + true residual + the executed two-iteration loop bodies
       if ((int)G->lvl_graph.size() == G->L && G->lvl_graph[k]) count_launch(2 + 4 * ((G->lvl_sc[k].iter + 1) / 2));
       int s = stats_from(G->lvl_sc[k], k < 2 ? 1e-14 : eps_lv[k], &st);
-      if (k < 2 && s == ECMG_ENOTCONV) s = ECMG_OK;
+      if (k < 2) s = dsolve_status(s, st);
       if (s != ECMG_OK && status == ECMG_OK) status = s;
     }
     cudaEvent_t* e = &G->lvl_ev[5 * k];

@@ -221,6 +221,13 @@ cudaError_t launch_jcg_persistent(const LevelGeom& g, const ConstStencil& cs, co
                                   double* z, double* p0, double* p1, double* w, double* dinv, const double* beta,
                                   const double* b, double* partials, JcgScalars* sc, cudaStream_t st);
 long long persistent_max_bricks(int elem_path);
+// co-resident CTAs of the cooperative TMA solves, and the partial-sum doubles every cooperative solve needs
+// (6 per CTA of the largest grid + 64); call after the init_*_attributes
+int const_pers_slots();
+int elem_pers_slots_count();
+long long coop_partials_doubles();
+bool const_pers_fits(const LevelGeom& g);   // the cooperative TMA solves take this level's shape
+bool elem_pers_fits(const LevelGeom& g);
 bool cta_solve_fits(const LevelGeom& g, int elem_path, long long max_nodes);
 cudaError_t init_cta_kernel_attributes();
 cudaError_t launch_jcg_cta(const LevelGeom& g, const ConstStencil& cs, const ElemStencil* es, double* x, double* r,

@@ -678,6 +678,13 @@ static int elem_pers_slots() {
   return slots;
 }
 
+int elem_pers_slots_count() { return elem_pers_slots(); }
+
+bool elem_pers_fits(const LevelGeom& g) {
+  const long long tiles = (long long)((g.nf[0] + TX - 1) / TX) * ((g.nf[1] + TY - 1) / TY);
+  return g.BP % 2 == 0 && g.zbeg == 0 && tiles <= elem_pers_slots();
+}
+
 cudaError_t init_elem_pers_attributes() {
   cudaError_t e = cudaFuncSetAttribute(k_jcg_elem_pers<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, EP_SMEM);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_jcg_elem_pers<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, EP_SMEM);

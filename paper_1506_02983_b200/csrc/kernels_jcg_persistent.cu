@@ -599,6 +599,14 @@ cudaError_t launch_jcg_cta(const LevelGeom& g, const ConstStencil& cs, const Ele
   return cudaGetLastError();
 }
 
+// partial-sum doubles the cooperative solves need: grid_sum3 / pers_grid_sum3 / elem_grid_sum3 ping-pong two
+// buffers of 3 doubles per CTA, and their grids are at most the co-resident CTAs of each kernel
+long long coop_partials_doubles() {
+  const long long g = std::max<long long>(std::max(persistent_grid<true>(1 << 30), persistent_grid<false>(1 << 30)),
+                                          std::max(const_pers_slots(), elem_pers_slots_count()));
+  return 6 * g + 64;
+}
+
 // largest level (in bricks of 8 x 8 x 4 nodes) the persistent kernel takes: MAXB bricks per resident CTA
 long long persistent_max_bricks(int elem_path) {
   return (long long)MAXB * (elem_path ? persistent_grid<true>(1 << 30) : persistent_grid<false>(1 << 30));

@@ -441,6 +441,13 @@ static int pers_slots() {
   return slots;
 }
 
+int const_pers_slots() { return pers_slots(); }
+
+bool const_pers_fits(const LevelGeom& g) {
+  const long long tiles = (long long)((g.nf[0] + TX - 1) / TX) * ((g.nf[1] + TY - 1) / TY);
+  return g.zbeg == 0 && tiles <= pers_slots();
+}
+
 cudaError_t init_pers_kernel_attributes() {
   return cudaFuncSetAttribute(k_jcg_const_pers, cudaFuncAttributeMaxDynamicSharedMemorySize, PS_SBYTES * PS_NS + 128);
 }

@@ -263,6 +263,7 @@ class Grid:
             stream = torch.cuda.current_stream().cuda_stream
         coarsest = [coarsest] * 3 if isinstance(coarsest, int) else list(coarsest)
         self.coarsest, self.L, self.problem_id = coarsest, num_levels, problem_id
+        self.device = torch.cuda.current_device()
         st, self.h = create_grid(lo, hi, coarsest, num_levels, stream, dist)
         if st != OK:
             raise EcmgError(st, "ecmg_create_grid")
@@ -283,36 +284,69 @@ class Grid:
         _, n, nodes, _, _ = level_shape(self.h, level)
         return n, nodes
 
+    def _vec(self, t, level, where, host_ok=False):
+        """Check a caller vector before its raw pointer crosses the ABI: float64, contiguous, at least the
+        level's node count, and on this grid's device (or, where the ABI allows it, in host memory)."""
+        if t is None:
+            return None
+        if not hasattr(t, "data_ptr"):
+            raise TypeError(f"{where}: expected a torch tensor")
+        if str(t.dtype) != "torch.float64" or not t.is_contiguous():
+            raise TypeError(f"{where}: libecmg takes contiguous float64 tensors")
+        _, nodes = self.shape(level)
+        if t.numel() < nodes:
+            raise ValueError(f"{where}: tensor has {t.numel()} elements, level {level} has {nodes} nodes")
+        if t.is_cuda:
+            if t.device.index != self.device:
+                raise ValueError(f"{where}: tensor on cuda:{t.device.index}, grid on cuda:{self.device}")
+        elif not host_ok:
+            raise ValueError(f"{where}: a device tensor is required")
+        return t
+
     def new_vec(self, level, device="cuda"):
         import torch
         n, nodes = self.shape(level)
         return torch.zeros(nodes, dtype=torch.float64, device=device)
 
     def solve_level(self, level, eps, max_iter, u):
+        self._vec(u, level, "solve_level(u)")
         st, stats = solve_level(self.h, level, eps, max_iter, u)
         self._check(st, "ecmg_solve_level", allow=(OK, ENOTCONV))
         return st, stats.as_dict()
 
     def prolongate_extrapolate(self, level, u2h, u4h, w):
+        self._vec(u2h, level - 1, "prolongate_extrapolate(u2h)")
+        self._vec(u4h, level - 2, "prolongate_extrapolate(u4h)")
+        self._vec(w, level, "prolongate_extrapolate(w)")
         self._check(prolongate_extrapolate(self.h, level, u2h, u4h, w), "ecmg_prolongate_extrapolate")
 
     def richardson(self, level, uh, u2h, ut):
+        self._vec(uh, level, "richardson(uh)")
+        self._vec(u2h, level - 1, "richardson(u2h)")
+        self._vec(ut, level, "richardson(ut)")
         self._check(richardson(self.h, level, uh, u2h, ut), "ecmg_richardson")
 
     def run(self, eps, u_fine, ut_fine=None):
+        self._vec(u_fine, self.L - 1, "run(u_fine)", host_ok=True)
+        self._vec(ut_fine, self.L - 1, "run(ut_fine)", host_ok=True)
         st, stats = run(self.h, eps, self.L, u_fine, ut_fine)
         self._check(st, "ecmg_run", allow=(OK, ENOTCONV))
         return st, [s.as_dict() for s in stats]
 
     def run_fixed(self, m_L, ratio, u_fine, ut_fine=None):
+        self._vec(u_fine, self.L - 1, "run_fixed(u_fine)", host_ok=True)
+        self._vec(ut_fine, self.L - 1, "run_fixed(ut_fine)", host_ok=True)
         st, stats = run_fixed(self.h, m_L, ratio, self.L, u_fine, ut_fine)
         self._check(st, "ecmg_run_fixed")
         return st, [s.as_dict() for s in stats]
 
     def apply_operator(self, level, p, q):
+        self._vec(p, level, "apply_operator(p)")
+        self._vec(q, level, "apply_operator(q)")
         self._check(apply_operator(self.h, level, p, q), "ecmg_apply_operator")
 
     def level_rhs(self, level, b):
+        self._vec(b, level, "level_rhs(b)")
         st, nb = level_rhs(self.h, level, b)
         self._check(st, "ecmg_level_rhs")
         return nb

@@ -76,13 +76,15 @@ def test_virtual_slab_fixed_iterations(pid, P):
 def test_nccl_single_rank_selftest():
     # one NCCL rank with every sharded-eligible level forced onto the slab path: exercises dlopen of
     # libnccl, ncclGetUniqueId, ncclCommInitRank and the allreduce -> finalize passes on one GPU
-    # (no inter-rank waiting). Run in a subprocess: the force flag is process-wide.
+    # (no inter-rank waiting). Run in a subprocess against libecmg_test.so (the -DECMG_TESTING build of the same
+    # sources: the force switch is not in the product library); the flag is process-wide.
     import subprocess, sys, os, json
     code = r'''
 import os, sys, json
 sys.path.insert(0, os.getcwd())
 import torch, numpy as np
 from paper_1506_02983_b200 import Grid, ecmg, PROB
+ecmg.LIB_PATH = os.path.join(os.path.dirname(ecmg.LIB_PATH), "libecmg_test.so")   # the -DECMG_TESTING build
 nid = ecmg.nccl_unique_id()
 g1 = Grid(4, 5, PROB["C2"]); u1 = g1.new_vec(4); st1, s1 = g1.run(1e-10, u1)
 d = ecmg.make_dist(0, 1, nid)
