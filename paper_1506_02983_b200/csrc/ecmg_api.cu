@@ -490,9 +490,8 @@ int run_jcg(ecmg_grid* G, int k, double eps, int max_iter, double* u_out, ecmg_s
     ++it;
     return e;
   };
-  ECMG_CUDA(cudaEventRecord(G->ev[0], G->stream));
   if (eps <= 0.0 && G->unfused && !G->elem_path) {
-    // ablation: the unfused textbook sequence (kernels_textbook.cu), nine passes per iteration
+    // the ablation's scratch z is allocated before the timed window opens
     const long long need = g.S * g.nza + 64;
     if (G->aux_doubles < need) {
       cudaFree(G->aux[0]); cudaFree(G->aux[1]);
@@ -502,6 +501,10 @@ int run_jcg(ecmg_grid* G, int k, double eps, int max_iter, double* u_out, ecmg_s
       ECMG_CUDA(cudaMalloc(&G->aux[1], sizeof(double) * need));
       G->aux_doubles = need;
     }
+  }
+  ECMG_CUDA(cudaEventRecord(G->ev[0], G->stream));
+  if (eps <= 0.0 && G->unfused && !G->elem_path) {
+    // ablation: the unfused textbook sequence (kernels_textbook.cu), nine passes per iteration
     double* z = G->aux[0];
     double* p = G->p[0];
     double* w = G->p[1];

@@ -54,7 +54,12 @@ def test_alg4_fullsize_vs_oracle(cfg):
     assert all(abs(a - b) <= 1 for a, b in zip(it_g, it_o)), (it_g, it_o)
     for k, s in enumerate(stats[2:], start=2):
         assert s["rel_res_recur"] <= eps, (k, s)
-        assert abs(s["norm_b"] - G["per_level"][k]["normb"]) <= 1e-12 * G["per_level"][k]["normb"], k
+        # against the correctly rounded norm of the oracle's b (tests/golden/add_normb_exact.py): the oracle's own
+        # serial ||b|| carries the recursive-summation error of ~1e8 terms (9e-13 at 256^3, 4.7e-10 at 512^3)
+        ref = G["per_level"][k]
+        assert "normb_exact" in ref, f"{cfg}: run tests/golden/add_normb_exact.py {cfg}"
+        print(f"{cfg} level {k}: ||b|| gpu {s['norm_b']!r} exact {ref['normb_exact']!r} oracle serial {ref['normb']!r}")
+        assert abs(s["norm_b"] - ref["normb_exact"]) <= 1e-13 * ref["normb_exact"], k
     idx = torch.from_numpy(np.array(G["sample_index"], dtype=np.int64)).cuda()
     torch.cuda.synchronize()
     for name, t in (("u", u), ("ut", ut)):
