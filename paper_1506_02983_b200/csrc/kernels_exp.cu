@@ -154,33 +154,54 @@ __global__ void __launch_bounds__(64) k_exp_interp(const LevelGeom gf, const Pro
   }
 }
 
-// (1+2) fused: EXP_finite as one z-march over 4h block layers. A CTA owns XB x YB 4h blocks in (x, y)
-// (64 x 8 fine nodes, plus the domain's last node row / column) and a chunk of 4h layers. Per layer it
-// stages the three 2h planes of u_2h and the two 4h planes of u_4h it touches in shared memory, forms
-// the seeds of the layer's blocks there (the same expressions as k_exp_seeds), evaluates the
-// interpolant per (block, fine row, fine plane) with the per-row coefficients of k_exp_interp into a
-// shared output tile, and writes the tile with coalesced row stores. HBM traffic: the fine level
-// written once (8 B / node) plus ~1/8 + 1/64 of it read, instead of a seed array written and re-read.
-// Results are bitwise those of k_exp_seeds + k_exp_interp (same operations in the same order).
+// (1+2) fused: EXP_finite as one z-march over 4h block layers, evaluated SEPARABLY. A CTA owns XB x YB 4h
+// blocks in (x, y) (64 x 8 fine nodes, plus the domain's last node row / column) and a chunk of 4h layers.
+// Per layer it stages the three 2h planes of u_2h and the two 4h planes of u_4h it touches in shared memory
+// and forms there the values at all 27 2h nodes of every block:
+//   * corners and edge midpoints: Eq. (jiedian) / Eq. (zhongdian), k_exp_seeds' expressions;
+//   * face and cell centres: variant 0 (Serendipity) the value of the 20-node interpolant W there -- face
+//     centre = 1/2 (its 4 edge midpoints) - 1/4 (its 4 corners), cell centre = 1/4 (12 midpoints) - 1/4 (8
+//     corners) (pinned for the oracle in tests/test_oracle_exp.py); variant 1 (Remark 2,
+//     P:513-516) the mean of Eq. (zhongdian) over the diagonals.
+// The 20-node Serendipity space lies inside the tri-quadratic space Q2, so W equals the Q2
+// Lagrange interpolant of its own 27 values; with the centres filled that way both variants are the
+// tensor-product quadratic interpolation of the 27 values, applied axis by axis: along x into XS (fine x,
+// 2h y, 2h z), then, per thread (fine column x, fine plane z), along z to the five 2h rows and along y to
+// the eight fine rows, stored with coalesced row stores. Every per-node index map (which 2h node a thread
+// forms, from which staged values) is fixed per thread and computed once before the z-march. HBM traffic:
+// the fine level written once (8 B / node) plus ~1/8 + 1/64 of it read. Results equal the two-pass blending
+// evaluation (k_exp_seeds + k_exp_interp) to rounding (tests/test_gpu_parity.py).
 constexpr int XB = 16, YB = 2;                                 // 4h blocks per tile
 constexpr int FXT = 4 * XB + 1, FYT = 4 * YB + 1;              // fine nodes per tile incl. the last node
 constexpr int S2X = 2 * XB + 1, S2Y = 2 * YB + 1;              // 2h nodes per tile plane
 constexpr int FNTH = 256;
+constexpr int N1 = 3 * S2Y * S2X, N0 = 2 * (YB + 1) * (XB + 1);   // staged u_2h / u_4h values per layer
+static_assert(FNTH == 4 * 64 && FXT == 65 && FYT == 9, "thread map: (fine column, fine plane) = (tid & 63, tid >> 6)");
+static_assert(N1 <= 2 * FNTH && N0 <= FNTH, "staging: two u_2h and one u_4h value per thread");
 
-template <bool FREEBOX>
+// 1D quadratic through the 2h nodes (t = -1, 0, 1) of a 4h block at fine offset l = 0..4 (t = (l - 2) / 2)
+__device__ __forceinline__ void q2w(int l, double& w0, double& w1, double& w2) {
+  w0 = (l == 0) ? 1.0 : (l == 1) ? 0.375 : (l == 3) ? -0.125 : 0.0;
+  w1 = (l == 2) ? 1.0 : (l == 1 || l == 3) ? 0.75 : 0.0;
+  w2 = (l == 4) ? 1.0 : (l == 1) ? -0.125 : (l == 3) ? 0.375 : 0.0;
+}
+
+// flat index of tile-local 2h node (i, j, k) in U1s / Ss, and of tile-local 4h node (i, j, k) in U0s
+__device__ __forceinline__ int f2(int i, int j, int k) { return i + S2X * (j + S2Y * k); }
+__device__ __forceinline__ int f4(int i, int j, int k) { return i + (XB + 1) * (j + (YB + 1) * k); }
+
+template <bool FREEBOX, int VARIANT>
 #ifndef EXP_FUSED_MINB
-#define EXP_FUSED_MINB 3   // 4 (64 registers): 0.54 -> 0.61 ms inside ecmg_run at 512^3
+#define EXP_FUSED_MINB 3
 #endif
-__global__ void __launch_bounds__(FNTH, EXP_FUSED_MINB) k_exp_fused(const LevelGeom gf, const Problem pb, const double* __restrict__ u2h,
-                                                       const double* __restrict__ u4h, double* __restrict__ out, int variant,
-                                                       int F0, int F1, int bzA, int lchunk) {
-  __shared__ double U1s[3][S2Y][S2X];          // u_2h on 2h planes 2bz .. 2bz+2
-  __shared__ double U0s[2][YB + 1][XB + 1];    // u_4h on 4h planes bz, bz+1
-  __shared__ double Ss[3][S2Y][S2X];           // seeds of the layer
-  __shared__ double Os[5][FYT][FXT];           // fine output tile, planes 4bz .. 4bz+4
-  __shared__ double Wq[5][3], Wl[5][2];        // 1D quadratic / linear weights at xi = (l - 2) / 2
+__global__ void __launch_bounds__(FNTH, EXP_FUSED_MINB) k_exp_fused(const LevelGeom gf, const double* __restrict__ u2h,
+                                                                    const double* __restrict__ u4h, double* __restrict__ out,
+                                                                    int F0, int F1, int bzA, int lchunk) {
+  __shared__ double U1s[N1];                   // u_2h on 2h planes 2bz .. 2bz+2 (f2 layout)
+  __shared__ double U0s[N0];                   // u_4h on 4h planes bz, bz+1 (f4 layout)
+  __shared__ double Ss[N1];                    // the 27 values of every block of the layer (f2 layout)
+  __shared__ double XS[3][S2Y][FXT];           // ... interpolated along x: (fine x, 2h y, 2h z)
   const int tid = threadIdx.x;
-  if (tid < 5) { quad_w(tid, Wq[tid]); lin_w(tid, Wl[tid]); }
   const int n4x = gf.n[0] / 4, n4y = gf.n[1] / 4, n4z = gf.n[2] / 4;
   const int n2x = gf.n[0] / 2, n2y = gf.n[1] / 2;
   const long long nn2x = n2x + 1, nn2y = n2y + 1;
@@ -193,8 +214,8 @@ __global__ void __launch_bounds__(FNTH, EXP_FUSED_MINB) k_exp_fused(const LevelG
   const int I0 = 2 * bx0, J0 = 2 * by0;
   const long long nx = gf.n[0] + 1, ny = gf.n[1] + 1;
   const int bzs = bzA + blockIdx.z * lchunk, bze = min(bzs + lchunk, n4z);
-  // staging assignments (compile-time index maps): each thread loads at most 2 u_2h and 1 u_4h values
-  constexpr int N1 = 3 * S2Y * S2X, N0 = 2 * (YB + 1) * (XB + 1);
+  // ---- per-thread maps, fixed for the whole z-march ------------------------------------------------------
+  // staging: u_2h values t = tid, tid + 256 (f2 order), u_4h value tid (f4 order)
   long long o1[2];
   bool v1[2];
 #pragma unroll
@@ -208,50 +229,114 @@ __global__ void __launch_bounds__(FNTH, EXP_FUSED_MINB) k_exp_fused(const LevelG
   const bool v0 = tid < N0 && bx0 + i0 <= n4x && by0 + j0 <= n4y;
   const long long o0 = (bx0 + i0) + nn4x * ((by0 + j0) + nn4y * (long long)k0);
   const long long pl2 = nn2x * nn2y, pl4 = nn4x * nn4y;
+  // 2h-node values, nodes t = tid, tid + 256: kind 0 corner (Eq. jiedian), 1 edge midpoint (Eq. zhongdian:
+  // U1 at t plus the differences at its two 4h-coincident neighbours t -/+ e), 2 face / cell centre
+  int sk[2], se[2], su[3][2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int t = min(tid + r * FNTH, N1 - 1);
+    const int i = t % S2X, j = (t / S2X) % S2Y, k = t / (S2X * S2Y);
+    const int oi = i & 1, oj = j & 1, ok = k & 1, nodd = oi + oj + ok;
+    sk[r] = nodd == 0 ? 0 : nodd == 1 ? 1 : 2;
+    se[r] = f2(oi, oj, ok);
+    su[0][r] = f4(i >> 1, j >> 1, k >> 1);                                   // corner: its own 4h node
+    su[1][r] = f4((i - oi) >> 1, (j - oj) >> 1, (k - ok) >> 1);              // midpoint: the two ends
+    su[2][r] = f4((i + oi) >> 1, (j + oj) >> 1, (k + ok) >> 1);
+  }
+  // Serendipity face / cell centres (VARIANT 0): the tile's 2h nodes with >= 2 odd indices, one per thread:
+  // k odd: (i or j odd) -> 2 odd with k, or 3; k even: i and j odd
+  int ct = -1, ce = 0, cf = 0, cc = 0;   // node, unit strides along its two odd axes, 1 = cell centre
+  if (VARIANT == 0) {
+    int c = tid;
+    constexpr int NK1 = S2Y * S2X - (YB + 1) * (XB + 1);   // k = 1 plane: nodes with i or j odd
+    constexpr int NK0 = YB * XB;                            // k = 0 / 2 planes: i and j odd
+    if (c < NK1) {
+      // enumerate the k = 1 plane, skipping the (even, even) nodes
+      int i = 0, j = 0, m = c;
+      for (j = 0; j < S2Y; ++j) {
+        const int cnt = (j & 1) ? S2X : XB;   // odd row: all; even row: odd i only
+        if (m < cnt) { i = (j & 1) ? m : 2 * m + 1; break; }
+        m -= cnt;
+      }
+      ct = f2(i, j, 1);
+      cc = (i & 1) && (j & 1);
+      ce = (i & 1) ? f2(1, 0, 0) : f2(0, 1, 0);
+      cf = ((i & 1) && !(j & 1)) || (!(i & 1) && (j & 1)) ? f2(0, 0, 1) : 0;
+    } else if (c < NK1 + 2 * NK0) {
+      c -= NK1;
+      const int k = 2 * (c / NK0), m = c % NK0;
+      ct = f2(2 * (m % XB) + 1, 2 * (m / XB) + 1, k);
+      ce = f2(1, 0, 0);
+      cf = f2(0, 1, 0);
+    }
+  }
+  // x pass: lane lx of a line reads 2h nodes xb .. xb+2 with weights (wx0, wx1, wx2) -- a unit weight on an
+  // even (2h-coincident) column, so those are copied exactly, and xb kept inside the line
+  const int lx = tid & 63, lzt = tid >> 6;
+  int xb;
+  double wx0, wx1, wx2;
+  {
+    const int m = lx >> 1;
+    if (lx & 1) { xb = (lx & 2) ? m - 1 : m; q2w(lx & 3, wx0, wx1, wx2); }
+    else { xb = min(m, S2X - 3); wx0 = (m == xb) ? 1.0 : 0.0; wx1 = (m == xb + 1) ? 1.0 : 0.0; wx2 = 0.0; }
+  }
+  double wz0, wz1, wz2;
+  q2w(lzt, wz0, wz1, wz2);
+  // rows of the tile inside the free box (FREEBOX output)
+  const int rlo = FREEBOX ? max(0, gf.flo[1] - Y0) : 0;
+  const int rhi = FREEBOX ? min(nfy, gf.flo[1] + gf.nf[1] - Y0) : nfy;
+  const long long rstride = FREEBOX ? gf.P : nx;
+  // one fine column (x = X0 + cx) of fine plane fz0 + cz: along z to the five 2h rows, along y to the rows
+  auto column = [&](int cx, int cz, double a0, double a1, double a2, int fz0) {
+    double Z[S2Y];
+#pragma unroll
+    for (int j = 0; j < S2Y; ++j) Z[j] = a0 * XS[0][j][cx] + a1 * XS[1][j][cx] + a2 * XS[2][j][cx];
+    const int fx = X0 + cx, fz = fz0 + cz;
+    if (FREEBOX && !(fz >= gf.flo[2] && fz < gf.flo[2] + gf.nf[2] && fx >= gf.flo[0] && fx < gf.flo[0] + gf.nf[0])) return;
+    double* o = FREEBOX ? out + (long long)(fz - gf.flo[2] - gf.zoff) * gf.S + (long long)(Y0 - gf.flo[1]) * gf.P + (fx - gf.flo[0])
+                        : out + fx + nx * ((long long)Y0 + ny * fz);
+#pragma unroll
+    for (int r = 0; r < FYT; ++r) {
+      const int b = 2 * (r >> 2), l = r & 3;   // row 8 (the domain's last): 2h row 4
+      double W;
+      if (l == 0) W = Z[b];
+      else if (l == 2) W = Z[b + 1];
+      else if (l == 1) W = 0.375 * Z[b] + 0.75 * Z[b + 1] - 0.125 * Z[b + 2];
+      else W = -0.125 * Z[b] + 0.75 * Z[b + 1] + 0.375 * Z[b + 2];
+      if (r >= rlo && r < rhi) o[r * rstride] = W;   // full output: Dirichlet nodes by launch_exp_finite's face fill
+    }
+  };
   double r1[2] = {0.0, 0.0}, r0 = 0.0;
   auto fetch = [&](int bz) {
 #pragma unroll
     for (int r = 0; r < 2; ++r) r1[r] = v1[r] ? __ldg(u2h + o1[r] + 2LL * bz * pl2) : 0.0;
     r0 = v0 ? __ldg(u4h + o0 + (long long)bz * pl4) : 0.0;
   };
-  // regular stores (free-box output): thread -> column st_lx, rows st_row and st_row + 4 of the tile
-  const int st_lx = tid & 63, st_row = tid >> 6;
-  bool st_ok[2];
-  long long st_off[2];
-#pragma unroll
-  for (int r2 = 0; r2 < 2; ++r2) {
-    const int fx = X0 + st_lx, fy = Y0 + st_row + 4 * r2;
-    st_ok[r2] = st_lx < nfx && st_row + 4 * r2 < nfy && fx >= gf.flo[0] && fx < gf.flo[0] + gf.nf[0] &&
-                fy >= gf.flo[1] && fy < gf.flo[1] + gf.nf[1];
-    st_off[r2] = (long long)(fy - gf.flo[1]) * gf.P + (fx - gf.flo[0]);
-  }
   if (bzs < bze) fetch(bzs);
   for (int bz = bzs; bz < bze; ++bz) {
     const int fz0 = 4 * bz, nfz = (bz == n4z - 1) ? 5 : 4;
     const int pz0 = max(fz0, F0), pz1 = min(fz0 + nfz, F1);   // fine planes of this layer to write
     __syncthreads();   // previous layer's tiles consumed
-#pragma unroll
-    for (int r = 0; r < 2; ++r)
-      if (tid + r * FNTH < N1) (&U1s[0][0][0])[tid + r * FNTH] = r1[r];
-    if (tid < N0) (&U0s[0][0][0])[tid] = r0;
+    U1s[tid] = r1[0];
+    if (tid + FNTH < N1) U1s[tid + FNTH] = r1[1];
+    if (tid < N0) U0s[tid] = r0;
     if (bz + 1 < bze) fetch(bz + 1);   // next layer's loads in flight during this layer's work
     __syncthreads();
     if (pz0 >= pz1) continue;
-    // seeds (k_exp_seeds' expressions; (i, j, k) tile-local 2h indices, even = 4h-coincident)
-    auto U1 = [&](int i, int j, int k) { return U1s[k][j][i]; };
-    auto U0 = [&](int i, int j, int k) { return U0s[k >> 1][j >> 1][i >> 1]; };
-    auto D = [&](int i, int j, int k) { return U1(i, j, k) - U0(i, j, k); };
-    for (int t = tid; t < N1; t += FNTH) {
-      const int i = t % S2X, j = (t / S2X) % S2Y, k = t / (S2X * S2Y);
+    // the 2h-node values
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int t = tid + r * FNTH;
+      if (t >= N1) break;
       double v = 0.0;
-      const int oi = i & 1, oj = j & 1, ok = k & 1;
-      const int nodd = oi + oj + ok;
-      if (nodd == 0) {
-        v = (5.0 * U1(i, j, k) - U0(i, j, k)) / 4.0;                              // Eq. (jiedian)
-      } else if (nodd == 1) {
-        v = U1(i, j, k) + (D(i - oi, j - oj, k - ok) + D(i + oi, j + oj, k + ok)) / 8.0;   // Eq. (zhongdian)
-      } else if (variant == 1) {   // Remark 2: mean of Eq. (zhongdian) over the diagonals
-        const int odd[3] = {oi, oj, ok};
+      if (sk[r] == 0) {
+        v = (5.0 * U1s[t] - U0s[su[0][r]]) / 4.0;                                          // Eq. (jiedian)
+      } else if (sk[r] == 1) {
+        v = U1s[t] + ((U1s[t - se[r]] - U0s[su[1][r]]) + (U1s[t + se[r]] - U0s[su[2][r]])) / 8.0;   // Eq. (zhongdian)
+      } else if (VARIANT == 1) {   // Remark 2: mean of Eq. (zhongdian) over the diagonals through the node
+        const int i = t % S2X, j = (t / S2X) % S2Y, k = t / (S2X * S2Y);
+        const int odd[3] = {i & 1, j & 1, k & 1};
+        auto D = [&](int a, int b, int c) { return U1s[f2(a, b, c)] - U0s[f4(a >> 1, b >> 1, c >> 1)]; };
         double sum = 0.0;
         int ax[3], na = 0;
         for (int d = 0; d < 3; ++d) if (odd[d]) ax[na++] = d;
@@ -260,120 +345,54 @@ __global__ void __launch_bounds__(FNTH, EXP_FUSED_MINB) k_exp_fused(const LevelG
           int oa[3] = {0, 0, 0};
           oa[ax[0]] = -1;
           for (int q = 1; q < na; ++q) oa[ax[q]] = ((sgn >> (q - 1)) & 1) ? -1 : 1;
-          sum += U1(i, j, k) + (D(i + oa[0], j + oa[1], k + oa[2]) + D(i - oa[0], j - oa[1], k - oa[2])) / 8.0;
+          sum += U1s[t] + (D(i + oa[0], j + oa[1], k + oa[2]) + D(i - oa[0], j - oa[1], k - oa[2])) / 8.0;
         }
         v = sum / nseg;
       }
-      (&Ss[0][0][0])[t] = v;   // outside the tile's blocks: never read
+      Ss[t] = v;   // outside the tile's blocks: finite, never used with a nonzero weight
     }
     __syncthreads();
-    // interpolation: one item per (fine row, block, fine plane) of the tile, k_exp_interp's expressions.
-    // The 4 x 8 x 16 regular items map to threads at compile time (row fastest: conflict-free shared
-    // stores, row stride 65 doubles); the domain's last row (row 8) and last plane (lz 4) follow as extras.
-    auto interp_item = [&](int row, int lb, int lz) {
-      const int lby = min(row >> 2, nby - 1), ly = row - 4 * lby;
-      const double qz[3] = {Wq[lz][0], Wq[lz][1], Wq[lz][2]}, lz2[2] = {Wl[lz][0], Wl[lz][1]};
-      const double qy[3] = {Wq[ly][0], Wq[ly][1], Wq[ly][2]}, ly2[2] = {Wl[ly][0], Wl[ly][1]};
-      auto s = [&](int k, int j, int i) { return Ss[k][2 * lby + j][2 * lb + i]; };
-      double C[3], E[2];
-      if (variant == 1) {
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-          double tt = 0.0;
-#pragma unroll
-          for (int k = 0; k < 3; ++k) tt += qz[k] * (qy[0] * s(k, 0, i) + qy[1] * s(k, 1, i) + qy[2] * s(k, 2, i));
-          C[i] = tt;
+    if (VARIANT == 0) {   // Serendipity: the face and cell centres from the block's corners and midpoints
+      if (ct >= 0) {
+        double v;
+        if (!cc) {   // face centre: midpoints at +-e, +-f, corners at +-e+-f
+          const double mids = Ss[ct + ce] + Ss[ct - ce] + Ss[ct + cf] + Ss[ct - cf];
+          const double corn = Ss[ct + ce + cf] + Ss[ct + ce - cf] + Ss[ct - ce + cf] + Ss[ct - ce - cf];
+          v = 0.5 * mids - 0.25 * corn;
+        } else {     // cell centre
+          constexpr int X = 1, Y = S2X, Zs = S2X * S2Y;
+          const double mids = Ss[ct + Y + Zs] + Ss[ct - Y + Zs] + Ss[ct + Y - Zs] + Ss[ct - Y - Zs] +
+                              Ss[ct + X + Zs] + Ss[ct - X + Zs] + Ss[ct + X - Zs] + Ss[ct - X - Zs] +
+                              Ss[ct + X + Y] + Ss[ct - X + Y] + Ss[ct + X - Y] + Ss[ct - X - Y];
+          const double corn = Ss[ct + X + Y + Zs] + Ss[ct - X + Y + Zs] + Ss[ct + X - Y + Zs] + Ss[ct - X - Y + Zs] +
+                              Ss[ct + X + Y - Zs] + Ss[ct - X + Y - Zs] + Ss[ct + X - Y - Zs] + Ss[ct - X - Y - Zs];
+          v = 0.25 * mids - 0.25 * corn;
         }
-        E[0] = E[1] = 0.0;
-      } else {
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-          C[i] = ly2[0] * (lz2[0] * s(0, 0, i) + lz2[1] * s(2, 0, i)) + ly2[1] * (lz2[0] * s(0, 2, i) + lz2[1] * s(2, 2, i));
-#pragma unroll
-        for (int a = 0; a < 2; ++a) {
-          const int A = 2 * a;
-          const double Py = lz2[0] * (qy[0] * s(0, 0, A) + qy[1] * s(0, 1, A) + qy[2] * s(0, 2, A)) +
-                            lz2[1] * (qy[0] * s(2, 0, A) + qy[1] * s(2, 1, A) + qy[2] * s(2, 2, A));
-          const double Pz = ly2[0] * (qz[0] * s(0, 0, A) + qz[1] * s(1, 0, A) + qz[2] * s(2, 0, A)) +
-                            ly2[1] * (qz[0] * s(0, 2, A) + qz[1] * s(1, 2, A) + qz[2] * s(2, 2, A));
-          const double T = ly2[0] * (lz2[0] * s(0, 0, A) + lz2[1] * s(2, 0, A)) + ly2[1] * (lz2[0] * s(0, 2, A) + lz2[1] * s(2, 2, A));
-          E[a] = Py + Pz - 2.0 * T;
-        }
+        Ss[ct] = v;   // reads only nodes with at most one odd index: no race with the writes
       }
-      double* orow = &Os[lz][row][4 * lb];
+      __syncthreads();
+    }
+    // along x: XS[k][j][x] for the 3 x S2Y lines, lanes = fine columns 0..63, column 64 by a few threads
 #pragma unroll
-      for (int l = 0; l < 4; ++l) {
-        double qx[3], lx[2];
-        quad_w(l, qx); lin_w(l, lx);
-        orow[l] = qx[0] * C[0] + qx[1] * C[1] + qx[2] * C[2] + lx[0] * E[0] + lx[1] * E[1];
+    for (int q = 0; q < (3 * S2Y + 3) / 4; ++q) {
+      const int line = lzt + 4 * q;
+      if (line < 3 * S2Y) {
+        const double* sl = Ss + line * S2X;
+        (&XS[0][0][0])[line * FXT + lx] = wx0 * sl[xb] + wx1 * sl[xb + 1] + wx2 * sl[xb + 2];
       }
-      if (bx0 + lb == n4x - 1) {   // the domain's last node column (l = 4)
-        double qx[3], lx[2];
-        quad_w(4, qx); lin_w(4, lx);
-        orow[4] = qx[0] * C[0] + qx[1] * C[1] + qx[2] * C[2] + lx[0] * E[0] + lx[1] * E[1];
-      }
-    };
+    }
+    if (tid < 3 * S2Y) (&XS[0][0][0])[tid * FXT + 64] = Ss[tid * S2X + 2 * XB];
+    __syncthreads();
     const int lzs = pz0 - fz0, lze = pz1 - fz0;   // planes of the layer to produce
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const int t = tid + r * FNTH;
-      const int row = t & 7, lb = (t >> 3) & 15, lz = t >> 7;
-      if (lb < nbx && row < nfy && lz >= lzs && lz < lze) interp_item(row, lb, lz);
-    }
-    if (nfy > 8 || lze > 4) {   // extras: row 8 of the domain's last block row, plane 4 of the last layer
-      const int nx8 = (nfy > 8) ? 4 * XB : 0;                     // (row 8, lb, lz < 4)
-      const int n4p = (lze > 4) ? FYT * XB : 0;                   // (row, lb, lz = 4)
-      for (int t = tid; t < nx8 + n4p; t += FNTH) {
-        int row, lb, lz;
-        if (t < nx8) { row = 8; lb = t & 15; lz = t >> 4; }
-        else { const int u = t - nx8; row = u % FYT; lb = u / FYT; lz = 4; }
-        if (lb < nbx && row < nfy && lz >= lzs && lz < lze) interp_item(row, lb, lz);
-      }
-    }
-    __syncthreads();
-    // stores: the 4 x 8 x 64 regular nodes map to threads at compile time (coalesced rows), then the
-    // domain's last column / row / plane as extras
-    auto put = [&](int lz, int row, int lx) {
-      const int fx = X0 + lx, fy = Y0 + row, fz = fz0 + lz;
-      double W = Os[lz][row][lx];
-      const bool fr = fz >= gf.flo[2] && fz < gf.flo[2] + gf.nf[2] && fy >= gf.flo[1] && fy < gf.flo[1] + gf.nf[1] &&
-                      fx >= gf.flo[0] && fx < gf.flo[0] + gf.nf[0];
-      if (FREEBOX) {
-        if (fr) out[(long long)(fz - gf.flo[2] - gf.zoff) * gf.S + (long long)(fy - gf.flo[1]) * gf.P + (fx - gf.flo[0])] = W;
-      } else {
-        out[(long long)fx + nx * ((long long)fy + ny * fz)] = W;   // Dirichlet nodes: launch_exp_finite's face fill
-      }
-    };
-    if (FREEBOX) {   // free-box output: per-thread (x, y) offsets fixed, the plane term per layer
-#pragma unroll
-      for (int lz = 0; lz < 4; ++lz) {
-        const int fz = fz0 + lz;
-        if (lz < lzs || lz >= lze || fz < gf.flo[2] || fz >= gf.flo[2] + gf.nf[2]) continue;
-        const long long zt = (long long)(fz - gf.flo[2] - gf.zoff) * gf.S;
-#pragma unroll
-        for (int r2 = 0; r2 < 2; ++r2)
-          if (st_ok[r2]) out[zt + st_off[r2]] = Os[lz][st_row + 4 * r2][st_lx];
-      }
-    } else {
-      const int lx = tid & 63, row0 = tid >> 6;
-      if (lx < nfx) {
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          const int row = row0 + 4 * (r & 1), lz = r >> 1;
-          if (row < nfy && lz >= lzs && lz < lze) put(lz, row, lx);
-        }
-      }
-    }
-    if (nfx > 64 || nfy > 8 || lze > 4) {
-      // extras: A = column 64 (rows < 8, planes < 4), B = row 8 (planes < 4), C = plane 4
-      const int nA = nfx > 64 ? 32 : 0, nB = nfy > 8 ? 4 * FXT : 0, nC = lze > 4 ? FYT * FXT : 0;
-      for (int t = tid; t < nA + nB + nC; t += FNTH) {
-        int lx, row, lz;
-        if (t < nA) { lx = 64; row = t & 7; lz = t >> 3; }
-        else if (t < nA + nB) { const int u = t - nA; lx = u % FXT; row = 8; lz = u / FXT; }
-        else { const int u = t - nA - nB; lx = u % FXT; row = u / FXT; lz = 4; }
-        if (lx < nfx && row < nfy && lz >= lzs && lz < lze) put(lz, row, lx);
-      }
+    if (lx < nfx && lzt >= lzs && lzt < lze) column(lx, lzt, wz0, wz1, wz2, fz0);
+    // extras: column 64 (the domain's last node column) for planes 0..3, plane 4 (the domain's last plane)
+    const int nA = (nfx > 64) ? 4 : 0, nC = (lze > 4) ? nfx : 0;
+    for (int t = tid; t < nA + nC; t += FNTH) {
+      const int cx = t < nA ? 64 : t - nA, cz = t < nA ? t : 4;
+      if (cz < lzs || cz >= lze) continue;
+      double a0, a1, a2;
+      q2w(cz, a0, a1, a2);
+      column(cx, cz, a0, a1, a2, fz0);
     }
   }
 }
@@ -511,8 +530,10 @@ cudaError_t launch_exp_finite(const LevelGeom& gf, const Problem& pb, const doub
     const int lchunk = std::max(1, std::min(8, tiles * nl / 2000));   // >= ~2000 CTAs where the level allows
     dim3 g((gf.n[0] / 4 + XB - 1) / XB, (gf.n[1] / 4 + YB - 1) / YB, (nl + lchunk - 1) / lchunk);
     count_launch();
-    if (freebox) k_exp_fused<true><<<g, FNTH, 0, st>>>(gf, pb, u2h, u4h, w, variant, F0, F1, bz0, lchunk);
-    else k_exp_fused<false><<<g, FNTH, 0, st>>>(gf, pb, u2h, u4h, w, variant, F0, F1, bz0, lchunk);
+    if (freebox && variant == 0) k_exp_fused<true, 0><<<g, FNTH, 0, st>>>(gf, u2h, u4h, w, F0, F1, bz0, lchunk);
+    else if (freebox) k_exp_fused<true, 1><<<g, FNTH, 0, st>>>(gf, u2h, u4h, w, F0, F1, bz0, lchunk);
+    else if (variant == 0) k_exp_fused<false, 0><<<g, FNTH, 0, st>>>(gf, u2h, u4h, w, F0, F1, bz0, lchunk);
+    else k_exp_fused<false, 1><<<g, FNTH, 0, st>>>(gf, u2h, u4h, w, F0, F1, bz0, lchunk);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || freebox) return e;
     return launch_dirichlet_fill(gf, pb, w, 0.0, 0, st);   // full output: g_D on the Dirichlet nodes (§8c A15)

@@ -9,6 +9,9 @@ import torch  # noqa: E402
 
 from paper_1506_02983_b200 import Grid, PROB, ecmg  # noqa: E402
 
+if os.environ.get("ECMG_LIB_PATH"):   # A/B timing of a variant build (tuning only)
+    ecmg.LIB_PATH = os.environ["ECMG_LIB_PATH"]
+
 
 def best(fn, reps=5):
     st = torch.cuda.current_stream()
