@@ -25,6 +25,86 @@ using namespace ecmg;
 static std::atomic<long long> g_launches{0};
 namespace ecmg { void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); } }
 
+#ifdef ECMG_TESTING
+// test build: guard bands of kGuard bytes of the pattern 0xA5 before and after every device buffer; a write out of
+// bounds by up to kGuard bytes on either side changes them. Checked on free and by ecmg_test_guard_check.
+#include <mutex>
+#include <unordered_map>
+namespace {
+constexpr size_t kGuard = 8192;
+std::mutex g_guard_mu;
+std::unordered_map<void*, size_t> g_guarded;   // user pointer -> size in bytes
+long long g_guard_bad = 0;                      // corrupted guard bytes found on frees so far
+
+long long guard_bad_bytes(const char* user, size_t bytes) {
+  std::vector<unsigned char> h(2 * kGuard);
+  const size_t tail = kGuard + (bytes + 255) / 256 * 256 - bytes;   // the pad to the next 256 B belongs to the band
+  if (cudaMemcpy(h.data(), user - kGuard, kGuard, cudaMemcpyDeviceToHost) != cudaSuccess ||
+      cudaMemcpy(h.data() + kGuard, user + bytes, std::min(tail, kGuard), cudaMemcpyDeviceToHost) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  long long bad = 0;
+  for (size_t i = 0; i < kGuard + std::min(tail, kGuard); ++i) bad += h[i] != 0xA5;
+  return bad;
+}
+}  // namespace
+namespace ecmg {
+cudaError_t dev_malloc(void** p, size_t bytes) {
+  char* base = nullptr;
+  const size_t padded = (bytes + 255) / 256 * 256;
+  cudaError_t e = cudaMalloc(&base, padded + 2 * kGuard);
+  if (e != cudaSuccess) { *p = nullptr; return e; }
+  cudaMemset(base, 0xA5, kGuard);
+  cudaMemset(base + kGuard + bytes, 0xA5, padded - bytes + kGuard);
+  cudaDeviceSynchronize();
+  std::lock_guard<std::mutex> lk(g_guard_mu);
+  g_guarded[base + kGuard] = bytes;
+  *p = base + kGuard;
+  return cudaSuccess;
+}
+void dev_free(void* p) {
+  if (!p) return;
+  size_t bytes = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_guard_mu);
+    auto it = g_guarded.find(p);
+    if (it == g_guarded.end()) { cudaFree(p); return; }
+    bytes = it->second;
+    g_guarded.erase(it);
+  }
+  cudaDeviceSynchronize();
+  const long long bad = guard_bad_bytes(static_cast<const char*>(p), bytes);
+  if (bad) {
+    std::lock_guard<std::mutex> lk(g_guard_mu);
+    g_guard_bad += bad > 0 ? bad : 1;
+  }
+  cudaFree(static_cast<char*>(p) - kGuard);
+}
+}  // namespace ecmg
+// corrupted guard bytes over every live device buffer plus those found on frees since the last call (then reset)
+extern "C" long long ecmg_test_guard_check(void) {
+  cudaDeviceSynchronize();
+  std::lock_guard<std::mutex> lk(g_guard_mu);
+  long long bad = g_guard_bad;
+  g_guard_bad = 0;
+  for (const auto& kv : g_guarded) {
+    const long long b = guard_bad_bytes(static_cast<const char*>(kv.first), kv.second);
+    bad += b > 0 ? b : (b < 0 ? 1 : 0);
+  }
+  return bad;
+}
+extern "C" long long ecmg_test_guarded_buffers(void) {
+  std::lock_guard<std::mutex> lk(g_guard_mu);
+  return (long long)g_guarded.size();
+}
+#else
+namespace ecmg {
+cudaError_t dev_malloc(void** p, size_t bytes) { return cudaMalloc(p, bytes); }
+void dev_free(void* p) { cudaFree(p); }
+}  // namespace ecmg
+#endif
+
 using ParamHost = JcgParams;
 
 struct ecmg_grid {
@@ -385,12 +465,12 @@ cudaError_t launch_persistent(ecmg_grid* G, const LevelGeom& g) {
   // w = A p (and on the element path D^-1) in scratch vectors sized for the level (grown on demand)
   const long long need = g.S * g.nza + 64;
   if (G->aux_doubles < need) {
-    cudaFree(G->aux[0]);
-    cudaFree(G->aux[1]);
+    dfree(G->aux[0]);
+    dfree(G->aux[1]);
     G->aux[0] = G->aux[1] = nullptr;
     G->aux_doubles = 0;
-    cudaError_t e = cudaMalloc(&G->aux[0], sizeof(double) * need);
-    if (e == cudaSuccess) e = cudaMalloc(&G->aux[1], sizeof(double) * need);
+    cudaError_t e = dmalloc(&G->aux[0], sizeof(double) * need);
+    if (e == cudaSuccess) e = dmalloc(&G->aux[1], sizeof(double) * need);
     if (e != cudaSuccess) return e;
     G->aux_doubles = need;
   }
@@ -494,11 +574,11 @@ int run_jcg(ecmg_grid* G, int k, double eps, int max_iter, double* u_out, ecmg_s
     // the ablation's scratch z is allocated before the timed window opens
     const long long need = g.S * g.nza + 64;
     if (G->aux_doubles < need) {
-      cudaFree(G->aux[0]); cudaFree(G->aux[1]);
+      dfree(G->aux[0]); dfree(G->aux[1]);
       G->aux[0] = G->aux[1] = nullptr;
       G->aux_doubles = 0;
-      ECMG_CUDA(cudaMalloc(&G->aux[0], sizeof(double) * need));
-      ECMG_CUDA(cudaMalloc(&G->aux[1], sizeof(double) * need));
+      ECMG_CUDA(dmalloc(&G->aux[0], sizeof(double) * need));
+      ECMG_CUDA(dmalloc(&G->aux[1], sizeof(double) * need));
       G->aux_doubles = need;
     }
   }
@@ -663,7 +743,7 @@ int ecmg_create_grid(const ecmg_box* dom, const int coarsest_cells[3], int num_l
   int st = ECMG_OK;
   auto alloc = [&](double** p, long long n) {
     if (st != ECMG_OK) return;
-    if (cudaMalloc(p, sizeof(double) * n) != cudaSuccess) { cudaGetLastError(); st = ECMG_ENOMEM; return; }
+    if (dmalloc(p, sizeof(double) * n) != cudaSuccess) { cudaGetLastError(); st = ECMG_ENOMEM; return; }
     if (cudaMemsetAsync(*p, 0, sizeof(double) * n, G->stream) != cudaSuccess) st = ECMG_ECUDA;
   };
   alloc(&G->x, G->vec_doubles);
@@ -683,7 +763,7 @@ int ecmg_create_grid(const ecmg_box* dom, const int coarsest_cells[3], int num_l
   }
   G->b = G->bl[num_levels - 1];
   alloc(&G->seeds, (long long)(gmax.n[0] / 2 + 1) * (gmax.n[1] / 2 + 1) * (gmax.n[2] / 2 + 1));
-  if (st == ECMG_OK && cudaMalloc(&G->sc, sizeof(JcgScalars)) != cudaSuccess) st = ECMG_ENOMEM;
+  if (st == ECMG_OK && dmalloc(&G->sc, sizeof(JcgScalars)) != cudaSuccess) st = ECMG_ENOMEM;
   if (st == ECMG_OK && cudaMemsetAsync(G->sc, 0, sizeof(JcgScalars), G->stream) != cudaSuccess) st = ECMG_ECUDA;
   if (st == ECMG_OK && cudaHostAlloc(&G->sc_host, 2 * sizeof(JcgScalars), cudaHostAllocDefault) != cudaSuccess) st = ECMG_ENOMEM;
   if (st == ECMG_OK && cudaHostAlloc(&G->param_host, sizeof(*G->param_host), cudaHostAllocDefault) != cudaSuccess) st = ECMG_ENOMEM;
@@ -751,20 +831,20 @@ int ecmg_destroy_grid(ecmg_grid* G) {
   if (!G) return ECMG_EINVAL;
   if (G->stream) cudaStreamSynchronize(G->stream); else cudaDeviceSynchronize();
   if (G->slab) slab_driver_destroy(G->slab);
-  cudaFree(G->x); cudaFree(G->r); cudaFree(G->p[0]); cudaFree(G->p[1]);
-  for (double* p : G->bl) cudaFree(p);
-  for (double* p : G->betal) cudaFree(p);
-  for (double* p : G->s1d) cudaFree(p);
-  cudaFree(G->zv); cudaFree(G->aux[0]); cudaFree(G->aux[1]); cudaFree(G->partials); cudaFree(G->sc);
-  for (double* p : G->u) cudaFree(p);
-  cudaFree(G->ut_tmp);
+  dfree(G->x); dfree(G->r); dfree(G->p[0]); dfree(G->p[1]);
+  for (double* p : G->bl) dfree(p);
+  for (double* p : G->betal) dfree(p);
+  for (double* p : G->s1d) dfree(p);
+  dfree(G->zv); dfree(G->aux[0]); dfree(G->aux[1]); dfree(G->partials); dfree(G->sc);
+  for (double* p : G->u) dfree(p);
+  dfree(G->ut_tmp);
   for (auto& e : G->setup_ev) if (e) cudaEventDestroy(e);
   if (G->fork_ev) cudaEventDestroy(G->fork_ev);
   if (G->join_ev) cudaEventDestroy(G->join_ev);
   if (G->hi_stream) cudaStreamDestroy(G->hi_stream);
   if (G->lo_stream) cudaStreamDestroy(G->lo_stream);
   if (G->lo2_stream) cudaStreamDestroy(G->lo2_stream);
-  cudaFree(G->seeds);
+  dfree(G->seeds);
   if (G->sc_host) cudaFreeHost(G->sc_host);
   if (G->param_host) cudaFreeHost(G->param_host);
   if (G->lvl_param) cudaFreeHost(G->lvl_param);
@@ -819,11 +899,11 @@ int ecmg_set_coeffs(ecmg_grid* G, const ecmg_problem* pr) {
     int face_none[6] = {FACE_ROBIN, FACE_ROBIN, FACE_ROBIN, FACE_ROBIN, FACE_ROBIN, FACE_ROBIN};
     for (int k = 0; k < G->L; ++k) {
       const LevelGeom gk = make_geom(G->dom, G->n0, std::min(k, size_level), face_none, 1);
-      if (cudaMalloc(&G->betal[k], sizeof(double) * beta_doubles(gk)) != cudaSuccess) { cudaGetLastError(); return ECMG_ENOMEM; }
+      if (dmalloc(&G->betal[k], sizeof(double) * beta_doubles(gk)) != cudaSuccess) { cudaGetLastError(); return ECMG_ENOMEM; }
     }
   }
   if (elem_path && !G->zv) {
-    if (cudaMalloc(&G->zv, sizeof(double) * G->vec_doubles) != cudaSuccess) { cudaGetLastError(); return ECMG_ENOMEM; }
+    if (dmalloc(&G->zv, sizeof(double) * G->vec_doubles) != cudaSuccess) { cudaGetLastError(); return ECMG_ENOMEM; }
     if (cudaMemsetAsync(G->zv, 0, sizeof(double) * G->vec_doubles, G->stream) != cudaSuccess) return ECMG_ECUDA;
   }
   G->prob = pb;
@@ -993,11 +1073,11 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
   for (int k = 2; k < G->L; ++k)
     for (int d = 0; d < 3; ++d) if (G->geom[k].n[d] % 4) return ECMG_EMISMATCH;
   if ((int)G->u.size() != G->L) {
-    for (double* p : G->u) cudaFree(p);
+    for (double* p : G->u) dfree(p);
     G->u.assign(G->L, nullptr);
   }
   for (int k = 0; k < k_end; ++k)   // per-level solutions, allocated on first use
-    if (!G->u[k] && cudaMalloc(&G->u[k], sizeof(double) * level_nodes(G->geom[k])) != cudaSuccess) {
+    if (!G->u[k] && dmalloc(&G->u[k], sizeof(double) * level_nodes(G->geom[k])) != cudaSuccess) {
       cudaGetLastError();
       return ECMG_ENOMEM;
     }
@@ -1005,7 +1085,7 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
   const bool u_dev = u_fine && is_device_ptr(u_fine);
   const long long Nf = level_nodes(G->geom[G->L - 1]);
   if (ut_fine && !ut_dev && !G->ut_tmp) {
-    if (cudaMalloc(&G->ut_tmp, sizeof(double) * Nf) != cudaSuccess) { cudaGetLastError(); return ECMG_ENOMEM; }
+    if (dmalloc(&G->ut_tmp, sizeof(double) * Nf) != cudaSuccess) { cudaGetLastError(); return ECMG_ENOMEM; }
   }
   int status = ECMG_OK;
   std::vector<ecmg_stats> stv(G->L);

@@ -254,4 +254,14 @@ cudaError_t launch_exp_true(const LevelGeom& gf, const Problem& pb, const double
                             double* ut, cudaStream_t st);
 cudaError_t launch_zero_vec(const LevelGeom& g, double* v, cudaStream_t st);
 
+// Device workspace allocation. The product build is cudaMalloc / cudaFree; the test build (libecmg_test.so,
+// -DECMG_TESTING, defined in ecmg_api.cu) surrounds every buffer with guard bands of a fixed byte pattern and
+// checks them on free and on request (ecmg_test_guard_check), the out-of-bounds-write check that stands in for
+// compute-sanitizer memcheck (closed on this GPU pool).
+cudaError_t dev_malloc(void** p, size_t bytes);
+void dev_free(void* p);
+template <class T>
+cudaError_t dmalloc(T** p, size_t bytes) { return dev_malloc(reinterpret_cast<void**>(p), bytes); }
+inline void dfree(void* p) { dev_free(p); }
+
 }  // namespace ecmg

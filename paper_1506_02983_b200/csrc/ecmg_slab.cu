@@ -533,7 +533,7 @@ SlabDriver* slab_driver_create(const SlabCfg& cfg, int P, int rank, bool virt, c
     const long long beta_n = beta_doubles(gf);
     const long long part_n = 3LL * ((gf.nf[0] + 7) / 8) * ((gf.nf[1] + 7) / 8) * (gf.nf[2] + 3) / 4 * 4 + 3 * 65536;
     auto alloc = [&](double** p, long long n) -> bool {
-      if (cudaMalloc(p, sizeof(double) * n) != cudaSuccess) { cudaGetLastError(); return false; }
+      if (dmalloc(p, sizeof(double) * n) != cudaSuccess) { cudaGetLastError(); return false; }
       return cudaMemset(*p, 0, sizeof(double) * n) == cudaSuccess;
     };
     bool ok = alloc(&c.x, vec) && alloc(&c.r, vec) && alloc(&c.z, vec) && alloc(&c.p[0], vec) && alloc(&c.p[1], vec) && alloc(&c.b, vec) &&
@@ -543,7 +543,7 @@ SlabDriver* slab_driver_create(const SlabCfg& cfg, int P, int rank, bool virt, c
               alloc(&c.seeds, (long long)(gf.n[0] / 2 + 1) * (gf.n[1] / 2 + 1) * (gf.n[2] / 2 + 1)) &&
               alloc(&c.ut, level_nodes(gf));
     if (ok) {
-      if (cudaMalloc(&c.sc, sizeof(JcgScalars)) != cudaSuccess || cudaMemset(c.sc, 0, sizeof(JcgScalars)) != cudaSuccess) ok = false;
+      if (dmalloc(&c.sc, sizeof(JcgScalars)) != cudaSuccess || cudaMemset(c.sc, 0, sizeof(JcgScalars)) != cudaSuccess) ok = false;
     }
     c.u.assign(cfg.L, nullptr);
     for (int k = 0; ok && k < cfg.L; ++k) ok = alloc(&c.u[k], level_nodes(make_geom(cfg.dom, cfg.n0, k, face_none, 1)));
@@ -596,10 +596,10 @@ void slab_driver_destroy(SlabDriver* d) {
         if (c.peer_r[s]) cudaIpcCloseMemHandle(c.peer_r[s]);
         if (c.peer_z[s]) cudaIpcCloseMemHandle(c.peer_z[s]);
       }
-    cudaFree(c.x); cudaFree(c.r); cudaFree(c.z); cudaFree(c.p[0]); cudaFree(c.p[1]); cudaFree(c.b); cudaFree(c.beta);
-    cudaFree(c.b_fin); cudaFree(c.beta_fin); cudaFree(c.s1d_fin);
-    cudaFree(c.partials); cudaFree(c.scratch1d); cudaFree(c.seeds); cudaFree(c.sc); cudaFree(c.ut);
-    for (double* p : c.u) cudaFree(p);
+    dfree(c.x); dfree(c.r); dfree(c.z); dfree(c.p[0]); dfree(c.p[1]); dfree(c.b); dfree(c.beta);
+    dfree(c.b_fin); dfree(c.beta_fin); dfree(c.s1d_fin);
+    dfree(c.partials); dfree(c.scratch1d); dfree(c.seeds); dfree(c.sc); dfree(c.ut);
+    for (double* p : c.u) dfree(p);
   }
   if (d->comm) nccl().CommDestroy(d->comm);
   if (d->sc_host) cudaFreeHost(d->sc_host);
