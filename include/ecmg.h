@@ -15,7 +15,9 @@
  *    Device pointers are required except where a parameter says "device or host".
  *    The caller owns them; the library reads / writes them only during the call.
  *  - The grid owns all internal workspace (pitched free-box vectors, element coefficients,
- *    reduction buffers); nothing the caller passes is retained after a call returns.
+ *    reduction buffers). Nothing the caller passes is retained after a call returns, with ONE
+ *    exception: the per-level device arrays of ECMG_PROB_ARRAYS (ecmg_problem.level_arrays), which
+ *    the grid keeps from ecmg_set_coeffs until the next ecmg_set_coeffs or ecmg_destroy_grid.
  *  - There is no CPU fallback: without a usable CUDA device ecmg_create_grid fails with
  *    ECMG_ECUDA.
  *  - A grid is not thread safe; distinct grids may be used from distinct threads.
@@ -87,7 +89,10 @@ typedef struct {
   ecmg_face_kind face[6];   /* x-, x+, y-, y+, z-, z+; must equal the problem's own boundary kinds */
   int problem_id;           /* ecmg_problem_id */
   const double* params;     /* host array, problem parameters (C5: 48 doubles, PATCH_LAYERED: 15,
-                               ARRAYS: 6 = alpha per face, read on Robin faces, >= 0) */
+                               ARRAYS: 6 = alpha per face, read on Robin faces, >= 0). alpha is ONE
+                               constant per face (P:44-47 allows a piecewise smooth alpha; this library
+                               takes the constant-per-face case, reading R6); a spatially
+                               varying alpha cannot be expressed and is not supported. Copied. */
   int n_params;
   /* ECMG_PROB_ARRAYS only (else NULL / 0): n_level_arrays = 4 * num_levels device pointers, level k's
    * data of Eq. (bvp) at the points the discretisation reads:
