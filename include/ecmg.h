@@ -154,8 +154,9 @@ typedef enum {
   ECMG_OPT_CTA_SOLVE = 13,   /* levels with at most this many free unknowns (default 1000, at most 4096)
                                 are solved by ONE CTA with every vector in shared memory (no grid barrier);
                                 0: off (the cooperative persistent kernel takes them) */
-  ECMG_OPT_PERS_TMA = 14,    /* levels with at most this many free unknowns (default 3000000, i.e. up to
-                                128^3; both operators) and more than ECMG_OPT_PERSISTENT run the whole
+  ECMG_OPT_PERS_TMA = 14,    /* levels with at most this many free unknowns (default 20000000, i.e. up to
+                                256^3; the element operator at most 3000000, i.e. 128^3, where it measured
+                                faster) and more than ECMG_OPT_PERSISTENT run the whole
                                 tolerance-stopped solve as ONE cooperative launch of TMA z-marching passes
                                 (no per-iteration kernel launches); 0: the CUDA-graph loop of K1 / K2 */
   ECMG_OPT_BETA_FLY = 15,    /* element-beta path, cubic cells, analytic beta (C3, C5, layers, beta = 1 with

@@ -157,7 +157,7 @@ struct ecmg_grid {
   int pdl = 0;              // ECMG_OPT_PDL: programmatic dependent launch between the JCG kernels (measured: no gain
                             // inside the CUDA graphs, tools/tune_pdl.py; off by default)
   long long cta_max = 1000;           // ECMG_OPT_CTA_SOLVE: one-CTA solve up to this many free unknowns (0: off)
-  long long pers_tma_max = 3000000;   // ECMG_OPT_PERS_TMA: constant stencil, one cooperative TMA solve up to this size
+  long long pers_tma_max = 20000000;  // ECMG_OPT_PERS_TMA: constant stencil, one cooperative TMA solve up to this size (256^3: 2.68 -> 2.29 ms per solve, tools/tts_ab.py)
   long long persistent_max = 40000;   // ECMG_OPT_PERSISTENT: register-resident cooperative solve up to this size (tools/tune_persistent.py:
                                       // 64^3 is faster as the cooperative TMA solve, 0.67 vs 0.82 ms on C4)
   double* aux[2] = {nullptr, nullptr};   // persistent element-path solve: w = A p and D^-1 (level-sized)
@@ -431,11 +431,15 @@ bool use_persistent(const ecmg_grid* G, const LevelGeom& g) {
 }
 
 // mid-size levels, constant stencil: the whole solve in one cooperative launch of TMA z-marching passes
+constexpr long long kElemPersTmaMax = 3000000;
+
 bool use_pers_tma(ecmg_grid* G, const LevelGeom& g) {
   if (G->pers_tma_max <= 0 || free_count(g) > G->pers_tma_max) return false;
   // the cooperative launch needs every (x, y) tile resident at once: wide, flat levels (or a GPU with
   // fewer SMs) take the graph path instead
-  if (G->elem_path) return elem_pers_fits(g);
+  // the element operator's cooperative solve is capped at 128^3: at C3's 256^3 it measured slower than the
+  // graph loop of K1 / K2 (32.5 -> 37.4 ms for the level, tools/tts_ab.py)
+  if (G->elem_path) return free_count(g) <= kElemPersTmaMax && elem_pers_fits(g);
   return const_pers_fits(g) && G->kernel_variant == 1 && ensure_maps(G, g, level_of(G, g));
 }
 

@@ -461,7 +461,14 @@ cudaError_t launch_jcg_const_pers(const LevelGeom& g, const ConstStencil& cs, do
   const long long tiles = (long long)ntx * nty;
   if (tiles > slots || g.zbeg != 0) return cudaErrorInvalidValue;
   const int nch = (int)std::max(1LL, slots / tiles);          // z chunks per tile
-  const int zc = (nz + nch - 1) / nch;
+#ifndef PERS_MIN_ZC
+// at least 4 planes per (tile, chunk) item: the 64^3 level then runs on 64 CTAs instead of 252 and leaves most
+// SMs to the finest level's right-hand side, which the setup-ahead stream runs beside the coarse solves.
+// Measured on C4 (tools/tts_ab.py, 11 interleaved runs): 64^3 solve 0.66 -> 0.89 ms, but the finest level no
+// longer waits 0.43 ms for its setup; TTS 15.20 -> 14.96 ms (with the 256^3 level on this solve, below)
+#define PERS_MIN_ZC 4
+#endif
+  const int zc = std::max(PERS_MIN_ZC, (nz + nch - 1) / nch);
   const int items = (int)(tiles * ((nz + zc - 1) / zc));
   PersMaps M{maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6]};
   int grid = std::min(items, slots);
