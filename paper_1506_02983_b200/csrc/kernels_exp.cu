@@ -171,13 +171,19 @@ __global__ void __launch_bounds__(64) k_exp_interp(const LevelGeom gf, const Pro
 // forms, from which staged values) is fixed per thread and computed once before the z-march. HBM traffic:
 // the fine level written once (8 B / node) plus ~1/8 + 1/64 of it read. Results equal the two-pass blending
 // evaluation (k_exp_seeds + k_exp_interp) to rounding (tests/test_gpu_parity.py).
-constexpr int XB = 16, YB = 2;                                 // 4h blocks per tile
+#ifndef EXP_YB
+#define EXP_YB 2
+#endif
+constexpr int XB = 16, YB = EXP_YB;                            // 4h blocks per tile
 constexpr int FXT = 4 * XB + 1, FYT = 4 * YB + 1;              // fine nodes per tile incl. the last node
 constexpr int S2X = 2 * XB + 1, S2Y = 2 * YB + 1;              // 2h nodes per tile plane
 constexpr int FNTH = 256;
 constexpr int N1 = 3 * S2Y * S2X, N0 = 2 * (YB + 1) * (XB + 1);   // staged u_2h / u_4h values per layer
-static_assert(FNTH == 4 * 64 && FXT == 65 && FYT == 9, "thread map: (fine column, fine plane) = (tid & 63, tid >> 6)");
-static_assert(N1 <= 2 * FNTH && N0 <= FNTH, "staging: two u_2h and one u_4h value per thread");
+constexpr int NQ = (N1 + FNTH - 1) / FNTH;                        // u_2h values (and 2h nodes) per thread
+constexpr int NCK1 = S2Y * S2X - (YB + 1) * (XB + 1), NCK0 = YB * XB;   // face / cell centres (k = 1; k = 0, 2)
+constexpr int NCQ = (NCK1 + 2 * NCK0 + FNTH - 1) / FNTH;
+static_assert(FNTH == 4 * 64 && FXT == 65, "thread map: (fine column, fine plane) = (tid & 63, tid >> 6)");
+static_assert(N0 <= FNTH && N1 < 1024, "per-thread maps");
 
 // 1D quadratic through the 2h nodes (t = -1, 0, 1) of a 4h block at fine offset l = 0..4 (t = (l - 2) / 2)
 __device__ __forceinline__ void q2w(int l, double& w0, double& w1, double& w2) {
@@ -192,7 +198,7 @@ __device__ __forceinline__ int f4(int i, int j, int k) { return i + (XB + 1) * (
 
 template <bool FREEBOX, int VARIANT>
 #ifndef EXP_FUSED_MINB
-#define EXP_FUSED_MINB 3
+#define EXP_FUSED_MINB 4   // 64 registers, 4 CTAs / SM: 512^3 in-run 0.387 -> 0.369 ms (3 CTAs: 0.387; 5: spills, 0.434)
 #endif
 __global__ void __launch_bounds__(FNTH, EXP_FUSED_MINB) k_exp_fused(const LevelGeom gf, const double* __restrict__ u2h,
                                                                     const double* __restrict__ u4h, double* __restrict__ out,
@@ -204,70 +210,70 @@ __global__ void __launch_bounds__(FNTH, EXP_FUSED_MINB) k_exp_fused(const LevelG
   const int tid = threadIdx.x;
   const int n4x = gf.n[0] / 4, n4y = gf.n[1] / 4, n4z = gf.n[2] / 4;
   const int n2x = gf.n[0] / 2, n2y = gf.n[1] / 2;
-  const long long nn2x = n2x + 1, nn2y = n2y + 1;
-  const long long nn4x = n4x + 1, nn4y = n4y + 1;
+  const int nn2x = n2x + 1, nn2y = n2y + 1, nn4x = n4x + 1, nn4y = n4y + 1;
   const int bx0 = blockIdx.x * XB, by0 = blockIdx.y * YB;
   const int nbx = min(XB, n4x - bx0), nby = min(YB, n4y - by0);   // blocks in this tile
   const int X0 = 4 * bx0, Y0 = 4 * by0;
   const int nfx = 4 * nbx + (bx0 + nbx == n4x ? 1 : 0);          // fine nodes of the tile along x
   const int nfy = 4 * nby + (by0 + nby == n4y ? 1 : 0);
-  const int I0 = 2 * bx0, J0 = 2 * by0;
   const long long nx = gf.n[0] + 1, ny = gf.n[1] + 1;
   const int bzs = bzA + blockIdx.z * lchunk, bze = min(bzs + lchunk, n4z);
+  const long long pl2 = (long long)nn2x * nn2y, pl4 = (long long)nn4x * nn4y;
+  const double* u2t = u2h + 2 * bx0 + (long long)nn2x * 2 * by0;   // the tile's corner on 2h plane 0
+  const double* u4t = u4h + bx0 + (long long)nn4x * by0;
   // ---- per-thread maps, fixed for the whole z-march ------------------------------------------------------
-  // staging: u_2h values t = tid, tid + 256 (f2 order), u_4h value tid (f4 order)
-  long long o1[2];
-  bool v1[2];
+  // staging: u_2h values t = tid + 256 q (f2 order) at offset i + nn2x (j + nn2y k) from the layer's corner
+  // (-1: outside the domain / tile); the u_4h value tid likewise
+  int so1[NQ];
 #pragma unroll
-  for (int r = 0; r < 2; ++r) {
-    const int t = tid + r * FNTH;
+  for (int q = 0; q < NQ; ++q) {
+    const int t = tid + q * FNTH;
     const int i = t % S2X, j = (t / S2X) % S2Y, k = t / (S2X * S2Y);
-    v1[r] = t < N1 && I0 + i <= n2x && J0 + j <= n2y;
-    o1[r] = (I0 + i) + nn2x * ((J0 + j) + nn2y * (long long)k);   // + (2 bz) nn2x nn2y per layer
+    so1[q] = (t < N1 && 2 * bx0 + i <= n2x && 2 * by0 + j <= n2y) ? i + nn2x * (j + nn2y * k) : -1;
   }
-  const int i0 = tid % (XB + 1), j0 = (tid / (XB + 1)) % (YB + 1), k0 = tid / ((XB + 1) * (YB + 1));
-  const bool v0 = tid < N0 && bx0 + i0 <= n4x && by0 + j0 <= n4y;
-  const long long o0 = (bx0 + i0) + nn4x * ((by0 + j0) + nn4y * (long long)k0);
-  const long long pl2 = nn2x * nn2y, pl4 = nn4x * nn4y;
-  // 2h-node values, nodes t = tid, tid + 256: kind 0 corner (Eq. jiedian), 1 edge midpoint (Eq. zhongdian:
-  // U1 at t plus the differences at its two 4h-coincident neighbours t -/+ e), 2 face / cell centre
-  int sk[2], se[2], su[3][2];
+  int so0;
+  {
+    const int i = tid % (XB + 1), j = (tid / (XB + 1)) % (YB + 1), k = tid / ((XB + 1) * (YB + 1));
+    so0 = (tid < N0 && bx0 + i <= n4x && by0 + j <= n4y) ? i + nn4x * (j + nn4y * k) : -1;
+  }
+  // 2h-node values of nodes t = tid + 256 q, packed: kind (bits 0-1: 0 corner, 1 edge midpoint, 2 centre),
+  // stride of the midpoint's odd axis (bits 2-11), its two 4h-coincident ends in U0s (bits 12-20, 21-29; a
+  // corner: its own 4h node in bits 12-20)
+  int sm[NQ];
 #pragma unroll
-  for (int r = 0; r < 2; ++r) {
-    const int t = min(tid + r * FNTH, N1 - 1);
+  for (int q = 0; q < NQ; ++q) {
+    const int t = min(tid + q * FNTH, N1 - 1);
     const int i = t % S2X, j = (t / S2X) % S2Y, k = t / (S2X * S2Y);
     const int oi = i & 1, oj = j & 1, ok = k & 1, nodd = oi + oj + ok;
-    sk[r] = nodd == 0 ? 0 : nodd == 1 ? 1 : 2;
-    se[r] = f2(oi, oj, ok);
-    su[0][r] = f4(i >> 1, j >> 1, k >> 1);                                   // corner: its own 4h node
-    su[1][r] = f4((i - oi) >> 1, (j - oj) >> 1, (k - ok) >> 1);              // midpoint: the two ends
-    su[2][r] = f4((i + oi) >> 1, (j + oj) >> 1, (k + ok) >> 1);
+    const int kind = nodd == 0 ? 0 : nodd == 1 ? 1 : 2;
+    const int a = nodd == 0 ? f4(i >> 1, j >> 1, k >> 1) : f4((i - oi) >> 1, (j - oj) >> 1, (k - ok) >> 1);
+    const int b = f4((i + oi) >> 1, (j + oj) >> 1, (k + ok) >> 1);
+    sm[q] = kind | (f2(oi, oj, ok) << 2) | (a << 12) | (b << 21);
   }
-  // Serendipity face / cell centres (VARIANT 0): the tile's 2h nodes with >= 2 odd indices, one per thread:
-  // k odd: (i or j odd) -> 2 odd with k, or 3; k even: i and j odd
-  int ct = -1, ce = 0, cf = 0, cc = 0;   // node, unit strides along its two odd axes, 1 = cell centre
-  if (VARIANT == 0) {
-    int c = tid;
-    constexpr int NK1 = S2Y * S2X - (YB + 1) * (XB + 1);   // k = 1 plane: nodes with i or j odd
-    constexpr int NK0 = YB * XB;                            // k = 0 / 2 planes: i and j odd
-    if (c < NK1) {
-      // enumerate the k = 1 plane, skipping the (even, even) nodes
+  // Serendipity face / cell centres (VARIANT 0): nodes c = tid + 256 q of the tile's 2h nodes with >= 2 odd
+  // indices (k = 1: i or j odd; k = 0, 2: i and j odd), packed: node (bits 0-9), strides e, f of its two odd
+  // axes (bits 10-19, 20-29; a face centre), bit 30 = cell centre; -1 = none
+  int cm[NCQ];
+#pragma unroll
+  for (int q = 0; q < NCQ; ++q) {
+    cm[q] = -1;
+    int c = tid + q * FNTH;
+    if (VARIANT != 0) continue;
+    if (c < NCK1) {
       int i = 0, j = 0, m = c;
       for (j = 0; j < S2Y; ++j) {
-        const int cnt = (j & 1) ? S2X : XB;   // odd row: all; even row: odd i only
+        const int cnt = (j & 1) ? S2X : XB;   // odd row: every node; even row: odd i only
         if (m < cnt) { i = (j & 1) ? m : 2 * m + 1; break; }
         m -= cnt;
       }
-      ct = f2(i, j, 1);
-      cc = (i & 1) && (j & 1);
-      ce = (i & 1) ? f2(1, 0, 0) : f2(0, 1, 0);
-      cf = ((i & 1) && !(j & 1)) || (!(i & 1) && (j & 1)) ? f2(0, 0, 1) : 0;
-    } else if (c < NK1 + 2 * NK0) {
-      c -= NK1;
-      const int k = 2 * (c / NK0), m = c % NK0;
-      ct = f2(2 * (m % XB) + 1, 2 * (m / XB) + 1, k);
-      ce = f2(1, 0, 0);
-      cf = f2(0, 1, 0);
+      const int cell = (i & 1) && (j & 1);
+      const int e = (i & 1) ? f2(1, 0, 0) : f2(0, 1, 0);
+      const int f = cell ? 0 : f2(0, 0, 1);
+      cm[q] = f2(i, j, 1) | (e << 10) | (f << 20) | (cell << 30);
+    } else if (c < NCK1 + 2 * NCK0) {
+      c -= NCK1;
+      const int k = 2 * (c / NCK0), m = c % NCK0;
+      cm[q] = f2(2 * (m % XB) + 1, 2 * (m / XB) + 1, k) | (f2(1, 0, 0) << 10) | (f2(0, 1, 0) << 20);
     }
   }
   // x pass: lane lx of a line reads 2h nodes xb .. xb+2 with weights (wx0, wx1, wx2) -- a unit weight on an
@@ -306,33 +312,36 @@ __global__ void __launch_bounds__(FNTH, EXP_FUSED_MINB) k_exp_fused(const LevelG
       if (r >= rlo && r < rhi) o[r * rstride] = W;   // full output: Dirichlet nodes by launch_exp_finite's face fill
     }
   };
-  double r1[2] = {0.0, 0.0}, r0 = 0.0;
+  double r1[NQ], r0 = 0.0;
   auto fetch = [&](int bz) {
+    const double* b2 = u2t + 2LL * bz * pl2;
 #pragma unroll
-    for (int r = 0; r < 2; ++r) r1[r] = v1[r] ? __ldg(u2h + o1[r] + 2LL * bz * pl2) : 0.0;
-    r0 = v0 ? __ldg(u4h + o0 + (long long)bz * pl4) : 0.0;
+    for (int q = 0; q < NQ; ++q) r1[q] = so1[q] >= 0 ? __ldg(b2 + so1[q]) : 0.0;
+    r0 = so0 >= 0 ? __ldg(u4t + (long long)bz * pl4 + so0) : 0.0;
   };
   if (bzs < bze) fetch(bzs);
   for (int bz = bzs; bz < bze; ++bz) {
     const int fz0 = 4 * bz, nfz = (bz == n4z - 1) ? 5 : 4;
     const int pz0 = max(fz0, F0), pz1 = min(fz0 + nfz, F1);   // fine planes of this layer to write
     __syncthreads();   // previous layer's tiles consumed
-    U1s[tid] = r1[0];
-    if (tid + FNTH < N1) U1s[tid + FNTH] = r1[1];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+      if (tid + q * FNTH < N1) U1s[tid + q * FNTH] = r1[q];
     if (tid < N0) U0s[tid] = r0;
     if (bz + 1 < bze) fetch(bz + 1);   // next layer's loads in flight during this layer's work
     __syncthreads();
     if (pz0 >= pz1) continue;
     // the 2h-node values
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const int t = tid + r * FNTH;
+    for (int q = 0; q < NQ; ++q) {
+      const int t = tid + q * FNTH;
       if (t >= N1) break;
+      const int kind = sm[q] & 3, se = (sm[q] >> 2) & 1023, ua = (sm[q] >> 12) & 511, ub = (sm[q] >> 21) & 511;
       double v = 0.0;
-      if (sk[r] == 0) {
-        v = (5.0 * U1s[t] - U0s[su[0][r]]) / 4.0;                                          // Eq. (jiedian)
-      } else if (sk[r] == 1) {
-        v = U1s[t] + ((U1s[t - se[r]] - U0s[su[1][r]]) + (U1s[t + se[r]] - U0s[su[2][r]])) / 8.0;   // Eq. (zhongdian)
+      if (kind == 0) {
+        v = (5.0 * U1s[t] - U0s[ua]) / 4.0;                                               // Eq. (jiedian)
+      } else if (kind == 1) {
+        v = U1s[t] + ((U1s[t - se] - U0s[ua]) + (U1s[t + se] - U0s[ub])) / 8.0;           // Eq. (zhongdian)
       } else if (VARIANT == 1) {   // Remark 2: mean of Eq. (zhongdian) over the diagonals through the node
         const int i = t % S2X, j = (t / S2X) % S2Y, k = t / (S2X * S2Y);
         const int odd[3] = {i & 1, j & 1, k & 1};
@@ -344,7 +353,7 @@ __global__ void __launch_bounds__(FNTH, EXP_FUSED_MINB) k_exp_fused(const LevelG
         for (int sgn = 0; sgn < nseg; ++sgn) {
           int oa[3] = {0, 0, 0};
           oa[ax[0]] = -1;
-          for (int q = 1; q < na; ++q) oa[ax[q]] = ((sgn >> (q - 1)) & 1) ? -1 : 1;
+          for (int qq = 1; qq < na; ++qq) oa[ax[qq]] = ((sgn >> (qq - 1)) & 1) ? -1 : 1;
           sum += U1s[t] + (D(i + oa[0], j + oa[1], k + oa[2]) + D(i - oa[0], j - oa[1], k - oa[2])) / 8.0;
         }
         v = sum / nseg;
@@ -353,13 +362,17 @@ __global__ void __launch_bounds__(FNTH, EXP_FUSED_MINB) k_exp_fused(const LevelG
     }
     __syncthreads();
     if (VARIANT == 0) {   // Serendipity: the face and cell centres from the block's corners and midpoints
-      if (ct >= 0) {
+#pragma unroll
+      for (int q = 0; q < NCQ; ++q) {
+        if (cm[q] < 0) continue;
+        const int ct = cm[q] & 1023;
         double v;
-        if (!cc) {   // face centre: midpoints at +-e, +-f, corners at +-e+-f
+        if (!(cm[q] >> 30)) {   // face centre: midpoints at +-e, +-f, corners at +-e+-f
+          const int ce = (cm[q] >> 10) & 1023, cf = (cm[q] >> 20) & 1023;
           const double mids = Ss[ct + ce] + Ss[ct - ce] + Ss[ct + cf] + Ss[ct - cf];
           const double corn = Ss[ct + ce + cf] + Ss[ct + ce - cf] + Ss[ct - ce + cf] + Ss[ct - ce - cf];
           v = 0.5 * mids - 0.25 * corn;
-        } else {     // cell centre
+        } else {                // cell centre
           constexpr int X = 1, Y = S2X, Zs = S2X * S2Y;
           const double mids = Ss[ct + Y + Zs] + Ss[ct - Y + Zs] + Ss[ct + Y - Zs] + Ss[ct - Y - Zs] +
                               Ss[ct + X + Zs] + Ss[ct - X + Zs] + Ss[ct + X - Zs] + Ss[ct - X - Zs] +
