@@ -219,6 +219,7 @@ SlabCfg slab_cfg(const ecmg_grid* G) {
   c.fused_halo = G->fused_halo;
   c.beta_fly = G->beta_fly;
   c.shard_min = G->shard_min;
+  c.use_graph = G->use_graph;
   return c;
 }
 

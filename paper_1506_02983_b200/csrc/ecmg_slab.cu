@@ -21,10 +21,12 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <utility>
 #include <vector>
 
 #include "host_common.h"
@@ -127,6 +129,14 @@ struct SlabDriver {
   cudaStream_t ahead_stream = nullptr;
   cudaEvent_t ahead_ev = nullptr, fork_ev = nullptr;
   bool fin_ahead = false;
+  // device-driven loop of the sharded levels: one instantiated graph per level (built on first use, dropped
+  // when the configuration changes); graph_failed: capture / instantiation failed once (e.g. a communication
+  // backend that cannot be captured), the host loop is used from then on
+  std::vector<cudaGraphExec_t> graphs;
+  cudaStream_t cap_stream = nullptr;
+  bool graph_failed = false;
+  std::vector<std::pair<int, int>> graph_launches;   // per level: kernels of prologue + epilogue, of one body
+  int cap_count[3] = {0, 0, 0};
 };
 
 namespace {
@@ -325,6 +335,8 @@ int slab_jcg(SlabDriver* d, int k, double eps, int max_iter, ecmg_stats* st, cud
   d->param_host->u_out = nullptr;
   for (int i = 0; i < nloc; ++i)
     SL_CUDA(cudaMemcpyAsync(&d->s[i].sc->in, d->param_host, sizeof(JcgParams), cudaMemcpyHostToDevice, stream));
+  const cudaStream_t user_stream = stream;   // the work below goes to `stream`; graph capture points it elsewhere
+  KArgs cond{};                              // the WHILE node's handle for the finalize kernels (graph build only)
   // one pass of `mode` over all local slabs (+ allreduce and finalize when sharded)
   auto pass = [&](int mode, auto fill) -> int {
     for (int i = 0; i < nloc; ++i) {
@@ -335,12 +347,16 @@ int slab_jcg(SlabDriver* d, int k, double eps, int max_iter, ecmg_stats* st, cud
     if (sh) {
       int r = comm_allreduce(d, stream);
       if (r) return r;
-      for (int i = 0; i < nloc; ++i) SL_CUDA(launch_finalize(mode, base_args(d, d->s[i], k, sh), stream));
+      for (int i = 0; i < nloc; ++i) {
+        KArgs af = base_args(d, d->s[i], k, sh);
+        af.use_cond = cond.use_cond; af.cond = cond.cond;
+        SL_CUDA(launch_finalize(mode, af, stream));
+      }
     }
     return ECMG_OK;
   };
   int rc;
-  if (sh) {
+  auto zero_boundary_halos = [&]() -> int {
     // halo planes at the global z boundary stand for Dirichlet / outside nodes: they must read as 0
     // (the buffers were used by earlier levels with other geometries)
     for (int i = 0; i < nloc; ++i) {
@@ -353,8 +369,8 @@ int slab_jcg(SlabDriver* d, int k, double eps, int max_iter, ecmg_stats* st, cud
         if (c.rank == d->P - 1) SL_CUDA(cudaMemsetAsync(v + (long long)g.zend * g.S, 0, plane, stream));
       }
     }
-  }
-  if (sh && (rc = comm_halo(d, k, 0, stream))) return rc;
+    return ECMG_OK;
+  };
   // K1 reads r (constant stencil) or z = D^-1 r (element path) on its halo planes. Fused halo: the init
   // and K2 passes store their boundary planes of that vector straight into the neighbours' halo planes
   // (peer memory); the allreduce that follows every pass orders those stores before the next K1.
@@ -372,12 +388,18 @@ int slab_jcg(SlabDriver* d, int k, double eps, int max_iter, ecmg_stats* st, cud
     a.peer_lo = c.rank > 0 ? base[0] + (long long)c.nb_lo_zend[k] * g.S : nullptr;
     a.peer_hi = c.rank + 1 < d->P ? base[1] + (long long)(c.nb_hi_zbeg[k] - 1) * g.S : nullptr;
   };
-  if ((rc = pass(MODE_INIT, [&](SlabCtx& c, KArgs& a) {
-         a.h0 = c.x; a.i0 = bvec(d, c, k); a.o0 = c.r; a.o1 = c.z;
-         set_peers(c, a);
-       })))
-    return rc;
-  if (sh && !fused && (rc = comm_halo(d, k, k1_vec, stream))) return rc;   // halo planes for the first K1
+  auto prologue = [&]() -> int {   // boundary halos, x halo, init pass (r = b - A x, rho, rr, ||b||)
+    int q;
+    if (sh && (q = zero_boundary_halos())) return q;
+    if (sh && (q = comm_halo(d, k, 0, stream))) return q;
+    if ((q = pass(MODE_INIT, [&](SlabCtx& c, KArgs& a) {
+           a.h0 = c.x; a.i0 = bvec(d, c, k); a.o0 = c.r; a.o1 = c.z;
+           set_peers(c, a);
+         })))
+      return q;
+    if (sh && !fused && (q = comm_halo(d, k, k1_vec, stream))) return q;   // halo planes for the first K1
+    return ECMG_OK;
+  };
   long long it = 0;
   auto iteration = [&]() -> int {
     int q = pass(MODE_K1, [&](SlabCtx& c, KArgs& a) { a.h0 = elem ? c.z : c.r; a.h1 = c.p[it & 1]; a.o0 = c.p[(it + 1) & 1]; });
@@ -391,6 +413,98 @@ int slab_jcg(SlabDriver* d, int k, double eps, int max_iter, ecmg_stats* st, cud
     ++it;
     return ECMG_OK;
   };
+  auto epilogue = [&]() -> int {   // x halo, true residual ||b - A x||
+    int q;
+    if (sh && (q = comm_halo(d, k, 0, stream))) return q;
+    return pass(MODE_TRUE, [&](SlabCtx& c, KArgs& a) { a.h0 = c.x; a.i0 = bvec(d, c, k); });
+  };
+  // Device-driven solve of a sharded level (Alg. 4 l.7-9 without host round trips): one CUDA graph =
+  // prologue -> WHILE(cond){2 iterations: K1, allreduce, finalize, K2, allreduce, finalize (sets cond =
+  // !done), halo} -> epilogue, captured once per level. Every rank's finalize sees the same allreduced
+  // scalars, so all ranks run the same number of bodies (matching communication sequences); a
+  // speculative second iteration after convergence is a no-op (the kernels and finalize check done).
+  auto build_graph = [&](cudaGraphExec_t* out) -> int {
+    if (!d->cap_stream) SL_CUDA(cudaStreamCreateWithFlags(&d->cap_stream, cudaStreamNonBlocking));
+    cudaGraph_t graph = nullptr;
+    SL_CUDA(cudaGraphCreate(&graph, 0));
+    cudaGraphConditionalHandle h;
+    cudaGraphNode_t cond_node = nullptr;
+    std::vector<cudaGraphNode_t> leaves;
+    int q = ECMG_OK;
+    auto fail = [&](int code) { cudaStreamEndCapture(d->cap_stream, &graph); cudaGetLastError(); cudaGraphDestroy(graph); stream = user_stream; cond.use_cond = 0; return code; };
+    if (cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault) != cudaSuccess) return fail(ECMG_ECUDA);
+    cond.use_cond = 1; cond.cond = h;
+    stream = d->cap_stream;
+    if (cudaStreamBeginCaptureToGraph(stream, graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return fail(ECMG_ECUDA);
+    long long lc = ecmg_kernel_launches();
+    if ((q = prologue())) return fail(q);
+    if (cudaStreamEndCapture(stream, &graph) != cudaSuccess) return fail(ECMG_ECUDA);
+    d->cap_count[0] = (int)(ecmg_kernel_launches() - lc);
+    {   // the prologue's sinks (nodes without successors): the WHILE node follows them
+      size_t nn = 0, ne = 0;
+      if (cudaGraphGetNodes(graph, nullptr, &nn) != cudaSuccess || cudaGraphGetEdges(graph, nullptr, nullptr, &ne) != cudaSuccess)
+        return fail(ECMG_ECUDA);
+      std::vector<cudaGraphNode_t> nodes(nn), from(ne), to(ne);
+      if (cudaGraphGetNodes(graph, nodes.data(), &nn) != cudaSuccess ||
+          (ne && cudaGraphGetEdges(graph, from.data(), to.data(), &ne) != cudaSuccess))
+        return fail(ECMG_ECUDA);
+      for (cudaGraphNode_t nd : nodes)
+        if (std::find(from.begin(), from.end(), nd) == from.end()) leaves.push_back(nd);
+      if (leaves.empty()) return fail(ECMG_ECUDA);
+    }
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    if (cudaGraphAddNode(&cond_node, graph, leaves.data(), leaves.size(), &cp) != cudaSuccess) return fail(ECMG_ECUDA);
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    if (cudaStreamBeginCaptureToGraph(stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return fail(ECMG_ECUDA);
+    it = 0;
+    lc = ecmg_kernel_launches();
+    if ((q = iteration()) || (q = iteration())) return fail(q);   // p ping-pong: two iterations per body
+    if (cudaStreamEndCapture(stream, &body) != cudaSuccess) return fail(ECMG_ECUDA);
+    d->cap_count[1] = (int)(ecmg_kernel_launches() - lc);
+    cond.use_cond = 0;
+    if (cudaStreamBeginCaptureToGraph(stream, graph, &cond_node, nullptr, 1, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return fail(ECMG_ECUDA);
+    lc = ecmg_kernel_launches();
+    if ((q = epilogue())) return fail(q);
+    if (cudaStreamEndCapture(stream, &graph) != cudaSuccess) return fail(ECMG_ECUDA);
+    d->cap_count[2] = (int)(ecmg_kernel_launches() - lc);
+    stream = user_stream;
+    const cudaError_t e = cudaGraphInstantiate(out, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) { cudaGetLastError(); *out = nullptr; return ECMG_ECUDA; }
+    return ECMG_OK;
+  };
+  if (sh && eps > 0.0 && d->cfg.use_graph && !d->graph_failed) {
+    if ((int)d->graphs.size() != d->L) d->graphs.assign(d->L, nullptr);
+    if ((int)d->graph_launches.size() != d->L) d->graph_launches.assign(d->L, {0, 0});
+    if (!d->graphs[k]) {
+      // kernels are counted when they run, not when they are captured: the per-part counts are kept
+      const long long l0 = ecmg_kernel_launches();
+      const int q = build_graph(&d->graphs[k]);
+      d->graph_launches[k] = {d->cap_count[0] + d->cap_count[2], d->cap_count[1]};
+      count_launch((int)(l0 - ecmg_kernel_launches()));
+      if (q != ECMG_OK) {
+        d->graph_failed = true;   // host loop below
+        if (std::getenv("ECMG_DEBUG")) std::fprintf(stderr, "libecmg(slab): graph capture failed at level %d; host loop\n", k);
+      }
+    }
+    if (d->graphs[k]) {
+      SL_CUDA(cudaEventRecord(d->ev[0], stream));
+      SL_CUDA(cudaGraphLaunch(d->graphs[k], stream));
+      SL_CUDA(cudaEventRecord(d->ev[1], stream));
+      const int status = read_stats(d, k, eps, st, stream);
+      count_launch(d->graph_launches[k].first + d->graph_launches[k].second * ((d->last_jcg_iters + 1) / 2));
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, d->ev[0], d->ev[1]);
+      d->last_jcg_ms = ms;   // prologue + loop + true residual (the host loop times the loop only)
+      return status;
+    }
+  }
+  if ((rc = prologue())) return rc;
+  it = 0;
   SL_CUDA(cudaEventRecord(d->ev[0], stream));
   if (eps <= 0.0) {
     for (int i = 0; i < max_iter; ++i)
@@ -418,8 +532,7 @@ int slab_jcg(SlabDriver* d, int k, double eps, int max_iter, ecmg_stats* st, cud
     }
   }
   SL_CUDA(cudaEventRecord(d->ev[1], stream));
-  if (sh && (rc = comm_halo(d, k, 0, stream))) return rc;
-  if ((rc = pass(MODE_TRUE, [&](SlabCtx& c, KArgs& a) { a.h0 = c.x; a.i0 = bvec(d, c, k); }))) return rc;
+  if ((rc = epilogue())) return rc;
   const int status = read_stats(d, k, eps, st, stream);
   float ms = 0.f;
   cudaEventElapsedTime(&ms, d->ev[0], d->ev[1]);
@@ -567,6 +680,8 @@ SlabDriver* slab_driver_create(const SlabCfg& cfg, int P, int rank, bool virt, c
 }
 
 void slab_driver_configure(SlabDriver* d, const SlabCfg& cfg) {
+  for (cudaGraphExec_t& gx : d->graphs)   // captured for the previous configuration
+    if (gx) { cudaGraphExecDestroy(gx); gx = nullptr; }
   d->cfg = cfg;
   d->fin_ahead = false;   // a pending ahead setup belongs to the previous configuration
   for (auto& c : d->s) {
@@ -606,6 +721,9 @@ void slab_driver_destroy(SlabDriver* d) {
   if (d->param_host) cudaFreeHost(d->param_host);
   cudaGetLastError();
   if (d->ahead_stream) cudaStreamDestroy(d->ahead_stream);
+  for (cudaGraphExec_t gx : d->graphs)
+    if (gx) cudaGraphExecDestroy(gx);
+  if (d->cap_stream) cudaStreamDestroy(d->cap_stream);
   if (d->ahead_ev) cudaEventDestroy(d->ahead_ev);
   if (d->fork_ev) cudaEventDestroy(d->fork_ev);
   delete d;

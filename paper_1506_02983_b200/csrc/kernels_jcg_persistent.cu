@@ -214,6 +214,42 @@ __device__ __forceinline__ void stage(const LevelGeom& g, const Brick& br, const
   }
 }
 
+// The halo windows of all nb bricks of a CTA (origins in sb[3 i ..]), in batches of 8 loads per thread that
+// are all in flight together (one L2 latency per batch instead of one per value); values as in stage().
+template <bool FORM, int NBMAX>
+__device__ __forceinline__ void stage_all(const LevelGeom& g, const int* sb, int nb, const double* zsrc, const double* pold,
+                                          double zscale, double bcg, double* s) {
+  const int tot = nb * SN;
+  for (int base = 0; base < tot; base += 8 * PNTH) {
+    double v[8], w[8];
+    int o[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int t = base + q * PNTH + threadIdx.x;
+      o[q] = -1;
+      if (t < tot) {
+        const int i = t / SN, h = t - i * SN;
+        const int hx = h % SX, hy = (h / SX) % SY, hz = h / (SX * SY);
+        const int x = sb[3 * i] - 1 + hx, y = sb[3 * i + 1] - 1 + hy, z = sb[3 * i + 2] - 1 + hz;
+        if (x >= 0 && x < g.nf[0] && y >= 0 && y < g.nf[1] && z >= 0 && z < g.nf[2]) o[q] = z * (int)g.S + y * (int)g.P + x;
+      }
+      v[q] = o[q] >= 0 ? __ldcg(zsrc + o[q]) : 0.0;
+      w[q] = (FORM && bcg != 0.0 && o[q] >= 0) ? __ldcg(pold + o[q]) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int t = base + q * PNTH + threadIdx.x;
+      if (t >= tot) break;
+      double val = v[q];
+      if (FORM) {
+        val *= zscale;
+        if (bcg != 0.0) val = __fma_rn(bcg, w[q], val);
+      }
+      s[t] = val;
+    }
+  }
+}
+
 __device__ __forceinline__ void window27(const double* s, int lx, int ly, int lz, double p27[3][3][3]) {
 #pragma unroll
   for (int dz = 0; dz < 3; ++dz)
@@ -234,17 +270,55 @@ __device__ __forceinline__ double apply_node(const LevelGeom& g, const ConstSten
   return apply_const(cs, p27);
 }
 
-// Each CTA owns at most MAXB bricks (k = blockIdx.x + i gridDim.x) for the whole solve, and each thread
+// Each CTA owns at most MB bricks (k = blockIdx.x + i gridDim.x) for the whole solve, and each thread
 // keeps its nodes' x, r, D^-1, p_new and A p_new in registers: phase 2 needs no global loads, A p is never
 // stored, x is stored once at the end. Only the halo exchange goes through L2: z (element path) or r
-// (constant path, z = D^-1 r with D constant) and p_new.
-constexpr int MAXB = 4;
+// (constant path, z = D^-1 r with D constant) and p_new. The halo windows of all of a CTA's bricks are
+// staged in one round of loads (one L2 latency per phase, not one per brick).
+// Two launch forms:
+//  * cooperative (CL = false): up to MAXB = 4 bricks per CTA, grid reductions through L2 partials and
+//    grid.sync (measured 1.2 us per barrier);
+//  * one thread-block cluster (CL = true, <= 16 CTAs of one brick each): the levels of at most 16 bricks
+//    (16^3 cells). The reductions go through distributed shared memory -- every CTA publishes its block sum
+//    in its own shared memory, one cluster barrier (release / acquire: it also orders the global halo
+//    stores), then every CTA reads the C sums in rank order, so every CTA holds the bitwise same total --
+//    and the solve occupies at most 16 SMs, leaving the rest of the GPU to the setups that run ahead beside
+//    the coarse solves. Measured on C4 (tools/tts_ab.py): 16^3 0.225 -> 0.179 ms; at 32^3 (128 bricks: 8
+//    per CTA of a 16-CTA cluster) 0.364 -> 0.549 ms, so 32^3 stays on the cooperative form.
+constexpr int MAXB = 4, MAXBC = 1, MAXC = 16;
 
-template <bool ELEM>
-__global__ void __launch_bounds__(PNTH, 2) k_jcg_persistent(const LevelGeom g, const ConstStencil cs, const ElemStencil es,
-                                                         const PArgs a) {
-  __shared__ double sp[SN];
-  cg::grid_group grid = cg::this_grid();
+// cluster-wide sum of 3 values through distributed shared memory, result in every thread of every CTA
+__device__ __forceinline__ void cluster_sum3(double v[3], double (*csum)[3], int& buf) {
+  block_sum3_all(v);
+  cg::cluster_group cl = cg::this_cluster();
+  if (threadIdx.x == 0)
+    for (int k = 0; k < 3; ++k) csum[buf][k] = v[k];
+  cl.sync();
+  __shared__ double res[3];
+  const unsigned C = cl.num_blocks();
+  if (threadIdx.x < 3) {
+    double part[MAXC];
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c)   // independent remote loads first, then the fixed-order sum
+      part[c] = c < (int)C ? *cl.map_shared_rank(&csum[buf][threadIdx.x], (unsigned)c) : 0.0;
+    double sum = 0.0;
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c)
+      if (c < (int)C) sum += part[c];
+    res[threadIdx.x] = sum;
+  }
+  __syncthreads();
+  v[0] = res[0]; v[1] = res[1]; v[2] = res[2];
+  __syncthreads();
+  buf ^= 1;   // the other buffer next time: a slow CTA may still be reading this one
+}
+
+template <bool ELEM, bool CL>
+__global__ void __launch_bounds__(PNTH, CL ? 1 : 2) k_jcg_persistent(const LevelGeom g, const ConstStencil cs,
+                                                                    const ElemStencil es, const PArgs a) {
+  constexpr int MB = CL ? MAXBC : MAXB;
+  extern __shared__ double sp_all[];       // MB halo windows of SN values
+  __shared__ double csum[2][3];            // cluster form: this CTA's block sums (ping-pong)
   const int nbricks = ((g.nf[0] + BX - 1) / BX) * ((g.nf[1] + BY - 1) / BY) * ((g.nf[2] + BZ - 1) / BZ);
   const int lx = threadIdx.x % BX, ly = (threadIdx.x / BX) % BY, lz = threadIdx.x / (BX * BY);
   const double cdinv = cs.dinv;
@@ -254,34 +328,49 @@ __global__ void __launch_bounds__(PNTH, 2) k_jcg_persistent(const LevelGeom g, c
   double* const u_out = sc->in.u_out;
   double* const zsrc = ELEM ? a.z : a.r;   // what neighbours stage: p_new = zscale * zsrc + beta p_old
   const double zscale = ELEM ? 1.0 : cdinv;
+  int buf = 0;
+  auto allsum = [&](double v[3]) {
+    if constexpr (CL) {
+      cluster_sum3(v, csum, buf);
+    } else {
+      cg::grid_group grid = cg::this_grid();
+      grid_sum3(v, a.partials, buf, grid);
+    }
+  };
+  auto allsync = [&]() {
+    if constexpr (CL) cg::this_cluster().sync();
+    else cg::this_grid().sync();
+  };
 
-  bool act[MAXB], own[MAXB];
-  Brick br[MAXB];
-  Node nd[MAXB];
+  bool act[MB], own[MB];
+  Brick br[MB];
+  Node nd[MB];
+  __shared__ int sb[3 * MB];   // brick origins for the batched staging
+  int nact = 0;                // active bricks of this CTA: 0 .. nact-1
 #pragma unroll
-  for (int i = 0; i < MAXB; ++i) {
+  for (int i = 0; i < MB; ++i) {
     const int k = blockIdx.x + i * gridDim.x;
     act[i] = k < nbricks;   // uniform over the CTA
+    nact += act[i] ? 1 : 0;
     br[i] = brick_of(g, act[i] ? k : 0);
+    if (threadIdx.x == 0) { sb[3 * i] = br[i].X0; sb[3 * i + 1] = br[i].Y0; sb[3 * i + 2] = br[i].Z0; }
     nd[i].fx = br[i].X0 + lx; nd[i].fy = br[i].Y0 + ly; nd[i].fz = br[i].Z0 + lz;
     nd[i].off = nd[i].fz * (int)g.S + nd[i].fy * (int)g.P + nd[i].fx;
     own[i] = act[i] && nd[i].fx < g.nf[0] && nd[i].fy < g.nf[1] && nd[i].fz < g.nf[2];
   }
-  double xr[MAXB], rr_[MAXB], di[MAXB], pc[MAXB], wv[MAXB];
-  int buf = 0;
+  double xr[MB], rr_[MB], di[MB], pc[MB], wv[MB];
   // init: D^-1 (element path), r = b - A x, z = D^-1 r, rho = r.z, rr, ||b||^2
   double v[3] = {0.0, 0.0, 0.0};
+  __syncthreads();   // sb
+  stage_all<false, MB>(g, sb, nact, a.x, nullptr, 1.0, 0.0, sp_all);
+  __syncthreads();
 #pragma unroll
-  for (int i = 0; i < MAXB; ++i) {
+  for (int i = 0; i < MB; ++i) {
     xr[i] = rr_[i] = pc[i] = wv[i] = 0.0;
     di[i] = cdinv;
-    if (!act[i]) continue;
-    __syncthreads();
-    stage<false>(g, br[i], a.x, nullptr, 1.0, 0.0, sp);
-    __syncthreads();
     if (!own[i]) continue;
     double p27[3][3][3];
-    window27(sp, lx, ly, lz, p27);
+    window27(sp_all + i * SN, lx, ly, lz, p27);
     double d = 0.0;
     const double ax = apply_node<ELEM>(g, cs, es, a.beta, nd[i], p27, &d);
     if (ELEM) di[i] = es.precond ? (d > 0.0 ? 1.0 / d : 0.0) : 1.0;
@@ -295,7 +384,7 @@ __global__ void __launch_bounds__(PNTH, 2) k_jcg_persistent(const LevelGeom g, c
     v[1] = __fma_rn(rn, rn, v[1]);
     v[2] = __fma_rn(bi, bi, v[2]);
   }
-  grid_sum3(v, a.partials, buf, grid);
+  allsum(v);
   double rho = v[0], rr = v[1];
   const double bb = v[2];
   const double nb = sqrt(bb), nbe = nb > 0.0 ? nb : 1.0;
@@ -306,33 +395,32 @@ __global__ void __launch_bounds__(PNTH, 2) k_jcg_persistent(const LevelGeom g, c
   if (!isfinite(rr)) { status = ST_EBREAKDOWN; done = true; }
   int cur = 0;   // a.p[cur] holds p_old
   while (!done) {
-    // phase 1: p_new = z + beta p_old on the brick and its halo, w = A p_new, sigma = p_new . w
+    // phase 1: p_new = z + beta p_old on the bricks and their halos, w = A p_new, sigma = p_new . w
     const double bcg = iter == 0 ? 0.0 : beta;
     double* pnew = a.p[cur ^ 1];
     const double* pold = a.p[cur];
     v[0] = v[1] = v[2] = 0.0;
+    __syncthreads();   // the previous phase's windows consumed
+    stage_all<true, MB>(g, sb, nact, zsrc, pold, zscale, bcg, sp_all);
+    __syncthreads();
 #pragma unroll
-    for (int i = 0; i < MAXB; ++i) {
-      if (!act[i]) continue;
-      __syncthreads();
-      stage<true>(g, br[i], zsrc, pold, zscale, bcg, sp);
-      __syncthreads();
+    for (int i = 0; i < MB; ++i) {
       if (!own[i]) continue;
       double p27[3][3][3];
-      window27(sp, lx, ly, lz, p27);
+      window27(sp_all + i * SN, lx, ly, lz, p27);
       wv[i] = apply_node<ELEM>(g, cs, es, a.beta, nd[i], p27, nullptr);
       pc[i] = p27[1][1][1];
       pnew[nd[i].off] = pc[i];
       v[0] = __fma_rn(pc[i], wv[i], v[0]);
     }
-    grid_sum3(v, a.partials, buf, grid);
+    allsum(v);
     const double sigma = v[0];
     if (!(sigma > 0.0)) { status = ST_EBREAKDOWN; break; }
     const double alpha = rho / sigma;
     // phase 2 (own nodes, registers): x += alpha p, r -= alpha w, z = D^-1 r, rho' = r.z, rr = r.r
     v[0] = v[1] = v[2] = 0.0;
 #pragma unroll
-    for (int i = 0; i < MAXB; ++i) {
+    for (int i = 0; i < MB; ++i) {
       if (!own[i]) continue;
       xr[i] = __fma_rn(alpha, pc[i], xr[i]);
       const double rn = __fma_rn(-alpha, wv[i], rr_[i]);
@@ -342,7 +430,7 @@ __global__ void __launch_bounds__(PNTH, 2) k_jcg_persistent(const LevelGeom g, c
       v[0] = __fma_rn(rn, zz, v[0]);
       v[1] = __fma_rn(rn, rn, v[1]);
     }
-    grid_sum3(v, a.partials, buf, grid);
+    allsum(v);
     beta = v[0] / rho;
     rho = v[0];
     rr = v[1];
@@ -353,28 +441,27 @@ __global__ void __launch_bounds__(PNTH, 2) k_jcg_persistent(const LevelGeom g, c
   }
   // x (and r, for the caller's inspection) back to memory, then the true residual ||b - A x||
 #pragma unroll
-  for (int i = 0; i < MAXB; ++i)
+  for (int i = 0; i < MB; ++i)
     if (own[i]) { a.x[nd[i].off] = xr[i]; a.r[nd[i].off] = rr_[i]; }
-  grid.sync();
+  allsync();
   v[0] = v[1] = v[2] = 0.0;
+  stage_all<false, MB>(g, sb, nact, a.x, nullptr, 1.0, 0.0, sp_all);
+  __syncthreads();
 #pragma unroll
-  for (int i = 0; i < MAXB; ++i) {
-    if (!act[i]) continue;
-    __syncthreads();
-    stage<false>(g, br[i], a.x, nullptr, 1.0, 0.0, sp);
-    __syncthreads();
+  for (int i = 0; i < MB; ++i) {
     if (!own[i]) continue;
     double p27[3][3][3];
-    window27(sp, lx, ly, lz, p27);
+    window27(sp_all + i * SN, lx, ly, lz, p27);
     const double rn = a.b[nd[i].off] - apply_node<ELEM>(g, cs, es, a.beta, nd[i], p27, nullptr);
     v[1] = __fma_rn(rn, rn, v[1]);
     if (u_out) u_out[full_index(g, nd[i].fx, nd[i].fy, nd[i].fz)] = xr[i];   // fused scatter of u_h
   }
-  grid_sum3(v, a.partials, buf, grid);
+  allsum(v);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     sc->rho = rho; sc->rr = rr; sc->bb = bb; sc->rr_true = v[1]; sc->beta = beta;
     sc->iter = iter; sc->max_iter = max_iter; sc->thresh = thresh; sc->status = status; sc->done = 1;
   }
+  if constexpr (CL) cg::this_cluster().sync();   // no CTA exits while another may still read its csum
 }
 
 // ---- the smallest levels: the whole solve in ONE CTA, every vector in shared memory -------------------
@@ -565,10 +652,35 @@ int persistent_grid(int want) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jcg_persistent<ELEM>, PNTH, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jcg_persistent<ELEM, false>, PNTH, sizeof(double) * MAXB * SN);
     slots = sms * std::max(1, per_sm);
   }
   return std::max(1, std::min(want, slots));
+}
+
+#ifndef ECMG_PERS_CLUSTER
+#define ECMG_PERS_CLUSTER 1
+#endif
+// the cluster form of the persistent solve: can a cluster of C CTAs run on this GPU? (checked once per C)
+template <bool ELEM>
+bool cluster_fits(int C) {
+  static int ok[MAXC + 1] = {0};   // 0 unknown, 1 yes, -1 no
+  if (C < 1 || C > MAXC) return false;
+  if (!ok[C]) {
+    const void* fn = (const void*)k_jcg_persistent<ELEM, true>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(C); cfg.blockDim = dim3(PNTH); cfg.dynamicSmemBytes = sizeof(double) * MAXBC * SN;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    int n = 0;
+    const cudaError_t e = cudaOccupancyMaxActiveClusters(&n, fn, &cfg);
+    if (e != cudaSuccess) cudaGetLastError();
+    ok[C] = (e == cudaSuccess && n >= 1) ? 1 : -1;
+  }
+  return ok[C] > 0;
 }
 
 }  // namespace
@@ -618,19 +730,32 @@ cudaError_t launch_jcg_persistent(const LevelGeom& g, const ConstStencil& cs, co
                                   double* z, double* p0, double* p1, double* w, double* dinv, const double* beta,
                                   const double* b, double* partials, JcgScalars* sc, cudaStream_t st) {
   const long long nbricks = (long long)((g.nf[0] + BX - 1) / BX) * ((g.nf[1] + BY - 1) / BY) * ((g.nf[2] + BZ - 1) / BZ);
+  PArgs a{x, r, z, {p0, p1}, w, b, dinv, beta, partials, sc};
+  const ElemStencil e = es ? *es : ElemStencil{};
+  void* args[] = {(void*)&g, (void*)&cs, (void*)&e, (void*)&a};
+  // levels of at most MAXC bricks: one thread-block cluster, one brick per CTA
+  const int C = (int)std::min<long long>(nbricks, MAXC);
+  if (ECMG_PERS_CLUSTER && nbricks <= (long long)MAXC * MAXBC && (es ? cluster_fits<true>(C) : cluster_fits<false>(C))) {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(C); cfg.blockDim = dim3(PNTH); cfg.dynamicSmemBytes = sizeof(double) * MAXBC * SN;
+    cfg.stream = st; cfg.attrs = at; cfg.numAttrs = 1;
+    count_launch();
+    return cudaLaunchKernelExC(&cfg, es ? (const void*)k_jcg_persistent<true, true> : (const void*)k_jcg_persistent<false, true>,
+                               args);
+  }
   // one brick per CTA while the CTAs fit (parallelism), up to MAXB per CTA beyond that
   const int slots = es ? persistent_grid<true>(1 << 30) : persistent_grid<false>(1 << 30);
   if (nbricks > (long long)MAXB * slots) return cudaErrorInvalidValue;
   const int want = (int)std::min<long long>(nbricks, slots);
-  PArgs a{x, r, z, {p0, p1}, w, b, dinv, beta, partials, sc};
-  const ElemStencil e = es ? *es : ElemStencil{};
-  void* args[] = {(void*)&g, (void*)&cs, (void*)&e, (void*)&a};
   count_launch();
   if (es)
-    return cudaLaunchCooperativeKernel((const void*)k_jcg_persistent<true>, dim3(persistent_grid<true>(want)), dim3(PNTH),
-                                       args, 0, st);
-  return cudaLaunchCooperativeKernel((const void*)k_jcg_persistent<false>, dim3(persistent_grid<false>(want)),
-                                     dim3(PNTH), args, 0, st);
+    return cudaLaunchCooperativeKernel((const void*)k_jcg_persistent<true, false>, dim3(persistent_grid<true>(want)),
+                                       dim3(PNTH), args, sizeof(double) * MAXB * SN, st);
+  return cudaLaunchCooperativeKernel((const void*)k_jcg_persistent<false, false>, dim3(persistent_grid<false>(want)),
+                                     dim3(PNTH), args, sizeof(double) * MAXB * SN, st);
 }
 
 }  // namespace ecmg

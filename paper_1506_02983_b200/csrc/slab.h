@@ -14,6 +14,8 @@ struct SlabCfg {
   int fused_halo;   // 1: K2 / init store their boundary planes into the neighbours' halo planes
   int beta_fly;     // 1: element kernels form analytic beta from the level's axis tables
   int shard_min;    // levels with fewer z cells are replicated (ECMG_OPT_SHARD_MIN)
+  int use_graph;    // 1: tolerance-stopped solves of sharded levels run as one CUDA graph per level with a
+                    // device-set WHILE node (ECMG_OPT_GRAPH); 0: the host loop with batched readbacks
 };
 constexpr int kShardMinDefault = 256;
 

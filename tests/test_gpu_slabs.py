@@ -89,19 +89,26 @@ nid = ecmg.nccl_unique_id()
 g1 = Grid(4, 5, PROB["C2"]); u1 = g1.new_vec(4); st1, s1 = g1.run(1e-10, u1)
 d = ecmg.make_dist(0, 1, nid)
 gn = Grid(4, 5, PROB["C2"], dist=d); gn.set_option(ecmg.OPT_SHARD_MIN, 16); un = gn.new_vec(4); stn, sn = gn.run(1e-10, un)
+gh = Grid(4, 5, PROB["C2"], dist=ecmg.make_dist(0, 1, ecmg.nccl_unique_id())); gh.set_option(ecmg.OPT_SHARD_MIN, 16)
+gh.set_option(ecmg.OPT_GRAPH, 0); uh = gh.new_vec(4); sth, sh = gh.run(1e-10, uh)   # the host loop
 torch.cuda.synchronize()
-a, b = un.cpu().numpy(), u1.cpu().numpy()
-print(json.dumps(dict(st=[st1, stn], it1=[s["iterations"] for s in s1], itn=[s["iterations"] for s in sn],
+a, b, c = un.cpu().numpy(), u1.cpu().numpy(), uh.cpu().numpy()
+print(json.dumps(dict(st=[st1, stn, sth], it1=[s["iterations"] for s in s1], itn=[s["iterations"] for s in sn],
+                      ith=[s["iterations"] for s in sh], graph_vs_host_bitwise=bool(np.array_equal(a, c)),
                       d=float(np.max(np.abs(a - b)) / np.max(np.abs(b))))))
 '''
-    env = dict(os.environ, ECMG_TEST_NCCL_SINGLE="1")
+    env = dict(os.environ, ECMG_TEST_NCCL_SINGLE="1", ECMG_DEBUG="1")
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300,
                          cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert out.returncode == 0, out.stderr[-2000:]
     r = json.loads(out.stdout.strip().splitlines()[-1])
-    assert r["st"] == [0, 0]
-    assert r["it1"] == r["itn"]
+    assert r["st"] == [0, 0, 0]
+    assert r["it1"] == r["itn"] == r["ith"]
     assert r["d"] <= 1e-13
+    # the sharded levels ran as CUDA graphs with the NCCL allreduce captured inside the WHILE body (a failed
+    # capture would fall back to the host loop and say so on stderr under ECMG_DEBUG), bitwise = host loop
+    assert "graph capture failed" not in out.stderr, out.stderr[-2000:]
+    assert r["graph_vs_host_bitwise"]
 
 
 @pytest.mark.parametrize("pid,levels,eps,P", [(o.C2, 5, 1e-10, 2), (o.C3, 5, 1e-10, 2), (o.C5, 6, 1e-8, 4),
@@ -122,6 +129,33 @@ def test_fused_halo_equals_copied_halo(pid, levels, eps, P):
         res.append(([s["iterations"] for s in stats], host(u), host(ut)))
     assert res[0][0] == res[1][0]
     assert np.array_equal(res[0][1], res[1][1]) and np.array_equal(res[0][2], res[1][2])
+
+
+@pytest.mark.parametrize("pid,levels,eps,P,fused", [(o.C2, 5, 1e-10, 2, 1), (o.C3, 5, 1e-10, 2, 0),
+                                                    (o.C5, 6, 1e-8, 4, 1), (o.C4, 6, 1e-9, 8, 0)])
+def test_slab_graph_loop_equals_host_loop(pid, levels, eps, P, fused):
+    # ECMG_OPT_GRAPH on sharded levels: one CUDA graph per level (init pass, WHILE node whose body is two
+    # iterations of K1 / allreduce / finalize / K2 / allreduce / finalize / halo, true residual), the WHILE
+    # condition set by the finalize kernels -- the same kernels in the same order as the host loop, so
+    # every iterate is bitwise identical and the counts are equal
+    res = []
+    for graph in (0, 1):
+        g = Grid(4, levels, pid, params_for(pid))
+        g.set_option(ecmg.OPT_VIRTUAL_SLABS, P)
+        g.set_option(ecmg.OPT_SHARD_MIN, 16)   # split the small test levels too
+        g.set_option(ecmg.OPT_FUSED_HALO, fused)
+        g.set_option(ecmg.OPT_GRAPH, graph)
+        g.set_option(ecmg.OPT_PERS_TMA, 0)   # replicated mid levels: graph vs host loop of the same K1 / K2 too
+        u, ut = g.new_vec(levels - 1), g.new_vec(levels - 1)
+        l0 = ecmg.kernel_launches()
+        st, stats = g.run(eps, u, ut)
+        st2, stats2 = g.run(eps, u, ut)   # second run: the graphs are reused
+        assert st == 0 and st2 == 0
+        res.append(([s["iterations"] for s in stats], host(u), host(ut), [s["iterations"] for s in stats2],
+                    ecmg.kernel_launches() - l0))
+    assert res[0][0] == res[1][0] == res[1][3]
+    assert np.array_equal(res[0][1], res[1][1]) and np.array_equal(res[0][2], res[1][2])
+    assert res[1][4] > 0
 
 
 @pytest.mark.parametrize("pid,levels,eps,P", [(o.C2, 6, 1e-10, 2), (o.C4, 6, 1e-9, 8), (o.C3, 5, 1e-10, 2),
