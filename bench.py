@@ -44,7 +44,7 @@ UNIT = "unknown-iters/s"
 BYTES_PER_UNKNOWN_ITER = 64   # x 1R+1W, r 2R+1W, p 2R+1W (constant-beta path)
 
 CONFIGS = {
-    # name: (problem id, coarsest, levels, eps, description); C3 / C5 run the element-beta path (88 B/unknown)
+    # name: (problem id, coarsest, levels, eps, description); C3 / C5 run the element-beta path (80 B/unknown)
     "c4": (4, 4, 8, 1e-9, "C4 (BASELINE configs[3]): u=r^{3/2}, beta=1, Dirichlet, Q1, 4^3->512^3, eps=1e-9"),
     "c2": (2, 4, 6, 1e-10, "C2 (BASELINE configs[1]): u=exp(x+y+z), beta=1, Dirichlet, Q1, 4^3->128^3, eps=1e-10"),
     "c1": (1, 4, 4, 1e-8, "C1 (BASELINE configs[0]): u=sin sin sin, beta=1, Dirichlet, Q1, 4^3->32^3, eps=1e-8"),
@@ -52,9 +52,10 @@ CONFIGS = {
     "c5": (5, 4, 9, 1e-8, "C5 (BASELINE configs[4]): layered geology (seed 0), Dirichlet, Q1, 4^3->1024^3, eps=1e-8"),
 }
 # element-beta path (kernels_jcg_elem.cu): K1 reads z, p_old, beta_e and writes p; K2 reads p, beta_e,
-# x, r and writes x, r, z = D^-1 r (z replaces the halo diagonal): 11 x 8 B. With ECMG_OPT_BETA_FLY = 1
-# (ablation) beta_e is formed in registers from per-axis tables: 9 x 8 B
-BYTES_PER_UNKNOWN_ITER_ELEM = 88
+# x, z and writes x, z (the residual is carried as z = D^-1 r only; K2 forms r = D z): 10 x 8 B, the
+# survey's algorithmic 80 B. With ECMG_OPT_BETA_FLY = 1 (ablation) beta_e is formed in registers from
+# per-axis tables: 8 x 8 B
+BYTES_PER_UNKNOWN_ITER_ELEM = 80
 
 
 def load_peaks():
@@ -483,7 +484,7 @@ def main():
         ms_b = max_over_ranks(ms_b)
         grid.set_option(ecmg.OPT_BETA_FLY, 0)
         ablation_beta = {"value": nf_j * it_b / (ms_b / 1e3), "unit": UNIT, "ms_per_iteration": ms_b / max(1, it_b),
-                         "kernel": "element kernels forming beta_e from per-axis tables (ECMG_OPT_BETA_FLY=1), 72 B/unknown"}
+                         "kernel": "element kernels forming beta_e from per-axis tables (ECMG_OPT_BETA_FLY=1), 64 B/unknown"}
     # ablation: host-driven JCG loop (batched readbacks) instead of the CUDA-graph WHILE loop
     grid.set_option(ecmg.OPT_GRAPH, 0)
     grid.run(eps, u, ut)

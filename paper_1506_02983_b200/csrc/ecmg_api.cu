@@ -383,7 +383,7 @@ cudaError_t build_level_graph(ecmg_grid* G, int k, cudaGraphExec_t* out) {
     e = launch_mode(G, MODE_K1, g, a1);
     if (e != cudaSuccess) break;
     KArgs a2 = a;
-    a2.h0 = G->p[1 - half]; a2.i0 = G->x; a2.i1 = G->r; a2.o0 = G->x; a2.o1 = G->r; a2.o2 = G->zv;
+    a2.h0 = G->p[1 - half]; a2.i0 = G->x; a2.i1 = G->elem_path ? G->zv : G->r; a2.o0 = G->x; a2.o1 = G->r; a2.o2 = G->zv;
     e = launch_mode(G, MODE_K2, g, a2);
   }
   e2 = cudaStreamEndCapture(G->cap_stream, &body);
@@ -570,7 +570,7 @@ int run_jcg(ecmg_grid* G, int k, double eps, int max_iter, double* u_out, ecmg_s
     cudaError_t e = launch_mode(G, MODE_K1, g, a1);
     if (e != cudaSuccess) return e;
     KArgs a2 = a;
-    a2.h0 = G->p[(it + 1) & 1]; a2.i0 = G->x; a2.i1 = G->r; a2.o0 = G->x; a2.o1 = G->r; a2.o2 = G->zv;
+    a2.h0 = G->p[(it + 1) & 1]; a2.i0 = G->x; a2.i1 = G->elem_path ? G->zv : G->r; a2.o0 = G->x; a2.o1 = G->r; a2.o2 = G->zv;
     e = launch_mode(G, MODE_K2, g, a2);
     ++it;
     return e;

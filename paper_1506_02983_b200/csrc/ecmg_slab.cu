@@ -405,7 +405,7 @@ int slab_jcg(SlabDriver* d, int k, double eps, int max_iter, ecmg_stats* st, cud
     int q = pass(MODE_K1, [&](SlabCtx& c, KArgs& a) { a.h0 = elem ? c.z : c.r; a.h1 = c.p[it & 1]; a.o0 = c.p[(it + 1) & 1]; });
     if (q) return q;
     q = pass(MODE_K2, [&](SlabCtx& c, KArgs& a) {
-      a.h0 = c.p[(it + 1) & 1]; a.i0 = c.x; a.i1 = c.r; a.o0 = c.x; a.o1 = c.r; a.o2 = c.z;
+      a.h0 = c.p[(it + 1) & 1]; a.i0 = c.x; a.i1 = elem ? c.z : c.r; a.o0 = c.x; a.o1 = c.r; a.o2 = c.z;
       set_peers(c, a);
     });
     if (q) return q;

@@ -20,11 +20,12 @@
 // added; the layer-below half rides in registers from the previous step. About 40 fp64 operations
 // per node instead of the 64 + 8 of the element-by-element form, and every beta is read once.
 //
-// CG data flow of this path: K2 / INIT also write z = D^-1 r (D = Jacobi diagonal
-// kappa_0 sum_{e ni i} beta_e + Robin diagonal, formed from the beta sums the kernel holds anyway), so
-// K1 needs only z and p_old on its halo (p = z + beta_cg p_old): no diagonal on halo nodes.
-// HBM per unknown and iteration: K1 reads z, p_old, beta, writes p (32 B); K2 reads p, beta, x, r and
-// writes x, r, z (56 B): 88 B.
+// CG data flow of this path: the residual is carried as z = D^-1 r only (D = Jacobi diagonal
+// kappa_0 sum_{e ni i} beta_e + Robin diagonal, formed from the beta sums the kernel holds anyway): INIT
+// writes z_0, K2 forms r_k = D z_k at its own nodes, updates r_{k+1} = r_k - alpha A p and writes z_{k+1};
+// K1 needs only z and p_old on its halo (p = z + beta_cg p_old): no diagonal on halo nodes, no r vector.
+// HBM per unknown and iteration: K1 reads z, p_old, beta, writes p (32 B); K2 reads p, beta, x, z and
+// writes x, z (48 B): 80 B, the algorithmic figure of SURVEY.md §8d D.3 (reading R8).
 //
 // Data movement as in kernels_jcg_tma.cu: one cp.async.bulk.tensor.3d per CTA and vector per plane
 // into an NS-deep ring (mbarrier expect_tx), out-of-bounds boxes zero-filled (= p on Dirichlet /
@@ -346,12 +347,13 @@ __device__ __forceinline__ void elem_pass(const LevelGeom& g, const ElemStencil&
         } else if (MODE == MODE_K2) {
           const double dinv = es.precond ? (diag > 0.0 ? __drcp_rn(diag) : 0.0) : 1.0;
           const double xn = __fma_rn(alpha, pc, I0[io]);
-          const double rn = __fma_rn(-alpha, ap, I1[io]);
+          // r_k = D z_k: the residual is not stored on this path, only z = D^-1 r (reading R8)
+          const double rk = es.precond ? diag * I1[io] : I1[io];
+          const double rn = __fma_rn(-alpha, ap, rk);
           const double zz = dinv * rn;
           acc0 = __fma_rn(rn, zz, acc0);
           acc1 = __fma_rn(rn, rn, acc1);
           a.o0[off] = xn;
-          a.o1[off] = rn;
           a.o2[off] = zz;
           if (d == g.zbeg && a.peer_lo) a.peer_lo[own_off[j]] = zz;      // fused halo exchange (z)
           if (d == g.zend - 1 && a.peer_hi) a.peer_hi[own_off[j]] = zz;
@@ -363,8 +365,7 @@ __device__ __forceinline__ void elem_pass(const LevelGeom& g, const ElemStencil&
           const double zz = dinv * rn;
           acc0 = __fma_rn(rn, zz, acc0);
           acc1 = __fma_rn(rn, rn, acc1);
-          a.o0[off] = rn;
-          a.o1[off] = zz;
+          a.o1[off] = zz;   // r itself is not stored (K2 forms r_k = D z_k)
           if (d == g.zbeg && a.peer_lo) a.peer_lo[own_off[j]] = zz;      // fused halo exchange (z)
           if (d == g.zend - 1 && a.peer_hi) a.peer_hi[own_off[j]] = zz;
         } else if (MODE == MODE_TRUE) {
@@ -449,7 +450,7 @@ constexpr int EP_NS = 5;
 constexpr int EP_SB = ElemCfg<MODE_K2>::SBYTES > ElemCfg<MODE_K1>::SBYTES ? ElemCfg<MODE_K2>::SBYTES : ElemCfg<MODE_K1>::SBYTES;
 constexpr int EP_SMEM = EP_SB * EP_NS + 128;
 
-struct ElemPersMaps { CUtensorMap xh, zh, ph0, ph1, be, xi, ri, bi; };
+struct ElemPersMaps { CUtensorMap xh, zh, ph0, ph1, be, xi, zi, bi; };
 
 __device__ __forceinline__ void elem_grid_sum3(double v[3], double* partials, int& buf, double* red,
                                                cooperative_groups::grid_group& grid) {
@@ -517,7 +518,7 @@ __global__ void __launch_bounds__(NTH, ELEM_PERS_MINB)
     if (tid == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
   };
   double v[3];
-  a.o0 = r; a.o1 = z;   // init: r = b - A x, z = D^-1 r, rho = r.z, rr, ||b||^2
+  a.o1 = z;   // init: r = b - A x, z = D^-1 r (stored), rho = r.z, rr, ||b||^2
   pass(std::integral_constant<int, MODE_INIT>{}, &M.xh, &M.xh, &M.bi, &M.bi, 0.0, false, 0.0, v);
   double rho = v[0], rr = v[1];
   const double bb = v[2];
@@ -536,8 +537,8 @@ __global__ void __launch_bounds__(NTH, ELEM_PERS_MINB)
     const double sigma = v[0];
     if (!(sigma > 0.0)) { status = ST_EBREAKDOWN; break; }
     const double alpha = rho / sigma;
-    a.o0 = x; a.o1 = r; a.o2 = z;
-    pass(std::integral_constant<int, MODE_K2>{}, cur ? &M.ph0 : &M.ph1, &M.zh, &M.xi, &M.ri, 0.0, false, alpha, v);
+    a.o0 = x; a.o2 = z;
+    pass(std::integral_constant<int, MODE_K2>{}, cur ? &M.ph0 : &M.ph1, &M.zh, &M.xi, &M.zi, 0.0, false, alpha, v);
     beta = v[0] / rho;
     rho = v[0];
     rr = v[1];
@@ -709,7 +710,7 @@ cudaError_t launch_jcg_elem_pers(const LevelGeom& g, const ElemStencil& es, doub
   ElemPersMaps M;
   const bool ok = vec_map(&M.xh, x, g, HX, HY) && vec_map(&M.zh, z, g, HX, HY) && vec_map(&M.ph0, p0, g, HX, HY) &&
                   vec_map(&M.ph1, p1, g, HX, HY) && beta_map(&M.be, beta, g) && vec_map(&M.xi, x, g, TX, TY) &&
-                  vec_map(&M.ri, r, g, TX, TY) && vec_map(&M.bi, b, g, TX, TY);
+                  vec_map(&M.zi, z, g, TX, TY) && vec_map(&M.bi, b, g, TX, TY);
   if (!ok) return cudaErrorInvalidValue;
   const int grid = std::min(items, slots);
   void* args[] = {(void*)&g, (void*)&es, (void*)&x, (void*)&r, (void*)&z, (void*)&p0, (void*)&p1, (void*)&partials,
@@ -725,8 +726,8 @@ cudaError_t launch_jcg_elem_pers(const LevelGeom& g, const ElemStencil& es, doub
   return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(TX, WARPS), args, EP_SMEM, st);
 }
 
-// K1: h0 = z, h1 = p_old, o0 = p. K2: h0 = p, i0 = x, i1 = r, o0 = x, o1 = r, o2 = z.
-// INIT: h0 = x, i0 = b, o0 = r, o1 = z. TRUE: h0 = x, i0 = b. APPLY: h0 = p, o0 = A p.
+// K1: h0 = z, h1 = p_old, o0 = p. K2: h0 = p, i0 = x, i1 = z, o0 = x, o2 = z.
+// INIT: h0 = x, i0 = b, o1 = z. TRUE: h0 = x, i0 = b. APPLY: h0 = p, o0 = A p.
 cudaError_t launch_jcg_elem(int mode, const LevelGeom& g, const ElemStencil& es, const Problem&, const KArgs& a,
                             cudaStream_t st) {
   if (g.BP % 2 != 0 || !a.h0 || !a.beta) return cudaErrorInvalidValue;
