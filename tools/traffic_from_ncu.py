@@ -8,7 +8,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-ALG = {"c4": (64, 511 ** 3), "c3": (88, 255 * 255 * 256)}   # bytes per unknown, free unknowns
+ALG = {"c4": (64, 511 ** 3), "c3": (80, 255 * 255 * 256)}   # bytes per unknown, free unknowns
 
 
 def dram(path):
