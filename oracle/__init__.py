@@ -87,13 +87,13 @@ def lib():
             L.orc_ecmg.argtypes = [dp, dp, ip, C.c_int, C.c_int, dp, C.c_int, ip, C.c_double, C.c_int,
                                    C.c_int, C.c_int, dp, dp, dp, dp]
             L.orc_build_level_arrays.restype = vp
-            L.orc_build_level_arrays.argtypes = [dp, dp, ip, ip, dp, dp, dp, dp, dp]
+            L.orc_build_level_arrays.argtypes = [dp, dp, ip, ip, dp, dp, dp, dp, dp, dp]
             L.orc_ecmg_arrays.restype = C.c_int
-            L.orc_ecmg_arrays.argtypes = [dp, dp, ip, C.c_int, dp, ip, C.POINTER(dp), C.c_double, C.c_int,
+            L.orc_ecmg_arrays.argtypes = [dp, dp, ip, C.c_int, dp, ip, C.POINTER(dp), C.c_int, C.c_double, C.c_int,
                                           C.c_int, C.c_int, dp, dp, dp, dp]
             L.orc_ecmg_fixed_arrays.restype = C.c_int
-            L.orc_ecmg_fixed_arrays.argtypes = [dp, dp, ip, C.c_int, dp, ip, C.POINTER(dp), C.c_int, C.c_double,
-                                                C.c_int, C.c_int, dp, dp, dp, dp]
+            L.orc_ecmg_fixed_arrays.argtypes = [dp, dp, ip, C.c_int, dp, ip, C.POINTER(dp), C.c_int, C.c_int,
+                                                C.c_double, C.c_int, C.c_int, dp, dp, dp, dp]
             L.orc_ecmg_fixed.restype = C.c_int
             L.orc_ecmg_fixed.argtypes = [dp, dp, ip, C.c_int, C.c_int, dp, C.c_int, ip, C.c_int, C.c_double,
                                          C.c_int, C.c_int, dp, dp, dp, dp]
@@ -163,10 +163,12 @@ class Level:
             raise ValueError("oracle: invalid level / problem")
 
     @classmethod
-    def from_arrays(cls, n_cells, faces, alpha, beta_e=None, f_q=None, gD=None, gR=None, lo=(0, 0, 0), hi=(1, 1, 1)):
+    def from_arrays(cls, n_cells, faces, alpha, beta_e=None, f_q=None, gD=None, gR=None, lo=(0, 0, 0), hi=(1, 1, 1),
+                    alpha_q=None):
         """A level of the ARRAYS problem: beta_e[n_x n_y n_z] (x fastest), f_q[8 per element] (Gauss point
         q = q_x + 2 q_y + 4 q_z, bit set = +1/sqrt(3)), gD[(n_x+1)(n_y+1)(n_z+1)], gR[per face x-..z+ a block of
-        4 n_d1 n_d2: 4 (e1 + n_d1 e2) + q], alpha[6]; None = beta 1 / f 0 / g_D 0 / g_R 0."""
+        4 n_d1 n_d2: 4 (e1 + n_d1 e2) + q], alpha[6]; None = beta 1 / f 0 / g_D 0 / g_R 0. alpha_q: alpha at the
+        face Gauss points in gR's layout (Eq. bvp's piecewise smooth alpha), None = alpha[F] per face."""
         self = cls.__new__(cls)
         L = lib()
         self.n = tuple(int(v) for v in n_cells)
@@ -176,7 +178,7 @@ class Level:
         self.params = _f64(alpha)
         self.faces = np.array(faces, dtype=np.int32)
         self.lo, self.hi = _f64(lo), _f64(hi)
-        self._arrays = [None if a is None else _f64(a).reshape(-1) for a in (beta_e, f_q, gD, gR)]
+        self._arrays = [None if a is None else _f64(a).reshape(-1) for a in (beta_e, f_q, gD, gR, alpha_q)]
         n = np.array(self.n, dtype=np.int32)
         ptr = [_d(a) if a is not None else None for a in self._arrays]
         self._h = L.orc_build_level_arrays(_d(self.lo), _d(self.hi), _i(n), _i(self.faces), _d(self.params), *ptr)
@@ -303,19 +305,31 @@ def ecmg(n0, levels, problem_id, eps, params=None, lo=(0, 0, 0), hi=(1, 1, 1), f
     return st, stats, u, ut
 
 
+def _level_ptrs(level_arrays):
+    """The oracle's level-array list: (beta_e, f_q, gD, gR) of every level, then alpha_q of every level when the
+    tuples carry a fifth entry (n_level_arrays = 4 L or 5 L)."""
+    with_alpha = any(len(lv) > 4 for lv in level_arrays)
+    arrs = [a for lv in level_arrays for a in lv[:4]]
+    if with_alpha:
+        arrs += [lv[4] if len(lv) > 4 else None for lv in level_arrays]
+    keep = [None if a is None else _f64(a).reshape(-1) for a in arrs]
+    return keep, len(keep)
+
+
 def ecmg_arrays(n0, levels, faces, alpha, level_arrays, eps, lo=(0, 0, 0), hi=(1, 1, 1), max_iter=100000,
                 precond=True, want_w=False, exp_variant=0):
-    """Alg. 4 on ARRAYS data: level_arrays[k] = (beta_e, f_q, gD, gR) of level k (layouts: Level.from_arrays)."""
+    """Alg. 4 on ARRAYS data: level_arrays[k] = (beta_e, f_q, gD, gR[, alpha_q]) of level k (layouts:
+    Level.from_arrays); alpha_q given on every level or on none."""
     n0 = np.array([n0] * 3 if np.isscalar(n0) else list(n0), dtype=np.int32)
     nf = n0 * (1 << (levels - 1))
     N = int(np.prod(nf + 1))
     stats = np.empty(levels * NSTAT)
     u, ut = np.empty(N), np.empty(N)
     w = np.empty(N) if want_w else None
-    keep = [None if a is None else _f64(a).reshape(-1) for lv in level_arrays for a in lv]
+    keep, nla = _level_ptrs(level_arrays)
     ptrs = (C.POINTER(C.c_double) * len(keep))(*[_d(a) if a is not None else None for a in keep])
     fc = np.array(faces, dtype=np.int32)
-    st = lib().orc_ecmg_arrays(_d(_f64(lo)), _d(_f64(hi)), _i(n0), int(levels), _d(_f64(alpha)), _i(fc), ptrs,
+    st = lib().orc_ecmg_arrays(_d(_f64(lo)), _d(_f64(hi)), _i(n0), int(levels), _d(_f64(alpha)), _i(fc), ptrs, nla,
                                float(eps), int(max_iter), 1 if precond else 0, int(exp_variant), _d(stats), _d(u),
                                _d(ut), _d(w) if w is not None else None)
     del keep
@@ -332,10 +346,10 @@ def ecmg_fixed_arrays(n0, levels, faces, alpha, level_arrays, m_L, ratio, lo=(0,
     N = int(np.prod(n0 * (1 << (levels - 1)) + 1))
     stats = np.empty(levels * NSTAT)
     u, ut = np.empty(N), np.empty(N)
-    keep = [None if a is None else _f64(a).reshape(-1) for lv in level_arrays for a in lv]
+    keep, nla = _level_ptrs(level_arrays)
     ptrs = (C.POINTER(C.c_double) * len(keep))(*[_d(a) if a is not None else None for a in keep])
     st = lib().orc_ecmg_fixed_arrays(_d(_f64(lo)), _d(_f64(hi)), _i(n0), int(levels), _d(_f64(alpha)),
-                                     _i(np.array(faces, dtype=np.int32)), ptrs, int(m_L), float(ratio),
+                                     _i(np.array(faces, dtype=np.int32)), ptrs, nla, int(m_L), float(ratio),
                                      1 if precond else 0, int(exp_variant), _d(stats), _d(u), _d(ut), None)
     del keep
     return st, stats.reshape(levels, NSTAT), u, ut

@@ -82,8 +82,9 @@ struct Problem {
   // Gauss points of each element (index 8 e + q, q = q_x + 2 q_y + 4 q_z, bit set = +1/sqrt(3)), g_D per
   // node, g_R at the 4 Gauss points of each Robin face element (per face F in order x-..z+ a block of
   // n_d1 n_d2 4 values, index 4 (e1 + n_d1 e2) + q, q = q_1 + 2 q_2, d1 < d2 the in-face axes); alpha
-  // per face = params[F]. A null array means beta = 1, f = 0, g_D = 0, g_R = 0.
-  const double *a_beta = nullptr, *a_f = nullptr, *a_gD = nullptr, *a_gR = nullptr;
+  // at the same face Gauss points in the same layout (Eq. bvp: alpha piecewise smooth), or, if that
+  // array is null, one alpha per face = params[F]. A null array means beta = 1, f = 0, g_D = 0, g_R = 0.
+  const double *a_beta = nullptr, *a_f = nullptr, *a_gD = nullptr, *a_gR = nullptr, *a_alpha = nullptr;
 
   // C5 / layered geometry (params layout documented in synth/__init__.py)
   double layer_beta_at(double z) const {
@@ -423,7 +424,8 @@ bool build_level(Level* L, const double lo[3], const double hi[3], const int n[3
           x[d] = L->coord(d, fixed);
           x[d1] = L->lo[d1] + (e1 + (1.0 + xi1) / 2.0) * L->h[d1];
           x[d2] = L->lo[d2] + (e2 + (1.0 + xi2) / 2.0) * L->h[d2];
-          aq[q] = P.alpha(face);
+          aq[q] = (P.id == PROB_ARRAYS && P.a_alpha) ? P.a_alpha[block + 4L * (e1 + (long)n[d1] * e2) + q]
+                                                     : P.alpha(face);
           gq[q] = P.id == PROB_ARRAYS ? (P.a_gR ? P.a_gR[block + 4L * (e1 + (long)n[d1] * e2) + q] : 0.0)
                                       : P.gR(face, x[0], x[1], x[2]);
         }
@@ -917,13 +919,14 @@ orc_level* orc_build_level(const double* lo, const double* hi, const int* n, int
   return h;
 }
 
-// PROB_ARRAYS level: alpha[6] per face, arrays as documented at Problem::a_beta (each may be NULL)
+// PROB_ARRAYS level: alpha[6] per face (used where alpha_q is NULL), arrays as documented at Problem::a_beta
+// (each may be NULL)
 orc_level* orc_build_level_arrays(const double* lo, const double* hi, const int* n, const int* face,
                                   const double* alpha, const double* beta_e, const double* f_q, const double* gD_n,
-                                  const double* gR_q) {
+                                  const double* gR_q, const double* alpha_q) {
   Problem P;
   if (!make_problem(PROB_ARRAYS, alpha, 6, face, &P)) return nullptr;
-  P.a_beta = beta_e; P.a_f = f_q; P.a_gD = gD_n; P.a_gR = gR_q;
+  P.a_beta = beta_e; P.a_f = f_q; P.a_gD = gD_n; P.a_gR = gR_q; P.a_alpha = alpha_q;
   orc_level* h = new orc_level;
   if (!build_level(&h->L, lo, hi, n, P)) { delete h; return nullptr; }
   return h;
@@ -1084,7 +1087,8 @@ void orc_serendipity_weights(double xi, double eta, double zeta, double* w20) {
 static int ecmg_impl(const double* lo, const double* hi, const int* coarsest, int num_levels, int problem_id,
                      const double* params, int nparams, const int* face, const double* eps_k, const int* maxit_k,
                      int precond, int exp_variant, double* stats, double* u_fine, double* ut_fine, double* w_fine,
-                     const double* const* level_arrays = nullptr /* PROB_ARRAYS: 4 per level */) {
+                     const double* const* level_arrays = nullptr /* PROB_ARRAYS: 4 per level */,
+                     int n_level_arrays = 0 /* 4 L, or 5 L: [4 L + k] = alpha at the face Gauss points of level k */) {
   Problem P;
   if (!make_problem(problem_id, params, nparams, face, &P)) return ORC_EINVAL;
   if (num_levels < 3) return ORC_EINVAL;
@@ -1101,6 +1105,7 @@ static int ecmg_impl(const double* lo, const double* hi, const int* coarsest, in
       if (!level_arrays) { delete L; return ORC_EINVAL; }
       P.a_beta = level_arrays[4 * k]; P.a_f = level_arrays[4 * k + 1];
       P.a_gD = level_arrays[4 * k + 2]; P.a_gR = level_arrays[4 * k + 3];
+      P.a_alpha = n_level_arrays >= 5 * num_levels ? level_arrays[4 * num_levels + k] : nullptr;
     }
     if (!build_level(L, lo, hi, n, P)) { delete L; return ORC_EINVAL; }
     double t1 = now_s();
@@ -1186,21 +1191,23 @@ int orc_ecmg(const double* lo, const double* hi, const int* coarsest, int num_le
 // Alg. 3: the original ECMG with a fixed number of iterations per level, Eq. (ee)
 // (P:290-295): m_j = ceil(m_L * ratio^(L-j)) on the j-th ECMG level (j = 1..L, L = num_levels - 2;
 // reading R4 in DESIGN.md), plain CG by default (precond = 0). Levels 0, 1: DSOLVE.
-// Alg. 4 on PROB_ARRAYS data: level_arrays[4 k + {0, 1, 2, 3}] = beta_e, f_q, gD_n, gR_q of level k
+// Alg. 4 on PROB_ARRAYS data: level_arrays[4 k + {0, 1, 2, 3}] = beta_e, f_q, gD_n, gR_q of level k, and with
+// n_level_arrays = 5 L also [4 L + k] = alpha at the face Gauss points of level k
 int orc_ecmg_arrays(const double* lo, const double* hi, const int* coarsest, int num_levels, const double* alpha,
-                    const int* face, const double* const* level_arrays, double eps, int max_iter, int precond,
-                    int exp_variant, double* stats, double* u_fine, double* ut_fine, double* w_fine) {
+                    const int* face, const double* const* level_arrays, int n_level_arrays, double eps, int max_iter,
+                    int precond, int exp_variant, double* stats, double* u_fine, double* ut_fine, double* w_fine) {
   if (num_levels < 3 || num_levels > 16 || !level_arrays) return ORC_EINVAL;
+  if (n_level_arrays != 4 * num_levels && n_level_arrays != 5 * num_levels) return ORC_EINVAL;
   std::vector<double> e(num_levels, eps);
   std::vector<int> m(num_levels, max_iter);
   return ecmg_impl(lo, hi, coarsest, num_levels, PROB_ARRAYS, alpha, 6, face, e.data(), m.data(), precond,
-                   exp_variant, stats, u_fine, ut_fine, w_fine, level_arrays);
+                   exp_variant, stats, u_fine, ut_fine, w_fine, level_arrays, n_level_arrays);
 }
 
 static int ecmg_fixed_impl(const double* lo, const double* hi, const int* coarsest, int num_levels, int problem_id,
                            const double* params, int nparams, const int* face, int m_L, double ratio, int precond,
                            int exp_variant, double* stats, double* u_fine, double* ut_fine, double* w_fine,
-                           const double* const* level_arrays) {
+                           const double* const* level_arrays, int n_level_arrays) {
   if (num_levels < 3 || num_levels > 16 || m_L < 0 || !(ratio > 0.0)) return ORC_EINVAL;
   const int Lc = num_levels - 2;
   std::vector<double> e(num_levels, 0.0);
@@ -1210,24 +1217,25 @@ static int ecmg_fixed_impl(const double* lo, const double* hi, const int* coarse
     m[k] = (int)std::ceil(m_L * std::pow(ratio, (double)(Lc - j)) - 1e-12);
   }
   return ecmg_impl(lo, hi, coarsest, num_levels, problem_id, params, nparams, face, e.data(), m.data(), precond,
-                   exp_variant, stats, u_fine, ut_fine, w_fine, level_arrays);
+                   exp_variant, stats, u_fine, ut_fine, w_fine, level_arrays, n_level_arrays);
 }
 
 int orc_ecmg_fixed(const double* lo, const double* hi, const int* coarsest, int num_levels, int problem_id,
                    const double* params, int nparams, const int* face, int m_L, double ratio, int precond,
                    int exp_variant, double* stats, double* u_fine, double* ut_fine, double* w_fine) {
   return ecmg_fixed_impl(lo, hi, coarsest, num_levels, problem_id, params, nparams, face, m_L, ratio, precond,
-                         exp_variant, stats, u_fine, ut_fine, w_fine, nullptr);
+                         exp_variant, stats, u_fine, ut_fine, w_fine, nullptr, 0);
 }
 
-// Alg. 3 on PROB_ARRAYS data (level_arrays as in orc_ecmg_arrays)
+// Alg. 3 on PROB_ARRAYS data (level_arrays, n_level_arrays as in orc_ecmg_arrays)
 int orc_ecmg_fixed_arrays(const double* lo, const double* hi, const int* coarsest, int num_levels,
-                          const double* alpha, const int* face, const double* const* level_arrays, int m_L,
-                          double ratio, int precond, int exp_variant, double* stats, double* u_fine, double* ut_fine,
-                          double* w_fine) {
+                          const double* alpha, const int* face, const double* const* level_arrays, int n_level_arrays,
+                          int m_L, double ratio, int precond, int exp_variant, double* stats, double* u_fine,
+                          double* ut_fine, double* w_fine) {
   if (!level_arrays) return ORC_EINVAL;
+  if (n_level_arrays != 4 * num_levels && n_level_arrays != 5 * num_levels) return ORC_EINVAL;
   return ecmg_fixed_impl(lo, hi, coarsest, num_levels, PROB_ARRAYS, alpha, 6, face, m_L, ratio, precond,
-                         exp_variant, stats, u_fine, ut_fine, w_fine, level_arrays);
+                         exp_variant, stats, u_fine, ut_fine, w_fine, level_arrays, n_level_arrays);
 }
 
 }  // extern "C"

@@ -114,3 +114,36 @@ def patch_arrays(n, layer_beta, lo=(0, 0, 0), hi=(1, 1, 1)):
 
     return sample(n, lo, hi, lambda x, y, z: beta_z(z), lambda x, y, z: 0.0 * x, patch_u,
                   lambda F, x, y, z: PATCH_ALPHA[F] * patch_u(x, y, z) + beta_z(z) * PATCH_DUDN[F], PATCH_FACES)
+
+
+# ---- the same linear patch with alpha given at the face Gauss points (Eq. bvp's piecewise smooth alpha):
+#      alpha_q random in [0, 3] at every Robin face Gauss point, g_R = alpha_q u + beta_e du/dn at the same points.
+#      The Robin form int alpha u_h v and the load int g_R v use the same 2x2 Gauss points and alpha values, and
+#      u is in Q1, so u is still the exact FE solution for ANY alpha_q >= 0.
+def patch_alpha_q(n, seed=47, lo=(0, 0, 0), hi=(1, 1, 1)):
+    """alpha at the 4 Gauss points of every face element, per face a block of 4 n_d1 n_d2 (gR's layout)."""
+    blocks = []
+    for F in range(6):
+        d1, d2 = FACE_AXES[F]
+        m = 4 * n[d1] * n[d2]
+        blocks.append(3.0 * __import__("synth").counter_uniform(seed + F, m) if PATCH_FACES[F] == 1 else np.zeros(m))
+    return np.concatenate(blocks)
+
+
+def patch_arrays_alpha_q(n, layer_beta, aq, lo=(0, 0, 0), hi=(1, 1, 1)):
+    """(beta_e, f_q, gD, gR, alpha_q) of the layered linear patch with alpha_q (patch_alpha_q) on the Robin faces."""
+    b, fq, g, _ = patch_arrays(n, layer_beta, lo, hi)
+    lb = np.asarray(layer_beta, dtype=np.float64)
+    hz = (hi[2] - lo[2]) / n[2]
+    blocks, off = [], 0
+    for F in range(6):
+        P = face_points(n, lo, hi, F)
+        m = P[0].size
+        a = aq[off:off + m].reshape(P[0].shape)
+        off += m
+        if PATCH_FACES[F] == 1:
+            bz = lb[np.clip(np.floor((P[2] - lo[2]) / hz).astype(np.int64), 0, n[2] - 1)]
+            blocks.append((a * patch_u(*P) + bz * PATCH_DUDN[F]).reshape(-1))
+        else:
+            blocks.append(np.zeros(m))
+    return b, fq, g, np.concatenate(blocks), aq
