@@ -89,10 +89,9 @@ typedef struct {
   ecmg_face_kind face[6];   /* x-, x+, y-, y+, z-, z+; must equal the problem's own boundary kinds */
   int problem_id;           /* ecmg_problem_id */
   const double* params;     /* host array, problem parameters (C5: 48 doubles, PATCH_LAYERED: 15,
-                               ARRAYS: 6 = alpha per face, read on Robin faces, >= 0). alpha is ONE
-                               constant per face (P:44-47 allows a piecewise smooth alpha; this library
-                               takes the constant-per-face case, reading R6); a spatially
-                               varying alpha cannot be expressed and is not supported. Copied. */
+                               ARRAYS: 6 = alpha per face, read on Robin faces, >= 0; a spatially varying
+                               alpha is given at the face Gauss points through level_arrays
+                               [4L+k], below). Copied. */
   int n_params;
   /* ECMG_PROB_ARRAYS only (else NULL / 0): n_level_arrays = 4 * num_levels device pointers, level k's
    * data of Eq. (bvp) at the points the discretisation reads:
@@ -104,9 +103,15 @@ typedef struct {
    *   [4k+3] gR       per face F = x-, x+, y-, y+, z-, z+ a block of 4 n_d1 n_d2 values (d1 < d2 the in-face
    *                   axes), index 4 (e1 + n_d1 e2) + q, q = q_1 + 2 q_2 the 2x2 face Gauss point; read on
    *                   Robin faces only; NULL = 0
-   * The grid keeps the pointers: the arrays are read by every call that runs a level's setup or a
-   * Dirichlet fill (ecmg_run, ecmg_run_fixed, ecmg_solve_level, ecmg_level_rhs, the EXP calls) and must stay
-   * valid and unchanged until the next ecmg_set_coeffs or ecmg_destroy_grid (reading R6).
+   * n_level_arrays = 5 * num_levels adds, after those 4 * num_levels pointers, one per level:
+   *   [4L+k] alpha_q  alpha at the 2x2 face Gauss points, gR's layout and points (Eq. bvp's piecewise smooth
+   *                   alpha), read on Robin faces only, >= 0 (not checked); NULL on a level = the
+   *                   per-face alpha of params on that level. The Robin face mass of a face element is then
+   *                   h1 h2 / 4 sum_q alpha_q N_c(q) N_d(q), the 2x2 rule the Robin load uses.
+   * The grid keeps the pointers: the arrays are read by every call that runs a level's setup, a Dirichlet
+   * fill or the operator (ecmg_run, ecmg_run_fixed, ecmg_solve_level, ecmg_level_rhs, ecmg_apply_operator, the
+   * EXP calls) and must stay valid and unchanged until the next ecmg_set_coeffs or ecmg_destroy_grid (DESIGN.md
+   * reading R6).
    * Single GPU only (ECMG_EINVAL with dist / virtual slabs). */
   const double* const* level_arrays;
   int n_level_arrays;

@@ -127,7 +127,7 @@ struct ecmg_grid {
   std::vector<double*> betal;      // per-level element beta (element path)
   std::vector<double*> s1d;        // per-level 1D Gauss load tables (separable right-hand sides)
   std::vector<char> setup_ok;      // level k's b / beta hold the current problem's data
-  std::vector<const double*> arrays;   // ECMG_PROB_ARRAYS: the caller's 4 device arrays per level
+  std::vector<const double*> arrays;   // ECMG_PROB_ARRAYS: the caller's device arrays, 5 per level (alpha_q may be null)
   int setup_ahead = 1;             // ECMG_OPT_SETUP_AHEAD
   int beta_fly = 0;                // ECMG_OPT_BETA_FLY: element kernels form analytic beta from axis tables (measured:
                                    // 16 B/unknown less traffic but no faster -- the element kernels are latency bound)
@@ -257,9 +257,11 @@ int level_of(const ecmg_grid* G, const LevelGeom& g) {
   return -1;
 }
 
+Problem level_prob(const ecmg_grid* G, int k);
+
 cudaError_t launch_mode(ecmg_grid* G, int mode, const LevelGeom& g, const KArgs& a) {
   if (G->elem_path) {
-    ElemStencil es = make_elem_stencil(g, G->prob, G->precond);
+    ElemStencil es = make_elem_stencil(g, level_prob(G, level_of(G, g)), G->precond);
     if (G->beta_fly && a.beta) set_beta_fly(es, g, G->prob, a.beta);
     return launch_jcg_elem(mode, g, es, G->prob, a, G->stream);
   }
@@ -282,8 +284,8 @@ cudaError_t launch_mode(ecmg_grid* G, int mode, const LevelGeom& g, const KArgs&
 // the problem as level k's kernels see it (ECMG_PROB_ARRAYS: with that level's caller arrays)
 Problem level_prob(const ecmg_grid* G, int k) {
   Problem p = G->prob;
-  if (p.id == PROB_ARRAYS && (int)G->arrays.size() == 4 * G->L)
-    for (int j = 0; j < 4; ++j) p.arr[j] = G->arrays[4 * k + j];
+  if (p.id == PROB_ARRAYS && (int)G->arrays.size() == 5 * G->L)
+    for (int j = 0; j < 5; ++j) p.arr[j] = G->arrays[5 * k + j];
   return p;
 }
 
@@ -448,7 +450,7 @@ cudaError_t launch_pers_tma(ecmg_grid* G, const LevelGeom& g) {
   const int k = level_of(G, g);
   const ConstStencil cs = make_const_stencil(g, 1.0, G->precond);
   if (G->elem_path) {
-    ElemStencil es = make_elem_stencil(g, G->prob, G->precond);
+    ElemStencil es = make_elem_stencil(g, level_prob(G, k), G->precond);
     if (G->beta_fly) set_beta_fly(es, g, G->prob, G->betal[k]);
     return launch_jcg_elem_pers(g, es, G->x, G->r, G->zv, G->p[0], G->p[1], G->bl[k], G->betal[k], G->partials, G->sc,
                                 G->stream);
@@ -464,7 +466,7 @@ cudaError_t launch_persistent(ecmg_grid* G, const LevelGeom& g) {
   const ConstStencil cs = make_const_stencil(g, 1.0, G->precond);
   if (use_cta(G, g)) {
     if (!G->elem_path) return launch_jcg_cta(g, cs, nullptr, G->x, G->r, nullptr, G->bl[k], G->sc, G->stream);
-    const ElemStencil es = make_elem_stencil(g, G->prob, G->precond);
+    const ElemStencil es = make_elem_stencil(g, level_prob(G, k), G->precond);
     return launch_jcg_cta(g, cs, &es, G->x, G->r, G->betal[k], G->bl[k], G->sc, G->stream);
   }
   // w = A p (and on the element path D^-1) in scratch vectors sized for the level (grown on demand)
@@ -482,7 +484,7 @@ cudaError_t launch_persistent(ecmg_grid* G, const LevelGeom& g) {
   if (!G->elem_path)
     return launch_jcg_persistent(g, cs, nullptr, G->x, G->r, nullptr, G->p[0], G->p[1], G->aux[0], nullptr, nullptr, G->bl[k],
                                  G->partials, G->sc, G->stream);
-  const ElemStencil es = make_elem_stencil(g, G->prob, G->precond);
+  const ElemStencil es = make_elem_stencil(g, level_prob(G, k), G->precond);
   return launch_jcg_persistent(g, cs, &es, G->x, G->r, G->zv, G->p[0], G->p[1], G->aux[0], G->aux[1], G->betal[k], G->bl[k],
                                G->partials, G->sc, G->stream);
 }
@@ -871,7 +873,9 @@ int ecmg_set_coeffs(ecmg_grid* G, const ecmg_problem* pr) {
   if (pr->problem_id == ECMG_PROB_ARRAYS) {
     // caller data per level: single grid only, alpha per face in params[0..5]
     if (G->slab || G->nranks > 1) return ECMG_EINVAL;
-    if (!pr->level_arrays || pr->n_level_arrays != 4 * G->L || pr->n_params != 6 || !pr->params) return ECMG_EINVAL;
+    if (!pr->level_arrays || (pr->n_level_arrays != 4 * G->L && pr->n_level_arrays != 5 * G->L) || pr->n_params != 6 ||
+        !pr->params)
+      return ECMG_EINVAL;
     for (int f = 0; f < 6; ++f) {
       if (pr->face[f] != ECMG_DIRICHLET && pr->face[f] != ECMG_ROBIN) return ECMG_EINVAL;
       pb.face[f] = pr->face[f];
@@ -913,8 +917,15 @@ int ecmg_set_coeffs(ecmg_grid* G, const ecmg_problem* pr) {
   }
   G->prob = pb;
   G->elem_path = elem_path;
-  if (pb.id == PROB_ARRAYS) G->arrays.assign(pr->level_arrays, pr->level_arrays + 4 * G->L);
-  else G->arrays.clear();
+  if (pb.id == PROB_ARRAYS) {   // 5 per level: beta_e, f_q, g_D, g_R, alpha_q (alpha_q null: alpha per face)
+    G->arrays.assign(5 * G->L, nullptr);
+    for (int k = 0; k < G->L; ++k) {
+      for (int j = 0; j < 4; ++j) G->arrays[5 * k + j] = pr->level_arrays[4 * k + j];
+      if (pr->n_level_arrays == 5 * G->L) G->arrays[5 * k + 4] = pr->level_arrays[4 * G->L + k];
+    }
+  } else {
+    G->arrays.clear();
+  }
   G->geom.clear();
   for (int k = 0; k < G->L; ++k) G->geom.push_back(make_geom(G->dom, G->n0, k, pb.face, elem_path));
   G->has_problem = true;

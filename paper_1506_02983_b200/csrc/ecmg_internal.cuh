@@ -29,9 +29,10 @@ struct Problem {
   double alpha[6];        // Robin alpha per face (0 = Neumann)
   double params[kMaxParams];
   int n_params;
-  // PROB_ARRAYS: the caller's device arrays of ONE level (beta_e, f at the Gauss points, g_D per node, g_R at
-  // the face Gauss points; layouts in include/ecmg.h), set per launch by the host (level_prob); null = 0 / 1
-  const double* arr[4];
+  // PROB_ARRAYS: the caller's device arrays of ONE level (beta_e, f at the Gauss points, g_D per node, g_R and
+  // alpha at the face Gauss points; layouts in include/ecmg.h), set per launch by the host (level_prob);
+  // null = 0 / 1 (alpha: null = alpha[F] per face)
+  const double* arr[5];
 };
 constexpr int PROB_ARRAYS = 100;
 
@@ -74,7 +75,57 @@ struct ElemStencil {
   int bkind;
   int bw;              // table row width W = max_d n_d + 4
   const double* baxes;
+  // PROB_ARRAYS with alpha at the face Gauss points: the level's alpha_q array (include/ecmg.h layout); then
+  // robin[F] = h1 h2 marks the Robin faces and the face mass is formed per face element (robin_elem_row)
+  const double* aq;
 };
+
+// ---- Robin face mass with alpha at the 2x2 face Gauss points (Eq. bvp's piecewise smooth alpha) -------
+// first value of face F's block of alpha_q (blocks x-, x+, y-, y+, z-, z+ of 4 n_d1 n_d2 values, d1 < d2 the in-face
+// axes) and of its face element (e1, e2)
+__host__ __device__ inline const double* robin_aq(const double* aq, const int n[3], int F, int e1, int e2) {
+  long long off = 0;
+  for (int f = 0; f < F; ++f) {
+    const int d = f >> 1, a1 = d == 0 ? 1 : 0, a2 = d == 2 ? 1 : 2;
+    off += 4LL * n[a1] * n[a2];
+  }
+  const int d = F >> 1, a1 = d == 0 ? 1 : 0;
+  return aq + off + 4LL * (e1 + (long long)n[a1] * e2);
+}
+// 1D linear shape value of local node c (0 / 1) at Gauss point q (0: xi = -1/sqrt3, 1: +1/sqrt3)
+__host__ __device__ inline double robin_n(int c, int q) {
+  const double ga = 0.21132486540518711775, gb = 0.78867513459481288225;   // (1 -+ 1/sqrt3) / 2
+  return c == q ? gb : ga;
+}
+// face element of area hh with alpha a4[q] (q = q1 + 2 q2) at its Gauss points: the mass row of local corner
+// (c1, c2) against nodal values v0..v3 (index c1' + 2 c2') added to acc, its diagonal entry to dg:
+// M[c][d] = hh / 4 sum_q a_q N_c(q) N_d(q), evaluated as hh / 4 sum_q a_q N_c(q) v(q)
+__host__ __device__ inline void robin_elem_row(const double* a4, int c1, int c2, double v0, double v1, double v2, double v3,
+                                                double hh, double& acc, double& dg) {
+  double s = 0.0, d = 0.0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int q1 = q & 1, q2 = q >> 1;
+    const double n10 = robin_n(0, q1), n11 = robin_n(1, q1), n20 = robin_n(0, q2), n21 = robin_n(1, q2);
+    const double vq = n20 * (n10 * v0 + n11 * v1) + n21 * (n10 * v2 + n11 * v3);
+    const double nc = robin_n(c1, q1) * robin_n(c2, q2);
+    const double a = a4[q];
+    s += a * nc * vq;
+    d += a * nc * nc;
+  }
+  acc += 0.25 * hh * s;
+  dg += 0.25 * hh * d;
+}
+// one entry M[c][j] of that face element (the lifting against a Dirichlet node j of the same face element)
+__host__ __device__ inline double robin_elem_entry(const double* a4, int c1, int c2, int j1, int j2, double hh) {
+  double s = 0.0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int q1 = q & 1, q2 = q >> 1;
+    s += a4[q] * (robin_n(c1, q1) * robin_n(c2, q2)) * (robin_n(j1, q1) * robin_n(j2, q2));
+  }
+  return 0.25 * hh * s;
+}
 
 // Analytic beta at element centroids (Eq. bvp, reading A3) from per-axis tables, so that the beta array
 // (k_beta) and the element kernels' on-the-fly values are the same function of the same table entries:

@@ -64,6 +64,12 @@ inline ElemStencil make_elem_stencil(const LevelGeom& g, const Problem& pb, int 
     const int d1 = (d == 0) ? 1 : 0, d2 = (d == 2) ? 1 : 2;
     es.robin[F] = (pb.face[F] == FACE_ROBIN && pb.alpha[F] != 0.0) ? pb.alpha[F] * g.h[d1] * g.h[d2] : 0.0;
   }
+  es.aq = (pb.id == PROB_ARRAYS) ? pb.arr[4] : nullptr;
+  if (es.aq)   // alpha at the face Gauss points: every Robin face carries a mass term, its alpha read per element
+    for (int F = 0; F < 6; ++F) {
+      const int d = F >> 1, d1 = (d == 0) ? 1 : 0, d2 = (d == 2) ? 1 : 2;
+      es.robin[F] = pb.face[F] == FACE_ROBIN ? g.h[d1] * g.h[d2] : 0.0;
+    }
   es.precond = precond;
   es.cube = g.h[0] == g.h[1] && g.h[0] == g.h[2];
   es.bkind = -1;   // the caller enables beta on the fly (set_beta_fly) where the tables exist

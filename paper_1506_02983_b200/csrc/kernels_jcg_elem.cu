@@ -118,15 +118,18 @@ __device__ __forceinline__ void issue_elem_stage(unsigned char* smem, uint64_t* 
 // ring continues at the running step count G (stage (G + s) % NS, parity ((G + s) / NS) & 1), so that a
 // persistent CTA can run several passes over the same mbarriers. Adds the thread's partial sums to
 // acc0..acc2. The caller has initialised the mbarriers and synchronised the CTA since its previous pass.
-// BF: 0 = beta from the array (TMA box per layer); 1 = on the fly, product kind (C3); 2 = on the fly,
-// bit-mask kinds (beta = 1, layers, C5 boxes) -- see beta_combine
-template <int MODE, int NS, bool CUBE, int SB, int BF>
+// BFA: 0 = beta from the array (TMA box per layer); 1 = on the fly, product kind (C3); 2 = on the fly,
+// bit-mask kinds (beta = 1, layers, C5 boxes) -- see beta_combine; 3 = beta from the array and the Robin alpha
+// at the face Gauss points (ARRAYS alpha_q, es.aq): the only instantiations that carry that branch
+template <int MODE, int NS, bool CUBE, int SB, int BFA>
 __device__ __forceinline__ void elem_pass(const LevelGeom& g, const ElemStencil& es, const KArgs& a, int X0, int Y0, int z0,
                                           int z1, double bcg_eff, bool first, double alpha, double* u_out,
                                           const CUtensorMap* pH0, const CUtensorMap* pH1, const CUtensorMap* pE,
                                           const CUtensorMap* pI0, const CUtensorMap* pI1, unsigned char* smem, uint64_t* full,
                                           const uint32_t G, double& acc0, double& acc1, double& acc2) {
   using C = ElemCfg<MODE>;
+  constexpr int BF = BFA == 3 ? 0 : BFA;   // how beta arrives
+  constexpr bool AQ = BFA == 3;            // alpha at the face Gauss points
   const int lane = threadIdx.x, w = threadIdx.y, tid = lane + TX * w;
   const int nfx = g.nf[0], nfy = g.nf[1];
   const long long S = g.S;
@@ -298,7 +301,60 @@ __device__ __forceinline__ void elem_pass(const LevelGeom& g, const ElemStencil&
             __fma_rn(k4, gd0, __fma_rn(k5, gd1, __fma_rn(k6, gd2, k7 * gd3)))))));
       }
       double diag_d = k0 * B4, diag_u = k0 * B4;
-      if (rare) {
+      if (AQ && rare) {
+        // Robin face mass with alpha at the face Gauss points (ARRAYS alpha_q): per face element, its 4 alphas
+        // read from the caller's array (boundary nodes only). Windows: rows j..j+2 = y-1..y+1, columns 0..2 =
+        // x-1..x+1 of planes d (wd) and u (wu)
+        double ad = 0.0, au = 0.0, gdd = 0.0, gdu = 0.0;
+        const int gy = gy0 + j;
+        if (layer_ok)
+          for (int F = 0; F < 2; ++F) {   // x faces through this layer: face elements (y-1 | y) x (layer)
+            if (es.robin[F] == 0.0 || gx != (F ? g.n[0] : 0)) continue;
+            const double hh = es.robin[F];
+            if (gy >= 1) {
+              const double* a4 = robin_aq(es.aq, g.n, F, gy - 1, gzd);
+              robin_elem_row(a4, 1, 0, wd[j][1], wd[j + 1][1], wu[j][1], wu[j + 1][1], hh, ad, gdd);
+              robin_elem_row(a4, 1, 1, wd[j][1], wd[j + 1][1], wu[j][1], wu[j + 1][1], hh, au, gdu);
+            }
+            if (gy < g.n[1]) {
+              const double* a4 = robin_aq(es.aq, g.n, F, gy, gzd);
+              robin_elem_row(a4, 0, 0, wd[j + 1][1], wd[j + 2][1], wu[j + 1][1], wu[j + 2][1], hh, ad, gdd);
+              robin_elem_row(a4, 0, 1, wd[j + 1][1], wd[j + 2][1], wu[j + 1][1], wu[j + 2][1], hh, au, gdu);
+            }
+          }
+        if (layer_ok)
+          for (int F = 2; F < 4; ++F) {   // y faces through this layer: face elements (x-1 | x) x (layer)
+            if (es.robin[F] == 0.0 || gy != (F == 3 ? g.n[1] : 0)) continue;
+            const double hh = es.robin[F];
+            if (gx >= 1) {
+              const double* a4 = robin_aq(es.aq, g.n, F, gx - 1, gzd);
+              robin_elem_row(a4, 1, 0, wd[j + 1][0], wd[j + 1][1], wu[j + 1][0], wu[j + 1][1], hh, ad, gdd);
+              robin_elem_row(a4, 1, 1, wd[j + 1][0], wd[j + 1][1], wu[j + 1][0], wu[j + 1][1], hh, au, gdu);
+            }
+            if (gx < g.n[0]) {
+              const double* a4 = robin_aq(es.aq, g.n, F, gx, gzd);
+              robin_elem_row(a4, 0, 0, wd[j + 1][1], wd[j + 1][2], wu[j + 1][1], wu[j + 1][2], hh, ad, gdd);
+              robin_elem_row(a4, 0, 1, wd[j + 1][1], wd[j + 1][2], wu[j + 1][1], wu[j + 1][2], hh, au, gdu);
+            }
+          }
+        for (int F = 4; F < 6; ++F) {     // z face through plane d: the in-plane face elements (x-1 | x) x (y-1 | y)
+          if (es.robin[F] == 0.0 || gzd != (F == 5 ? g.n[2] : 0)) continue;
+          const double hh = es.robin[F];
+          for (int sy = 0; sy < 2; ++sy)
+            for (int sx = 0; sx < 2; ++sx) {
+              const int ex = gx - 1 + sx, ey = gy - 1 + sy;
+              if (ex < 0 || ex >= g.n[0] || ey < 0 || ey >= g.n[1]) continue;
+              const double* a4 = robin_aq(es.aq, g.n, F, ex, ey);
+              // element corners (ex, ey) .. (ex+1, ey+1) at window rows j+sy, j+sy+1 and columns sx, sx+1
+              robin_elem_row(a4, 1 - sx, 1 - sy, wd[j + sy][sx], wd[j + sy][sx + 1], wd[j + sy + 1][sx],
+                             wd[j + sy + 1][sx + 1], hh, ad, gdd);
+            }
+        }
+        upd += ad;
+        dnu += au;
+        diag_d += gdd;
+        diag_u += gdu;
+      } else if (rare) {
         // Robin face mass: x- / y-faces through this layer, z-face of plane d (in-plane)
         double ad = 0.0, au = 0.0, gdg = 0.0;
         const int gy = gy0 + j;
@@ -565,6 +621,8 @@ cudaError_t set_elem_tma_attr() {
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_jcg_elem_tma<MODE, NS, true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_jcg_elem_tma<MODE, NS, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_jcg_elem_tma<MODE, NS, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_jcg_elem_tma<MODE, NS, false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_jcg_elem_tma<MODE, NS, true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   return e;
 }
 
@@ -581,6 +639,10 @@ cudaError_t launch_elem_tma_mode(const LevelGeom& g, const ElemStencil& es, cons
   count_launch();
   const int sm = elem_smem<MODE, NS>();
   const dim3 blk(TX, WARPS);
+  if (es.aq) {   // Robin alpha at the face Gauss points (ARRAYS)
+    if (es.cube) return launch_maybe_pdl(k_jcg_elem_tma<MODE, NS, true, 3>, grid, blk, sm, st, a.pdl, g, es, a, m[0], m[1], m[2], m[3], m[4]);
+    return launch_maybe_pdl(k_jcg_elem_tma<MODE, NS, false, 3>, grid, blk, sm, st, a.pdl, g, es, a, m[0], m[1], m[2], m[3], m[4]);
+  }
   switch (es.cube ? 1 + beta_fly_variant(es) : 0) {
     case 1: return launch_maybe_pdl(k_jcg_elem_tma<MODE, NS, true, 0>, grid, blk, sm, st, a.pdl, g, es, a, m[0], m[1], m[2], m[3], m[4]);
     case 2: return launch_maybe_pdl(k_jcg_elem_tma<MODE, NS, true, 1>, grid, blk, sm, st, a.pdl, g, es, a, m[0], m[1], m[2], m[3], m[4]);
@@ -691,6 +753,8 @@ cudaError_t init_elem_pers_attributes() {
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_jcg_elem_pers<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, EP_SMEM);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_jcg_elem_pers<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, EP_SMEM);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_jcg_elem_pers<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, EP_SMEM);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_jcg_elem_pers<true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, EP_SMEM);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_jcg_elem_pers<false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, EP_SMEM);
   return e;
 }
 
@@ -717,7 +781,8 @@ cudaError_t launch_jcg_elem_pers(const LevelGeom& g, const ElemStencil& es, doub
                   (void*)&sc, (void*)&zc, (void*)&ntx, (void*)&nty, (void*)&items, (void*)&M};
   count_launch();
   const void* fn = (const void*)k_jcg_elem_pers<false, 0>;
-  switch (es.cube ? 1 + beta_fly_variant(es) : 0) {
+  if (es.aq) fn = es.cube ? (const void*)k_jcg_elem_pers<true, 3> : (const void*)k_jcg_elem_pers<false, 3>;
+  else switch (es.cube ? 1 + beta_fly_variant(es) : 0) {
     case 1: fn = (const void*)k_jcg_elem_pers<true, 0>; break;
     case 2: fn = (const void*)k_jcg_elem_pers<true, 1>; break;
     case 3: fn = (const void*)k_jcg_elem_pers<true, 2>; break;

@@ -164,7 +164,29 @@ __device__ __forceinline__ double apply_elem(const LevelGeom& g, const ElemStenc
   const double rfx = (gx == 0 ? es.robin[0] : 0.0) + (gx == g.n[0] ? es.robin[1] : 0.0);
   const double rfy = (gy == 0 ? es.robin[2] : 0.0) + (gy == g.n[1] ? es.robin[3] : 0.0);
   const double rfz = (gz == 0 ? es.robin[4] : 0.0) + (gz == g.n[2] ? es.robin[5] : 0.0);
-  if (rfx != 0.0 || rfy != 0.0 || rfz != 0.0) {
+  if ((rfx != 0.0 || rfy != 0.0 || rfz != 0.0) && es.aq) {
+    // alpha at the face Gauss points (ARRAYS alpha_q): every face element of every Robin face through the node
+    const int gc[3] = {gx, gy, gz};
+#pragma unroll
+    for (int F = 0; F < 6; ++F) {
+      const int D = F >> 1;
+      if (es.robin[F] == 0.0 || gc[D] != ((F & 1) ? g.n[D] : 0)) continue;
+      const int t1 = D == 0 ? 1 : 0, t2 = D == 2 ? 1 : 2;
+      for (int s2 = 0; s2 < 2; ++s2)
+        for (int s1 = 0; s1 < 2; ++s1) {
+          const int e1 = gc[t1] - 1 + s1, e2 = gc[t2] - 1 + s2;
+          if (e1 < 0 || e1 >= g.n[t1] || e2 < 0 || e2 >= g.n[t2]) continue;
+          const double* a4 = robin_aq(es.aq, g.n, F, e1, e2);
+          double v[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {   // element corner (e1 + (c & 1), e2 + (c >> 1)) at offsets from the node
+            const int o1 = s1 - 1 + (c & 1), o2 = s2 - 1 + (c >> 1);
+            v[c] = D == 0 ? p27[1 + o2][1 + o1][1] : (D == 1 ? p27[1 + o2][1][1 + o1] : p27[1][1 + o2][1 + o1]);
+          }
+          robin_elem_row(a4, 1 - s1, 1 - s2, v[0], v[1], v[2], v[3], es.robin[F], ap, dg);
+        }
+    }
+  } else if (rfx != 0.0 || rfy != 0.0 || rfz != 0.0) {
     const double cm[3] = {gx >= 1 ? 1.0 : 0.0, gy >= 1 ? 1.0 : 0.0, gz >= 1 ? 1.0 : 0.0};
     const double cp[3] = {gx < g.n[0] ? 1.0 : 0.0, gy < g.n[1] ? 1.0 : 0.0, gz < g.n[2] ? 1.0 : 0.0};
     if (rfx != 0.0) robin_face<0>(rfx, p27, cm, cp, ap, dg);

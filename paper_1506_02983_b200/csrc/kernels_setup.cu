@@ -431,6 +431,14 @@ __global__ void k_rhs_shell(const LevelGeom g, const Problem pb, const ElemStenc
         const int dF = F >> 1;
         const int plane = (F & 1) ? g.n[dF] : 0;
         if (sel3(dF, gx, gy, gz) != plane || sel3(dF, jx, jy, jz) != plane) continue;
+        if (es.aq) {   // alpha at the face Gauss points: the entry of this volume element's face element
+          const int t1 = dF == 0 ? 1 : 0, t2 = dF == 2 ? 1 : 2;
+          const int e1 = ge[t1], e2 = ge[t2];
+          const double* a4 = robin_aq(es.aq, g.n, F, e1, e2);
+          sub += robin_elem_entry(a4, sel3(t1, gx, gy, gz) - e1, sel3(t2, gx, gy, gz) - e2, sel3(t1, jx, jy, jz) - e1,
+                                  sel3(t2, jx, jy, jz) - e2, es.robin[F]) * gD;
+          continue;
+        }
         const int nd = (dF != 0 && jx != gx) + (dF != 1 && jy != gy) + (dF != 2 && jz != gz);
         sub += es.robin[F] * (nd == 0 ? (1.0 / 9.0) : (nd == 1 ? (1.0 / 18.0) : (1.0 / 36.0))) * gD;
       }

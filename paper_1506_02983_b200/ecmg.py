@@ -133,7 +133,8 @@ def create_grid(lo, hi, coarsest_cells, num_levels, stream=None, dist=None):
 
 
 def set_coeffs(grid, problem_id, faces, params=None, level_arrays=None):
-    """level_arrays (ECMG_PROB_ARRAYS): 4 device arrays (or None) per level, flattened in level order; the
+    """level_arrays (ECMG_PROB_ARRAYS): 4 device arrays (or None) per level, flattened in level order, optionally
+    followed by one alpha_q array (or None) per level (5 L in all); the
     library keeps the pointers, the caller keeps the arrays alive (include/ecmg.h)."""
     pr = ecmg_problem()
     for i, f in enumerate(faces):
@@ -267,8 +268,13 @@ class Grid:
         st, self.h = create_grid(lo, hi, coarsest, num_levels, stream, dist)
         if st != OK:
             raise EcmgError(st, "ecmg_create_grid")
-        # ARRAYS: level_arrays[k] = (beta_e, f_q, gD, gR) device float64 tensors (or None), kept alive here
-        self._arrays = [a for lv in level_arrays for a in lv] if level_arrays is not None else None
+        # ARRAYS: level_arrays[k] = (beta_e, f_q, gD, gR[, alpha_q]) device float64 tensors (or None), kept alive
+        # here; the ABI order is the 4 of every level, then alpha_q of every level (n_level_arrays = 5 L)
+        self._arrays = None
+        if level_arrays is not None:
+            self._arrays = [a for lv in level_arrays for a in lv[:4]]
+            if any(len(lv) > 4 for lv in level_arrays):
+                self._arrays += [lv[4] if len(lv) > 4 else None for lv in level_arrays]
         self._check(set_coeffs(self.h, problem_id, faces if faces is not None else default_faces(problem_id), params,
                                self._arrays), "ecmg_set_coeffs")
         self._check(set_option(self.h, OPT_EXP_VARIANT, exp_variant), "ecmg_set_option")

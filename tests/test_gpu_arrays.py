@@ -182,3 +182,73 @@ def test_arrays_zero_data():
     assert float(u.abs().max()) == 0.0 and float(ut.abs().max()) == 0.0
     assert np.max(np.abs(ou)) == 0.0
     g.close()
+
+
+# ---- alpha at the face Gauss points (ARRAYS alpha_q, n_level_arrays = 5 L; Eq. bvp) -------------------
+from arrays_data import FACE_AXES, PATCH_FACES, patch_alpha_q, patch_arrays_alpha_q, patch_u, node_points  # noqa: E402
+
+
+def alpha_q(n, seed):
+    """alpha >= 0 at the 4 Gauss points of every face element (gR's layout), seeded."""
+    m = sum(4 * n[FACE_AXES[F][0]] * n[FACE_AXES[F][1]] for F in range(6))
+    return 3.0 * synth.counter_uniform(seed, m)
+
+
+@pytest.mark.parametrize("case", ["robin", "neumann_z"])
+def test_arrays_alpha_q_rhs_and_operator(case):
+    # the Robin mass from alpha_q on the GPU (TMA element kernels, box cells) against the oracle's level
+    n0, levels = (5, 3, 4), 4
+    faces, alpha, wb = CASES[case]
+    data = [lv + (alpha_q(tuple(c << k for c in n0), 90 + k),) for k, lv in enumerate(level_data(n0, levels, wb))]
+    g, _ = make(n0, levels, case, data)
+    for k in (2, 3):
+        n = tuple(c << k for c in n0)
+        L = o.Level.from_arrays(n, faces, alpha, *data[k][:4], alpha_q=data[k][4])
+        free = L.dirichlet()[0] == 0
+        b = g.new_vec(k)
+        g.level_rhs(k, b)
+        bo, _ = L.rhs()
+        assert rel(host(b)[free], bo[free]) <= 1e-13
+        p = np.where(free, synth.random_nodal(11, n), 0.0)
+        q = g.new_vec(k)
+        g.apply_operator(k, dev(p), q)
+        assert rel(host(q)[free], L.apply(p)[free]) <= 1e-13
+    g.close()
+
+
+@pytest.mark.parametrize("n0", [(5, 3, 4), (4, 4, 4)])
+def test_arrays_alpha_q_ecmg_run(n0):
+    # Alg. 4 with alpha_q on every level (one-CTA, cluster / cooperative and TMA solves on the way) vs the oracle
+    levels, eps, case = 4, 1e-10, "robin"
+    faces, alpha, wb = CASES[case]
+    data = [lv + (alpha_q(tuple(c << k for c in n0), 70 + k),) for k, lv in enumerate(level_data(n0, levels, wb, seed=60))]
+    g, _ = make(n0, levels, case, data)
+    u, ut = g.new_vec(levels - 1), g.new_vec(levels - 1)
+    st, stats = g.run(eps, u, ut)
+    ost, ostats, ou, out = o.ecmg_arrays(n0, levels, faces, alpha, data, eps)
+    assert st == 0 and ost == 0
+    it_g = [s["iterations"] for s in stats[2:]]
+    it_o = [int(v) for v in ostats[2:, 0]]
+    assert all(abs(a - b) <= 1 for a, b in zip(it_g, it_o)), (it_g, it_o)
+    assert np.max(np.abs(host(u) - ou)) <= 1e-9 * np.max(np.abs(ou))
+    assert np.max(np.abs(host(ut) - out)) <= 1e-9 * np.max(np.abs(out))
+    g.close()
+
+
+def test_arrays_alpha_q_patch_exact():
+    # the layered linear patch with random alpha_q >= 0 on four Robin faces: the FE solution is u itself (Galerkin
+    # exactness, pinned for the oracle in test_oracle_arrays.py), on every path of the cascade to 64^3
+    n0, levels = 4, 5
+    lv = []
+    for k in range(levels):
+        n = (n0 << k,) * 3
+        lv.append(patch_arrays_alpha_q(n, np.full(n[2], 1.3), patch_alpha_q(n)))
+    dv = [tuple(dev(a) for a in x) for x in lv]
+    g = Grid(n0, levels, PROB["ARRAYS"], params=[0.0] * 6, faces=PATCH_FACES, level_arrays=dv)
+    u, ut = g.new_vec(levels - 1), g.new_vec(levels - 1)
+    st, stats = g.run(1e-13, u, ut)
+    assert st == 0
+    nf = (n0 << (levels - 1),) * 3
+    ue = patch_u(*node_points(nf, (0, 0, 0), (1, 1, 1))).reshape(-1)
+    assert np.max(np.abs(host(u) - ue)) <= 1e-10 and np.max(np.abs(host(ut) - ue)) <= 1e-10
+    g.close()
