@@ -1,3 +1,7 @@
 mkdir -p gpurun_out
-timeout 300 python tools/tts_ab.py 11 PERS_TMA=20000000,PERSISTENT=40000 PERS_TMA=20000000,PERSISTENT=300000 > gpurun_out/ab_persist.log 2>&1
-TTS_CFG=c3 timeout 300 python tools/tts_ab.py 5 PERS_TMA=20000000,PERSISTENT=40000 PERS_TMA=20000000,PERSISTENT=300000 >> gpurun_out/ab_persist.log 2>&1
+: > gpurun_out/ab_prio.log
+for v in default prio_zc1 prio_zc4 zc1; do
+  echo "== $v" >> gpurun_out/ab_prio.log
+  if [ $v = default ]; then timeout 300 python tools/tts_ab.py 11 PERS_TMA=20000000 >> gpurun_out/ab_prio.log 2>&1;
+  else ECMG_LIB_PATH=$PWD/build/variants/libfull_$v.so timeout 300 python tools/tts_ab.py 11 PERS_TMA=20000000 >> gpurun_out/ab_prio.log 2>&1; fi
+done
