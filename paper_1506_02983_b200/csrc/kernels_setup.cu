@@ -257,7 +257,7 @@ struct RhsC4Consts {
 // form y (1 + e/4), e = 1 - r^2 y^4 (error 5e^2/32: ~3e-14). r^2 > 0 at every Gauss point (interior to
 // the elements) and stays in the normal fp32 range on every level.
 __device__ __forceinline__ double rpow_m14(double r2, const RhsC4Consts& k) {
-  const float xf = (float)r2;
+  const float xf = (float)r2;   // (an F2F-free narrowing by integer operations measured no faster: 1.762 ms either way)
   float y;
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(xf));
   asm("sqrt.approx.ftz.f32 %0, %0;" : "+f"(y));
