@@ -31,9 +31,9 @@ def one(path, cfg, zcs=(0,)):
             g.solve_level(k, 0.0, 40, xb)
             ms, it, nf = g.last_jcg_timing()
             best = min(best, ms / it)
-        bpu = 88 if cfg in ("c3", "c5", "c3_128") else 64
+        bpu = 80 if cfg in ("c3", "c5", "c3_128") else 64
         print(json.dumps(dict(lib=os.path.basename(path), cfg=cfg, zc=zc, ms_per_iter=round(best, 5),
-                              frac=round(bpu * nf / (best / 1e3) / 1e9 / 6538.9, 4))), flush=True)
+                              frac=round(bpu * nf / (best / 1e3) / 1e9 / 6553.6, 4))), flush=True)
 
 
 if __name__ == "__main__":
