@@ -132,7 +132,9 @@ typedef enum {
   ECMG_OPT_KERNEL = 4,       /* constant-coefficient JCG kernels: 1 (default) TMA-fed smem ring,
                                 0 register-prefetch loads (ablation) */
   ECMG_OPT_GRAPH = 5,        /* tolerance-stopped JCG loop: 1 (default) one CUDA graph per level with a
-                                device-set conditional WHILE node; 0 host loop with batched readbacks */
+                                device-set conditional WHILE node (z-slab split levels too: the allreduces
+                                and halo exchanges are captured into the WHILE body; if capture fails the
+                                slab driver falls back to the host loop); 0 host loop with batched readbacks */
   ECMG_OPT_PERSISTENT = 7,   /* levels with at most this many free unknowns (and at most 4 bricks of
                                 8x8x4 nodes per resident CTA) run the whole JCG solve in one cooperative
                                 launch with the nodes' values in registers, both operators (default
