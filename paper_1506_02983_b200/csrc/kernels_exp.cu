@@ -313,13 +313,18 @@ __global__ void __launch_bounds__(FNTH, EXP_FUSED_MINB) k_exp_fused(const LevelG
     }
   };
   double r1[NQ], r0 = 0.0;
-  auto fetch = [&](int bz) {
-    const double* b2 = u2t + 2LL * bz * pl2;
+  // the next layer's first u_2h / u_4h planes, advanced by one 4h layer per fetch (loop-carried: the per-thread
+  // offsets above are 32-bit, the layer bases uniform)
+  const double* b2 = u2t + 2LL * bzs * pl2;
+  const double* b4 = u4t + (long long)bzs * pl4;
+  auto fetch = [&]() {
 #pragma unroll
     for (int q = 0; q < NQ; ++q) r1[q] = so1[q] >= 0 ? __ldg(b2 + so1[q]) : 0.0;
-    r0 = so0 >= 0 ? __ldg(u4t + (long long)bz * pl4 + so0) : 0.0;
+    r0 = so0 >= 0 ? __ldg(b4 + so0) : 0.0;
+    b2 += 2 * pl2;
+    b4 += pl4;
   };
-  if (bzs < bze) fetch(bzs);
+  if (bzs < bze) fetch();
   for (int bz = bzs; bz < bze; ++bz) {
     const int fz0 = 4 * bz, nfz = (bz == n4z - 1) ? 5 : 4;
     const int pz0 = max(fz0, F0), pz1 = min(fz0 + nfz, F1);   // fine planes of this layer to write
@@ -328,7 +333,7 @@ __global__ void __launch_bounds__(FNTH, EXP_FUSED_MINB) k_exp_fused(const LevelG
     for (int q = 0; q < NQ; ++q)
       if (tid + q * FNTH < N1) U1s[tid + q * FNTH] = r1[q];
     if (tid < N0) U0s[tid] = r0;
-    if (bz + 1 < bze) fetch(bz + 1);   // next layer's loads in flight during this layer's work
+    if (bz + 1 < bze) fetch();   // next layer's loads in flight during this layer's work
     __syncthreads();
     if (pz0 >= pz1) continue;
     // the 2h-node values
@@ -540,7 +545,8 @@ cudaError_t launch_exp_finite(const LevelGeom& gf, const Problem& pb, const doub
   if (fused) {
     const int nl = bz1 - bz0 + 1;
     const int tiles = ((gf.n[0] / 4 + XB - 1) / XB) * ((gf.n[1] / 4 + YB - 1) / YB);
-    const int lchunk = std::max(1, std::min(8, tiles * nl / 2000));   // >= ~2000 CTAs where the level allows
+    // >= ~2000 CTAs where the level allows (16 or 32 layers per CTA at 512^3: measured no faster)
+    const int lchunk = std::max(1, std::min(8, tiles * nl / 2000));
     dim3 g((gf.n[0] / 4 + XB - 1) / XB, (gf.n[1] / 4 + YB - 1) / YB, (nl + lchunk - 1) / lchunk);
     count_launch();
     if (freebox && variant == 0) k_exp_fused<true, 0><<<g, FNTH, 0, st>>>(gf, u2h, u4h, w, F0, F1, bz0, lchunk);
