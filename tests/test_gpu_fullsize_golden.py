@@ -23,7 +23,7 @@ import synth
 pytestmark = pytest.mark.gpu
 
 if torch.cuda.is_available():
-    from paper_1506_02983_b200 import Grid
+    from paper_1506_02983_b200 import Grid, ecmg
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 CFGS = ["c3", "c4", "c5_256", "c5_512"]
@@ -105,4 +105,35 @@ def test_patch_layered_1024_exact():
     assert e <= 1e-9 * 2.0 and et <= 1e-9 * 2.0
     g.close()
     del u, ut, ue
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("cfg,P", [("c4", 8), ("c5_512", 8)])
+def test_virtual_slabs_vs_oracle(cfg, P):
+    # the z-slab path at the configured sizes: C4 4^3 -> 512^3 and C5's geometry 4^3 -> 512^3 split into P = 8
+    # virtual slabs (levels >= 256^3 split, the smaller ones replicated through the single-GPU path, as NCCL ranks
+    # would run them; the split levels as CUDA graphs with the in-order sum kernel standing in for the
+    # allreduce), against the same oracle goldens (for C5 this is SURVEY.md §8d D.4 (i) and (ii) together: the
+    # oracle cannot hold 1024^3, and one GPU cannot hold the 1024^3 grid twice)
+    G = load(cfg)
+    pid = G["problem_id"]
+    g = Grid(G["coarsest"], G["levels"], pid, params_for(pid))
+    g.set_option(ecmg.OPT_VIRTUAL_SLABS, P)
+    L = G["levels"]
+    u, ut = g.new_vec(L - 1), g.new_vec(L - 1)
+    st, stats = g.run(G["eps"], u, ut)
+    assert st == 0
+    it_g = [s["iterations"] for s in stats[2:]]
+    it_o = [int(r["iterations"]) for r in G["per_level"][2:]]
+    print(f"{cfg} P={P} virtual slabs: iterations gpu {it_g} oracle {it_o}")
+    assert all(abs(a - b) <= 1 for a, b in zip(it_g, it_o)), (it_g, it_o)
+    idx = torch.from_numpy(np.array(G["sample_index"], dtype=np.int64)).cuda()
+    for name, t in (("u", u), ("ut", ut)):
+        ref = G[name]
+        d = float(np.max(np.abs(t[idx].cpu().numpy() - np.array(ref["samples"]))))
+        print(f"{cfg} P={P} {name}: max sampled |d| / ||u||_inf = {d / ref['inf']:.2e}")
+        assert d <= 1e-9 * ref["inf"]
+        assert abs(float(t.abs().max()) - ref["inf"]) <= 1e-9 * ref["inf"]
+    g.close()
+    del u, ut
     torch.cuda.empty_cache()
