@@ -196,7 +196,7 @@ def run_reference(args):
             "vs_baseline": None, "dtype": "f64", "data": f"synthetic (analytic {args.config.upper()} problem; no dataset)",
             "config": {"workload": cfg[4], "levels": cfg[2], "eps": cfg[3]},
             "iterations_per_level": samples[-1]["iterations_per_level"],
-            "cpu_baseline": {k: samples[-1][k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "cpu_baseline": dict({k: samples[-1][k] for k in ("unit", "cores", "kind", "sample")}, value=v),
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "note": f"steps capped to a {REFERENCE_BUDGET_S:.0f} s budget; one step = one full oracle run of the config"}
     print(json.dumps(line), flush=True)
