@@ -728,7 +728,6 @@ int ecmg_create_grid(const ecmg_box* dom, const int coarsest_cells[3], int num_l
   G->L = num_levels;
   // size workspace for the finest level with the largest possible free box (no Dirichlet faces)
   int face_none[6] = {FACE_ROBIN, FACE_ROBIN, FACE_ROBIN, FACE_ROBIN, FACE_ROBIN, FACE_ROBIN};
-  // NCCL ranks keep their work vectors in the slab driver: size the single-GPU workspace minimally
   // NCCL ranks keep the sharded levels' work vectors in the slab driver; the levels below the first
   // sharded one are solved replicated by this grid's single-GPU kernels (ecmg_run), so size for those
   int size_level = num_levels - 1;
