@@ -514,6 +514,13 @@ int enqueue_jcg(ecmg_grid* G, int k, double eps, int max_iter, double* u_out, Pa
   param->max_iter = max_iter;
   param->u_out = u_out;
   ECMG_CUDA(cudaMemcpyAsync(&G->sc->in, param, sizeof(JcgParams), cudaMemcpyHostToDevice, G->stream));
+  if (free_count(g) == 0) {   // nothing to solve
+    ECMG_CUDA(launch_empty_solve(G->sc, G->stream));
+    if ((int)G->lvl_graph.size() != G->L) G->lvl_graph.assign(G->L, 0);
+    G->lvl_graph[k] = 0;
+    ECMG_CUDA(cudaMemcpyAsync(slot, G->sc, sizeof(JcgScalars), cudaMemcpyDeviceToHost, G->stream));
+    return ECMG_OK;
+  }
   if (persistent) {
     ECMG_CUDA(launch_persistent(G, g));
   } else if (use_pers_tma(G, g)) {
@@ -546,6 +553,15 @@ int run_jcg(ecmg_grid* G, int k, double eps, int max_iter, double* u_out, ecmg_s
   G->param_host->max_iter = max_iter;
   G->param_host->u_out = u_out;
   ECMG_CUDA(cudaMemcpyAsync(&G->sc->in, G->param_host, sizeof(JcgParams), cudaMemcpyHostToDevice, G->stream));
+  if (free_count(g) == 0) {   // nothing to solve
+    ECMG_CUDA(cudaEventRecord(G->ev[0], G->stream));
+    ECMG_CUDA(launch_empty_solve(G->sc, G->stream));
+    ECMG_CUDA(cudaEventRecord(G->ev[1], G->stream));
+    ECMG_CUDA(cudaMemcpyAsync(&G->sc_host[0], G->sc, sizeof(JcgScalars), cudaMemcpyDeviceToHost, G->stream));
+    ECMG_CUDA(cudaStreamSynchronize(G->stream));
+    G->last_jcg_ms = 0.0;
+    return fill_stats(G, g, eps, st);
+  }
   if (use_persistent(G, g)) return run_jcg_persistent(G, k, eps, st);
   if (eps > 0.0 && G->use_graph && use_pers_tma(G, g)) {
     ECMG_CUDA(cudaEventRecord(G->ev[0], G->stream));

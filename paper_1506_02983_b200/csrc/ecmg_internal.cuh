@@ -266,6 +266,7 @@ cudaError_t launch_jcg_const_pers(const LevelGeom& g, const ConstStencil& cs, do
 // z-slabs: finalize pass after the allreduce, and the in-order sum of P slabs' partial dots
 // (virtual slabs on one GPU; NCCL's allreduce on real ranks)
 cudaError_t launch_finalize(int mode, const KArgs& a, cudaStream_t st);
+cudaError_t launch_empty_solve(JcgScalars* sc, cudaStream_t st);
 struct SlabScalars { JcgScalars* p[16]; int n; };
 cudaError_t launch_vsum(const SlabScalars& s, cudaStream_t st);
 cudaError_t launch_jcg_persistent(const LevelGeom& g, const ConstStencil& cs, const ElemStencil* es, double* x, double* r,

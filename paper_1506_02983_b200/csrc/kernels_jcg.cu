@@ -216,6 +216,18 @@ cudaError_t launch_finalize(int mode, const KArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// a level without free unknowns (one cell along an all-Dirichlet axis): the solve is empty -- 0 iterations,
+// ||b|| = 0, the residuals 0 -- and its scalars are written as a finished solve would leave them
+__global__ void k_empty_solve(JcgScalars* sc) {
+  sc->rho = 0.0; sc->rr = 0.0; sc->bb = 0.0; sc->rr_true = 0.0; sc->beta = 0.0; sc->alpha = 0.0; sc->sigma = 0.0;
+  sc->iter = 0; sc->max_iter = sc->in.max_iter; sc->thresh = -1.0; sc->status = ST_OK; sc->done = 1; sc->counter = 0;
+}
+cudaError_t launch_empty_solve(JcgScalars* sc, cudaStream_t st) {
+  count_launch();
+  k_empty_solve<<<1, 1, 0, st>>>(sc);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_vsum(const SlabScalars& s, cudaStream_t st) {
   count_launch();
   k_vsum<<<1, 1, 0, st>>>(s);

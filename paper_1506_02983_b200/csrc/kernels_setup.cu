@@ -521,6 +521,8 @@ cudaError_t init_setup_kernel_attributes() {
 
 cudaError_t launch_rhs(const LevelGeom& g, const Problem& pb, const ElemStencil& es, double beta_const, const double* beta,
                        double* b, double* scratch, cudaStream_t st, int ctas_per_sm) {
+  // an empty free box (a level of 1 cell along an all-Dirichlet axis): there is no right-hand side to form
+  if (g.nf[0] <= 0 || g.nf[1] <= 0 || g.zend <= g.zbeg) return cudaSuccess;
   if (prob_separable(pb.id)) {
     const int nmax = std::max(g.n[0], std::max(g.n[1], g.n[2]));
     const int stride = nmax + 1;
@@ -598,6 +600,7 @@ cudaError_t launch_dirichlet_fill(const LevelGeom& g, const Problem& pb, double*
 }
 
 cudaError_t launch_zero_vec(const LevelGeom& g, double* v, cudaStream_t st) {
+  if (g.nf[0] <= 0 || g.nf[1] <= 0 || g.nza <= 0) return cudaSuccess;   // an empty free box
   dim3 grid((g.nf[0] + 127) / 128, g.nf[1], g.nza);
   count_launch();
   k_zero_free<<<grid, 128, 0, st>>>(g, v);

@@ -495,3 +495,22 @@ def test_unfused_textbook_equals_fused(pid, level):
     xo, _ = L.jcg(x0, 0.0, 10)
     fr = ~m
     assert rel(res[1][0][fr], xo[fr]) <= 1e-12
+
+
+@pytest.mark.parametrize("pid,n0,levels,eps", [(o.C1, 1, 5, 1e-8), (o.C3, 1, 5, 1e-10), (o.C2, (8, 4, 1), 4, 1e-10),
+                                               (o.P1, (2, 1, 3), 4, 1e-9)])
+def test_degenerate_hierarchies(pid, n0, levels, eps):
+    # hierarchies that start from an EMPTY level (1 cell per axis: all-Dirichlet leaves no free unknown, a Robin
+    # / Neumann face leaves one plane) and flat / ragged coarsest boxes: every path handles the empty and
+    # one-node systems (0 iterations, no hang) and Alg. 4 matches the oracle level by level
+    g = Grid(n0, levels, pid, params_for(pid))
+    u, ut = g.new_vec(levels - 1), g.new_vec(levels - 1)
+    st, stats = g.run(eps, u, ut)
+    ost, ostats, ou, out = o.ecmg(n0, levels, pid, eps, params=params_for(pid))
+    assert st == 0 and ost == 0
+    it_g = [s["iterations"] for s in stats[2:]]
+    it_o = [int(v) for v in ostats[2:, 0]]
+    assert all(abs(a - b) <= 1 for a, b in zip(it_g, it_o)), (it_g, it_o)
+    assert np.max(np.abs(host(u) - ou)) <= 1e-9 * np.max(np.abs(ou))
+    assert np.max(np.abs(host(ut) - out)) <= 1e-9 * np.max(np.abs(out))
+    g.close()
