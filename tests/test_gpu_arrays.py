@@ -38,6 +38,7 @@ CASES = {
     "neumann_z": ([0, 0, 0, 1, 0, 1], [0.0, 0.0, 0.0, 0.7, 0.0, 0.0], True),
     "dirichlet_beta": ([0] * 6, [0.0] * 6, True),
     "dirichlet_const": ([0] * 6, [0.0] * 6, False),
+    "robin_all": ([1] * 6, [0.5, 1.0, 2.0, 0.25, 1.5, 3.0], True),   # no Dirichlet face at all (still SPD: alpha > 0)
 }
 
 
