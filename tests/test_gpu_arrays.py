@@ -253,3 +253,42 @@ def test_arrays_alpha_q_patch_exact():
     ue = patch_u(*node_points(nf, (0, 0, 0), (1, 1, 1))).reshape(-1)
     assert np.max(np.abs(host(u) - ue)) <= 1e-10 and np.max(np.abs(host(ut) - ue)) <= 1e-10
     g.close()
+
+
+def test_arrays_shifted_box_domain():
+    # a domain that is not the unit cube (shifted and stretched box, anisotropic cells): C3's data sampled on it,
+    # Alg. 4 on the GPU against the oracle on the same box (grid coordinates lo + i h with h = (hi - lo) / n)
+    lo, hi = (-0.5, 0.0, 0.25), (1.5, 0.75, 1.0)
+    n0, levels, eps = (4, 3, 2), 4, 1e-10
+    data = [c3_arrays(tuple(c << k for c in n0), lo, hi) for k in range(levels)]
+    dv = [tuple(dev(a) for a in lv) for lv in data]
+    g = Grid(n0, levels, PROB["ARRAYS"], params=C3_ALPHA, faces=C3_FACES, level_arrays=dv, lo=lo, hi=hi)
+    u, ut = g.new_vec(levels - 1), g.new_vec(levels - 1)
+    st, stats = g.run(eps, u, ut)
+    ost, ostats, ou, out = o.ecmg_arrays(n0, levels, C3_FACES, C3_ALPHA, data, eps, lo=lo, hi=hi)
+    assert st == 0 and ost == 0
+    it_g = [s["iterations"] for s in stats[2:]]
+    it_o = [int(v) for v in ostats[2:, 0]]
+    assert all(abs(a - b) <= 1 for a, b in zip(it_g, it_o)), (it_g, it_o)
+    assert np.max(np.abs(host(u) - ou)) <= 1e-9 * np.max(np.abs(ou))
+    assert np.max(np.abs(host(ut) - out)) <= 1e-9 * np.max(np.abs(out))
+    g.close()
+
+
+@pytest.mark.parametrize("pid", ["C1", "PATCH_TRILINEAR"])
+def test_registry_problem_on_shifted_box(pid):
+    # the registry problems on a shifted box: the GPU evaluates f, g_D at lo + i h exactly as the oracle does
+    lo, hi = (0.25, -1.0, 0.5), (1.25, 0.5, 2.5)
+    n0, levels, eps = (4, 4, 4), 4, 1e-9
+    p = PROB[pid]
+    g = Grid(n0, levels, p, lo=lo, hi=hi)
+    u, ut = g.new_vec(levels - 1), g.new_vec(levels - 1)
+    st, stats = g.run(eps, u, ut)
+    ost, ostats, ou, out = o.ecmg(n0, levels, p, eps, lo=lo, hi=hi)
+    assert st == 0 and ost == 0
+    it_g = [s["iterations"] for s in stats[2:]]
+    it_o = [int(v) for v in ostats[2:, 0]]
+    assert all(abs(a - b) <= 1 for a, b in zip(it_g, it_o)), (it_g, it_o)
+    assert np.max(np.abs(host(u) - ou)) <= 1e-9 * np.max(np.abs(ou))
+    assert np.max(np.abs(host(ut) - out)) <= 1e-9 * np.max(np.abs(out))
+    g.close()
