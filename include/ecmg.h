@@ -112,7 +112,8 @@ typedef struct {
    * fill or the operator (ecmg_run, ecmg_run_fixed, ecmg_solve_level, ecmg_level_rhs, ecmg_apply_operator, the
    * EXP calls) and must stay valid and unchanged until the next ecmg_set_coeffs or ecmg_destroy_grid (DESIGN.md
    * reading R6).
-   * Single GPU only (ECMG_EINVAL with dist / virtual slabs). */
+   * On z-slabs (NCCL ranks or virtual slabs) every rank passes the global-domain arrays in its own device
+   * memory; each rank reads its planes by global index. */
   const double* const* level_arrays;
   int n_level_arrays;
 } ecmg_problem;

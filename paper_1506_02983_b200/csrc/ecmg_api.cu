@@ -220,6 +220,7 @@ SlabCfg slab_cfg(const ecmg_grid* G) {
   c.beta_fly = G->beta_fly;
   c.shard_min = G->shard_min;
   c.use_graph = G->use_graph;
+  c.arrays = G->arrays;
   return c;
 }
 
@@ -886,8 +887,8 @@ int ecmg_set_coeffs(ecmg_grid* G, const ecmg_problem* pr) {
   int need = 0;
   bool arrays_beta = false;
   if (pr->problem_id == ECMG_PROB_ARRAYS) {
-    // caller data per level: single grid only, alpha per face in params[0..5]
-    if (G->slab || G->nranks > 1) return ECMG_EINVAL;
+    // caller data per level, alpha per face in params[0..5] (or at the face Gauss points); on
+    // z-slabs every rank holds the global-domain arrays and reads its planes by global index
     if (!pr->level_arrays || (pr->n_level_arrays != 4 * G->L && pr->n_level_arrays != 5 * G->L) || pr->n_params != 6 ||
         !pr->params)
       return ECMG_EINVAL;
@@ -972,7 +973,7 @@ int ecmg_set_option(ecmg_grid* G, int option, int value) {
     case ECMG_OPT_PDL: if (value != 0 && value != 1) return ECMG_EINVAL; G->pdl = value; clear_graphs(G); break;
     case ECMG_OPT_FUSED_HALO: if (value != 0 && value != 1) return ECMG_EINVAL; G->fused_halo = value; break;
     case ECMG_OPT_VIRTUAL_SLABS: {
-      if (value < 0 || value > 16 || G->nranks > 1 || (value > 1 && G->prob.id == PROB_ARRAYS)) return ECMG_EINVAL;
+      if (value < 0 || value > 16 || G->nranks > 1) return ECMG_EINVAL;
       if (G->slab) { slab_driver_destroy(G->slab); G->slab = nullptr; }
       G->virt_slabs = value > 1 ? value : 0;
       if (G->virt_slabs) {

@@ -155,6 +155,14 @@ namespace {
     if ((call) != ncclSuccess) return ECMG_ENCCL;       \
   } while (0)
 
+// the problem as level k's kernels see it (ECMG_PROB_ARRAYS: with that level's caller arrays)
+Problem level_problem(const SlabCfg& cf, int k) {
+  Problem p = cf.prob;
+  if (p.id == PROB_ARRAYS && (int)cf.arrays.size() == 5 * cf.L)
+    for (int j = 0; j < 5; ++j) p.arr[j] = cf.arrays[5 * k + j];
+  return p;
+}
+
 // ---- communication ---------------------------------------------------------------------------
 int comm_allreduce(SlabDriver* d, cudaStream_t st) {
   if (d->virt) {
@@ -250,9 +258,10 @@ cudaError_t slab_launch(SlabDriver* d, SlabCtx& c, int mode, int k, const KArgs&
   const SlabCfg& cf = d->cfg;
   const LevelGeom& g = c.geom[k];
   if (cf.elem_path) {
-    ElemStencil es = make_elem_stencil(g, cf.prob, cf.precond);
-    if (cf.beta_fly && a.beta) set_beta_fly(es, g, cf.prob, a.beta);
-    return launch_jcg_elem(mode, g, es, cf.prob, a, st);
+    const Problem pk = level_problem(cf, k);
+    ElemStencil es = make_elem_stencil(g, pk, cf.precond);
+    if (cf.beta_fly && a.beta) set_beta_fly(es, g, pk, a.beta);
+    return launch_jcg_elem(mode, g, es, pk, a, st);
   }
   const ConstStencil cs = make_const_stencil(g, 1.0, cf.precond);
   if (cf.kernel_variant == 1 && slab_maps(d, c, k)) {
@@ -294,9 +303,10 @@ KArgs base_args(SlabDriver* d, SlabCtx& c, int k, bool local_only) {
 int setup_slab_level(SlabDriver* d, SlabCtx& c, int k, cudaStream_t st) {
   const SlabCfg& cf = d->cfg;
   const LevelGeom& g = c.geom[k];
-  const ElemStencil es = make_elem_stencil(g, cf.prob, cf.precond);
-  if (cf.elem_path) SL_CUDA(launch_beta(g, cf.prob, betavec(d, c, k), st));
-  SL_CUDA(launch_rhs(g, cf.prob, es, 1.0, cf.elem_path ? betavec(d, c, k) : nullptr, bvec(d, c, k), s1dvec(d, c, k), st));
+  const Problem pk = level_problem(cf, k);
+  const ElemStencil es = make_elem_stencil(g, pk, cf.precond);
+  if (cf.elem_path) SL_CUDA(launch_beta(g, pk, betavec(d, c, k), st));
+  SL_CUDA(launch_rhs(g, pk, es, 1.0, cf.elem_path ? betavec(d, c, k) : nullptr, bvec(d, c, k), s1dvec(d, c, k), st));
   return ECMG_OK;
 }
 
@@ -802,7 +812,7 @@ int slab_run(SlabDriver* d, double eps, ecmg_stats* per_level, double* u_out, bo
       SlabCtx& c = d->s[i];
       const LevelGeom& g = c.geom[k];
       if (k < 2) SL_CUDA(launch_zero_vec(g, c.x, stream));   // DSOLVE: zero free guess (reading A12)
-      else SL_CUDA(launch_exp_finite(g, cf.prob, c.u[k - 1], c.u[k - 2], c.x, cf.exp_variant, c.seeds, 1, stream));
+      else SL_CUDA(launch_exp_finite(g, level_problem(cf, k), c.u[k - 1], c.u[k - 2], c.x, cf.exp_variant, c.seeds, 1, stream));
     }
     SL_CUDA(cudaEventRecord(e2, stream));
     int s = slab_jcg(d, k, k < 2 ? 1e-14 : eps, 10000, &st, stream);
@@ -812,7 +822,7 @@ int slab_run(SlabDriver* d, double eps, ecmg_stats* per_level, double* u_out, bo
     for (int i = 0; i < nloc; ++i) {
       SlabCtx& c = d->s[i];
       SL_CUDA(launch_scatter(c.geom[k], c.x, c.u[k], stream));
-      SL_CUDA(launch_dirichlet_fill(c.geom[k], cf.prob, c.u[k], 0.0, 0, stream));
+      SL_CUDA(launch_dirichlet_fill(c.geom[k], level_problem(cf, k), c.u[k], 0.0, 0, stream));
     }
     if (sh) {
       int r = comm_u_halo(d, k, stream);
@@ -825,7 +835,7 @@ int slab_run(SlabDriver* d, double eps, ecmg_stats* per_level, double* u_out, bo
     SL_CUDA(cudaEventRecord(e3, stream));
     if (k == L - 1 && k >= 2 && ut_out)
       for (int i = 0; i < nloc; ++i)
-        SL_CUDA(launch_exp_true(d->s[i].geom[k], cf.prob, d->s[i].u[k], d->s[i].u[k - 1], d->s[i].ut, stream));
+        SL_CUDA(launch_exp_true(d->s[i].geom[k], level_problem(cf, k), d->s[i].u[k], d->s[i].u[k - 1], d->s[i].ut, stream));
     SL_CUDA(cudaStreamSynchronize(stream));
     float a = 0.f, b = 0.f, c3 = 0.f;
     cudaEventElapsedTime(&a, e0, e1); cudaEventElapsedTime(&b, e1, e2); cudaEventElapsedTime(&c3, e2, e3);
@@ -877,7 +887,7 @@ int slab_solve_level(SlabDriver* d, int k, double eps, int max_iter, double* u, 
   for (int i = 0; i < nloc; ++i) {
     SlabCtx& c = d->s[i];
     SL_CUDA(launch_scatter(c.geom[k], c.x, c.u[k], stream));
-    SL_CUDA(launch_dirichlet_fill(c.geom[k], cf.prob, c.u[k], 0.0, 0, stream));
+    SL_CUDA(launch_dirichlet_fill(c.geom[k], level_problem(cf, k), c.u[k], 0.0, 0, stream));
     const long long z0 = c.geom[k].zlo, z1 = c.geom[k].zhi;
     const long long dst0 = d->virt ? z0 * pl : 0;
     SL_CUDA(cudaMemcpyAsync(u + dst0, c.u[k] + z0 * pl, sizeof(double) * (z1 - z0) * pl, cudaMemcpyDeviceToDevice, stream));

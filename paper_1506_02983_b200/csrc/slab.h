@@ -1,5 +1,6 @@
 // slab.h -- z-slab driver interface (ecmg_slab.cu), used by ecmg_api.cu. Not part of the ABI.
 #pragma once
+#include <vector>
 #include "../../include/ecmg.h"
 #include "ecmg_internal.cuh"
 
@@ -16,6 +17,9 @@ struct SlabCfg {
   int shard_min;    // levels with fewer z cells are replicated (ECMG_OPT_SHARD_MIN)
   int use_graph;    // 1: tolerance-stopped solves of sharded levels run as one CUDA graph per level with a
                     // device-set WHILE node (ECMG_OPT_GRAPH); 0: the host loop with batched readbacks
+  // ECMG_PROB_ARRAYS: the caller's device arrays, 5 per level (beta_e, f_q, g_D, g_R, alpha_q), global-domain
+  // layouts (every slab reads its planes by global index); empty for the registry problems
+  std::vector<const double*> arrays;
 };
 constexpr int kShardMinDefault = 256;
 

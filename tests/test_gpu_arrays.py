@@ -17,7 +17,7 @@ from arrays_data import C3_ALPHA, C3_FACES, c3_arrays
 pytestmark = pytest.mark.gpu
 
 if torch.cuda.is_available():
-    from paper_1506_02983_b200 import Grid, PROB
+    from paper_1506_02983_b200 import Grid, PROB, ecmg
 
 
 def rel(a, b):
@@ -130,7 +130,7 @@ def test_arrays_rejects():
         Grid(4, 3, PROB["ARRAYS"], params=[0.0] * 6, faces=[0] * 6, level_arrays=dv[:2])
 
 
-def test_arrays_setup_ahead_bitwise_and_slabs_rejected():
+def test_arrays_setup_ahead_bitwise():
     from paper_1506_02983_b200 import ecmg
     n0, levels = (5, 3, 4), 4
     data = level_data(n0, levels, True, seed=80)
@@ -143,8 +143,6 @@ def test_arrays_setup_ahead_bitwise_and_slabs_rejected():
         assert st == 0
         outs.append((u, ut))
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
-    # the z-slab driver does not take caller arrays
-    assert ecmg.set_option(g.h, ecmg.OPT_VIRTUAL_SLABS, 2) == ecmg.EINVAL
     g.close()
 
 
@@ -285,6 +283,28 @@ def test_registry_problem_on_shifted_box(pid):
     u, ut = g.new_vec(levels - 1), g.new_vec(levels - 1)
     st, stats = g.run(eps, u, ut)
     ost, ostats, ou, out = o.ecmg(n0, levels, p, eps, lo=lo, hi=hi)
+    assert st == 0 and ost == 0
+    it_g = [s["iterations"] for s in stats[2:]]
+    it_o = [int(v) for v in ostats[2:, 0]]
+    assert all(abs(a - b) <= 1 for a, b in zip(it_g, it_o)), (it_g, it_o)
+    assert np.max(np.abs(host(u) - ou)) <= 1e-9 * np.max(np.abs(ou))
+    assert np.max(np.abs(host(ut) - out)) <= 1e-9 * np.max(np.abs(out))
+    g.close()
+
+
+@pytest.mark.parametrize("case,P", [("robin", 2), ("neumann_z", 4), ("dirichlet_const", 8)])
+def test_arrays_on_virtual_slabs(case, P):
+    # the caller's data on z-slabs: every slab reads its planes of the global-domain arrays (alpha_q included),
+    # P slabs against the oracle; levels with 32 or more z cells split
+    n0, levels, eps = (4, 4, 4), 5, 1e-10
+    faces, alpha, wb = CASES[case]
+    data = [lv + (alpha_q(tuple(c << k for c in n0), 110 + k),) for k, lv in enumerate(level_data(n0, levels, wb, seed=80))]
+    g, _ = make(n0, levels, case, data)
+    g.set_option(ecmg.OPT_VIRTUAL_SLABS, P)
+    g.set_option(ecmg.OPT_SHARD_MIN, 16)
+    u, ut = g.new_vec(levels - 1), g.new_vec(levels - 1)
+    st, stats = g.run(eps, u, ut)
+    ost, ostats, ou, out = o.ecmg_arrays(n0, levels, faces, alpha, data, eps)
     assert st == 0 and ost == 0
     it_g = [s["iterations"] for s in stats[2:]]
     it_o = [int(v) for v in ostats[2:, 0]]
