@@ -42,6 +42,9 @@ sys.path.insert(0, ROOT)
 METRIC = "fine-grid JCG unknown-iters/s (fp64) + ECMG time-to-solution at 512^3"
 UNIT = "unknown-iters/s"
 BYTES_PER_UNKNOWN_ITER = 64   # x 1R+1W, r 2R+1W, p 2R+1W (constant-beta path)
+# constant-beta path with the deferred x update (ECMG_OPT_XDEFER, default on one GPU): per pair of iterations
+# K1 24 B, K2 without x 24 B, K1 24 B, K2 with x and p_{k-1} 48 B = 120 B, i.e. 60 B per unknown and iteration
+BYTES_PER_UNKNOWN_ITER_XDEFER = 60
 
 CONFIGS = {
     # name: (problem id, coarsest, levels, eps, description); C3 / C5 run the element-beta path (80 B/unknown)
@@ -465,6 +468,15 @@ def main():
     ms_p, it_p, _ = grid.last_jcg_timing()
     ms_p = max_over_ranks(ms_p)
     grid.set_option(ecmg.OPT_KERNEL, 1)
+    ablation_xdefer = None
+    if pid not in (3, 5) and ws == 1:   # ablation: x updated in every K2 (64 B/unknown)
+        grid.set_option(ecmg.OPT_XDEFER, 0)
+        xb.copy_(x0)
+        grid.solve_level(fine, 0.0, args.fixed_iters, xb)
+        ms_x, it_x, _ = grid.last_jcg_timing()
+        grid.set_option(ecmg.OPT_XDEFER, 1)
+        ablation_xdefer = {"value": nf_j * it_x / (ms_x / 1e3), "unit": UNIT, "ms_per_iteration": ms_x / max(1, it_x),
+                           "kernel": "x updated in every K2 (ECMG_OPT_XDEFER=0), 64 B/unknown"}
     ablation_unfused = None
     if pid not in (3, 5) and ws == 1:   # ablation: the unfused textbook PCG sequence (9 passes, 144 B/unknown)
         grid.set_option(ecmg.OPT_UNFUSED, 1)
@@ -506,7 +518,8 @@ def main():
     tts_inline = max_over_ranks(ev_s[0].elapsed_time(ev_s[1]))
     grid.set_option(ecmg.OPT_SETUP_AHEAD, 1)
     peak, peak_src = load_peaks()
-    bpu = BYTES_PER_UNKNOWN_ITER_ELEM if pid in (3, 5) else BYTES_PER_UNKNOWN_ITER
+    bpu = (BYTES_PER_UNKNOWN_ITER_ELEM if pid in (3, 5) else
+           BYTES_PER_UNKNOWN_ITER_XDEFER if (ws == 1 and it_j % 2 == 0) else BYTES_PER_UNKNOWN_ITER)
     achieved = bpu * nf_j * it_j / (ms_j / 1e3) / 1e9 / ws   # per GPU
     traffic = None
     try:
@@ -579,6 +592,7 @@ def main():
                                             "ms_per_iteration": ms_p / max(1, it_p),
                                             "kernel": "register-prefetch loads (ECMG_OPT_KERNEL=0)"},
             "jcg_fixed_ablation_beta_fly": ablation_beta,
+            "jcg_fixed_ablation_xdefer": ablation_xdefer,
             "jcg_fixed_ablation_unfused": ablation_unfused,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "kernel": "jcg K1+K2 (one CG iteration)",

@@ -186,6 +186,10 @@ typedef enum {
                                 256); smaller levels are solved replicated on every rank. A split level pays
                                 two allreduces and two finalize launches per iteration (~35-50 us), more
                                 than a whole 128^3 iteration on one GPU (~29 us) */
+  ECMG_OPT_XDEFER = 19,      /* 1 (default): the constant-stencil K2 writes x every second iteration only
+                                (x_{k+2} = x_k + alpha_k p_k + alpha_{k+1} p_{k+1}, the two roundings of two
+                                single updates: bitwise the same iterates; 60 instead of 64 B per unknown and
+                                iteration); 0: x updated in every K2 */
   ECMG_OPT_SETUP_CTAS = 11,  /* tuning: CTAs per SM of the fp64-ALU-bound volume-load kernel when it runs
                                 ahead (0 = one CTA per work item, the full grid) */
   ECMG_OPT_VIRTUAL_SLABS = 6 /* P in 2..16: run the z-slab decomposition with P slabs on this one GPU

@@ -151,6 +151,7 @@ struct ecmg_grid {
   int kernel_variant = 1;   // ECMG_OPT_KERNEL
   int use_graph = 1;        // ECMG_OPT_GRAPH: device-driven JCG loop (CUDA graph, conditional WHILE node)
   int unfused = 0;          // ECMG_OPT_UNFUSED: fixed-count constant-stencil solves by the textbook sequence
+  int xdefer = 1;           // ECMG_OPT_XDEFER: TMA K2 updates x every second iteration (bitwise the same iterates)
   int shard_min = kShardMinDefault;   // ECMG_OPT_SHARD_MIN: z-slabs split only levels with >= this many z cells
   int hybrid = 1;           // ECMG_OPT_SLAB_HYBRID: z-slabs, replicated levels through the single-GPU path
   int fused_halo = 1;       // ECMG_OPT_FUSED_HALO: z-slab halo planes stored by K2 / init into the neighbours
@@ -165,7 +166,7 @@ struct ecmg_grid {
   cudaStream_t cap_stream = nullptr;          // private stream used only for graph capture
   ParamHost* param_host = nullptr;   // pinned
   std::vector<cudaGraphExec_t> graphs;        // per level, lazily built
-  struct Maps { int level = -1; CUtensorMap xh, xi, rh, ri, ph[2], bi; bool ok = false; } maps;
+  struct Maps { int level = -1; CUtensorMap xh, xi, rh, ri, ph[2], pi[2], bi; bool ok = false; } maps;
   double last_jcg_ms = 0.0;
   int last_jcg_iters = 0;
   long long last_free = 0;
@@ -232,6 +233,7 @@ bool ensure_maps(ecmg_grid* G, const LevelGeom& g, int level) {
   M.ok = make_vec_tensor_map(&M.xh, G->x, g, hx, hy) == 0 && make_vec_tensor_map(&M.xi, G->x, g, ix, iy) == 0 &&
          make_vec_tensor_map(&M.rh, G->r, g, hx, hy) == 0 && make_vec_tensor_map(&M.ri, G->r, g, ix, iy) == 0 &&
          make_vec_tensor_map(&M.ph[0], G->p[0], g, hx, hy) == 0 && make_vec_tensor_map(&M.ph[1], G->p[1], g, hx, hy) == 0 &&
+         make_vec_tensor_map(&M.pi[0], G->p[0], g, ix, iy) == 0 && make_vec_tensor_map(&M.pi[1], G->p[1], g, ix, iy) == 0 &&
          make_vec_tensor_map(&M.bi, G->bl[level], g, ix, iy) == 0;
   M.level = level;
   return M.ok;
@@ -249,6 +251,8 @@ const CUtensorMap* int_map(ecmg_grid* G, const double* p) {
   auto& M = G->maps;
   if (p == G->x) return &M.xi;
   if (p == G->r) return &M.ri;
+  if (p == G->p[0]) return &M.pi[0];
+  if (p == G->p[1]) return &M.pi[1];
   if (M.level >= 0 && p == G->bl[M.level]) return &M.bi;
   return nullptr;
 }
@@ -272,8 +276,9 @@ cudaError_t launch_mode(ecmg_grid* G, int mode, const LevelGeom& g, const KArgs&
     const CUtensorMap* h1 = a.h1 ? halo_map(G, a.h1) : h0;
     const CUtensorMap* i0 = a.i0 ? int_map(G, a.i0) : h0;
     const CUtensorMap* i1 = a.i1 ? int_map(G, a.i1) : h0;
-    if (h0 && h1 && i0 && i1) {
-      CUtensorMap m[4] = {*h0, *h1, *i0, *i1};
+    const CUtensorMap* i2 = a.i2 ? int_map(G, a.i2) : h0;
+    if (h0 && h1 && i0 && i1 && i2) {
+      CUtensorMap m[5] = {*h0, *h1, *i0, *i1, *i2};
       return launch_jcg_const_tma(mode, g, cs, a, m, G->stream);
     }
   }
@@ -344,8 +349,14 @@ int fill_stats(ecmg_grid* G, const LevelGeom& g, double eps, ecmg_stats* st) {
 // residual. The init pass and every K2 (and K1 on breakdown) set cond = !done from their last CTA,
 // so the loop stops after exactly the iteration that meets ||r|| <= eps ||f|| (the second K1/K2 of a
 // body run after convergence sees done and returns). No host round trip per iteration.
+// deferred x update (KArgs::xdefer): the constant-stencil TMA K1 / K2 kernels only
+bool use_xdefer(ecmg_grid* G, const LevelGeom& g) {
+  return G->xdefer && !G->elem_path && G->kernel_variant == 1 && ensure_maps(G, g, level_of(G, g));
+}
+
 cudaError_t build_level_graph(ecmg_grid* G, int k, cudaGraphExec_t* out) {
   const LevelGeom& g = G->geom[k];
+  const bool defer = use_xdefer(G, g);
   cudaGraph_t graph = nullptr;
   cudaError_t e = cudaGraphCreate(&graph, 0);
   if (e != cudaSuccess) return e;
@@ -387,6 +398,7 @@ cudaError_t build_level_graph(ecmg_grid* G, int k, cudaGraphExec_t* out) {
     if (e != cudaSuccess) break;
     KArgs a2 = a;
     a2.h0 = G->p[1 - half]; a2.i0 = G->x; a2.i1 = G->elem_path ? G->zv : G->r; a2.o0 = G->x; a2.o1 = G->r; a2.o2 = G->zv;
+    if (defer) { a2.xdefer = 1 + half; a2.i2 = G->p[half]; }   // even k: skip x; odd k: both updates
     e = launch_mode(G, MODE_K2, g, a2);
   }
   e2 = cudaStreamEndCapture(G->cap_stream, &body);
@@ -394,7 +406,8 @@ cudaError_t build_level_graph(ecmg_grid* G, int k, cudaGraphExec_t* out) {
   // true residual after the loop
   e = cudaStreamBeginCaptureToGraph(G->cap_stream, graph, &cond_node, nullptr, 1, cudaStreamCaptureModeThreadLocal);
   if (e != cudaSuccess) return done(e);
-  { KArgs at = a; at.use_cond = 0; at.h0 = G->x; at.i0 = G->bl[k]; e = launch_mode(G, MODE_TRUE, g, at); }
+  if (defer) e = launch_xfix(g, G->x, G->p[1], G->sc, G->stream);   // a skipped update still owed
+  if (e == cudaSuccess) { KArgs at = a; at.use_cond = 0; at.h0 = G->x; at.i0 = G->bl[k]; e = launch_mode(G, MODE_TRUE, g, at); }
   e2 = cudaStreamEndCapture(G->cap_stream, &graph);
   if (e != cudaSuccess || e2 != cudaSuccess) return done(e != cudaSuccess ? e : e2);
   e = cudaGraphInstantiate(out, graph, 0);
@@ -576,6 +589,7 @@ int run_jcg(ecmg_grid* G, int k, double eps, int max_iter, double* u_out, ecmg_s
     return fill_stats(G, g, eps, st);
   }
   if (eps > 0.0 && G->use_graph) return run_jcg_graph(G, k, eps, st);
+  const bool defer = use_xdefer(G, g) && !(eps <= 0.0 && G->unfused);
   // r = b - A x, rho = r.z, rr = r.r, stop test
   {
     KArgs ai = a;
@@ -590,6 +604,7 @@ int run_jcg(ecmg_grid* G, int k, double eps, int max_iter, double* u_out, ecmg_s
     if (e != cudaSuccess) return e;
     KArgs a2 = a;
     a2.h0 = G->p[(it + 1) & 1]; a2.i0 = G->x; a2.i1 = G->elem_path ? G->zv : G->r; a2.o0 = G->x; a2.o1 = G->r; a2.o2 = G->zv;
+    if (defer) { a2.xdefer = 1 + (int)(it & 1); a2.i2 = G->p[it & 1]; }
     e = launch_mode(G, MODE_K2, g, a2);
     ++it;
     return e;
@@ -654,6 +669,7 @@ int run_jcg(ecmg_grid* G, int k, double eps, int max_iter, double* u_out, ecmg_s
       if (++guard > (long long)max_iter + 8) break;   // cannot happen: done is set at max_iter
     }
   }
+  if (defer) ECMG_CUDA(launch_xfix(g, G->x, G->p[1], G->sc, G->stream));   // inside the timed window
   ECMG_CUDA(cudaEventRecord(G->ev[1], G->stream));
   // true residual RRe = ||b - A x|| / ||b||
   {
@@ -967,6 +983,7 @@ int ecmg_set_option(ecmg_grid* G, int option, int value) {
     case ECMG_OPT_PERSISTENT: if (value < 0) return ECMG_EINVAL; G->persistent_max = value; break;
     case ECMG_OPT_PERS_TMA: if (value < 0) return ECMG_EINVAL; G->pers_tma_max = value; break;
     case ECMG_OPT_UNFUSED: if (value != 0 && value != 1) return ECMG_EINVAL; G->unfused = value; break;
+    case ECMG_OPT_XDEFER: if (value != 0 && value != 1) return ECMG_EINVAL; G->xdefer = value; clear_graphs(G); break;
     case ECMG_OPT_SHARD_MIN: if (value < 0) return ECMG_EINVAL; G->shard_min = value; break;
     case ECMG_OPT_SLAB_HYBRID: if (value != 0 && value != 1) return ECMG_EINVAL; G->hybrid = value; break;
     case ECMG_OPT_CTA_SOLVE: if (value < 0) return ECMG_EINVAL; G->cta_max = value; break;

@@ -176,6 +176,7 @@ struct JcgScalars {
   int pad_;
   double loc[3];     // z-slabs: this slab's partial dot products (before the allreduce)
   double glob[3];    // z-slabs: allreduced dot products (input of the finalize pass)
+  double alpha_prev; // alpha of the previous iteration (deferred x update, KArgs::xdefer)
 };
 
 enum KMode { MODE_K1 = 1, MODE_K2 = 2, MODE_INIT = 3, MODE_TRUE = 4, MODE_APPLY = 5 };
@@ -209,6 +210,12 @@ struct KArgs {
   // neighbour rank's buffer over NVLink. nullptr: no fused store (halo by copy / NCCL).
   double* peer_lo;
   double* peer_hi;
+  // deferred solution update (K2 of the TMA kernels): 0 = x += alpha_k p_k every
+  // iteration; 1 = skip (even k: x is neither read nor written); 2 = combine (odd k: x += alpha_{k-1} p_{k-1}
+  // + alpha_k p_k with p_{k-1} = i2, the same two roundings as two single updates, so the iterates are
+  // bitwise those of xdefer = 0)
+  int xdefer;
+  const double* i2;   // K2, xdefer = 2: p_{k-1} (interior box)
 };
 
 // launch kernel<<<grid, block, smem, st>>>(args...), with programmatic dependent launch if pdl
@@ -267,6 +274,7 @@ cudaError_t launch_jcg_const_pers(const LevelGeom& g, const ConstStencil& cs, do
 // (virtual slabs on one GPU; NCCL's allreduce on real ranks)
 cudaError_t launch_finalize(int mode, const KArgs& a, cudaStream_t st);
 cudaError_t launch_empty_solve(JcgScalars* sc, cudaStream_t st);
+cudaError_t launch_xfix(const LevelGeom& g, double* x, const double* p, const JcgScalars* sc, cudaStream_t st);
 struct SlabScalars { JcgScalars* p[16]; int n; };
 cudaError_t launch_vsum(const SlabScalars& s, cudaStream_t st);
 cudaError_t launch_jcg_persistent(const LevelGeom& g, const ConstStencil& cs, const ElemStencil* es, double* x, double* r,

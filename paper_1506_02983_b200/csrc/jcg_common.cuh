@@ -74,7 +74,7 @@ __device__ void finalize(int mode, const KArgs& a, double s0, double s1, double 
         sc->done = 1;
         if (a.use_cond) cudaGraphSetConditional(a.cond, 0u);
       }
-      else sc->alpha = sc->rho / s0;
+      else { sc->alpha_prev = sc->alpha; sc->alpha = sc->rho / s0; }
       break;
     }
     case MODE_K2: {

@@ -14,6 +14,7 @@
 // planes; each plane of the input is read once from HBM (plus a 1-node halo ring, L2 hits from
 // neighbouring CTAs) and staged in shared memory; the 27-point stencil is split into per-plane
 // partial sums kept in registers, so every value is loaded from shared memory a few times only.
+#include <algorithm>
 #include "ecmg_internal.cuh"
 #include "problems.cuh"
 #include "jcg_common.cuh"
@@ -225,6 +226,25 @@ __global__ void k_empty_solve(JcgScalars* sc) {
 cudaError_t launch_empty_solve(JcgScalars* sc, cudaStream_t st) {
   count_launch();
   k_empty_solve<<<1, 1, 0, st>>>(sc);
+  return cudaGetLastError();
+}
+
+// deferred x update (KArgs::xdefer): a solve that stopped after a skipping K2 (iteration count odd) still owes
+// x += alpha_{k} p_{k} with p_k in p; otherwise a no-op. Same rounding as the K2 update it stands in for.
+__global__ void k_xfix(const LevelGeom g, double* __restrict__ x, const double* __restrict__ p, const JcgScalars* sc) {
+  if (!(sc->iter & 1)) return;
+  const double alpha = sc->alpha;
+  const long long nrow = (long long)g.nf[1] * (g.zend - g.zbeg);
+  for (long long row = blockIdx.x * (long long)blockDim.y + threadIdx.y; row < nrow; row += (long long)gridDim.x * blockDim.y) {
+    const long long off = (long long)(g.zbeg + row / g.nf[1]) * g.S + (row % g.nf[1]) * g.P;
+    for (int i = threadIdx.x; i < g.nf[0]; i += blockDim.x) x[off + i] = __fma_rn(alpha, p[off + i], x[off + i]);
+  }
+}
+cudaError_t launch_xfix(const LevelGeom& g, double* x, const double* p, const JcgScalars* sc, cudaStream_t st) {
+  count_launch();
+  const long long nrow = (long long)g.nf[1] * (g.zend - g.zbeg);
+  const int blocks = (int)std::max(1LL, std::min(nrow / 8 + 1, 148LL * 16));
+  k_xfix<<<blocks, dim3(32, 8), 0, st>>>(g, x, p, sc);
   return cudaGetLastError();
 }
 

@@ -60,11 +60,17 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+// interior boxes per stage: K2 x, r (xdefer 0) | r (1) | x, r, p_{k-1} (2); INIT / TRUE b
+template <int MODE, int XD>
+__host__ __device__ constexpr int num_interior() {
+  return MODE == MODE_K2 ? (XD == 1 ? 1 : (XD == 2 ? 3 : 2)) : ((MODE == MODE_INIT || MODE == MODE_TRUE) ? 1 : 0);
+}
+
 // loads of step t (halo plane z0-1+t, interior plane z0-2+t) into stage st
 template <bool kH1, int kNI, int SBYTES>
 __device__ __forceinline__ void issue_stage(unsigned char* smem, uint64_t* full, int st, int t, int z0, int X0, int Y0,
                                             uint32_t tx_bytes, bool first, const CUtensorMap* pH0, const CUtensorMap* pH1,
-                                            const CUtensorMap* pI0, const CUtensorMap* pI1) {
+                                            const CUtensorMap* pI0, const CUtensorMap* pI1, const CUtensorMap* pI2) {
   unsigned char* base = smem + st * SBYTES;
   mbar_expect_tx(&full[st], tx_bytes);
   const int zh = z0 - 1 + t;
@@ -72,6 +78,7 @@ __device__ __forceinline__ void issue_stage(unsigned char* smem, uint64_t* full,
   if (kH1 && !first) tma_load_3d(base + HSTRIDE, pH1, X0 - XO, Y0 - 1, zh, &full[st]);
   if (kNI >= 1) tma_load_3d(base + HSTRIDE * (kH1 ? 2 : 1), pI0, X0, Y0, zh - 1, &full[st]);
   if (kNI >= 2) tma_load_3d(base + HSTRIDE * (kH1 ? 2 : 1) + IBYTES, pI1, X0, Y0, zh - 1, &full[st]);
+  if (kNI >= 3) tma_load_3d(base + HSTRIDE * (kH1 ? 2 : 1) + 2 * IBYTES, pI2, X0, Y0, zh - 1, &full[st]);
 }
 
 // One z-march of the CTA over its (tile, z chunk) in mode MODE: the per-plane TMA pipeline of the kernels
@@ -79,14 +86,16 @@ __device__ __forceinline__ void issue_stage(unsigned char* smem, uint64_t* full,
 // ((gstep + s) / NS) & 1), so that a persistent CTA can run several passes over the same mbarriers.
 // Returns the thread's partial sums in acc0..acc2. The caller has initialised the mbarriers and
 // synchronised the CTA since its previous pass.
-template <int MODE, int NS, int SBYTES>
+// XD: deferred x update of K2 (KArgs::xdefer); alpha0 = alpha_{k-1} for XD = 2
+template <int MODE, int NS, int SBYTES, int XD = 0>
 __device__ __forceinline__ void tma_pass(const LevelGeom& g, const ConstStencil& cs, const KArgs& a, int X0, int Y0, int z0,
                                          int z1, double bcg, bool first, double alpha, double* u_out,
                                          const CUtensorMap* pH0, const CUtensorMap* pH1, const CUtensorMap* pI0,
                                          const CUtensorMap* pI1, unsigned char* smem, uint64_t* full, uint32_t gstep,
-                                         double& acc0, double& acc1, double& acc2) {
+                                         double& acc0, double& acc1, double& acc2, const CUtensorMap* pI2 = nullptr,
+                                         double alpha0 = 0.0) {
   constexpr bool kH1 = (MODE == MODE_K1);
-  constexpr int kNI = (MODE == MODE_K2) ? 2 : ((MODE == MODE_INIT || MODE == MODE_TRUE) ? 1 : 0);
+  constexpr int kNI = num_interior<MODE, XD>();
   const int lane = threadIdx.x, w = threadIdx.y, tid = lane + TX * w;
   const int nfx = g.nf[0], nfy = g.nf[1];
   const long long P = g.P, S = g.S;
@@ -98,7 +107,7 @@ __device__ __forceinline__ void tma_pass(const LevelGeom& g, const ConstStencil&
   if (tid == 0) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic accesses before async-proxy writes
     for (int t = 0; t < NS - 1 && t < nsteps; ++t)
-      issue_stage<kH1, kNI, SBYTES>(smem, full, (gstep + t) % NS, t, z0, X0, Y0, tx_bytes, first, pH0, pH1, pI0, pI1);
+      issue_stage<kH1, kNI, SBYTES>(smem, full, (gstep + t) % NS, t, z0, X0, Y0, tx_bytes, first, pH0, pH1, pI0, pI1, pI2);
   }
 
   // halo ring slot of this thread (transform in place, K1 only): rows y = Y0-1, Y0+32 (x = X0-1 ..
@@ -126,7 +135,7 @@ __device__ __forceinline__ void tma_pass(const LevelGeom& g, const ConstStencil&
     if (tid == 0 && s + NS - 1 < nsteps) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes before async-proxy writes
       const int t = s + NS - 1;                                      // into stage (s-1) % NS
-      issue_stage<kH1, kNI, SBYTES>(smem, full, (gstep + t) % NS, t, z0, X0, Y0, tx_bytes, first, pH0, pH1, pI0, pI1);
+      issue_stage<kH1, kNI, SBYTES>(smem, full, (gstep + t) % NS, t, z0, X0, Y0, tx_bytes, first, pH0, pH1, pI0, pI1, pI2);
     }
     mbar_wait(&full[st], (uint32_t)(((gstep + s) / NS) & 1));
     double* H = reinterpret_cast<double*>(stage_ptr(st));
@@ -169,12 +178,13 @@ __device__ __forceinline__ void tma_pass(const LevelGeom& g, const ConstStencil&
           acc0 = __fma_rn(pp[j], ap, acc0);
           a.o0[off] = pp[j];
         } else if (MODE == MODE_K2) {
-          const double xn = __fma_rn(alpha, pp[j], I0[io]);
-          const double rn = __fma_rn(-alpha, ap, I1[io]);
+          // interior boxes: XD 0 (x, r), 1 (r), 2 (x, r, p_{k-1})
+          const double rn = __fma_rn(-alpha, ap, XD == 1 ? I0[io] : I1[io]);
           const double zz = dinv * rn;
           acc0 = __fma_rn(rn, zz, acc0);
           acc1 = __fma_rn(rn, rn, acc1);
-          a.o0[off] = xn;
+          if (XD == 0) a.o0[off] = __fma_rn(alpha, pp[j], I0[io]);
+          if (XD == 2) a.o0[off] = __fma_rn(alpha, pp[j], __fma_rn(alpha0, I1[TX * TY + io], I0[io]));
           a.o1[off] = rn;
           if (z == g.zbeg && a.peer_lo) a.peer_lo[own_off[j]] = rn;      // fused halo exchange
           if (z == g.zend - 1 && a.peer_hi) a.peer_hi[own_off[j]] = rn;
@@ -202,13 +212,13 @@ __device__ __forceinline__ void tma_pass(const LevelGeom& g, const ConstStencil&
   }
 }
 
-template <int MODE, int NS>
+template <int MODE, int NS, int XD>
 __global__ void __launch_bounds__(NTH, 2)
     k_jcg_const_tma(const LevelGeom g, const ConstStencil cs, const KArgs a, const __grid_constant__ CUtensorMap mH0,
                     const __grid_constant__ CUtensorMap mH1, const __grid_constant__ CUtensorMap mI0,
-                    const __grid_constant__ CUtensorMap mI1) {
+                    const __grid_constant__ CUtensorMap mI1, const __grid_constant__ CUtensorMap mI2) {
   constexpr bool kH1 = (MODE == MODE_K1);
-  constexpr int kNI = (MODE == MODE_K2) ? 2 : ((MODE == MODE_INIT || MODE == MODE_TRUE) ? 1 : 0);
+  constexpr int kNI = num_interior<MODE, XD>();
   constexpr int SBYTES = HSTRIDE * (kH1 ? 2 : 1) + IBYTES * kNI;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[NS];
@@ -226,10 +236,10 @@ __global__ void __launch_bounds__(NTH, 2)
   const int X0 = blockIdx.x * TX, Y0 = blockIdx.y * TY;
   const int z0 = g.zbeg + blockIdx.z * a.zc;
   const int z1 = min(z0 + a.zc, g.zend);
-  double bcg = 0.0, alpha = 0.0;
+  double bcg = 0.0, alpha = 0.0, alpha0 = 0.0;
   bool first = false;
   if (MODE == MODE_K1) { bcg = sc->beta; first = (sc->iter == 0); }
-  if (MODE == MODE_K2) alpha = sc->alpha;
+  if (MODE == MODE_K2) { alpha = sc->alpha; alpha0 = XD == 2 ? sc->alpha_prev : 0.0; }
   double* const u_out = (MODE == MODE_TRUE) ? sc->in.u_out : nullptr;
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) mbar_init(&full[i], 1);
@@ -237,8 +247,9 @@ __global__ void __launch_bounds__(NTH, 2)
   }
   __syncthreads();
   double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
-  tma_pass<MODE, NS, SBYTES>(g, cs, a, X0, Y0, z0, z1, bcg, first, alpha, u_out, &mH0, &mH1, &mI0, &mI1, smem, full, 0u,
-                             acc0, acc1, acc2);
+  // XD = 1 (K2 without x): the one interior box is r (I1)
+  tma_pass<MODE, NS, SBYTES, XD>(g, cs, a, X0, Y0, z0, z1, bcg, first, alpha, u_out, &mH0, &mH1, XD == 1 ? &mI1 : &mI0, &mI1,
+                                 smem, full, 0u, acc0, acc1, acc2, &mI2, alpha0);
   if ((MODE == MODE_K2 || MODE == MODE_INIT) && (a.peer_lo || a.peer_hi)) __threadfence_system();   // peer stores
   if (MODE != MODE_APPLY) reduce_finalize(MODE, a, acc0, acc1, acc2);
 }
@@ -356,46 +367,53 @@ __global__ void __launch_bounds__(NTH, 2)
   }
 }
 
-template <int MODE, int NS>
+template <int MODE, int NS, int XD = 0>
 cudaError_t launch_tma_mode(dim3 grid, dim3 block, const LevelGeom& g, const ConstStencil& cs, const KArgs& a,
                             const CUtensorMap* maps, cudaStream_t st) {
   constexpr bool kH1 = (MODE == MODE_K1);
-  constexpr int kNI = (MODE == MODE_K2) ? 2 : ((MODE == MODE_INIT || MODE == MODE_TRUE) ? 1 : 0);
-  constexpr int SBYTES = HSTRIDE * (kH1 ? 2 : 1) + IBYTES * kNI;
+  constexpr int SBYTES = HSTRIDE * (kH1 ? 2 : 1) + IBYTES * num_interior<MODE, XD>();
   constexpr int SMEM = SBYTES * NS + 128;
   count_launch();
-  return launch_maybe_pdl(k_jcg_const_tma<MODE, NS>, grid, block, SMEM, st, a.pdl, g, cs, a, maps[0], maps[1], maps[2],
-                          maps[3]);
+  return launch_maybe_pdl(k_jcg_const_tma<MODE, NS, XD>, grid, block, SMEM, st, a.pdl, g, cs, a, maps[0], maps[1], maps[2],
+                          maps[3], maps[4]);
 }
 
-template <int MODE, int NS>
+template <int MODE, int NS, int XD = 0>
 cudaError_t set_tma_attr() {
   constexpr bool kH1 = (MODE == MODE_K1);
-  constexpr int kNI = (MODE == MODE_K2) ? 2 : ((MODE == MODE_INIT || MODE == MODE_TRUE) ? 1 : 0);
-  constexpr int SMEM = (HSTRIDE * (kH1 ? 2 : 1) + IBYTES * kNI) * NS + 128;
-  return cudaFuncSetAttribute(k_jcg_const_tma<MODE, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  constexpr int SMEM = (HSTRIDE * (kH1 ? 2 : 1) + IBYTES * num_interior<MODE, XD>()) * NS + 128;
+  return cudaFuncSetAttribute(k_jcg_const_tma<MODE, NS, XD>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
 }
 
 }  // namespace
+
+#ifndef NS_K2_SKIP   // ring depth of the x-less K2 (p halo + r interior per stage, the K1 stage size)
+#define NS_K2_SKIP 4
+#endif
 
 // set every dynamic-smem attribute up front (never inside a stream capture)
 cudaError_t init_tma_kernel_attributes() {
   cudaError_t e = set_tma_attr<MODE_K1, 4>();
   if (e == cudaSuccess) e = set_tma_attr<MODE_K2, 3>();
+  if (e == cudaSuccess) e = set_tma_attr<MODE_K2, NS_K2_SKIP, 1>();
+  if (e == cudaSuccess) e = set_tma_attr<MODE_K2, 3, 2>();
   if (e == cudaSuccess) e = set_tma_attr<MODE_INIT, 4>();
   if (e == cudaSuccess) e = set_tma_attr<MODE_TRUE, 4>();
   if (e == cudaSuccess) e = set_tma_attr<MODE_APPLY, 4>();
   return e;
 }
 
-// maps[0..3] = H0, H1, I0, I1 tensor maps (unused entries may be any valid map)
+// maps[0..4] = H0, H1, I0, I1, I2 tensor maps (unused entries may be any valid map)
 cudaError_t launch_jcg_const_tma(int mode, const LevelGeom& g, const ConstStencil& cs, const KArgs& a,
                                  const CUtensorMap* maps, cudaStream_t st) {
   dim3 block(TX, WARPS);
   dim3 grid((g.nf[0] + TX - 1) / TX, (g.nf[1] + TY - 1) / TY, (g.zend - g.zbeg + a.zc - 1) / a.zc);
   switch (mode) {
     case MODE_K1: return launch_tma_mode<MODE_K1, 4>(grid, block, g, cs, a, maps, st);
-    case MODE_K2: return launch_tma_mode<MODE_K2, 3>(grid, block, g, cs, a, maps, st);
+    case MODE_K2:
+      if (a.xdefer == 1) return launch_tma_mode<MODE_K2, NS_K2_SKIP, 1>(grid, block, g, cs, a, maps, st);
+      if (a.xdefer == 2) return launch_tma_mode<MODE_K2, 3, 2>(grid, block, g, cs, a, maps, st);
+      return launch_tma_mode<MODE_K2, 3>(grid, block, g, cs, a, maps, st);
     case MODE_INIT: return launch_tma_mode<MODE_INIT, 4>(grid, block, g, cs, a, maps, st);
     case MODE_TRUE: return launch_tma_mode<MODE_TRUE, 4>(grid, block, g, cs, a, maps, st);
     case MODE_APPLY: return launch_tma_mode<MODE_APPLY, 4>(grid, block, g, cs, a, maps, st);

@@ -474,6 +474,48 @@ def test_beta_on_the_fly_bitwise(pid, eps):
         assert np.array_equal(res[0][k], res[1][k])
 
 
+@pytest.mark.parametrize("mode", ["fixed1", "fixed2", "fixed7", "host", "graph", "run"])
+def test_xdefer_bitwise(mode):
+    # ECMG_OPT_XDEFER (the constant-stencil K2 writes x every second iteration, x_{k+2} = x_k + alpha_k p_k +
+    # alpha_{k+1} p_{k+1} with the roundings of two single updates): every iterate is bitwise that of the
+    # per-iteration update -- fixed counts ending on a skipped update (1, 7: the owed update is applied after the
+    # loop) or a combined one (2), the host-driven and the graph-driven tolerance loops on the TMA K1 / K2, and a
+    # whole ECMG run (C2 to 128^3, the default solve selection)
+    level = 4
+    n = (64,) * 3
+    L = o.Level(n, o.C2)
+    m, _ = L.dirichlet()
+    x0 = np.where(~m, synth.random_nodal(14, n), 0.0)
+    res = []
+    for xd in (0, 1):
+        if mode == "run":
+            g = Grid(4, 6, PROB["C2"])
+            g.set_option(ecmg.OPT_XDEFER, xd)
+            u, ut = g.new_vec(5), g.new_vec(5)
+            st, stats = g.run(1e-10, u, ut)
+            assert st == 0
+            res.append(([s["iterations"] for s in stats], host(u), host(ut)))
+            continue
+        g = Grid(4, level + 1, PROB["C2"])
+        g.set_option(ecmg.OPT_XDEFER, xd)
+        for opt in (ecmg.OPT_PERSISTENT, ecmg.OPT_PERS_TMA, ecmg.OPT_CTA_SOLVE):
+            g.set_option(opt, 0)
+        if mode == "host":
+            g.set_option(ecmg.OPT_GRAPH, 0)
+        u = dev(x0)
+        if mode.startswith("fixed"):
+            k = int(mode[5:])
+            st, stats = g.solve_level(level, 0.0, k, u)
+            assert stats["iterations"] == k
+        else:
+            st, stats = g.solve_level(level, 1e-10, 10000, u)
+        assert st == 0
+        res.append(([stats["iterations"]], host(u), np.array([stats["rel_res_true"]])))
+    assert res[0][0] == res[1][0]
+    for k in range(1, len(res[0])):
+        assert np.array_equal(res[0][k], res[1][k])
+
+
 @pytest.mark.parametrize("pid,level", [(o.C2, 4), (o.C4, 5), (o.C1, 3)])
 def test_unfused_textbook_equals_fused(pid, level):
     # ECMG_OPT_UNFUSED (the ablation of the fused K1 / K2 kernels): the textbook PCG sequence as separate
