@@ -518,9 +518,13 @@ def main():
     tts_inline = max_over_ranks(ev_s[0].elapsed_time(ev_s[1]))
     grid.set_option(ecmg.OPT_SETUP_AHEAD, 1)
     peak, peak_src = load_peaks()
-    bpu = (BYTES_PER_UNKNOWN_ITER_ELEM if pid in (3, 5) else
-           BYTES_PER_UNKNOWN_ITER_XDEFER if (ws == 1 and it_j % 2 == 0) else BYTES_PER_UNKNOWN_ITER)
+    # achieved = the ALGORITHMIC bytes of SURVEY.md §8d D.3 (64 B constant path, 80 B element path) per second. With
+    # the deferred x update the constant path moves fewer (60 B, confirmed by ncu: `traffic`): `moved` reports
+    # the bandwidth at the bytes the kernels really move, so that no figure hides behind the other
+    bpu = BYTES_PER_UNKNOWN_ITER_ELEM if pid in (3, 5) else BYTES_PER_UNKNOWN_ITER
+    bpu_moved = BYTES_PER_UNKNOWN_ITER_XDEFER if (pid not in (3, 5) and ws == 1 and it_j % 2 == 0) else bpu
     achieved = bpu * nf_j * it_j / (ms_j / 1e3) / 1e9 / ws   # per GPU
+    moved = bpu_moved * nf_j * it_j / (ms_j / 1e3) / 1e9 / ws
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "jcg_traffic.json")) as f:
@@ -597,6 +601,9 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "kernel": "jcg K1+K2 (one CG iteration)",
                          "bytes_per_unit": bpu, "peak_source": peak_src,
+                         "moved": {"bytes_per_unit": bpu_moved, "achieved": moved, "frac": moved / peak,
+                                   "note": "bytes the kernels move per unknown and iteration (deferred x update: "
+                                           "60 B on the constant path); `traffic` is the ncu DRAM figure"},
                          "per": "GPU (average over ranks)",
                          # also against BASELINE's "about 8 TB/s" (target >= 0.70 of it)
                          "frac_nominal_8tbs": achieved / 8000.0},

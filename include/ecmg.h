@@ -186,10 +186,19 @@ typedef enum {
                                 256); smaller levels are solved replicated on every rank. A split level pays
                                 two allreduces and two finalize launches per iteration (~35-50 us), more
                                 than a whole 128^3 iteration on one GPU (~29 us) */
-  ECMG_OPT_XDEFER = 19,      /* 1 (default): the constant-stencil K2 writes x every second iteration only
-                                (x_{k+2} = x_k + alpha_k p_k + alpha_{k+1} p_{k+1}, the two roundings of two
+  ECMG_OPT_XDEFER = 19,      /* 1 (default): the launched constant-stencil TMA K2 writes x every second iteration
+                                only (x_{k+2} = x_k + alpha_k p_k + alpha_{k+1} p_{k+1}, the two roundings of two
                                 single updates: bitwise the same iterates; 60 instead of 64 B per unknown and
-                                iteration); 0: x updated in every K2 */
+                                iteration); 2: also the launched element-operator K2 (beta from the array,
+                                per-face alpha; 76 instead of 80 B -- bitwise too, but measured slower: those
+                                kernels are issue bound, C3 256^3 0.256 -> 0.261-0.285 ms, C5 1024^3 16.0-16.5 ->
+                                16.5-16.7 ms per iteration; ablation); 0: x updated in every K2 */
+  ECMG_OPT_RHS_SYM = 20,     /* C4 (f a function of r only) on a level that is a cube in n, h, lo and free box: the
+                                volume load is invariant under permutations of the node indices, so about a
+                                third of the 31^3-node tiles is evaluated and the others are written as
+                                permuted copies (k_rhs_c4_sym; equal to the plain kernel up to rounding
+                                order). Value = the smallest free-box extent that uses it (default 248, i.e.
+                                256^3 and larger); 0: never (ablation) */
   ECMG_OPT_SETUP_CTAS = 11,  /* tuning: CTAs per SM of the fp64-ALU-bound volume-load kernel when it runs
                                 ahead (0 = one CTA per work item, the full grid) */
   ECMG_OPT_VIRTUAL_SLABS = 6 /* P in 2..16: run the z-slab decomposition with P slabs on this one GPU

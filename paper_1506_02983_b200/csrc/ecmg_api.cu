@@ -132,6 +132,7 @@ struct ecmg_grid {
   int beta_fly = 0;                // ECMG_OPT_BETA_FLY: element kernels form analytic beta from axis tables (measured:
                                    // 16 B/unknown less traffic but no faster -- the element kernels are latency bound)
   int exp_fused = 1;               // ECMG_OPT_EXP_KERNEL: 1 fused one-pass EXP_finite, 0 seeds + interpolation passes
+  int rhs_sym_min = 248;           // ECMG_OPT_RHS_SYM: smallest free-box extent for the permutation-symmetric C4 load
   int setup_ctas = 0;              // ECMG_OPT_SETUP_CTAS: CTAs per SM of the ALU-bound RHS kernel when run ahead
   cudaStream_t hi_stream = nullptr, lo_stream = nullptr;   // ecmg_run: solves (high) / level setup (low priority)
   cudaStream_t lo2_stream = nullptr;                        // the finest level's setup (starts at once, beside lo_stream)
@@ -300,7 +301,7 @@ int setup_level_on(ecmg_grid* G, int k, cudaStream_t st, int ctas_per_sm = 0) {
   const Problem pk = level_prob(G, k);
   const ElemStencil es = make_elem_stencil(g, pk, G->precond);
   if (G->elem_path) ECMG_CUDA(launch_beta(g, pk, G->betal[k], st));
-  ECMG_CUDA(launch_rhs(g, pk, es, 1.0, G->elem_path ? G->betal[k] : nullptr, G->bl[k], G->s1d[k], st, ctas_per_sm));
+  ECMG_CUDA(launch_rhs(g, pk, es, 1.0, G->elem_path ? G->betal[k] : nullptr, G->bl[k], G->s1d[k], st, ctas_per_sm, G->rhs_sym_min));
   G->setup_ok[k] = 1;
   return ECMG_OK;
 }
@@ -349,9 +350,17 @@ int fill_stats(ecmg_grid* G, const LevelGeom& g, double eps, ecmg_stats* st) {
 // residual. The init pass and every K2 (and K1 on breakdown) set cond = !done from their last CTA,
 // so the loop stops after exactly the iteration that meets ||r|| <= eps ||f|| (the second K1/K2 of a
 // body run after convergence sees done and returns). No host round trip per iteration.
-// deferred x update (KArgs::xdefer): the constant-stencil TMA K1 / K2 kernels only
+// deferred x update (KArgs::xdefer): the launched TMA K1 / K2 kernels -- the constant
+// stencil, and the element operator with beta from the array and per-face alpha (the conditions under which
+// launch_jcg_elem has the deferred-x K2 variants; they must agree, the host owes the update k_xfix applies)
 bool use_xdefer(ecmg_grid* G, const LevelGeom& g) {
-  return G->xdefer && !G->elem_path && G->kernel_variant == 1 && ensure_maps(G, g, level_of(G, g));
+  if (!G->xdefer) return false;
+  if (G->elem_path) {
+    const int k = level_of(G, g);
+    // (value 2 only: measured slower there -- the element kernels are issue bound, not HBM bound)
+    return G->xdefer == 2 && k >= 0 && !G->beta_fly && !(G->prob.id == PROB_ARRAYS && level_prob(G, k).arr[4]);
+  }
+  return G->kernel_variant == 1 && ensure_maps(G, g, level_of(G, g));
 }
 
 cudaError_t build_level_graph(ecmg_grid* G, int k, cudaGraphExec_t* out) {
@@ -976,6 +985,7 @@ int ecmg_set_option(ecmg_grid* G, int option, int value) {
     case ECMG_OPT_SETUP_AHEAD: if (value != 0 && value != 1) return ECMG_EINVAL; G->setup_ahead = value; break;
     case ECMG_OPT_BETA_FLY: if (value != 0 && value != 1) return ECMG_EINVAL; G->beta_fly = value; clear_graphs(G); break;
     case ECMG_OPT_EXP_KERNEL: if (value != 0 && value != 1) return ECMG_EINVAL; G->exp_fused = value; break;
+    case ECMG_OPT_RHS_SYM: if (value < 0) return ECMG_EINVAL; G->rhs_sym_min = value; invalidate_setup(G); break;
     case ECMG_OPT_SETUP_CTAS: if (value < 0) return ECMG_EINVAL; G->setup_ctas = value; break;
     case ECMG_OPT_ZCHUNK: if (value < 0) return ECMG_EINVAL; G->zchunk = value; clear_graphs(G); break;
     case ECMG_OPT_KERNEL: if (value != 0 && value != 1) return ECMG_EINVAL; G->kernel_variant = value; clear_graphs(G); break;
@@ -983,7 +993,7 @@ int ecmg_set_option(ecmg_grid* G, int option, int value) {
     case ECMG_OPT_PERSISTENT: if (value < 0) return ECMG_EINVAL; G->persistent_max = value; break;
     case ECMG_OPT_PERS_TMA: if (value < 0) return ECMG_EINVAL; G->pers_tma_max = value; break;
     case ECMG_OPT_UNFUSED: if (value != 0 && value != 1) return ECMG_EINVAL; G->unfused = value; break;
-    case ECMG_OPT_XDEFER: if (value != 0 && value != 1) return ECMG_EINVAL; G->xdefer = value; clear_graphs(G); break;
+    case ECMG_OPT_XDEFER: if (value < 0 || value > 2) return ECMG_EINVAL; G->xdefer = value; clear_graphs(G); break;
     case ECMG_OPT_SHARD_MIN: if (value < 0) return ECMG_EINVAL; G->shard_min = value; break;
     case ECMG_OPT_SLAB_HYBRID: if (value != 0 && value != 1) return ECMG_EINVAL; G->hybrid = value; break;
     case ECMG_OPT_CTA_SOLVE: if (value < 0) return ECMG_EINVAL; G->cta_max = value; break;

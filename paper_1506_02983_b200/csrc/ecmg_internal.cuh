@@ -303,7 +303,8 @@ int tma_int_box_y();
 
 cudaError_t launch_beta(const LevelGeom& g, const Problem& pb, double* beta, cudaStream_t st);
 cudaError_t launch_rhs(const LevelGeom& g, const Problem& pb, const ElemStencil& es, double beta_const,
-                       const double* beta, double* b, double* scratch, cudaStream_t st, int ctas_per_sm = 0);
+                       const double* beta, double* b, double* scratch, cudaStream_t st, int ctas_per_sm = 0,
+                       int sym_min = 248);
 cudaError_t launch_gather(const LevelGeom& g, const double* u, double* x, cudaStream_t st);
 cudaError_t launch_scatter(const LevelGeom& g, const double* x, double* u, cudaStream_t st);
 cudaError_t launch_dirichlet_fill(const LevelGeom& g, const Problem& pb, double* u, double value_if_none,

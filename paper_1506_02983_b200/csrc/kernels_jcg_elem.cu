@@ -88,22 +88,24 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
-template <int MODE>
+// XD: deferred x update of K2 (KArgs::xdefer): interior boxes x, z (0) | z (1: x skipped) | x, z, p_{k-1} (2)
+template <int MODE, int XD = 0>
 struct ElemCfg {
   static constexpr bool kH1 = (MODE == MODE_K1);
-  static constexpr int kNI = (MODE == MODE_K2) ? 2 : ((MODE == MODE_INIT || MODE == MODE_TRUE) ? 1 : 0);
+  static constexpr int kNI = (MODE == MODE_K2) ? (XD == 1 ? 1 : (XD == 2 ? 3 : 2)) : ((MODE == MODE_INIT || MODE == MODE_TRUE) ? 1 : 0);
   static constexpr int OFF_E = HSTRIDE * (kH1 ? 2 : 1);
   static constexpr int OFF_I = OFF_E + ESTRIDE;
   static constexpr int SBYTES = OFF_I + IBYTES * kNI;
 };
 
 // loads of step t: node plane zh = z0-1+t (halo boxes), element layer (zh-1, zh), interior plane zh-1
-template <int MODE, int SB, int BF>
+template <int MODE, int SB, int BF, int XD = 0>
 __device__ __forceinline__ void issue_elem_stage(unsigned char* smem, uint64_t* full, int st, int t, int z0, int X0,
                                                  int Y0, int ey0, int ez_base, uint32_t tx_bytes, bool first,
                                                  const CUtensorMap* pH0, const CUtensorMap* pH1, const CUtensorMap* pE,
-                                                 const CUtensorMap* pI0, const CUtensorMap* pI1) {
-  using C = ElemCfg<MODE>;
+                                                 const CUtensorMap* pI0, const CUtensorMap* pI1,
+                                                 const CUtensorMap* pI2 = nullptr) {
+  using C = ElemCfg<MODE, XD>;
   unsigned char* base = smem + st * SB;
   mbar_expect_tx(&full[st], tx_bytes);
   const int zh = z0 - 1 + t;
@@ -112,6 +114,7 @@ __device__ __forceinline__ void issue_elem_stage(unsigned char* smem, uint64_t* 
   if (BF == 0) tma_load_3d(base + C::OFF_E, pE, X0, ey0, ez_base + zh, &full[st]);   // else: beta on the fly
   if (C::kNI >= 1) tma_load_3d(base + C::OFF_I, pI0, X0, Y0, zh - 1, &full[st]);
   if (C::kNI >= 2) tma_load_3d(base + C::OFF_I + IBYTES, pI1, X0, Y0, zh - 1, &full[st]);
+  if (C::kNI >= 3) tma_load_3d(base + C::OFF_I + 2 * IBYTES, pI2, X0, Y0, zh - 1, &full[st]);
 }
 
 // One z-march of the CTA over its (tile, z chunk) in mode MODE (the body of k_jcg_elem_tma): the stage
@@ -121,13 +124,16 @@ __device__ __forceinline__ void issue_elem_stage(unsigned char* smem, uint64_t* 
 // BFA: 0 = beta from the array (TMA box per layer); 1 = on the fly, product kind (C3); 2 = on the fly,
 // bit-mask kinds (beta = 1, layers, C5 boxes) -- see beta_combine; 3 = beta from the array and the Robin alpha
 // at the face Gauss points (ARRAYS alpha_q, es.aq): the only instantiations that carry that branch
-template <int MODE, int NS, bool CUBE, int SB, int BFA>
+// XD: deferred x update of K2 (KArgs::xdefer): 1 = x untouched (the one interior box, pI0, is z); 2 = both pending
+// updates, x <- fma(alpha, p_k, fma(alpha0, p_{k-1}, x)) with p_{k-1} in the third interior box pI2
+template <int MODE, int NS, bool CUBE, int SB, int BFA, int XD = 0>
 __device__ __forceinline__ void elem_pass(const LevelGeom& g, const ElemStencil& es, const KArgs& a, int X0, int Y0, int z0,
                                           int z1, double bcg_eff, bool first, double alpha, double* u_out,
                                           const CUtensorMap* pH0, const CUtensorMap* pH1, const CUtensorMap* pE,
                                           const CUtensorMap* pI0, const CUtensorMap* pI1, unsigned char* smem, uint64_t* full,
-                                          const uint32_t G, double& acc0, double& acc1, double& acc2) {
-  using C = ElemCfg<MODE>;
+                                          const uint32_t G, double& acc0, double& acc1, double& acc2,
+                                          const CUtensorMap* pI2 = nullptr, double alpha0 = 0.0) {
+  using C = ElemCfg<MODE, XD>;
   constexpr int BF = BFA == 3 ? 0 : BFA;   // how beta arrives
   constexpr bool AQ = BFA == 3;            // alpha at the face Gauss points
   const int lane = threadIdx.x, w = threadIdx.y, tid = lane + TX * w;
@@ -153,8 +159,8 @@ __device__ __forceinline__ void elem_pass(const LevelGeom& g, const ElemStencil&
   const int ey0 = g.flo[1] + Y0 + 1;               // beta-array row of the element below node row Y0
   if (tid == 0) {
     for (int t = 0; t < NS - 1 && t < nsteps; ++t)
-      issue_elem_stage<MODE, SB, BF>(smem, full, (G + t) % NS, t, z0, X0, Y0, ey0, ez_base, tx_bytes, first, pH0, pH1, pE, pI0,
-                             pI1);
+      issue_elem_stage<MODE, SB, BF, XD>(smem, full, (G + t) % NS, t, z0, X0, Y0, ey0, ez_base, tx_bytes, first, pH0, pH1, pE, pI0,
+                             pI1, pI2);
   }
 
   bool own_ok[RY];
@@ -216,8 +222,8 @@ __device__ __forceinline__ void elem_pass(const LevelGeom& g, const ElemStencil&
     if (tid == 0 && s + NS - 1 < nsteps) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       const int t = s + NS - 1;
-      issue_elem_stage<MODE, SB, BF>(smem, full, (G + t) % NS, t, z0, X0, Y0, ey0, ez_base, tx_bytes, first, pH0, pH1, pE,
-                             pI0, pI1);
+      issue_elem_stage<MODE, SB, BF, XD>(smem, full, (G + t) % NS, t, z0, X0, Y0, ey0, ez_base, tx_bytes, first, pH0, pH1, pE,
+                             pI0, pI1, pI2);
     }
     mbar_wait(&full[st], (gs / NS) & 1u);
     unsigned char* stage = smem + st * SB;
@@ -402,14 +408,15 @@ __device__ __forceinline__ void elem_pass(const LevelGeom& g, const ElemStencil&
           a.o0[off] = pc;
         } else if (MODE == MODE_K2) {
           const double dinv = es.precond ? (diag > 0.0 ? __drcp_rn(diag) : 0.0) : 1.0;
-          const double xn = __fma_rn(alpha, pc, I0[io]);
+          const double zk = XD == 1 ? I0[io] : I1[io];
           // r_k = D z_k: the residual is not stored on this path, only z = D^-1 r (reading R8)
-          const double rk = es.precond ? diag * I1[io] : I1[io];
+          const double rk = es.precond ? diag * zk : zk;
           const double rn = __fma_rn(-alpha, ap, rk);
           const double zz = dinv * rn;
           acc0 = __fma_rn(rn, zz, acc0);
           acc1 = __fma_rn(rn, rn, acc1);
-          a.o0[off] = xn;
+          if (XD == 0) a.o0[off] = __fma_rn(alpha, pc, I0[io]);
+          if (XD == 2) a.o0[off] = __fma_rn(alpha, pc, __fma_rn(alpha0, I1[TX * TY + io], I0[io]));
           a.o2[off] = zz;
           if (d == g.zbeg && a.peer_lo) a.peer_lo[own_off[j]] = zz;      // fused halo exchange (z)
           if (d == g.zend - 1 && a.peer_hi) a.peer_hi[own_off[j]] = zz;
@@ -452,7 +459,8 @@ __device__ __forceinline__ void elem_pass(const LevelGeom& g, const ElemStencil&
 #undef k7
 }
 
-template <int MODE, int NS, bool CUBE, int BF>
+// XD != 0 (K2 only): the slot of mH1 (K1's second halo vector, unused by K2) carries the interior map of p_{k-1}
+template <int MODE, int NS, bool CUBE, int BF, int XD = 0>
 __global__ void __launch_bounds__(NTH, ELEM_MINB)
     k_jcg_elem_tma(const LevelGeom g, const ElemStencil es, const KArgs a, const __grid_constant__ CUtensorMap mH0,
                    const __grid_constant__ CUtensorMap mH1, const __grid_constant__ CUtensorMap mE,
@@ -469,10 +477,10 @@ __global__ void __launch_bounds__(NTH, ELEM_MINB)
     if (*(volatile int*)&sc->done) return;
   }
   const int tid = threadIdx.x + TX * threadIdx.y;
-  double bcg = 0.0, alpha = 0.0;
+  double bcg = 0.0, alpha = 0.0, alpha0 = 0.0;
   bool first = false;
   if (MODE == MODE_K1) { bcg = sc->beta; first = (sc->iter == 0); }
-  if (MODE == MODE_K2) alpha = sc->alpha;
+  if (MODE == MODE_K2) { alpha = sc->alpha; alpha0 = XD == 2 ? sc->alpha_prev : 0.0; }
   double* const u_out = (MODE == MODE_TRUE) ? sc->in.u_out : nullptr;
   // iteration 0 of K1 (p = z): the p_old slot is filled from z and beta_cg = 0 (exact for finite z), so
   // the window update is one FMA with no per-element select
@@ -492,8 +500,8 @@ __global__ void __launch_bounds__(NTH, ELEM_MINB)
   const int z0 = g.zbeg + blockIdx.z * a.zc;
   const int z1 = min(z0 + a.zc, g.zend);
   double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
-  elem_pass<MODE, NS, CUBE, ElemCfg<MODE>::SBYTES, BF>(g, es, a, X0, Y0, z0, z1, bcg_eff, first, alpha, u_out, &mH0, pH1, &mE, &mI0, &mI1, smem, full,
-                            0u, acc0, acc1, acc2);
+  elem_pass<MODE, NS, CUBE, ElemCfg<MODE, XD>::SBYTES, BF, XD>(g, es, a, X0, Y0, z0, z1, bcg_eff, first, alpha, u_out, &mH0, pH1, &mE, &mI0, &mI1, smem, full,
+                            0u, acc0, acc1, acc2, &mH1, alpha0);
   if ((MODE == MODE_K2 || MODE == MODE_INIT) && (a.peer_lo || a.peer_hi)) __threadfence_system();   // peer stores
   if (MODE != MODE_APPLY) reduce_finalize(MODE, a, acc0, acc1, acc2);
 }
@@ -611,8 +619,8 @@ __global__ void __launch_bounds__(NTH, ELEM_PERS_MINB)
   }
 }
 
-template <int MODE, int NS>
-constexpr int elem_smem() { return ElemCfg<MODE>::SBYTES * NS + 128; }
+template <int MODE, int NS, int XD = 0>
+constexpr int elem_smem() { return ElemCfg<MODE, XD>::SBYTES * NS + 128; }
 
 template <int MODE, int NS>
 cudaError_t set_elem_tma_attr() {
@@ -624,6 +632,23 @@ cudaError_t set_elem_tma_attr() {
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_jcg_elem_tma<MODE, NS, false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_jcg_elem_tma<MODE, NS, true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   return e;
+}
+// the deferred-x K2 variants exist for beta from the array only (BF = 0)
+template <int NS, int XD>
+cudaError_t set_elem_xd_attr() {
+  const int sm = elem_smem<MODE_K2, NS, XD>();
+  cudaError_t e = cudaFuncSetAttribute(k_jcg_elem_tma<MODE_K2, NS, false, 0, XD>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_jcg_elem_tma<MODE_K2, NS, true, 0, XD>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  return e;
+}
+template <int NS, int XD>
+cudaError_t launch_elem_k2_xd(const LevelGeom& g, const ElemStencil& es, const KArgs& a, const CUtensorMap* m, cudaStream_t st) {
+  dim3 grid((g.nf[0] + TX - 1) / TX, (g.nf[1] + TY - 1) / TY, (g.zend - g.zbeg + a.zc - 1) / a.zc);
+  count_launch();
+  const int sm = elem_smem<MODE_K2, NS, XD>();
+  const dim3 blk(TX, WARPS);
+  if (es.cube) return launch_maybe_pdl(k_jcg_elem_tma<MODE_K2, NS, true, 0, XD>, grid, blk, sm, st, a.pdl, g, es, a, m[0], m[1], m[2], m[3], m[4]);
+  return launch_maybe_pdl(k_jcg_elem_tma<MODE_K2, NS, false, 0, XD>, grid, blk, sm, st, a.pdl, g, es, a, m[0], m[1], m[2], m[3], m[4]);
 }
 
 // beta on the fly for cubic cells with the level's tables (ElemStencil::bkind >= 0): 1 = product kind
@@ -716,7 +741,13 @@ bool beta_map(CUtensorMap* m, const double* beta, const LevelGeom& g) {
 #ifndef ELEM_NS_K2
 #define ELEM_NS_K2 5
 #endif
-constexpr int NS_K1 = ELEM_NS_K1, NS_K2 = ELEM_NS_K2, NS_OTHER = 4;
+#ifndef ELEM_NS_K2_SKIP
+#define ELEM_NS_K2_SKIP 6
+#endif
+#ifndef ELEM_NS_K2_BOTH
+#define ELEM_NS_K2_BOTH 4
+#endif
+constexpr int NS_K1 = ELEM_NS_K1, NS_K2 = ELEM_NS_K2, NS_OTHER = 4, NS_K2_SKIP = ELEM_NS_K2_SKIP, NS_K2_BOTH = ELEM_NS_K2_BOTH;
 
 cudaError_t init_elem_kernel_attributes() {
   cudaError_t e = set_elem_tma_attr<MODE_K1, NS_K1>();
@@ -724,6 +755,8 @@ cudaError_t init_elem_kernel_attributes() {
   if (e == cudaSuccess) e = set_elem_tma_attr<MODE_INIT, NS_OTHER>();
   if (e == cudaSuccess) e = set_elem_tma_attr<MODE_TRUE, NS_OTHER>();
   if (e == cudaSuccess) e = set_elem_tma_attr<MODE_APPLY, NS_OTHER>();
+  if (e == cudaSuccess) e = set_elem_xd_attr<NS_K2_SKIP, 1>();
+  if (e == cudaSuccess) e = set_elem_xd_attr<NS_K2_BOTH, 2>();
   return e;
 }
 
@@ -804,7 +837,13 @@ cudaError_t launch_jcg_elem(int mode, const LevelGeom& g, const ElemStencil& es,
   if (ok && mode == MODE_K1) ok = a.h1 && vec_map(&m[1], a.h1, g, HX, HY);
   if (ok && (mode == MODE_K2 || mode == MODE_INIT || mode == MODE_TRUE)) ok = a.i0 && vec_map(&m[3], a.i0, g, TX, TY);
   if (ok && mode == MODE_K2) ok = a.i1 && vec_map(&m[4], a.i1, g, TX, TY);
+  // deferred x update (KArgs::xdefer; beta from the array, no alpha_q): 1 = the one interior box is z;
+  // 2 = x, z and p_{k-1} (its interior map rides in the slot of K1's second halo vector)
+  const bool xd = mode == MODE_K2 && a.xdefer && !es.aq && !(es.cube && beta_fly_variant(es));
+  if (ok && xd && a.xdefer == 1) m[3] = m[4];
+  if (ok && xd && a.xdefer == 2) ok = a.i2 && vec_map(&m[1], a.i2, g, TX, TY);
   if (!ok) return cudaErrorInvalidValue;
+  if (xd) return a.xdefer == 1 ? launch_elem_k2_xd<NS_K2_SKIP, 1>(g, es, a, m, st) : launch_elem_k2_xd<NS_K2_BOTH, 2>(g, es, a, m, st);
   switch (mode) {
     case MODE_K1: return launch_elem_tma_mode<MODE_K1, NS_K1>(g, es, a, m, st);
     case MODE_K2: return launch_elem_tma_mode<MODE_K2, NS_K2>(g, es, a, m, st);

@@ -480,11 +480,12 @@ cudaError_t launch_jcg_const_pers(const LevelGeom& g, const ConstStencil& cs, do
   if (tiles > slots || g.zbeg != 0) return cudaErrorInvalidValue;
   const int nch = (int)std::max(1LL, slots / tiles);          // z chunks per tile
 #ifndef PERS_MIN_ZC
-// at least 4 planes per (tile, chunk) item: the 64^3 level then runs on 64 CTAs instead of 252 and leaves most
-// SMs to the finest level's right-hand side, which the setup-ahead stream runs beside the coarse solves.
-// Measured on C4 (tools/tts_ab.py, 11 interleaved runs): 64^3 solve 0.66 -> 0.89 ms, but the finest level no
-// longer waits 0.43 ms for its setup; TTS 15.20 -> 14.96 ms (with the 256^3 level on this solve, below)
-#define PERS_MIN_ZC 4
+// planes per (tile, chunk) item, at least. Round 2 first ran 4 (the 64^3 level on 64 CTAs instead of 252, 0.66 ->
+// 0.89 ms) to leave SMs to the finest level's ALU-bound right-hand side running ahead beside the coarse solves;
+// with the permutation-symmetric C4 load (k_rhs_c4_sym, 0.69 instead of 1.55 ms) the finest level no longer waits
+// for its setup and 1 measures faster again (tools/tts_ab.py, 2 x 15 runs: TTS 14.63 -> 14.39 ms with 2 z chunks
+// per load tile; profiles/r02/tuning/ab_rhs_sym_variants.log)
+#define PERS_MIN_ZC 1
 #endif
   const int zc = std::max(PERS_MIN_ZC, (nz + nch - 1) / nch);
   const int items = (int)(tiles * ((nz + zc - 1) / zc));

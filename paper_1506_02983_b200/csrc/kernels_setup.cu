@@ -349,6 +349,116 @@ __global__ void __launch_bounds__(C4NTH, RHS_C4_MINB) k_rhs_c4(const LevelGeom g
   }
 }
 
+// C4 volume load on a cubic level (same n, h, lo and free box along the three axes): f depends on r only, so the
+// load is invariant under every permutation of the node indices, F(i, j, k) = F(j, i, k) = F(i, k, j) = ...
+// The free box is cut into cubic tiles of 31^3 nodes, tile index (a, b, c) along (x, y, z), and only about a third
+// of them is evaluated; the others are written as permuted copies by the CTA that evaluates their image:
+//   * a >= b >= c: the tile itself; its x<->y transpose at (b, a, c) if a != b; its y<->z swap at (a, c, b) if
+//     b != c; the image (i, j, k) -> (j, k, i) at (b, c, a) if a != b;
+//   * a < c <= b (x strictly lowest): the tile itself and its y<->z swap at (a, c, b) if b != c.
+// Every tile of the box is written exactly once (the cases are disjoint and cover all index triples), every store
+// is a row segment along x (the transposes go through shared memory), and a value is the same function of its
+// three Gauss abscissa sets whichever image carries it, so the result differs from k_rhs_c4's by rounding order only.
+// 1024 threads = 32 x 32 elements per plane (node tile 31 x 31), the same per-element arithmetic as k_rhs_c4.
+constexpr int C4S = 31, C4SNTH = 1024;
+#ifndef C4S_ZCH
+#define C4S_ZCH 2   // z chunks per tile (a chunk re-evaluates one element layer; shorter CTAs give way sooner to the
+                    // high-priority coarse solves: measured 1 / 2 / 4, profiles/r02/tuning/ab_rhs_sym_variants.log)
+#endif
+constexpr int C4SZ = (C4S + C4S_ZCH - 1) / C4S_ZCH;
+__global__ void __launch_bounds__(C4SNTH, 1) k_rhs_c4_sym(const LevelGeom g, double* __restrict__ b, const RhsC4Consts k) {
+  const int ta = blockIdx.x, tb = blockIdx.y, tc = blockIdx.z / C4S_ZCH, ch = blockIdx.z % C4S_ZCH;
+  const bool canon = ta >= tb && tb >= tc, lowx = ta < tc && tc <= tb;
+  if (!canon && !lowx) return;
+  const bool f_xy = canon && ta != tb;    // (i, j, k) -> (j, i, k) at tile (b, a, c)
+  const bool f_yz = tb != tc;             // (i, j, k) -> (i, k, j) at tile (a, c, b)
+  const bool f_rot = canon && ta != tb;   // (i, j, k) -> (j, k, i) at tile (b, c, a)
+  __shared__ double lo_s[2][2][32][32];   // [layer parity][qz][element row][lane]: y share of the row below
+  __shared__ double tr[32][33];           // in-plane transpose of the node plane
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const double ga = (1.0 - kGauss) / 2.0, gb = (1.0 + kGauss) / 2.0;   // Gauss points at xi = -+1/sqrt(3)
+  const double wA = k.wA, wB = k.wB, dA = k.dA, dB = k.dB;
+  const int X0 = ta * C4S, Y0 = tb * C4S, z0 = tc * C4S + ch * C4SZ, z1 = min(min(z0 + C4SZ, (tc + 1) * C4S), g.nf[2]);
+  if (z0 >= z1) return;
+  const int gex = g.flo[0] + X0 - 1 + lane, gey = g.flo[1] + Y0 - 1 + w;
+  const bool xy_in = gex >= 0 && gex < g.n[0] && gey >= 0 && gey < g.n[1];
+  const double xa = g.lo[0] + (gex + ga) * g.h[0], xb = g.lo[0] + (gex + gb) * g.h[0];
+  const double ya = g.lo[1] + (gey + ga) * g.h[1], yb = g.lo[1] + (gey + gb) * g.h[1];
+  const double sxy[2][2] = {{xa * xa + ya * ya, xb * xb + ya * ya}, {xa * xa + yb * yb, xb * xb + yb * yb}};   // [qy][qx]
+  const int fx = X0 + lane, fy = Y0 + w;
+  const bool node_ok = lane < C4S && w < C4S && fx < g.nf[0] && fy < g.nf[1];
+  // the transposed node of this thread: (i, j) = (w, lane) of the tile
+  const int tx = Y0 + lane, ty = X0 + w;
+  const bool tnode_ok = lane < C4S && w < C4S && tx < g.nf[1] && ty < g.nf[0];
+  double carry = 0.0;
+  int par = 0;
+  for (int fez = z0 - 1; fez < z1; ++fez, par ^= 1) {
+    const int gez = g.flo[2] + fez;
+    double X[2][2];   // [qy][qz]: x-contracted load of node column fx (this element's right node)
+    {
+      double h0[2][2], h1[2][2];
+      if (xy_in && gez >= 0 && gez < g.n[2]) {
+        const double za = g.lo[2] + (gez + ga) * g.h[2], zb = g.lo[2] + (gez + gb) * g.h[2];
+        const double z2[2] = {za * za, zb * zb};
+#pragma unroll
+        for (int qy = 0; qy < 2; ++qy)
+#pragma unroll
+          for (int qz = 0; qz < 2; ++qz) {
+            const double fa = rpow_m14(sxy[qy][0] + z2[qz], k);
+            const double fb = rpow_m14(sxy[qy][1] + z2[qz], k);
+            h0[qy][qz] = __fma_rn(wA, fa, wB * fb);   // to the element's left node
+            h1[qy][qz] = __fma_rn(wB, fa, wA * fb);   // to its right node
+          }
+      } else {
+#pragma unroll
+        for (int qy = 0; qy < 2; ++qy)
+#pragma unroll
+          for (int qz = 0; qz < 2; ++qz) h0[qy][qz] = h1[qy][qz] = 0.0;
+      }
+#pragma unroll
+      for (int qy = 0; qy < 2; ++qy)
+#pragma unroll
+        for (int qz = 0; qz < 2; ++qz) X[qy][qz] = h1[qy][qz] + __shfl_down_sync(0xffffffffu, h0[qy][qz], 1);
+    }
+    double hi[2];
+#pragma unroll
+    for (int qz = 0; qz < 2; ++qz) {
+      lo_s[par][qz][w][lane] = __fma_rn(wA, X[0][qz], wB * X[1][qz]);
+      hi[qz] = __fma_rn(wB, X[0][qz], wA * X[1][qz]);
+    }
+    __syncthreads();   // (also: every thread has read tr of the previous plane)
+    double v = 0.0;
+    if (node_ok) {
+      const double Ya = hi[0] + lo_s[par][0][w + 1][lane];
+      const double Yb = hi[1] + lo_s[par][1][w + 1][lane];
+      v = carry + __fma_rn(dA, Ya, dB * Yb);
+      carry = __fma_rn(dB, Ya, dA * Yb);
+    }
+    if (fez < z0) continue;   // (CTA-uniform) the layer below the tile only feeds carry
+    if (node_ok) {
+      b[(long long)fez * g.S + (long long)fy * g.P + fx] = v;
+      if (f_yz) b[(long long)fy * g.S + (long long)fez * g.P + fx] = v;
+    }
+    if (f_xy) {   // (CTA-uniform)
+      tr[w][lane] = v;
+      __syncthreads();
+      if (tnode_ok) {
+        const double vt = tr[lane][w];
+        b[(long long)fez * g.S + (long long)ty * g.P + tx] = vt;
+        if (f_rot) b[(long long)ty * g.S + (long long)fez * g.P + tx] = vt;
+      }
+    }
+  }
+}
+
+// the symmetric C4 load applies when the level is a cube in every respect the load depends on
+static bool rhs_c4_sym_ok(const LevelGeom& g, int sym_min) {
+  if (sym_min <= 0) return false;
+  for (int d = 1; d < 3; ++d)
+    if (g.n[d] != g.n[0] || g.nf[d] != g.nf[0] || g.flo[d] != g.flo[0] || g.h[d] != g.h[0] || g.lo[d] != g.lo[0]) return false;
+  return g.zoff == 0 && g.zbeg == 0 && g.zend == g.nf[2] && g.nf[0] >= sym_min;
+}
+
 __device__ __forceinline__ int sel3(int d, int a, int b, int c) { return d == 0 ? a : (d == 1 ? b : c); }
 
 // Boundary shell of the free box: Robin load G and lifting -A_fD g_D, added to b.
@@ -520,7 +630,7 @@ cudaError_t init_setup_kernel_attributes() {
 }
 
 cudaError_t launch_rhs(const LevelGeom& g, const Problem& pb, const ElemStencil& es, double beta_const, const double* beta,
-                       double* b, double* scratch, cudaStream_t st, int ctas_per_sm) {
+                       double* b, double* scratch, cudaStream_t st, int ctas_per_sm, int sym_min) {
   // an empty free box (a level of 1 cell along an all-Dirichlet axis): there is no right-hand side to form
   if (g.nf[0] <= 0 || g.nf[1] <= 0 || g.zend <= g.zbeg) return cudaSuccess;
   if (prob_separable(pb.id)) {
@@ -553,15 +663,20 @@ cudaError_t launch_rhs(const LevelGeom& g, const Problem& pb, const ElemStencil&
       k.dA = detJ * k.wA;
       k.dB = detJ * k.wB;
       k.one = 1.0; k.c3 = 0.25;
-      const int items = (int)(grid.x * grid.y * grid.z);
-      int nblk = items;
-      if (ctas_per_sm > 0) {
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        nblk = std::min(items, sms * ctas_per_sm);
+      if (rhs_c4_sym_ok(g, sym_min)) {
+        const int nt = (g.nf[0] + C4S - 1) / C4S;
+        k_rhs_c4_sym<<<dim3(nt, nt, nt * C4S_ZCH), C4SNTH, 0, st>>>(g, b, k);
+      } else {
+        const int items = (int)(grid.x * grid.y * grid.z);
+        int nblk = items;
+        if (ctas_per_sm > 0) {
+          int dev = 0, sms = 148;
+          cudaGetDevice(&dev);
+          cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+          nblk = std::min(items, sms * ctas_per_sm);
+        }
+        k_rhs_c4<<<nblk, C4NTH, 0, st>>>(g, b, zc, k, (int)grid.x, (int)grid.y, items);
       }
-      k_rhs_c4<<<nblk, C4NTH, 0, st>>>(g, b, zc, k, (int)grid.x, (int)grid.y, items);
     }
     else if (pb.id == PROB_ARRAYS) k_rhs_vol<PROB_ARRAYS><<<grid, dim3(32, 8), VSMEM, st>>>(g, pb, b, zc);
     else k_rhs_vol<0><<<grid, dim3(32, 8), VSMEM, st>>>(g, pb, b, zc);

@@ -87,6 +87,42 @@ def test_rhs(pid, n0, level):
         assert abs(nb - nb_exact) <= np.linalg.norm(host(b) - bo) + 1e-13 * nb_exact
 
 
+# the permutation-symmetric C4 load (k_rhs_c4_sym, ECMG_OPT_RHS_SYM) at sizes the oracle assembles whole: free boxes
+# of 63 = 2 x 31 + 1, 79 = 2 x 31 + 17 and 95 = 3 x 31 + 2 nodes (every tile class: a > b > c, ties, x strictly
+# lowest, ragged last tiles), every node against the oracle; the plain kernel on the same level agrees to rounding,
+# and a level that is not a cube in h (stretched box) or in n must take the plain kernel (same bar)
+@pytest.mark.parametrize("n0,level,lo,hi", [(4, 4, (0, 0, 0), (1, 1, 1)), (5, 4, (0, 0, 0), (1, 1, 1)),
+                                            (6, 4, (0.25, 0.25, 0.25), (1.5, 1.5, 1.5)),
+                                            (4, 4, (0, 0, 0), (1, 2, 1)), ((4, 4, 8), 4, (0, 0, 0), (1, 1, 2))])
+def test_rhs_c4_symmetric(n0, level, lo, hi):
+    n0 = (n0,) * 3 if np.isscalar(n0) else n0
+    n = tuple(c << level for c in n0)
+    L = o.Level(n, o.C4, lo=lo, hi=hi)
+    bo, nbo = L.rhs()
+    got = {}
+    for sym_min in (1, 0):
+        g = Grid(n0, level + 1, o.C4, lo=lo, hi=hi)
+        g.set_option(ecmg.OPT_RHS_SYM, sym_min)
+        b = g.new_vec(level)
+        nb = g.level_rhs(level, b)
+        got[sym_min] = host(b).copy()
+        d = rel(got[sym_min], bo)
+        print(f"C4 rhs n={n} lo={lo} hi={hi} RHS_SYM={sym_min}: rel diff vs oracle {d:.3e}")
+        assert d <= 1e-13
+        nb_exact = math.sqrt(math.fsum((bo * bo).tolist()))
+        assert abs(nb - nb_exact) <= np.linalg.norm(got[sym_min] - bo) + 1e-13 * nb_exact
+        g.close()
+    cube = len(set(n)) == 1 and len(set(np.subtract(hi, lo))) == 1 and len(set(lo)) == 1
+    if cube:
+        B = got[1].reshape(n[2] + 1, n[1] + 1, n[0] + 1)
+        # the images are copies: the symmetric kernel's b is exactly symmetric between tiles (spot check: the
+        # x <-> y transpose of every plane agrees to rounding everywhere, bitwise off the diagonal tiles)
+        assert rel(B.transpose(0, 2, 1), B) <= 1e-15
+        assert rel(B.transpose(1, 0, 2), B) <= 1e-15
+    else:
+        assert np.array_equal(got[1], got[0])   # not a cube: the plain kernel ran both times
+
+
 @pytest.mark.parametrize("variant", [0, 1])
 @pytest.mark.parametrize("pid,n0,level", [(o.C1, 4, 3), (o.C3, 4, 4), (o.P1, 4, 3), (o.P2, (10, 4, 5), 2),
                                           (o.C2, 4, 5), (o.P2, (10, 4, 5), 3)])
@@ -475,28 +511,35 @@ def test_beta_on_the_fly_bitwise(pid, eps):
 
 
 @pytest.mark.parametrize("mode", ["fixed1", "fixed2", "fixed7", "host", "graph", "run"])
-def test_xdefer_bitwise(mode):
-    # ECMG_OPT_XDEFER (the constant-stencil K2 writes x every second iteration, x_{k+2} = x_k + alpha_k p_k +
-    # alpha_{k+1} p_{k+1} with the roundings of two single updates): every iterate is bitwise that of the
-    # per-iteration update -- fixed counts ending on a skipped update (1, 7: the owed update is applied after the
-    # loop) or a combined one (2), the host-driven and the graph-driven tolerance loops on the TMA K1 / K2, and a
-    # whole ECMG run (C2 to 128^3, the default solve selection)
-    level = 4
-    n = (64,) * 3
-    L = o.Level(n, o.C2)
+@pytest.mark.parametrize("pname", ["C2", "C3", "C5", "P2"])
+def test_xdefer_bitwise(pname, mode):
+    # ECMG_OPT_XDEFER (the TMA K2 writes x every second iteration, x_{k+2} = x_k + alpha_k p_k + alpha_{k+1} p_{k+1}
+    # with the roundings of two single updates): every iterate is bitwise that of the per-iteration update -- fixed
+    # counts ending on a skipped update (1, 7: the owed update is applied after the loop) or a combined one (2), the
+    # host-driven and the graph-driven tolerance loops on the TMA K1 / K2, and a whole ECMG run (the default solve
+    # selection). C2: constant stencil; C3 (Robin face), C5 (beta contrast 100), P2 (box cells, Neumann faces): the
+    # element operator
+    pid = getattr(o, pname)
+    n0 = (10, 4, 5) if pname == "P2" else (4, 4, 4)
+    level = 3 if pname == "P2" else 4
+    eps = 1e-8 if pname == "C5" else 1e-10
+    n = tuple(c << level for c in n0)
+    L = o.Level(n, pid, params=params_for(pid))
     m, _ = L.dirichlet()
     x0 = np.where(~m, synth.random_nodal(14, n), 0.0)
     res = []
-    for xd in (0, 1):
+    for xd in (0, 1 if pname == "C2" else 2):   # 2: the element operator's deferred-x K2 (ablation, default off)
         if mode == "run":
-            g = Grid(4, 6, PROB["C2"])
+            g = Grid(n0, level + 2, pid, params_for(pid))
             g.set_option(ecmg.OPT_XDEFER, xd)
-            u, ut = g.new_vec(5), g.new_vec(5)
-            st, stats = g.run(1e-10, u, ut)
+            if pname != "C2":
+                g.set_option(ecmg.OPT_PERS_TMA, 0)   # the 128^3 element level on the graph loop of K1 / K2
+            u, ut = g.new_vec(level + 1), g.new_vec(level + 1)
+            st, stats = g.run(eps, u, ut)
             assert st == 0
             res.append(([s["iterations"] for s in stats], host(u), host(ut)))
             continue
-        g = Grid(4, level + 1, PROB["C2"])
+        g = Grid(n0, level + 1, pid, params_for(pid))
         g.set_option(ecmg.OPT_XDEFER, xd)
         for opt in (ecmg.OPT_PERSISTENT, ecmg.OPT_PERS_TMA, ecmg.OPT_CTA_SOLVE):
             g.set_option(opt, 0)
@@ -508,7 +551,7 @@ def test_xdefer_bitwise(mode):
             st, stats = g.solve_level(level, 0.0, k, u)
             assert stats["iterations"] == k
         else:
-            st, stats = g.solve_level(level, 1e-10, 10000, u)
+            st, stats = g.solve_level(level, eps, 10000, u)
         assert st == 0
         res.append(([stats["iterations"]], host(u), np.array([stats["rel_res_true"]])))
     assert res[0][0] == res[1][0]

@@ -1,5 +1,5 @@
 """C5 1024^3 element iteration with beta read from the array (80 B/unknown) vs formed on the fly from the
-per-axis tables (64 B/unknown; ECMG_OPT_BETA_FLY): 20 fixed iterations from x0 = 0, best of 3 each."""
+per-axis tables (64 B/unknown; ECMG_OPT_BETA_FLY) -- or any other 0/1 option named as argv[3], e.g. XDEFER: 20 fixed iterations from x0 = 0, best of 3 each."""
 import json
 import os
 import sys
@@ -17,7 +17,7 @@ k = levels - 1
 _, nodes = g.shape(k)
 x = torch.zeros(nodes, dtype=torch.float64, device="cuda")
 for fly in (0, 1, 0, 1):
-    g.set_option(ecmg.OPT_BETA_FLY, fly)
+    g.set_option(getattr(ecmg, "OPT_" + (sys.argv[3] if len(sys.argv) > 3 else "BETA_FLY")), fly)
     g.solve_level(k, 0.0, 2, x)
     best = 1e30
     for _ in range(3):
@@ -25,5 +25,5 @@ for fly in (0, 1, 0, 1):
         g.solve_level(k, 0.0, 20, x)
         ms, it, nf = g.last_jcg_timing()
         best = min(best, ms / it)
-    print(json.dumps(dict(cfg=cfg, n=4 << k, beta_fly=fly, ms_per_iter=round(best, 4),
+    print(json.dumps(dict(cfg=cfg, n=4 << k, option=(sys.argv[3] if len(sys.argv) > 3 else "BETA_FLY"), value=fly, ms_per_iter=round(best, 4),
                           frac_at_80B=round(80 * nf / (best / 1e3) / 1e9 / 6553.6, 4))), flush=True)

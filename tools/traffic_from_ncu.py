@@ -35,9 +35,13 @@ def main():
         cfg, path = arg.split("=")
         ks = dram(path)
         bpu, nf = ALG[cfg]
-        tot = sum(k["dram_bytes"] for k in ks)
+        # 4 launches = K1, K2 with x, K1, K2 without x (deferred x update): two iterations
+        tot = sum(k["dram_bytes"] for k in ks) / (len(ks) // 2)
         out[cfg] = {"bytes_per_iteration_k1_k2": tot, "algorithmic_bytes": bpu * nf,
                     "ratio": tot / (bpu * nf), "launches": ks, "source": os.path.basename(path)}
+        if cfg == "c4" and len(ks) == 4:
+            out[cfg]["moved_bytes_deferred_x"] = 60 * nf
+            out[cfg]["ratio_to_moved"] = tot / (60 * nf)
     json.dump(out, open(os.path.join(ROOT, "profiles", "jcg_traffic.json"), "w"), indent=1)
     print(json.dumps(out, indent=1))
 
