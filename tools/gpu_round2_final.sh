@@ -1,8 +1,16 @@
-# round-2 re-validation on one B200 at HEAD: smoke, every -m gpu test, the default bench line, then (after those
-# exited 0 without ncu) the K1/K2 captures with the deferred x update (4 launches: K1, K2 with x, K1, K2 without x)
+# round-2 final evidence on one B200: smoke, every -m gpu test, the bench lines (default as the driver runs it,
+# reference arm, C3); then -- each only after its plain command exited 0 -- the ncu captures: K1 / K2 of the constant
+# path with the deferred x update (K1, K2 with x, K1, K2 without x), the symmetric C4 load, and the launch list of the
+# bench command itself
 mkdir -p gpurun_out
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo exit=$? >> gpurun_out/smoke.log
 timeout 2700 python -m pytest tests -m gpu -q --timeout 1200 -rA > gpurun_out/gpu_tests.log 2>&1; echo tests_exit=$? >> gpurun_out/gpu_tests.log
 timeout 900 python bench.py > gpurun_out/bench_default.log 2>&1; echo exit=$? >> gpurun_out/bench_default.log
+timeout 900 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_reference.log 2>&1; echo exit=$? >> gpurun_out/bench_reference.log
+timeout 600 python bench.py --config c3 --steps 3 --warmup 3 > gpurun_out/bench_c3.log 2>&1; echo exit=$? >> gpurun_out/bench_c3.log
 timeout 300 python tools/ncu_step.py --config c4 --skip-run --iters 4 > gpurun_out/plain_c4.log 2>&1 || exit 1
 timeout 900 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:k_jcg_const_tma --launch-skip 3 --launch-count 4 -o gpurun_out/p_const_xdefer python tools/ncu_step.py --config c4 --skip-run --iters 4 > gpurun_out/ncu_pc.log 2>&1
+timeout 300 python tools/exp_timing.py 8 run > gpurun_out/exp_timing_run.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_rhs_c4_sym -c 1 -o gpurun_out/rhs_c4_sym python tools/exp_timing.py 8 run > gpurun_out/ncu_rhs_sym.log 2>&1
+timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-c5 --no-arrays > gpurun_out/bench_for_launches.log 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-c5 --no-arrays > gpurun_out/ncu_lbench.log 2>&1
