@@ -24,10 +24,10 @@ WANT = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum
 for rep in sys.argv[1:]:
     out = subprocess.run(['ncu', '-i', rep, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    h = rows[0]
+    h, units = rows[0], rows[1]
     for v in rows[2:]:
         name = v[h.index('Kernel Name')] if 'Kernel Name' in h else '?'
         print('==', rep, name[:90])
         for w in WANT:
             if w in h:
-                print(f'  {w:80s} {v[h.index(w)]}')
+                print(f'  {w:80s} {v[h.index(w)]} {units[h.index(w)]}')
