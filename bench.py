@@ -601,6 +601,9 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "kernel": "jcg K1+K2 (one CG iteration)",
                          "bytes_per_unit": bpu, "peak_source": peak_src,
+                         "note": "achieved / frac count SURVEY.md §8d's algorithmic bytes (64 B constant path, 80 B "
+                                 "element path); the constant-path kernels move 60 B (deferred x update), so frac "
+                                 "can come close to 1 -- moved.frac is the share of the peak the hardware delivers",
                          "moved": {"bytes_per_unit": bpu_moved, "achieved": moved, "frac": moved / peak,
                                    "note": "bytes the kernels move per unknown and iteration (deferred x update: "
                                            "60 B on the constant path); `traffic` is the ncu DRAM figure"},

@@ -92,3 +92,14 @@ def test_struct_layouts_match_header(tmp_path):
         assert int(out[name]) == C.sizeof(cls), name
         for f, _ in cls._fields_:
             assert int(out[f"{name}.{f}"]) == getattr(cls, f).offset, (name, f)
+
+
+def test_binding_option_ids_match_the_header():
+    # every ECMG_OPT_* of include/ecmg.h has the same value in the Python binding, and the binding names no other
+    from paper_1506_02983_b200 import ecmg
+    src = open(os.path.join(ROOT, "include", "ecmg.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    hdr = {m.group(1): int(m.group(2)) for m in re.finditer(r"\bECMG_(OPT_[A-Z_0-9]+)\s*=\s*(\d+)", src)}
+    assert len(hdr) >= 20 and len(set(hdr.values())) == len(hdr)
+    py = {k: v for k, v in vars(ecmg).items() if k.startswith("OPT_")}
+    assert py == hdr

@@ -79,6 +79,38 @@ def test_fullsize_rhs(level):
     assert rel(host_at(b, lin(n, nodes)), bo) <= 1e-13
 
 
+def test_fullsize_rhs_c4_symmetric_load():
+    # the permutation-symmetric C4 load (k_rhs_c4_sym, the bench's default at 512^3 and 256^3): (a) every node of
+    # the level against the plain kernel (ECMG_OPT_RHS_SYM = 0) -- a tile that is not written, written twice or
+    # written with the wrong image shows up here; (b) nodes on both sides of its 31-node tile seams along every
+    # axis, in every class of tile triple, against the oracle's rows
+    pid, levels, n = o.C4, 8, (512,) * 3
+    for lv in (levels - 1, levels - 2):
+        g = Grid(4, lv + 1, pid)
+        b1 = g.new_vec(lv)
+        g.level_rhs(lv, b1)
+        g.set_option(ecmg.OPT_RHS_SYM, 0)
+        b0 = g.new_vec(lv)
+        g.level_rhs(lv, b0)
+        torch.cuda.synchronize()
+        d = float((b1 - b0).abs().max() / b0.abs().max())
+        print(f"C4 load at {4 << lv}^3: symmetric vs plain kernel, max rel diff {d:.2e}")
+        assert d <= 1e-14
+        assert not torch.equal(b1, b0)   # (the two kernels do differ in rounding order: both really ran)
+        if lv == levels - 1:
+            rng = np.random.default_rng(31)
+            seams = np.concatenate([31 * np.arange(1, 17), 31 * np.arange(1, 17) + 1])   # free index 31k-1 | 31k
+            pts = rng.choice(seams, size=(4000, 3))
+            pts[:1000, 2] = rng.integers(1, 512, size=1000)      # seams in x, y only
+            pts[1000:2000, 0] = rng.integers(1, 512, size=1000)  # seams in y, z only
+            nodes = np.unique(pts, axis=0)
+            _, bo = o.rows(n, pid, nodes)
+            assert rel(host_at(b1, lin(n, nodes)), bo) <= 1e-13
+        g.close()
+        del b0, b1
+        torch.cuda.empty_cache()
+
+
 def test_fullsize_stencil_apply(level):
     pid, levels, n, g, nodes = level
     p = synth.random_nodal(11, n)
