@@ -1,7 +1,7 @@
 """Add the correctly rounded ||b|| of every level to the full-size goldens (tests/golden/fullsize_<cfg>.json) --
 calls ONLY oracle/ (and synth/ for C5's geometry). The oracle's own ||b|| (Alg. 4's stopping-test norm)
 is a serial recursive sum of b_i^2 in node order; at 512^3 that sum is off by 4.7e-10 relative (C4,
-tools/diag_c4_rhs.py: the oracle's b and the GPU's b agree to ||db||_2 = 8e-16, their math.fsum norms agree to
+tests/diag_c4_rhs.py: the oracle's b and the GPU's b agree to ||db||_2 = 8e-16, their math.fsum norms agree to
 1 ulp). The golden test compares the GPU's ||b|| with normb_exact = sqrt(fsum(b_i^2)) of the oracle's b.
 
 Usage: python tests/golden/add_normb_exact.py c3 c4 c5_256 c5_512 [--threads T]"""

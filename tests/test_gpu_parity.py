@@ -81,7 +81,7 @@ def test_rhs(pid, n0, level):
         assert rel(host(b), bo) <= 1e-13
         # ||b|| against the correctly rounded norm of the oracle's b (math.fsum of the squares): the oracle's own
         # ||b|| is a serial recursive sum, whose rounding error grows with N (4.7e-10 relative at C4 512^3,
-        # tools/diag_c4_rhs.py); the bar is ||b - b'||_2 + 1e-13 ||b'||
+        # tests/diag_c4_rhs.py); the bar is ||b - b'||_2 + 1e-13 ||b'||
         nb_exact = math.sqrt(math.fsum((bo * bo).tolist()))
         print(f"||b|| gpu {nb!r} exact(oracle b) {nb_exact!r} oracle serial {nbo!r}")
         assert abs(nb - nb_exact) <= np.linalg.norm(host(b) - bo) + 1e-13 * nb_exact
