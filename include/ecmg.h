@@ -193,6 +193,12 @@ typedef enum {
                                 per-face alpha; 76 instead of 80 B -- bitwise too, but measured slower: those
                                 kernels are issue bound, C3 256^3 0.256 -> 0.261-0.285 ms, C5 1024^3 16.0-16.5 ->
                                 16.5-16.7 ms per iteration; ablation); 0: x updated in every K2 */
+  ECMG_OPT_RICH_FUSED = 21,  /* ecmg_run / ecmg_run_fixed, constant-stencil TMA path on one GPU: 1 (default) the finest
+                                level's true-residual pass (which reads x and scatters u_h anyway) also forms
+                                u~_h = EXP_true(u_h, u_2h) at its nodes -- the same expression as the EXP_true
+                                kernel, bit for bit -- so x is read once instead of u_h being read back (33
+                                instead of 41 B per fine node for the two steps); 0: the separate EXP_true
+                                kernel (ablation). ecmg_richardson always runs the separate kernel */
   ECMG_OPT_RHS_SYM = 20,     /* C4 (f a function of r only) on a level that is a cube in n, h, lo and free box: the
                                 volume load is invariant under permutations of the node indices, so about a
                                 third of the 31^3-node tiles is evaluated and the others are written as

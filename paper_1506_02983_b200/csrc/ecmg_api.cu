@@ -152,6 +152,9 @@ struct ecmg_grid {
   int kernel_variant = 1;   // ECMG_OPT_KERNEL
   int use_graph = 1;        // ECMG_OPT_GRAPH: device-driven JCG loop (CUDA graph, conditional WHILE node)
   int unfused = 0;          // ECMG_OPT_UNFUSED: fixed-count constant-stencil solves by the textbook sequence
+  int rich_fused = 1;       // ECMG_OPT_RICH_FUSED: the finest level's true-residual pass also forms EXP_true
+  double* rich_ut = nullptr;          // set by run_cascade around the finest level's solve (else null)
+  const double* rich_u2h = nullptr;
   int xdefer = 1;           // ECMG_OPT_XDEFER: TMA K2 updates x every second iteration (bitwise the same iterates)
   int shard_min = kShardMinDefault;   // ECMG_OPT_SHARD_MIN: z-slabs split only levels with >= this many z cells
   int hybrid = 1;           // ECMG_OPT_SLAB_HYBRID: z-slabs, replicated levels through the single-GPU path
@@ -363,6 +366,8 @@ bool use_xdefer(ecmg_grid* G, const LevelGeom& g) {
   return G->kernel_variant == 1 && ensure_maps(G, g, level_of(G, g));
 }
 
+bool rich_level_ok(ecmg_grid* G, int k);
+
 cudaError_t build_level_graph(ecmg_grid* G, int k, cudaGraphExec_t* out) {
   const LevelGeom& g = G->geom[k];
   const bool defer = use_xdefer(G, g);
@@ -416,7 +421,11 @@ cudaError_t build_level_graph(ecmg_grid* G, int k, cudaGraphExec_t* out) {
   e = cudaStreamBeginCaptureToGraph(G->cap_stream, graph, &cond_node, nullptr, 1, cudaStreamCaptureModeThreadLocal);
   if (e != cudaSuccess) return done(e);
   if (defer) e = launch_xfix(g, G->x, G->p[1], G->sc, G->stream);   // a skipped update still owed
-  if (e == cudaSuccess) { KArgs at = a; at.use_cond = 0; at.h0 = G->x; at.i0 = G->bl[k]; e = launch_mode(G, MODE_TRUE, g, at); }
+  if (e == cudaSuccess) {
+    KArgs at = a; at.use_cond = 0; at.h0 = G->x; at.i0 = G->bl[k];
+    at.rich = rich_level_ok(G, k) ? 1 : 0;   // (forms u~_h only in a run that sets JcgParams::ut_out)
+    e = launch_mode(G, MODE_TRUE, g, at);
+  }
   e2 = cudaStreamEndCapture(G->cap_stream, &graph);
   if (e != cudaSuccess || e2 != cudaSuccess) return done(e != cudaSuccess ? e : e2);
   e = cudaGraphInstantiate(out, graph, 0);
@@ -467,6 +476,18 @@ bool use_pers_tma(ecmg_grid* G, const LevelGeom& g) {
   // graph loop of K1 / K2 (32.5 -> 37.4 ms for the level, tools/tts_ab.py)
   if (G->elem_path) return free_count(g) <= kElemPersTmaMax && elem_pers_fits(g);
   return const_pers_fits(g) && G->kernel_variant == 1 && ensure_maps(G, g, level_of(G, g));
+}
+
+// EXP_true inside the true-residual pass (ECMG_OPT_RICH_FUSED): the launched constant-stencil TMA TRUE kernel of
+// the finest level has the variant that also forms u~_h (KArgs::rich; it acts only when JcgParams::ut_out is set)
+bool rich_level_ok(ecmg_grid* G, int k) {
+  return G->rich_fused && !G->elem_path && G->kernel_variant == 1 && G->nranks == 1 && !G->slab && k == G->L - 1 && k >= 2 &&
+         ensure_maps(G, G->geom[k], k);
+}
+// ... and the level's solve ends in that launched kernel (graph loop or host loop), not in a one-launch solve
+bool rich_fused_solve(ecmg_grid* G, int k, double eps) {
+  const LevelGeom& g = G->geom[k];
+  return rich_level_ok(G, k) && !use_persistent(G, g) && !(eps > 0.0 && G->use_graph && use_pers_tma(G, g));
 }
 
 cudaError_t launch_pers_tma(ecmg_grid* G, const LevelGeom& g) {
@@ -536,6 +557,8 @@ int enqueue_jcg(ecmg_grid* G, int k, double eps, int max_iter, double* u_out, Pa
   param->eps = eps;
   param->max_iter = max_iter;
   param->u_out = u_out;
+  param->ut_out = G->rich_ut;
+  param->u2h = G->rich_u2h;
   ECMG_CUDA(cudaMemcpyAsync(&G->sc->in, param, sizeof(JcgParams), cudaMemcpyHostToDevice, G->stream));
   if (free_count(g) == 0) {   // nothing to solve
     ECMG_CUDA(launch_empty_solve(G->sc, G->stream));
@@ -575,6 +598,8 @@ int run_jcg(ecmg_grid* G, int k, double eps, int max_iter, double* u_out, ecmg_s
   G->param_host->eps = eps;
   G->param_host->max_iter = max_iter;
   G->param_host->u_out = u_out;
+  G->param_host->ut_out = G->rich_ut;
+  G->param_host->u2h = G->rich_u2h;
   ECMG_CUDA(cudaMemcpyAsync(&G->sc->in, G->param_host, sizeof(JcgParams), cudaMemcpyHostToDevice, G->stream));
   if (free_count(g) == 0) {   // nothing to solve
     ECMG_CUDA(cudaEventRecord(G->ev[0], G->stream));
@@ -684,6 +709,7 @@ int run_jcg(ecmg_grid* G, int k, double eps, int max_iter, double* u_out, ecmg_s
   {
     KArgs at = a;
     at.h0 = G->x; at.i0 = G->bl[k];
+    at.rich = rich_level_ok(G, k) ? 1 : 0;
     ECMG_CUDA(launch_mode(G, MODE_TRUE, g, at));
   }
   ECMG_CUDA(cudaMemcpyAsync(&G->sc_host[0], G->sc, sizeof(JcgScalars), cudaMemcpyDeviceToHost, G->stream));
@@ -993,6 +1019,7 @@ int ecmg_set_option(ecmg_grid* G, int option, int value) {
     case ECMG_OPT_PERSISTENT: if (value < 0) return ECMG_EINVAL; G->persistent_max = value; break;
     case ECMG_OPT_PERS_TMA: if (value < 0) return ECMG_EINVAL; G->pers_tma_max = value; break;
     case ECMG_OPT_UNFUSED: if (value != 0 && value != 1) return ECMG_EINVAL; G->unfused = value; break;
+    case ECMG_OPT_RICH_FUSED: if (value != 0 && value != 1) return ECMG_EINVAL; G->rich_fused = value; clear_graphs(G); break;
     case ECMG_OPT_XDEFER: if (value < 0 || value > 2) return ECMG_EINVAL; G->xdefer = value; clear_graphs(G); break;
     case ECMG_OPT_SHARD_MIN: if (value < 0) return ECMG_EINVAL; G->shard_min = value; break;
     case ECMG_OPT_SLAB_HYBRID: if (value != 0 && value != 1) return ECMG_EINVAL; G->hybrid = value; break;
@@ -1224,6 +1251,11 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
     // u_k: the finest level goes straight into the caller's device buffer (no copy at the end); the
     // true-residual pass of the solve writes its free nodes (fused scatter)
     double* uk = level_u(k);
+    // the finest level's true-residual pass also forms u~_h = EXP_true(u_h, u_2h) (l.10) when it is the launched
+    // constant-stencil TMA kernel: x is read once for the residual, the scatter of u_h and u~_h
+    const bool fuse_rich = k >= 2 && k == G->L - 1 && ut_fine && rich_fused_solve(G, k, eps_k);
+    if (fuse_rich) { G->rich_ut = ut_dev ? ut_fine : G->ut_tmp; G->rich_u2h = G->u[k - 1]; }
+    struct RichOff { ecmg_grid* G; ~RichOff() { G->rich_ut = nullptr; G->rich_u2h = nullptr; } } rich_off{G};
     int s = enqueue_jcg(G, k, eps_k, maxit_k, uk, &G->lvl_param[k], &G->lvl_sc[k]);
     if (s == ECMG_OK) {
       async[k] = 1;
@@ -1237,7 +1269,10 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
     ECMG_CUDA(cudaEventRecord(e[3], G->stream));
     if (k >= 2 && k == G->L - 1 && ut_fine) {
       // u~_h = EXP_true(u_h, u_2h) (Alg. 4 l.10) on the finest level
-      ECMG_CUDA(launch_exp_true(g, level_prob(G, k), uk, G->u[k - 1], ut_dev ? ut_fine : G->ut_tmp, G->stream));
+      if (fuse_rich)   // the free nodes are written by the solve's last pass; u~ = g_D on the Dirichlet nodes (A15)
+        ECMG_CUDA(launch_dirichlet_fill(g, level_prob(G, k), ut_dev ? ut_fine : G->ut_tmp, 0.0, 0, G->stream));
+      else
+        ECMG_CUDA(launch_exp_true(g, level_prob(G, k), uk, G->u[k - 1], ut_dev ? ut_fine : G->ut_tmp, G->stream));
     }
     ECMG_CUDA(cudaEventRecord(e[4], G->stream));
     if (ahead) { int s = setups_until(k + 2); if (s) return s; }

@@ -160,6 +160,10 @@ struct JcgParams {
                      // fills with the solution (fused scatter); nullptr: no write
   int max_iter;      // requested max_iter
   int pad_;
+  // the finest level's true-residual pass in its EXP_true form (KArgs::rich): u~_h = EXP_true(u_h, u_2h) is written
+  // to the free nodes of ut_out (full layout) from u2h = the 2h level's solution (full layout); nullptr: not formed
+  double* ut_out;
+  const double* u2h;
 };
 
 // Device-resident CG scalars (no host round trip inside the iteration).
@@ -215,6 +219,7 @@ struct KArgs {
   // + alpha_k p_k with p_{k-1} = i2, the same two roundings as two single updates, so the iterates are
   // bitwise those of xdefer = 0)
   int xdefer;
+  int rich;           // TRUE (constant-stencil TMA kernel): the variant that also forms EXP_true (JcgParams::ut_out)
   const double* i2;   // K2, xdefer = 2: p_{k-1} (interior box)
 };
 

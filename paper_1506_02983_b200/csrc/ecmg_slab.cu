@@ -343,6 +343,8 @@ int slab_jcg(SlabDriver* d, int k, double eps, int max_iter, ecmg_stats* st, cud
   d->param_host->eps = eps;
   d->param_host->max_iter = max_iter;
   d->param_host->u_out = nullptr;
+  d->param_host->ut_out = nullptr;
+  d->param_host->u2h = nullptr;
   for (int i = 0; i < nloc; ++i)
     SL_CUDA(cudaMemcpyAsync(&d->s[i].sc->in, d->param_host, sizeof(JcgParams), cudaMemcpyHostToDevice, stream));
   const cudaStream_t user_stream = stream;   // the work below goes to `stream`; graph capture points it elsewhere

@@ -93,8 +93,12 @@ __device__ __forceinline__ void tma_pass(const LevelGeom& g, const ConstStencil&
                                          const CUtensorMap* pH0, const CUtensorMap* pH1, const CUtensorMap* pI0,
                                          const CUtensorMap* pI1, unsigned char* smem, uint64_t* full, uint32_t gstep,
                                          double& acc0, double& acc1, double& acc2, const CUtensorMap* pI2 = nullptr,
-                                         double alpha0 = 0.0) {
+                                         double alpha0 = 0.0, const double* rich_u2h = nullptr, double* rich_ut = nullptr) {
   constexpr bool kH1 = (MODE == MODE_K1);
+  // MODE_TRUE with XD = 3: the true-residual pass also forms u~_h = EXP_true(u_h, u_2h) (Alg. 4 l.10) at its own
+  // nodes, from the x planes it holds anyway (see the step loop); rich_ut == nullptr: plain true-residual pass
+  constexpr bool kRich = (MODE == MODE_TRUE && XD == 3);
+  const bool rich = kRich && rich_ut != nullptr;
   constexpr int kNI = num_interior<MODE, XD>();
   const int lane = threadIdx.x, w = threadIdx.y, tid = lane + TX * w;
   const int nfx = g.nf[0], nfy = g.nf[1];
@@ -127,6 +131,35 @@ __device__ __forceinline__ void tma_pass(const LevelGeom& g, const ConstStencil&
   double part[RY], q1p[RY], pp[RY];
 #pragma unroll
   for (int j = 0; j < RY; ++j) { part[j] = q1p[j] = pp[j] = 0.0; }
+  // EXP_true inside the true-residual pass (kRich). u~ = u_h + (1/3) I(d), d = u_h - u_2h at the 2h nodes and I the
+  // trilinear interpolation (A13; k_exp_true evaluates the same expression, means along x, then y, then
+  // z, so the two agree bit for bit). ea / eb: I_xy(d) at the thread's nodes on the last two even (2h) node planes.
+  // Nodes outside the free box are Dirichlet nodes, where u_h = u_2h = g_D and d = 0.
+  double ea[RY], eb[RY];
+#pragma unroll
+  for (int j = 0; j < RY; ++j) { ea[j] = eb[j] = 0.0; }
+  const int gx = g.flo[0] + x, gy0 = g.flo[1] + yb;   // global node indices of the thread's column / first row
+  const int xodd = gx & 1;
+  const long long nx2 = g.n[0] / 2 + 1, pl2 = nx2 * (g.n[1] / 2 + 1);
+  const bool fxl = x - xodd >= 0 && x - xodd < nfx, fxr = x + xodd >= 0 && x + xodd < nfx;   // 2h columns in the free box
+  // u_2h at the 2h nodes the thread needs on the NEXT 2h plane, fetched one 2h plane (two steps) ahead so that no
+  // step waits for these loads: rows rp, rp + 2, rp + 4 of the window (rp = parity of its first row: CTA-uniform),
+  // left / right 2h column; 0 outside the free box, where the x planes hold 0 as well (TMA zero fill), so d = 0
+  double u2n[3][2];
+  const int rp = (gy0 - 1) & 1;
+  auto fetch_u2 = [&](int zn) {   // for the arriving plane zn (local free index)
+    const bool zf = kRich && rich && g.zoff + zn >= 0 && g.zoff + zn < g.nf[2] && zn <= z1;
+    const double* u2p = zf ? rich_u2h + (long long)((g.flo[2] + g.zoff + zn) >> 1) * pl2 : nullptr;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const int r = rp + 2 * i, fy = yb - 1 + r;
+      const bool rf = zf && r < RY + 2 && fy >= 0 && fy < nfy;
+      const double* u2r = rf ? u2p + (long long)((gy0 - 1 + r) >> 1) * nx2 : nullptr;
+      u2n[i][0] = (rf && fxl) ? __ldg(u2r + ((gx - xodd) >> 1)) : 0.0;
+      u2n[i][1] = (rf && fxr) ? __ldg(u2r + ((gx + xodd) >> 1)) : 0.0;
+    }
+  };
+  if (kRich && rich) fetch_u2(z0 - 1 + ((g.flo[2] + g.zoff + z0 - 1) & 1));   // the first 2h plane of the march
 
   for (int s = 0; s < nsteps; ++s) {
     const int zl = z0 - 1 + s;
@@ -162,6 +195,27 @@ __device__ __forceinline__ void tma_pass(const LevelGeom& g, const ConstStencil&
     const double* I0 = reinterpret_cast<const double*>(stage_ptr(st) + HSTRIDE * (kH1 ? 2 : 1));
     const double* I1 = I0 + TX * TY;
     const int z = zl - 1;
+    if (kRich && rich && !((g.flo[2] + g.zoff + zl) & 1)) {   // (CTA-uniform) a 2h node plane arrives
+      auto plane = [&](auto rp_tag) {
+        constexpr int RP = decltype(rp_tag)::value;
+        double xi[3];   // I_x(d) on the window's 2h rows RP, RP + 2, RP + 4
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          const int r = RP + 2 * i;
+          if (r >= RY + 2) { xi[i] = 0.0; continue; }
+          const double dl = (xodd ? col[r][0] : col[r][1]) - u2n[i][0];
+          const double dr = (xodd ? col[r][2] : col[r][1]) - u2n[i][1];
+          xi[i] = 0.5 * dl + 0.5 * dr;
+        }
+#pragma unroll
+        for (int j = 0; j < RY; ++j) {   // node row j = window row j + 1: a 2h row iff (j + 1 - RP) is even
+          ea[j] = eb[j];
+          eb[j] = ((j + 1 - RP) & 1) ? 0.5 * xi[(j - RP) / 2] + 0.5 * xi[(j - RP) / 2 + 1] : xi[(j + 1 - RP) / 2];
+        }
+      };
+      if (rp) plane(std::integral_constant<int, 1>{}); else plane(std::integral_constant<int, 0>{});
+      fetch_u2(zl + 2);
+    }
 #pragma unroll
     for (int j = 0; j < RY; ++j) {
       const double cc = col[j + 1][1];
@@ -201,6 +255,10 @@ __device__ __forceinline__ void tma_pass(const LevelGeom& g, const ConstStencil&
           const double rn = I0[io] - ap;
           acc1 = __fma_rn(rn, rn, acc1);
           if (u_out) u_out[full_index(g, x, yb + j, z)] = pp[j];   // fused scatter of u_h
+          if (kRich && rich) {   // plane z between two 2h planes: the mean of their I_xy(d); on a 2h plane: its own
+            const double e = ((g.flo[2] + g.zoff + z) & 1) ? 0.5 * (ea[j] + eb[j]) : eb[j];
+            rich_ut[full_index(g, x, yb + j, z)] = __fma_rn(e, 1.0 / 3.0, pp[j]);
+          }
         } else {
           a.o0[off] = ap;
         }
@@ -241,6 +299,8 @@ __global__ void __launch_bounds__(NTH, 2)
   if (MODE == MODE_K1) { bcg = sc->beta; first = (sc->iter == 0); }
   if (MODE == MODE_K2) { alpha = sc->alpha; alpha0 = XD == 2 ? sc->alpha_prev : 0.0; }
   double* const u_out = (MODE == MODE_TRUE) ? sc->in.u_out : nullptr;
+  double* const rich_ut = (MODE == MODE_TRUE && XD == 3) ? sc->in.ut_out : nullptr;
+  const double* const rich_u2h = (MODE == MODE_TRUE && XD == 3) ? sc->in.u2h : nullptr;
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) mbar_init(&full[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -249,7 +309,7 @@ __global__ void __launch_bounds__(NTH, 2)
   double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
   // XD = 1 (K2 without x): the one interior box is r (I1)
   tma_pass<MODE, NS, SBYTES, XD>(g, cs, a, X0, Y0, z0, z1, bcg, first, alpha, u_out, &mH0, &mH1, XD == 1 ? &mI1 : &mI0, &mI1,
-                                 smem, full, 0u, acc0, acc1, acc2, &mI2, alpha0);
+                                 smem, full, 0u, acc0, acc1, acc2, &mI2, alpha0, rich_u2h, rich_ut);
   if ((MODE == MODE_K2 || MODE == MODE_INIT) && (a.peer_lo || a.peer_hi)) __threadfence_system();   // peer stores
   if (MODE != MODE_APPLY) reduce_finalize(MODE, a, acc0, acc1, acc2);
 }
@@ -399,6 +459,7 @@ cudaError_t init_tma_kernel_attributes() {
   if (e == cudaSuccess) e = set_tma_attr<MODE_K2, 3, 2>();
   if (e == cudaSuccess) e = set_tma_attr<MODE_INIT, 4>();
   if (e == cudaSuccess) e = set_tma_attr<MODE_TRUE, 4>();
+  if (e == cudaSuccess) e = set_tma_attr<MODE_TRUE, 4, 3>();
   if (e == cudaSuccess) e = set_tma_attr<MODE_APPLY, 4>();
   return e;
 }
@@ -415,7 +476,9 @@ cudaError_t launch_jcg_const_tma(int mode, const LevelGeom& g, const ConstStenci
       if (a.xdefer == 2) return launch_tma_mode<MODE_K2, 3, 2>(grid, block, g, cs, a, maps, st);
       return launch_tma_mode<MODE_K2, 3>(grid, block, g, cs, a, maps, st);
     case MODE_INIT: return launch_tma_mode<MODE_INIT, 4>(grid, block, g, cs, a, maps, st);
-    case MODE_TRUE: return launch_tma_mode<MODE_TRUE, 4>(grid, block, g, cs, a, maps, st);
+    case MODE_TRUE:
+      if (a.rich) return launch_tma_mode<MODE_TRUE, 4, 3>(grid, block, g, cs, a, maps, st);   // + EXP_true (JcgParams::ut_out)
+      return launch_tma_mode<MODE_TRUE, 4>(grid, block, g, cs, a, maps, st);
     case MODE_APPLY: return launch_tma_mode<MODE_APPLY, 4>(grid, block, g, cs, a, maps, st);
     default: return cudaErrorInvalidValue;
   }

@@ -186,8 +186,15 @@ def test_fullsize_ecmg_run_bench_config():
         runs.append(([s["iterations"] for s in stats], u, ut))
     assert runs[0][0] == runs[1][0]
     assert torch.equal(runs[0][1], runs[1][1]) and torch.equal(runs[0][2], runs[1][2])
+    # the default run forms u~_h inside the finest level's true-residual pass (ECMG_OPT_RICH_FUSED); the separate
+    # EXP_true kernel gives the same u~_h bit for bit, and u_h / the counts are untouched
+    g.set_option(ecmg.OPT_RICH_FUSED, 0)
+    u, ut = g.new_vec(levels - 1), g.new_vec(levels - 1)
+    st, stats = g.run(1e-9, u, ut)
+    assert st == 0 and [s["iterations"] for s in stats] == runs[0][0]
+    assert torch.equal(u, runs[0][1]) and torch.equal(ut, runs[0][2])
     g.close()
-    del runs
+    del runs, u, ut
     torch.cuda.empty_cache()
 
 

@@ -559,6 +559,46 @@ def test_xdefer_bitwise(pname, mode):
         assert np.array_equal(res[0][k], res[1][k])
 
 
+@pytest.mark.parametrize("pname,n0,levels,loop", [("C2", 4, 5, "graph"), ("C2", 4, 5, "host"), ("C4", 5, 5, "graph"),
+                                                  ("C1", 6, 4, "graph"), ("C2", (4, 6, 5), 5, "graph"), ("C2", 4, 5, "fixed")])
+def test_rich_fused_bitwise(pname, n0, levels, loop):
+    # ECMG_OPT_RICH_FUSED: the finest level's true-residual pass (launched constant-stencil TMA kernel) also forms
+    # u~_h = EXP_true(u_h, u_2h). Same expression as the EXP_true kernel (means along x, y, z of d = u_h - u_2h at the
+    # 2h nodes, d = 0 on Dirichlet nodes), so u~_h must be bitwise the separate kernel's, and u_h / the counts
+    # untouched; against the oracle as usual. Finest levels 64^3, 80^3, 48^3 (ragged tiles) and a 64 x 96 x 80 box;
+    # CUDA-graph loop, host loop and Alg. 3's fixed counts
+    pid = getattr(o, pname)
+    n0 = (n0,) * 3 if np.isscalar(n0) else n0
+    res = []
+    for fused in (1, 0):
+        g = Grid(n0, levels, pid)
+        g.set_option(ecmg.OPT_RICH_FUSED, fused)
+        for opt in (ecmg.OPT_PERSISTENT, ecmg.OPT_PERS_TMA):
+            g.set_option(opt, 0)     # the finest level on the launched K1 / K2 / true-residual kernels
+        if loop == "host":
+            g.set_option(ecmg.OPT_GRAPH, 0)
+        u, ut = g.new_vec(levels - 1), g.new_vec(levels - 1)
+        ut.fill_(float("nan"))
+        if loop == "fixed":
+            st, stats = g.run_fixed(3, 2.0, u, ut)
+        else:
+            st, stats = g.run(1e-10, u, ut)
+        assert st == 0
+        res.append(([s["iterations"] for s in stats], host(u).copy(), host(ut).copy()))
+        if fused and loop == "graph":   # u~_h into a host buffer (staged through the grid's device copy)
+            uth = torch.empty(ut.numel(), dtype=torch.float64).pin_memory()
+            st2, _ = g.run(1e-10, u, uth)
+            assert st2 == 0 and np.array_equal(uth.numpy(), res[0][2])
+        g.close()
+    assert res[0][0] == res[1][0]
+    assert np.array_equal(res[0][1], res[1][1])
+    assert not np.isnan(res[0][2]).any()
+    assert np.array_equal(res[0][2], res[1][2])
+    if loop == "graph":
+        ost, ostats, ou, out = o.ecmg(n0, levels, pid, 1e-10)
+        assert rel(res[0][2], out) <= 1e-9
+
+
 @pytest.mark.parametrize("pid,level", [(o.C2, 4), (o.C4, 5), (o.C1, 3)])
 def test_unfused_textbook_equals_fused(pid, level):
     # ECMG_OPT_UNFUSED (the ablation of the fused K1 / K2 kernels): the textbook PCG sequence as separate
