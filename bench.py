@@ -589,7 +589,9 @@ def main():
             "ecmg_tts_ms_ablation_hostloop": tts_hostloop,
             "ecmg_tts_ms_ablation_setup_inline": tts_inline,
             "fine_grid_jcg_in_run": {"value": fine_units / (fine_ms / 1e3), "unit": UNIT,
-                                     "iterations": int(per_level[-1]["iterations"])},
+                                     "iterations": int(per_level[-1]["iterations"]),
+                                     "window": "the finest level's whole solve: init pass, the iterations, and the "
+                                               "true-residual pass, which also forms EXP_true (ECMG_OPT_RICH_FUSED)"},
             "jcg_fixed": {"value": jcg_ups, "unit": UNIT, "iterations": it_j, "ms": ms_j,
                           "ms_per_iteration": ms_j / it_j, "kernel": "TMA-fed (default)"},
             "jcg_fixed_ablation_prefetch": {"value": nf_j * it_p / (ms_p / 1e3), "unit": UNIT,

@@ -221,7 +221,10 @@ typedef struct {
   double norm_b;         /* ||f_h||_2 over free rows (lifted RHS) */
   int converged;
   int status;            /* ecmg_status of this level */
-  double ms_setup, ms_exp, ms_solve, ms_rich;  /* device time (CUDA events) of the level's phases */
+  double ms_setup, ms_exp, ms_solve, ms_rich;  /* device time (CUDA events) of the level's phases: waiting for /
+                            running the setup, EXP_finite, the JCG solve incl. its true-residual pass, EXP_true.
+                            With ECMG_OPT_RICH_FUSED the finest level's EXP_true is formed inside the solve's
+                            last pass: it is then part of ms_solve, and ms_rich is the g_D fill of u~_h only */
 } ecmg_stats;
 
 /* JCG solve of level `level` (Alg. 4 l.7-9): textbook PCG with M = diag(A_h),

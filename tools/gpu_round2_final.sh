@@ -13,7 +13,7 @@ timeout 900 ncu --profile-from-start off --set full --clock-control none --impor
 timeout 300 python tools/exp_timing.py 8 run > gpurun_out/exp_timing_run.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_rhs_c4_sym -c 1 -o gpurun_out/rhs_c4_sym python tools/exp_timing.py 8 run > gpurun_out/ncu_rhs_sym.log 2>&1
 # the finest level's true-residual pass in its EXP_true form (ECMG_OPT_RICH_FUSED): one ecmg_run inside the profiler range
-timeout 300 python tools/ncu_step.py --config c4 --iters 1 > gpurun_out/plain_c4_run.log 2>&1 || exit 1
-timeout 900 ncu --profile-from-start off --set full --clock-control none --import-source on --kernel-name-base demangled -k 'regex:k_jcg_const_tma<4, 4, 3>' --launch-count 1 -o gpurun_out/true_rich python tools/ncu_step.py --config c4 --iters 1 > gpurun_out/ncu_tr.log 2>&1
+timeout 300 python tools/ncu_step.py --config c4 --iters 1 --host-loop > gpurun_out/plain_c4_run.log 2>&1 || exit 1
+timeout 900 ncu --profile-from-start off --set full --clock-control none --import-source on --kernel-name-base demangled -k 'regex:k_jcg_const_tma<\(int\)4, \(int\)4, \(int\)3>' --launch-count 1 -o gpurun_out/true_rich python tools/ncu_step.py --config c4 --iters 1 --host-loop > gpurun_out/ncu_tr.log 2>&1
 timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-c5 --no-arrays > gpurun_out/bench_for_launches.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-c5 --no-arrays > gpurun_out/ncu_lbench.log 2>&1
