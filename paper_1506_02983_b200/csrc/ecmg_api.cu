@@ -152,6 +152,7 @@ struct ecmg_grid {
   int kernel_variant = 1;   // ECMG_OPT_KERNEL
   int use_graph = 1;        // ECMG_OPT_GRAPH: device-driven JCG loop (CUDA graph, conditional WHILE node)
   int unfused = 0;          // ECMG_OPT_UNFUSED: fixed-count constant-stencil solves by the textbook sequence
+  int p0_init = 1;          // ECMG_OPT_P0_INIT: the init pass stores p_0 = D^-1 r_0 instead of r_0 (KArgs::p0)
   int rich_fused = 1;       // ECMG_OPT_RICH_FUSED: the finest level's true-residual pass also forms EXP_true
   double* rich_ut = nullptr;          // set by run_cascade around the finest level's solve (else null)
   const double* rich_u2h = nullptr;
@@ -278,7 +279,8 @@ cudaError_t launch_mode(ecmg_grid* G, int mode, const LevelGeom& g, const KArgs&
   if (G->kernel_variant == 1 && ensure_maps(G, g, level_of(G, g))) {
     const CUtensorMap* h0 = halo_map(G, a.h0);
     const CUtensorMap* h1 = a.h1 ? halo_map(G, a.h1) : h0;
-    const CUtensorMap* i0 = a.i0 ? int_map(G, a.i0) : h0;
+    // (KArgs::p0: the first K1 reads p_0 from its own output vector -- that halo map rides in the I0 slot)
+    const CUtensorMap* i0 = (mode == MODE_K1 && a.p0) ? halo_map(G, a.o0) : (a.i0 ? int_map(G, a.i0) : h0);
     const CUtensorMap* i1 = a.i1 ? int_map(G, a.i1) : h0;
     const CUtensorMap* i2 = a.i2 ? int_map(G, a.i2) : h0;
     if (h0 && h1 && i0 && i1 && i2) {
@@ -368,6 +370,12 @@ bool use_xdefer(ecmg_grid* G, const LevelGeom& g) {
 
 bool rich_level_ok(ecmg_grid* G, int k);
 
+// p_0 from the init pass (KArgs::p0): the launched constant-stencil TMA kernels
+// of this grid's own (single-GPU) solves
+bool use_p0(ecmg_grid* G, const LevelGeom& g) {
+  return G->p0_init && !G->elem_path && G->kernel_variant == 1 && ensure_maps(G, g, level_of(G, g));
+}
+
 cudaError_t build_level_graph(ecmg_grid* G, int k, cudaGraphExec_t* out) {
   const LevelGeom& g = G->geom[k];
   const bool defer = use_xdefer(G, g);
@@ -388,7 +396,9 @@ cudaError_t build_level_graph(ecmg_grid* G, int k, cudaGraphExec_t* out) {
   // init pass
   e = cudaStreamBeginCaptureToGraph(G->cap_stream, graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
   if (e != cudaSuccess) return done(e);
-  { KArgs ai = a; ai.h0 = G->x; ai.i0 = G->bl[k]; ai.o0 = G->r; ai.o1 = G->zv; e = launch_mode(G, MODE_INIT, g, ai); }
+  const bool p0 = use_p0(G, g);
+  a.p0 = p0 ? 1 : 0;   // (the init pass then writes p_0 into p[1], the first K1's output vector)
+  { KArgs ai = a; ai.h0 = G->x; ai.i0 = G->bl[k]; ai.o0 = p0 ? G->p[1] : G->r; ai.o1 = G->zv; e = launch_mode(G, MODE_INIT, g, ai); }
   cudaError_t e2 = cudaStreamEndCapture(G->cap_stream, &graph);
   if (e != cudaSuccess || e2 != cudaSuccess) return done(e != cudaSuccess ? e : e2);
   size_t nn = 1;
@@ -624,10 +634,12 @@ int run_jcg(ecmg_grid* G, int k, double eps, int max_iter, double* u_out, ecmg_s
   }
   if (eps > 0.0 && G->use_graph) return run_jcg_graph(G, k, eps, st);
   const bool defer = use_xdefer(G, g) && !(eps <= 0.0 && G->unfused);
+  const bool p0 = use_p0(G, g) && !(eps <= 0.0 && G->unfused);
+  a.p0 = p0 ? 1 : 0;
   // r = b - A x, rho = r.z, rr = r.r, stop test
   {
     KArgs ai = a;
-    ai.h0 = G->x; ai.i0 = G->bl[k]; ai.o0 = G->r; ai.o1 = G->zv;
+    ai.h0 = G->x; ai.i0 = G->bl[k]; ai.o0 = p0 ? G->p[1] : G->r; ai.o1 = G->zv;
     ECMG_CUDA(launch_mode(G, MODE_INIT, g, ai));
   }
   long long it = 0;
@@ -1019,6 +1031,7 @@ int ecmg_set_option(ecmg_grid* G, int option, int value) {
     case ECMG_OPT_PERSISTENT: if (value < 0) return ECMG_EINVAL; G->persistent_max = value; break;
     case ECMG_OPT_PERS_TMA: if (value < 0) return ECMG_EINVAL; G->pers_tma_max = value; break;
     case ECMG_OPT_UNFUSED: if (value != 0 && value != 1) return ECMG_EINVAL; G->unfused = value; break;
+    case ECMG_OPT_P0_INIT: if (value != 0 && value != 1) return ECMG_EINVAL; G->p0_init = value; clear_graphs(G); break;
     case ECMG_OPT_RICH_FUSED: if (value != 0 && value != 1) return ECMG_EINVAL; G->rich_fused = value; clear_graphs(G); break;
     case ECMG_OPT_XDEFER: if (value < 0 || value > 2) return ECMG_EINVAL; G->xdefer = value; clear_graphs(G); break;
     case ECMG_OPT_SHARD_MIN: if (value < 0) return ECMG_EINVAL; G->shard_min = value; break;

@@ -59,6 +59,7 @@ struct LevelGeom {
 struct ConstStencil {
   double c0[2], cx[2], cy[2], cd[2];
   double dinv;   // 1 / diag (Jacobi), or 1 for plain CG
+  double diag;   // diag (Jacobi), or 1: r_0 = diag p_0 where only p_0 = D^-1 r_0 is stored (KArgs::p0)
 };
 
 // Element stencil: K_ref[a][b] = kappa[pattern(a,b)], pattern = bit d set if a, b differ along d.
@@ -219,6 +220,10 @@ struct KArgs {
   // + alpha_k p_k with p_{k-1} = i2, the same two roundings as two single updates, so the iterates are
   // bitwise those of xdefer = 0)
   int xdefer;
+  // p0 (constant-stencil TMA kernels, one GPU): the init pass stores p_0 = D^-1 r_0 (into the first K1's output
+  // vector) instead of r_0; the first K1 reads it (no transform, no store) and the first K2 forms r_0 = D p_0
+  // instead of reading r: 16 B per unknown less in iteration 0
+  int p0;
   int rich;           // TRUE (constant-stencil TMA kernel): the variant that also forms EXP_true (JcgParams::ut_out)
   const double* i2;   // K2, xdefer = 2: p_{k-1} (interior box)
 };

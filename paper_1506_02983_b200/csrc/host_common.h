@@ -101,6 +101,7 @@ inline ConstStencil make_const_stencil(const LevelGeom& g, double beta, int prec
     cs.cd[oz] = c(1, 1, oz);
   }
   cs.dinv = precond ? 1.0 / c(0, 0, 0) : 1.0;
+  cs.diag = precond ? c(0, 0, 0) : 1.0;
   return cs;
 }
 

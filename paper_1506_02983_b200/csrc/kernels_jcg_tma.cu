@@ -70,14 +70,15 @@ __host__ __device__ constexpr int num_interior() {
 template <bool kH1, int kNI, int SBYTES>
 __device__ __forceinline__ void issue_stage(unsigned char* smem, uint64_t* full, int st, int t, int z0, int X0, int Y0,
                                             uint32_t tx_bytes, bool first, const CUtensorMap* pH0, const CUtensorMap* pH1,
-                                            const CUtensorMap* pI0, const CUtensorMap* pI1, const CUtensorMap* pI2) {
+                                            const CUtensorMap* pI0, const CUtensorMap* pI1, const CUtensorMap* pI2,
+                                            int skip_int = -1) {   // interior box not loaded (K2 of iteration 0, KArgs::p0)
   unsigned char* base = smem + st * SBYTES;
   mbar_expect_tx(&full[st], tx_bytes);
   const int zh = z0 - 1 + t;
   tma_load_3d(base, pH0, X0 - XO, Y0 - 1, zh, &full[st]);
   if (kH1 && !first) tma_load_3d(base + HSTRIDE, pH1, X0 - XO, Y0 - 1, zh, &full[st]);
-  if (kNI >= 1) tma_load_3d(base + HSTRIDE * (kH1 ? 2 : 1), pI0, X0, Y0, zh - 1, &full[st]);
-  if (kNI >= 2) tma_load_3d(base + HSTRIDE * (kH1 ? 2 : 1) + IBYTES, pI1, X0, Y0, zh - 1, &full[st]);
+  if (kNI >= 1 && skip_int != 0) tma_load_3d(base + HSTRIDE * (kH1 ? 2 : 1), pI0, X0, Y0, zh - 1, &full[st]);
+  if (kNI >= 2 && skip_int != 1) tma_load_3d(base + HSTRIDE * (kH1 ? 2 : 1) + IBYTES, pI1, X0, Y0, zh - 1, &full[st]);
   if (kNI >= 3) tma_load_3d(base + HSTRIDE * (kH1 ? 2 : 1) + 2 * IBYTES, pI2, X0, Y0, zh - 1, &full[st]);
 }
 
@@ -106,12 +107,16 @@ __device__ __forceinline__ void tma_pass(const LevelGeom& g, const ConstStencil&
   const int x = X0 + lane, yb = Y0 + RY * w;
   const int nsteps = z1 - z0 + 2;
   const double dinv = cs.dinv;
-  const uint32_t tx_bytes = HBYTES + ((kH1 && !first) ? HBYTES : 0) + IBYTES * kNI;
+  // KArgs::p0, iteration 0 (`first`): K1 reads p_0 as stored by the init pass (pH0 is its map: no transform, no
+  // store); K2 forms r_0 = diag p_0 and does not load r (interior box XD == 1 ? 0 : 1)
+  const bool p0k1 = MODE == MODE_K1 && first && a.p0, p0k2 = MODE == MODE_K2 && first && a.p0;
+  const int skip_int = p0k2 ? (XD == 1 ? 0 : 1) : -1;
+  const uint32_t tx_bytes = HBYTES + ((kH1 && !first) ? HBYTES : 0) + IBYTES * kNI - (p0k2 ? IBYTES : 0);
   auto stage_ptr = [&](int st) { return smem + st * SBYTES; };
   if (tid == 0) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic accesses before async-proxy writes
     for (int t = 0; t < NS - 1 && t < nsteps; ++t)
-      issue_stage<kH1, kNI, SBYTES>(smem, full, (gstep + t) % NS, t, z0, X0, Y0, tx_bytes, first, pH0, pH1, pI0, pI1, pI2);
+      issue_stage<kH1, kNI, SBYTES>(smem, full, (gstep + t) % NS, t, z0, X0, Y0, tx_bytes, first, pH0, pH1, pI0, pI1, pI2, skip_int);
   }
 
   // halo ring slot of this thread (transform in place, K1 only): rows y = Y0-1, Y0+32 (x = X0-1 ..
@@ -168,24 +173,26 @@ __device__ __forceinline__ void tma_pass(const LevelGeom& g, const ConstStencil&
     if (tid == 0 && s + NS - 1 < nsteps) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes before async-proxy writes
       const int t = s + NS - 1;                                      // into stage (s-1) % NS
-      issue_stage<kH1, kNI, SBYTES>(smem, full, (gstep + t) % NS, t, z0, X0, Y0, tx_bytes, first, pH0, pH1, pI0, pI1, pI2);
+      issue_stage<kH1, kNI, SBYTES>(smem, full, (gstep + t) % NS, t, z0, X0, Y0, tx_bytes, first, pH0, pH1, pI0, pI1, pI2, skip_int);
     }
     mbar_wait(&full[st], (uint32_t)(((gstep + s) / NS) & 1));
     double* H = reinterpret_cast<double*>(stage_ptr(st));
     if (MODE == MODE_K1) {
       const double* H1 = reinterpret_cast<const double*>(stage_ptr(st) + HSTRIDE);
       const bool halo_store = (zl == g.zbeg - 1 || zl == g.zend) && zl >= 0 && zl < g.nza;
+      if (!p0k1) {   // (uniform)
 #pragma unroll
-      for (int j = 0; j < RY; ++j) {
-        const int o = (1 + RY * w + j) * HX + XO + lane;
-        H[o] = pcg_direction(dinv, H[o], bcg, H1[o], first);
-        if (halo_store && own_ok[j]) a.o0[(long long)zl * S + own_off[j]] = H[o];   // slab halo plane of p
+        for (int j = 0; j < RY; ++j) {
+          const int o = (1 + RY * w + j) * HX + XO + lane;
+          H[o] = pcg_direction(dinv, H[o], bcg, H1[o], first);
+          if (halo_store && own_ok[j]) a.o0[(long long)zl * S + own_off[j]] = H[o];   // slab halo plane of p
+        }
+        if (rhx >= 0) {
+          const int o = rhy * HX + rhx;
+          H[o] = pcg_direction(dinv, H[o], bcg, H1[o], first);
+        }
+        __syncthreads();
       }
-      if (rhx >= 0) {
-        const int o = rhy * HX + rhx;
-        H[o] = pcg_direction(dinv, H[o], bcg, H1[o], first);
-      }
-      __syncthreads();
     }
     double col[RY + 2][3];
 #pragma unroll
@@ -230,10 +237,10 @@ __device__ __forceinline__ void tma_pass(const LevelGeom& g, const ConstStencil&
         const int io = (RY * w + j) * TX + lane;
         if (MODE == MODE_K1) {
           acc0 = __fma_rn(pp[j], ap, acc0);
-          a.o0[off] = pp[j];
+          if (!p0k1) a.o0[off] = pp[j];
         } else if (MODE == MODE_K2) {
           // interior boxes: XD 0 (x, r), 1 (r), 2 (x, r, p_{k-1})
-          const double rn = __fma_rn(-alpha, ap, XD == 1 ? I0[io] : I1[io]);
+          const double rn = __fma_rn(-alpha, ap, p0k2 ? cs.diag * pp[j] : (XD == 1 ? I0[io] : I1[io]));
           const double zz = dinv * rn;
           acc0 = __fma_rn(rn, zz, acc0);
           acc1 = __fma_rn(rn, rn, acc1);
@@ -248,7 +255,7 @@ __device__ __forceinline__ void tma_pass(const LevelGeom& g, const ConstStencil&
           const double zz = dinv * rn;
           acc0 = __fma_rn(rn, zz, acc0);
           acc1 = __fma_rn(rn, rn, acc1);
-          a.o0[off] = rn;
+          a.o0[off] = a.p0 ? zz : rn;   // (p0: o0 is the first K1's output vector and receives p_0 = D^-1 r_0)
           if (z == g.zbeg && a.peer_lo) a.peer_lo[own_off[j]] = rn;      // fused halo exchange
           if (z == g.zend - 1 && a.peer_hi) a.peer_hi[own_off[j]] = rn;
         } else if (MODE == MODE_TRUE) {
@@ -297,7 +304,7 @@ __global__ void __launch_bounds__(NTH, 2)
   double bcg = 0.0, alpha = 0.0, alpha0 = 0.0;
   bool first = false;
   if (MODE == MODE_K1) { bcg = sc->beta; first = (sc->iter == 0); }
-  if (MODE == MODE_K2) { alpha = sc->alpha; alpha0 = XD == 2 ? sc->alpha_prev : 0.0; }
+  if (MODE == MODE_K2) { alpha = sc->alpha; alpha0 = XD == 2 ? sc->alpha_prev : 0.0; first = a.p0 && sc->iter == 0; }
   double* const u_out = (MODE == MODE_TRUE) ? sc->in.u_out : nullptr;
   double* const rich_ut = (MODE == MODE_TRUE && XD == 3) ? sc->in.ut_out : nullptr;
   const double* const rich_u2h = (MODE == MODE_TRUE && XD == 3) ? sc->in.u2h : nullptr;
@@ -308,7 +315,9 @@ __global__ void __launch_bounds__(NTH, 2)
   __syncthreads();
   double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
   // XD = 1 (K2 without x): the one interior box is r (I1)
-  tma_pass<MODE, NS, SBYTES, XD>(g, cs, a, X0, Y0, z0, z1, bcg, first, alpha, u_out, &mH0, &mH1, XD == 1 ? &mI1 : &mI0, &mI1,
+  // (p0, the first K1: the halo map of its own output vector, which holds p_0, rides in the I0 slot)
+  tma_pass<MODE, NS, SBYTES, XD>(g, cs, a, X0, Y0, z0, z1, bcg, first, alpha, u_out,
+                                 (MODE == MODE_K1 && first && a.p0) ? &mI0 : &mH0, &mH1, XD == 1 ? &mI1 : &mI0, &mI1,
                                  smem, full, 0u, acc0, acc1, acc2, &mI2, alpha0, rich_u2h, rich_ut);
   if ((MODE == MODE_K2 || MODE == MODE_INIT) && (a.peer_lo || a.peer_hi)) __threadfence_system();   // peer stores
   if (MODE != MODE_APPLY) reduce_finalize(MODE, a, acc0, acc1, acc2);

@@ -35,6 +35,7 @@ OPT_SHARD_MIN = 18
 OPT_XDEFER = 19
 OPT_RHS_SYM = 20
 OPT_RICH_FUSED = 21
+OPT_P0_INIT = 22
 
 EXPORTS = ["ecmg_create_grid", "ecmg_set_coeffs", "ecmg_set_option", "ecmg_solve_level",
            "ecmg_prolongate_extrapolate", "ecmg_richardson", "ecmg_run", "ecmg_run_fixed", "ecmg_apply_operator",

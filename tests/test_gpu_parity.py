@@ -302,6 +302,7 @@ def test_tma_and_prefetch_kernels_bitwise(pid, level):
     for kv in (1, 0):
         g = Grid(4, level + 1, pid)
         g.set_option(ecmg.OPT_KERNEL, kv)
+        g.set_option(ecmg.OPT_P0_INIT, 0)   # (the TMA kernels' p_0-from-the-init-pass form rounds r_0 once more)
         u = dev(x0)
         st, s = g.solve_level(level, 0.0, 20, u)
         assert st == 0
@@ -557,6 +558,58 @@ def test_xdefer_bitwise(pname, mode):
     assert res[0][0] == res[1][0]
     for k in range(1, len(res[0])):
         assert np.array_equal(res[0][k], res[1][k])
+
+
+@pytest.mark.parametrize("precond", [True, False])
+@pytest.mark.parametrize("mode", ["fixed1", "fixed2", "fixed9", "host", "graph", "run"])
+def test_p0_from_init_pass(mode, precond):
+    # ECMG_OPT_P0_INIT: the init pass stores p_0 = D^-1 r_0 instead of r_0, the first K1 reads it and the first K2
+    # forms r_0 = D p_0. With Jacobi scaling r_0 carries one more rounding (<= 1 ulp), so the iterates agree with the
+    # r_0-stored form to rounding (1e-13 normwise, equal counts) and with the oracle within the usual bars; for plain
+    # CG (D = 1) the two forms are bitwise equal. Fixed counts 1, 2, 9, the host and graph loops, a whole run
+    level, n = 4, (64,) * 3
+    L = o.Level(n, o.C2)
+    m, _ = L.dirichlet()
+    x0 = np.where(~m, synth.random_nodal(14, n), 0.0)
+    res = []
+    for p0 in (1, 0):
+        if mode == "run":
+            g = Grid(4, 6, PROB["C2"], precond=precond)
+            g.set_option(ecmg.OPT_P0_INIT, p0)
+            g.set_option(ecmg.OPT_PERS_TMA, 0)   # 64^3 and 128^3 on the launched kernels
+            u, ut = g.new_vec(5), g.new_vec(5)
+            st, stats = g.run(1e-10, u, ut)
+            assert st == 0
+            res.append(([s["iterations"] for s in stats], host(u), host(ut)))
+            g.close()
+            continue
+        g = Grid(4, level + 1, PROB["C2"], precond=precond)
+        g.set_option(ecmg.OPT_P0_INIT, p0)
+        for opt in (ecmg.OPT_PERSISTENT, ecmg.OPT_PERS_TMA, ecmg.OPT_CTA_SOLVE):
+            g.set_option(opt, 0)
+        if mode == "host":
+            g.set_option(ecmg.OPT_GRAPH, 0)
+        u = dev(x0)
+        if mode.startswith("fixed"):
+            k = int(mode[5:])
+            st, stats = g.solve_level(level, 0.0, k, u)
+            assert stats["iterations"] == k
+            if p0 and precond:
+                xo, _ = L.jcg(x0, 0.0, k)
+                assert rel(host(u)[~m], xo[~m]) <= 1e-12
+        else:
+            st, stats = g.solve_level(level, 1e-10, 10000, u)
+        assert st == 0
+        res.append(([stats["iterations"]], host(u), np.array([stats["rel_res_true"]])))
+        g.close()
+    assert res[0][0] == res[1][0]
+    for k in (1, 2):
+        if not precond:
+            assert np.array_equal(res[0][k], res[1][k])
+        elif k == 2 and mode != "run":   # RRe of a converged solve: a rounding-level change of x moves it visibly
+            assert abs(res[0][k][0] - res[1][k][0]) <= 1e-3 * res[1][k][0]
+        else:
+            assert rel(res[0][k], res[1][k]) <= 1e-13
 
 
 @pytest.mark.parametrize("pname,n0,levels,loop", [("C2", 4, 5, "graph"), ("C2", 4, 5, "host"), ("C4", 5, 5, "graph"),
