@@ -561,22 +561,24 @@ def test_xdefer_bitwise(pname, mode):
 
 
 @pytest.mark.parametrize("precond", [True, False])
-@pytest.mark.parametrize("mode", ["fixed1", "fixed2", "fixed9", "host", "graph", "run"])
+@pytest.mark.parametrize("mode", ["fixed1", "fixed2", "fixed9", "host", "graph", "run", "run_pers"])
 def test_p0_from_init_pass(mode, precond):
     # ECMG_OPT_P0_INIT: the init pass stores p_0 = D^-1 r_0 instead of r_0, the first K1 reads it and the first K2
     # forms r_0 = D p_0. With Jacobi scaling r_0 carries one more rounding (<= 1 ulp), so the iterates agree with the
     # r_0-stored form to rounding (1e-13 normwise, equal counts) and with the oracle within the usual bars; for plain
-    # CG (D = 1) the two forms are bitwise equal. Fixed counts 1, 2, 9, the host and graph loops, a whole run
+    # CG (D = 1) the two forms are bitwise equal. Fixed counts 1, 2, 9, the host and graph loops, a whole run on the
+    # launched kernels and on the cooperative one-launch solves (which take the same two forms)
     level, n = 4, (64,) * 3
     L = o.Level(n, o.C2)
     m, _ = L.dirichlet()
     x0 = np.where(~m, synth.random_nodal(14, n), 0.0)
     res = []
     for p0 in (1, 0):
-        if mode == "run":
+        if mode.startswith("run"):   # run_pers: the default selection (64^3, 128^3 as one cooperative launch each)
             g = Grid(4, 6, PROB["C2"], precond=precond)
             g.set_option(ecmg.OPT_P0_INIT, p0)
-            g.set_option(ecmg.OPT_PERS_TMA, 0)   # 64^3 and 128^3 on the launched kernels
+            if mode == "run":
+                g.set_option(ecmg.OPT_PERS_TMA, 0)   # 64^3 and 128^3 on the launched kernels
             u, ut = g.new_vec(5), g.new_vec(5)
             st, stats = g.run(1e-10, u, ut)
             assert st == 0
@@ -606,7 +608,7 @@ def test_p0_from_init_pass(mode, precond):
     for k in (1, 2):
         if not precond:
             assert np.array_equal(res[0][k], res[1][k])
-        elif k == 2 and mode != "run":   # RRe of a converged solve: a rounding-level change of x moves it visibly
+        elif k == 2 and not mode.startswith("run"):   # RRe of a converged solve: a rounding-level change of x moves it visibly
             assert abs(res[0][k][0] - res[1][k][0]) <= 1e-3 * res[1][k][0]
         else:
             assert rel(res[0][k], res[1][k]) <= 1e-13
