@@ -520,6 +520,9 @@ __global__ void k_rhs_shell(const LevelGeom g, const Problem pb, const ElemStenc
   }
   // lifting: couplings to Dirichlet neighbours (domain nodes outside the free box)
   double sub = 0.0;
+  bool any_robin = false;
+#pragma unroll
+  for (int F = 0; F < 6; ++F) any_robin = any_robin || es.robin[F] != 0.0;
   for (int e = 0; e < 8; ++e) {
     const int ex = e & 1, ey = (e >> 1) & 1, ez = (e >> 2) & 1;
     const int ge[3] = {gx - 1 + ex, gy - 1 + ey, gz - 1 + ez};
@@ -534,6 +537,7 @@ __global__ void k_rhs_shell(const LevelGeom g, const Problem pb, const ElemStenc
       const double gD = prob_gD_node(pb, g, jx, jy, jz);
       const int pat = ((ex + bx) != 1 ? 1 : 0) | ((ey + by) != 1 ? 2 : 0) | ((ez + bz) != 1 ? 4 : 0);
       sub += be * es.kappa[pat] * gD;
+      if (!any_robin) continue;   // (all-Dirichlet problems: most of the pairs; the face loop below is 6 tests each)
       // Robin face mass between this node and the Dirichlet node j on a common Robin face
 #pragma unroll
       for (int F = 0; F < 6; ++F) {
