@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <chrono>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -1165,6 +1166,10 @@ int ecmg_last_jcg_timing(const ecmg_grid* G, double* ms, int* iterations, long l
 static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const std::vector<int>& maxit_lv,
                        ecmg_stats* per_level, double* u_fine, double* ut_fine, int k_end = -1) {
   const double eps = eps_lv.back();
+  // ECMG_HOSTPROF=1: host-side time of the phases of this call on stderr (enqueue, wait for the GPU, statistics)
+  static const bool hostprof = std::getenv("ECMG_HOSTPROF") != nullptr;
+  const auto hp0 = std::chrono::steady_clock::now();
+  auto hp_us = [&](std::chrono::steady_clock::time_point t) { return std::chrono::duration<double, std::micro>(t - hp0).count(); };
   if (k_end < 0) k_end = G ? G->L : 0;
   const bool partial = G && k_end < G->L;
   if (!G || !G->has_problem || (!u_fine && !partial)) return ECMG_EINVAL;
@@ -1294,7 +1299,9 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
     ECMG_CUDA(cudaMemcpyAsync(u_fine, G->u[G->L - 1], sizeof(double) * Nf, cudaMemcpyDeviceToHost, G->stream));
   if (ut_fine && !ut_dev)
     ECMG_CUDA(cudaMemcpyAsync(ut_fine, G->ut_tmp, sizeof(double) * Nf, cudaMemcpyDeviceToHost, G->stream));
+  const auto hp1 = std::chrono::steady_clock::now();
   ECMG_CUDA(cudaStreamSynchronize(G->stream));   // (the caller's stream is joined by `join` on return)
+  const auto hp2 = std::chrono::steady_clock::now();
   for (int k = 0; k < L_run; ++k) {
     ecmg_stats& st = stv[k];
     if (async[k]) {
@@ -1316,6 +1323,9 @@ static int run_cascade(ecmg_grid* G, const std::vector<double>& eps_lv, const st
     G->last_jcg_ms = elapsed(G->lvl_ev[5 * (L_run - 1) + 2], G->lvl_ev[5 * (L_run - 1) + 3]);
   }
   if (per_level) for (int k = 0; k < L_run; ++k) per_level[k] = stv[k];
+  if (hostprof)
+    std::fprintf(stderr, "ecmg host: enqueued at %.0f us, GPU done at %.0f us, statistics done at %.0f us\n", hp_us(hp1),
+                 hp_us(hp2), hp_us(std::chrono::steady_clock::now()));
   (void)eps;
   return status;
 }
