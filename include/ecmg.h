@@ -193,7 +193,8 @@ typedef enum {
                                 per-face alpha; 76 instead of 80 B -- bitwise too, but measured slower: those
                                 kernels are issue bound, C3 256^3 0.256 -> 0.261-0.285 ms, C5 1024^3 16.0-16.5 ->
                                 16.5-16.7 ms per iteration; ablation); 0: x updated in every K2 */
-  ECMG_OPT_P0_INIT = 22,     /* launched constant-stencil TMA kernels on one GPU: 1 (default) the init pass stores
+  ECMG_OPT_P0_INIT = 22,     /* constant-stencil TMA kernels on one GPU (the launched K1 / K2 and the cooperative
+                                one-launch solves): 1 (default) the init pass stores
                                 p_0 = D^-1 r_0 instead of r_0; the first K1 reads it (no transform, no store)
                                 and the first K2 forms r_0 = D p_0 instead of reading r -- 16 B per unknown
                                 less in iteration 0. r_0 carries one extra rounding (<= 1 ulp; exact for plain

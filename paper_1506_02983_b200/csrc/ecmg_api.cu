@@ -512,7 +512,7 @@ cudaError_t launch_pers_tma(ecmg_grid* G, const LevelGeom& g) {
   }
   const auto& M = G->maps;
   CUtensorMap maps[7] = {M.xh, M.rh, M.ph[0], M.ph[1], M.xi, M.ri, M.bi};
-  return launch_jcg_const_pers(g, cs, G->x, G->r, G->p[0], G->p[1], G->partials, G->sc, maps, G->stream);
+  return launch_jcg_const_pers(g, cs, G->x, G->r, G->p[0], G->p[1], G->partials, G->sc, maps, G->stream, G->p0_init ? 1 : 0);
 }
 
 // the whole solve of a small level in one cooperative launch (kernels_jcg_persistent.cu)

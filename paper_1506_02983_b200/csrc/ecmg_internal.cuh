@@ -279,7 +279,7 @@ cudaError_t launch_jcg_elem_pers(const LevelGeom& g, const ElemStencil& es, doub
                                  double* p1, const double* b, const double* beta, double* partials, JcgScalars* sc,
                                  cudaStream_t st);
 cudaError_t launch_jcg_const_pers(const LevelGeom& g, const ConstStencil& cs, double* x, double* r, double* p0, double* p1,
-                                  double* partials, JcgScalars* sc, const CUtensorMap* maps, cudaStream_t st);
+                                  double* partials, JcgScalars* sc, const CUtensorMap* maps, cudaStream_t st, int p0_init);
 // z-slabs: finalize pass after the allreduce, and the in-order sum of P slabs' partial dots
 // (virtual slabs on one GPU; NCCL's allreduce on real ranks)
 cudaError_t launch_finalize(int mode, const KArgs& a, cudaStream_t st);

@@ -360,7 +360,7 @@ __device__ __forceinline__ void pers_grid_sum3(double v[3], double* partials, in
 
 __global__ void __launch_bounds__(NTH, 2)
     k_jcg_const_pers(const LevelGeom g, const ConstStencil cs, double* x, double* r, double* p0, double* p1, double* partials,
-                     JcgScalars* sc, int zc, int ntx, int nty, int items, const __grid_constant__ PersMaps M) {
+                     JcgScalars* sc, int zc, int ntx, int nty, int items, int p0_init, const __grid_constant__ PersMaps M) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[PS_NS];
   __shared__ double red[3 * (NTH / 32)];
@@ -378,6 +378,7 @@ __global__ void __launch_bounds__(NTH, 2)
   uint32_t gstep = 0;
   int buf = 0;
   KArgs a{};
+  a.p0 = p0_init;   // p_0 from the init pass (KArgs::p0), as on the launched kernels
   // one pass of MODE over this CTA's items
   auto pass = [&](auto mode_tag, const CUtensorMap* h0, const CUtensorMap* h1, const CUtensorMap* i0, const CUtensorMap* i1,
                   double bcg, bool first, double alpha, double v[3]) {
@@ -399,7 +400,7 @@ __global__ void __launch_bounds__(NTH, 2)
   };
   // init: r = b - A x, rho = r.z, rr, ||b||^2
   double v[3];
-  a.o0 = r;
+  a.o0 = a.p0 ? p1 : r;   // (p0: p_0 = D^-1 r_0 goes to the first K1's output vector)
   pass(std::integral_constant<int, MODE_INIT>{}, &M.xh, &M.xh, &M.bi, &M.bi, 0.0, false, 0.0, v);
   double rho = v[0], rr = v[1];
   const double bb = v[2];
@@ -413,12 +414,14 @@ __global__ void __launch_bounds__(NTH, 2)
   while (!done) {
     double* pnew = cur ? p0 : p1;
     a.o0 = pnew;
-    pass(std::integral_constant<int, MODE_K1>{}, &M.rh, cur ? &M.ph1 : &M.ph0, &M.rh, &M.rh, beta, iter == 0, 0.0, v);
+    // (p0, iteration 0: the halo vector is p_0 itself, in the output vector p1)
+    pass(std::integral_constant<int, MODE_K1>{}, (a.p0 && iter == 0) ? &M.ph1 : &M.rh, cur ? &M.ph1 : &M.ph0, &M.rh, &M.rh,
+         beta, iter == 0, 0.0, v);
     const double sigma = v[0];
     if (!(sigma > 0.0)) { status = ST_EBREAKDOWN; break; }
     const double alpha = rho / sigma;
     a.o0 = x; a.o1 = r;
-    pass(std::integral_constant<int, MODE_K2>{}, cur ? &M.ph0 : &M.ph1, &M.rh, &M.xi, &M.ri, 0.0, false, alpha, v);
+    pass(std::integral_constant<int, MODE_K2>{}, cur ? &M.ph0 : &M.ph1, &M.rh, &M.xi, &M.ri, 0.0, iter == 0, alpha, v);
     beta = v[0] / rho;
     rho = v[0];
     rr = v[1];
@@ -544,7 +547,7 @@ cudaError_t init_pers_kernel_attributes() {
 
 // maps: x halo, r halo, p0 halo, p1 halo, x interior, r interior, b interior (make_vec_tensor_map)
 cudaError_t launch_jcg_const_pers(const LevelGeom& g, const ConstStencil& cs, double* x, double* r, double* p0, double* p1,
-                                  double* partials, JcgScalars* sc, const CUtensorMap* maps, cudaStream_t st) {
+                                  double* partials, JcgScalars* sc, const CUtensorMap* maps, cudaStream_t st, int p0_init) {
   const int ntx = (g.nf[0] + TX - 1) / TX, nty = (g.nf[1] + TY - 1) / TY;
   const int nz = g.zend - g.zbeg;
   const int slots = pers_slots();
@@ -564,7 +567,7 @@ cudaError_t launch_jcg_const_pers(const LevelGeom& g, const ConstStencil& cs, do
   PersMaps M{maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6]};
   int grid = std::min(items, slots);
   void* args[] = {(void*)&g, (void*)&cs, (void*)&x, (void*)&r, (void*)&p0, (void*)&p1, (void*)&partials, (void*)&sc,
-                  (void*)&zc, (void*)&ntx, (void*)&nty, (void*)&items, (void*)&M};
+                  (void*)&zc, (void*)&ntx, (void*)&nty, (void*)&items, (void*)&p0_init, (void*)&M};
   count_launch();
   return cudaLaunchCooperativeKernel((const void*)k_jcg_const_pers, dim3(grid), dim3(TX, WARPS), args,
                                      PS_SBYTES * PS_NS + 128, st);
